@@ -1,0 +1,237 @@
+/*
+ * rtec.h -- C ABI of librtec.so, the B200 (sm_100a) incremental RTEC engine.
+ *
+ * The reference (`streamgnn`, pure Python) exposes no FFI; this header is the
+ * drop-in boundary for its hot path.  Each entry point names
+ * the reference interface it replaces (file:line, relative to
+ * /root/reference/pkg/src/streamgnn/).
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers unless the name ends in `_host`.
+ *  - Every call is asynchronous on the given stream, returns an rtec_status
+ *    for argument errors detected on the host, and reports data-dependent
+ *    errors (InvalidVertex, ConfigError, ...) through a device status word
+ *    (`err`: uint64 packed as position << 32 | code, all-ones = ok; the
+ *    smallest position wins) that the caller reads after the batch.
+ *  - The library allocates nothing persistent.  Persistent state lives in
+ *    caller-owned device buffers described by the POD structs below; scratch
+ *    space comes from the caller's workspace (`ws`, `ws_bytes`), sized with
+ *    rtec_workspace_bytes().
+ *  - Vertex ids are int32 (n < 2^31), edge slots int64.
+ *  - One host thread / stream per graph; not re-entrant per graph
+ *    (pma.py:22).
+ */
+#ifndef RTEC_H_
+#define RTEC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* rtec_stream_t; /* == cudaStream_t */
+
+/* status codes: 1:1 with errors.py:6-35 exception classes */
+enum {
+  RTEC_OK = 0,
+  RTEC_INVALID_VERTEX = 1,   /* errors.InvalidVertex   */
+  RTEC_CONFIG_ERROR = 2,     /* errors.ConfigError     */
+  RTEC_SHAPE_ERROR = 3,      /* errors.ShapeError      */
+  RTEC_NUMERIC_ERROR = 4,    /* errors.NumericError    */
+  RTEC_SINGULAR_CONTEXT = 5, /* errors.SingularContext */
+  RTEC_STALE_STATE = 6,      /* errors.StaleState      */
+  RTEC_UNSUPPORTED_MODEL = 7,/* errors.UnsupportedModel*/
+  RTEC_CUDA_ERROR = 100
+};
+
+/* update ops (graph.py:28-30) */
+enum { RTEC_OP_INSERT = 0, RTEC_OP_DELETE = 1 };
+
+/* models (models.py:42-52); only the hot-path four are implemented */
+enum { RTEC_MODEL_GCN = 0, RTEC_MODEL_SAGE = 1, RTEC_MODEL_GIN = 2, RTEC_MODEL_GAT = 3 };
+
+/* One direction of the adjacency: gapped per-vertex runs.  Run of v is
+ * nbr[beg[v] .. beg[v]+len[v]) ascending, with cap[v] >= len[v] slots reserved.
+ * Runs that outgrow their capacity are relocated to the arena tail (*top).
+ * Replaces one PackedMemoryArray (pma.py:37-326) of composite keys. */
+typedef struct {
+  int64_t slots;     /* capacity of nbr[] / ts[] */
+  int64_t* beg;      /* [n] */
+  int32_t* len;      /* [n] */
+  int32_t* cap;      /* [n] */
+  int32_t* nbr;      /* [slots] */
+  int64_t* ts;       /* [slots] timestamps (out direction) or NULL */
+  int64_t* top;      /* [1] arena bump pointer */
+} rtec_adj_t;
+
+/* DynamicGraph (graph.py:59-235): out + in adjacency, degrees. */
+typedef struct {
+  int64_t n;
+  rtec_adj_t out;    /* src -> dst runs, with ts (graph.py:73-76 `_out`) */
+  rtec_adj_t in;     /* dst -> src runs (graph.py `_in`) */
+  int32_t* out_deg;  /* [n] current degrees */
+  int32_t* in_deg;   /* [n] */
+  int32_t* out_deg_prev; /* [n] degrees before the current batch (== current between batches) */
+  int32_t* in_deg_prev;  /* [n] */
+  int64_t* num_edges;    /* [1] */
+  float slack;           /* relocated / rebuilt runs get cap = len + max(min_slack, ceil(len*slack)) */
+  int32_t min_slack;
+} rtec_graph_t;
+
+/* Internal status: the arena (or the in-place merge scratch) cannot hold this
+ * batch; nothing was mutated.  The host compacts / grows and re-applies. */
+#define RTEC_ARENA_FULL 8
+
+/* Per-batch derived data (capacity `cap` updates).  Written by
+ * rtec_batch_apply, read by the frontier / layer kernels of the same batch. */
+typedef struct {
+  int64_t cap;
+  uint64_t* err;       /* [1] packed (position << 32 | code); ~0 = ok */
+  uint8_t* status;     /* [cap] per update in batch order: 1 applied, 0 rejected */
+  /* applied updates sorted by (src, dst) -- out-key order */
+  int32_t* a_src; int32_t* a_dst; uint8_t* a_op; int64_t* a_ts;
+  int64_t* n_applied;  /* [1] */
+  /* applied updates sorted by (dst, src) -- in-key order */
+  int32_t* i_src; int32_t* i_dst; uint8_t* i_op;
+  /* DegreeDelta rows (graph.py:41-48), ascending vertex */
+  int32_t* d_vertex; int32_t* d_old_in; int32_t* d_new_in; int32_t* d_old_out; int32_t* d_new_out;
+  int64_t* n_delta;    /* [1] */
+} rtec_batch_t;
+
+/* Per-layer frontier (Alg. 4).  Bitmaps
+ * are n bits (uint32 words).  Lists ascending. */
+typedef struct {
+  uint32_t* bm_src;    /* [words] S(l) = Dg ∪ V_chg(l-1) */
+  uint32_t* bm_dst;    /* [words] V_dst(l) */
+  int32_t* src_list;  int64_t* n_src;   /* S(l) */
+  int32_t* dst_list;  int64_t* n_dst;   /* V_dst(l) */
+  int32_t* src_slot;   /* [n] vertex -> index in src_list (valid where bm_src bit set) */
+  int32_t* dst_slot;   /* [n] vertex -> index in dst_list (valid where bm_dst bit set) */
+  int64_t* counters;   /* [8] |E_curr|, |V_dst|, |S|, |R|, Σ outdeg(new S), Σ indeg(V_dst), Σ indeg(R), reserved */
+} rtec_frontier_t;
+
+/* Layer descriptor (operators.py:42-47 LayerWeights + bundle flags).
+ * Weights are fp32 copies of make_bundle's f64 weights (models.py:364). */
+typedef struct {
+  int32_t model;       /* RTEC_MODEL_* */
+  int32_t d_in;        /* input width  */
+  int32_t d_out;       /* output width */
+  int32_t heads;       /* GAT heads (1 for others) */
+  float degree_offset; /* GCN: 1 if degree_smoothing else 0 (models.py:89) */
+  int32_t pad;
+  const float* W;      /* [d_out, d_in] row-major (GAT: heads stacked [heads*dh, d_in]) */
+  const float* W2;     /* GIN second matrix [d_out, d_out] (models.py:181) */
+  const float* att;    /* GAT attention [heads, 2*dh] (dst half first, models.py:266-271) */
+} rtec_layer_t;
+
+/* Per-layer cached state (SPEC.md:355-419 state_cache; stored un-normalised):
+ *   S   [n, d_agg]  aggregate before ms_cbn (= ms_cbn_inv(ctx, a))
+ *   ctx [n, heads]  GAT attention sums (count contexts are the in-degrees)
+ *   H_out [n, d_out] layer output; H_in = previous layer's output (or X)
+ *   log_out [n_dst cap, d_out] DeltaLog: pre-batch H_out rows of V_dst(l),
+ *            indexed by frontier.dst_slot
+ *   GAT caches for the layer: Z [n, d_out] = W h, el/er [n, heads]. */
+typedef struct {
+  const float* H_in;   float* H_out;
+  float* S;            float* ctx;
+  float* log_out;      /* DeltaLog rows of this layer's output */
+  const float* log_in; /* previous layer's DeltaLog (NULL for layer 0); rows indexed by
+                          the previous frontier's dst_slot, membership = its bm_dst */
+  float* Z; float* el; float* er;           /* GAT caches */
+  float* Z_log; float* er_log;              /* GAT DeltaLog of Z/er rows of V_chg(l-1) */
+  float* gemm_in;      /* [n_dst cap, max(d_agg,d_in)] scratch: composed rows fed to the update GEMM */
+  float* gemm_mid;     /* [n_dst cap, d_out] GIN hidden */
+} rtec_state_t;
+
+/* ---- workspace ---- */
+/* per-batch calls (apply / frontier / layers); m_slots bounds the in-place merge scratch */
+size_t rtec_workspace_bytes(int64_t n, int64_t max_batch, int64_t m_slots, int32_t max_dim);
+/* bulk build / compaction of m edges */
+size_t rtec_build_workspace_bytes(int64_t n, int64_t m);
+
+/* ---- graph store (graph.py) ---- */
+/* from_edges (graph.py:81-121): builds both adjacencies with slack capacity
+ * (cap = len + max(min_slack, ceil(len*slack))).  err <- InvalidVertex /
+ * ConfigError("duplicate edges in bulk load"). */
+int rtec_graph_build(rtec_graph_t* g, const int32_t* src, const int32_t* dst, const int64_t* ts,
+                     int64_t m, float slack, int32_t min_slack, uint64_t* err,
+                     void* ws, size_t ws_bytes, rtec_stream_t stream);
+/* Degree histogram of a bulk edge list; err <- InvalidVertex (graph.py:101-102). */
+int rtec_graph_count(const int32_t* src, const int32_t* dst, int64_t m, int64_t n, int32_t* out_deg,
+                     int32_t* in_deg, uint64_t* err, rtec_stream_t stream);
+/* Required slots for a build/compaction of `m` edges at the given slack, given
+ * per-vertex run lengths `len` (device) -- written to *slots_dev. */
+int rtec_graph_slots_needed(const int32_t* len, int64_t n, float slack, int32_t min_slack,
+                            int64_t* slots_dev, void* ws, size_t ws_bytes, rtec_stream_t stream);
+/* Compaction: copy every run of `src` into `dst` (fresh arrays) with fresh
+ * slack.  Replaces PMA rebalancing (pma.py:304-326). */
+int rtec_adj_compact(int64_t n, const rtec_adj_t* src, rtec_adj_t* dst, float slack, int32_t min_slack,
+                     void* ws, size_t ws_bytes, rtec_stream_t stream);
+/* edges() (graph.py:166-170): all runs of `a` flattened in (vertex, nbr) order;
+ * out_ts may be NULL. Caller sizes outputs with num_edges. */
+int rtec_adj_export(int64_t n, const rtec_adj_t* a, int32_t* out_v, int32_t* out_nbr, int64_t* out_ts,
+                    void* ws, size_t ws_bytes, rtec_stream_t stream);
+
+/* coalesce_batch (graph.py:241-260): net effect per (src, dst), survivors in
+ * first-appearance order; *n_out written on device. */
+int rtec_batch_coalesce(const int32_t* src, const int32_t* dst, const uint8_t* op, const int64_t* ts,
+                        int64_t B, int32_t* out_src, int32_t* out_dst, uint8_t* out_op, int64_t* out_ts,
+                        int64_t* n_out, void* ws, size_t ws_bytes, rtec_stream_t stream);
+
+/* apply_batch (graph.py:184-231): validate (range -> InvalidVertex, repeated
+ * edge -> ConfigError; first offender in batch order wins; nothing mutated on
+ * error), probe, reject duplicate inserts / absent deletes, update degrees,
+ * merge both adjacencies, emit DegreeDelta rows. */
+int rtec_batch_apply(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src, const int32_t* dst,
+                     const uint8_t* op, const int64_t* ts, int64_t B,
+                     void* ws, size_t ws_bytes, rtec_stream_t stream);
+/* Close the batch: degree snapshots catch up (out_deg_prev = out_deg ...). */
+int rtec_batch_commit(rtec_graph_t* g, const rtec_batch_t* b, rtec_stream_t stream);
+
+/* ---- frontier (Alg. 4 / SPEC frontier.build SPEC.md:311-319, F1 rule) ---- */
+/* Layer `l` (0-based).  prev == NULL for l = 0.  src_degree_dependent seeds
+ * S with Dg (degree-changed sources) at every layer. */
+int rtec_frontier_layer(const rtec_graph_t* g, const rtec_batch_t* b, int32_t l,
+                        int32_t src_degree_dependent, const rtec_frontier_t* prev, rtec_frontier_t* f,
+                        void* ws, size_t ws_bytes, rtec_stream_t stream);
+
+/* ---- layers ---- */
+/* Alg. 1 / Alg. 3 for V_dst(l) \ R(l),
+ * full-neighbourhood recompute (models.py:431) for R(l), then the update
+ * (operators.py:180) on the affected rows with DeltaLog capture. */
+int rtec_layer_incremental(const rtec_graph_t* g, const rtec_batch_t* b, const rtec_layer_t* L,
+                           rtec_state_t* st, const rtec_frontier_t* prev, const rtec_frontier_t* f,
+                           uint64_t* err, void* ws, size_t ws_bytes, rtec_stream_t stream);
+/* layer_embeddings (models.py:461-477) for all vertices (rows == NULL) or the
+ * listed rows: bootstrap, refresh and dense fallback. */
+int rtec_layer_full(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* st,
+                    const int32_t* rows, const int64_t* n_rows, int64_t max_rows, uint64_t* err,
+                    void* ws, size_t ws_bytes, rtec_stream_t stream);
+/* GAT f_nn / logit halves for rows (models.py:265-279): Z = W h, el, er. */
+int rtec_gat_project(const rtec_layer_t* L, const float* H, const int32_t* rows, const int64_t* n_rows,
+                     int64_t n_or_max_rows, float* Z, float* el, float* er,
+                     float* Z_log, float* er_log, const uint64_t* err, rtec_stream_t stream);
+
+/* Dense update GEMM on gathered rows (operators.py:180; linalg.py:22):
+ * Y[i] = act(X[i] · W^T) (act: 0 none, 1 relu).  Rows i < *n_rows. */
+int rtec_update_gemm(const float* X, int64_t ldx, const float* W, int32_t d_in, int32_t d_out,
+                     const int64_t* n_rows, int64_t max_rows, int32_t act, float* Y, int64_t ldy,
+                     const int32_t* scatter_rows, float* scatter_dst, float* log_dst,
+                     rtec_stream_t stream);
+
+/* materialize / query final-layer rows (SPEC materialize_h SPEC.md:379). */
+int rtec_query(const float* H, int64_t d, const int32_t* ids, int64_t k, float* out, int32_t n,
+               uint64_t* err, rtec_stream_t stream);
+
+/* ---- diagnostics ---- */
+void rtec_struct_sizes(int64_t* out6); /* sizeof adj, graph, batch, frontier, layer, state */
+const char* rtec_last_error(void);
+const char* rtec_version(void);
+int rtec_device_sm_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RTEC_H_ */

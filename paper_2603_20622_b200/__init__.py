@@ -1,1 +1,19 @@
-"""B200-native incremental RTEC engine."""
+"""B200-native incremental RTEC engine (drop-in for the streamgnn hot path).
+
+Public surface mirrors the reference (`streamgnn.graph`, `streamgnn.models`,
+the SPEC engine API): see DESIGN.md.  All compute runs in librtec.so
+(hand-written sm_100a CUDA) through the C ABI in include/rtec.h.
+"""
+
+from .errors import (  # noqa: F401
+    ConfigError, InvalidVertex, NativeError, NumericError, ShapeError, SingularContext, StaleState, StreamGNNError,
+    UnsupportedModel,
+)
+from .graph import (  # noqa: F401
+    ApplyResult, DegreeDelta, DynamicGraph, EdgeUpdate, UpdateOp, coalesce_batch, invert_batch, read_stream,
+    write_stream,
+)
+from .models import MODELS, Bundle, LayerWeights, from_reference, make_bundle  # noqa: F401
+from .engine import Metrics, RTECEngine, RunResult  # noqa: F401
+
+__version__ = "0.1.0"

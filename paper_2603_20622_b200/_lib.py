@@ -1,0 +1,164 @@
+"""ctypes binding of librtec.so (the C ABI declared in include/rtec.h).
+
+The library is built in-tree (`paper_2603_20622_b200/librtec.so`, see
+`__graft_entry__.build()`).  There is no fallback: if the library or a CUDA
+device is missing, `lib()` raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from . import errors as E
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librtec.so")
+
+OP_INSERT = 0
+OP_DELETE = 1
+MODEL_IDS = {"gcn": 0, "graphsage": 1, "gin": 2, "gat": 3}
+ARENA_FULL = 8
+ERR_OK = (1 << 64) - 1
+
+P = C.c_void_p
+I64 = C.c_int64
+I32 = C.c_int32
+SZ = C.c_size_t
+F32 = C.c_float
+
+
+class Adj(C.Structure):
+    _fields_ = [("slots", I64), ("beg", P), ("len", P), ("cap", P), ("nbr", P), ("ts", P), ("top", P)]
+
+
+class Graph(C.Structure):
+    _fields_ = [
+        ("n", I64), ("out", Adj), ("inn", Adj),
+        ("out_deg", P), ("in_deg", P), ("out_deg_prev", P), ("in_deg_prev", P),
+        ("num_edges", P), ("slack", F32), ("min_slack", I32),
+    ]
+
+
+class Batch(C.Structure):
+    _fields_ = [
+        ("cap", I64), ("err", P), ("status", P),
+        ("a_src", P), ("a_dst", P), ("a_op", P), ("a_ts", P), ("n_applied", P),
+        ("i_src", P), ("i_dst", P), ("i_op", P),
+        ("d_vertex", P), ("d_old_in", P), ("d_new_in", P), ("d_old_out", P), ("d_new_out", P),
+        ("n_delta", P),
+    ]
+
+
+class Frontier(C.Structure):
+    _fields_ = [
+        ("bm_src", P), ("bm_dst", P), ("src_list", P), ("n_src", P), ("dst_list", P), ("n_dst", P),
+        ("src_slot", P), ("dst_slot", P), ("counters", P),
+    ]
+
+
+class Layer(C.Structure):
+    _fields_ = [
+        ("model", I32), ("d_in", I32), ("d_out", I32), ("heads", I32),
+        ("degree_offset", F32), ("pad", I32), ("W", P), ("W2", P), ("att", P),
+    ]
+
+
+class State(C.Structure):
+    _fields_ = [
+        ("H_in", P), ("H_out", P), ("S", P), ("ctx", P), ("log_out", P), ("log_in", P),
+        ("Z", P), ("el", P), ("er", P), ("Z_log", P), ("er_log", P), ("gemm_in", P), ("gemm_mid", P),
+    ]
+
+
+_SIGS = {
+    "rtec_workspace_bytes": (SZ, [I64, I64, I64, I32]),
+    "rtec_build_workspace_bytes": (SZ, [I64, I64]),
+    "rtec_graph_count": (C.c_int, [P, P, I64, I64, P, P, P, P]),
+    "rtec_graph_slots_needed": (C.c_int, [P, I64, F32, I32, P, P, SZ, P]),
+    "rtec_graph_build": (C.c_int, [C.POINTER(Graph), P, P, P, I64, F32, I32, P, P, SZ, P]),
+    "rtec_adj_compact": (C.c_int, [I64, C.POINTER(Adj), C.POINTER(Adj), F32, I32, P, SZ, P]),
+    "rtec_adj_export": (C.c_int, [I64, C.POINTER(Adj), P, P, P, P, SZ, P]),
+    "rtec_batch_coalesce": (C.c_int, [P, P, P, P, I64, P, P, P, P, P, P, SZ, P]),
+    "rtec_batch_apply": (C.c_int, [C.POINTER(Graph), C.POINTER(Batch), P, P, P, P, I64, P, SZ, P]),
+    "rtec_batch_commit": (C.c_int, [C.POINTER(Graph), C.POINTER(Batch), P]),
+    "rtec_frontier_layer": (C.c_int, [C.POINTER(Graph), C.POINTER(Batch), I32, I32, C.POINTER(Frontier),
+                                      C.POINTER(Frontier), P, SZ, P]),
+    "rtec_layer_incremental": (C.c_int, [C.POINTER(Graph), C.POINTER(Batch), C.POINTER(Layer), C.POINTER(State),
+                                         C.POINTER(Frontier), C.POINTER(Frontier), P, P, SZ, P]),
+    "rtec_layer_full": (C.c_int, [C.POINTER(Graph), C.POINTER(Layer), C.POINTER(State), P, P, I64, P, P, SZ, P]),
+    "rtec_gat_project": (C.c_int, [C.POINTER(Layer), P, P, P, I64, P, P, P, P, P, P, P]),
+    "rtec_update_gemm": (C.c_int, [P, I64, P, I32, I32, P, I64, I32, P, I64, P, P, P, P]),
+    "rtec_query": (C.c_int, [P, I64, P, I64, P, I32, P, P]),
+    "rtec_struct_sizes": (None, [C.POINTER(I64)]),
+    "rtec_last_error": (C.c_char_p, []),
+    "rtec_version": (C.c_char_p, []),
+    "rtec_device_sm_count": (C.c_int, []),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+def load(require_cuda: bool = True):
+    """Load librtec.so; raises NativeError if it is missing (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise E.NativeError(
+                f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        lib = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    if require_cuda:
+        import torch
+
+        if not torch.cuda.is_available():
+            raise E.NativeError("librtec needs a CUDA device (B200); none is visible")
+    return _lib
+
+
+def check(status: int, what: str = "") -> None:
+    if status == 0:
+        return
+    msg = (_lib.rtec_last_error() or b"").decode(errors="replace")
+    cls = E.BY_CODE.get(status)
+    if cls is None:
+        raise E.NativeError(f"{what}: status {status}: {msg}")
+    raise cls(f"{what}: {msg}")
+
+
+def decode_err(word: int):
+    """Device status word -> (code, position) or None when ok."""
+    word = int(word) & ERR_OK
+    if word == ERR_OK:
+        return None
+    return word & 0xFFFFFFFF, word >> 32
+
+
+def raise_err(word: int, what: str, messages=None) -> None:
+    d = decode_err(word)
+    if d is None:
+        return
+    code, pos = d
+    cls = E.BY_CODE.get(code)
+    text = (messages or {}).get(code, f"status {code} at position {pos}")
+    if cls is None:
+        raise E.NativeError(f"{what}: {text}")
+    raise cls(f"{what}: {text}")
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (None -> NULL)."""
+    return None if t is None else t.data_ptr()
+
+
+def stream_handle():
+    import torch
+
+    return torch.cuda.current_stream().cuda_stream

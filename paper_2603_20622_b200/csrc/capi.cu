@@ -1,0 +1,55 @@
+// capi.cu -- library-level C entry points (workspace sizing, diagnostics).
+#include "prims.cuh"
+
+namespace rtec {
+const char* last_error_cstr();
+size_t batch_ws_bytes(int64_t n, int64_t B, int64_t scr_cap);
+size_t frontier_ws_bytes(int64_t n);
+}  // namespace rtec
+
+using namespace rtec;
+
+extern "C" {
+
+// Workspace for every per-batch call: max over batch apply (sorts + merge
+// plans + in-place merge scratch), frontier (lists) and layer (δ rows).
+// `m_slots` bounds the in-place merge scratch (touched run lengths).
+size_t rtec_workspace_bytes(int64_t n, int64_t max_batch, int64_t m_slots, int32_t max_dim) {
+  int64_t scr = 64 * max_batch + (1 << 20);
+  if (scr > m_slots + max_batch) scr = m_slots + max_batch;
+  if (scr < (1 << 16)) scr = 1 << 16;
+  size_t b = batch_ws_bytes(n, max_batch, scr) + static_cast<size_t>(scr) * 13 * 2;
+  size_t f = frontier_ws_bytes(n);
+  size_t l = static_cast<size_t>(n) * static_cast<size_t>(max_dim) * sizeof(float) + (1 << 20);
+  size_t r = b > f ? b : f;
+  return (r > l ? r : l) + (1 << 20);
+}
+
+// Workspace for a bulk build / compaction of m edges over n vertices.
+size_t rtec_build_workspace_bytes(int64_t n, int64_t m) {
+  size_t sort = sort_ws_bytes(m) + static_cast<size_t>(m) * 24;
+  size_t scan = sizeof(int64_t) * (scan_blocks_for(n > m ? n : m) + 2) * 4 + static_cast<size_t>(n + 1) * 8;
+  return sort + scan + (1 << 20);
+}
+
+// sizeof of the ABI structs, for binding self-checks (ctypes / cgo / JNI mirrors)
+void rtec_struct_sizes(int64_t* out6) {
+  out6[0] = sizeof(rtec_adj_t);
+  out6[1] = sizeof(rtec_graph_t);
+  out6[2] = sizeof(rtec_batch_t);
+  out6[3] = sizeof(rtec_frontier_t);
+  out6[4] = sizeof(rtec_layer_t);
+  out6[5] = sizeof(rtec_state_t);
+}
+
+const char* rtec_last_error(void) { return last_error_cstr(); }
+const char* rtec_version(void) { return "rtec-b200 0.1 (sm_100a)"; }
+
+int rtec_device_sm_count(void) {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+  return sms;
+}
+
+}  // extern "C"

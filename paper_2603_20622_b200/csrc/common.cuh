@@ -1,0 +1,119 @@
+// common.cuh -- shared device/host helpers for librtec (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+
+#include "../../include/rtec.h"
+
+namespace rtec {
+
+constexpr int kWarp = 32;
+constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs
+
+// ---------------------------------------------------------------- errors
+void set_error(const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* where);
+
+#define RTEC_CUDA(call)                                   \
+  do {                                                    \
+    cudaError_t _e = (call);                              \
+    if (_e != cudaSuccess) return ::rtec::cuda_status(_e, #call); \
+  } while (0)
+
+#define RTEC_LAUNCH_CHECK(name) RTEC_CUDA(cudaGetLastError())
+
+#define RTEC_TRY(expr)              \
+  do {                              \
+    int _s = (expr);                \
+    if (_s != RTEC_OK) return _s;   \
+  } while (0)
+
+// ---------------------------------------------------------------- workspace
+// Bump allocator over the caller's workspace; every chunk 256-B aligned.
+struct Ws {
+  uint8_t* base;
+  size_t bytes;
+  size_t off = 0;
+  bool ok = true;
+  Ws(void* p, size_t b) : base(static_cast<uint8_t*>(p)), bytes(b) {}
+  template <typename T>
+  T* alloc(int64_t count) {
+    size_t need = (static_cast<size_t>(count > 0 ? count : 1) * sizeof(T) + 255) & ~size_t(255);
+    if (off + need > bytes) {
+      ok = false;
+      return nullptr;
+    }
+    T* p = reinterpret_cast<T*>(base + off);
+    off += need;
+    return p;
+  }
+};
+
+#define RTEC_WS_CHECK(ws)                                                                  \
+  do {                                                                                     \
+    if (!(ws).ok) {                                                                        \
+      ::rtec::set_error("workspace too small (%zu bytes given, need more)", (ws).bytes);   \
+      return RTEC_CONFIG_ERROR;                                                            \
+    }                                                                                      \
+  } while (0)
+
+inline int grid_for(int64_t work, int block, int max_ctas = kSMs * 16) {
+  int64_t g = (work + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > max_ctas) g = max_ctas;
+  return static_cast<int>(g);
+}
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// first index i in [lo, hi) with a[i] >= key (a ascending)
+template <typename T, typename K>
+__device__ __forceinline__ int64_t lower_bound_dev(const T* a, int64_t lo, int64_t hi, K key) {
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ bool bm_test(const uint32_t* bm, int32_t v) {
+  return (__ldg(bm + (v >> 5)) >> (v & 31)) & 1u;
+}
+
+// Warp-aggregated atomicOr of bit v (lanes sharing a word issue one atomic).
+__device__ __forceinline__ void bm_set_warp(uint32_t* bm, int32_t v, bool active) {
+  unsigned mask = __ballot_sync(0xffffffffu, active);
+  if (!active) return;
+  int word = v >> 5;
+  unsigned peers = __match_any_sync(mask, word);
+  uint32_t acc = __reduce_or_sync(peers, 1u << (v & 31));
+  if ((__ffs(peers) - 1) == lane_id()) atomicOr(bm + word, acc);
+}
+
+__device__ __forceinline__ void atomic_min_i32(int32_t* p, int32_t v) { atomicMin(p, v); }
+
+// Device status word: packed (position << 32 | code), all-ones = ok.  The
+// smallest position wins (first offender in batch order); ties keep the
+// smaller code.
+constexpr uint64_t kErrOk = ~0ull;
+__device__ __forceinline__ void report_error(uint64_t* err, int32_t code, int64_t pos) {
+  unsigned long long packed = (static_cast<unsigned long long>(static_cast<uint32_t>(pos)) << 32) |
+                              static_cast<uint32_t>(code);
+  atomicMin(reinterpret_cast<unsigned long long*>(err), packed);
+}
+__device__ __forceinline__ bool err_set(const uint64_t* err) { return *((volatile const uint64_t*)err) != kErrOk; }
+
+}  // namespace rtec

@@ -1,0 +1,190 @@
+// frontier.cu -- per-layer affected subgraph (§8(a)-F1).
+//
+// Alg. 4 with the every-layer source-degree rule:
+//   S(l)     = Dg ∪ V_chg(l-1)              (Dg = out-degree-changed sources, GCN only)
+//   E_curr(l)= I ∪ D ∪ {(u,w) ∈ G_post : u ∈ S(l)}
+//   V_dst(l) = dst(E_curr(l)),  V_chg(l) = V_dst(l)
+// V_dst is monotone in l, so layer l only expands the NEW sources
+// S(l) \ S(l-1) into a copy of V_dst(l-1).  Sets are n-bit bitmaps; lists are
+// ascending id arrays produced by a popcount scan over the bitmap words.
+// Expansion is edge-balanced: a prefix over the new sources' out-run lengths
+// maps every edge to a thread, and bits are set with warp-aggregated atomicOr.
+#include "prims.cuh"
+
+namespace rtec {
+
+constexpr int kFBlk = 256;
+
+// Dg bits and dst(I ∪ D) bits
+__global__ void k_seed_layer0(const rtec_batch_t b, int32_t src_degree_dependent, uint32_t* bm_src,
+                              uint32_t* bm_dst) {
+  if (err_set(b.err)) return;
+  int64_t nd = *b.n_delta, na = *b.n_applied;
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // loop bound uniform across the warp for the ballot-based helper
+  int64_t lim = nd > na ? nd : na;
+  for (int64_t i0 = tid - lane_id(); i0 < lim; i0 += stride) {
+    int64_t i = i0 + lane_id();
+    bool dg = src_degree_dependent && i < nd && b.d_old_out[i] != b.d_new_out[i];
+    bm_set_warp(bm_src, dg ? b.d_vertex[i] : 0, dg);
+    bool ad = i < na;
+    bm_set_warp(bm_dst, ad ? b.a_dst[i] : 0, ad);
+  }
+}
+
+__global__ void k_union_words(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, uint32_t* out,
+                              int64_t words) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < words; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = a[i] | b[i];
+}
+
+// popcount of (a & ~b) per word (b may be null)
+struct WordPop {
+  const uint32_t* a;
+  const uint32_t* b;
+  __device__ __forceinline__ uint32_t word(int64_t i) const { return a[i] & (b ? ~b[i] : 0xffffffffu); }
+  __device__ __forceinline__ int64_t operator()(int64_t i) const { return __popc(word(i)); }
+};
+struct WordList {
+  WordPop f;
+  int32_t* list;
+  int32_t* slot;  // may be null
+  __device__ __forceinline__ void operator()(int64_t i, int64_t off, int64_t) const {
+    uint32_t w = f.word(i);
+    while (w) {
+      int bit = __ffs(w) - 1;
+      w &= w - 1;
+      int32_t v = static_cast<int32_t>(i * 32 + bit);
+      list[off] = v;
+      if (slot) slot[v] = static_cast<int32_t>(off);
+      ++off;
+    }
+  }
+};
+
+struct OutLenOf {
+  const int32_t* list;
+  const int32_t* len;
+  __device__ __forceinline__ int64_t operator()(int64_t i) const { return len[list[i]]; }
+};
+struct StoreOffTailF {
+  int64_t* dst;
+  const int64_t* n;
+  __device__ __forceinline__ void operator()(int64_t i, int64_t off, int64_t v) const {
+    dst[i] = off;
+    if (i == *n - 1) dst[i + 1] = off + v;
+  }
+};
+
+// edge-balanced expansion of the new sources' out-runs into bm_dst
+__global__ void __launch_bounds__(kFBlk) k_expand(const int32_t* __restrict__ nlist, const int64_t* n_new,
+                                                  const int64_t* __restrict__ off, rtec_adj_t out,
+                                                  uint32_t* bm_dst) {
+  int64_t N = *n_new;
+  if (N == 0) return;
+  int64_t E = off[N];
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e0 = tid - lane_id(); e0 < E; e0 += stride) {
+    int64_t e = e0 + lane_id();
+    bool act = e < E;
+    int32_t w = 0;
+    if (act) {
+      // owner: last i with off[i] <= e
+      int64_t lo = 0, hi = N;
+      while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (off[mid] <= e) lo = mid + 1;
+        else hi = mid;
+      }
+      int64_t i = lo - 1;
+      int32_t u = nlist[i];
+      w = out.nbr[out.beg[u] + (e - off[i])];
+    }
+    bm_set_warp(bm_dst, w, act);
+  }
+}
+
+// |E_curr(l)| = Σ_{u∈S} outdeg_post(u) + |{e ∈ I : src ∉ S}| + |D|; plus list sizes
+__global__ void k_counters(const int32_t* __restrict__ slist, const int64_t* n_src, const int64_t* n_dst,
+                           const int32_t* __restrict__ out_len, const int32_t* __restrict__ in_len,
+                           const int32_t* __restrict__ dlist, const rtec_batch_t b, const uint32_t* bm_src,
+                           int64_t* counters) {
+  int64_t ns = *n_src, nd = *n_dst, na = err_set(b.err) ? 0 : *b.n_applied;
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t e = 0, sin = 0;
+  for (int64_t i = tid; i < ns; i += stride) e += out_len[slist[i]];
+  for (int64_t i = tid; i < na; i += stride) {
+    if (b.a_op[i] == RTEC_OP_DELETE) e += 1;
+    else if (!bm_test(bm_src, b.a_src[i])) e += 1;
+  }
+  for (int64_t i = tid; i < nd; i += stride) sin += in_len[dlist[i]];
+  e = warp_sum(e);
+  sin = warp_sum(sin);
+  if (lane_id() == 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(counters + 0), static_cast<unsigned long long>(e));
+    atomicAdd(reinterpret_cast<unsigned long long*>(counters + 5), static_cast<unsigned long long>(sin));
+  }
+  if (tid == 0) {
+    counters[1] = nd;
+    counters[2] = ns;
+  }
+}
+
+size_t frontier_ws_bytes(int64_t n) {
+  int64_t words = (n + 31) / 32;
+  return sizeof(int32_t) * (n + 1) + sizeof(int64_t) * (n + 2) + 256 * 4 +
+         sizeof(int64_t) * (scan_blocks_for(n > words ? n : words) + 2) * 4 + 8192;
+}
+
+}  // namespace rtec
+
+using namespace rtec;
+
+extern "C" int rtec_frontier_layer(const rtec_graph_t* g, const rtec_batch_t* b, int32_t l,
+                                   int32_t src_degree_dependent, const rtec_frontier_t* prev, rtec_frontier_t* f,
+                                   void* ws, size_t ws_bytes, rtec_stream_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int64_t n = g->n;
+  int64_t words = (n + 31) / 32;
+  if (l > 0 && prev == nullptr) {
+    set_error("frontier layer %d needs the previous layer's frontier", l);
+    return RTEC_CONFIG_ERROR;
+  }
+  Ws w(ws, ws_bytes);
+  int32_t* nlist = w.alloc<int32_t>(n + 1);
+  int64_t* noff = w.alloc<int64_t>(n + 2);
+  int64_t* n_new = w.alloc<int64_t>(4);
+  RTEC_WS_CHECK(w);
+  RTEC_CUDA(cudaMemsetAsync(f->counters, 0, sizeof(int64_t) * 8, s));
+  RTEC_CUDA(cudaMemsetAsync(n_new, 0, sizeof(int64_t) * 4, s));
+  RTEC_CUDA(cudaMemsetAsync(noff, 0, sizeof(int64_t), s));
+  const uint32_t* prev_src = nullptr;
+  if (l == 0) {
+    RTEC_CUDA(cudaMemsetAsync(f->bm_src, 0, sizeof(uint32_t) * words, s));
+    RTEC_CUDA(cudaMemsetAsync(f->bm_dst, 0, sizeof(uint32_t) * words, s));
+    k_seed_layer0<<<grid_for(b->cap * 2, kFBlk), kFBlk, 0, s>>>(*b, src_degree_dependent, f->bm_src, f->bm_dst);
+  } else {
+    // S(l) = S(l-1) ∪ V_dst(l-1); V_dst(l) starts as V_dst(l-1)
+    k_union_words<<<grid_for(words, kFBlk), kFBlk, 0, s>>>(prev->bm_src, prev->bm_dst, f->bm_src, words);
+    RTEC_CUDA(cudaMemcpyAsync(f->bm_dst, prev->bm_dst, sizeof(uint32_t) * words, cudaMemcpyDeviceToDevice, s));
+    prev_src = prev->bm_src;
+  }
+  // new sources N = S(l) \ S(l-1)
+  WordPop np{f->bm_src, prev_src};
+  RTEC_TRY(exclusive_scan(np, Count{nullptr, words}, words, WordList{np, nlist, nullptr}, n_new, w, s));
+  RTEC_TRY(exclusive_scan(OutLenOf{nlist, g->out.len}, Count{n_new, n}, n, StoreOffTailF{noff, n_new}, nullptr, w, s));
+  k_expand<<<kSMs * 8, kFBlk, 0, s>>>(nlist, n_new, noff, g->out, f->bm_dst);
+  RTEC_LAUNCH_CHECK("k_expand");
+  // lists + slots
+  WordPop sp{f->bm_src, nullptr};
+  RTEC_TRY(exclusive_scan(sp, Count{nullptr, words}, words, WordList{sp, f->src_list, f->src_slot}, f->n_src, w, s));
+  WordPop dp{f->bm_dst, nullptr};
+  RTEC_TRY(exclusive_scan(dp, Count{nullptr, words}, words, WordList{dp, f->dst_list, f->dst_slot}, f->n_dst, w, s));
+  k_counters<<<kSMs * 2, kFBlk, 0, s>>>(f->src_list, f->n_src, f->n_dst, g->out.len, g->in.len, f->dst_list, *b,
+                                        f->bm_src, f->counters);
+  RTEC_LAUNCH_CHECK("k_counters");
+  return RTEC_OK;
+}

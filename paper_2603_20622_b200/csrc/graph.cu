@@ -1,0 +1,811 @@
+// graph.cu -- the streaming CSR/CSC delta store.
+//
+// Replaces streamgnn/graph.py (DynamicGraph, coalesce_batch) and the PMA of
+// pma.py.  Each direction is a set of gapped per-vertex runs (rtec_adj_t):
+// sorted neighbour ids with reserved slack; a batch merges into touched runs
+// in place when the new length fits the capacity and relocates the run to the
+// arena tail otherwise.  All batch arithmetic is integer and bit-exact with
+// the reference.
+#include "prims.cuh"
+
+namespace rtec {
+
+constexpr int kBlk = 256;
+constexpr int32_t kArenaFullPos = 0x7fffffff;  // err position for arena/scratch exhaustion
+constexpr int32_t kCodeArenaFull = RTEC_ARENA_FULL;  // compact (or grow workspace) and retry
+
+__host__ __device__ __forceinline__ int32_t cap_for(int32_t len, float slack, int32_t min_slack) {
+  int32_t extra = static_cast<int32_t>(ceilf(static_cast<float>(len) * slack));
+  if (extra < min_slack) extra = min_slack;
+  return len + extra;
+}
+
+// ------------------------------------------------------------------ small kernels
+__global__ void k_fill_u64(uint64_t* p, uint64_t v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+// degrees of a bulk edge list (from_edges graph.py:101-102, :118-119)
+__global__ void k_count_degrees(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t m,
+                                int64_t n, int32_t* out_deg, int32_t* in_deg, uint64_t* err) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t s = src[i], d = dst[i];
+    if (s < 0 || s >= n || d < 0 || d >= n) {
+      report_error(err, RTEC_INVALID_VERTEX, 0);
+      continue;
+    }
+    atomicAdd(out_deg + s, 1);
+    atomicAdd(in_deg + d, 1);
+  }
+}
+
+struct CapOf {
+  const int32_t* len;
+  float slack;
+  int32_t min_slack;
+  __device__ __forceinline__ int64_t operator()(int64_t v) const { return cap_for(len[v], slack, min_slack); }
+};
+
+// build runs: beg/cap/len from degrees
+struct StoreBeg {
+  const int32_t* len;
+  int64_t* beg;
+  int32_t* cap;
+  int32_t* lenout;
+  __device__ __forceinline__ void operator()(int64_t v, int64_t off, int64_t c) const {
+    beg[v] = off;
+    cap[v] = static_cast<int32_t>(c);
+    lenout[v] = len[v];
+  }
+};
+
+__global__ void k_make_keys_bulk(const int32_t* __restrict__ a, const int32_t* __restrict__ b, int64_t m, int64_t n,
+                                 uint64_t* keys, uint32_t* vals) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = static_cast<uint64_t>(a[i]) * static_cast<uint64_t>(n) + static_cast<uint64_t>(b[i]);
+    vals[i] = static_cast<uint32_t>(i);
+  }
+}
+
+// scatter sorted keys into runs; duplicates -> ConfigError (graph.py:106-107)
+__global__ void k_fill_runs(const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ sidx, int64_t m, int64_t n,
+                            const int64_t* __restrict__ beg, int32_t* __restrict__ nbr, int64_t* __restrict__ ts_out,
+                            const int64_t* __restrict__ ts_in, uint64_t* err) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = skeys[i];
+    if (i > 0 && skeys[i - 1] == k) report_error(err, RTEC_CONFIG_ERROR, 1);
+    int64_t v = static_cast<int64_t>(k / static_cast<uint64_t>(n));
+    int32_t w = static_cast<int32_t>(k - static_cast<uint64_t>(v) * n);
+    // position inside the run = i - first index of v's keys; runs are contiguous in sorted order
+    int64_t lo = lower_bound_dev(skeys, 0, i + 1, static_cast<uint64_t>(v) * n);
+    int64_t slot = beg[v] + (i - lo);
+    nbr[slot] = w;
+    if (ts_out) ts_out[slot] = ts_in ? ts_in[sidx[i]] : static_cast<int64_t>(sidx[i]);
+  }
+}
+
+// ------------------------------------------------------------------ build
+static int build_direction(int64_t n, rtec_adj_t* a, const int32_t* own, const int32_t* nb, const int64_t* ts,
+                           int64_t m, const int32_t* deg, float slack, int32_t min_slack, uint64_t* err,
+                           Ws& ws, cudaStream_t s) {
+  RTEC_TRY(exclusive_scan(CapOf{deg, slack, min_slack}, Count{nullptr, n}, n,
+                          StoreBeg{deg, a->beg, a->cap, a->len}, a->top, ws, s));
+  if (m == 0) return RTEC_OK;
+  uint64_t* keys = ws.alloc<uint64_t>(m);
+  uint32_t* vals = ws.alloc<uint32_t>(m);
+  uint64_t* sk = ws.alloc<uint64_t>(m);
+  uint32_t* sv = ws.alloc<uint32_t>(m);
+  RTEC_WS_CHECK(ws);
+  k_make_keys_bulk<<<grid_for(m, kBlk), kBlk, 0, s>>>(own, nb, m, n, keys, vals);
+  int bits = bits_for(static_cast<uint64_t>(n) * static_cast<uint64_t>(n));
+  RTEC_TRY(sort_pairs(keys, vals, sk, sv, Count{nullptr, m}, m, bits, ws, s));
+  k_fill_runs<<<grid_for(m, kBlk), kBlk, 0, s>>>(sk, sv, m, n, a->beg, a->nbr, a->ts, ts, err);
+  RTEC_LAUNCH_CHECK("k_fill_runs");
+  return RTEC_OK;
+}
+
+// ------------------------------------------------------------------ export / compact
+// warp per vertex: copy run v to dst at off[v]
+__global__ void k_copy_runs(int64_t n, const int64_t* __restrict__ beg, const int32_t* __restrict__ len,
+                            const int32_t* __restrict__ nbr, const int64_t* __restrict__ ts,
+                            const int64_t* __restrict__ off, int32_t* out_v, int32_t* out_nbr, int64_t* out_ts,
+                            int64_t* new_beg, int32_t* new_len) {
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int lane = lane_id();
+  for (int64_t v = warp; v < n; v += nw) {
+    int64_t b = beg[v], o = off[v];
+    int32_t L = len[v];
+    for (int32_t j = lane; j < L; j += 32) {
+      out_nbr[o + j] = nbr[b + j];
+      if (out_ts && ts) out_ts[o + j] = ts[b + j];
+      if (out_v) out_v[o + j] = static_cast<int32_t>(v);
+    }
+    if (lane == 0 && new_beg) {
+      new_beg[v] = o;
+      new_len[v] = L;
+    }
+  }
+}
+
+struct NopOut {
+  __device__ __forceinline__ void operator()(int64_t, int64_t, int64_t) const {}
+};
+
+struct LenAt {
+  const int32_t* len;
+  __device__ __forceinline__ int64_t operator()(int64_t v) const { return len[v]; }
+};
+
+// ------------------------------------------------------------------ coalesce
+__global__ void k_coalesce_keys(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t B,
+                                uint64_t* keys, uint32_t* vals) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = (static_cast<uint64_t>(static_cast<uint32_t>(src[i])) << 32) | static_cast<uint32_t>(dst[i]);
+    vals[i] = static_cast<uint32_t>(i);
+  }
+}
+
+// group heads fold the per-key FSM (graph.py:248-259) sequentially and
+// record the survivor at the key's first position.
+__global__ void k_coalesce_fold(const uint64_t* __restrict__ sk, const uint32_t* __restrict__ sv, int64_t B,
+                                const uint8_t* __restrict__ op, uint8_t* keep) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i > 0 && sk[i - 1] == sk[i]) continue;  // not a head
+    uint32_t first = sv[i];
+    int64_t cur = sv[i];  // index of the surviving event, -1 = None
+    for (int64_t j = i + 1; j < B && sk[j] == sk[i]; ++j) {
+      uint32_t e = sv[j];
+      if (cur < 0) cur = e;
+      else if (op[cur] != op[e]) cur = -1;
+    }
+    // keep[first] = 1 + (survivor index encoded separately)
+    keep[first] = cur >= 0 ? 1 : 0;
+    // stash survivor index in the sorted-value slot of the head (re-used below)
+    const_cast<uint32_t*>(sv)[i] = cur >= 0 ? static_cast<uint32_t>(cur) : 0xffffffffu;
+    // map first appearance -> head position via keys (done by k_coalesce_map)
+  }
+}
+
+__global__ void k_coalesce_map(const uint64_t* __restrict__ sk, const uint32_t* __restrict__ sv_orig,
+                               const uint32_t* __restrict__ sv_surv, int64_t B, uint32_t* surv_at_first) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i > 0 && sk[i - 1] == sk[i]) continue;
+    surv_at_first[sv_orig[i]] = sv_surv[i];
+  }
+}
+
+struct KeepAt {
+  const uint8_t* keep;
+  __device__ __forceinline__ int64_t operator()(int64_t i) const { return keep[i]; }
+};
+struct CoalesceOut {
+  const uint8_t* keep;
+  const uint32_t* surv;
+  const int32_t* src; const int32_t* dst; const uint8_t* op; const int64_t* ts;
+  int32_t* os; int32_t* od; uint8_t* oo; int64_t* ot;
+  __device__ __forceinline__ void operator()(int64_t i, int64_t off, int64_t v) const {
+    if (!v) return;
+    uint32_t e = surv[i];
+    os[off] = src[e];
+    od[off] = dst[e];
+    oo[off] = op[e];
+    ot[off] = ts[e];
+  }
+};
+
+// ------------------------------------------------------------------ apply: validation + probe
+__global__ void k_apply_keys(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t B, int64_t n,
+                             uint64_t* keys, uint32_t* vals, uint64_t* err) {
+  uint64_t inval = static_cast<uint64_t>(n) * static_cast<uint64_t>(n);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t s = src[i], d = dst[i];
+    bool ok = s >= 0 && s < n && d >= 0 && d < n;  // graph.py:192-194 (_check)
+    if (!ok) report_error(err, RTEC_INVALID_VERTEX, i);
+    keys[i] = ok ? static_cast<uint64_t>(s) * n + static_cast<uint64_t>(d) : inval;
+    vals[i] = static_cast<uint32_t>(i);
+  }
+}
+
+__global__ void k_apply_dups(const uint64_t* __restrict__ sk, const uint32_t* __restrict__ sv, int64_t B, int64_t n,
+                             uint64_t* err) {
+  uint64_t inval = static_cast<uint64_t>(n) * static_cast<uint64_t>(n);
+  for (int64_t i = 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x) {
+    if (sk[i] == sk[i - 1] && sk[i] != inval) report_error(err, RTEC_CONFIG_ERROR, sv[i]);  // graph.py:195-197
+  }
+}
+
+// existence probe of each (sorted) update in the pre-batch out-run of its src
+__global__ void k_apply_probe(const uint64_t* __restrict__ sk, const uint32_t* __restrict__ sv, int64_t B, int64_t n,
+                              rtec_adj_t out, const uint8_t* __restrict__ op, uint8_t* status, uint8_t* aflag,
+                              const uint64_t* err) {
+  if (err_set(err)) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = sk[i];
+    int32_t s = static_cast<int32_t>(k / static_cast<uint64_t>(n));
+    int32_t d = static_cast<int32_t>(k - static_cast<uint64_t>(s) * n);
+    int64_t b = out.beg[s];
+    int32_t L = out.len[s];
+    int64_t p = lower_bound_dev(out.nbr, b, b + L, d);
+    bool exists = p < b + L && out.nbr[p] == d;
+    uint32_t e = sv[i];
+    bool applied = (op[e] == RTEC_OP_INSERT) ? !exists : exists;  // graph.py:209-219
+    status[e] = applied ? 1 : 0;
+    aflag[i] = applied ? 1 : 0;
+  }
+}
+
+struct FlagAt {
+  const uint8_t* f;
+  __device__ __forceinline__ int64_t operator()(int64_t i) const { return f[i]; }
+};
+struct CompactApplied {
+  const uint8_t* f;
+  const uint64_t* sk; const uint32_t* sv; int64_t n;
+  const uint8_t* op; const int64_t* ts;
+  int32_t* as; int32_t* ad; uint8_t* ao; int64_t* at;
+  __device__ __forceinline__ void operator()(int64_t i, int64_t off, int64_t v) const {
+    if (!v) return;
+    uint64_t k = sk[i];
+    int32_t s = static_cast<int32_t>(k / static_cast<uint64_t>(n));
+    as[off] = s;
+    ad[off] = static_cast<int32_t>(k - static_cast<uint64_t>(s) * n);
+    uint32_t e = sv[i];
+    ao[off] = op[e];
+    at[off] = ts[e];
+  }
+};
+
+__global__ void k_in_keys(const int32_t* __restrict__ as, const int32_t* __restrict__ ad, const int64_t* cnt, int64_t n,
+                          uint64_t* keys, uint32_t* vals) {
+  int64_t K = *cnt;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = static_cast<uint64_t>(ad[i]) * n + static_cast<uint64_t>(as[i]);
+    vals[i] = static_cast<uint32_t>(i);
+  }
+}
+
+__global__ void k_in_gather(const uint32_t* __restrict__ sv, const int64_t* cnt, const int32_t* __restrict__ as,
+                            const int32_t* __restrict__ ad, const uint8_t* __restrict__ ao, int32_t* is, int32_t* id,
+                            uint8_t* io) {
+  int64_t K = *cnt;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t e = sv[i];
+    is[i] = as[e];
+    id[i] = ad[e];
+    io[i] = ao[e];
+  }
+}
+
+// ------------------------------------------------------------------ run merge
+// Updates of one direction sorted by (owner, neighbour); groups = touched runs.
+struct MergeIn {
+  const int32_t* own;
+  const int32_t* nbr;
+  const uint8_t* op;
+  const int64_t* ts;  // may be null
+  const int64_t* K;   // device count
+  int64_t maxK;
+};
+
+struct MergePlan {
+  int64_t* pre_ins;   // [maxK+1] exclusive prefix of is_insert
+  int64_t* gstart;    // [maxK+1]
+  int32_t* gv;        // [maxK]
+  int64_t* G;         // [1]
+  int64_t* work_off;  // [maxK+1]
+  int64_t* scr_off;   // [maxK+1]
+  int64_t* arena_off; // [maxK+1]
+  int64_t* dest;      // [maxK]
+  int32_t* newlen;    // [maxK]
+  int32_t* newcap;    // [maxK]
+  uint8_t* inplace;   // [maxK]
+  int64_t* totals;    // [4]: work, scratch, arena demand, base(top before)
+  int32_t* scr_nbr;   // [scr_cap]
+  int64_t* scr_ts;    // [scr_cap] or null
+  int64_t scr_cap;
+};
+
+struct IsIns {
+  const uint8_t* op;
+  __device__ __forceinline__ int64_t operator()(int64_t i) const { return op[i] == RTEC_OP_INSERT ? 1 : 0; }
+};
+struct StorePrefixTail {
+  int64_t* dst;
+  const int64_t* K;
+  __device__ __forceinline__ void operator()(int64_t i, int64_t off, int64_t v) const {
+    dst[i] = off;
+    if (i == *K - 1) dst[i + 1] = off + v;
+  }
+};
+struct IsHead {
+  const int32_t* own;
+  __device__ __forceinline__ int64_t operator()(int64_t i) const { return (i == 0 || own[i] != own[i - 1]) ? 1 : 0; }
+};
+struct StoreHead {
+  const int32_t* own;
+  int64_t* gstart;
+  int32_t* gv;
+  const int64_t* K;
+  __device__ __forceinline__ void operator()(int64_t i, int64_t off, int64_t v) const {
+    if (v) {
+      gstart[off] = i;
+      gv[off] = own[i];
+    }
+    if (i == *K - 1) gstart[off + v] = *K;
+  }
+};
+
+__global__ void k_group_info(MergeIn in, MergePlan p, rtec_adj_t a, float slack, int32_t min_slack,
+                             const uint64_t* err) {
+  int64_t G = *p.G;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x) {
+    int64_t s = p.gstart[g], e = p.gstart[g + 1];
+    int32_t v = p.gv[g];
+    int64_t nins = p.pre_ins[e] - p.pre_ins[s];
+    int64_t ndel = (e - s) - nins;
+    int32_t L = a.len[v];
+    int32_t nl = static_cast<int32_t>(L + nins - ndel);
+    bool inpl = nl <= a.cap[v];
+    p.newlen[g] = nl;
+    p.inplace[g] = inpl ? 1 : 0;
+    p.newcap[g] = inpl ? a.cap[v] : cap_for(nl, slack, min_slack);
+  }
+}
+
+struct WorkOf {
+  MergePlan p;
+  const int32_t* len;
+  __device__ __forceinline__ int64_t operator()(int64_t g) const {
+    return static_cast<int64_t>(len[p.gv[g]]) + (p.gstart[g + 1] - p.gstart[g]);
+  }
+};
+struct ScrOf {
+  MergePlan p;
+  __device__ __forceinline__ int64_t operator()(int64_t g) const { return p.inplace[g] ? p.newlen[g] : 0; }
+};
+struct ArenaOf {
+  MergePlan p;
+  __device__ __forceinline__ int64_t operator()(int64_t g) const { return p.inplace[g] ? 0 : p.newcap[g]; }
+};
+struct StoreOffTail {
+  int64_t* dst;
+  const int64_t* G;
+  __device__ __forceinline__ void operator()(int64_t i, int64_t off, int64_t v) const {
+    dst[i] = off;
+    if (i == *G - 1) dst[i + 1] = off + v;
+  }
+};
+
+// reserve arena space for relocated runs (single thread): all-or-nothing
+__global__ void k_reserve(MergePlan p, rtec_adj_t a, uint64_t* err) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int64_t G = *p.G;
+  int64_t demand = G > 0 ? p.arena_off[G] : 0;
+  int64_t scr = G > 0 ? p.scr_off[G] : 0;
+  int64_t top = *a.top;
+  p.totals[0] = G > 0 ? p.work_off[G] : 0;
+  p.totals[1] = scr;
+  p.totals[2] = demand;
+  p.totals[3] = top;
+  if (err_set(err)) return;
+  if (top + demand > a.slots || scr > p.scr_cap) {
+    report_error(err, kCodeArenaFull, kArenaFullPos);
+    return;
+  }
+}
+
+__global__ void k_commit_reserve(MergePlan p, rtec_adj_t a, const uint64_t* err) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (err_set(err)) return;
+  *a.top = p.totals[3] + p.totals[2];
+}
+
+__global__ void k_set_dest(MergePlan p, const uint64_t* err) {
+  int64_t G = *p.G;
+  int64_t base = p.totals[3];
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x) {
+    p.dest[g] = p.inplace[g] ? -1 : base + p.arena_off[g];
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ int64_t upper_bound_dev(const T* a, int64_t lo, int64_t hi, T key) {
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (a[mid] <= key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// element-parallel merge: old elements and update items of every group
+__global__ void k_merge_items(MergeIn in, MergePlan p, rtec_adj_t a, const uint64_t* err) {
+  if (err_set(err)) return;
+  int64_t G = *p.G;
+  if (G == 0) return;
+  int64_t W = p.work_off[G];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < W; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t g = upper_bound_dev<int64_t>(p.work_off, 0, G, i) - 1;
+    int64_t t = i - p.work_off[g];
+    int32_t v = p.gv[g];
+    int64_t s = p.gstart[g], e = p.gstart[g + 1];
+    int64_t b = a.beg[v];
+    int32_t L = a.len[v];
+    int32_t w;
+    int64_t tsv = 0;
+    int64_t out;
+    if (t < L) {
+      w = a.nbr[b + t];
+      int64_t q = lower_bound_dev(in.nbr, s, e, w);
+      if (q < e && in.nbr[q] == w) continue;  // deleted (an applied insert never hits an existing key)
+      int64_t ins_before = p.pre_ins[q] - p.pre_ins[s];
+      int64_t del_before = (q - s) - ins_before;
+      out = t - del_before + ins_before;
+      if (a.ts) tsv = a.ts[b + t];
+    } else {
+      int64_t k = s + (t - L);
+      if (in.op[k] != RTEC_OP_INSERT) continue;
+      w = in.nbr[k];
+      int64_t pos = lower_bound_dev(a.nbr, b, b + L, w) - b;
+      int64_t ins_before = p.pre_ins[k] - p.pre_ins[s];
+      int64_t del_before = (k - s) - ins_before;
+      out = pos - del_before + ins_before;
+      if (in.ts) tsv = in.ts[k];
+    }
+    int64_t dst = p.inplace[g] ? -1 : p.dest[g] + out;
+    if (dst < 0) {
+      int64_t so = p.scr_off[g] + out;
+      p.scr_nbr[so] = w;
+      if (p.scr_ts) p.scr_ts[so] = tsv;
+    } else {
+      a.nbr[dst] = w;
+      if (a.ts) a.ts[dst] = tsv;
+    }
+  }
+}
+
+// copy in-place runs back from scratch (after all reads of the old runs)
+__global__ void k_merge_copyback(MergePlan p, rtec_adj_t a, const uint64_t* err) {
+  if (err_set(err)) return;
+  int64_t G = *p.G;
+  if (G == 0) return;
+  int64_t S = p.scr_off[G];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t g = upper_bound_dev<int64_t>(p.scr_off, 0, G, i) - 1;
+    int32_t v = p.gv[g];
+    int64_t t = i - p.scr_off[g];
+    a.nbr[a.beg[v] + t] = p.scr_nbr[i];
+    if (a.ts) a.ts[a.beg[v] + t] = p.scr_ts[i];
+  }
+}
+
+__global__ void k_merge_commit(MergePlan p, rtec_adj_t a, const uint64_t* err) {
+  if (err_set(err)) return;
+  int64_t G = *p.G;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x) {
+    int32_t v = p.gv[g];
+    a.len[v] = p.newlen[g];
+    if (!p.inplace[g]) {
+      a.beg[v] = p.dest[g];
+      a.cap[v] = p.newcap[g];
+    }
+  }
+}
+
+static int plan_alloc(MergePlan& p, int64_t maxK, int64_t scr_cap, bool with_ts, Ws& ws) {
+  p.pre_ins = ws.alloc<int64_t>(maxK + 2);
+  p.gstart = ws.alloc<int64_t>(maxK + 2);
+  p.gv = ws.alloc<int32_t>(maxK + 1);
+  p.G = ws.alloc<int64_t>(4);
+  p.work_off = ws.alloc<int64_t>(maxK + 2);
+  p.scr_off = ws.alloc<int64_t>(maxK + 2);
+  p.arena_off = ws.alloc<int64_t>(maxK + 2);
+  p.dest = ws.alloc<int64_t>(maxK + 1);
+  p.newlen = ws.alloc<int32_t>(maxK + 1);
+  p.newcap = ws.alloc<int32_t>(maxK + 1);
+  p.inplace = ws.alloc<uint8_t>(maxK + 1);
+  p.totals = ws.alloc<int64_t>(4);
+  p.scr_cap = scr_cap;
+  p.scr_nbr = ws.alloc<int32_t>(scr_cap);
+  p.scr_ts = with_ts ? ws.alloc<int64_t>(scr_cap) : nullptr;
+  RTEC_WS_CHECK(ws);
+  return RTEC_OK;
+}
+
+// plan: groups, new lengths, offsets, arena reservation; no mutation
+static int merge_plan(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, float slack, int32_t min_slack,
+                      uint64_t* err, Ws& ws, cudaStream_t s) {
+  RTEC_CUDA(cudaMemsetAsync(p.G, 0, sizeof(int64_t), s));
+  RTEC_CUDA(cudaMemsetAsync(p.pre_ins, 0, sizeof(int64_t), s));
+  RTEC_CUDA(cudaMemsetAsync(p.gstart, 0, sizeof(int64_t), s));
+  Count K{in.K, in.maxK};
+  RTEC_TRY(exclusive_scan(IsIns{in.op}, K, in.maxK, StorePrefixTail{p.pre_ins, in.K}, nullptr, ws, s));
+  RTEC_TRY(exclusive_scan(IsHead{in.own}, K, in.maxK, StoreHead{in.own, p.gstart, p.gv, in.K}, p.G, ws, s));
+  k_group_info<<<grid_for(in.maxK, kBlk), kBlk, 0, s>>>(in, p, a, slack, min_slack, err);
+  Count G{p.G, in.maxK};
+  RTEC_CUDA(cudaMemsetAsync(p.work_off, 0, sizeof(int64_t), s));
+  RTEC_CUDA(cudaMemsetAsync(p.scr_off, 0, sizeof(int64_t), s));
+  RTEC_CUDA(cudaMemsetAsync(p.arena_off, 0, sizeof(int64_t), s));
+  RTEC_TRY(exclusive_scan(WorkOf{p, a.len}, G, in.maxK, StoreOffTail{p.work_off, p.G}, nullptr, ws, s));
+  RTEC_TRY(exclusive_scan(ScrOf{p}, G, in.maxK, StoreOffTail{p.scr_off, p.G}, nullptr, ws, s));
+  RTEC_TRY(exclusive_scan(ArenaOf{p}, G, in.maxK, StoreOffTail{p.arena_off, p.G}, nullptr, ws, s));
+  k_reserve<<<1, 32, 0, s>>>(p, a, err);
+  k_set_dest<<<grid_for(in.maxK, kBlk), kBlk, 0, s>>>(p, err);
+  RTEC_LAUNCH_CHECK("merge_plan");
+  return RTEC_OK;
+}
+
+static int merge_exec(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, int64_t work_bound, uint64_t* err,
+                      cudaStream_t s) {
+  k_merge_items<<<grid_for(work_bound, kBlk, kSMs * 32), kBlk, 0, s>>>(in, p, a, err);
+  k_merge_copyback<<<grid_for(work_bound, kBlk, kSMs * 32), kBlk, 0, s>>>(p, a, err);
+  k_merge_commit<<<grid_for(in.maxK, kBlk), kBlk, 0, s>>>(p, a, err);
+  k_commit_reserve<<<1, 32, 0, s>>>(p, a, err);
+  RTEC_LAUNCH_CHECK("merge_exec");
+  return RTEC_OK;
+}
+
+// ------------------------------------------------------------------ degrees + deltas
+__global__ void k_apply_degrees(const int32_t* __restrict__ as, const int32_t* __restrict__ ad,
+                                const uint8_t* __restrict__ ao, const int64_t* cnt, int32_t* out_deg,
+                                int32_t* in_deg, int64_t* num_edges, const uint64_t* err) {
+  if (err_set(err)) return;
+  int64_t K = *cnt;
+  int64_t local = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t d = ao[i] == RTEC_OP_INSERT ? 1 : -1;
+    atomicAdd(out_deg + as[i], d);
+    atomicAdd(in_deg + ad[i], d);
+    local += d;
+  }
+  local = warp_sum(local);
+  if (lane_id() == 0 && local != 0) atomicAdd(reinterpret_cast<unsigned long long*>(num_edges),
+                                              static_cast<unsigned long long>(local));
+}
+
+__global__ void k_touched_keys(const int32_t* __restrict__ as, const int32_t* __restrict__ ad, const int64_t* cnt,
+                               uint64_t* keys, uint32_t* vals, int64_t* cnt2) {
+  int64_t K = *cnt;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *cnt2 = 2 * K;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x) {
+    keys[2 * i] = static_cast<uint64_t>(as[i]);
+    keys[2 * i + 1] = static_cast<uint64_t>(ad[i]);
+    vals[2 * i] = 0;
+    vals[2 * i + 1] = 0;
+  }
+}
+
+struct DeltaFlag {
+  const uint64_t* sk;
+  const int32_t* in_deg; const int32_t* out_deg; const int32_t* in_prev; const int32_t* out_prev;
+  __device__ __forceinline__ int64_t operator()(int64_t i) const {
+    if (i > 0 && sk[i] == sk[i - 1]) return 0;
+    int32_t v = static_cast<int32_t>(sk[i]);
+    return (in_deg[v] != in_prev[v] || out_deg[v] != out_prev[v]) ? 1 : 0;
+  }
+};
+struct DeltaOut {
+  DeltaFlag f;
+  int32_t* dv; int32_t* doi; int32_t* dni; int32_t* doo; int32_t* dno;
+  __device__ __forceinline__ void operator()(int64_t i, int64_t off, int64_t v) const {
+    if (!v) return;
+    int32_t x = static_cast<int32_t>(f.sk[i]);
+    dv[off] = x;
+    doi[off] = f.in_prev[x];
+    dni[off] = f.in_deg[x];
+    doo[off] = f.out_prev[x];
+    dno[off] = f.out_deg[x];
+  }
+};
+
+__global__ void k_commit_degrees(const int32_t* __restrict__ dv, const int64_t* cnt, const int32_t* in_deg,
+                                 const int32_t* out_deg, int32_t* in_prev, int32_t* out_prev) {
+  int64_t K = *cnt;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t v = dv[i];
+    in_prev[v] = in_deg[v];
+    out_prev[v] = out_deg[v];
+  }
+}
+
+// ------------------------------------------------------------------ workspace sizing
+size_t batch_ws_bytes(int64_t n, int64_t B, int64_t scr_cap) {
+  size_t b = 0;
+  auto add = [&](size_t x) { b += (x + 255) & ~size_t(255); };
+  int64_t B2 = 2 * B + 2;
+  for (int i = 0; i < 3; ++i) {  // keys/vals/sorted copies for up to 2B entries
+    add(sizeof(uint64_t) * B2);
+    add(sizeof(uint32_t) * B2);
+  }
+  add(B2);
+  add(sizeof(int64_t) * 8);
+  for (int d = 0; d < 2; ++d) {  // two merge plans
+    add(sizeof(int64_t) * (B + 2) * 6);
+    add(sizeof(int32_t) * (B + 2) * 3);
+    add(B + 2);
+    add(sizeof(int64_t) * 8);
+    add(sizeof(int32_t) * scr_cap);
+    add(sizeof(int64_t) * scr_cap);
+  }
+  add(sort_ws_bytes(B2));
+  add(sizeof(int64_t) * (scan_blocks_for(B2) + 2) * 12);
+  return b + (1 << 16);
+}
+
+}  // namespace rtec
+
+using namespace rtec;
+
+extern "C" {
+
+int rtec_graph_count(const int32_t* src, const int32_t* dst, int64_t m, int64_t n, int32_t* out_deg,
+                     int32_t* in_deg, uint64_t* err, rtec_stream_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (m > 0) k_count_degrees<<<grid_for(m, kBlk), kBlk, 0, s>>>(src, dst, m, n, out_deg, in_deg, err);
+  RTEC_LAUNCH_CHECK("k_count_degrees");
+  return RTEC_OK;
+}
+
+int rtec_graph_slots_needed(const int32_t* len, int64_t n, float slack, int32_t min_slack, int64_t* slots_dev,
+                            void* ws, size_t ws_bytes, rtec_stream_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Ws w(ws, ws_bytes);
+  return exclusive_scan(CapOf{len, slack, min_slack}, Count{nullptr, n}, n, NopOut{}, slots_dev, w, s);
+}
+
+int rtec_graph_build(rtec_graph_t* g, const int32_t* src, const int32_t* dst, const int64_t* ts, int64_t m,
+                     float slack, int32_t min_slack, uint64_t* err, void* ws, size_t ws_bytes,
+                     rtec_stream_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int64_t n = g->n;
+  {
+    Ws w(ws, ws_bytes);
+    RTEC_TRY(build_direction(n, &g->out, src, dst, ts, m, g->out_deg, slack, min_slack, err, w, s));
+  }
+  {
+    Ws w(ws, ws_bytes);
+    RTEC_TRY(build_direction(n, &g->in, dst, src, nullptr, m, g->in_deg, slack, min_slack, err, w, s));
+  }
+  RTEC_CUDA(cudaMemcpyAsync(g->out_deg_prev, g->out_deg, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
+  RTEC_CUDA(cudaMemcpyAsync(g->in_deg_prev, g->in_deg, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
+  RTEC_CUDA(cudaMemcpyAsync(g->num_edges, &m, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  RTEC_CUDA(cudaStreamSynchronize(s));  // &m is a host stack value
+  return RTEC_OK;
+}
+
+int rtec_adj_export(int64_t n, const rtec_adj_t* a, int32_t* out_v, int32_t* out_nbr, int64_t* out_ts, void* ws,
+                    size_t ws_bytes, rtec_stream_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Ws w(ws, ws_bytes);
+  int64_t* off = w.alloc<int64_t>(n + 1);
+  RTEC_WS_CHECK(w);
+  RTEC_TRY(exclusive_scan(LenAt{a->len}, Count{nullptr, n}, n, StorePrefix{off}, nullptr, w, s));
+  k_copy_runs<<<grid_for(n * 32, kBlk, kSMs * 16), kBlk, 0, s>>>(n, a->beg, a->len, a->nbr, a->ts, off, out_v,
+                                                                 out_nbr, out_ts, nullptr, nullptr);
+  RTEC_LAUNCH_CHECK("k_copy_runs");
+  return RTEC_OK;
+}
+
+int rtec_adj_compact(int64_t n, const rtec_adj_t* src, rtec_adj_t* dst, float slack, int32_t min_slack, void* ws,
+                     size_t ws_bytes, rtec_stream_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Ws w(ws, ws_bytes);
+  // new beg/cap from current lengths (dst->len receives the lengths)
+  RTEC_TRY(exclusive_scan(CapOf{src->len, slack, min_slack}, Count{nullptr, n}, n,
+                          StoreBeg{src->len, dst->beg, dst->cap, dst->len}, dst->top, w, s));
+  k_copy_runs<<<grid_for(n * 32, kBlk, kSMs * 16), kBlk, 0, s>>>(n, src->beg, src->len, src->nbr, src->ts, dst->beg,
+                                                                 nullptr, dst->nbr, dst->ts, nullptr, nullptr);
+  RTEC_LAUNCH_CHECK("compact");
+  return RTEC_OK;
+}
+
+int rtec_batch_coalesce(const int32_t* src, const int32_t* dst, const uint8_t* op, const int64_t* ts, int64_t B,
+                        int32_t* out_src, int32_t* out_dst, uint8_t* out_op, int64_t* out_ts, int64_t* n_out,
+                        void* ws, size_t ws_bytes, rtec_stream_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  RTEC_CUDA(cudaMemsetAsync(n_out, 0, sizeof(int64_t), s));
+  if (B <= 0) return RTEC_OK;
+  Ws w(ws, ws_bytes);
+  uint64_t* keys = w.alloc<uint64_t>(B);
+  uint32_t* vals = w.alloc<uint32_t>(B);
+  uint64_t* sk = w.alloc<uint64_t>(B);
+  uint32_t* sv = w.alloc<uint32_t>(B);
+  uint32_t* sv2 = w.alloc<uint32_t>(B);
+  uint8_t* keep = w.alloc<uint8_t>(B);
+  uint32_t* surv = w.alloc<uint32_t>(B);
+  RTEC_WS_CHECK(w);
+  k_coalesce_keys<<<grid_for(B, kBlk), kBlk, 0, s>>>(src, dst, B, keys, vals);
+  RTEC_TRY(sort_pairs(keys, vals, sk, sv, Count{nullptr, B}, B, 64, w, s));
+  RTEC_CUDA(cudaMemcpyAsync(sv2, sv, sizeof(uint32_t) * B, cudaMemcpyDeviceToDevice, s));
+  RTEC_CUDA(cudaMemsetAsync(keep, 0, B, s));
+  k_coalesce_fold<<<grid_for(B, kBlk), kBlk, 0, s>>>(sk, sv2, B, op, keep);
+  k_coalesce_map<<<grid_for(B, kBlk), kBlk, 0, s>>>(sk, sv, sv2, B, surv);
+  RTEC_TRY(exclusive_scan(KeepAt{keep}, Count{nullptr, B}, B,
+                          CoalesceOut{keep, surv, src, dst, op, ts, out_src, out_dst, out_op, out_ts}, n_out, w, s));
+  return RTEC_OK;
+}
+
+int rtec_batch_apply(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src, const int32_t* dst, const uint8_t* op,
+                     const int64_t* ts, int64_t B, void* ws, size_t ws_bytes, rtec_stream_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int64_t n = g->n;
+  if (B > b->cap) {
+    set_error("batch of %lld updates exceeds capacity %lld", (long long)B, (long long)b->cap);
+    return RTEC_SHAPE_ERROR;
+  }
+  RTEC_CUDA(cudaMemsetAsync(b->err, 0xff, sizeof(uint64_t), s));
+  RTEC_CUDA(cudaMemsetAsync(b->n_applied, 0, sizeof(int64_t), s));
+  RTEC_CUDA(cudaMemsetAsync(b->n_delta, 0, sizeof(int64_t), s));
+  if (B <= 0) return RTEC_OK;
+  Ws w(ws, ws_bytes);
+  int64_t B2 = 2 * B;
+  uint64_t* keys = w.alloc<uint64_t>(B2);
+  uint32_t* vals = w.alloc<uint32_t>(B2);
+  uint64_t* sk = w.alloc<uint64_t>(B2);
+  uint32_t* sv = w.alloc<uint32_t>(B2);
+  uint8_t* aflag = w.alloc<uint8_t>(B);
+  int64_t* cnt2 = w.alloc<int64_t>(2);
+  // scratch capacity for in-place run merges: whatever workspace remains, split over 2 plans
+  MergePlan po, pi;
+  size_t plan_fixed = sizeof(int64_t) * (B + 2) * 7 + sizeof(int32_t) * (B + 2) * 3 + (B + 2) + 4096;
+  size_t sort_reserve = sort_ws_bytes(B2) + sizeof(int64_t) * (scan_blocks_for(B2) + 2) * 16 + (1 << 16);
+  size_t used = w.off + 2 * plan_fixed + sort_reserve;
+  int64_t scr_cap = used < w.bytes ? static_cast<int64_t>((w.bytes - used) / 2 / (sizeof(int32_t) + sizeof(int64_t) + 1)) : 0;
+  RTEC_TRY(plan_alloc(po, B, scr_cap, true, w));
+  RTEC_TRY(plan_alloc(pi, B, scr_cap, false, w));
+  RTEC_WS_CHECK(w);
+  size_t mark = w.off;
+  const int grid = grid_for(B, kBlk);
+  // 1. keys + range validation; 2. sort; 3. duplicate validation
+  k_apply_keys<<<grid, kBlk, 0, s>>>(src, dst, B, n, keys, vals, b->err);
+  int bits = bits_for(static_cast<uint64_t>(n) * static_cast<uint64_t>(n));
+  RTEC_TRY(sort_pairs(keys, vals, sk, sv, Count{nullptr, B}, B, bits, w, s));
+  w.off = mark;
+  k_apply_dups<<<grid, kBlk, 0, s>>>(sk, sv, B, n, b->err);
+  // 4. probe against the pre-batch graph (skipped on validation error: no flags -> nothing applied)
+  RTEC_CUDA(cudaMemsetAsync(aflag, 0, B, s));
+  k_apply_probe<<<grid, kBlk, 0, s>>>(sk, sv, B, n, g->out, op, b->status, aflag, b->err);
+  // 5. applied updates in out-key order
+  RTEC_TRY(exclusive_scan(FlagAt{aflag}, Count{nullptr, B}, B,
+                          CompactApplied{aflag, sk, sv, n, op, ts, b->a_src, b->a_dst, b->a_op, b->a_ts},
+                          b->n_applied, w, s));
+  w.off = mark;
+  // 6. in-key order
+  k_in_keys<<<grid, kBlk, 0, s>>>(b->a_src, b->a_dst, b->n_applied, n, keys, vals);
+  RTEC_TRY(sort_pairs(keys, vals, sk, sv, Count{b->n_applied, B}, B, bits, w, s));
+  w.off = mark;
+  k_in_gather<<<grid, kBlk, 0, s>>>(sv, b->n_applied, b->a_src, b->a_dst, b->a_op, b->i_src, b->i_dst, b->i_op);
+  // 7. plan both merges (no mutation; all-or-nothing arena reservation)
+  MergeIn mo{b->a_src, b->a_dst, b->a_op, b->a_ts, b->n_applied, B};
+  MergeIn mi{b->i_dst, b->i_src, b->i_op, nullptr, b->n_applied, B};
+  RTEC_TRY(merge_plan(mo, po, g->out, g->slack, g->min_slack, b->err, w, s));
+  w.off = mark;
+  RTEC_TRY(merge_plan(mi, pi, g->in, g->slack, g->min_slack, b->err, w, s));
+  w.off = mark;
+  // 8. mutate: degrees, runs
+  k_apply_degrees<<<grid, kBlk, 0, s>>>(b->a_src, b->a_dst, b->a_op, b->n_applied, g->out_deg, g->in_deg,
+                                        g->num_edges, b->err);
+  int64_t work_bound = g->out.slots + B;  // grid-stride loops read the real totals on device
+  RTEC_TRY(merge_exec(mo, po, g->out, work_bound, b->err, s));
+  RTEC_TRY(merge_exec(mi, pi, g->in, work_bound, b->err, s));
+  // 9. DegreeDelta rows: unique endpoints of applied updates whose degrees changed
+  k_touched_keys<<<grid, kBlk, 0, s>>>(b->a_src, b->a_dst, b->n_applied, keys, vals, cnt2);
+  RTEC_TRY(sort_pairs(keys, vals, sk, sv, Count{cnt2, B2}, B2, bits_for(static_cast<uint64_t>(n)), w, s));
+  w.off = mark;
+  DeltaFlag df{sk, g->in_deg, g->out_deg, g->in_deg_prev, g->out_deg_prev};
+  RTEC_TRY(exclusive_scan(df, Count{cnt2, B2}, B2,
+                          DeltaOut{df, b->d_vertex, b->d_old_in, b->d_new_in, b->d_old_out, b->d_new_out},
+                          b->n_delta, w, s));
+  return RTEC_OK;
+}
+
+int rtec_batch_commit(rtec_graph_t* g, const rtec_batch_t* b, rtec_stream_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  k_commit_degrees<<<grid_for(b->cap * 2, kBlk), kBlk, 0, s>>>(b->d_vertex, b->n_delta, g->in_deg, g->out_deg,
+                                                               g->in_deg_prev, g->out_deg_prev);
+  RTEC_LAUNCH_CHECK("k_commit_degrees");
+  return RTEC_OK;
+}
+
+}  // extern "C"

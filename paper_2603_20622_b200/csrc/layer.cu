@@ -1,0 +1,699 @@
+// layer.cu -- per-layer incremental / full aggregation and the update
+// (SURVEY §2.1 K10-K15, K17, K18).
+//
+// State per layer (rtec_state_t): S = aggregate before ms_cbn (the stripped
+// form of Alg. 1 line 4, kept resident so strip/compose never round-trip),
+// ctx (GAT attention sums; count contexts are the in-degrees), H_out, and the
+// DeltaLog of pre-batch H_out rows of V_dst(l).
+//
+// Incremental (Alg. 1), v ∈ V_dst(l) \ R(l):
+//   ValueChange edge (u,v), u ∈ S(l), (u,v) ∉ I :  + δ_u,  δ_u = c_new(u) h_new(u) - c_old(u) h_old(u)
+//   StructInsert (u,v) ∈ I                      :  + c_new(u) h_new(u)
+//   StructDelete (u,v) ∈ D                      :  - c_old(u) h_old(u)
+//   S_v <- (indeg_new(v) == 0) ? 0 : S_v + Σ ;  a_v = ms_cbn(ctx_new, S_v);  h_v = update(h_v, a_v)
+// with c = 1/sqrt(d_out + off) for GCN (models.py:98-99), 1 otherwise.
+// GAT (Alg. 3) carries per-edge attention instead of c and
+// recomputes R(l) = V_dst(l) ∩ V_chg(l-1) over the full post-batch
+// neighbourhood (models.py:431-458).
+#include "prims.cuh"
+#include "rowops.cuh"
+
+namespace rtec {
+
+constexpr int kLBlk = 256;
+constexpr int kUnroll = 4;
+
+__device__ __forceinline__ float src_coeff(int model, int32_t deg, float off) {
+  return model == RTEC_MODEL_GCN ? 1.0f / sqrtf(static_cast<float>(deg) + off) : 1.0f;
+}
+
+__device__ __forceinline__ float leaky02(float x) { return x < 0.f ? 0.2f * x : x; }  // models.py:272-273
+__device__ __forceinline__ float elu1(float x) { return x >= 0.f ? x : expm1f(x); }   // linalg.py:41-43
+
+struct LayerArgs {
+  rtec_graph_t g;
+  rtec_batch_t b;
+  rtec_layer_t L;
+  rtec_state_t st;
+  rtec_frontier_t f;
+  const uint32_t* prev_bm_dst;  // V_chg(l-1) (null for l = 0)
+  const int32_t* prev_slot;     // vertex -> DeltaLog row of the previous layer
+  const float* delta;           // [n_src, d_agg] δ rows (non-GAT)
+  int d_agg;
+  int layer;
+  uint64_t* err;
+};
+
+// ------------------------------------------------------------------ δ rows (K10)
+template <int VEC, int K>
+__global__ void __launch_bounds__(kLBlk) k_src_delta(LayerArgs a, float* delta) {
+  using R = RowAcc<VEC, K>;
+  int64_t ns = *a.f.n_src;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int d = a.d_agg;
+  for (int64_t i = warp; i < ns; i += nw) {
+    int32_t u = a.f.src_list[i];
+    int32_t dn = a.g.out_deg[u], dp = a.g.out_deg_prev[u];
+    R acc;
+    acc.zero();
+    if (dn > 0 && dp > 0) {  // otherwise u has no ValueChange edges
+      float cn = src_coeff(a.L.model, dn, a.L.degree_offset);
+      float co = src_coeff(a.L.model, dp, a.L.degree_offset);
+      float hn[K][VEC], ho[K][VEC];
+      R::load(a.st.H_in + static_cast<int64_t>(u) * d, d, hn);
+      const float* orow = a.st.H_in + static_cast<int64_t>(u) * d;
+      if (a.prev_bm_dst && bm_test(a.prev_bm_dst, u)) orow = a.st.log_in + static_cast<int64_t>(a.prev_slot[u]) * d;
+      R::load(orow, d, ho);
+      acc.fma(hn, cn);
+      acc.fma(ho, -co);
+    }
+    acc.store(delta + i * d, d);
+  }
+}
+
+// is (u, v) an applied insert?  I/D entries of v are i_src[p, q) ascending
+__device__ __forceinline__ bool in_range_has(const int32_t* __restrict__ is, int64_t p, int64_t q, int32_t u) {
+  if (p >= q) return false;
+  int64_t k = lower_bound_dev(is, p, q, u);
+  return k < q && is[k] == u;
+}
+
+// ------------------------------------------------------------------ incremental aggregate (K11), non-GAT
+template <int VEC, int K>
+__global__ void __launch_bounds__(kLBlk) k_agg_inc(LayerArgs a) {
+  using R = RowAcc<VEC, K>;
+  if (err_set(a.err)) return;
+  const int64_t nd = *a.f.n_dst;
+  const int64_t ns = *a.f.n_src;
+  const int64_t na = *a.b.n_applied;
+  const int d = a.d_agg;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = lane_id();
+  for (int64_t i = warp; i < nd; i += nw) {
+    int32_t v = a.f.dst_list[i];
+    int64_t p = lower_bound_dev(a.b.i_dst, 0, na, v);
+    int64_t q = lower_bound_dev(a.b.i_dst, p, na, v + 1);
+    R acc;
+    acc.zero();
+    // ValueChange edges: scan v's post-batch in-run for sources in S(l)
+    if (ns > 0) {
+      int64_t beg = a.g.in.beg[v];
+      int32_t len = a.g.in.len[v];
+      for (int32_t c0 = 0; c0 < len; c0 += 32) {
+        int32_t j = c0 + lane;
+        int32_t u = 0;
+        bool hit = false;
+        if (j < len) {
+          u = a.g.in.nbr[beg + j];
+          hit = bm_test(a.f.bm_src, u) && !in_range_has(a.b.i_src, p, q, u);
+        }
+        unsigned m = __ballot_sync(0xffffffffu, hit);
+        int32_t slot = hit ? a.f.src_slot[u] : 0;
+        while (m) {
+          int32_t sl[kUnroll];
+          int cnt = 0;
+#pragma unroll
+          for (int t = 0; t < kUnroll; ++t) {
+            sl[t] = 0;
+            if (m) {
+              int src = __ffs(m) - 1;
+              m &= m - 1;
+              sl[t] = __shfl_sync(0xffffffffu, slot, src);
+              cnt = t + 1;
+            } else {
+              __shfl_sync(0xffffffffu, slot, 0);
+            }
+          }
+          float r[kUnroll][K][VEC];
+#pragma unroll
+          for (int t = 0; t < kUnroll; ++t)
+            if (t < cnt) R::load(a.delta + static_cast<int64_t>(sl[t]) * d, d, r[t]);
+#pragma unroll
+          for (int t = 0; t < kUnroll; ++t)
+            if (t < cnt) acc.add(r[t]);
+        }
+      }
+    }
+    // structural edges of v (graph.py:202-224 applied set)
+    for (int64_t k = p; k < q; ++k) {
+      int32_t u = a.b.i_src[k];
+      float r[K][VEC];
+      if (a.b.i_op[k] == RTEC_OP_INSERT) {
+        R::load(a.st.H_in + static_cast<int64_t>(u) * d, d, r);
+        acc.fma(r, src_coeff(a.L.model, a.g.out_deg[u], a.L.degree_offset));
+      } else {
+        const float* orow = a.st.H_in + static_cast<int64_t>(u) * d;
+        if (a.prev_bm_dst && bm_test(a.prev_bm_dst, u)) orow = a.st.log_in + static_cast<int64_t>(a.prev_slot[u]) * d;
+        R::load(orow, d, r);
+        acc.fma(r, -src_coeff(a.L.model, a.g.out_deg_prev[u], a.L.degree_offset));
+      }
+    }
+    // S_v update, compose, GEMM input row
+    int32_t indeg = a.g.in_deg[v];
+    float* srow = a.st.S + static_cast<int64_t>(v) * d;
+    float sv[K][VEC];
+    if (indeg == 0) {
+      acc.zero();  // empty neighbourhood -> zero aggregate
+    } else if (a.g.in_deg_prev[v] > 0) {
+      R::load_rw(srow, d, sv);
+      acc.add(sv);
+    }
+    acc.store(srow, d);
+    float scale = 1.f;
+    if (indeg > 0) {
+      if (a.L.model == RTEC_MODEL_GCN) scale = 1.0f / sqrtf(static_cast<float>(indeg) + a.L.degree_offset);
+      else if (a.L.model == RTEC_MODEL_SAGE) scale = 1.0f / static_cast<float>(indeg);
+    }
+    R out;
+    out.zero();
+    out.fma(acc.v, scale);
+    if (a.L.model == RTEC_MODEL_GIN) {  // update input h_v + a_v (models.py:187-189)
+      float h[K][VEC];
+      R::load(a.st.H_in + static_cast<int64_t>(v) * d, d, h);
+      out.add(h);
+    }
+    out.store(a.st.gemm_in + i * d, d);
+  }
+}
+
+// ------------------------------------------------------------------ full aggregate (K17), non-GAT
+// rows == null: all vertices, output row i = v.  Else rows[i].
+template <int VEC, int K>
+__global__ void __launch_bounds__(kLBlk) k_agg_full(LayerArgs a, const int32_t* rows, const int64_t* n_rows,
+                                                    int64_t n_all) {
+  using R = RowAcc<VEC, K>;
+  const int64_t nr = rows ? *n_rows : n_all;
+  const int d = a.d_agg;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = lane_id();
+  for (int64_t i = warp; i < nr; i += nw) {
+    int32_t v = rows ? rows[i] : static_cast<int32_t>(i);
+    int64_t beg = a.g.in.beg[v];
+    int32_t len = a.g.in.len[v];
+    R acc;
+    acc.zero();
+    for (int32_t c0 = 0; c0 < len; c0 += 32) {
+      int32_t j = c0 + lane;
+      int32_t u = 0;
+      float cu = 0.f;
+      if (j < len) {
+        u = a.g.in.nbr[beg + j];
+        cu = src_coeff(a.L.model, a.g.out_deg[u], a.L.degree_offset);
+      }
+      int cnt_all = min(32, len - c0);
+      for (int t0 = 0; t0 < cnt_all; t0 += kUnroll) {
+        float r[kUnroll][K][VEC];
+        float cs[kUnroll];
+#pragma unroll
+        for (int t = 0; t < kUnroll; ++t) {
+          int src = t0 + t;
+          int32_t uu = __shfl_sync(0xffffffffu, u, src & 31);
+          cs[t] = __shfl_sync(0xffffffffu, cu, src & 31);
+          if (src < cnt_all) R::load(a.st.H_in + static_cast<int64_t>(uu) * d, d, r[t]);
+        }
+#pragma unroll
+        for (int t = 0; t < kUnroll; ++t)
+          if (t0 + t < cnt_all) acc.fma(r[t], cs[t]);
+      }
+    }
+    acc.store(a.st.S + static_cast<int64_t>(v) * d, d);
+    float scale = 1.f;
+    if (len > 0) {
+      if (a.L.model == RTEC_MODEL_GCN) scale = 1.0f / sqrtf(static_cast<float>(len) + a.L.degree_offset);
+      else if (a.L.model == RTEC_MODEL_SAGE) scale = 1.0f / static_cast<float>(len);
+    }
+    R out;
+    out.zero();
+    out.fma(acc.v, scale);
+    if (a.L.model == RTEC_MODEL_GIN) {
+      float h[K][VEC];
+      R::load(a.st.H_in + static_cast<int64_t>(v) * d, d, h);
+      out.add(h);
+    }
+    out.store(a.st.gemm_in + i * d, d);
+  }
+}
+
+// ------------------------------------------------------------------ GAT (K13-K15)
+// attention of edge (u -> v) for the head of chunk k
+template <int VEC>
+__device__ __forceinline__ int chunk_head(int k, int dh) {
+  return ((lane_id() + 32 * k) * VEC) / dh;
+}
+
+template <int VEC, int K>
+__global__ void __launch_bounds__(kLBlk) k_gat_layer(LayerArgs a, int recompute_all) {
+  using R = RowAcc<VEC, K>;
+  if (err_set(a.err)) return;
+  const int d = a.L.d_out;
+  const int H = a.L.heads;
+  const int dh = d / H;
+  const int64_t nd = recompute_all ? a.g.n : *a.f.n_dst;
+  const int64_t ns = recompute_all ? 0 : *a.f.n_src;
+  const int64_t na = recompute_all ? 0 : *a.b.n_applied;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = lane_id();
+  for (int64_t i = warp; i < nd; i += nw) {
+    int32_t v = recompute_all ? static_cast<int32_t>(i) : a.f.dst_list[i];
+    bool recompute = recompute_all || (a.prev_bm_dst && bm_test(a.prev_bm_dst, v));
+    float elv[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) elv[k] = R::has(k, d) ? a.st.el[static_cast<int64_t>(v) * H + chunk_head<VEC>(k, dh)] : 0.f;
+    R acc;
+    acc.zero();
+    float cacc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) cacc[k] = 0.f;
+    int64_t beg = a.g.in.beg[v];
+    int32_t len = a.g.in.len[v];
+    if (recompute) {
+      // full edge softmax over the post-batch in-run (vertex_aggregate models.py:444-458)
+      for (int32_t c0 = 0; c0 < len; c0 += 32) {
+        int32_t j = c0 + lane;
+        int32_t u = j < len ? a.g.in.nbr[beg + j] : 0;
+        int cnt_all = min(32, len - c0);
+        for (int t = 0; t < cnt_all; ++t) {
+          int32_t uu = __shfl_sync(0xffffffffu, u, t);
+          float z[K][VEC];
+          R::load(a.st.Z + static_cast<int64_t>(uu) * d, d, z);
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            float at = 0.f;
+            if (R::has(k, d)) at = expf(leaky02(elv[k] + a.st.er[static_cast<int64_t>(uu) * H + chunk_head<VEC>(k, dh)]));
+            cacc[k] += at;
+#pragma unroll
+            for (int jj = 0; jj < VEC; ++jj) acc.v[k][jj] = fmaf(at, z[k][jj], acc.v[k][jj]);
+          }
+        }
+      }
+    } else {
+      int64_t p = lower_bound_dev(a.b.i_dst, 0, na, v);
+      int64_t q = lower_bound_dev(a.b.i_dst, p, na, v + 1);
+      if (ns > 0) {  // ValueChange edges: sources whose h^{l-1} changed
+        for (int32_t c0 = 0; c0 < len; c0 += 32) {
+          int32_t j = c0 + lane;
+          int32_t u = 0;
+          bool hit = false;
+          if (j < len) {
+            u = a.g.in.nbr[beg + j];
+            hit = bm_test(a.f.bm_src, u) && !in_range_has(a.b.i_src, p, q, u);
+          }
+          unsigned m = __ballot_sync(0xffffffffu, hit);
+          while (m) {
+            int src = __ffs(m) - 1;
+            m &= m - 1;
+            int32_t uu = __shfl_sync(0xffffffffu, u, src);
+            int32_t sl = a.prev_slot[uu];
+            float zn[K][VEC], zo[K][VEC];
+            R::load(a.st.Z + static_cast<int64_t>(uu) * d, d, zn);
+            R::load(a.st.Z_log + static_cast<int64_t>(sl) * d, d, zo);
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              float an = 0.f, ao = 0.f;
+              if (R::has(k, d)) {
+                int h = chunk_head<VEC>(k, dh);
+                an = expf(leaky02(elv[k] + a.st.er[static_cast<int64_t>(uu) * H + h]));
+                ao = expf(leaky02(elv[k] + a.st.er_log[static_cast<int64_t>(sl) * H + h]));
+              }
+              cacc[k] += an - ao;
+#pragma unroll
+              for (int jj = 0; jj < VEC; ++jj) acc.v[k][jj] += an * zn[k][jj] - ao * zo[k][jj];
+            }
+          }
+        }
+      }
+      for (int64_t kk = p; kk < q; ++kk) {
+        int32_t u = a.b.i_src[kk];
+        bool ins = a.b.i_op[kk] == RTEC_OP_INSERT;
+        const float* zrow = a.st.Z + static_cast<int64_t>(u) * d;
+        const float* errow = a.st.er + static_cast<int64_t>(u) * H;
+        if (!ins && a.prev_bm_dst && bm_test(a.prev_bm_dst, u)) {
+          int32_t sl = a.prev_slot[u];
+          zrow = a.st.Z_log + static_cast<int64_t>(sl) * d;
+          errow = a.st.er_log + static_cast<int64_t>(sl) * H;
+        }
+        float z[K][VEC];
+        R::load(zrow, d, z);
+        float sgn = ins ? 1.f : -1.f;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          float at = 0.f;
+          if (R::has(k, d)) at = expf(leaky02(elv[k] + errow[chunk_head<VEC>(k, dh)]));
+          cacc[k] += sgn * at;
+#pragma unroll
+          for (int jj = 0; jj < VEC; ++jj) acc.v[k][jj] = fmaf(sgn * at, z[k][jj], acc.v[k][jj]);
+        }
+      }
+      // add the cached state (Alg. 3 lines 5-7: strip with the old sum = keep S un-normalised)
+      if (a.g.in_deg_prev[v] > 0 && a.g.in_deg[v] > 0) {
+        float sv[K][VEC];
+        R::load_rw(a.st.S + static_cast<int64_t>(v) * d, d, sv);
+        acc.add(sv);
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+          if (R::has(k, d)) cacc[k] += a.st.ctx[static_cast<int64_t>(v) * H + chunk_head<VEC>(k, dh)];
+      }
+    }
+    int32_t indeg = recompute ? len : a.g.in_deg[v];
+    if (indeg == 0) {
+      acc.zero();
+#pragma unroll
+      for (int k = 0; k < K; ++k) cacc[k] = 0.f;
+    }
+    acc.store(a.st.S + static_cast<int64_t>(v) * d, d);
+    // ctx per head: written by the lane holding the head's first chunk
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      int c = lane + 32 * k;
+      if (c * VEC < d && (c * VEC) % dh == 0)
+        for (int hh = 0; hh < (VEC > dh ? VEC / dh : 1); ++hh) {
+          int h = (c * VEC) / dh + hh;
+          a.st.ctx[static_cast<int64_t>(v) * H + h] = cacc[k];
+        }
+    }
+    // a = S / ctx (models.py:280), h = elu(a) (models.py:282); DeltaLog capture
+    float* hrow = a.st.H_out + static_cast<int64_t>(v) * d;
+    if (!recompute_all && a.st.log_out) {
+      float old[K][VEC];
+      R::load_rw(hrow, d, old);
+      R o;
+      o.zero();
+      o.add(old);
+      o.store(a.st.log_out + i * d, d);
+    }
+    R o;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int jj = 0; jj < VEC; ++jj) o.v[k][jj] = indeg > 0 ? elu1(acc.v[k][jj] / cacc[k]) : 0.f;
+    o.store(hrow, d);
+  }
+}
+
+// el / er for projected rows: el = a[:dh]·z_h, er = a[dh:]·z_h per head
+__global__ void k_gat_logits(const float* __restrict__ Z, const int32_t* rows, const int64_t* n_rows, int64_t n_all,
+                             int d, int H, const float* __restrict__ att, float* el, float* er, float* er_log,
+                             const uint64_t* err) {
+  if (err && err_set(err)) return;
+  int dh = d / H;
+  int64_t nr = rows ? *n_rows : n_all;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int lane = lane_id();
+  for (int64_t i = warp; i < nr; i += nw) {
+    int32_t v = rows ? rows[i] : static_cast<int32_t>(i);
+    for (int h = 0; h < H; ++h) {
+      float sl = 0.f, sr = 0.f;
+      for (int j = lane; j < dh; j += 32) {
+        float z = Z[static_cast<int64_t>(v) * d + h * dh + j];
+        sl = fmaf(att[h * 2 * dh + j], z, sl);
+        sr = fmaf(att[h * 2 * dh + dh + j], z, sr);
+      }
+      sl = warp_sum(sl);
+      sr = warp_sum(sr);
+      if (lane == 0) {
+        if (er_log) er_log[i * H + h] = er[static_cast<int64_t>(v) * H + h];
+        el[static_cast<int64_t>(v) * H + h] = sl;
+        er[static_cast<int64_t>(v) * H + h] = sr;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ update GEMM (K12), SIMT fp32
+// Y[i] = act(X[i] · W^T); X rows optionally gathered, Y rows optionally
+// scattered with DeltaLog capture of the overwritten rows.
+struct GemmArgs {
+  const float* X; int64_t ldx; const int32_t* x_rows;
+  const float* W; int d_in; int d_out;
+  const int64_t* n_rows; int64_t max_rows;
+  int act;
+  float* Y; int64_t ldy; const int32_t* y_rows;
+  float* log;
+  const uint64_t* err;  // skip when the batch failed validation / reservation
+};
+
+constexpr int kGM = 64, kGN = 64, kGK = 16;
+
+__global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs g) {
+  __shared__ float As[kGK][kGM + 4];
+  __shared__ float Bs[kGK][kGN + 4];
+  if (g.err && err_set(g.err)) return;
+  const int64_t nr = g.n_rows ? *g.n_rows : g.max_rows;
+  const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kGM;
+  if (row0 >= nr) return;
+  const int col0 = blockIdx.y * kGN;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < g.d_in; k0 += kGK) {
+    // load A tile: 64 rows x 16 k -> 1024 values, 4 per thread
+    for (int e = threadIdx.x; e < kGM * kGK; e += 256) {
+      int r = e / kGK, kk = e % kGK;
+      int64_t gr = row0 + r;
+      float val = 0.f;
+      if (gr < nr && k0 + kk < g.d_in) {
+        int64_t src = g.x_rows ? g.x_rows[gr] : gr;
+        val = g.X[src * g.ldx + k0 + kk];
+      }
+      As[kk][r] = val;
+    }
+    for (int e = threadIdx.x; e < kGN * kGK; e += 256) {
+      int c = e / kGK, kk = e % kGK;
+      float val = 0.f;
+      if (col0 + c < g.d_out && k0 + kk < g.d_in) val = g.W[static_cast<int64_t>(col0 + c) * g.d_in + k0 + kk];
+      Bs[kk][c] = val;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kGK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) a[r] = As[kk][ty * 4 + r];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) b[c] = Bs[kk][tx * 4 + c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = fmaf(a[r], b[c], acc[r][c]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    int64_t gr = row0 + ty * 4 + r;
+    if (gr >= nr) continue;
+    int64_t dst = g.y_rows ? g.y_rows[gr] : gr;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      int col = col0 + tx * 4 + c;
+      if (col >= g.d_out) continue;
+      float y = acc[r][c];
+      if (g.act == 1) y = fmaxf(y, 0.f);
+      float* yp = g.Y + dst * g.ldy + col;
+      if (g.log) g.log[gr * g.d_out + col] = *yp;
+      *yp = y;
+    }
+  }
+}
+
+int gemm_launch(const GemmArgs& g, cudaStream_t s) {
+  if (g.max_rows <= 0) return RTEC_OK;
+  dim3 grid(static_cast<unsigned>((g.max_rows + kGM - 1) / kGM), static_cast<unsigned>((g.d_out + kGN - 1) / kGN));
+  k_gemm_simt<<<grid, 256, 0, s>>>(g);
+  RTEC_LAUNCH_CHECK("k_gemm_simt");
+  return RTEC_OK;
+}
+
+// ------------------------------------------------------------------ query (K18)
+__global__ void k_query(const float* __restrict__ H, int64_t d, const int32_t* __restrict__ ids, int64_t k, int32_t n,
+                        float* out, uint64_t* err) {
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < k; i += nw) {
+    int32_t v = ids[i];
+    if (v < 0 || v >= n) {
+      if (lane_id() == 0) report_error(err, RTEC_INVALID_VERTEX, i);
+      continue;
+    }
+    for (int64_t j = lane_id(); j < d; j += 32) out[i * d + j] = H[static_cast<int64_t>(v) * d + j];
+  }
+}
+
+}  // namespace rtec
+
+using namespace rtec;
+
+static int layer_dims_ok(const rtec_layer_t* L) {
+  if (L->model < 0 || L->model > 3) {
+    set_error("unsupported model id %d", L->model);
+    return RTEC_UNSUPPORTED_MODEL;
+  }
+  if (L->d_in <= 0 || L->d_out <= 0 || L->heads <= 0 || (L->d_out % L->heads) != 0) {
+    set_error("bad layer dims d_in=%d d_out=%d heads=%d", L->d_in, L->d_out, L->heads);
+    return RTEC_SHAPE_ERROR;
+  }
+  return RTEC_OK;
+}
+
+extern "C" {
+
+int rtec_update_gemm(const float* X, int64_t ldx, const float* W, int32_t d_in, int32_t d_out, const int64_t* n_rows,
+                     int64_t max_rows, int32_t act, float* Y, int64_t ldy, const int32_t* scatter_rows,
+                     float* scatter_dst, float* log_dst, rtec_stream_t stream) {
+  GemmArgs g{X, ldx, nullptr, W, d_in, d_out, n_rows, max_rows, act,
+             scatter_rows ? scatter_dst : Y, ldy, scatter_rows, log_dst, nullptr};
+  return gemm_launch(g, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rtec_layer_incremental(const rtec_graph_t* g, const rtec_batch_t* b, const rtec_layer_t* L, rtec_state_t* st,
+                           const rtec_frontier_t* prev, const rtec_frontier_t* f, uint64_t* err, void* ws,
+                           size_t ws_bytes, rtec_stream_t stream) {
+  RTEC_TRY(layer_dims_ok(L));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int64_t n = g->n;
+  Ws w(ws, ws_bytes);
+  LayerArgs a{};
+  a.g = *g;
+  a.b = *b;
+  a.L = *L;
+  a.st = *st;
+  a.f = *f;
+  a.prev_bm_dst = prev ? prev->bm_dst : nullptr;
+  a.prev_slot = prev ? prev->dst_slot : nullptr;
+  a.err = err;
+  const int grid = kSMs * 8;
+  if (L->model == RTEC_MODEL_GAT) {
+    a.d_agg = L->d_out;
+    int dh = L->d_out / L->heads;
+    bool ok;
+    if (L->d_out % 4 == 0 && dh % 4 == 0) {
+      ok = RTEC_ROW_DISPATCH(L->d_out, (k_gat_layer<VEC, K><<<grid, kLBlk, 0, s>>>(a, 0)));
+    } else {
+      int kk = (L->d_out + 31) / 32;
+      ok = true;
+      if (kk <= 1) k_gat_layer<1, 1><<<grid, kLBlk, 0, s>>>(a, 0);
+      else if (kk <= 4) k_gat_layer<1, 4><<<grid, kLBlk, 0, s>>>(a, 0);
+      else if (kk <= 8) k_gat_layer<1, 8><<<grid, kLBlk, 0, s>>>(a, 0);
+      else ok = false;
+    }
+    if (!ok) {
+      set_error("row width %d unsupported", L->d_out);
+      return RTEC_SHAPE_ERROR;
+    }
+    RTEC_LAUNCH_CHECK("k_gat_layer");
+    return RTEC_OK;
+  }
+  a.d_agg = L->d_in;
+  float* delta = w.alloc<float>(n * static_cast<int64_t>(L->d_in));
+  RTEC_WS_CHECK(w);
+  a.delta = delta;
+  bool ok = RTEC_ROW_DISPATCH(L->d_in, (k_src_delta<VEC, K><<<grid, kLBlk, 0, s>>>(a, delta),
+                                        k_agg_inc<VEC, K><<<grid, kLBlk, 0, s>>>(a)));
+  if (!ok) {
+    set_error("row width %d unsupported", L->d_in);
+    return RTEC_SHAPE_ERROR;
+  }
+  RTEC_LAUNCH_CHECK("k_agg_inc");
+  // update on V_dst(l) rows with DeltaLog capture (operators.py:180)
+  if (L->model == RTEC_MODEL_GIN) {
+    GemmArgs g1{st->gemm_in, L->d_in, nullptr, L->W, L->d_in, L->d_out, f->n_dst, n, 1,
+                st->gemm_mid, L->d_out, nullptr, nullptr, err};
+    RTEC_TRY(gemm_launch(g1, s));
+    GemmArgs g2{st->gemm_mid, L->d_out, nullptr, L->W2, L->d_out, L->d_out, f->n_dst, n, 0,
+                st->H_out, L->d_out, f->dst_list, st->log_out, err};
+    return gemm_launch(g2, s);
+  }
+  GemmArgs g1{st->gemm_in, L->d_in, nullptr, L->W, L->d_in, L->d_out, f->n_dst, n, 1,
+              st->H_out, L->d_out, f->dst_list, st->log_out, err};
+  return gemm_launch(g1, s);
+}
+
+int rtec_layer_full(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* st, const int32_t* rows,
+                    const int64_t* n_rows, int64_t max_rows, uint64_t* err, void* ws, size_t ws_bytes,
+                    rtec_stream_t stream) {
+  RTEC_TRY(layer_dims_ok(L));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int64_t n = g->n;
+  LayerArgs a{};
+  a.g = *g;
+  a.L = *L;
+  a.st = *st;
+  a.err = err;
+  const int grid = kSMs * 8;
+  if (L->model == RTEC_MODEL_GAT) {
+    if (rows) {
+      set_error("GAT full layer supports all rows only");
+      return RTEC_CONFIG_ERROR;
+    }
+    // Z = W H (all rows), logits, then the full softmax aggregation
+    GemmArgs gz{st->H_in, L->d_in, nullptr, L->W, L->d_in, L->d_out, nullptr, n, 0, st->Z, L->d_out, nullptr, nullptr, nullptr};
+    RTEC_TRY(gemm_launch(gz, s));
+    k_gat_logits<<<grid, kLBlk, 0, s>>>(st->Z, nullptr, nullptr, n, L->d_out, L->heads, L->att, st->el, st->er,
+                                        nullptr, nullptr);
+    a.d_agg = L->d_out;
+    int dh = L->d_out / L->heads;
+    bool ok;
+    if (L->d_out % 4 == 0 && dh % 4 == 0) {
+      ok = RTEC_ROW_DISPATCH(L->d_out, (k_gat_layer<VEC, K><<<grid, kLBlk, 0, s>>>(a, 1)));
+    } else {
+      int kk = (L->d_out + 31) / 32;
+      ok = true;
+      if (kk <= 1) k_gat_layer<1, 1><<<grid, kLBlk, 0, s>>>(a, 1);
+      else if (kk <= 4) k_gat_layer<1, 4><<<grid, kLBlk, 0, s>>>(a, 1);
+      else if (kk <= 8) k_gat_layer<1, 8><<<grid, kLBlk, 0, s>>>(a, 1);
+      else ok = false;
+    }
+    if (!ok) {
+      set_error("row width %d unsupported", L->d_out);
+      return RTEC_SHAPE_ERROR;
+    }
+    RTEC_LAUNCH_CHECK("k_gat_layer(full)");
+    return RTEC_OK;
+  }
+  a.d_agg = L->d_in;
+  int64_t mr = rows ? max_rows : n;
+  bool ok = RTEC_ROW_DISPATCH(L->d_in, (k_agg_full<VEC, K><<<grid, kLBlk, 0, s>>>(a, rows, n_rows, n)));
+  if (!ok) {
+    set_error("row width %d unsupported", L->d_in);
+    return RTEC_SHAPE_ERROR;
+  }
+  RTEC_LAUNCH_CHECK("k_agg_full");
+  const int64_t* nr = rows ? n_rows : nullptr;
+  if (L->model == RTEC_MODEL_GIN) {
+    GemmArgs g1{st->gemm_in, L->d_in, nullptr, L->W, L->d_in, L->d_out, nr, mr, 1, st->gemm_mid, L->d_out, nullptr, nullptr, nullptr};
+    RTEC_TRY(gemm_launch(g1, s));
+    GemmArgs g2{st->gemm_mid, L->d_out, nullptr, L->W2, L->d_out, L->d_out, nr, mr, 0, st->H_out, L->d_out, rows, nullptr, nullptr};
+    return gemm_launch(g2, s);
+  }
+  GemmArgs g1{st->gemm_in, L->d_in, nullptr, L->W, L->d_in, L->d_out, nr, mr, 1, st->H_out, L->d_out, rows, nullptr, nullptr};
+  return gemm_launch(g1, s);
+}
+
+int rtec_gat_project(const rtec_layer_t* L, const float* H, const int32_t* rows, const int64_t* n_rows,
+                     int64_t n_or_max_rows, float* Z, float* el, float* er, float* Z_log, float* er_log,
+                     const uint64_t* err, rtec_stream_t stream) {
+  RTEC_TRY(layer_dims_ok(L));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  GemmArgs gz{H, L->d_in, rows, L->W, L->d_in, L->d_out, rows ? n_rows : nullptr, n_or_max_rows, 0,
+              Z, L->d_out, rows, Z_log, err};
+  RTEC_TRY(gemm_launch(gz, s));
+  k_gat_logits<<<kSMs * 8, kLBlk, 0, s>>>(Z, rows, n_rows, n_or_max_rows, L->d_out, L->heads, L->att, el, er, er_log,
+                                          err);
+  RTEC_LAUNCH_CHECK("k_gat_logits");
+  return RTEC_OK;
+}
+
+int rtec_query(const float* H, int64_t d, const int32_t* ids, int64_t k, float* out, int32_t n, uint64_t* err,
+               rtec_stream_t stream) {
+  if (k <= 0) return RTEC_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  k_query<<<grid_for(k * 32, 256), 256, 0, s>>>(H, d, ids, k, n, out, err);
+  RTEC_LAUNCH_CHECK("k_query");
+  return RTEC_OK;
+}
+
+}  // extern "C"

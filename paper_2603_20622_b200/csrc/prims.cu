@@ -1,0 +1,222 @@
+// prims.cu -- scan-of-block-sums and the (u64 key, u32 value) sort.
+#include <stdarg.h>
+
+#include "prims.cuh"
+
+namespace rtec {
+
+// ---------------------------------------------------------------- errors
+static thread_local std::string g_last_error;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+  set_error("CUDA error %s (%s) at %s", cudaGetErrorName(e), cudaGetErrorString(e), where);
+  return RTEC_CUDA_ERROR;
+}
+
+const char* last_error_cstr() { return g_last_error.c_str(); }
+
+// ---------------------------------------------------------------- scan
+__global__ void __launch_bounds__(kScanBlock) k_scan_blocks(int64_t* bs, int64_t nb, int64_t* total) {
+  __shared__ int64_t sw[kScanBlock / 32];
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < nb; base += kScanBlock) {
+    int64_t i = base + threadIdx.x;
+    int64_t v = i < nb ? bs[i] : 0;
+    int64_t tot;
+    int64_t ex = block_exclusive_scan<int64_t>(v, sw, &tot);
+    if (i < nb) bs[i] = ex + carry;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    bs[nb] = carry;
+    if (total) *total = carry;
+  }
+}
+
+// ---------------------------------------------------------------- small sort
+// One CTA of 1024 threads, bitonic over (key, val) lexicographic; N <= 2048.
+constexpr int kSmallSort = 2048;
+
+__global__ void __launch_bounds__(1024) k_sort_small(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                     uint64_t* kout, uint32_t* vout, Count cnt) {
+  __shared__ uint64_t sk[kSmallSort];
+  __shared__ uint32_t sv[kSmallSort];
+  int64_t n = cnt.get();
+  int N = 2;
+  while (N < n) N <<= 1;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    if (i < n) {
+      sk[i] = kin[i];
+      sv[i] = vin[i];
+    } else {
+      sk[i] = ~0ull;
+      sv[i] = 0xffffffffu;
+    }
+  }
+  __syncthreads();
+  for (int size = 2; size <= N; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < N / 2; t += blockDim.x) {
+        int lo = 2 * t - (t & (stride - 1));
+        int hi = lo + stride;
+        bool up = ((lo & size) == 0);
+        uint64_t ka = sk[lo], kb = sk[hi];
+        uint32_t va = sv[lo], vb = sv[hi];
+        bool gt = (ka > kb) || (ka == kb && va > vb);
+        if (gt == up) {
+          sk[lo] = kb;
+          sk[hi] = ka;
+          sv[lo] = vb;
+          sv[hi] = va;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    kout[i] = sk[i];
+    vout[i] = sv[i];
+  }
+}
+
+// ---------------------------------------------------------------- radix sort
+constexpr int kRxBlock = 256;
+constexpr int kRxItems = 8;
+constexpr int kRxTile = kRxBlock * kRxItems;
+constexpr int kRxBins = 256;
+
+__global__ void __launch_bounds__(kRxBlock) k_rx_hist(const uint64_t* __restrict__ keys, Count cnt, int shift,
+                                                      int64_t ntiles, uint32_t* __restrict__ counts) {
+  __shared__ uint32_t hist[kRxBins];
+  hist[threadIdx.x] = 0;
+  __syncthreads();
+  int64_t n = cnt.get();
+  int64_t base = static_cast<int64_t>(blockIdx.x) * kRxTile;
+#pragma unroll
+  for (int k = 0; k < kRxItems; ++k) {
+    int64_t i = base + k * kRxBlock + threadIdx.x;
+    if (i < n) atomicAdd(&hist[(keys[i] >> shift) & 0xff], 1u);
+  }
+  __syncthreads();
+  counts[static_cast<int64_t>(threadIdx.x) * ntiles + blockIdx.x] = hist[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(kRxBlock) k_rx_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                         uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                         Count cnt, int shift, int64_t ntiles,
+                                                         const int64_t* __restrict__ offsets) {
+  constexpr int kWarps = kRxBlock / 32;
+  __shared__ uint32_t run[kRxBins];
+  __shared__ uint32_t whist[kWarps][kRxBins];
+  __shared__ int64_t goff[kRxBins];
+  int t = threadIdx.x, lane = lane_id(), wid = warp_id();
+  run[t] = 0;
+  for (int w = 0; w < kWarps; ++w) whist[w][t] = 0;
+  goff[t] = offsets[static_cast<int64_t>(t) * ntiles + blockIdx.x];
+  __syncthreads();
+  int64_t n = cnt.get();
+  int64_t base = static_cast<int64_t>(blockIdx.x) * kRxTile;
+  unsigned lt_mask = (1u << lane) - 1u;
+  for (int k = 0; k < kRxItems; ++k) {
+    int64_t i = base + k * kRxBlock + t;
+    bool valid = i < n;
+    uint64_t key = valid ? kin[i] : 0;
+    uint32_t val = valid ? vin[i] : 0;
+    int d = valid ? static_cast<int>((key >> shift) & 0xff) : -1;
+    unsigned peers = __match_any_sync(0xffffffffu, d);
+    int rank_w = __popc(peers & lt_mask);
+    if (valid && (__ffs(peers) - 1) == lane) whist[wid][d] = __popc(peers);
+    __syncthreads();
+    uint32_t pos = 0;
+    if (valid) {
+      pos = run[d] + rank_w;
+      for (int w = 0; w < wid; ++w) pos += whist[w][d];
+    }
+    __syncthreads();
+    {
+      uint32_t add = 0;
+      for (int w = 0; w < kWarps; ++w) {
+        add += whist[w][t];
+        whist[w][t] = 0;
+      }
+      run[t] += add;
+    }
+    if (valid) {
+      int64_t o = goff[d] + pos;
+      kout[o] = key;
+      vout[o] = val;
+    }
+    __syncthreads();
+  }
+}
+
+size_t sort_ws_bytes(int64_t max_n) {
+  int64_t ntiles = (max_n + kRxTile - 1) / kRxTile;
+  if (ntiles < 1) ntiles = 1;
+  size_t b = 0;
+  auto add = [&](size_t x) { b += (x + 255) & ~size_t(255); };
+  add(sizeof(uint64_t) * max_n);
+  add(sizeof(uint32_t) * max_n);
+  add(sizeof(uint64_t) * max_n);
+  add(sizeof(uint32_t) * max_n);
+  add(sizeof(uint32_t) * kRxBins * ntiles);
+  add(sizeof(int64_t) * kRxBins * ntiles);
+  add(sizeof(int64_t) * (scan_blocks_for(kRxBins * ntiles) + 2));
+  return b + 4096;
+}
+
+struct U32At {
+  const uint32_t* p;
+  __device__ __forceinline__ int64_t operator()(int64_t i) const { return p[i]; }
+};
+
+int sort_pairs(const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* keys_out, uint32_t* vals_out,
+               Count cnt, int64_t max_n, int bits, Ws& ws, cudaStream_t s) {
+  if (max_n <= 0) return RTEC_OK;
+  if (max_n <= kSmallSort) {
+    k_sort_small<<<1, 1024, 0, s>>>(keys_in, vals_in, keys_out, vals_out, cnt);
+    RTEC_LAUNCH_CHECK("k_sort_small");
+    return RTEC_OK;
+  }
+  int64_t ntiles = (max_n + kRxTile - 1) / kRxTile;
+  uint64_t* ka = ws.alloc<uint64_t>(max_n);
+  uint32_t* va = ws.alloc<uint32_t>(max_n);
+  uint64_t* kb = ws.alloc<uint64_t>(max_n);
+  uint32_t* vb = ws.alloc<uint32_t>(max_n);
+  uint32_t* counts = ws.alloc<uint32_t>(kRxBins * ntiles);
+  int64_t* offs = ws.alloc<int64_t>(kRxBins * ntiles);
+  int64_t* bs = ws.alloc<int64_t>(scan_blocks_for(kRxBins * ntiles) + 2);
+  RTEC_WS_CHECK(ws);
+  int passes = (bits + 7) / 8;
+  const uint64_t* ki = keys_in;
+  const uint32_t* vi = vals_in;
+  for (int p = 0; p < passes; ++p) {
+    bool last = (p == passes - 1);
+    uint64_t* ko = last ? keys_out : ((p & 1) ? kb : ka);
+    uint32_t* vo = last ? vals_out : ((p & 1) ? vb : va);
+    int shift = 8 * p;
+    k_rx_hist<<<static_cast<unsigned>(ntiles), kRxBlock, 0, s>>>(ki, cnt, shift, ntiles, counts);
+    RTEC_TRY(exclusive_scan_bs(U32At{counts}, Count{nullptr, kRxBins * ntiles}, kRxBins * ntiles,
+                               StorePrefix{offs}, nullptr, bs, s));
+    k_rx_scatter<<<static_cast<unsigned>(ntiles), kRxBlock, 0, s>>>(ki, vi, ko, vo, cnt, shift, ntiles, offs);
+    RTEC_LAUNCH_CHECK("k_rx_scatter");
+    ki = ko;
+    vi = vo;
+  }
+  return RTEC_OK;
+}
+
+}  // namespace rtec

@@ -1,0 +1,137 @@
+// prims.cuh -- device-wide primitives used by the batch / frontier kernels:
+// exclusive scans over functor-generated values and a (key u64, value u32)
+// sort (single-CTA bitonic for small batches, LSD radix with 8-bit digits and
+// stable warp-match ranking otherwise).  Counts may live on the device: the
+// host passes an upper bound for the launch shape, kernels read the real count.
+#pragma once
+#include "common.cuh"
+
+namespace rtec {
+
+// ---------------------------------------------------------------- count helpers
+struct Count {
+  const int64_t* dev;  // device count or nullptr
+  int64_t host;        // host count (upper bound when dev != nullptr)
+  __device__ __forceinline__ int64_t get() const { return dev ? *dev : host; }
+};
+
+// ---------------------------------------------------------------- scan
+constexpr int kScanBlock = 512;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanBlock * kScanItems;
+
+template <typename T>
+__device__ __forceinline__ T block_exclusive_scan(T v, T* smem_warp, T* total) {
+  // 512 threads = 16 warps
+  int lane = lane_id(), wid = warp_id();
+  T x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) smem_warp[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    T w = lane < (kScanBlock / 32) ? smem_warp[lane] : T(0);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      T y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < (kScanBlock / 32)) smem_warp[lane] = w;  // inclusive warp totals
+  }
+  __syncthreads();
+  T warp_off = wid > 0 ? smem_warp[wid - 1] : T(0);
+  if (total) *total = smem_warp[kScanBlock / 32 - 1];
+  T r = warp_off + x - v;
+  __syncthreads();
+  return r;
+}
+
+template <typename F>
+__global__ void __launch_bounds__(kScanBlock) k_scan_reduce(F f, Count cnt, int64_t* block_sums) {
+  __shared__ int64_t sw[kScanBlock / 32];
+  int64_t n = cnt.get();
+  int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile;
+  int64_t s = 0;
+  if (base < n) {
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      int64_t i = base + static_cast<int64_t>(threadIdx.x) * kScanItems + k;
+      if (i < n) s += f(i);
+    }
+  }
+  int64_t tot;
+  block_exclusive_scan<int64_t>(s, sw, &tot);
+  if (threadIdx.x == 0) block_sums[blockIdx.x] = tot;
+}
+
+// single CTA: exclusive scan of block_sums in place; total -> *total
+__global__ void __launch_bounds__(kScanBlock) k_scan_blocks(int64_t* block_sums, int64_t nb, int64_t* total);
+
+template <typename F, typename O>
+__global__ void __launch_bounds__(kScanBlock) k_scan_down(F f, Count cnt, const int64_t* block_sums, O out) {
+  __shared__ int64_t sw[kScanBlock / 32];
+  int64_t n = cnt.get();
+  int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile;
+  if (base >= n) return;
+  int64_t vals[kScanItems];
+  int64_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    int64_t i = base + static_cast<int64_t>(threadIdx.x) * kScanItems + k;
+    vals[k] = (i < n) ? f(i) : 0;
+    s += vals[k];
+  }
+  int64_t off = block_exclusive_scan<int64_t>(s, sw, nullptr) + block_sums[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    int64_t i = base + static_cast<int64_t>(threadIdx.x) * kScanItems + k;
+    if (i < n) out(i, off, vals[k]);
+    off += vals[k];
+  }
+}
+
+inline int64_t scan_blocks_for(int64_t max_n) { return (max_n + kScanTile - 1) / kScanTile; }
+
+// Exclusive scan: out(i, prefix, value) is called for every i < count; *total
+// (device, may be null) receives the sum.  ws needs scan_blocks_for(max)+1 int64.
+template <typename F, typename O>
+int exclusive_scan_bs(F f, Count cnt, int64_t max_n, O out, int64_t* total, int64_t* bs, cudaStream_t s) {
+  int64_t nb = scan_blocks_for(max_n);
+  if (nb < 1) nb = 1;
+  k_scan_reduce<F><<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(f, cnt, bs);
+  k_scan_blocks<<<1, kScanBlock, 0, s>>>(bs, nb, total);
+  k_scan_down<F, O><<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(f, cnt, bs, out);
+  RTEC_LAUNCH_CHECK("exclusive_scan");
+  return RTEC_OK;
+}
+
+template <typename F, typename O>
+int exclusive_scan(F f, Count cnt, int64_t max_n, O out, int64_t* total, Ws& ws, cudaStream_t s) {
+  int64_t* bs = ws.alloc<int64_t>(scan_blocks_for(max_n) + 2);
+  RTEC_WS_CHECK(ws);
+  return exclusive_scan_bs(f, cnt, max_n, out, total, bs, s);
+}
+
+// common out-functors
+struct StorePrefix {
+  int64_t* dst;
+  __device__ __forceinline__ void operator()(int64_t i, int64_t off, int64_t) const { dst[i] = off; }
+};
+
+// ---------------------------------------------------------------- sort
+// Sorts (key, val) pairs ascending by key (stable w.r.t. input order) over
+// bits [0, bits).  Result lands in keys_out/vals_out.  Needs sort_ws_bytes.
+size_t sort_ws_bytes(int64_t max_n);
+int sort_pairs(const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* keys_out, uint32_t* vals_out,
+               Count cnt, int64_t max_n, int bits, Ws& ws, cudaStream_t s);
+
+inline int bits_for(uint64_t max_key) {
+  int b = 0;
+  while (b < 64 && (max_key >> b) != 0) ++b;
+  return b < 1 ? 1 : b;
+}
+
+}  // namespace rtec

@@ -1,0 +1,111 @@
+// rowops.cuh -- warp-cooperative feature-row accumulators.
+// A warp owns one destination row; lane l holds chunks c = l + 32*k (k < K)
+// of VEC consecutive floats (VEC = 4 -> 128-bit loads when d % 4 == 0).
+#pragma once
+#include "common.cuh"
+
+namespace rtec {
+
+template <int VEC>
+struct VecT;
+template <>
+struct VecT<4> {
+  using T = float4;
+};
+template <>
+struct VecT<1> {
+  using T = float;
+};
+
+template <int VEC, int K>
+struct RowAcc {
+  float v[K][VEC];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) v[k][j] = 0.f;
+  }
+  __device__ __forceinline__ static bool has(int k, int d) { return ((lane_id() + 32 * k) * VEC) < d; }
+  __device__ __forceinline__ static void load(const float* __restrict__ row, int d, float (&r)[K][VEC]) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      int c = lane_id() + 32 * k;
+      if (c * VEC < d) {
+        if constexpr (VEC == 4) {
+          float4 x = __ldg(reinterpret_cast<const float4*>(row) + c);
+          r[k][0] = x.x; r[k][1] = x.y; r[k][2] = x.z; r[k][3] = x.w;
+        } else {
+          r[k][0] = __ldg(row + c);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) r[k][j] = 0.f;
+      }
+    }
+  }
+  // plain (non-__ldg) load for rows written earlier in the same kernel
+  __device__ __forceinline__ static void load_rw(const float* row, int d, float (&r)[K][VEC]) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      int c = lane_id() + 32 * k;
+      if (c * VEC < d) {
+        if constexpr (VEC == 4) {
+          float4 x = reinterpret_cast<const float4*>(row)[c];
+          r[k][0] = x.x; r[k][1] = x.y; r[k][2] = x.z; r[k][3] = x.w;
+        } else {
+          r[k][0] = row[c];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) r[k][j] = 0.f;
+      }
+    }
+  }
+  __device__ __forceinline__ void fma(const float (&r)[K][VEC], float s) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) v[k][j] = fmaf(s, r[k][j], v[k][j]);
+  }
+  __device__ __forceinline__ void add(const float (&r)[K][VEC]) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) v[k][j] += r[k][j];
+  }
+  __device__ __forceinline__ void store(float* row, int d) const {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      int c = lane_id() + 32 * k;
+      if (c * VEC < d) {
+        if constexpr (VEC == 4) {
+          reinterpret_cast<float4*>(row)[c] = make_float4(v[k][0], v[k][1], v[k][2], v[k][3]);
+        } else {
+          row[c] = v[k][0];
+        }
+      }
+    }
+  }
+};
+
+// dispatch (VEC, K) from the row width; returns false if unsupported
+#define RTEC_ROW_DISPATCH(d, ...)                                         \
+  [&]() -> bool {                                                         \
+    if ((d) % 4 == 0) {                                                   \
+      int _k = ((d) / 4 + 31) / 32;                                       \
+      if (_k <= 1) { constexpr int VEC = 4, K = 1; __VA_ARGS__; return true; } \
+      if (_k <= 2) { constexpr int VEC = 4, K = 2; __VA_ARGS__; return true; } \
+      if (_k <= 4) { constexpr int VEC = 4, K = 4; __VA_ARGS__; return true; } \
+      if (_k <= 5) { constexpr int VEC = 4, K = 5; __VA_ARGS__; return true; } \
+      return false;                                                       \
+    }                                                                     \
+    int _k = ((d) + 31) / 32;                                             \
+    if (_k <= 1) { constexpr int VEC = 1, K = 1; __VA_ARGS__; return true; }   \
+    if (_k <= 4) { constexpr int VEC = 1, K = 4; __VA_ARGS__; return true; }   \
+    if (_k <= 8) { constexpr int VEC = 1, K = 8; __VA_ARGS__; return true; }   \
+    if (_k <= 20) { constexpr int VEC = 1, K = 20; __VA_ARGS__; return true; } \
+    return false;                                                         \
+  }()
+
+}  // namespace rtec

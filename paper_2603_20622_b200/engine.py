@@ -1,0 +1,266 @@
+"""Incremental RTEC engine on B200 (the SPEC engines/state_cache/frontier layer).
+
+The reference ships no engine; this implements its
+contract: `bootstrap` (== layer_embeddings per layer,
+models.py:461-477), `run_incremental` (Alg. 1 / Alg. 3 on
+the F1 frontier), `run_full`, `query` / `materialize_h`
+(SPEC.md:379), with device-side access counters (SPEC.md:430-433 Metrics).
+
+Per batch the host only enqueues C-ABI calls on one stream:
+
+    rtec_batch_apply            graph.py:184 apply_batch (validate, probe, merge, deltas)
+    for l in 0..L-1:
+      rtec_frontier_layer       Alg. 4 layer l (F1 rule)
+      rtec_gat_project          GAT only, l >= 1: Z/el/er of V_chg(l-1) rows (+ DeltaLog)
+      rtec_layer_incremental    Alg. 1 / Alg. 3 + recompute R(l) + update GEMM (+ DeltaLog)
+    rtec_batch_commit           degree snapshots catch up
+
+No host synchronisation happens inside a batch (all sizes stay on the
+device), so the whole step can be captured in a CUDA graph (`capture()`).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import errors as E
+from .graph import DynamicGraph, EdgeUpdate, updates_to_arrays
+from .models import GAT, GIN, Bundle, MODELS
+
+_MODEL_ID = _lib.MODEL_IDS
+
+
+@dataclass
+class Metrics:
+    """Per-layer device counters."""
+
+    e_curr: list = field(default_factory=list)   # |E_curr(l)|
+    v_dst: list = field(default_factory=list)    # |V_dst(l)|
+    n_src: list = field(default_factory=list)    # |S(l)|
+    in_edges_vdst: list = field(default_factory=list)  # Σ indeg(V_dst(l)) (scanned in-runs)
+
+
+@dataclass
+class RunResult:
+    status: np.ndarray
+    deltas: np.ndarray
+    changed_final: np.ndarray | None
+    metrics: Metrics
+
+
+class _Frontier:
+    def __init__(self, n, dev):
+        words = (n + 31) // 32
+        z = lambda k, dt: torch.zeros(max(k, 1), dtype=dt, device=dev)  # noqa: E731
+        self.bm_src, self.bm_dst = z(words, torch.int32), z(words, torch.int32)
+        self.src_list, self.dst_list = z(n, torch.int32), z(n, torch.int32)
+        self.n_src, self.n_dst = z(1, torch.int64), z(1, torch.int64)
+        self.src_slot, self.dst_slot = z(n, torch.int32), z(n, torch.int32)
+        self.counters = z(8, torch.int64)
+
+    def c(self):
+        p = _lib.ptr
+        return _lib.Frontier(p(self.bm_src), p(self.bm_dst), p(self.src_list), p(self.n_src), p(self.dst_list),
+                             p(self.n_dst), p(self.src_slot), p(self.dst_slot), p(self.counters))
+
+
+class RTECEngine:
+    """B200 incremental engine over a DynamicGraph and an operator Bundle."""
+
+    def __init__(self, bundle: Bundle, graph: DynamicGraph, features, *, max_batch: int | None = None):
+        if not isinstance(bundle, Bundle) or bundle.model not in MODELS:
+            raise E.UnsupportedModel("engine needs a bundle from paper_2603_20622_b200.models")
+        self.b = bundle
+        self.g = graph
+        self.lib = graph.lib
+        self.dev = graph.dev
+        n = graph.n
+        self.n = n
+        dims = bundle.dims
+        X = torch.as_tensor(np.asarray(features), device=self.dev) if not isinstance(features, torch.Tensor) else features
+        if tuple(X.shape) != (n, dims[0]):
+            raise E.ShapeError(f"features shape {tuple(X.shape)} != ({n}, {dims[0]})")
+        self.H = [X.to(self.dev, torch.float32).contiguous()]
+        self.L = bundle.num_layers
+        z = lambda *s: torch.zeros(*s, dtype=torch.float32, device=self.dev)  # noqa: E731
+        self.layers, self.wt = [], []
+        self.S, self.ctx, self.log = [], [], []
+        self.Z, self.el, self.er, self.Zlog, self.erlog = [], [], [], [], []
+        heads = bundle.heads
+        for l, w in enumerate(bundle.layers):
+            d_in, d_out = w.in_dim, w.out_dim
+            W = torch.as_tensor(np.asarray(w.tensors["W"], np.float32), device=self.dev).contiguous()
+            W2 = torch.as_tensor(np.asarray(w.tensors["W2"], np.float32), device=self.dev).contiguous() if bundle.model == GIN else None
+            att = torch.as_tensor(np.asarray(w.tensors["a"], np.float32).reshape(heads, -1), device=self.dev).contiguous() if bundle.model == GAT else None
+            self.wt.append((W, W2, att))
+            self.layers.append(_lib.Layer(_MODEL_ID[bundle.model], d_in, d_out, heads if bundle.model == GAT else 1,
+                                          float(bundle.degree_offset), 0, _lib.ptr(W), _lib.ptr(W2), _lib.ptr(att)))
+            d_agg = bundle.agg_dims[l]
+            self.H.append(z(n, d_out))
+            self.S.append(z(n, d_agg))
+            self.log.append(z(n, d_out))
+            if bundle.model == GAT:
+                self.ctx.append(z(n, heads))
+                self.Z.append(z(n, d_out))
+                self.el.append(z(n, heads))
+                self.er.append(z(n, heads))
+                self.Zlog.append(z(n, d_out))
+                self.erlog.append(z(n, heads))
+            else:
+                self.ctx.append(None)
+                for lst in (self.Z, self.el, self.er, self.Zlog, self.erlog):
+                    lst.append(None)
+        self.max_dim = max(max(dims), 1)
+        self.gemm_in = z(n, max(bundle.agg_dims)) if bundle.model != GAT else None
+        self.gemm_mid = z(n, max(dims[1:])) if bundle.model == GIN else None
+        self.fr = [_Frontier(n, self.dev) for _ in range(self.L)]
+        self._ensure_ws(max_batch or graph.batch.cap)
+        self.bootstrap()
+
+    # ---------------------------------------------------------------- plumbing
+    def _ensure_ws(self, B):
+        need = int(self.lib.rtec_workspace_bytes(self.n, max(int(B), 1), max(self.g.out.slots, self.g.inn.slots),
+                                                 self.max_dim))
+        if self.g.ws.numel() < need:
+            self.g.ws = torch.empty(need, dtype=torch.uint8, device=self.dev)
+
+    def _state(self, l):
+        p = _lib.ptr
+        return _lib.State(p(self.H[l]), p(self.H[l + 1]), p(self.S[l]), p(self.ctx[l]), p(self.log[l]),
+                          p(self.log[l - 1]) if l > 0 else None, p(self.Z[l]), p(self.el[l]), p(self.er[l]),
+                          p(self.Zlog[l]), p(self.erlog[l]), p(self.gemm_in), p(self.gemm_mid))
+
+    # ---------------------------------------------------------------- SPEC bootstrap / run_full
+    def bootstrap(self):
+        """Full forward populating every layer's state (models.py:461-477)."""
+        err = torch.full((1,), -1, dtype=torch.int64, device=self.dev)
+        g = self.g.c()
+        st = _lib.stream_handle()
+        for l in range(self.L):
+            s = self._state(l)
+            _lib.check(self.lib.rtec_layer_full(C.byref(g), C.byref(self.layers[l]), C.byref(s), None, None, self.n,
+                                                _lib.ptr(err), _lib.ptr(self.g.ws), self.g.ws.numel(), st), "bootstrap")
+        _lib.raise_err(err.item(), "bootstrap")
+
+    run_full = bootstrap
+
+    # ---------------------------------------------------------------- incremental step
+    def enqueue_step(self, B: int) -> None:
+        """Enqueue the whole incremental pipeline for the staged batch (no sync)."""
+        gr = self.g
+        self._ensure_ws(gr.batch.cap)
+        gr.apply_staged(B)
+        g, b = gr._gc, gr._bc
+        st = _lib.stream_handle()
+        ws, wsb = _lib.ptr(gr.ws), gr.ws.numel()
+        errp = _lib.ptr(gr.batch.err)
+        sdd = 1 if self.b.src_degree_dependent else 0
+        self._fc = [f.c() for f in self.fr]
+        self._sc = [self._state(l) for l in range(self.L)]
+        for l in range(self.L):
+            prev = C.byref(self._fc[l - 1]) if l > 0 else None
+            _lib.check(self.lib.rtec_frontier_layer(C.byref(g), C.byref(b), l, sdd, prev, C.byref(self._fc[l]), ws, wsb,
+                                                    st), "frontier")
+            if self.b.model == GAT and l > 0:
+                pf = self.fr[l - 1]
+                _lib.check(self.lib.rtec_gat_project(C.byref(self.layers[l]), _lib.ptr(self.H[l]), _lib.ptr(pf.dst_list),
+                                                     _lib.ptr(pf.n_dst), self.n, _lib.ptr(self.Z[l]), _lib.ptr(self.el[l]),
+                                                     _lib.ptr(self.er[l]), _lib.ptr(self.Zlog[l]), _lib.ptr(self.erlog[l]),
+                                                     errp, st), "gat_project")
+            _lib.check(self.lib.rtec_layer_incremental(C.byref(g), C.byref(b), C.byref(self.layers[l]),
+                                                       C.byref(self._sc[l]), prev, C.byref(self._fc[l]), errp, ws, wsb,
+                                                       st), "layer")
+        _lib.check(self.lib.rtec_batch_commit(C.byref(g), C.byref(b), st), "commit")
+
+    def step(self, op, src, dst, ts) -> RunResult:
+        """run_incremental on array inputs; syncs once at the end to read the result."""
+        B = self.g.stage(op, src, dst, ts)
+        for attempt in range(4):
+            self.enqueue_step(B)
+            word = self.g.batch_error()
+            d = _lib.decode_err(word)
+            if d is not None and d[0] == _lib.ARENA_FULL:
+                # nothing was mutated (validation-before-mutation); make room and replay
+                self.g.compact(min_reserve=(16 * B + 4096) * 4 ** attempt)
+                self.g._ensure_ws(self.g.batch.cap, grow=2.0 ** (attempt + 1))
+                self._ensure_ws(self.g.batch.cap)
+                continue
+            _lib.raise_err(word, "run_incremental", self.g._ERR_MSG)
+            break
+        else:
+            raise E.NativeError("run_incremental: arena still full after compaction")
+        status, deltas = self.g.read_result(B)
+        return RunResult(status, deltas, None, self.metrics())
+
+    def run_incremental(self, batch) -> RunResult:
+        """SPEC run_incremental on a coalesced EdgeUpdate list."""
+        return self.step(*updates_to_arrays(list(batch)))
+
+    # ---------------------------------------------------------------- reads
+    def metrics(self) -> Metrics:
+        m = Metrics()
+        for f in self.fr:
+            c = f.counters.cpu().numpy()
+            m.e_curr.append(int(c[0]))
+            m.v_dst.append(int(c[1]))
+            m.n_src.append(int(c[2]))
+            m.in_edges_vdst.append(int(c[5]))
+        return m
+
+    def frontier(self, l: int):
+        """(V_dst(l), S(l)) ascending id arrays of the last batch."""
+        f = self.fr[l]
+        nd, ns = int(f.n_dst.item()), int(f.n_src.item())
+        return f.dst_list[:nd].cpu().numpy().astype(np.int64), f.src_list[:ns].cpu().numpy().astype(np.int64)
+
+    def embeddings(self, l: int) -> np.ndarray:
+        """H^l (l = 0 features, l = L final layer) as float32 numpy."""
+        return self.H[l].cpu().numpy()
+
+    def aggregates(self, l: int) -> np.ndarray:
+        """Composed aggregate a^l = ms_cbn(ctx, S^l) for every vertex (reference layout)."""
+        S = self.S[l]
+        indeg = self.g.in_deg[: self.n].to(torch.float32)
+        if self.b.model == GAT:
+            h = self.b.heads
+            ctx = self.ctx[l]
+            safe = torch.where(ctx > 0, ctx, torch.ones_like(ctx))
+            A = (S.view(self.n, h, -1) / safe[:, :, None]).reshape(self.n, -1)
+        elif self.b.model == "gcn":
+            A = S / torch.sqrt(indeg + self.b.degree_offset)[:, None]
+        elif self.b.model == "graphsage":
+            A = S / torch.clamp(indeg, min=1.0)[:, None]
+        else:
+            A = S
+        A = torch.where((indeg > 0)[:, None], A, torch.zeros_like(A))
+        return A.cpu().numpy()
+
+    def contexts(self, l: int) -> np.ndarray:
+        indeg = self.g.in_deg[: self.n].cpu().numpy().astype(np.float64)
+        if self.b.model == GAT:
+            c = self.ctx[l].cpu().numpy().astype(np.float64)
+            return c[:, 0] if self.b.heads == 1 else c
+        if self.b.ctx_kind == "count":
+            return indeg
+        return np.ones(self.n)
+
+    def query(self, ids) -> np.ndarray:
+        """Refreshed final-layer rows for `ids` (SPEC materialize_h SPEC.md:379)."""
+        ids_t = torch.as_tensor(np.asarray(ids, np.int64), device=self.dev)
+        if ids_t.numel() and (int(ids_t.min()) < 0 or int(ids_t.max()) >= self.n):
+            raise E.InvalidVertex("query vertex outside the vertex range")
+        ids_t = ids_t.to(torch.int32)
+        d = self.b.dims[-1]
+        out = torch.empty(max(ids_t.numel(), 1), d, dtype=torch.float32, device=self.dev)
+        err = torch.full((1,), -1, dtype=torch.int64, device=self.dev)
+        _lib.check(self.lib.rtec_query(_lib.ptr(self.H[-1]), d, _lib.ptr(ids_t), ids_t.numel(), _lib.ptr(out), self.n,
+                                       _lib.ptr(err), _lib.stream_handle()), "query")
+        _lib.raise_err(err.item(), "query")
+        return out[: ids_t.numel()].cpu().numpy()
+
+    materialize_h = query

@@ -1,0 +1,162 @@
+"""GPU parity of the incremental engine (frontier K7/K8, layers K10-K17).
+
+- against the reference's own full recomputation (golden fixtures: H^l, A^l,
+  C^l after every batch of a mixed stream), fp32 vs f64, row-wise relative
+  tolerance 1e-4;
+- against the oracle engine on larger power-law graphs: ApplyResult and the
+  per-layer affected sets V_dst(l) bit-exact, embeddings within 1e-4;
+- properties: deletion round trip, multi-batch drift, query.
+"""
+
+import numpy as np
+import pytest
+
+from helpers import MODEL_CASES, golden, rowwise_rel
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4  # row-wise max relative error, fp32 engine vs f64 reference (north star)
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2603_20622_b200 as P
+
+    return P
+
+
+def _model(case):
+    return {"gcn_raw": "gcn", "gat_h4": "gat"}.get(case, case)
+
+
+def _engine_for_case(P, case, z):
+    n = int(z["n"])
+    dims = [int(x) for x in z["dims"]]
+    b = P.make_bundle(_model(case), dims, rng_seed=0, degree_smoothing=bool(int(z["smoothing"])),
+                      heads=int(z["heads"]))
+    g = P.DynamicGraph.from_edges(n, (z["src"], z["dst"]))
+    return P.RTECEngine(b, g, z["X"].astype(np.float32)), b
+
+
+def _check_against(eng, z, tag, L):
+    for l in range(L):
+        assert rowwise_rel(eng.embeddings(l + 1), z[f"{tag}_H{l + 1}"]) <= TOL, (tag, "H", l)
+        assert rowwise_rel(eng.aggregates(l), z[f"{tag}_A{l}"]) <= TOL, (tag, "A", l)
+        c = eng.contexts(l).reshape(z[f"{tag}_C{l}"].shape)
+        assert np.allclose(c, z[f"{tag}_C{l}"], rtol=1e-4, atol=1e-5), (tag, "C", l)
+
+
+@pytest.mark.parametrize("case", MODEL_CASES)
+def test_golden_models(P, case):
+    z = golden(f"models_{case}.npz")
+    eng, b = _engine_for_case(P, case, z)
+    L = b.num_layers
+    # weights are the reference's make_bundle draws (models.py:56-63)
+    if int(z["heads"]) == 1:
+        for l in range(L):
+            assert np.array_equal(b.layers[l].tensors["W"], z[f"w{l}_W"])
+    _check_against(eng, z, "boot", L)
+    for bi in range(int(z["nb"])):
+        p = f"b{bi}_"
+        eng.step(z[p + "op"], z[p + "src"], z[p + "dst"], z[p + "ts"])
+        _check_against(eng, z, f"b{bi}", L)
+
+
+def _run_vs_oracle(P, model, dims, n, m, B, nb, seed, heads=1, smoothing=True):
+    from oracle import models as OM
+    from oracle.engine import OracleEngine
+    from oracle.graph import OracleGraph
+    from paper_2603_20622_b200.workload import UpdateStream, chung_lu_edges, features
+
+    s, d = chung_lu_edges(n, m, seed=seed)
+    stream = UpdateStream(s, d, holdout=0.1, seed=seed)
+    bs, bd, bt = stream.base()
+    X = features(n, dims[0], seed=seed + 1)
+    g = P.DynamicGraph.from_edges(n, (bs, bd, bt))
+    eng = P.RTECEngine(P.make_bundle(model, dims, heads=heads, degree_smoothing=smoothing), g, X)
+    oe = OracleEngine(OM.make_bundle(model, dims, heads=heads, degree_smoothing=smoothing),
+                      OracleGraph.from_edges(n, bs, bd, bt), X.astype(np.float64))
+    L = len(dims) - 1
+    worst = 0.0
+    for _ in range(nb):
+        op, s1, d1, t1 = stream.next_batch(B)
+        r = eng.step(op, s1, d1, t1)
+        o = oe.step(op, s1, d1, t1)
+        assert np.array_equal(r.status, o["status"])
+        assert np.array_equal(r.deltas, o["deltas"])
+        for l in range(L):
+            vdst, _ = eng.frontier(l)
+            assert np.array_equal(vdst, o["frontier"][l]["vdst"]), ("V_dst", l)
+            assert r.metrics.e_curr[l] == o["frontier"][l]["n_ecurr"], ("|E_curr|", l)
+        for l in range(L):
+            e = rowwise_rel(eng.embeddings(l + 1), oe.H[l + 1])
+            worst = max(worst, e)
+            assert e <= TOL, (l, e)
+            assert rowwise_rel(eng.aggregates(l), oe.A[l]) <= TOL
+    return eng, oe, worst
+
+
+@pytest.mark.parametrize("model,dims", [("gcn", [32, 64, 32]), ("graphsage", [48, 64, 32]), ("gin", [32, 32, 32]),
+                                        ("gat", [40, 32, 32])])
+def test_engine_vs_oracle(P, model, dims):
+    _run_vs_oracle(P, model, dims, n=4000, m=60000, B=400, nb=4, seed=3)
+
+
+def test_engine_vs_oracle_gat_heads(P):
+    _run_vs_oracle(P, "gat", [24, 64, 64], n=3000, m=40000, B=300, nb=3, seed=5, heads=4)
+
+
+def test_engine_gcn_raw_degrees(P):
+    _run_vs_oracle(P, "gcn", [16, 16, 16], n=2000, m=20000, B=200, nb=3, seed=6, smoothing=False)
+
+
+def test_engine_large_batch_radix_path(P):
+    # B > 2048 exercises the multi-CTA radix sort and the radix-sorted merges
+    _run_vs_oracle(P, "gcn", [16, 32, 16], n=20000, m=200000, B=6000, nb=2, seed=8)
+
+
+def test_engine_three_layers_gin(P):
+    _run_vs_oracle(P, "gin", [16, 16, 16, 16], n=3000, m=30000, B=200, nb=3, seed=9)
+
+
+def test_drift_many_batches(P):
+    eng, oe, worst = _run_vs_oracle(P, "graphsage", [16, 16, 16], n=1500, m=12000, B=64, nb=30, seed=10)
+    assert worst <= TOL
+
+
+def test_deletion_round_trip(P):
+    from paper_2603_20622_b200.workload import chung_lu_edges, features
+
+    n = 2000
+    s, d = chung_lu_edges(n, 20000, seed=11)
+    X = features(n, 16, seed=2)
+    for model in ("gcn", "graphsage", "gin", "gat"):
+        g = P.DynamicGraph.from_edges(n, (s, d))
+        eng = P.RTECEngine(P.make_bundle(model, [16, 16, 16]), g, X)
+        H0 = eng.embeddings(2).copy()
+        rng = np.random.default_rng(3)
+        pick = rng.choice(s.size, 100, replace=False)
+        op = np.ones(100, np.uint8)
+        eng.step(op, s[pick], d[pick], np.zeros(100, np.int64))
+        eng.step(1 - op, s[pick], d[pick], np.zeros(100, np.int64))
+        assert rowwise_rel(eng.embeddings(2), H0) <= 1e-5, model
+
+
+def test_query_and_errors(P):
+    from paper_2603_20622_b200.workload import chung_lu_edges, features
+
+    n = 500
+    s, d = chung_lu_edges(n, 4000, seed=12)
+    eng = P.RTECEngine(P.make_bundle("gcn", [8, 8]), P.DynamicGraph.from_edges(n, (s, d)), features(n, 8))
+    ids = np.array([0, 7, 499, 7])
+    q = eng.query(ids)
+    assert np.array_equal(q, eng.embeddings(1)[ids])
+    with pytest.raises(P.InvalidVertex):
+        eng.query([500])
+    with pytest.raises(P.InvalidVertex):
+        eng.step(np.array([0], np.uint8), np.array([0]), np.array([n]), np.array([0]))
+    with pytest.raises(P.UnsupportedModel):
+        P.make_bundle("monet", [4, 4])
