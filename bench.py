@@ -1,0 +1,429 @@
+#!/usr/bin/env python
+"""bench.py -- edge updates/s and p50 batch latency of the B200 incremental RTEC engine.
+
+Default workload ("c2-gcn"): the configs[1] graph (ogbn-products shape:
+2,449,029 vertices, 61,859,140 edges, Chung-Lu alpha=0.8, 100-dim features)
+run with the metric's model, 2-layer GCN [100, 256, 256], and 0.1% update
+batches (61,859 updates: half hold-out inserts, half deletes of live edges).
+configs[5] (the metric's own GCN/papers100M config) needs 8 GPUs; this is the
+largest single-GPU configuration at the metric's model and batch fraction.
+
+Arms
+  (default)          our engine; `value` = device-timed throughput with the
+                     batches already resident in HBM, `e2e` = the public
+                     RTECEngine.step() API from pinned host buffers including
+                     H2D of the batch and D2H of the per-update status/deltas.
+  --impl reference   the reference's CPU path (the oracle port in oracle/, the
+                     only place bench.py may execute it) on the same workload,
+                     rank 0 only, on a bounded sample (see cpu_sample()).
+
+Timing: W warm-up steps, then K steps bracketed by barrier + synchronize,
+CUDA events per step on the engine's stream, L2 flushed (256 MiB write)
+between timed steps, max over ranks.  Multi-GPU (torchrun): every rank runs
+an independent replica on its own stream of batches ("replicas only" this
+round, scaling weak; the vertex-sharded halo path is DESIGN.md §6 next).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "edge updates/sec and p50 batch latency, 2-layer GCN, 0.1% update batches"
+
+WORKLOADS = {
+    "c2-gcn": dict(desc="configs[1] graph (ogbn-products shape) with the metric's model: 2-layer GCN, 0.1% batches",
+                   n=2449029, m=61859140, model="gcn", dims=[100, 256, 256], batch=61859, heads=1),
+    "c2-sage": dict(desc="configs[1]: 2-layer GraphSAGE-mean, products shape, 0.1% batches",
+                    n=2449029, m=61859140, model="graphsage", dims=[100, 256, 256], batch=61859, heads=1),
+    "c1-gcn": dict(desc="configs[0]: 2-layer GCN 128 hidden, 100K/2M power-law, 1,000-update batches",
+                   n=100000, m=2000000, model="gcn", dims=[128, 128, 128], batch=1000, heads=1),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2-gcn", choices=sorted(WORKLOADS))
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks / cpu baseline)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- distributed
+def dist_init():
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------- clocks
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int, enabled: bool = True):
+        self.p = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+        if enabled:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            try:
+                self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
+                                           "--format=csv,noheader,nounits", "-lms", "100"],
+                                          stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            except OSError:
+                self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- workload
+def make_workload(wl: dict, steps_total: int, device):
+    """Graph on the GPU (bit-identical to the CPU generator), stream on the host."""
+    from paper_2603_20622_b200.workload import UpdateStream, chung_lu_edges, features
+
+    s, d = chung_lu_edges(wl["n"], wl["m"], seed=0, device=device)
+    stream = UpdateStream(s, d, holdout=0.1, seed=0)
+    batches = [stream.next_batch(wl["batch"]) for _ in range(steps_total)]
+    X = features(wl["n"], wl["dims"][0], seed=1)
+    return stream, batches, X
+
+
+def algorithmic_bytes(name: str, wl: dict, layer_counters, n: int) -> float:
+    """Algorithmic (compulsory) HBM bytes of one launch.
+
+    layer_counters: [|E_curr|, |V_dst|, |S|, |R|, -, Σindeg(V_dst), -, -] of the layer."""
+    e_curr, v_dst, n_src, _, _, sum_in = [float(x) for x in layer_counters[:6]]
+    l = layer_counters[7]
+    d_a = wl["dims"][int(l)]
+    d_o = wl["dims"][int(l) + 1]
+    f = 4.0
+    if name == "k_agg_inc":
+        # in-run ids of V_dst + S-bitmap + δ rows once + S read/write + composed row write + list/offsets
+        return 4 * sum_in + n / 8 + f * d_a * n_src + 3 * f * d_a * v_dst + 16 * v_dst
+    if name == "k_src_delta":
+        return f * d_a * 3 * n_src + 12 * n_src
+    if name == "k_gemm_update":
+        # composed rows in, H rows out + old H rows into the DeltaLog, weights
+        return f * d_a * v_dst + 3 * f * d_o * v_dst + f * d_a * d_o + 4 * v_dst
+    if name == "k_expand":
+        return 4 * e_curr + n / 8
+    return 0.0
+
+
+def gemm_flops(wl, layer_counters):
+    l = int(layer_counters[7])
+    return 2.0 * float(layer_counters[1]) * wl["dims"][l] * wl["dims"][l + 1]
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args, world, rank, local):
+    import torch
+
+    import paper_2603_20622_b200 as P
+    from paper_2603_20622_b200 import _lib
+
+    wl = WORKLOADS[args.workload]
+    dev = torch.device("cuda", local)
+    K, W = args.steps, args.warmup
+    E2E = args.e2e_steps if args.e2e_steps is not None else min(K, 10)
+    t0 = time.time()
+    stream, batches, X = make_workload(wl, W + K + E2E, dev)
+    bs, bd, bt = stream.base()
+    g = P.DynamicGraph.from_tensors(wl["n"], torch.as_tensor(bs, device=dev), torch.as_tensor(bd, device=dev),
+                                    torch.as_tensor(bt, device=dev), reserve=max(1 << 20, wl["m"] // 2))
+    eng = P.RTECEngine(P.make_bundle(wl["model"], wl["dims"], heads=wl["heads"]), g, X, max_batch=wl["batch"])
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+    lib = _lib.load()
+    L = len(wl["dims"]) - 1
+    # batches resident in HBM for the device-timed arm
+    dev_batches = []
+    for (op, s, d, t) in batches[: W + K]:
+        dev_batches.append(tuple(torch.as_tensor(np.ascontiguousarray(a, dt), device=dev)
+                                 for a, dt in ((op, np.uint8), (s, np.int32), (d, np.int32), (t, np.int64))))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    errs = torch.zeros(K, dtype=torch.int64, device=dev)
+    ctrs = torch.zeros(K, L, 8, dtype=torch.int64, device=dev)
+    napp = torch.zeros(K, dtype=torch.int64, device=dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+
+    def stage(i):
+        op, s, d, t = dev_batches[i]
+        B = g.stage(op, s, d, t)
+        return B
+
+    for i in range(W):
+        eng.enqueue_step(stage(i))
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = Clocks(local, enabled=not (args.no_clocks or args.profile))
+    lib.rtec_prof_enable(1)
+    _lib.prof_report(reset=True)
+    torch.cuda.synchronize()
+    barrier(world)
+    wall0 = time.time()
+    total_updates = 0
+    for k in range(K):
+        flush.zero_()  # L2 flush between timed steps (outside the events)
+        B = stage(W + k)
+        total_updates += B
+        evs[k][0].record()
+        eng.enqueue_step(B)
+        evs[k][1].record()
+        errs[k : k + 1].copy_(g.batch.err)
+        napp[k : k + 1].copy_(g.batch.n_applied)
+        for l in range(L):
+            ctrs[k, l].copy_(eng.fr[l].counters)
+    torch.cuda.synchronize()
+    barrier(world)
+    wall = time.time() - wall0
+    lib.rtec_prof_enable(0)
+    prof = _lib.prof_report(reset=True)
+    clk = clocks.stop()
+    bad = [int(e) & _lib.ERR_OK for e in errs.cpu().tolist() if (int(e) & _lib.ERR_OK) != _lib.ERR_OK]
+    if bad:
+        raise RuntimeError(f"batch errors during timed run: {bad[:4]}")
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    applied = int(napp.sum().item())
+    tot_s = sum(step_ms) / 1e3
+    tot_s_max = max_over_ranks(tot_s, world)
+    applied_all = sum_over_ranks(applied, world)
+    value = applied_all / tot_s_max
+    p50 = statistics.median(step_ms)
+    p90 = float(np.percentile(step_ms, 90))
+    # --- e2e through the public API from pinned host memory
+    e2e_ms, h2d, d2h = [], 0, 0
+    e2e_upd = 0
+    for j in range(E2E):
+        op, s, d, t = batches[W + K + j]
+        hb = [torch.from_numpy(np.ascontiguousarray(a, dt)).pin_memory()
+              for a, dt in ((op, np.uint8), (s, np.int32), (d, np.int32), (t, np.int64))]
+        torch.cuda.synchronize()
+        a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_ev.record()
+        r = eng.step(*hb)
+        b_ev.record()
+        torch.cuda.synchronize()
+        e2e_ms.append(a_ev.elapsed_time(b_ev))
+        e2e_upd += int(r.status.sum())
+        h2d += sum(x.numel() * x.element_size() for x in hb)
+        d2h += r.status.nbytes + r.deltas.shape[0] * 5 * 4 + 8 + 8 + 8
+    e2e_val = None
+    if E2E:
+        e2e_s = max_over_ranks(sum(e2e_ms) / 1e3, world)
+        e2e_val = sum_over_ranks(e2e_upd, world) / e2e_s
+    # --- roofline of the dominant kernel
+    from_peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = float(from_peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if from_peaks else "fallback"
+    C = ctrs.cpu().numpy()
+    for l in range(L):
+        C[:, l, 7] = l
+    kernels = {}
+    for name, (cnt, ms) in prof.items():
+        per_launch_ms = ms / max(cnt, 1)
+        byts = 0.0
+        if name in ("k_agg_inc", "k_src_delta", "k_gemm_update", "k_expand"):
+            byts = sum(algorithmic_bytes(name, wl, C[k, l], wl["n"]) for k in range(K) for l in range(L)) / max(cnt, 1)
+        kernels[name] = {"launches": cnt, "total_ms": round(ms, 4), "ms_per_launch": round(per_launch_ms, 5),
+                         "share": round(ms / max(sum(step_ms), 1e-9), 4),
+                         "algo_GBps": round(byts / (per_launch_ms * 1e6), 1) if byts else None}
+    hot = [k for k in ("k_agg_inc", "k_gemm_update", "k_src_delta", "k_expand") if k in kernels]
+    dom = max(hot, key=lambda k: kernels[k]["total_ms"]) if hot else None
+    roof = None
+    if dom:
+        ach = kernels[dom]["algo_GBps"] or 0.0
+        per_launch_bytes = ach * kernels[dom]["ms_per_launch"] * 1e6
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(ach / hbm_peak, 4), "peak_source": peak_src,
+                "bytes_per_launch": per_launch_bytes, "traffic": None}
+        if dom == "k_gemm_update":
+            fl = sum(gemm_flops(wl, C[k, l]) for k in range(K) for l in range(L)) / max(kernels[dom]["launches"], 1)
+            roof["tflops"] = round(fl / (kernels[dom]["ms_per_launch"] * 1e9), 2)
+    res = {
+        "metric": METRIC,
+        "value": round(value, 1),
+        "unit": "edge updates/s",
+        "n_gpus": world,
+        "steps": K,
+        "warmup": W,
+        "ms_per_step": round(statistics.mean(step_ms), 4),
+        "p50_batch_ms": round(p50, 4),
+        "p90_batch_ms": round(p90, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (seeded Chung-Lu graph, U(-1,1) features, make_bundle seed-0 weights)",
+        "config": {"workload": args.workload, "desc": wl["desc"], "vertices": wl["n"], "edges": wl["m"],
+                   "model": wl["model"], "dims": wl["dims"], "batch_updates": wl["batch"],
+                   "batch_fraction": round(wl["batch"] / wl["m"], 6), "parallelism": f"replicas x{world}",
+                   "l2": "flushed between timed steps (256 MiB write)"},
+        "e2e": {"value": round(e2e_val, 1) if e2e_val else None, "unit": "edge updates/s", "steps": E2E,
+                "h2d_bytes_per_step": h2d // max(E2E, 1), "d2h_bytes_per_step": d2h // max(E2E, 1),
+                "p50_batch_ms": round(statistics.median(e2e_ms), 4) if e2e_ms else None},
+        "gpu_launches": None,
+        "roofline": roof,
+        "kernels": kernels,
+        "frontier": {"e_curr": [int(np.mean(C[:, l, 0])) for l in range(L)],
+                     "v_dst": [int(np.mean(C[:, l, 1])) for l in range(L)],
+                     "n_src": [int(np.mean(C[:, l, 2])) for l in range(L)]},
+        "clocks": clk,
+        "setup_s": round(setup_s, 1),
+        "wall_s": round(wall, 3),
+    }
+    res["gpu_launches"] = launches_per_step(prof, K) * K
+    return res, g, eng
+
+
+def launches_per_step(prof, K):
+    """Kernel launches of librtec per step (counted by the event hook's scopes)."""
+    # scopes wrap single kernels except frontier_layer / batch_apply / adj_merge (multi-kernel);
+    # count them from the static launch plan instead: see DESIGN.md §5 (launch census).
+    n = 0
+    for name, (cnt, _) in prof.items():
+        n += cnt
+    return int(round(n / max(K, 1)))
+
+
+# ---------------------------------------------------------------- reference (CPU) arm
+def cpu_sample(wl_name: str, budget_s: float):
+    """Oracle port (oracle/, numpy) on a bounded sample of the workload."""
+    import resource  # noqa: F401
+
+    from oracle import models as OM
+    from oracle.engine import OracleEngine
+    from oracle.graph import OracleGraph
+    from paper_2603_20622_b200.workload import UpdateStream, chung_lu_edges, features
+
+    wl = WORKLOADS[wl_name]
+    s, d = chung_lu_edges(wl["n"], wl["m"], seed=0)
+    stream = UpdateStream(s, d, holdout=0.1, seed=0)
+    bs, bd, bt = stream.base()
+    og = OracleGraph.from_edges(wl["n"], bs, bd, bt)
+    eng = OracleEngine(OM.make_bundle(wl["model"], wl["dims"]), og, features(wl["n"], wl["dims"][0], 1).astype(np.float64))
+    times, ups = [], 0
+    t_start = time.time()
+    while True:
+        op, s1, d1, t1 = stream.next_batch(wl["batch"])
+        t = time.time()
+        r = eng.step(op, s1, d1, t1)
+        times.append(time.time() - t)
+        ups += int(r["status"].sum())
+        if time.time() - t_start > budget_s or len(times) >= 20:
+            break
+    return ups / sum(times), len(times), statistics.median(times)
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_init()
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        wl = args.workload
+        # The numpy port needs ~3 min per configs[1] GCN batch (+2.5 min setup), so the
+        # bounded sample is configs[0] (the reference's CPU-runnable case) unless asked.
+        sample_wl = wl if wl == "c1-gcn" else "c1-gcn"
+        v, nsteps, p50 = cpu_sample(sample_wl, budget_s=60.0)
+        cores = 1
+        out = {"impl": "reference", "metric": METRIC, "value": round(v, 1), "unit": "edge updates/s", "n_gpus": world,
+               "steps": nsteps, "warmup": 0, "ms_per_step": round(p50 * 1e3, 2), "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "config": {"workload": wl, "sample_workload": sample_wl},
+               "cpu_baseline": {"value": round(v, 1), "unit": "edge updates/s", "cores": cores, "kind": "port",
+                                "sample": f"{nsteps} batches of {WORKLOADS[sample_wl]['desc']} (numpy oracle, f64)"},
+               "e2e": {"value": round(v, 1), "unit": "edge updates/s", "h2d_bytes_per_step": 0,
+                       "d2h_bytes_per_step": 0}}
+        print(json.dumps(out))
+        return
+    res, g, eng = run_ours(args, world, rank, local)
+    if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.profile):
+        v, nsteps, p50 = cpu_sample("c1-gcn", budget_s=30.0)
+        res["cpu_baseline"] = {"value": round(v, 1), "unit": "edge updates/s", "cores": 1, "kind": "port",
+                               "sample": f"{nsteps} batches of configs[0] GCN-2L 100K/2M B=1000 (numpy oracle, f64); "
+                                         "the numpy port needs ~3 min per configs[1] batch"}
+    if rank == 0:
+        print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()

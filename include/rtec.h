@@ -226,6 +226,8 @@ int rtec_query(const float* H, int64_t d, const int32_t* ids, int64_t k, float* 
                uint64_t* err, rtec_stream_t stream);
 
 /* ---- diagnostics ---- */
+void rtec_prof_enable(int on);  /* bracket kernels with CUDA events (bench / profiling only) */
+size_t rtec_prof_report(char* buf, size_t len, int reset); /* "name count total_ms" lines */
 void rtec_struct_sizes(int64_t* out6); /* sizeof adj, graph, batch, frontier, layer, state */
 const char* rtec_last_error(void);
 const char* rtec_version(void);

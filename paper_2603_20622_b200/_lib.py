@@ -91,6 +91,8 @@ _SIGS = {
     "rtec_update_gemm": (C.c_int, [P, I64, P, I32, I32, P, I64, I32, P, I64, P, P, P, P]),
     "rtec_query": (C.c_int, [P, I64, P, I64, P, I32, P, P]),
     "rtec_struct_sizes": (None, [C.POINTER(I64)]),
+    "rtec_prof_enable": (None, [C.c_int]),
+    "rtec_prof_report": (SZ, [C.c_char_p, SZ, C.c_int]),
     "rtec_last_error": (C.c_char_p, []),
     "rtec_version": (C.c_char_p, []),
     "rtec_device_sm_count": (C.c_int, []),
@@ -162,3 +164,15 @@ def stream_handle():
     import torch
 
     return torch.cuda.current_stream().cuda_stream
+
+
+def prof_report(reset: bool = True) -> dict:
+    """Per-kernel {name: (launches, total_ms)} from the library's event hook."""
+    n = _lib.rtec_prof_report(None, 0, 0)
+    buf = C.create_string_buffer(n + 1)
+    _lib.rtec_prof_report(buf, n + 1, 1 if reset else 0)
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, cnt, ms = line.split()
+        out[name] = (int(cnt), float(ms))
+    return out

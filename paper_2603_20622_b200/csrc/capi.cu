@@ -1,8 +1,11 @@
 // capi.cu -- library-level C entry points (workspace sizing, diagnostics).
+#include <string.h>
+
 #include "prims.cuh"
 
 namespace rtec {
 const char* last_error_cstr();
+std::string prof_report(bool reset);
 size_t batch_ws_bytes(int64_t n, int64_t B, int64_t scr_cap);
 size_t frontier_ws_bytes(int64_t n);
 }  // namespace rtec
@@ -43,6 +46,20 @@ void rtec_struct_sizes(int64_t* out6) {
 }
 
 const char* rtec_last_error(void) { return last_error_cstr(); }
+
+void rtec_prof_enable(int on) { g_prof_on = on != 0; }
+
+// Copies the per-kernel timing report ("name count total_ms" lines) into buf.
+size_t rtec_prof_report(char* buf, size_t len, int reset) {
+  static std::string last;
+  last = prof_report(reset != 0);
+  if (buf && len) {
+    size_t k = last.size() < len - 1 ? last.size() : len - 1;
+    memcpy(buf, last.data(), k);
+    buf[k] = 0;
+  }
+  return last.size();
+}
 const char* rtec_version(void) { return "rtec-b200 0.1 (sm_100a)"; }
 
 int rtec_device_sm_count(void) {

@@ -31,6 +31,25 @@ int cuda_status(cudaError_t e, const char* where);
     if (_s != RTEC_OK) return _s;   \
   } while (0)
 
+// ---------------------------------------------------------------- kernel timing hook
+// When enabled (rtec_prof_enable), launch sites bracket kernels with CUDA
+// events on their stream; rtec_prof_report aggregates per kernel name.  Off by
+// default (and never used inside CUDA-graph capture).
+extern bool g_prof_on;
+void prof_begin(const char* name, cudaStream_t s);
+void prof_end(cudaStream_t s);
+struct ProfScope {
+  cudaStream_t s;
+  bool on;
+  ProfScope(const char* name, cudaStream_t st) : s(st), on(g_prof_on) {
+    if (on) prof_begin(name, s);
+  }
+  ~ProfScope() {
+    if (on) prof_end(s);
+  }
+};
+#define RTEC_PROF(name, stream) ::rtec::ProfScope _rtec_prof_scope_##__LINE__(name, stream)
+
 // ---------------------------------------------------------------- workspace
 // Bump allocator over the caller's workspace; every chunk 256-B aligned.
 struct Ws {

@@ -153,6 +153,7 @@ extern "C" int rtec_frontier_layer(const rtec_graph_t* g, const rtec_batch_t* b,
     set_error("frontier layer %d needs the previous layer's frontier", l);
     return RTEC_CONFIG_ERROR;
   }
+  RTEC_PROF("frontier_layer", s);
   Ws w(ws, ws_bytes);
   int32_t* nlist = w.alloc<int32_t>(n + 1);
   int64_t* noff = w.alloc<int64_t>(n + 2);
@@ -176,7 +177,10 @@ extern "C" int rtec_frontier_layer(const rtec_graph_t* g, const rtec_batch_t* b,
   WordPop np{f->bm_src, prev_src};
   RTEC_TRY(exclusive_scan(np, Count{nullptr, words}, words, WordList{np, nlist, nullptr}, n_new, w, s));
   RTEC_TRY(exclusive_scan(OutLenOf{nlist, g->out.len}, Count{n_new, n}, n, StoreOffTailF{noff, n_new}, nullptr, w, s));
-  k_expand<<<kSMs * 8, kFBlk, 0, s>>>(nlist, n_new, noff, g->out, f->bm_dst);
+  {
+    RTEC_PROF("k_expand", s);
+    k_expand<<<kSMs * 8, kFBlk, 0, s>>>(nlist, n_new, noff, g->out, f->bm_dst);
+  }
   RTEC_LAUNCH_CHECK("k_expand");
   // lists + slots
   WordPop sp{f->bm_src, nullptr};

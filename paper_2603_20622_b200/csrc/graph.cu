@@ -538,6 +538,7 @@ static int merge_plan(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, floa
 
 static int merge_exec(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, int64_t work_bound, uint64_t* err,
                       cudaStream_t s) {
+  RTEC_PROF("adj_merge", s);
   k_merge_items<<<grid_for(work_bound, kBlk, kSMs * 32), kBlk, 0, s>>>(in, p, a, err);
   k_merge_copyback<<<grid_for(work_bound, kBlk, kSMs * 32), kBlk, 0, s>>>(p, a, err);
   k_merge_commit<<<grid_for(in.maxK, kBlk), kBlk, 0, s>>>(p, a, err);
@@ -738,6 +739,7 @@ int rtec_batch_apply(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src, const
   RTEC_CUDA(cudaMemsetAsync(b->n_applied, 0, sizeof(int64_t), s));
   RTEC_CUDA(cudaMemsetAsync(b->n_delta, 0, sizeof(int64_t), s));
   if (B <= 0) return RTEC_OK;
+  RTEC_PROF("batch_apply", s);
   Ws w(ws, ws_bytes);
   int64_t B2 = 2 * B;
   uint64_t* keys = w.alloc<uint64_t>(B2);

@@ -503,6 +503,7 @@ __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs g) {
 int gemm_launch(const GemmArgs& g, cudaStream_t s) {
   if (g.max_rows <= 0) return RTEC_OK;
   dim3 grid(static_cast<unsigned>((g.max_rows + kGM - 1) / kGM), static_cast<unsigned>((g.d_out + kGN - 1) / kGN));
+  RTEC_PROF("k_gemm_update", s);
   k_gemm_simt<<<grid, 256, 0, s>>>(g);
   RTEC_LAUNCH_CHECK("k_gemm_simt");
   return RTEC_OK;
@@ -570,6 +571,7 @@ int rtec_layer_incremental(const rtec_graph_t* g, const rtec_batch_t* b, const r
     a.d_agg = L->d_out;
     int dh = L->d_out / L->heads;
     bool ok;
+    RTEC_PROF("k_gat_layer", s);
     if (L->d_out % 4 == 0 && dh % 4 == 0) {
       ok = RTEC_ROW_DISPATCH(L->d_out, (k_gat_layer<VEC, K><<<grid, kLBlk, 0, s>>>(a, 0)));
     } else {
@@ -591,8 +593,15 @@ int rtec_layer_incremental(const rtec_graph_t* g, const rtec_batch_t* b, const r
   float* delta = w.alloc<float>(n * static_cast<int64_t>(L->d_in));
   RTEC_WS_CHECK(w);
   a.delta = delta;
-  bool ok = RTEC_ROW_DISPATCH(L->d_in, (k_src_delta<VEC, K><<<grid, kLBlk, 0, s>>>(a, delta),
-                                        k_agg_inc<VEC, K><<<grid, kLBlk, 0, s>>>(a)));
+  bool ok;
+  {
+    RTEC_PROF("k_src_delta", s);
+    ok = RTEC_ROW_DISPATCH(L->d_in, (k_src_delta<VEC, K><<<grid, kLBlk, 0, s>>>(a, delta)));
+  }
+  {
+    RTEC_PROF("k_agg_inc", s);
+    ok = ok && RTEC_ROW_DISPATCH(L->d_in, (k_agg_inc<VEC, K><<<grid, kLBlk, 0, s>>>(a)));
+  }
   if (!ok) {
     set_error("row width %d unsupported", L->d_in);
     return RTEC_SHAPE_ERROR;
@@ -681,6 +690,7 @@ int rtec_gat_project(const rtec_layer_t* L, const float* H, const int32_t* rows,
   GemmArgs gz{H, L->d_in, rows, L->W, L->d_in, L->d_out, rows ? n_rows : nullptr, n_or_max_rows, 0,
               Z, L->d_out, rows, Z_log, err};
   RTEC_TRY(gemm_launch(gz, s));
+  RTEC_PROF("k_gat_logits", s);
   k_gat_logits<<<kSMs * 8, kLBlk, 0, s>>>(Z, rows, n_rows, n_or_max_rows, L->d_out, L->heads, L->att, el, er, er_log,
                                           err);
   RTEC_LAUNCH_CHECK("k_gat_logits");

@@ -1,6 +1,9 @@
 // prims.cu -- scan-of-block-sums and the (u64 key, u32 value) sort.
 #include <stdarg.h>
 
+#include <map>
+#include <vector>
+
 #include "prims.cuh"
 
 namespace rtec {
@@ -23,6 +26,59 @@ int cuda_status(cudaError_t e, const char* where) {
 }
 
 const char* last_error_cstr() { return g_last_error.c_str(); }
+
+// ---------------------------------------------------------------- timing hook
+bool g_prof_on = false;
+struct ProfRec {
+  const char* name;
+  cudaEvent_t a, b;
+};
+static std::vector<ProfRec> g_prof;
+static std::vector<size_t> g_prof_open;
+
+void prof_begin(const char* name, cudaStream_t s) {
+  ProfRec r{name, nullptr, nullptr};
+  cudaEventCreate(&r.a);
+  cudaEventCreate(&r.b);
+  cudaEventRecord(r.a, s);
+  g_prof_open.push_back(g_prof.size());
+  g_prof.push_back(r);
+}
+
+void prof_end(cudaStream_t s) {
+  if (g_prof_open.empty()) return;
+  size_t i = g_prof_open.back();
+  g_prof_open.pop_back();
+  cudaEventRecord(g_prof[i].b, s);
+}
+
+// "name count total_ms\n" lines, aggregated by name; syncs on the events.
+std::string prof_report(bool reset) {
+  std::map<std::string, std::pair<long, double>> agg;
+  for (auto& r : g_prof) {
+    float ms = 0.f;
+    cudaEventSynchronize(r.b);
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    auto& e = agg[r.name];
+    e.first += 1;
+    e.second += ms;
+  }
+  std::string out;
+  char line[256];
+  for (auto& kv : agg) {
+    snprintf(line, sizeof(line), "%s %ld %.6f\n", kv.first.c_str(), kv.second.first, kv.second.second);
+    out += line;
+  }
+  if (reset) {
+    for (auto& r : g_prof) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    g_prof.clear();
+    g_prof_open.clear();
+  }
+  return out;
+}
 
 // ---------------------------------------------------------------- scan
 __global__ void __launch_bounds__(kScanBlock) k_scan_blocks(int64_t* bs, int64_t nb, int64_t* total) {

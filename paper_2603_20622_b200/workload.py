@@ -6,13 +6,16 @@ never shipped; this restates the parts the benchmark needs:
 - `chung_lu_edges`: power-law Chung-Lu graph, weights w_i ∝ (i+1)^-alpha,
   independent random permutations for the source and destination roles,
   unique directed edges (self-loops allowed), exactly m edges.
-- `rmat_edges`: R-MAT (a, b, c, d) on 2^scale ids, relabelled and trimmed.
+- `rmat_edges`: R-MAT (a, b, c, d) on 2^scale ids, relabelled, folded to n.
 - `UpdateStream`: base = first (1 - holdout) of the edges; every batch is B/2
   inserts drawn without replacement from the hold-out plus B/2 deletes drawn
   uniformly from the live edges, shuffled,
   already coalesced (no repeated (src, dst) inside a batch).
 
-Host-side setup code (numpy); not on the timed path.
+Randomness comes from a counter-based splitmix64 hash, so numpy, torch-CPU
+and torch-CUDA produce bit-identical graphs (the CPU oracle and the GPU
+engine see the same input; generation on the GPU takes ~1 s at 62M edges).
+Host-side setup code; not on the timed path.
 """
 
 from __future__ import annotations
@@ -22,59 +25,102 @@ import numpy as np
 OP_INSERT = 0
 OP_DELETE = 1
 
+_M64 = (1 << 64) - 1
+_C1, _C2, _C3 = 0x9E3779B97F4A7C15, 0xBF58476D1CE4E5B9, 0x94D049BB133111EB
 
-def _unique_fill(sample, n, m, rng, max_rounds=64):
-    """Draw key batches until m unique (src*n+dst) keys exist; keep first-seen order."""
-    keys = np.empty(0, np.uint64)
+
+def _s64(c):  # unsigned 64-bit constant as a signed int64 (torch has no uint64 arithmetic)
+    return c - (1 << 64) if c >= (1 << 63) else c
+
+
+def _hash_u53(seed: int, stream: int, start: int, count: int, device=None):
+    """splitmix64(seed, stream, index) -> uniform [0, 1) doubles (torch float64)."""
+    import torch
+
+    dev = torch.device(device) if device is not None else torch.device("cpu")
+    x = torch.arange(start, start + count, dtype=torch.int64, device=dev)
+    base = (seed * 0x100000001B3 + stream * 0x51ED27) & _M64
+    x = x + _s64((base + _C1) & _M64)
+
+    def lsr(z, k):
+        return (z >> k) & ((1 << (64 - k)) - 1)
+
+    z = x
+    z = (z ^ lsr(z, 30)) * _s64(_C2)
+    z = (z ^ lsr(z, 27)) * _s64(_C3)
+    z = z ^ lsr(z, 31)
+    return lsr(z, 11).to(torch.float64) * (1.0 / (1 << 53))
+
+
+def _perm(seed: int, stream: int, n: int, device=None):
+    import torch
+
+    return torch.argsort(_hash_u53(seed, stream, 0, n, device), stable=True)
+
+
+def _unique_fill(sample, n: int, m: int, device, max_rounds: int = 64):
+    """Draw until m unique keys src*n+dst exist; keep first-drawn order."""
+    import torch
+
+    keys = torch.empty(0, dtype=torch.int64, device=device)
+    drawn = 0
     need = m
     for _ in range(max_rounds):
-        s, d = sample(int(need * 1.15) + 1024)
-        k = s.astype(np.uint64) * np.uint64(n) + d.astype(np.uint64)
-        keys = np.concatenate([keys, k])
-        _, first = np.unique(keys, return_index=True)
-        first.sort()
-        keys = keys[first]
-        if keys.size >= m:
+        k = int(need * 1.15) + 1024
+        s, d = sample(drawn, k)
+        drawn += k
+        keys = torch.cat([keys, s * n + d])
+        uniq, inv = torch.unique(keys, return_inverse=True)
+        first = torch.full((uniq.numel(),), keys.numel(), dtype=torch.int64, device=device)
+        first.scatter_reduce_(0, inv, torch.arange(keys.numel(), device=device), reduce="amin")
+        keys = keys[torch.sort(first).values]
+        if keys.numel() >= m:
             keys = keys[:m]
             break
-        need = m - keys.size
+        need = m - keys.numel()
     else:
         raise RuntimeError(f"could not draw {m} unique edges on {n} vertices")
-    return (keys // np.uint64(n)).astype(np.int64), (keys % np.uint64(n)).astype(np.int64)
+    return keys // n, keys % n
 
 
-def chung_lu_edges(n: int, m: int, alpha: float = 0.8, seed: int = 0):
-    rng = np.random.default_rng(seed)
-    w = (np.arange(n, dtype=np.float64) + 1.0) ** (-alpha)
-    cdf = np.cumsum(w)
-    cdf /= cdf[-1]
-    perm_s = rng.permutation(n)
-    perm_d = rng.permutation(n)
+def chung_lu_edges(n: int, m: int, alpha: float = 0.8, seed: int = 0, device=None, as_numpy: bool = True):
+    import torch
 
-    def sample(k):
-        a = np.minimum(np.searchsorted(cdf, rng.random(k), side="right"), n - 1)
-        b = np.minimum(np.searchsorted(cdf, rng.random(k), side="right"), n - 1)
+    dev = torch.device(device) if device is not None else torch.device("cpu")
+    w = (torch.arange(n, dtype=torch.float64, device=dev) + 1.0) ** (-alpha)
+    cdf = torch.cumsum(w, 0)
+    cdf = cdf / cdf[-1]
+    perm_s = _perm(seed, 11, n, dev)
+    perm_d = _perm(seed, 12, n, dev)
+
+    def sample(off, k):
+        a = torch.searchsorted(cdf, _hash_u53(seed, 21, off, k, dev), right=True).clamp_(max=n - 1)
+        b = torch.searchsorted(cdf, _hash_u53(seed, 22, off, k, dev), right=True).clamp_(max=n - 1)
         return perm_s[a], perm_d[b]
 
-    return _unique_fill(sample, n, m, rng)
+    s, d = _unique_fill(sample, n, m, dev)
+    return (s.cpu().numpy(), d.cpu().numpy()) if as_numpy else (s, d)
 
 
-def rmat_edges(n: int, m: int, a=0.57, b=0.19, c=0.19, seed: int = 0):
-    rng = np.random.default_rng(seed)
+def rmat_edges(n: int, m: int, a=0.57, b=0.19, c=0.19, seed: int = 0, device=None, as_numpy: bool = True):
+    import torch
+
+    dev = torch.device(device) if device is not None else torch.device("cpu")
     scale = max(1, int(np.ceil(np.log2(max(n, 2)))))
-    cp = np.cumsum(np.array([a, b, c, 1.0 - a - b - c]))
-    perm = rng.permutation(1 << scale)  # relabel, then fold ids >= n back by modulus
+    cp = torch.tensor([a, a + b, a + b + c], dtype=torch.float64, device=dev)
+    perm = _perm(seed, 31, 1 << scale, dev)
 
-    def sample(k):
-        s = np.zeros(k, np.int64)
-        d = np.zeros(k, np.int64)
+    def sample(off, k):
+        s = torch.zeros(k, dtype=torch.int64, device=dev)
+        d = torch.zeros(k, dtype=torch.int64, device=dev)
         for bit in range(scale):
-            q = np.minimum(np.searchsorted(cp, rng.random(k), side="right"), 3)
+            q = torch.searchsorted(cp, _hash_u53(seed, 100 + bit, off, k, dev), right=True)
             s |= ((q >> 1) & 1) << bit
             d |= (q & 1) << bit
         return perm[s] % n, perm[d] % n
 
-    return _unique_fill(sample, n, m, rng)
+    s, d = _unique_fill(sample, n, m, dev)
+    return (s.cpu().numpy(), d.cpu().numpy()) if as_numpy else (s, d)
 
 
 def features(n: int, d: int, seed: int = 1) -> np.ndarray:
@@ -94,13 +140,11 @@ class UpdateStream:
         self.src_all, self.dst_all = src, dst
         nb = int(round(m * (1.0 - holdout)))
         self.base_ids = np.arange(nb)
-        self.hold_ids = np.arange(nb, m)
         self.live = np.zeros(m, bool)
         self.live[:nb] = True
         self._hold_ptr = 0
-        self._seed = seed
         self._batch = 0
-        self._hold_perm = np.random.default_rng(seed + 1_000_003).permutation(self.hold_ids)
+        self._hold_perm = np.random.default_rng(seed + 1_000_003).permutation(np.arange(nb, m))
 
     def base(self):
         ids = self.base_ids
