@@ -321,11 +321,15 @@ class DynamicGraph:
             self._ensure_ws(self.batch.cap)
         b = self.batch
         if B:
-            for dst_t, arr, dt in ((b.op, op, np.uint8), (b.src, _i32_ids(src), np.int32),
-                                   (b.dst, _i32_ids(dst), np.int32), (b.ts, ts, np.int64)):
+            for dst_t, arr, dt in ((b.op, op, np.uint8), (b.src, src, np.int32), (b.dst, dst, np.int32),
+                                   (b.ts, ts, np.int64)):
                 if isinstance(arr, torch.Tensor):
+                    if arr.dtype != dst_t.dtype:
+                        raise E.ShapeError(f"batch tensor dtype {arr.dtype} != {dst_t.dtype}")
                     dst_t[:B].copy_(arr, non_blocking=True)
                 else:
+                    if dt == np.int32:
+                        arr = _i32_ids(arr)
                     dst_t[:B].copy_(torch.from_numpy(np.ascontiguousarray(arr, dt)))
         return B
 
