@@ -79,162 +79,299 @@ __device__ __forceinline__ bool in_range_has(const int32_t* __restrict__ is, int
   return k < q && is[k] == u;
 }
 
-// ------------------------------------------------------------------ incremental aggregate (K11), non-GAT
-template <int VEC, int K>
-__global__ void __launch_bounds__(kLBlk) k_agg_inc(LayerArgs a) {
+// ------------------------------------------------------------------ aggregation (K11 incremental, K17 full)
+// Edge-balanced: destinations whose scanned in-run is <= kChunk edges are
+// handled by one warp each ("light" pass); longer runs ("heavy": hubs, up to
+// 392K in-edges at configs[1]) are cut into kChunk-edge chunks, one warp per
+// chunk, partial rows written to scratch and reduced in chunk order by the
+// last-arriving warp (deterministic; threadfence + per-vertex arrival counter).
+constexpr int kChunk = 512;
+
+template <int VEC, int K, bool FULL>
+__device__ __forceinline__ void agg_edges(const LayerArgs& a, int64_t beg, int32_t e0, int32_t e1, int64_t p,
+                                          int64_t q, RowAcc<VEC, K>& acc) {
   using R = RowAcc<VEC, K>;
-  if (err_set(a.err)) return;
-  const int64_t nd = *a.f.n_dst;
-  const int64_t ns = *a.f.n_src;
-  const int64_t na = *a.b.n_applied;
   const int d = a.d_agg;
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int lane = lane_id();
-  for (int64_t i = warp; i < nd; i += nw) {
-    int32_t v = a.f.dst_list[i];
-    int64_t p = lower_bound_dev(a.b.i_dst, 0, na, v);
-    int64_t q = lower_bound_dev(a.b.i_dst, p, na, v + 1);
-    R acc;
-    acc.zero();
-    // ValueChange edges: scan v's post-batch in-run for sources in S(l)
-    if (ns > 0) {
-      int64_t beg = a.g.in.beg[v];
-      int32_t len = a.g.in.len[v];
-      for (int32_t c0 = 0; c0 < len; c0 += 32) {
-        int32_t j = c0 + lane;
-        int32_t u = 0;
-        bool hit = false;
-        if (j < len) {
-          u = a.g.in.nbr[beg + j];
-          hit = bm_test(a.f.bm_src, u) && !in_range_has(a.b.i_src, p, q, u);
-        }
-        unsigned m = __ballot_sync(0xffffffffu, hit);
-        int32_t slot = hit ? a.f.src_slot[u] : 0;
-        while (m) {
-          int32_t sl[kUnroll];
-          int cnt = 0;
-#pragma unroll
-          for (int t = 0; t < kUnroll; ++t) {
-            sl[t] = 0;
-            if (m) {
-              int src = __ffs(m) - 1;
-              m &= m - 1;
-              sl[t] = __shfl_sync(0xffffffffu, slot, src);
-              cnt = t + 1;
-            } else {
-              __shfl_sync(0xffffffffu, slot, 0);
-            }
-          }
-          float r[kUnroll][K][VEC];
-#pragma unroll
-          for (int t = 0; t < kUnroll; ++t)
-            if (t < cnt) R::load(a.delta + static_cast<int64_t>(sl[t]) * d, d, r[t]);
-#pragma unroll
-          for (int t = 0; t < kUnroll; ++t)
-            if (t < cnt) acc.add(r[t]);
-        }
-      }
-    }
-    // structural edges of v (graph.py:202-224 applied set)
-    for (int64_t k = p; k < q; ++k) {
-      int32_t u = a.b.i_src[k];
-      float r[K][VEC];
-      if (a.b.i_op[k] == RTEC_OP_INSERT) {
-        R::load(a.st.H_in + static_cast<int64_t>(u) * d, d, r);
-        acc.fma(r, src_coeff(a.L.model, a.g.out_deg[u], a.L.degree_offset));
+  for (int32_t c0 = e0; c0 < e1; c0 += 32) {
+    int32_t j = c0 + lane;
+    int32_t u = 0;
+    bool hit = false;
+    float cu = 0.f;
+    if (j < e1) {
+      u = a.g.in.nbr[beg + j];
+      if (FULL) {
+        hit = true;
+        cu = src_coeff(a.L.model, a.g.out_deg[u], a.L.degree_offset);
       } else {
-        const float* orow = a.st.H_in + static_cast<int64_t>(u) * d;
-        if (a.prev_bm_dst && bm_test(a.prev_bm_dst, u)) orow = a.st.log_in + static_cast<int64_t>(a.prev_slot[u]) * d;
-        R::load(orow, d, r);
-        acc.fma(r, -src_coeff(a.L.model, a.g.out_deg_prev[u], a.L.degree_offset));
+        hit = bm_test(a.f.bm_src, u) && !in_range_has(a.b.i_src, p, q, u);
       }
     }
-    // S_v update, compose, GEMM input row
-    int32_t indeg = a.g.in_deg[v];
-    float* srow = a.st.S + static_cast<int64_t>(v) * d;
-    float sv[K][VEC];
-    if (indeg == 0) {
-      acc.zero();  // SPEC.md:277: empty neighbourhood -> zero aggregate
-    } else if (a.g.in_deg_prev[v] > 0) {
-      R::load_rw(srow, d, sv);
-      acc.add(sv);
+    unsigned m = __ballot_sync(0xffffffffu, hit);
+    const float* base = FULL ? a.st.H_in : a.delta;
+    int32_t row = FULL ? u : (hit ? a.f.src_slot[u] : 0);
+    while (m) {
+      int32_t rw[kUnroll];
+      float cs[kUnroll];
+      int cnt = 0;
+#pragma unroll
+      for (int t = 0; t < kUnroll; ++t) {
+        int src = m ? __ffs(m) - 1 : 0;
+        if (m) {
+          m &= m - 1;
+          cnt = t + 1;
+        }
+        rw[t] = __shfl_sync(0xffffffffu, row, src);
+        cs[t] = __shfl_sync(0xffffffffu, cu, src);
+      }
+      float r[kUnroll][K][VEC];
+#pragma unroll
+      for (int t = 0; t < kUnroll; ++t)
+        if (t < cnt) R::load(base + static_cast<int64_t>(rw[t]) * d, d, r[t]);
+#pragma unroll
+      for (int t = 0; t < kUnroll; ++t) {
+        if (t < cnt) {
+          if (FULL) acc.fma(r[t], cs[t]);
+          else acc.add(r[t]);
+        }
+      }
     }
-    acc.store(srow, d);
-    float scale = 1.f;
-    if (indeg > 0) {
-      if (a.L.model == RTEC_MODEL_GCN) scale = 1.0f / sqrtf(static_cast<float>(indeg) + a.L.degree_offset);
-      else if (a.L.model == RTEC_MODEL_SAGE) scale = 1.0f / static_cast<float>(indeg);
-    }
-    R out;
-    out.zero();
-    out.fma(acc.v, scale);
-    if (a.L.model == RTEC_MODEL_GIN) {  // update input h_v + a_v (models.py:187-189)
-      float h[K][VEC];
-      R::load(a.st.H_in + static_cast<int64_t>(v) * d, d, h);
-      out.add(h);
-    }
-    out.store(a.st.gemm_in + i * d, d);
   }
 }
 
-// ------------------------------------------------------------------ full aggregate (K17), non-GAT
-// rows == null: all vertices, output row i = v.  Else rows[i].
+// structural edges of v (graph.py:202-224 applied set): + c_new h_new for I, - c_old h_old for D
 template <int VEC, int K>
-__global__ void __launch_bounds__(kLBlk) k_agg_full(LayerArgs a, const int32_t* rows, const int64_t* n_rows,
-                                                    int64_t n_all) {
+__device__ __forceinline__ void agg_struct(const LayerArgs& a, int64_t p, int64_t q, RowAcc<VEC, K>& acc) {
   using R = RowAcc<VEC, K>;
-  const int64_t nr = rows ? *n_rows : n_all;
+  const int d = a.d_agg;
+  for (int64_t k = p; k < q; ++k) {
+    int32_t u = a.b.i_src[k];
+    float r[K][VEC];
+    if (a.b.i_op[k] == RTEC_OP_INSERT) {
+      R::load(a.st.H_in + static_cast<int64_t>(u) * d, d, r);
+      acc.fma(r, src_coeff(a.L.model, a.g.out_deg[u], a.L.degree_offset));
+    } else {
+      const float* orow = a.st.H_in + static_cast<int64_t>(u) * d;
+      if (a.prev_bm_dst && bm_test(a.prev_bm_dst, u)) orow = a.st.log_in + static_cast<int64_t>(a.prev_slot[u]) * d;
+      R::load(orow, d, r);
+      acc.fma(r, -src_coeff(a.L.model, a.g.out_deg_prev[u], a.L.degree_offset));
+    }
+  }
+}
+
+// S_v update (INC: S += Σ, zero-in-degree rule; FULL: S = Σ), compose, GEMM input row i
+template <int VEC, int K, bool FULL>
+__device__ __forceinline__ void agg_finalize(const LayerArgs& a, int64_t i, int32_t v, int32_t len,
+                                             RowAcc<VEC, K>& acc) {
+  using R = RowAcc<VEC, K>;
+  const int d = a.d_agg;
+  float* srow = a.st.S + static_cast<int64_t>(v) * d;
+  int32_t indeg = FULL ? len : a.g.in_deg[v];
+  if (!FULL) {
+    if (indeg == 0) {
+      acc.zero();  // SPEC.md:277: empty neighbourhood -> zero aggregate
+    } else if (a.g.in_deg_prev[v] > 0) {
+      float sv[K][VEC];
+      R::load_rw(srow, d, sv);
+      acc.add(sv);
+    }
+  }
+  acc.store(srow, d);
+  float scale = 1.f;
+  if (indeg > 0) {
+    if (a.L.model == RTEC_MODEL_GCN) scale = 1.0f / sqrtf(static_cast<float>(indeg) + a.L.degree_offset);
+    else if (a.L.model == RTEC_MODEL_SAGE) scale = 1.0f / static_cast<float>(indeg);
+  }
+  R out;
+  out.zero();
+  out.fma(acc.v, scale);
+  if (a.L.model == RTEC_MODEL_GIN) {  // update input h_v + a_v (models.py:187-189)
+    float h[K][VEC];
+    R::load(a.st.H_in + static_cast<int64_t>(v) * d, d, h);
+    out.add(h);
+  }
+  out.store(a.st.gemm_in + i * d, d);
+}
+
+struct AggRows {
+  const int32_t* list;  // null -> identity
+  const int64_t* n_dev; // null -> n_all
+  int64_t n_all;
+  __device__ __forceinline__ int64_t count() const { return n_dev ? *n_dev : n_all; }
+  __device__ __forceinline__ int32_t at(int64_t i) const { return list ? list[i] : static_cast<int32_t>(i); }
+};
+
+struct HeavyPlan {
+  int32_t* heavy;   // dst indices i of heavy destinations
+  int64_t* n_heavy; // [1]
+  int64_t* hoff;    // [n_heavy + 1] chunk offsets
+  int32_t* cmap;    // chunk -> heavy index j
+  int32_t* arrive;  // [n_heavy] arrival counters (zeroed per launch)
+  float* part;      // [chunks, d] partial rows
+};
+
+template <int VEC, int K, bool FULL>
+__global__ void __launch_bounds__(kLBlk) k_agg_light(LayerArgs a, AggRows rows) {
+  using R = RowAcc<VEC, K>;
+  if (!FULL && err_set(a.err)) return;
+  const int64_t nr = rows.count();
+  const bool scan = FULL || *a.f.n_src > 0;
+  const int64_t na = FULL ? 0 : *a.b.n_applied;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < nr; i += nw) {
+    int32_t v = rows.at(i);
+    int32_t len = a.g.in.len[v];
+    if (scan && len > kChunk) continue;  // heavy pass
+    int64_t p = 0, q = 0;
+    if (!FULL) {
+      p = lower_bound_dev(a.b.i_dst, 0, na, v);
+      q = lower_bound_dev(a.b.i_dst, p, na, v + 1);
+    }
+    R acc;
+    acc.zero();
+    if (scan) agg_edges<VEC, K, FULL>(a, a.g.in.beg[v], 0, len, p, q, acc);
+    if (!FULL) agg_struct<VEC, K>(a, p, q, acc);
+    agg_finalize<VEC, K, FULL>(a, i, v, len, acc);
+  }
+}
+
+template <int VEC, int K, bool FULL>
+__global__ void __launch_bounds__(kLBlk) k_agg_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
+  using R = RowAcc<VEC, K>;
+  if (!FULL && err_set(a.err)) return;
+  const int64_t nh = *hp.n_heavy;
+  if (nh == 0) return;
+  const int64_t T = hp.hoff[nh];
+  const int64_t na = FULL ? 0 : *a.b.n_applied;
   const int d = a.d_agg;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int lane = lane_id();
-  for (int64_t i = warp; i < nr; i += nw) {
-    int32_t v = rows ? rows[i] : static_cast<int32_t>(i);
-    int64_t beg = a.g.in.beg[v];
+  for (int64_t t = warp; t < T; t += nw) {
+    int32_t j = hp.cmap[t];
+    int64_t c0 = hp.hoff[j];
+    int32_t nch = static_cast<int32_t>(hp.hoff[j + 1] - c0);
+    int32_t c = static_cast<int32_t>(t - c0);
+    int64_t i = hp.heavy[j];
+    int32_t v = rows.at(i);
     int32_t len = a.g.in.len[v];
+    int64_t p = 0, q = 0;
+    if (!FULL) {
+      p = lower_bound_dev(a.b.i_dst, 0, na, v);
+      q = lower_bound_dev(a.b.i_dst, p, na, v + 1);
+    }
     R acc;
     acc.zero();
-    for (int32_t c0 = 0; c0 < len; c0 += 32) {
-      int32_t j = c0 + lane;
-      int32_t u = 0;
-      float cu = 0.f;
-      if (j < len) {
-        u = a.g.in.nbr[beg + j];
-        cu = src_coeff(a.L.model, a.g.out_deg[u], a.L.degree_offset);
-      }
-      int cnt_all = min(32, len - c0);
-      for (int t0 = 0; t0 < cnt_all; t0 += kUnroll) {
-        float r[kUnroll][K][VEC];
-        float cs[kUnroll];
+    int32_t e0 = c * kChunk, e1 = min(len, e0 + kChunk);
+    agg_edges<VEC, K, FULL>(a, a.g.in.beg[v], e0, e1, p, q, acc);
+    if (!FULL && c == 0) agg_struct<VEC, K>(a, p, q, acc);
+    acc.store(hp.part + t * d, d);
+    __threadfence();
+    int old = 0;
+    if (lane_id() == 0) old = atomicAdd(hp.arrive + j, 1);
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old != nch - 1) continue;
+    __threadfence();
+    acc.zero();
+    for (int32_t cc = 0; cc < nch; ++cc) {  // chunk order: deterministic sum
 #pragma unroll
-        for (int t = 0; t < kUnroll; ++t) {
-          int src = t0 + t;
-          int32_t uu = __shfl_sync(0xffffffffu, u, src & 31);
-          cs[t] = __shfl_sync(0xffffffffu, cu, src & 31);
-          if (src < cnt_all) R::load(a.st.H_in + static_cast<int64_t>(uu) * d, d, r[t]);
+      for (int k = 0; k < K; ++k) {
+        int col = lane_id() + 32 * k;
+        if (col * VEC < d) {
+          const float* src = hp.part + (c0 + cc) * d + col * VEC;
+#pragma unroll
+          for (int jj = 0; jj < VEC; ++jj) acc.v[k][jj] += __ldcg(src + jj);
         }
-#pragma unroll
-        for (int t = 0; t < kUnroll; ++t)
-          if (t0 + t < cnt_all) acc.fma(r[t], cs[t]);
       }
     }
-    acc.store(a.st.S + static_cast<int64_t>(v) * d, d);
-    float scale = 1.f;
-    if (len > 0) {
-      if (a.L.model == RTEC_MODEL_GCN) scale = 1.0f / sqrtf(static_cast<float>(len) + a.L.degree_offset);
-      else if (a.L.model == RTEC_MODEL_SAGE) scale = 1.0f / static_cast<float>(len);
-    }
-    R out;
-    out.zero();
-    out.fma(acc.v, scale);
-    if (a.L.model == RTEC_MODEL_GIN) {
-      float h[K][VEC];
-      R::load(a.st.H_in + static_cast<int64_t>(v) * d, d, h);
-      out.add(h);
-    }
-    out.store(a.st.gemm_in + i * d, d);
+    agg_finalize<VEC, K, FULL>(a, i, v, len, acc);
   }
+}
+
+// heavy-destination planning: list, chunk offsets, chunk -> heavy map
+struct HeavyFlagF {
+  AggRows rows;
+  const int32_t* len;
+  const int64_t* n_src;  // null in FULL mode
+  __device__ __forceinline__ int64_t operator()(int64_t i) const {
+    if (n_src && *n_src == 0) return 0;
+    return len[rows.at(i)] > kChunk ? 1 : 0;
+  }
+};
+struct HeavyStore {
+  HeavyFlagF f;
+  int32_t* heavy;
+  __device__ __forceinline__ void operator()(int64_t i, int64_t off, int64_t v) const {
+    if (v) heavy[off] = static_cast<int32_t>(i);
+  }
+};
+struct HeavyChunks {
+  AggRows rows;
+  const int32_t* len;
+  const int32_t* heavy;
+  __device__ __forceinline__ int64_t operator()(int64_t j) const {
+    return (len[rows.at(heavy[j])] + kChunk - 1) / kChunk;
+  }
+};
+struct StoreOffTailL {
+  int64_t* dst;
+  const int64_t* n;
+  __device__ __forceinline__ void operator()(int64_t i, int64_t off, int64_t v) const {
+    dst[i] = off;
+    if (i == *n - 1) dst[i + 1] = off + v;
+  }
+};
+
+__global__ void k_chunk_map(HeavyPlan hp) {
+  int64_t nh = *hp.n_heavy;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = warp; j < nh; j += nw) {
+    int64_t c0 = hp.hoff[j], c1 = hp.hoff[j + 1];
+    for (int64_t c = c0 + lane_id(); c < c1; c += 32) hp.cmap[c] = static_cast<int32_t>(j);
+    if (lane_id() == 0) hp.arrive[j] = 0;
+  }
+}
+
+// plan + light + heavy launches for one aggregation
+template <bool FULL>
+static int launch_aggregation(LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_edges, Ws& w,
+                              cudaStream_t s) {
+  const int d = a.d_agg;
+  HeavyPlan hp{};
+  hp.heavy = w.alloc<int32_t>(max_rows + 1);
+  hp.n_heavy = w.alloc<int64_t>(2);
+  hp.hoff = w.alloc<int64_t>(max_rows + 2);
+  int64_t max_chunks = max_edges / kChunk + 2 + max_rows / 64;
+  hp.cmap = w.alloc<int32_t>(max_chunks);
+  hp.arrive = w.alloc<int32_t>(max_rows + 1);
+  hp.part = w.alloc<float>(max_chunks * static_cast<int64_t>(d));
+  RTEC_WS_CHECK(w);
+  RTEC_CUDA(cudaMemsetAsync(hp.n_heavy, 0, sizeof(int64_t) * 2, s));
+  RTEC_CUDA(cudaMemsetAsync(hp.hoff, 0, sizeof(int64_t), s));
+  HeavyFlagF hf{rows, a.g.in.len, FULL ? nullptr : a.f.n_src};
+  Count cnt{rows.n_dev, max_rows};
+  if (!rows.n_dev) cnt = Count{nullptr, rows.n_all};
+  RTEC_TRY(exclusive_scan(hf, cnt, max_rows, HeavyStore{hf, hp.heavy}, hp.n_heavy, w, s));
+  RTEC_TRY(exclusive_scan(HeavyChunks{rows, a.g.in.len, hp.heavy}, Count{hp.n_heavy, max_rows}, max_rows,
+                          StoreOffTailL{hp.hoff, hp.n_heavy}, nullptr, w, s));
+  k_chunk_map<<<kSMs * 4, kLBlk, 0, s>>>(hp);
+  const int grid = kSMs * 8;
+  bool ok;
+  {
+    RTEC_PROF(FULL ? "k_agg_full_light" : "k_agg_inc", s);
+    ok = RTEC_ROW_DISPATCH(d, (k_agg_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows)));
+  }
+  {
+    RTEC_PROF(FULL ? "k_agg_full_heavy" : "k_agg_inc_heavy", s);
+    ok = ok && RTEC_ROW_DISPATCH(d, (k_agg_heavy<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows, hp)));
+  }
+  if (!ok) {
+    set_error("row width %d unsupported", d);
+    return RTEC_SHAPE_ERROR;
+  }
+  RTEC_LAUNCH_CHECK("aggregation");
+  return RTEC_OK;
 }
 
 // ------------------------------------------------------------------ GAT (K13-K15)
@@ -598,15 +735,11 @@ int rtec_layer_incremental(const rtec_graph_t* g, const rtec_batch_t* b, const r
     RTEC_PROF("k_src_delta", s);
     ok = RTEC_ROW_DISPATCH(L->d_in, (k_src_delta<VEC, K><<<grid, kLBlk, 0, s>>>(a, delta)));
   }
-  {
-    RTEC_PROF("k_agg_inc", s);
-    ok = ok && RTEC_ROW_DISPATCH(L->d_in, (k_agg_inc<VEC, K><<<grid, kLBlk, 0, s>>>(a)));
-  }
   if (!ok) {
     set_error("row width %d unsupported", L->d_in);
     return RTEC_SHAPE_ERROR;
   }
-  RTEC_LAUNCH_CHECK("k_agg_inc");
+  RTEC_TRY(launch_aggregation<false>(a, AggRows{f->dst_list, f->n_dst, n}, n, g->in.slots, w, s));
   // update on V_dst(l) rows with DeltaLog capture (operators.py:180)
   if (L->model == RTEC_MODEL_GIN) {
     GemmArgs g1{st->gemm_in, L->d_in, nullptr, L->W, L->d_in, L->d_out, f->n_dst, n, 1,
@@ -665,12 +798,10 @@ int rtec_layer_full(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* 
   }
   a.d_agg = L->d_in;
   int64_t mr = rows ? max_rows : n;
-  bool ok = RTEC_ROW_DISPATCH(L->d_in, (k_agg_full<VEC, K><<<grid, kLBlk, 0, s>>>(a, rows, n_rows, n)));
-  if (!ok) {
-    set_error("row width %d unsupported", L->d_in);
-    return RTEC_SHAPE_ERROR;
+  {
+    Ws w(ws, ws_bytes);
+    RTEC_TRY(launch_aggregation<true>(a, AggRows{rows, rows ? n_rows : nullptr, n}, mr, g->in.slots, w, s));
   }
-  RTEC_LAUNCH_CHECK("k_agg_full");
   const int64_t* nr = rows ? n_rows : nullptr;
   if (L->model == RTEC_MODEL_GIN) {
     GemmArgs g1{st->gemm_in, L->d_in, nullptr, L->W, L->d_in, L->d_out, nr, mr, 1, st->gemm_mid, L->d_out, nullptr, nullptr, nullptr};
