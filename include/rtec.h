@@ -124,6 +124,11 @@ typedef struct {
   const float* W;      /* [d_out, d_in] row-major (GAT: heads stacked [heads*dh, d_in]) */
   const float* W2;     /* GIN second matrix [d_out, d_out] (models.py:181) */
   const float* att;    /* GAT attention [heads, 2*dh] (dst half first, models.py:266-271) */
+  /* tcgen05 3xTF32 operand images of W / W2 from rtec_gemm_prepare_weights
+   * (NULL -> SIMT fp32 update).  With them set, state.gemm_in / gemm_mid hold
+   * the SW128 tile image: ceil(rows/128)*128 x ceil(d/32)*32 floats. */
+  const float* Wt_hi; const float* Wt_lo;
+  const float* W2t_hi; const float* W2t_lo;
 } rtec_layer_t;
 
 /* Per-layer cached state (SPEC.md:355-419 state_cache; stored un-normalised):
@@ -220,6 +225,11 @@ int rtec_update_gemm(const float* X, int64_t ldx, const float* W, int32_t d_in, 
                      const int64_t* n_rows, int64_t max_rows, int32_t act, float* Y, int64_t ldy,
                      const int32_t* scatter_rows, float* scatter_dst, float* log_dst,
                      rtec_stream_t stream);
+
+/* Split + swizzle W[d_out, d_in] for the tcgen05 update GEMM: Bhi/Blo each
+ * ceil(d_in/32) * round_up(d_out,16) * 32 floats.  d_out <= 256. */
+int rtec_gemm_prepare_weights(const float* W, int32_t d_in, int32_t d_out, float* Bhi, float* Blo,
+                              rtec_stream_t stream);
 
 /* materialize / query final-layer rows (SPEC materialize_h SPEC.md:379). */
 int rtec_query(const float* H, int64_t d, const int32_t* ids, int64_t k, float* out, int32_t n,

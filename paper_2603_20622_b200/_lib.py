@@ -61,6 +61,7 @@ class Layer(C.Structure):
     _fields_ = [
         ("model", I32), ("d_in", I32), ("d_out", I32), ("heads", I32),
         ("degree_offset", F32), ("pad", I32), ("W", P), ("W2", P), ("att", P),
+        ("Wt_hi", P), ("Wt_lo", P), ("W2t_hi", P), ("W2t_lo", P),
     ]
 
 
@@ -90,6 +91,7 @@ _SIGS = {
     "rtec_gat_project": (C.c_int, [C.POINTER(Layer), P, P, P, I64, P, P, P, P, P, P, P]),
     "rtec_update_gemm": (C.c_int, [P, I64, P, I32, I32, P, I64, I32, P, I64, P, P, P, P]),
     "rtec_query": (C.c_int, [P, I64, P, I64, P, I32, P, P]),
+    "rtec_gemm_prepare_weights": (C.c_int, [P, I32, I32, P, P, P]),
     "rtec_struct_sizes": (None, [C.POINTER(I64)]),
     "rtec_prof_enable": (None, [C.c_int]),
     "rtec_prof_report": (SZ, [C.c_char_p, SZ, C.c_int]),

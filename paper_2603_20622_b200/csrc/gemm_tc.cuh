@@ -1,0 +1,29 @@
+// gemm_tc.cuh -- launcher interface of the tcgen05 3xTF32 update GEMM (gemm_tc.cu).
+#pragma once
+#include "common.cuh"
+
+namespace rtec {
+
+struct TcArgs {
+  const float* A;    // [tiles][nkb][128][32] SW128-swizzled A image
+  const float* Bhi;  // [nkb][npad][32] swizzled weights (tf32 hi / lo)
+  const float* Blo;
+  int nkb, npad, d_out;
+  const int64_t* n_rows;  // device row count (or null -> max_rows)
+  int64_t max_rows;
+  int act;                // 0 none, 1 relu
+  float* Y;               // row-major output (scattered by y_rows) ...
+  int64_t ldy;
+  const int32_t* y_rows;
+  float* log;             // DeltaLog of overwritten Y rows (or null)
+  float* Yt;              // ... or a tile-layout output feeding a chained GEMM
+  int nkb_out;
+  const uint64_t* err;
+};
+
+int gemm_tc_launch(const TcArgs& g, cudaStream_t s);
+
+__host__ __device__ __forceinline__ int tc_nkb_of(int d) { return (d + 31) / 32; }
+__host__ __device__ __forceinline__ int tc_npad_of(int d) { return (d + 15) / 16 * 16; }
+
+}  // namespace rtec

@@ -17,6 +17,7 @@
 // neighbourhood (models.py:431-458).
 #include "prims.cuh"
 #include "rowops.cuh"
+#include "gemm_tc.cuh"
 
 namespace rtec {
 
@@ -40,6 +41,7 @@ struct LayerArgs {
   const int32_t* prev_slot;     // vertex -> DeltaLog row of the previous layer
   const float* delta;           // [n_src, d_agg] δ rows (non-GAT)
   int d_agg;
+  int tc_nkb;                   // > 0: gemm_in is the tcgen05 A image with tc_nkb K-blocks
   int layer;
   uint64_t* err;
 };
@@ -190,7 +192,8 @@ __device__ __forceinline__ void agg_finalize(const LayerArgs& a, int64_t i, int3
     R::load(a.st.H_in + static_cast<int64_t>(v) * d, d, h);
     out.add(h);
   }
-  out.store(a.st.gemm_in + i * d, d);
+  if (a.tc_nkb > 0) out.store_tiled(a.st.gemm_in, i, d, a.tc_nkb);
+  else out.store(a.st.gemm_in + i * d, d);
 }
 
 struct AggRows {
@@ -637,6 +640,8 @@ __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs g) {
   }
 }
 
+
+
 int gemm_launch(const GemmArgs& g, cudaStream_t s) {
   if (g.max_rows <= 0) return RTEC_OK;
   dim3 grid(static_cast<unsigned>((g.max_rows + kGM - 1) / kGM), static_cast<unsigned>((g.d_out + kGN - 1) / kGN));
@@ -665,6 +670,11 @@ __global__ void k_query(const float* __restrict__ H, int64_t d, const int32_t* _
 
 using namespace rtec;
 
+// update (and GIN's chained MLP) on rows of gemm_in: tcgen05 3xTF32 when the
+// layer carries prepared weights, SIMT fp32 otherwise
+static int run_update(const rtec_layer_t* L, rtec_state_t* st, const int64_t* n_rows, int64_t max_rows,
+                      const int32_t* y_rows, float* log, const uint64_t* err, cudaStream_t s);
+
 static int layer_dims_ok(const rtec_layer_t* L) {
   if (L->model < 0 || L->model > 3) {
     set_error("unsupported model id %d", L->model);
@@ -675,6 +685,36 @@ static int layer_dims_ok(const rtec_layer_t* L) {
     return RTEC_SHAPE_ERROR;
   }
   return RTEC_OK;
+}
+
+static int run_update(const rtec_layer_t* L, rtec_state_t* st, const int64_t* n_rows, int64_t max_rows,
+                      const int32_t* y_rows, float* log, const uint64_t* err, cudaStream_t s) {
+  if (L->Wt_hi) {
+    const int nkb = tc_nkb_of(L->d_in);
+    if (L->model == RTEC_MODEL_GIN) {  // W2 relu(W (h + a)) (models.py:187-189), hidden kept in tile layout
+      const int nkb2 = tc_nkb_of(L->d_out);
+      TcArgs t1{st->gemm_in, L->Wt_hi, L->Wt_lo, nkb, tc_npad_of(L->d_out), L->d_out, n_rows, max_rows, 1,
+                nullptr, 0, nullptr, nullptr, st->gemm_mid, nkb2, err};
+      RTEC_TRY(gemm_tc_launch(t1, s));
+      TcArgs t2{st->gemm_mid, L->W2t_hi, L->W2t_lo, nkb2, tc_npad_of(L->d_out), L->d_out, n_rows, max_rows, 0,
+                st->H_out, L->d_out, y_rows, log, nullptr, 0, err};
+      return gemm_tc_launch(t2, s);
+    }
+    TcArgs t{st->gemm_in, L->Wt_hi, L->Wt_lo, nkb, tc_npad_of(L->d_out), L->d_out, n_rows, max_rows, 1,
+             st->H_out, L->d_out, y_rows, log, nullptr, 0, err};
+    return gemm_tc_launch(t, s);
+  }
+  if (L->model == RTEC_MODEL_GIN) {
+    GemmArgs g1{st->gemm_in, L->d_in, nullptr, L->W, L->d_in, L->d_out, n_rows, max_rows, 1,
+                st->gemm_mid, L->d_out, nullptr, nullptr, err};
+    RTEC_TRY(gemm_launch(g1, s));
+    GemmArgs g2{st->gemm_mid, L->d_out, nullptr, L->W2, L->d_out, L->d_out, n_rows, max_rows, 0,
+                st->H_out, L->d_out, y_rows, log, err};
+    return gemm_launch(g2, s);
+  }
+  GemmArgs g1{st->gemm_in, L->d_in, nullptr, L->W, L->d_in, L->d_out, n_rows, max_rows, 1,
+              st->H_out, L->d_out, y_rows, log, err};
+  return gemm_launch(g1, s);
 }
 
 extern "C" {
@@ -739,20 +779,12 @@ int rtec_layer_incremental(const rtec_graph_t* g, const rtec_batch_t* b, const r
     set_error("row width %d unsupported", L->d_in);
     return RTEC_SHAPE_ERROR;
   }
+  a.tc_nkb = L->Wt_hi ? tc_nkb_of(L->d_in) : 0;
   RTEC_TRY(launch_aggregation<false>(a, AggRows{f->dst_list, f->n_dst, n}, n, g->in.slots, w, s));
   // update on V_dst(l) rows with DeltaLog capture (operators.py:180)
-  if (L->model == RTEC_MODEL_GIN) {
-    GemmArgs g1{st->gemm_in, L->d_in, nullptr, L->W, L->d_in, L->d_out, f->n_dst, n, 1,
-                st->gemm_mid, L->d_out, nullptr, nullptr, err};
-    RTEC_TRY(gemm_launch(g1, s));
-    GemmArgs g2{st->gemm_mid, L->d_out, nullptr, L->W2, L->d_out, L->d_out, f->n_dst, n, 0,
-                st->H_out, L->d_out, f->dst_list, st->log_out, err};
-    return gemm_launch(g2, s);
-  }
-  GemmArgs g1{st->gemm_in, L->d_in, nullptr, L->W, L->d_in, L->d_out, f->n_dst, n, 1,
-              st->H_out, L->d_out, f->dst_list, st->log_out, err};
-  return gemm_launch(g1, s);
+  return run_update(L, st, f->n_dst, n, f->dst_list, st->log_out, err, s);
 }
+
 
 int rtec_layer_full(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* st, const int32_t* rows,
                     const int64_t* n_rows, int64_t max_rows, uint64_t* err, void* ws, size_t ws_bytes,
@@ -797,20 +829,13 @@ int rtec_layer_full(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* 
     return RTEC_OK;
   }
   a.d_agg = L->d_in;
+  a.tc_nkb = L->Wt_hi ? tc_nkb_of(L->d_in) : 0;
   int64_t mr = rows ? max_rows : n;
   {
     Ws w(ws, ws_bytes);
     RTEC_TRY(launch_aggregation<true>(a, AggRows{rows, rows ? n_rows : nullptr, n}, mr, g->in.slots, w, s));
   }
-  const int64_t* nr = rows ? n_rows : nullptr;
-  if (L->model == RTEC_MODEL_GIN) {
-    GemmArgs g1{st->gemm_in, L->d_in, nullptr, L->W, L->d_in, L->d_out, nr, mr, 1, st->gemm_mid, L->d_out, nullptr, nullptr, nullptr};
-    RTEC_TRY(gemm_launch(g1, s));
-    GemmArgs g2{st->gemm_mid, L->d_out, nullptr, L->W2, L->d_out, L->d_out, nr, mr, 0, st->H_out, L->d_out, rows, nullptr, nullptr};
-    return gemm_launch(g2, s);
-  }
-  GemmArgs g1{st->gemm_in, L->d_in, nullptr, L->W, L->d_in, L->d_out, nr, mr, 1, st->H_out, L->d_out, rows, nullptr, nullptr};
-  return gemm_launch(g1, s);
+  return run_update(L, st, rows ? n_rows : nullptr, mr, rows, nullptr, nullptr, s);
 }
 
 int rtec_gat_project(const rtec_layer_t* L, const float* H, const int32_t* rows, const int64_t* n_rows,

@@ -87,6 +87,31 @@ struct RowAcc {
       }
     }
   }
+  // Row i into the tcgen05 A-operand image: [tile][kb][128][32] with the
+  // SW128 16-byte-chunk XOR swizzle; columns d .. nkb*32 are zero padding.
+  __device__ __forceinline__ void store_tiled(float* A, int64_t i, int d, int nkb) const {
+    const int64_t tile = i >> 7;
+    const int r = static_cast<int>(i & 127);
+    float* tbase = A + tile * static_cast<int64_t>(nkb) * 4096;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      int c = (lane_id() + 32 * k) * VEC;
+      if (c < d) {
+        int kb = c >> 5, cc = c & 31;
+        float* blk = tbase + kb * 4096 + r * 32;
+        if constexpr (VEC == 4) {
+          *reinterpret_cast<float4*>(blk + ((((cc >> 2) ^ (r & 7)) << 2))) =
+              make_float4(v[k][0], v[k][1], v[k][2], v[k][3]);
+        } else {
+          blk[(((cc >> 2) ^ (r & 7)) << 2) | (cc & 3)] = v[k][0];
+        }
+      }
+    }
+    for (int c = d + lane_id(); c < nkb * 32; c += 32) {  // zero padding
+      int kb = c >> 5, cc = c & 31;
+      tbase[kb * 4096 + r * 32 + ((((cc >> 2) ^ (r & 7)) << 2) | (cc & 3))] = 0.f;
+    }
+  }
 };
 
 // dispatch (VEC, K) from the row width; returns false if unsupported

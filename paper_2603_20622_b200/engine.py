@@ -72,7 +72,8 @@ class _Frontier:
 class RTECEngine:
     """B200 incremental engine over a DynamicGraph and an operator Bundle."""
 
-    def __init__(self, bundle: Bundle, graph: DynamicGraph, features, *, max_batch: int | None = None):
+    def __init__(self, bundle: Bundle, graph: DynamicGraph, features, *, max_batch: int | None = None,
+                 update: str = "tc"):
         if not isinstance(bundle, Bundle) or bundle.model not in MODELS:
             raise E.UnsupportedModel("engine needs a bundle from paper_2603_20622_b200.models")
         self.b = bundle
@@ -92,18 +93,28 @@ class RTECEngine:
         self.S, self.ctx, self.log = [], [], []
         self.Z, self.el, self.er, self.Zlog, self.erlog = [], [], [], [], []
         heads = bundle.heads
+        # tcgen05 3xTF32 update (gemm_tc.cu) for every dense update with d_out <= 256
+        self.tc = update == "tc" and bundle.model != GAT and max(dims[1:]) <= 256
         for l, w in enumerate(bundle.layers):
             d_in, d_out = w.in_dim, w.out_dim
             W = torch.as_tensor(np.asarray(w.tensors["W"], np.float32), device=self.dev).contiguous()
             W2 = torch.as_tensor(np.asarray(w.tensors["W2"], np.float32), device=self.dev).contiguous() if bundle.model == GIN else None
             att = torch.as_tensor(np.asarray(w.tensors["a"], np.float32).reshape(heads, -1), device=self.dev).contiguous() if bundle.model == GAT else None
-            self.wt.append((W, W2, att))
+            tcw = [None, None, None, None]
+            if self.tc:
+                tcw[0], tcw[1] = self._prep_weights(W, d_in, d_out)
+                if W2 is not None:
+                    tcw[2], tcw[3] = self._prep_weights(W2, d_out, d_out)
+            self.wt.append((W, W2, att, *tcw))
+            p = _lib.ptr
             self.layers.append(_lib.Layer(_MODEL_ID[bundle.model], d_in, d_out, heads if bundle.model == GAT else 1,
-                                          float(bundle.degree_offset), 0, _lib.ptr(W), _lib.ptr(W2), _lib.ptr(att)))
+                                          float(bundle.degree_offset), 0, p(W), p(W2), p(att),
+                                          p(tcw[0]), p(tcw[1]), p(tcw[2]), p(tcw[3])))
             d_agg = bundle.agg_dims[l]
             self.H.append(z(n, d_out))
             self.S.append(z(n, d_agg))
-            self.log.append(z(n, d_out))
+            # DeltaLog of this layer's output; the final layer's is never read (no layer L+1)
+            self.log.append(z(n, d_out) if l + 1 < bundle.num_layers else None)
             if bundle.model == GAT:
                 self.ctx.append(z(n, heads))
                 self.Z.append(z(n, d_out))
@@ -116,13 +127,27 @@ class RTECEngine:
                 for lst in (self.Z, self.el, self.er, self.Zlog, self.erlog):
                     lst.append(None)
         self.max_dim = max(max(dims), 1)
-        self.gemm_in = z(n, max(bundle.agg_dims)) if bundle.model != GAT else None
-        self.gemm_mid = z(n, max(dims[1:])) if bundle.model == GIN else None
+        if self.tc:  # SW128 tile image: ceil(n/128)*128 rows x ceil(d/32)*32 columns
+            rows = (n + 127) // 128 * 128
+            pad = lambda d: (d + 31) // 32 * 32  # noqa: E731
+            self.gemm_in = z(rows * pad(max(bundle.agg_dims)))
+            self.gemm_mid = z(rows * pad(max(dims[1:]))) if bundle.model == GIN else None
+        else:
+            self.gemm_in = z(n, max(bundle.agg_dims)) if bundle.model != GAT else None
+            self.gemm_mid = z(n, max(dims[1:])) if bundle.model == GIN else None
         self.fr = [_Frontier(n, self.dev) for _ in range(self.L)]
         self._ensure_ws(max_batch or graph.batch.cap)
         self.bootstrap()
 
     # ---------------------------------------------------------------- plumbing
+    def _prep_weights(self, W, d_in, d_out):
+        nkb, npad = (d_in + 31) // 32, (d_out + 15) // 16 * 16
+        hi = torch.zeros(nkb * npad * 32, dtype=torch.float32, device=self.dev)
+        lo = torch.zeros_like(hi)
+        _lib.check(self.lib.rtec_gemm_prepare_weights(_lib.ptr(W), d_in, d_out, _lib.ptr(hi), _lib.ptr(lo),
+                                                      _lib.stream_handle()), "prepare_weights")
+        return hi, lo
+
     def _ensure_ws(self, B):
         need = int(self.lib.rtec_workspace_bytes(self.n, max(int(B), 1), max(self.g.out.slots, self.g.inn.slots),
                                                  self.max_dim))

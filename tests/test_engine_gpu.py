@@ -65,7 +65,7 @@ def test_golden_models(P, case):
         _check_against(eng, z, f"b{bi}", L)
 
 
-def _run_vs_oracle(P, model, dims, n, m, B, nb, seed, heads=1, smoothing=True):
+def _run_vs_oracle(P, model, dims, n, m, B, nb, seed, heads=1, smoothing=True, update="tc"):
     from oracle import models as OM
     from oracle.engine import OracleEngine
     from oracle.graph import OracleGraph
@@ -76,7 +76,7 @@ def _run_vs_oracle(P, model, dims, n, m, B, nb, seed, heads=1, smoothing=True):
     bs, bd, bt = stream.base()
     X = features(n, dims[0], seed=seed + 1)
     g = P.DynamicGraph.from_edges(n, (bs, bd, bt))
-    eng = P.RTECEngine(P.make_bundle(model, dims, heads=heads, degree_smoothing=smoothing), g, X)
+    eng = P.RTECEngine(P.make_bundle(model, dims, heads=heads, degree_smoothing=smoothing), g, X, update=update)
     oe = OracleEngine(OM.make_bundle(model, dims, heads=heads, degree_smoothing=smoothing),
                       OracleGraph.from_edges(n, bs, bd, bt), X.astype(np.float64))
     L = len(dims) - 1
@@ -103,6 +103,17 @@ def _run_vs_oracle(P, model, dims, n, m, B, nb, seed, heads=1, smoothing=True):
                                         ("gat", [40, 32, 32])])
 def test_engine_vs_oracle(P, model, dims):
     _run_vs_oracle(P, model, dims, n=4000, m=60000, B=400, nb=4, seed=3)
+
+
+@pytest.mark.parametrize("model", ["gcn", "gin"])
+def test_engine_simt_update_path(P, model):
+    # the SIMT fp32 update (used for d_out > 256 and GAT projections) stays parity-green
+    _run_vs_oracle(P, model, [32, 48, 16], n=3000, m=30000, B=300, nb=2, seed=4, update="simt")
+
+
+def test_tc_gemm_wide_and_padded(P):
+    # d_in not a multiple of 32 (K padding), d_out not a multiple of 16 (N padding), 256-wide N
+    _run_vs_oracle(P, "graphsage", [100, 256, 40], n=3000, m=30000, B=300, nb=2, seed=13)
 
 
 def test_engine_vs_oracle_gat_heads(P):
