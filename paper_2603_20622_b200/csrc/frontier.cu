@@ -77,12 +77,19 @@ struct StoreOffTailF {
   }
 };
 
-// edge-balanced expansion of the new sources' out-runs into bm_dst
+// Direction-optimising switch (Beamer et al.): push when the new sources' out-edges
+// are a small part of the graph, pull (bottom-up over in-runs, early exit) otherwise.
+__device__ __forceinline__ bool pull_mode(const int64_t* n_new, const int64_t* off, const int64_t* num_edges) {
+  int64_t N = *n_new;
+  return N > 0 && off[N] * 16 > *num_edges;
+}
+
+// edge-balanced expansion of the new sources' out-runs into bm_dst (push)
 __global__ void __launch_bounds__(kFBlk) k_expand(const int32_t* __restrict__ nlist, const int64_t* n_new,
                                                   const int64_t* __restrict__ off, rtec_adj_t out,
-                                                  uint32_t* bm_dst) {
+                                                  uint32_t* bm_dst, const int64_t* num_edges) {
   int64_t N = *n_new;
-  if (N == 0) return;
+  if (N == 0 || pull_mode(n_new, off, num_edges)) return;
   int64_t E = off[N];
   int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -103,6 +110,36 @@ __global__ void __launch_bounds__(kFBlk) k_expand(const int32_t* __restrict__ nl
       w = out.nbr[out.beg[u] + (e - off[i])];
     }
     bm_set_warp(bm_dst, w, act);
+  }
+}
+
+// bottom-up: thread per vertex, 32 consecutive vertices = one bitmap word owned by one warp
+__global__ void __launch_bounds__(kFBlk) k_pull(const uint32_t* __restrict__ bm_src, const uint32_t* __restrict__ prev_src,
+                                                const int64_t* n_new, const int64_t* __restrict__ off,
+                                                const int64_t* num_edges, rtec_adj_t in, int64_t n, uint32_t* bm_dst) {
+  if (!pull_mode(n_new, off, num_edges)) return;
+  int64_t words = (n + 31) / 32;
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v0 = tid - lane_id(); v0 < words * 32; v0 += stride) {
+    int64_t v = v0 + lane_id();
+    int64_t w = v0 >> 5;
+    uint32_t have = bm_dst[w];
+    bool hit = (have >> lane_id()) & 1u;
+    if (!hit && v < n) {
+      int64_t b = in.beg[v];
+      int32_t L = in.len[v];
+      for (int32_t j = 0; j < L; ++j) {
+        int32_t u = in.nbr[b + j];
+        uint32_t word = __ldg(bm_src + (u >> 5)) & (prev_src ? ~__ldg(prev_src + (u >> 5)) : 0xffffffffu);
+        if ((word >> (u & 31)) & 1u) {
+          hit = true;
+          break;
+        }
+      }
+    }
+    unsigned bal = __ballot_sync(0xffffffffu, hit);
+    if (lane_id() == 0) bm_dst[w] = have | bal;
   }
 }
 
@@ -179,7 +216,8 @@ extern "C" int rtec_frontier_layer(const rtec_graph_t* g, const rtec_batch_t* b,
   RTEC_TRY(exclusive_scan(OutLenOf{nlist, g->out.len}, Count{n_new, n}, n, StoreOffTailF{noff, n_new}, nullptr, w, s));
   {
     RTEC_PROF("k_expand", s);
-    k_expand<<<kSMs * 8, kFBlk, 0, s>>>(nlist, n_new, noff, g->out, f->bm_dst);
+    k_expand<<<kSMs * 8, kFBlk, 0, s>>>(nlist, n_new, noff, g->out, f->bm_dst, g->num_edges);
+    k_pull<<<kSMs * 8, kFBlk, 0, s>>>(f->bm_src, prev_src, n_new, noff, g->num_edges, g->in, n, f->bm_dst);
   }
   RTEC_LAUNCH_CHECK("k_expand");
   // lists + slots

@@ -19,6 +19,8 @@
 #include "rowops.cuh"
 #include "gemm_tc.cuh"
 
+#include <stdlib.h>
+
 namespace rtec {
 
 constexpr int kLBlk = 256;
@@ -42,6 +44,7 @@ struct LayerArgs {
   const float* delta;           // [n_src, d_agg] δ rows (non-GAT)
   int d_agg;
   int tc_nkb;                   // > 0: gemm_in is the tcgen05 A image with tc_nkb K-blocks
+  int c0, cw;                   // feature slice [c0, c0 + cw) of the d_agg-wide rows (aggregation)
   int layer;
   uint64_t* err;
 };
@@ -70,7 +73,7 @@ __global__ void __launch_bounds__(kLBlk) k_src_delta(LayerArgs a, float* delta) 
       acc.fma(hn, cn);
       acc.fma(ho, -co);
     }
-    acc.store(delta + i * d, d);
+    acc.store(delta + static_cast<int64_t>(u) * d, d);  // indexed by vertex: no slot gather per edge
   }
 }
 
@@ -93,7 +96,8 @@ template <int VEC, int K, bool FULL>
 __device__ __forceinline__ void agg_edges(const LayerArgs& a, int64_t beg, int32_t e0, int32_t e1, int64_t p,
                                           int64_t q, RowAcc<VEC, K>& acc) {
   using R = RowAcc<VEC, K>;
-  const int d = a.d_agg;
+  constexpr int UNR = (VEC * K <= 2) ? 8 : kUnroll;  // more rows in flight for thin slices
+  const int d = a.d_agg, cw = a.cw;
   const int lane = lane_id();
   for (int32_t c0 = e0; c0 < e1; c0 += 32) {
     int32_t j = c0 + lane;
@@ -110,14 +114,14 @@ __device__ __forceinline__ void agg_edges(const LayerArgs& a, int64_t beg, int32
       }
     }
     unsigned m = __ballot_sync(0xffffffffu, hit);
-    const float* base = FULL ? a.st.H_in : a.delta;
-    int32_t row = FULL ? u : (hit ? a.f.src_slot[u] : 0);
+    const float* base = (FULL ? a.st.H_in : a.delta) + a.c0;
+    int32_t row = u;
     while (m) {
-      int32_t rw[kUnroll];
-      float cs[kUnroll];
+      int32_t rw[UNR];
+      float cs[UNR];
       int cnt = 0;
 #pragma unroll
-      for (int t = 0; t < kUnroll; ++t) {
+      for (int t = 0; t < UNR; ++t) {
         int src = m ? __ffs(m) - 1 : 0;
         if (m) {
           m &= m - 1;
@@ -126,12 +130,12 @@ __device__ __forceinline__ void agg_edges(const LayerArgs& a, int64_t beg, int32
         rw[t] = __shfl_sync(0xffffffffu, row, src);
         cs[t] = __shfl_sync(0xffffffffu, cu, src);
       }
-      float r[kUnroll][K][VEC];
+      float r[UNR][K][VEC];
 #pragma unroll
-      for (int t = 0; t < kUnroll; ++t)
-        if (t < cnt) R::load(base + static_cast<int64_t>(rw[t]) * d, d, r[t]);
+      for (int t = 0; t < UNR; ++t)
+        if (t < cnt) R::load(base + static_cast<int64_t>(rw[t]) * d, cw, r[t]);
 #pragma unroll
-      for (int t = 0; t < kUnroll; ++t) {
+      for (int t = 0; t < UNR; ++t) {
         if (t < cnt) {
           if (FULL) acc.fma(r[t], cs[t]);
           else acc.add(r[t]);
@@ -145,17 +149,17 @@ __device__ __forceinline__ void agg_edges(const LayerArgs& a, int64_t beg, int32
 template <int VEC, int K>
 __device__ __forceinline__ void agg_struct(const LayerArgs& a, int64_t p, int64_t q, RowAcc<VEC, K>& acc) {
   using R = RowAcc<VEC, K>;
-  const int d = a.d_agg;
+  const int d = a.d_agg, cw = a.cw;
   for (int64_t k = p; k < q; ++k) {
     int32_t u = a.b.i_src[k];
     float r[K][VEC];
     if (a.b.i_op[k] == RTEC_OP_INSERT) {
-      R::load(a.st.H_in + static_cast<int64_t>(u) * d, d, r);
+      R::load(a.st.H_in + static_cast<int64_t>(u) * d + a.c0, cw, r);
       acc.fma(r, src_coeff(a.L.model, a.g.out_deg[u], a.L.degree_offset));
     } else {
       const float* orow = a.st.H_in + static_cast<int64_t>(u) * d;
       if (a.prev_bm_dst && bm_test(a.prev_bm_dst, u)) orow = a.st.log_in + static_cast<int64_t>(a.prev_slot[u]) * d;
-      R::load(orow, d, r);
+      R::load(orow + a.c0, cw, r);
       acc.fma(r, -src_coeff(a.L.model, a.g.out_deg_prev[u], a.L.degree_offset));
     }
   }
@@ -166,19 +170,19 @@ template <int VEC, int K, bool FULL>
 __device__ __forceinline__ void agg_finalize(const LayerArgs& a, int64_t i, int32_t v, int32_t len,
                                              RowAcc<VEC, K>& acc) {
   using R = RowAcc<VEC, K>;
-  const int d = a.d_agg;
-  float* srow = a.st.S + static_cast<int64_t>(v) * d;
+  const int d = a.d_agg, cw = a.cw;
+  float* srow = a.st.S + static_cast<int64_t>(v) * d + a.c0;
   int32_t indeg = FULL ? len : a.g.in_deg[v];
   if (!FULL) {
     if (indeg == 0) {
       acc.zero();  // empty neighbourhood -> zero aggregate
     } else if (a.g.in_deg_prev[v] > 0) {
       float sv[K][VEC];
-      R::load_rw(srow, d, sv);
+      R::load_rw(srow, cw, sv);
       acc.add(sv);
     }
   }
-  acc.store(srow, d);
+  acc.store(srow, cw);
   float scale = 1.f;
   if (indeg > 0) {
     if (a.L.model == RTEC_MODEL_GCN) scale = 1.0f / sqrtf(static_cast<float>(indeg) + a.L.degree_offset);
@@ -189,11 +193,11 @@ __device__ __forceinline__ void agg_finalize(const LayerArgs& a, int64_t i, int3
   out.fma(acc.v, scale);
   if (a.L.model == RTEC_MODEL_GIN) {  // update input h_v + a_v (models.py:187-189)
     float h[K][VEC];
-    R::load(a.st.H_in + static_cast<int64_t>(v) * d, d, h);
+    R::load(a.st.H_in + static_cast<int64_t>(v) * d + a.c0, cw, h);
     out.add(h);
   }
-  if (a.tc_nkb > 0) out.store_tiled(a.st.gemm_in, i, d, a.tc_nkb);
-  else out.store(a.st.gemm_in + i * d, d);
+  if (a.tc_nkb > 0) out.store_tiled(a.st.gemm_in, i, a.c0, cw, d, a.tc_nkb);
+  else out.store(a.st.gemm_in + i * d + a.c0, cw);
 }
 
 struct AggRows {
@@ -247,7 +251,7 @@ __global__ void __launch_bounds__(kLBlk) k_agg_heavy(LayerArgs a, AggRows rows, 
   if (nh == 0) return;
   const int64_t T = hp.hoff[nh];
   const int64_t na = FULL ? 0 : *a.b.n_applied;
-  const int d = a.d_agg;
+  const int cw = a.cw;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t t = warp; t < T; t += nw) {
@@ -268,7 +272,7 @@ __global__ void __launch_bounds__(kLBlk) k_agg_heavy(LayerArgs a, AggRows rows, 
     int32_t e0 = c * kChunk, e1 = min(len, e0 + kChunk);
     agg_edges<VEC, K, FULL>(a, a.g.in.beg[v], e0, e1, p, q, acc);
     if (!FULL && c == 0) agg_struct<VEC, K>(a, p, q, acc);
-    acc.store(hp.part + t * d, d);
+    acc.store(hp.part + t * cw, cw);
     __threadfence();
     int old = 0;
     if (lane_id() == 0) old = atomicAdd(hp.arrive + j, 1);
@@ -280,8 +284,8 @@ __global__ void __launch_bounds__(kLBlk) k_agg_heavy(LayerArgs a, AggRows rows, 
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         int col = lane_id() + 32 * k;
-        if (col * VEC < d) {
-          const float* src = hp.part + (c0 + cc) * d + col * VEC;
+        if (col * VEC < cw) {
+          const float* src = hp.part + (c0 + cc) * cw + col * VEC;
 #pragma unroll
           for (int jj = 0; jj < VEC; ++jj) acc.v[k][jj] += __ldcg(src + jj);
         }
@@ -336,6 +340,18 @@ __global__ void k_chunk_map(HeavyPlan hp) {
   }
 }
 
+// RTEC_AGG_SLICE env: feature-slice width of the aggregation passes (default 64; 0 = whole rows)
+static int agg_slice_width() {
+  static int w = -1;
+  if (w < 0) {
+    const char* e = getenv("RTEC_AGG_SLICE");
+    w = e ? atoi(e) : 64;
+    if (w < 0 || w > 64) w = 64;
+    w &= ~1;
+  }
+  return w;
+}
+
 // plan + light + heavy launches for one aggregation
 template <bool FULL>
 static int launch_aggregation(LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_edges, Ws& w,
@@ -360,14 +376,26 @@ static int launch_aggregation(LayerArgs& a, AggRows rows, int64_t max_rows, int6
                           StoreOffTailL{hp.hoff, hp.n_heavy}, nullptr, w, s));
   k_chunk_map<<<kSMs * 4, kLBlk, 0, s>>>(hp);
   const int grid = kSMs * 8;
-  bool ok;
-  {
-    RTEC_PROF(FULL ? "k_agg_full_light" : "k_agg_inc", s);
-    ok = RTEC_ROW_DISPATCH(d, (k_agg_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows)));
-  }
-  {
-    RTEC_PROF(FULL ? "k_agg_full_heavy" : "k_agg_inc_heavy", s);
-    ok = ok && RTEC_ROW_DISPATCH(d, (k_agg_heavy<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows, hp)));
+  // Feature slicing: one pass per `sw`-column slice keeps the gathered rows'
+  // working set (|S| x sw x 4 B) small enough for the hot sources to stay in
+  // L2 (126 MB); the plan above is shared by all passes.
+  const int sw = agg_slice_width();
+  bool ok = true;
+  for (int c0 = 0; c0 < d && ok; c0 += (sw > 0 ? sw : d)) {
+    a.c0 = c0;
+    a.cw = sw > 0 ? (d - c0 < sw ? d - c0 : sw) : d;
+    if (c0 > 0) RTEC_CUDA(cudaMemsetAsync(hp.arrive, 0, sizeof(int32_t) * (max_rows + 1), s));
+    const bool sliced = a.cw <= 64;
+    {
+      RTEC_PROF(FULL ? "k_agg_full_light" : "k_agg_inc", s);
+      ok = sliced ? RTEC_SLICE_DISPATCH(a.cw, (k_agg_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows)))
+                  : RTEC_ROW_DISPATCH(a.cw, (k_agg_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows)));
+    }
+    {
+      RTEC_PROF(FULL ? "k_agg_full_heavy" : "k_agg_inc_heavy", s);
+      ok = ok && (sliced ? RTEC_SLICE_DISPATCH(a.cw, (k_agg_heavy<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows, hp)))
+                         : RTEC_ROW_DISPATCH(a.cw, (k_agg_heavy<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows, hp))));
+    }
   }
   if (!ok) {
     set_error("row width %d unsupported", d);

@@ -13,6 +13,10 @@ struct VecT<4> {
   using T = float4;
 };
 template <>
+struct VecT<2> {
+  using T = float2;
+};
+template <>
 struct VecT<1> {
   using T = float;
 };
@@ -35,6 +39,9 @@ struct RowAcc {
         if constexpr (VEC == 4) {
           float4 x = __ldg(reinterpret_cast<const float4*>(row) + c);
           r[k][0] = x.x; r[k][1] = x.y; r[k][2] = x.z; r[k][3] = x.w;
+        } else if constexpr (VEC == 2) {
+          float2 x = __ldg(reinterpret_cast<const float2*>(row) + c);
+          r[k][0] = x.x; r[k][1] = x.y;
         } else {
           r[k][0] = __ldg(row + c);
         }
@@ -53,6 +60,9 @@ struct RowAcc {
         if constexpr (VEC == 4) {
           float4 x = reinterpret_cast<const float4*>(row)[c];
           r[k][0] = x.x; r[k][1] = x.y; r[k][2] = x.z; r[k][3] = x.w;
+        } else if constexpr (VEC == 2) {
+          float2 x = reinterpret_cast<const float2*>(row)[c];
+          r[k][0] = x.x; r[k][1] = x.y;
         } else {
           r[k][0] = row[c];
         }
@@ -81,38 +91,53 @@ struct RowAcc {
       if (c * VEC < d) {
         if constexpr (VEC == 4) {
           reinterpret_cast<float4*>(row)[c] = make_float4(v[k][0], v[k][1], v[k][2], v[k][3]);
+        } else if constexpr (VEC == 2) {
+          reinterpret_cast<float2*>(row)[c] = make_float2(v[k][0], v[k][1]);
         } else {
           row[c] = v[k][0];
         }
       }
     }
   }
-  // Row i into the tcgen05 A-operand image: [tile][kb][128][32] with the
-  // SW128 16-byte-chunk XOR swizzle; columns d .. nkb*32 are zero padding.
-  __device__ __forceinline__ void store_tiled(float* A, int64_t i, int d, int nkb) const {
+  // Columns [col0, col0 + w) of row i into the tcgen05 A-operand image:
+  // [tile][kb][128][32] with the SW128 16-byte-chunk XOR swizzle.  The slice
+  // ending at d_total also writes the zero padding d_total .. nkb*32.
+  __device__ __forceinline__ void store_tiled(float* A, int64_t i, int col0, int w, int d_total, int nkb) const {
     const int64_t tile = i >> 7;
     const int r = static_cast<int>(i & 127);
     float* tbase = A + tile * static_cast<int64_t>(nkb) * 4096;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      int c = (lane_id() + 32 * k) * VEC;
-      if (c < d) {
+      int cl = (lane_id() + 32 * k) * VEC;
+      if (cl < w) {
+        int c = col0 + cl;
         int kb = c >> 5, cc = c & 31;
-        float* blk = tbase + kb * 4096 + r * 32;
+        float* blk = tbase + kb * 4096 + r * 32 + ((((cc >> 2) ^ (r & 7)) << 2) | (cc & 3));
         if constexpr (VEC == 4) {
-          *reinterpret_cast<float4*>(blk + ((((cc >> 2) ^ (r & 7)) << 2))) =
-              make_float4(v[k][0], v[k][1], v[k][2], v[k][3]);
+          *reinterpret_cast<float4*>(blk) = make_float4(v[k][0], v[k][1], v[k][2], v[k][3]);
+        } else if constexpr (VEC == 2) {
+          *reinterpret_cast<float2*>(blk) = make_float2(v[k][0], v[k][1]);
         } else {
-          blk[(((cc >> 2) ^ (r & 7)) << 2) | (cc & 3)] = v[k][0];
+          *blk = v[k][0];
         }
       }
     }
-    for (int c = d + lane_id(); c < nkb * 32; c += 32) {  // zero padding
-      int kb = c >> 5, cc = c & 31;
-      tbase[kb * 4096 + r * 32 + ((((cc >> 2) ^ (r & 7)) << 2) | (cc & 3))] = 0.f;
+    if (col0 + w >= d_total) {
+      for (int c = d_total + lane_id(); c < nkb * 32; c += 32) {  // zero padding
+        int kb = c >> 5, cc = c & 31;
+        tbase[kb * 4096 + r * 32 + ((((cc >> 2) ^ (r & 7)) << 2) | (cc & 3))] = 0.f;
+      }
     }
   }
 };
+
+// dispatch for a feature slice of width w <= 64: float2 lanes when even
+#define RTEC_SLICE_DISPATCH(w, ...)                                                 \
+  [&]() -> bool {                                                                  \
+    if ((w) <= 64 && ((w) % 2) == 0) { constexpr int VEC = 2, K = 1; __VA_ARGS__; return true; } \
+    if ((w) <= 64) { constexpr int VEC = 1, K = 2; __VA_ARGS__; return true; }      \
+    return false;                                                                  \
+  }()
 
 // dispatch (VEC, K) from the row width; returns false if unsupported
 #define RTEC_ROW_DISPATCH(d, ...)                                         \
