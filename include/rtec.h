@@ -98,6 +98,10 @@ typedef struct {
   /* DegreeDelta rows (graph.py:41-48), ascending vertex */
   int32_t* d_vertex; int32_t* d_old_in; int32_t* d_new_in; int32_t* d_old_out; int32_t* d_new_out;
   int64_t* n_delta;    /* [1] */
+  /* [2n] per-vertex (first, count) of its entries in the in-key list i_*;
+   * (-1, 0) for vertices without applied updates.  Caller initialises it once
+   * to (-1, 0); rtec_batch_apply sets it, rtec_batch_commit resets it. */
+  int32_t* irange;
 } rtec_batch_t;
 
 /* Per-layer frontier (Alg. 4).  Bitmaps

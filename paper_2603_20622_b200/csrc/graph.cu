@@ -547,6 +547,26 @@ static int merge_exec(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, int6
   return RTEC_OK;
 }
 
+// per-destination ranges of the in-key ordered applied list (replaces a binary
+// search per destination in the layer kernels)
+__global__ void k_irange_set(const int32_t* __restrict__ id, const int64_t* cnt, int2* irange, const uint64_t* err) {
+  if (err_set(err)) return;
+  int64_t K = *cnt;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t v = id[i];
+    if (i > 0 && id[i - 1] == v) continue;
+    int64_t j = i + 1;
+    while (j < K && id[j] == v) ++j;
+    irange[v] = make_int2(static_cast<int32_t>(i), static_cast<int32_t>(j - i));
+  }
+}
+
+__global__ void k_irange_reset(const int32_t* __restrict__ id, const int64_t* cnt, int2* irange) {
+  int64_t K = *cnt;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x)
+    irange[id[i]] = make_int2(-1, 0);
+}
+
 // ------------------------------------------------------------------ degrees + deltas
 __global__ void k_apply_degrees(const int32_t* __restrict__ as, const int32_t* __restrict__ ad,
                                 const uint8_t* __restrict__ ao, const int64_t* cnt, int32_t* out_deg,
@@ -785,7 +805,8 @@ int rtec_batch_apply(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src, const
   w.off = mark;
   RTEC_TRY(merge_plan(mi, pi, g->in, g->slack, g->min_slack, b->err, w, s));
   w.off = mark;
-  // 8. mutate: degrees, runs
+  // 8. mutate: degrees, runs, per-destination ranges
+  k_irange_set<<<grid, kBlk, 0, s>>>(b->i_dst, b->n_applied, reinterpret_cast<int2*>(b->irange), b->err);
   k_apply_degrees<<<grid, kBlk, 0, s>>>(b->a_src, b->a_dst, b->a_op, b->n_applied, g->out_deg, g->in_deg,
                                         g->num_edges, b->err);
   int64_t work_bound = g->out.slots + B;  // grid-stride loops read the real totals on device
@@ -804,6 +825,7 @@ int rtec_batch_apply(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src, const
 
 int rtec_batch_commit(rtec_graph_t* g, const rtec_batch_t* b, rtec_stream_t stream) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  k_irange_reset<<<grid_for(b->cap, kBlk), kBlk, 0, s>>>(b->i_dst, b->n_applied, reinterpret_cast<int2*>(b->irange));
   k_commit_degrees<<<grid_for(b->cap * 2, kBlk), kBlk, 0, s>>>(b->d_vertex, b->n_delta, g->in_deg, g->out_deg,
                                                                g->in_deg_prev, g->out_deg_prev);
   RTEC_LAUNCH_CHECK("k_commit_degrees");

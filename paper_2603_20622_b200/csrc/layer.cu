@@ -223,7 +223,6 @@ __global__ void __launch_bounds__(kLBlk) k_agg_light(LayerArgs a, AggRows rows) 
   if (!FULL && err_set(a.err)) return;
   const int64_t nr = rows.count();
   const bool scan = FULL || *a.f.n_src > 0;
-  const int64_t na = FULL ? 0 : *a.b.n_applied;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = warp; i < nr; i += nw) {
@@ -232,8 +231,11 @@ __global__ void __launch_bounds__(kLBlk) k_agg_light(LayerArgs a, AggRows rows) 
     if (scan && len > kChunk) continue;  // heavy pass
     int64_t p = 0, q = 0;
     if (!FULL) {
-      p = lower_bound_dev(a.b.i_dst, 0, na, v);
-      q = lower_bound_dev(a.b.i_dst, p, na, v + 1);
+      int2 rg = reinterpret_cast<const int2*>(a.b.irange)[v];
+      if (rg.x >= 0) {
+        p = rg.x;
+        q = rg.x + rg.y;
+      }
     }
     R acc;
     acc.zero();
@@ -250,7 +252,6 @@ __global__ void __launch_bounds__(kLBlk) k_agg_heavy(LayerArgs a, AggRows rows, 
   const int64_t nh = *hp.n_heavy;
   if (nh == 0) return;
   const int64_t T = hp.hoff[nh];
-  const int64_t na = FULL ? 0 : *a.b.n_applied;
   const int cw = a.cw;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -264,8 +265,11 @@ __global__ void __launch_bounds__(kLBlk) k_agg_heavy(LayerArgs a, AggRows rows, 
     int32_t len = a.g.in.len[v];
     int64_t p = 0, q = 0;
     if (!FULL) {
-      p = lower_bound_dev(a.b.i_dst, 0, na, v);
-      q = lower_bound_dev(a.b.i_dst, p, na, v + 1);
+      int2 rg = reinterpret_cast<const int2*>(a.b.irange)[v];
+      if (rg.x >= 0) {
+        p = rg.x;
+        q = rg.x + rg.y;
+      }
     }
     R acc;
     acc.zero();
@@ -340,12 +344,12 @@ __global__ void k_chunk_map(HeavyPlan hp) {
   }
 }
 
-// RTEC_AGG_SLICE env: feature-slice width of the aggregation passes (default 64; 0 = whole rows)
+// RTEC_AGG_SLICE env: feature-slice width of the aggregation passes (default 0 = whole rows)
 static int agg_slice_width() {
   static int w = -1;
   if (w < 0) {
     const char* e = getenv("RTEC_AGG_SLICE");
-    w = e ? atoi(e) : 64;
+    w = e ? atoi(e) : 0;  // measured: slicing costs more per-edge work than it saves in L2 misses
     if (w < 0 || w > 64) w = 64;
     w &= ~1;
   }
@@ -421,7 +425,6 @@ __global__ void __launch_bounds__(kLBlk) k_gat_layer(LayerArgs a, int recompute_
   const int dh = d / H;
   const int64_t nd = recompute_all ? a.g.n : *a.f.n_dst;
   const int64_t ns = recompute_all ? 0 : *a.f.n_src;
-  const int64_t na = recompute_all ? 0 : *a.b.n_applied;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int lane = lane_id();
@@ -459,8 +462,14 @@ __global__ void __launch_bounds__(kLBlk) k_gat_layer(LayerArgs a, int recompute_
         }
       }
     } else {
-      int64_t p = lower_bound_dev(a.b.i_dst, 0, na, v);
-      int64_t q = lower_bound_dev(a.b.i_dst, p, na, v + 1);
+      int64_t p = 0, q = 0;
+      {
+        int2 rg = reinterpret_cast<const int2*>(a.b.irange)[v];
+        if (rg.x >= 0) {
+          p = rg.x;
+          q = rg.x + rg.y;
+        }
+      }
       if (ns > 0) {  // ValueChange edges: sources whose h^{l-1} changed
         for (int32_t c0 = 0; c0 < len; c0 += 32) {
           int32_t j = c0 + lane;

@@ -95,9 +95,12 @@ class _Adj:
 class DeviceBatch:
     """rtec_batch_t buffers (capacity `cap` updates)."""
 
-    def __init__(self, cap: int, dev):
+    def __init__(self, cap: int, dev, n: int):
         cap = max(int(cap), 1)
         self.cap = cap
+        # per-vertex (first, count) into the in-key list, (-1, 0) when untouched
+        self.irange = torch.stack([torch.full((max(n, 1),), -1, dtype=torch.int32, device=dev),
+                                   torch.zeros(max(n, 1), dtype=torch.int32, device=dev)], dim=1).contiguous()
         z = lambda k, dt: torch.zeros(k, dtype=dt, device=dev)  # noqa: E731
         self.err = z(1, torch.int64)
         self.status = z(cap, torch.uint8)
@@ -115,7 +118,7 @@ class DeviceBatch:
         d = self.d
         return _lib.Batch(self.cap, p(self.err), p(self.status), p(self.a_src), p(self.a_dst), p(self.a_op),
                           p(self.a_ts), p(self.n_applied), p(self.i_src), p(self.i_dst), p(self.i_op),
-                          p(d[0]), p(d[1]), p(d[2]), p(d[3]), p(d[4]), p(self.n_delta))
+                          p(d[0]), p(d[1]), p(d[2]), p(d[3]), p(d[4]), p(self.n_delta), p(self.irange))
 
 
 class DynamicGraph:
@@ -133,7 +136,7 @@ class DynamicGraph:
         self.min_slack = int(min_slack)
         self.reserve = reserve
         self.ws = torch.empty(0, dtype=torch.uint8, device=self.dev)
-        self.batch = DeviceBatch(1024, self.dev)
+        self.batch = DeviceBatch(1024, self.dev, n)
         self.m_hint = 0
         self._build(np.zeros(0, np.int32), np.zeros(0, np.int32), None)
 
@@ -317,7 +320,7 @@ class DynamicGraph:
         """Copy one batch into the device staging buffers; returns B."""
         B = int(len(src))
         if B > self.batch.cap:
-            self.batch = DeviceBatch(max(B, 2 * self.batch.cap), self.dev)
+            self.batch = DeviceBatch(max(B, 2 * self.batch.cap), self.dev, self.n)
             self._ensure_ws(self.batch.cap)
         b = self.batch
         if B:
