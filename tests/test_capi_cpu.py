@@ -59,7 +59,7 @@ def test_struct_layouts_match_header(lib):
     assert list(sizes) == [ctypes.sizeof(t) for t in mirror]
     assert ctypes.sizeof(_lib.Adj) == 8 * 7
     assert ctypes.sizeof(_lib.Graph) == 8 + 2 * 56 + 5 * 8 + 8
-    assert ctypes.sizeof(_lib.Batch) == 8 * 17
+    assert ctypes.sizeof(_lib.Batch) == 8 * 18
     assert ctypes.sizeof(_lib.Layer) == 6 * 4 + 7 * 8
     assert ctypes.sizeof(_lib.State) == 13 * 8
 
