@@ -102,25 +102,51 @@ __host__ __device__ __forceinline__ int64_t sw128_off(int r, int c) {
 
 
 
-__global__ void __launch_bounds__(128, 1) k_gemm_tc(TcArgs g) {
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Warp-specialised persistent kernel (256 threads):
+//   warp 0      producer: bulk-copies A / Bhi / Blo of each K-block into a ring of S stages
+//   warp 1      MMA issuer: 12 tcgen05.mma per K-block into one of two TMEM accumulators
+//   warps 2-3   splitters: A -> (hi, lo) in shared memory, fence.proxy.async, arrive
+//   warps 4-7   epilogue: tcgen05.ld -> act -> global rows (+ DeltaLog), overlapping the
+//               next tile's main loop thanks to the double-buffered accumulator
+// mbarriers: full[s] (tx), split[s] (64 arrivals), empty[s] (tcgen05.commit),
+//            tfull[2] (tcgen05.commit), tempty[2] (128 arrivals)
+constexpr int kMaxStages = 4;
+
+__global__ void __launch_bounds__(256, 1) k_gemm_tc(TcArgs g, int S) {
   extern __shared__ uint8_t smem_raw[];
   if (g.err && err_set(g.err)) return;
   const int64_t nrows = g.n_rows ? *g.n_rows : g.max_rows;
   const int64_t ntiles = (nrows + kTM - 1) / kTM;
   if (static_cast<int64_t>(blockIdx.x) >= ntiles) return;
 
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t bbytes = static_cast<uint32_t>(g.npad) * kTK * 4;
   const uint32_t stage_bytes = 2 * kABlockBytes + 2 * bbytes;
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* stage[2] = {base, base + stage_bytes};
-  uint64_t* bars = reinterpret_cast<uint64_t*>(base + 2 * stage_bytes);  // load[2], mma[2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + S * stage_bytes);
+  uint64_t* full = bars;
+  uint64_t* split = bars + kMaxStages;
+  uint64_t* empty = bars + 2 * kMaxStages;
+  uint64_t* tfull = bars + 3 * kMaxStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   uint32_t ncols = 32;
-  while (ncols < static_cast<uint32_t>(g.npad)) ncols <<= 1;
+  while (ncols < static_cast<uint32_t>(2 * g.npad)) ncols <<= 1;
 
   if (tid == 0) {
-    for (int i = 0; i < 4; ++i) mbar_init(bars + i, 1);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(split + i, 64);
+      mbar_init(empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(tfull + i, 1);
+      mbar_init(tempty + i, 128);
+    }
     fence_barrier_init();
   }
   if (warp == 0) {
@@ -132,90 +158,104 @@ __global__ void __launch_bounds__(128, 1) k_gemm_tc(TcArgs g) {
   __syncthreads();
   tc_fence_after();
   const uint32_t taddr = *tmem_slot;
-  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(g.npad >> 3) << 17) |
-                         (static_cast<uint32_t>(kTM >> 4) << 24);
-
   const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
   const int64_t J = my_tiles * g.nkb;
-  auto issue_load = [&](int64_t j) {
-    int s = static_cast<int>(j & 1);
-    int64_t tile = blockIdx.x + (j / g.nkb) * gridDim.x;
-    int kb = static_cast<int>(j % g.nkb);
-    uint8_t* st = stage[s];
-    mbar_expect_tx(bars + s, kABlockBytes + 2 * bbytes);
-    bulk_g2s(st, g.A + (tile * g.nkb + kb) * (kABlockBytes / 4), kABlockBytes, bars + s);
-    bulk_g2s(st + 2 * kABlockBytes, g.Bhi + static_cast<int64_t>(kb) * g.npad * kTK, bbytes, bars + s);
-    bulk_g2s(st + 2 * kABlockBytes + bbytes, g.Blo + static_cast<int64_t>(kb) * g.npad * kTK, bbytes, bars + s);
-  };
-  if (tid == 0) issue_load(0);
 
-  for (int64_t j = 0; j < J; ++j) {
-    const int s = static_cast<int>(j & 1);
-    const int kb = static_cast<int>(j % g.nkb);
-    // prefetch step j+1 into the other stage once its previous MMAs have drained
-    if (j + 1 < J) {
-      if (j >= 1) mbar_wait(bars + 2 + (s ^ 1), static_cast<uint32_t>(((j - 1) >> 1) & 1));
-      if (tid == 0) issue_load(j + 1);
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int64_t j = 0; j < J; ++j) {
+        const int s = static_cast<int>(j % S);
+        const int64_t u = j / S;
+        if (u > 0) mbar_wait(empty + s, static_cast<uint32_t>((u - 1) & 1));
+        const int64_t tile = blockIdx.x + (j / g.nkb) * gridDim.x;
+        const int kb = static_cast<int>(j % g.nkb);
+        uint8_t* st = base + s * stage_bytes;
+        mbar_expect_tx(full + s, kABlockBytes + 2 * bbytes);
+        bulk_g2s(st, g.A + (tile * g.nkb + kb) * (kABlockBytes / 4), kABlockBytes, full + s);
+        bulk_g2s(st + 2 * kABlockBytes, g.Bhi + static_cast<int64_t>(kb) * g.npad * kTK, bbytes, full + s);
+        bulk_g2s(st + 2 * kABlockBytes + bbytes, g.Blo + static_cast<int64_t>(kb) * g.npad * kTK, bbytes, full + s);
+      }
     }
-    mbar_wait(bars + s, static_cast<uint32_t>((j >> 1) & 1));
-    // split A into hi (separate buffer) and lo (in place)
-    {
-      float4* raw = reinterpret_cast<float4*>(stage[s]);
-      float4* hi = reinterpret_cast<float4*>(stage[s] + kABlockBytes);
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(g.npad >> 3) << 17) |
+                             (static_cast<uint32_t>(kTM >> 4) << 24);
+      for (int64_t t = 0; t < my_tiles; ++t) {
+        const int b = static_cast<int>(t & 1);
+        const int64_t ub = t >> 1;
+        if (ub > 0) mbar_wait(tempty + b, static_cast<uint32_t>((ub - 1) & 1));
+        tc_fence_after();
+        const uint32_t acc_addr = taddr + static_cast<uint32_t>(b * g.npad);
+        for (int kb = 0; kb < g.nkb; ++kb) {
+          const int64_t j = t * g.nkb + kb;
+          const int s = static_cast<int>(j % S);
+          mbar_wait(split + s, static_cast<uint32_t>((j / S) & 1));
+          tc_fence_after();
+          const uint32_t a_lo = smem_u32(base + s * stage_bytes);
+          const uint32_t a_hi = a_lo + kABlockBytes;
+          const uint32_t b_hi = a_lo + 2 * kABlockBytes;
+          const uint32_t b_lo = b_hi + bbytes;
 #pragma unroll
-      for (int q = 0; q < kABlockBytes / 16 / 128; ++q) {
-        int idx = tid + 128 * q;
+          for (int k = 0; k < kTK / 8; ++k) {
+            const uint32_t off = k * 32;
+            const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+            mma_tf32(acc_addr, sw128_desc(a_hi + off), sw128_desc(b_hi + off), idesc, acc);
+            mma_tf32(acc_addr, sw128_desc(a_hi + off), sw128_desc(b_lo + off), idesc, 1u);
+            mma_tf32(acc_addr, sw128_desc(a_lo + off), sw128_desc(b_hi + off), idesc, 1u);
+          }
+          mma_commit(empty + s);  // smem stage reusable once these MMAs retire
+        }
+        mma_commit(tfull + b);    // accumulator b complete
+      }
+    }
+  } else if (warp < 4) {
+    const int st_id = tid - 64;  // 0..63
+    for (int64_t j = 0; j < J; ++j) {
+      const int s = static_cast<int>(j % S);
+      mbar_wait(full + s, static_cast<uint32_t>((j / S) & 1));
+      float4* raw = reinterpret_cast<float4*>(base + s * stage_bytes);
+      float4* hi = reinterpret_cast<float4*>(base + s * stage_bytes + kABlockBytes);
+#pragma unroll 4
+      for (int q = 0; q < kABlockBytes / 16 / 64; ++q) {
+        const int idx = st_id + 64 * q;
         float4 x = raw[idx];
         float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
         hi[idx] = h;
         raw[idx] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
       }
+      fence_proxy_async();
+      mbar_arrive(split + s);
     }
-    fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
+  } else {
+    // epilogue: thread owns accumulator row r = tid - 128 (TMEM lane r; warp w%4 -> lanes 32*(w%4))
+    const int r = tid - 128;
+    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    for (int64_t t = 0; t < my_tiles; ++t) {
+      const int b = static_cast<int>(t & 1);
+      mbar_wait(tfull + b, static_cast<uint32_t>((t >> 1) & 1));
       tc_fence_after();
-      const uint32_t a_lo = smem_u32(stage[s]);
-      const uint32_t a_hi = a_lo + kABlockBytes;
-      const uint32_t b_hi = a_lo + 2 * kABlockBytes;
-      const uint32_t b_lo = b_hi + bbytes;
-#pragma unroll
-      for (int k = 0; k < kTK / 8; ++k) {  // 4 MMAs of K = 8 (32 B) each
-        const uint32_t off = k * 32;
-        const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
-        mma_tf32(taddr, sw128_desc(a_hi + off), sw128_desc(b_hi + off), idesc, acc);
-        mma_tf32(taddr, sw128_desc(a_hi + off), sw128_desc(b_lo + off), idesc, 1u);
-        mma_tf32(taddr, sw128_desc(a_lo + off), sw128_desc(b_hi + off), idesc, 1u);
-      }
-      mma_commit(bars + 2 + s);
-    }
-    if (kb == g.nkb - 1) {
-      // epilogue: thread tid owns accumulator row tid (TMEM lane tid)
-      mbar_wait(bars + 2 + s, static_cast<uint32_t>((j >> 1) & 1));
-      tc_fence_after();
-      const int64_t tile = blockIdx.x + (j / g.nkb) * gridDim.x;
-      const int64_t i = tile * kTM + tid;
+      const int64_t tile = blockIdx.x + t * gridDim.x;
+      const int64_t i = tile * kTM + r;
       const bool valid = i < nrows;
       const int64_t dst = valid ? (g.y_rows ? static_cast<int64_t>(g.y_rows[i]) : i) : 0;
-      const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
       for (int c0 = 0; c0 < g.npad; c0 += 32) {
-        uint32_t r[32];
-        RTEC_TMEM_LD32(taddr + lane_base + static_cast<uint32_t>(c0), r);
+        uint32_t rr[32];
+        RTEC_TMEM_LD32(taddr + lane_base + static_cast<uint32_t>(b * g.npad + c0), rr);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (!valid) continue;
         float y[32];
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          float v = __uint_as_float(r[t]);
-          y[t] = g.act == 1 ? fmaxf(v, 0.f) : v;
+        for (int q = 0; q < 32; ++q) {
+          float v = __uint_as_float(rr[q]);
+          y[q] = g.act == 1 ? fmaxf(v, 0.f) : v;
         }
-        if (g.Yt) {  // chained GEMM input: write the SW128 tile image (zero padding beyond d_out)
+        if (g.Yt) {  // chained GEMM input: SW128 tile image (zero padding beyond d_out)
           float* blk = g.Yt + ((tile * g.nkb_out + c0 / 32) * kTM) * kTK;
 #pragma unroll
-          for (int t = 0; t < 32; t += 4) {
-            float4 v4 = make_float4(c0 + t < g.d_out ? y[t] : 0.f, c0 + t + 1 < g.d_out ? y[t + 1] : 0.f,
-                                    c0 + t + 2 < g.d_out ? y[t + 2] : 0.f, c0 + t + 3 < g.d_out ? y[t + 3] : 0.f);
-            *reinterpret_cast<float4*>(blk + sw128_off(tid, t)) = v4;
+          for (int q = 0; q < 32; q += 4) {
+            float4 v4 = make_float4(c0 + q < g.d_out ? y[q] : 0.f, c0 + q + 1 < g.d_out ? y[q + 1] : 0.f,
+                                    c0 + q + 2 < g.d_out ? y[q + 2] : 0.f, c0 + q + 3 < g.d_out ? y[q + 3] : 0.f);
+            *reinterpret_cast<float4*>(blk + sw128_off(r, q)) = v4;
           }
         } else {
           float* yrow = g.Y + dst * g.ldy;
@@ -224,27 +264,30 @@ __global__ void __launch_bounds__(128, 1) k_gemm_tc(TcArgs g) {
             if (g.log) {
               float4 old[8];
 #pragma unroll
-              for (int t = 0; t < 8; ++t) old[t] = y4[t];
+              for (int q = 0; q < 8; ++q) old[q] = y4[q];
               float4* l4 = reinterpret_cast<float4*>(g.log + i * g.d_out + c0);
 #pragma unroll
-              for (int t = 0; t < 8; ++t) l4[t] = old[t];
+              for (int q = 0; q < 8; ++q) l4[q] = old[q];
             }
 #pragma unroll
-            for (int t = 0; t < 8; ++t) y4[t] = make_float4(y[4 * t], y[4 * t + 1], y[4 * t + 2], y[4 * t + 3]);
+            for (int q = 0; q < 8; ++q) y4[q] = make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
           } else {
-            for (int t = 0; t < 32 && c0 + t < g.d_out; ++t) {
-              if (g.log) g.log[i * g.d_out + c0 + t] = yrow[c0 + t];
-              yrow[c0 + t] = y[t];
+            for (int q = 0; q < 32 && c0 + q < g.d_out; ++q) {
+              if (g.log) g.log[i * g.d_out + c0 + q] = yrow[c0 + q];
+              yrow[c0 + q] = y[q];
             }
           }
         }
       }
       tc_fence_before();
-      __syncthreads();  // TMEM reads done before the next tile overwrites the accumulator
+      mbar_arrive(tempty + b);
     }
   }
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+  }
 }
 
 // W [d_out, d_in] -> Bhi/Blo [nkb][npad][32] swizzled, zero padded
@@ -264,7 +307,14 @@ __global__ void k_prep_b(const float* __restrict__ W, int d_in, int d_out, int n
   }
 }
 
-size_t gemm_tc_smem(int npad) { return 2 * (2 * kABlockBytes + 2 * static_cast<size_t>(npad) * kTK * 4) + 1024 + 64; }
+static int gemm_tc_stages(int npad) {
+  size_t stage = 2 * kABlockBytes + 2 * static_cast<size_t>(npad) * kTK * 4;
+  int S = static_cast<int>((227 * 1024 - 1024 - 256) / stage);
+  return S < kMaxStages ? S : kMaxStages;
+}
+size_t gemm_tc_smem(int npad) {
+  return gemm_tc_stages(npad) * (2 * kABlockBytes + 2 * static_cast<size_t>(npad) * kTK * 4) + 1024 + 256;
+}
 
 int gemm_tc_launch(const TcArgs& g, cudaStream_t s) {
   if (g.max_rows <= 0) return RTEC_OK;
@@ -277,7 +327,7 @@ int gemm_tc_launch(const TcArgs& g, cudaStream_t s) {
   int64_t tiles = (g.max_rows + kTM - 1) / kTM;
   int grid = static_cast<int>(tiles < kSMs ? tiles : kSMs);
   RTEC_PROF("k_gemm_tc", s);
-  k_gemm_tc<<<grid, 128, smem, s>>>(g);
+  k_gemm_tc<<<grid, 256, smem, s>>>(g, gemm_tc_stages(g.npad));
   RTEC_LAUNCH_CHECK("k_gemm_tc");
   return RTEC_OK;
 }

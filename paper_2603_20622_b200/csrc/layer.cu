@@ -99,13 +99,14 @@ __device__ __forceinline__ void agg_edges(const LayerArgs& a, int64_t beg, int32
   constexpr int UNR = (VEC * K <= 2) ? 8 : kUnroll;  // more rows in flight for thin slices
   const int d = a.d_agg, cw = a.cw;
   const int lane = lane_id();
+  const uint64_t pol = l2_evict_first_policy();
   for (int32_t c0 = e0; c0 < e1; c0 += 32) {
     int32_t j = c0 + lane;
     int32_t u = 0;
     bool hit = false;
     float cu = 0.f;
     if (j < e1) {
-      u = a.g.in.nbr[beg + j];
+      u = ld_stream_i32(a.g.in.nbr + beg + j, pol);
       if (FULL) {
         hit = true;
         cu = src_coeff(a.L.model, a.g.out_deg[u], a.L.degree_offset);
@@ -178,11 +179,11 @@ __device__ __forceinline__ void agg_finalize(const LayerArgs& a, int64_t i, int3
       acc.zero();  // empty neighbourhood -> zero aggregate
     } else if (a.g.in_deg_prev[v] > 0) {
       float sv[K][VEC];
-      R::load_rw(srow, cw, sv);
+      R::load_stream(srow, cw, sv, l2_evict_first_policy());
       acc.add(sv);
     }
   }
-  acc.store(srow, cw);
+  acc.store_stream(srow, cw, l2_evict_first_policy());
   float scale = 1.f;
   if (indeg > 0) {
     if (a.L.model == RTEC_MODEL_GCN) scale = 1.0f / sqrtf(static_cast<float>(indeg) + a.L.degree_offset);
@@ -197,7 +198,7 @@ __device__ __forceinline__ void agg_finalize(const LayerArgs& a, int64_t i, int3
     out.add(h);
   }
   if (a.tc_nkb > 0) out.store_tiled(a.st.gemm_in, i, a.c0, cw, d, a.tc_nkb);
-  else out.store(a.st.gemm_in + i * d + a.c0, cw);
+  else out.store_stream(a.st.gemm_in + i * d + a.c0, cw, l2_evict_first_policy());
 }
 
 struct AggRows {
@@ -218,7 +219,7 @@ struct HeavyPlan {
 };
 
 template <int VEC, int K, bool FULL>
-__global__ void __launch_bounds__(kLBlk) k_agg_light(LayerArgs a, AggRows rows) {
+__global__ void __launch_bounds__(kLBlk, 4) k_agg_light(LayerArgs a, AggRows rows) {
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
   const int64_t nr = rows.count();
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(kLBlk) k_agg_light(LayerArgs a, AggRows rows) 
 }
 
 template <int VEC, int K, bool FULL>
-__global__ void __launch_bounds__(kLBlk) k_agg_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
+__global__ void __launch_bounds__(kLBlk, 4) k_agg_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
   const int64_t nh = *hp.n_heavy;

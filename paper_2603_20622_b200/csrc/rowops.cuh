@@ -21,6 +21,30 @@ struct VecT<1> {
   using T = float;
 };
 
+// L2 eviction-priority policy for streaming traffic (read/written once per
+// batch): keeps it from displacing re-used gathered rows in L2.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float4 ld_stream_f4(const float4* a, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_stream_f4(float4* a, float4 v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(a), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ int32_t ld_stream_i32(const int32_t* a, uint64_t pol) {
+  int32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+
 template <int VEC, int K>
 struct RowAcc {
   float v[K][VEC];
@@ -72,6 +96,35 @@ struct RowAcc {
       }
     }
   }
+  // streaming (evict-first) row load / store, VEC == 4 only; falls back otherwise
+  __device__ __forceinline__ static void load_stream(const float* row, int d, float (&r)[K][VEC], uint64_t pol) {
+    if constexpr (VEC == 4) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        int c = lane_id() + 32 * k;
+        if (c * VEC < d) {
+          float4 x = ld_stream_f4(reinterpret_cast<const float4*>(row) + c, pol);
+          r[k][0] = x.x; r[k][1] = x.y; r[k][2] = x.z; r[k][3] = x.w;
+        } else {
+          r[k][0] = r[k][1] = r[k][2] = r[k][3] = 0.f;
+        }
+      }
+    } else {
+      load_rw(row, d, r);
+    }
+  }
+  __device__ __forceinline__ void store_stream(float* row, int d, uint64_t pol) const {
+    if constexpr (VEC == 4) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        int c = lane_id() + 32 * k;
+        if (c * VEC < d)
+          st_stream_f4(reinterpret_cast<float4*>(row) + c, make_float4(v[k][0], v[k][1], v[k][2], v[k][3]), pol);
+      }
+    } else {
+      store(row, d);
+    }
+  }
   __device__ __forceinline__ void fma(const float (&r)[K][VEC], float s) {
 #pragma unroll
     for (int k = 0; k < K; ++k)
@@ -114,7 +167,8 @@ struct RowAcc {
         int kb = c >> 5, cc = c & 31;
         float* blk = tbase + kb * 4096 + r * 32 + ((((cc >> 2) ^ (r & 7)) << 2) | (cc & 3));
         if constexpr (VEC == 4) {
-          *reinterpret_cast<float4*>(blk) = make_float4(v[k][0], v[k][1], v[k][2], v[k][3]);
+          st_stream_f4(reinterpret_cast<float4*>(blk), make_float4(v[k][0], v[k][1], v[k][2], v[k][3]),
+                       l2_evict_first_policy());
         } else if constexpr (VEC == 2) {
           *reinterpret_cast<float2*>(blk) = make_float2(v[k][0], v[k][1]);
         } else {
