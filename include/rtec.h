@@ -78,6 +78,12 @@ typedef struct {
   int64_t* num_edges;    /* [1] */
   float slack;           /* relocated / rebuilt runs get cap = len + max(min_slack, ceil(len*slack)) */
   int32_t min_slack;
+  /* Vertex sharding: this graph is the shard of rank
+   * part_rank out of part_count and holds exactly the edges whose dst it owns
+   * (owner(v) = v mod part_count).  part_count <= 1: unsharded.  apply
+   * validates the whole batch but probes / mutates only owned-dst updates. */
+  int32_t part_rank;
+  int32_t part_count;
 } rtec_graph_t;
 
 /* Internal status: the arena (or the in-place merge scratch) cannot hold this
@@ -102,6 +108,10 @@ typedef struct {
    * (-1, 0) for vertices without applied updates.  Caller initialises it once
    * to (-1, 0); rtec_batch_apply sets it, rtec_batch_commit resets it. */
   int32_t* irange;
+  /* Sharded runs: bitmap of vertices whose GLOBAL out-degree changed in this
+   * batch (rtec_shard_degrees); the frontier seeds Dg from it instead of the
+   * shard-local DegreeDelta.  NULL when unsharded. */
+  const uint32_t* dg_bm;
 } rtec_batch_t;
 
 /* Per-layer frontier (Alg. 4).  Bitmaps
@@ -114,6 +124,12 @@ typedef struct {
   int32_t* src_slot;   /* [n] vertex -> index in src_list (valid where bm_src bit set) */
   int32_t* dst_slot;   /* [n] vertex -> index in dst_list (valid where bm_dst bit set) */
   int64_t* counters;   /* [8] |E_curr|, |V_dst|, |S|, |R|, Σ outdeg(new S), Σ indeg(V_dst), Σ indeg(R), reserved */
+  /* Sharded runs: V_chg(l) over ALL ranks (union of every shard's V_dst(l),
+   * assembled by rtec_halo_unpack) and vertex -> row of the exchanged
+   * DeltaLog.  The next layer reads S(l+1) = S(l) ∪ bm_chg and old rows through
+   * chg_slot.  NULL: bm_dst / dst_slot (unsharded). */
+  uint32_t* bm_chg;
+  int32_t* chg_slot;
 } rtec_frontier_t;
 
 /* Layer descriptor (operators.py:42-47 LayerWeights + bundle flags).
@@ -196,6 +212,14 @@ int rtec_batch_coalesce(const int32_t* src, const int32_t* dst, const uint8_t* o
 int rtec_batch_apply(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src, const int32_t* dst,
                      const uint8_t* op, const int64_t* ts, int64_t B,
                      void* ws, size_t ws_bytes, rtec_stream_t stream);
+/* apply_batch in two phases (phase 1: validate + probe + plan, no mutation;
+ * phase 2: mutate; 3: both == rtec_batch_apply).  Sharded runs combine the
+ * ranks' status words between the phases so an error (or a full arena) on
+ * any rank leaves every shard untouched.  Both phases must see the same
+ * arguments and workspace. */
+int rtec_batch_apply_phase(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src, const int32_t* dst,
+                           const uint8_t* op, const int64_t* ts, int64_t B, int32_t phase,
+                           void* ws, size_t ws_bytes, rtec_stream_t stream);
 /* Close the batch: degree snapshots catch up (out_deg_prev = out_deg ...). */
 int rtec_batch_commit(rtec_graph_t* g, const rtec_batch_t* b, rtec_stream_t stream);
 
@@ -234,6 +258,36 @@ int rtec_update_gemm(const float* X, int64_t ldx, const float* W, int32_t d_in, 
  * ceil(d_in/32) * round_up(d_out,16) * 32 floats.  d_out <= 256. */
 int rtec_gemm_prepare_weights(const float* W, int32_t d_in, int32_t d_out, float* Bhi, float* Blo,
                               rtec_stream_t stream);
+
+/* ---- vertex sharding (one process per GPU) ---- */
+/* Global degrees from the globally applied set of a batch: `gstatus` is the
+ * per-update status after a MAX all-reduce over ranks (every update is owned
+ * by exactly one rank).  Updates gout/gin (replicated [n] arrays), marks the
+ * touched endpoints in bm_touch, writes dg_bm (global Dg: out-degree changed)
+ * and the global DegreeDelta rows (graph.py:225-230, ascending vertex). */
+int rtec_shard_degrees(int64_t n, const int32_t* src, const int32_t* dst, const uint8_t* op,
+                       const uint8_t* gstatus, int64_t B, int32_t* gout, const int32_t* gout_prev,
+                       int32_t* gin, const int32_t* gin_prev, uint32_t* bm_touch, uint32_t* dg_bm,
+                       int32_t* d_vertex, int32_t* d_old_in, int32_t* d_new_in, int32_t* d_old_out,
+                       int32_t* d_new_out, int64_t* n_delta, void* ws, size_t ws_bytes, rtec_stream_t stream);
+/* Close the batch on the global degree arrays (prev catch-up, bitmaps cleared). */
+int rtec_shard_commit(const int32_t* src, const int32_t* dst, const uint8_t* gstatus, int64_t B,
+                      const int32_t* gout, int32_t* gout_prev, const int32_t* gin, int32_t* gin_prev,
+                      uint32_t* bm_touch, uint32_t* dg_bm, rtec_stream_t stream);
+/* Halo exchange of one layer's changed rows.  pack: rows H[list[i]] (i <
+ * *n_list) -> send_rows[i], ids -> send_ids[i] (the collective itself is an
+ * all-gather issued by the host over NCCL).  unpack: recv holds `world`
+ * slots of `slot_cap` rows, counts[r] valid in slot r; for every received
+ * (u, row) at global position k: bm_chg bit u, chg_slot[u] = k, and
+ * glog[k] = pre-batch row (the replica's H[u] for remote u, which is then
+ * overwritten; local_log[dst_slot[u]] for owned u).  glog == NULL: replica
+ * refresh only (bootstrap).  *n_chg = Σ counts. */
+int rtec_halo_pack(const float* H, int32_t d, const int32_t* list, const int64_t* n_list, int64_t max_rows,
+                   int32_t* send_ids, float* send_rows, rtec_stream_t stream);
+int rtec_halo_unpack(const rtec_graph_t* g, int32_t d, const int32_t* recv_ids, const float* recv_rows,
+                     const int64_t* counts, int32_t world, int64_t slot_cap, float* H, const float* local_log,
+                     const int32_t* dst_slot, float* glog, uint32_t* bm_chg, int32_t* chg_slot, int32_t* chg_list,
+                     int64_t* n_chg, rtec_stream_t stream);
 
 /* materialize / query final-layer rows (SPEC materialize_h SPEC.md:379). */
 int rtec_query(const float* H, int64_t d, const int32_t* ids, int64_t k, float* out, int32_t n,

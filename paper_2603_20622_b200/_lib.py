@@ -36,7 +36,7 @@ class Graph(C.Structure):
     _fields_ = [
         ("n", I64), ("out", Adj), ("inn", Adj),
         ("out_deg", P), ("in_deg", P), ("out_deg_prev", P), ("in_deg_prev", P),
-        ("num_edges", P), ("slack", F32), ("min_slack", I32),
+        ("num_edges", P), ("slack", F32), ("min_slack", I32), ("part_rank", I32), ("part_count", I32),
     ]
 
 
@@ -46,14 +46,14 @@ class Batch(C.Structure):
         ("a_src", P), ("a_dst", P), ("a_op", P), ("a_ts", P), ("n_applied", P),
         ("i_src", P), ("i_dst", P), ("i_op", P),
         ("d_vertex", P), ("d_old_in", P), ("d_new_in", P), ("d_old_out", P), ("d_new_out", P),
-        ("n_delta", P), ("irange", P),
+        ("n_delta", P), ("irange", P), ("dg_bm", P),
     ]
 
 
 class Frontier(C.Structure):
     _fields_ = [
         ("bm_src", P), ("bm_dst", P), ("src_list", P), ("n_src", P), ("dst_list", P), ("n_dst", P),
-        ("src_slot", P), ("dst_slot", P), ("counters", P),
+        ("src_slot", P), ("dst_slot", P), ("counters", P), ("bm_chg", P), ("chg_slot", P),
     ]
 
 
@@ -82,7 +82,12 @@ _SIGS = {
     "rtec_adj_export": (C.c_int, [I64, C.POINTER(Adj), P, P, P, P, SZ, P]),
     "rtec_batch_coalesce": (C.c_int, [P, P, P, P, I64, P, P, P, P, P, P, SZ, P]),
     "rtec_batch_apply": (C.c_int, [C.POINTER(Graph), C.POINTER(Batch), P, P, P, P, I64, P, SZ, P]),
+    "rtec_batch_apply_phase": (C.c_int, [C.POINTER(Graph), C.POINTER(Batch), P, P, P, P, I64, I32, P, SZ, P]),
     "rtec_batch_commit": (C.c_int, [C.POINTER(Graph), C.POINTER(Batch), P]),
+    "rtec_shard_degrees": (C.c_int, [I64, P, P, P, P, I64, P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
+    "rtec_shard_commit": (C.c_int, [P, P, P, I64, P, P, P, P, P, P, P]),
+    "rtec_halo_pack": (C.c_int, [P, I32, P, P, I64, P, P, P]),
+    "rtec_halo_unpack": (C.c_int, [C.POINTER(Graph), I32, P, P, P, I32, I64, P, P, P, P, P, P, P, P, P]),
     "rtec_frontier_layer": (C.c_int, [C.POINTER(Graph), C.POINTER(Batch), I32, I32, C.POINTER(Frontier),
                                       C.POINTER(Frontier), P, SZ, P]),
     "rtec_layer_incremental": (C.c_int, [C.POINTER(Graph), C.POINTER(Batch), C.POINTER(Layer), C.POINTER(State),

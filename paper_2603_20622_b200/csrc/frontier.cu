@@ -203,10 +203,15 @@ extern "C" int rtec_frontier_layer(const rtec_graph_t* g, const rtec_batch_t* b,
   if (l == 0) {
     RTEC_CUDA(cudaMemsetAsync(f->bm_src, 0, sizeof(uint32_t) * words, s));
     RTEC_CUDA(cudaMemsetAsync(f->bm_dst, 0, sizeof(uint32_t) * words, s));
-    k_seed_layer0<<<grid_for(b->cap * 2, kFBlk), kFBlk, 0, s>>>(*b, src_degree_dependent, f->bm_src, f->bm_dst);
+    // sharded: Dg is the global out-degree change set, not the shard's DegreeDelta
+    k_seed_layer0<<<grid_for(b->cap * 2, kFBlk), kFBlk, 0, s>>>(*b, b->dg_bm ? 0 : src_degree_dependent, f->bm_src,
+                                                                 f->bm_dst);
+    if (b->dg_bm && src_degree_dependent)
+      k_union_words<<<grid_for(words, kFBlk), kFBlk, 0, s>>>(f->bm_src, b->dg_bm, f->bm_src, words);
   } else {
-    // S(l) = S(l-1) ∪ V_dst(l-1); V_dst(l) starts as V_dst(l-1)
-    k_union_words<<<grid_for(words, kFBlk), kFBlk, 0, s>>>(prev->bm_src, prev->bm_dst, f->bm_src, words);
+    // S(l) = S(l-1) ∪ V_chg(l-1); V_dst(l) starts as V_dst(l-1) (this shard's part when sharded)
+    const uint32_t* chg = prev->bm_chg ? prev->bm_chg : prev->bm_dst;
+    k_union_words<<<grid_for(words, kFBlk), kFBlk, 0, s>>>(prev->bm_src, chg, f->bm_src, words);
     RTEC_CUDA(cudaMemcpyAsync(f->bm_dst, prev->bm_dst, sizeof(uint32_t) * words, cudaMemcpyDeviceToDevice, s));
     prev_src = prev->bm_src;
   }

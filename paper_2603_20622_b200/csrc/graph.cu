@@ -216,14 +216,22 @@ __global__ void k_apply_dups(const uint64_t* __restrict__ sk, const uint32_t* __
 }
 
 // existence probe of each (sorted) update in the pre-batch out-run of its src
+// Sharded graphs (part_count > 1) probe only the updates whose dst they own;
+// the others are neither applied nor reported here (status 0) -- their owner
+// rank applies them and the host combines the ranks' statuses.
 __global__ void k_apply_probe(const uint64_t* __restrict__ sk, const uint32_t* __restrict__ sv, int64_t B, int64_t n,
                               rtec_adj_t out, const uint8_t* __restrict__ op, uint8_t* status, uint8_t* aflag,
-                              const uint64_t* err) {
+                              int32_t part_rank, int32_t part_count, const uint64_t* err) {
   if (err_set(err)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t k = sk[i];
     int32_t s = static_cast<int32_t>(k / static_cast<uint64_t>(n));
     int32_t d = static_cast<int32_t>(k - static_cast<uint64_t>(s) * n);
+    if (part_count > 1 && d % part_count != part_rank) {
+      status[sv[i]] = 0;
+      aflag[i] = 0;
+      continue;
+    }
     int64_t b = out.beg[s];
     int32_t L = out.len[s];
     int64_t p = lower_bound_dev(out.nbr, b, b + L, d);
@@ -749,15 +757,30 @@ int rtec_batch_coalesce(const int32_t* src, const int32_t* dst, const uint8_t* o
 
 int rtec_batch_apply(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src, const int32_t* dst, const uint8_t* op,
                      const int64_t* ts, int64_t B, void* ws, size_t ws_bytes, rtec_stream_t stream) {
+  return rtec_batch_apply_phase(g, b, src, dst, op, ts, B, 3, ws, ws_bytes, stream);
+}
+
+// Phase 1 (plan) and phase 2 (mutate) carve the workspace identically, so the
+// merge plans phase 1 leaves in it are the ones phase 2 executes.
+int rtec_batch_apply_phase(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src, const int32_t* dst,
+                           const uint8_t* op, const int64_t* ts, int64_t B, int32_t phase, void* ws, size_t ws_bytes,
+                           rtec_stream_t stream) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   int64_t n = g->n;
   if (B > b->cap) {
     set_error("batch of %lld updates exceeds capacity %lld", (long long)B, (long long)b->cap);
     return RTEC_SHAPE_ERROR;
   }
-  RTEC_CUDA(cudaMemsetAsync(b->err, 0xff, sizeof(uint64_t), s));
-  RTEC_CUDA(cudaMemsetAsync(b->n_applied, 0, sizeof(int64_t), s));
-  RTEC_CUDA(cudaMemsetAsync(b->n_delta, 0, sizeof(int64_t), s));
+  if (phase < 1 || phase > 3) {
+    set_error("apply phase %d not in {1, 2, 3}", phase);
+    return RTEC_CONFIG_ERROR;
+  }
+  const bool plan = phase & 1, exec = phase & 2;
+  if (plan) {
+    RTEC_CUDA(cudaMemsetAsync(b->err, 0xff, sizeof(uint64_t), s));
+    RTEC_CUDA(cudaMemsetAsync(b->n_applied, 0, sizeof(int64_t), s));
+    RTEC_CUDA(cudaMemsetAsync(b->n_delta, 0, sizeof(int64_t), s));
+  }
   if (B <= 0) return RTEC_OK;
   RTEC_PROF("batch_apply", s);
   Ws w(ws, ws_bytes);
@@ -779,15 +802,19 @@ int rtec_batch_apply(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src, const
   RTEC_WS_CHECK(w);
   size_t mark = w.off;
   const int grid = grid_for(B, kBlk);
+  int bits = bits_for(static_cast<uint64_t>(n) * static_cast<uint64_t>(n));
+  MergeIn mo{b->a_src, b->a_dst, b->a_op, b->a_ts, b->n_applied, B};
+  MergeIn mi{b->i_dst, b->i_src, b->i_op, nullptr, b->n_applied, B};
+  if (plan) {
   // 1. keys + range validation; 2. sort; 3. duplicate validation
   k_apply_keys<<<grid, kBlk, 0, s>>>(src, dst, B, n, keys, vals, b->err);
-  int bits = bits_for(static_cast<uint64_t>(n) * static_cast<uint64_t>(n));
   RTEC_TRY(sort_pairs(keys, vals, sk, sv, Count{nullptr, B}, B, bits, w, s));
   w.off = mark;
   k_apply_dups<<<grid, kBlk, 0, s>>>(sk, sv, B, n, b->err);
   // 4. probe against the pre-batch graph (skipped on validation error: no flags -> nothing applied)
   RTEC_CUDA(cudaMemsetAsync(aflag, 0, B, s));
-  k_apply_probe<<<grid, kBlk, 0, s>>>(sk, sv, B, n, g->out, op, b->status, aflag, b->err);
+  k_apply_probe<<<grid, kBlk, 0, s>>>(sk, sv, B, n, g->out, op, b->status, aflag, g->part_rank, g->part_count,
+                                      b->err);
   // 5. applied updates in out-key order
   RTEC_TRY(exclusive_scan(FlagAt{aflag}, Count{nullptr, B}, B,
                           CompactApplied{aflag, sk, sv, n, op, ts, b->a_src, b->a_dst, b->a_op, b->a_ts},
@@ -799,12 +826,12 @@ int rtec_batch_apply(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src, const
   w.off = mark;
   k_in_gather<<<grid, kBlk, 0, s>>>(sv, b->n_applied, b->a_src, b->a_dst, b->a_op, b->i_src, b->i_dst, b->i_op);
   // 7. plan both merges (no mutation; all-or-nothing arena reservation)
-  MergeIn mo{b->a_src, b->a_dst, b->a_op, b->a_ts, b->n_applied, B};
-  MergeIn mi{b->i_dst, b->i_src, b->i_op, nullptr, b->n_applied, B};
   RTEC_TRY(merge_plan(mo, po, g->out, g->slack, g->min_slack, b->err, w, s));
   w.off = mark;
   RTEC_TRY(merge_plan(mi, pi, g->in, g->slack, g->min_slack, b->err, w, s));
   w.off = mark;
+  }
+  if (!exec) return RTEC_OK;
   // 8. mutate: degrees, runs, per-destination ranges
   k_irange_set<<<grid, kBlk, 0, s>>>(b->i_dst, b->n_applied, reinterpret_cast<int2*>(b->irange), b->err);
   k_apply_degrees<<<grid, kBlk, 0, s>>>(b->a_src, b->a_dst, b->a_op, b->n_applied, g->out_deg, g->in_deg,

@@ -778,8 +778,9 @@ int rtec_layer_incremental(const rtec_graph_t* g, const rtec_batch_t* b, const r
   a.L = *L;
   a.st = *st;
   a.f = *f;
-  a.prev_bm_dst = prev ? prev->bm_dst : nullptr;
-  a.prev_slot = prev ? prev->dst_slot : nullptr;
+  // V_chg(l-1) and its DeltaLog rows: all ranks' changed vertices when sharded
+  a.prev_bm_dst = prev ? (prev->bm_chg ? prev->bm_chg : prev->bm_dst) : nullptr;
+  a.prev_slot = prev ? (prev->chg_slot ? prev->chg_slot : prev->dst_slot) : nullptr;
   a.err = err;
   const int grid = kSMs * 8;
   if (L->model == RTEC_MODEL_GAT) {

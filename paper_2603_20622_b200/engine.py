@@ -62,11 +62,14 @@ class _Frontier:
         self.n_src, self.n_dst = z(1, torch.int64), z(1, torch.int64)
         self.src_slot, self.dst_slot = z(n, torch.int32), z(n, torch.int32)
         self.counters = z(8, torch.int64)
+        # sharded runs (shard.py): V_chg(l) over all ranks + exchanged DeltaLog slots
+        self.bm_chg = self.chg_slot = self.chg_list = self.n_chg = None
 
     def c(self):
         p = _lib.ptr
         return _lib.Frontier(p(self.bm_src), p(self.bm_dst), p(self.src_list), p(self.n_src), p(self.dst_list),
-                             p(self.n_dst), p(self.src_slot), p(self.dst_slot), p(self.counters))
+                             p(self.n_dst), p(self.src_slot), p(self.dst_slot), p(self.counters), p(self.bm_chg),
+                             p(self.chg_slot))
 
 
 class RTECEngine:

@@ -138,6 +138,8 @@ class DynamicGraph:
         self.ws = torch.empty(0, dtype=torch.uint8, device=self.dev)
         self.batch = DeviceBatch(1024, self.dev, n)
         self.m_hint = 0
+        # vertex sharding (shard.py): this graph holds the edges whose dst it owns
+        self.part_rank, self.part_count = 0, 1
         self._build(np.zeros(0, np.int32), np.zeros(0, np.int32), None)
 
     # ---------------------------------------------------------------- build
@@ -192,7 +194,8 @@ class DynamicGraph:
     def c(self) -> _lib.Graph:
         p = _lib.ptr
         return _lib.Graph(self.n, self.out.c(), self.inn.c(), p(self.out_deg), p(self.in_deg), p(self.out_deg_prev),
-                          p(self.in_deg_prev), p(self.num_edges_t), self.slack, self.min_slack)
+                          p(self.in_deg_prev), p(self.num_edges_t), self.slack, self.min_slack, self.part_rank,
+                          self.part_count)
 
     @classmethod
     def from_edges(cls, num_vertices: int, edges, **kw) -> "DynamicGraph":
@@ -336,14 +339,17 @@ class DynamicGraph:
                     dst_t[:B].copy_(torch.from_numpy(np.ascontiguousarray(arr, dt)))
         return B
 
-    def apply_staged(self, B: int) -> None:
-        """Enqueue rtec_batch_apply on the staged batch (no host sync)."""
-        g, b = self.c(), self.batch.c()
-        self._gc, self._bc = g, b  # keep the structs alive for later calls of the same batch
+    def apply_staged(self, B: int, phase: int = 3) -> None:
+        """Enqueue rtec_batch_apply on the staged batch (no host sync).  phase 1
+        validates + plans (no mutation), 2 mutates, 3 both."""
+        if phase & 1:
+            self._gc, self._bc = self.c(), self.batch.c()  # kept alive for later calls of the same batch
+        g, b = self._gc, self._bc
         p = _lib.ptr
         bb = self.batch
-        _lib.check(self.lib.rtec_batch_apply(C.byref(g), C.byref(b), p(bb.src), p(bb.dst), p(bb.op), p(bb.ts), B,
-                                             p(self.ws), self.ws.numel(), _lib.stream_handle()), "apply_batch")
+        _lib.check(self.lib.rtec_batch_apply_phase(C.byref(g), C.byref(b), p(bb.src), p(bb.dst), p(bb.op), p(bb.ts),
+                                                   B, phase, p(self.ws), self.ws.numel(), _lib.stream_handle()),
+                   "apply_batch")
 
     def commit(self) -> None:
         g, b = self.c(), self.batch.c()

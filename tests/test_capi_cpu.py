@@ -58,8 +58,9 @@ def test_struct_layouts_match_header(lib):
     mirror = [_lib.Adj, _lib.Graph, _lib.Batch, _lib.Frontier, _lib.Layer, _lib.State]
     assert list(sizes) == [ctypes.sizeof(t) for t in mirror]
     assert ctypes.sizeof(_lib.Adj) == 8 * 7
-    assert ctypes.sizeof(_lib.Graph) == 8 + 2 * 56 + 5 * 8 + 8
-    assert ctypes.sizeof(_lib.Batch) == 8 * 18
+    assert ctypes.sizeof(_lib.Graph) == 8 + 2 * 56 + 5 * 8 + 8 + 8  # + part_rank / part_count
+    assert ctypes.sizeof(_lib.Batch) == 8 * 19
+    assert ctypes.sizeof(_lib.Frontier) == 8 * 11
     assert ctypes.sizeof(_lib.Layer) == 6 * 4 + 7 * 8
     assert ctypes.sizeof(_lib.State) == 13 * 8
 
