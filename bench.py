@@ -19,9 +19,10 @@ Arms
 
 Timing: W warm-up steps, then K steps bracketed by barrier + synchronize,
 CUDA events per step on the engine's stream, L2 flushed (256 MiB write)
-between timed steps, max over ranks.  Multi-GPU (torchrun): every rank runs
-an independent replica on its own stream of batches ("replicas only" this
-round, scaling weak; the vertex-sharded halo path is DESIGN.md §6 next).
+between timed steps, max over ranks.  Multi-GPU (torchrun): the graph is
+vertex-sharded over the ranks (owner = v mod N, paper_2603_20622_b200/shard.py)
+and every batch runs once across all of them with one halo exchange per layer
+over NCCL; total work is fixed as N grows (scaling "strong").
 """
 
 from __future__ import annotations
@@ -75,8 +76,14 @@ def dist_init():
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # RTEC_BENCH_BACKEND=gloo: ranks may share one GPU (smoke runs of the sharded path on a 1-GPU box)
+        if os.environ.get("RTEC_BENCH_BACKEND", "nccl") == "gloo":
+            local = local % max(torch.cuda.device_count(), 1)
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return world, rank, local
@@ -95,7 +102,7 @@ def max_over_ranks(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -106,7 +113,7 @@ def sum_over_ranks(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
@@ -209,9 +216,18 @@ def run_ours(args, world, rank, local):
     t0 = time.time()
     stream, batches, X = make_workload(wl, W + K + E2E, dev)
     bs, bd, bt = stream.base()
-    g = P.DynamicGraph.from_tensors(wl["n"], torch.as_tensor(bs, device=dev), torch.as_tensor(bd, device=dev),
-                                    torch.as_tensor(bt, device=dev), reserve=max(1 << 20, wl["m"] // 2))
-    eng = P.RTECEngine(P.make_bundle(wl["model"], wl["dims"], heads=wl["heads"]), g, X, max_batch=wl["batch"])
+    bundle = P.make_bundle(wl["model"], wl["dims"], heads=wl["heads"])
+    sharded = world > 1
+    if sharded:  # vertex-sharded over the ranks: one halo exchange per layer over NCCL
+        from paper_2603_20622_b200.shard import Comm, ShardedRTECEngine
+
+        eng = ShardedRTECEngine(bundle, wl["n"], tuple(torch.as_tensor(a, device=dev) for a in (bs, bd, bt)), X,
+                                Comm(), max_batch=wl["batch"], reserve=max(1 << 20, wl["m"] // (2 * world)))
+        g = eng.g
+    else:
+        g = P.DynamicGraph.from_tensors(wl["n"], torch.as_tensor(bs, device=dev), torch.as_tensor(bd, device=dev),
+                                        torch.as_tensor(bt, device=dev), reserve=max(1 << 20, wl["m"] // 2))
+        eng = P.RTECEngine(bundle, g, X, max_batch=wl["batch"])
     torch.cuda.synchronize()
     setup_s = time.time() - t0
     lib = _lib.load()
@@ -227,13 +243,20 @@ def run_ours(args, world, rank, local):
     napp = torch.zeros(K, dtype=torch.int64, device=dev)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
 
-    def stage(i):
+    def run_step(i):
+        """One batch from HBM-resident tensors; returns B.  Unsharded: enqueue only
+        (no host sync inside the batch).  Sharded: step() synchronises for the
+        error-word combine and the exchange counts."""
         op, s, d, t = dev_batches[i]
+        if sharded:
+            eng.step(op, s, d, t)
+            return int(op.numel())
         B = g.stage(op, s, d, t)
+        eng.enqueue_step(B)
         return B
 
     for i in range(W):
-        eng.enqueue_step(stage(i))
+        run_step(i)
     torch.cuda.synchronize()
     barrier(world)
     clocks = Clocks(local, enabled=not (args.no_clocks or args.profile))
@@ -245,11 +268,10 @@ def run_ours(args, world, rank, local):
     total_updates = 0
     for k in range(K):
         flush.zero_()  # L2 flush between timed steps (outside the events)
-        B = stage(W + k)
-        total_updates += B
         evs[k][0].record()
-        eng.enqueue_step(B)
+        B = run_step(W + k)
         evs[k][1].record()
+        total_updates += B
         errs[k : k + 1].copy_(g.batch.err)
         napp[k : k + 1].copy_(g.batch.n_applied)
         for l in range(L):
@@ -345,13 +367,15 @@ def run_ours(args, world, rank, local):
         "p50_batch_ms": round(p50, 4),
         "p90_batch_ms": round(p90, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if sharded else "weak",
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (seeded Chung-Lu graph, U(-1,1) features, make_bundle seed-0 weights)",
         "config": {"workload": args.workload, "desc": wl["desc"], "vertices": wl["n"], "edges": wl["m"],
                    "model": wl["model"], "dims": wl["dims"], "batch_updates": wl["batch"],
-                   "batch_fraction": round(wl["batch"] / wl["m"], 6), "parallelism": f"replicas x{world}",
+                   "batch_fraction": round(wl["batch"] / wl["m"], 6),
+                   "parallelism": f"vertex-sharded x{world} (owner = v mod {world}, halo all-gather per layer)"
+                   if sharded else "single GPU",
                    "l2": "flushed between timed steps (256 MiB write)"},
         "e2e": {"value": round(e2e_val, 1) if e2e_val else None, "unit": "edge updates/s", "steps": E2E,
                 "h2d_bytes_per_step": h2d // max(E2E, 1), "d2h_bytes_per_step": d2h // max(E2E, 1),
