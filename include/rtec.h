@@ -49,8 +49,10 @@ enum {
 /* update ops (graph.py:28-30) */
 enum { RTEC_OP_INSERT = 0, RTEC_OP_DELETE = 1 };
 
-/* models (models.py:42-52); only the hot-path four are implemented */
-enum { RTEC_MODEL_GCN = 0, RTEC_MODEL_SAGE = 1, RTEC_MODEL_GIN = 2, RTEC_MODEL_GAT = 3 };
+/* models (models.py:42-52); the hot-path four, plus GIN with an elementwise
+ * max aggregator (configs[3]; no reference counterpart -- retract-and-recompute
+ * per destination) */
+enum { RTEC_MODEL_GCN = 0, RTEC_MODEL_SAGE = 1, RTEC_MODEL_GIN = 2, RTEC_MODEL_GAT = 3, RTEC_MODEL_GIN_MAX = 4 };
 
 /* One direction of the adjacency: gapped per-vertex runs.  Run of v is
  * nbr[beg[v] .. beg[v]+len[v]) ascending, with cap[v] >= len[v] slots reserved.

@@ -86,6 +86,8 @@ class OracleEngine:
             vdst[Id] = True
             vdst[Dd] = True
             R = (vdst & chg_prev) if b.dest_dependent else np.zeros(n, bool)
+            if b.model == M.GIN_MAX:  # max has no inverse: the oracle recomputes every affected row
+                R = vdst.copy()
             inc = vdst & ~R
             frontier.append(
                 dict(vdst=np.flatnonzero(vdst), R=np.flatnonzero(R),

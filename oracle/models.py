@@ -27,7 +27,11 @@ import numpy as np
 import scipy.sparse as sp
 
 GCN, SAGE, GIN, GAT = "gcn", "graphsage", "gin", "gat"
-MODELS = (GCN, SAGE, GIN, GAT)
+# GIN with an elementwise-max aggregator: NOT in the reference (no max
+# aggregator exists in models.py); restated here as the full recompute
+# a_v = max_{u in N_in(v)} h_u (0 for an empty neighbourhood), GIN update.
+GIN_MAX = "gin_max"
+MODELS = (GCN, SAGE, GIN, GAT, GIN_MAX)
 
 
 def _mat(rng, rows, cols):  # models.py:56-58
@@ -77,7 +81,7 @@ def make_bundle(model, dims, *, rng_seed=0, degree_smoothing=True, heads=1) -> O
     if model in (GCN, SAGE):  # models.py:88-96, :124-128
         for i, o in pairs:
             layers.append({"W": _mat(rng, o, i)})
-    elif model == GIN:  # models.py:178-183 (W then W2, layer by layer)
+    elif model in (GIN, GIN_MAX):  # models.py:178-183 (W then W2, layer by layer)
         for i, o in pairs:
             W = _mat(rng, o, i)
             W2 = _mat(rng, o, o)
@@ -107,7 +111,7 @@ def make_bundle(model, dims, *, rng_seed=0, degree_smoothing=True, heads=1) -> O
     elif model == SAGE:  # :131-141
         b.ctx_kind = "count"
         b.agg_dims = dims[:-1]
-    elif model == GIN:  # :191-200
+    elif model in (GIN, GIN_MAX):  # :191-200
         b.ctx_kind = "none"
         b.agg_dims = dims[:-1]
     else:  # GAT :276-287
@@ -142,7 +146,7 @@ def update(b: OracleBundle, l: int, h_v, a_v):
     L = b.layers[l]
     if b.model in (GCN, SAGE):  # models.py:107-108, :137: relu(W a)
         return np.maximum(a_v @ L["W"].T, 0.0)
-    if b.model == GIN:  # models.py:187-189: W2 relu(W (h_v + a_v))
+    if b.model in (GIN, GIN_MAX):  # models.py:187-189: W2 relu(W (h_v + a_v))
         return np.maximum((h_v + a_v) @ L["W"].T, 0.0) @ L["W2"].T
     # GAT models.py:282: elu(a) (linalg.py:41-43)
     return np.where(a_v >= 0, a_v, np.expm1(np.minimum(a_v, 0)))
@@ -207,6 +211,13 @@ def layer_full(b: OracleBundle, l: int, g, H_prev, rows=None):
         A[empty] = 0.0
         C[empty] = 0.0
         C = C[:, 0] if heads == 1 else C
+    elif b.model == GIN_MAX:
+        S = np.full((rows.size, H_prev.shape[1]), -np.inf)
+        np.maximum.at(S, e_row, H_prev[e_src])
+        empty = cnt == 0
+        S[empty] = 0.0
+        A = S
+        C = np.ones(rows.size)
     else:
         with np.errstate(divide="ignore"):  # raw GCN: sources with no out-edges never appear
             c = src_coeff(b, g.out_deg)

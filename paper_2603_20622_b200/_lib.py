@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "librtec.so")
 
 OP_INSERT = 0
 OP_DELETE = 1
-MODEL_IDS = {"gcn": 0, "graphsage": 1, "gin": 2, "gat": 3}
+MODEL_IDS = {"gcn": 0, "graphsage": 1, "gin": 2, "gat": 3, "gin_max": 4}
 ARENA_FULL = 8
 ERR_OK = (1 << 64) - 1
 

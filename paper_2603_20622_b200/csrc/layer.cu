@@ -30,6 +30,10 @@ __device__ __forceinline__ float src_coeff(int model, int32_t deg, float off) {
   return model == RTEC_MODEL_GCN ? 1.0f / sqrtf(static_cast<float>(deg) + off) : 1.0f;
 }
 
+__host__ __device__ __forceinline__ bool is_gin(int model) {
+  return model == RTEC_MODEL_GIN || model == RTEC_MODEL_GIN_MAX;
+}
+
 __device__ __forceinline__ float leaky02(float x) { return x < 0.f ? 0.2f * x : x; }  // models.py:272-273
 __device__ __forceinline__ float elu1(float x) { return x >= 0.f ? x : expm1f(x); }   // linalg.py:41-43
 
@@ -192,7 +196,7 @@ __device__ __forceinline__ void agg_finalize(const LayerArgs& a, int64_t i, int3
   R out;
   out.zero();
   out.fma(acc.v, scale);
-  if (a.L.model == RTEC_MODEL_GIN) {  // update input h_v + a_v (models.py:187-189)
+  if (is_gin(a.L.model)) {  // update input h_v + a_v (models.py:187-189)
     float h[K][VEC];
     R::load(a.st.H_in + static_cast<int64_t>(v) * d + a.c0, cw, h);
     out.add(h);
@@ -407,6 +411,159 @@ static int launch_aggregation(LayerArgs& a, AggRows rows, int64_t max_rows, int6
     return RTEC_SHAPE_ERROR;
   }
   RTEC_LAUNCH_CHECK("aggregation");
+  return RTEC_OK;
+}
+
+// ------------------------------------------------------------------ GIN-max (K16)
+// a_v = max_{u in N_in(v)} h_u elementwise (0 for an empty neighbourhood); the
+// cached S row is the max itself.  Incremental (retract-and-recompute): new
+// values of inserted / value-changed sources can only raise the max, so
+// S' = max(S, new rows) -- unless a retracted value (old row of a deleted or
+// value-changed source) attained the cached max in some column and did not
+// stay at least as large, in which case that destination is re-maxed over its
+// whole post-batch in-run.  Max is exact, so S' is bit-identical to a full
+// recompute in the same precision.
+template <int VEC, int K>
+__device__ __forceinline__ void max_row(const float (&r)[K][VEC], RowAcc<VEC, K>& acc) {
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) acc.v[k][j] = fmaxf(acc.v[k][j], r[k][j]);
+}
+
+template <int VEC, int K>
+__device__ __forceinline__ void max_full_run(const LayerArgs& a, int64_t beg, int32_t len, RowAcc<VEC, K>& acc) {
+  using R = RowAcc<VEC, K>;
+  const int d = a.d_agg;
+  const int lane = lane_id();
+  for (int32_t c0 = 0; c0 < len; c0 += 32) {
+    int32_t j = c0 + lane;
+    int32_t u = j < len ? a.g.in.nbr[beg + j] : 0;
+    int cnt = min(32, len - c0);
+    for (int t = 0; t < cnt; t += 4) {
+      float r[4][K][VEC];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int32_t uu = __shfl_sync(0xffffffffu, u, min(t + q, cnt - 1));
+        R::load(a.st.H_in + static_cast<int64_t>(uu) * d, d, r[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) max_row<VEC, K>(r[q], acc);  // repeats of the last row are harmless
+    }
+  }
+}
+
+template <int VEC, int K, bool FULL>
+__global__ void __launch_bounds__(kLBlk) k_max_layer(LayerArgs a, AggRows rows) {
+  using R = RowAcc<VEC, K>;
+  if (!FULL && err_set(a.err)) return;
+  const int d = a.d_agg;
+  const int64_t nr = rows.count();
+  const int lane = lane_id();
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < nr; i += nw) {
+    int32_t v = rows.at(i);
+    int64_t beg = a.g.in.beg[v];
+    int32_t len = a.g.in.len[v];
+    float* srow = a.st.S + static_cast<int64_t>(v) * d;
+    R acc;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) acc.v[k][j] = -INFINITY;
+    bool rescan = FULL;
+    if (!FULL && len > 0) {
+      int64_t p = 0, q = 0;
+      int2 rg = reinterpret_cast<const int2*>(a.b.irange)[v];
+      if (rg.x >= 0) {
+        p = rg.x;
+        q = rg.x + rg.y;
+      }
+      const bool had = a.g.in_deg_prev[v] > 0;
+      float sv[K][VEC];
+      R::load_rw(srow, d, sv);
+      bool retract = false;
+      // value-changed sources (u in S(l), edge not inserted)
+      if (*a.f.n_src > 0) {
+        for (int32_t c0 = 0; c0 < len; c0 += 32) {
+          int32_t j = c0 + lane;
+          int32_t u = 0;
+          bool hit = false;
+          if (j < len) {
+            u = a.g.in.nbr[beg + j];
+            hit = bm_test(a.f.bm_src, u) && !in_range_has(a.b.i_src, p, q, u);
+          }
+          unsigned m = __ballot_sync(0xffffffffu, hit);
+          while (m) {
+            int src = __ffs(m) - 1;
+            m &= m - 1;
+            int32_t uu = __shfl_sync(0xffffffffu, u, src);
+            float hn[K][VEC], ho[K][VEC];
+            R::load(a.st.H_in + static_cast<int64_t>(uu) * d, d, hn);
+            const float* orow = a.st.H_in + static_cast<int64_t>(uu) * d;
+            if (a.prev_bm_dst && bm_test(a.prev_bm_dst, uu))
+              orow = a.st.log_in + static_cast<int64_t>(a.prev_slot[uu]) * d;
+            R::load(orow, d, ho);
+            max_row<VEC, K>(hn, acc);
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+#pragma unroll
+              for (int jj = 0; jj < VEC; ++jj)
+                retract |= R::has(k, d) && ho[k][jj] >= sv[k][jj] && hn[k][jj] < ho[k][jj];
+          }
+        }
+      }
+      // structural edges: inserts raise, deletes may retract the max
+      for (int64_t kk = p; kk < q; ++kk) {
+        int32_t u = a.b.i_src[kk];
+        float r[K][VEC];
+        if (a.b.i_op[kk] == RTEC_OP_INSERT) {
+          R::load(a.st.H_in + static_cast<int64_t>(u) * d, d, r);
+          max_row<VEC, K>(r, acc);
+        } else {
+          const float* orow = a.st.H_in + static_cast<int64_t>(u) * d;
+          if (a.prev_bm_dst && bm_test(a.prev_bm_dst, u)) orow = a.st.log_in + static_cast<int64_t>(a.prev_slot[u]) * d;
+          R::load(orow, d, r);
+#pragma unroll
+          for (int k = 0; k < K; ++k)
+#pragma unroll
+            for (int jj = 0; jj < VEC; ++jj) retract |= R::has(k, d) && r[k][jj] >= sv[k][jj];
+        }
+      }
+      rescan = had && __any_sync(0xffffffffu, retract);
+      if (!rescan && had) max_row<VEC, K>(sv, acc);
+    }
+    if (rescan) {
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) acc.v[k][j] = -INFINITY;
+      max_full_run<VEC, K>(a, beg, len, acc);
+    }
+    if (len == 0) acc.zero();  // empty neighbourhood -> zero aggregate
+    acc.store(srow, d);
+    R out;
+    out.zero();
+    out.add(acc.v);
+    float h[K][VEC];
+    R::load(a.st.H_in + static_cast<int64_t>(v) * d, d, h);
+    out.add(h);  // GIN update input h_v + a_v (models.py:187-189)
+    if (a.tc_nkb > 0) out.store_tiled(a.st.gemm_in, i, 0, d, d, a.tc_nkb);
+    else out.store(a.st.gemm_in + i * d, d);
+  }
+}
+
+template <bool FULL>
+static int launch_max(LayerArgs& a, AggRows rows, cudaStream_t s) {
+  const int grid = kSMs * 8;
+  RTEC_PROF(FULL ? "k_max_full" : "k_max_inc", s);
+  bool ok = RTEC_ROW_DISPATCH(a.d_agg, (k_max_layer<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows)));
+  if (!ok) {
+    set_error("row width %d unsupported", a.d_agg);
+    return RTEC_SHAPE_ERROR;
+  }
+  RTEC_LAUNCH_CHECK("k_max_layer");
   return RTEC_OK;
 }
 
@@ -714,7 +871,7 @@ static int run_update(const rtec_layer_t* L, rtec_state_t* st, const int64_t* n_
                       const int32_t* y_rows, float* log, const uint64_t* err, cudaStream_t s);
 
 static int layer_dims_ok(const rtec_layer_t* L) {
-  if (L->model < 0 || L->model > 3) {
+  if (L->model < 0 || L->model > RTEC_MODEL_GIN_MAX) {
     set_error("unsupported model id %d", L->model);
     return RTEC_UNSUPPORTED_MODEL;
   }
@@ -729,7 +886,7 @@ static int run_update(const rtec_layer_t* L, rtec_state_t* st, const int64_t* n_
                       const int32_t* y_rows, float* log, const uint64_t* err, cudaStream_t s) {
   if (L->Wt_hi) {
     const int nkb = tc_nkb_of(L->d_in);
-    if (L->model == RTEC_MODEL_GIN) {  // W2 relu(W (h + a)) (models.py:187-189), hidden kept in tile layout
+    if (is_gin(L->model)) {  // W2 relu(W (h + a)) (models.py:187-189), hidden kept in tile layout
       const int nkb2 = tc_nkb_of(L->d_out);
       TcArgs t1{st->gemm_in, L->Wt_hi, L->Wt_lo, nkb, tc_npad_of(L->d_out), L->d_out, n_rows, max_rows, 1,
                 nullptr, 0, nullptr, nullptr, st->gemm_mid, nkb2, err};
@@ -742,7 +899,7 @@ static int run_update(const rtec_layer_t* L, rtec_state_t* st, const int64_t* n_
              st->H_out, L->d_out, y_rows, log, nullptr, 0, err};
     return gemm_tc_launch(t, s);
   }
-  if (L->model == RTEC_MODEL_GIN) {
+  if (is_gin(L->model)) {
     GemmArgs g1{st->gemm_in, L->d_in, nullptr, L->W, L->d_in, L->d_out, n_rows, max_rows, 1,
                 st->gemm_mid, L->d_out, nullptr, nullptr, err};
     RTEC_TRY(gemm_launch(g1, s));
@@ -806,6 +963,11 @@ int rtec_layer_incremental(const rtec_graph_t* g, const rtec_batch_t* b, const r
     return RTEC_OK;
   }
   a.d_agg = L->d_in;
+  if (L->model == RTEC_MODEL_GIN_MAX) {
+    a.tc_nkb = L->Wt_hi ? tc_nkb_of(L->d_in) : 0;
+    RTEC_TRY(launch_max<false>(a, AggRows{f->dst_list, f->n_dst, n}, s));
+    return run_update(L, st, f->n_dst, n, f->dst_list, st->log_out, err, s);
+  }
   float* delta = w.alloc<float>(n * static_cast<int64_t>(L->d_in));
   RTEC_WS_CHECK(w);
   a.delta = delta;
@@ -870,6 +1032,10 @@ int rtec_layer_full(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* 
   a.d_agg = L->d_in;
   a.tc_nkb = L->Wt_hi ? tc_nkb_of(L->d_in) : 0;
   int64_t mr = rows ? max_rows : n;
+  if (L->model == RTEC_MODEL_GIN_MAX) {
+    RTEC_TRY(launch_max<true>(a, AggRows{rows, rows ? n_rows : nullptr, n}, s));
+    return run_update(L, st, rows ? n_rows : nullptr, mr, rows, nullptr, nullptr, s);
+  }
   {
     Ws w(ws, ws_bytes);
     RTEC_TRY(launch_aggregation<true>(a, AggRows{rows, rows ? n_rows : nullptr, n}, mr, g->in.slots, w, s));

@@ -30,7 +30,7 @@ import torch
 from . import _lib
 from . import errors as E
 from .graph import DynamicGraph, EdgeUpdate, updates_to_arrays
-from .models import GAT, GIN, Bundle, MODELS
+from .models import GAT, GIN_FAMILY, Bundle, MODELS
 
 _MODEL_ID = _lib.MODEL_IDS
 
@@ -101,7 +101,7 @@ class RTECEngine:
         for l, w in enumerate(bundle.layers):
             d_in, d_out = w.in_dim, w.out_dim
             W = torch.as_tensor(np.asarray(w.tensors["W"], np.float32), device=self.dev).contiguous()
-            W2 = torch.as_tensor(np.asarray(w.tensors["W2"], np.float32), device=self.dev).contiguous() if bundle.model == GIN else None
+            W2 = torch.as_tensor(np.asarray(w.tensors["W2"], np.float32), device=self.dev).contiguous() if bundle.model in GIN_FAMILY else None
             att = torch.as_tensor(np.asarray(w.tensors["a"], np.float32).reshape(heads, -1), device=self.dev).contiguous() if bundle.model == GAT else None
             tcw = [None, None, None, None]
             if self.tc:
@@ -134,10 +134,10 @@ class RTECEngine:
             rows = (n + 127) // 128 * 128
             pad = lambda d: (d + 31) // 32 * 32  # noqa: E731
             self.gemm_in = z(rows * pad(max(bundle.agg_dims)))
-            self.gemm_mid = z(rows * pad(max(dims[1:]))) if bundle.model == GIN else None
+            self.gemm_mid = z(rows * pad(max(dims[1:]))) if bundle.model in GIN_FAMILY else None
         else:
             self.gemm_in = z(n, max(bundle.agg_dims)) if bundle.model != GAT else None
-            self.gemm_mid = z(n, max(dims[1:])) if bundle.model == GIN else None
+            self.gemm_mid = z(n, max(dims[1:])) if bundle.model in GIN_FAMILY else None
         self.fr = [_Frontier(n, self.dev) for _ in range(self.L)]
         self._ensure_ws(max_batch or graph.batch.cap)
         self.bootstrap()

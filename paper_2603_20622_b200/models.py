@@ -28,7 +28,12 @@ import numpy as np
 from . import errors as E
 
 GCN, GRAPHSAGE, GIN, GAT = "gcn", "graphsage", "gin", "gat"
-MODELS = (GCN, GRAPHSAGE, GIN, GAT)
+# GIN with an elementwise-max aggregator (configs[3] "GIN (max/sum agg)"); the
+# reference has no max aggregator, so this one is pinned only by the oracle's
+# restated full recompute (SURVEY §8(c) "Unpinned by the reference").
+GIN_MAX = "gin_max"
+MODELS = (GCN, GRAPHSAGE, GIN, GAT, GIN_MAX)
+GIN_FAMILY = (GIN, GIN_MAX)
 REFERENCE_ONLY = ("pinsage", "monet", "commnet", "ggcn", "agnn")
 
 
@@ -110,7 +115,7 @@ def make_bundle(model: str, dims: Sequence[int], *, dtype=np.float64, rng_seed: 
             layers.append(LayerWeights(i, o, {k: np.asarray(t, dt) for k, t in w.tensors.items()}, dict(w.scalars)))
     elif name in (GCN, GRAPHSAGE):  # models.py:88-96, :124-128
         layers = [LayerWeights(i, o, {"W": _mat(rng, o, i, dt)}) for i, o in pairs]
-    elif name == GIN:  # models.py:178-183
+    elif name in GIN_FAMILY:  # models.py:178-183 (gin_max: same draws)
         layers = []
         for i, o in pairs:
             W = _mat(rng, o, i, dt)
@@ -133,7 +138,7 @@ def make_bundle(model: str, dims: Sequence[int], *, dtype=np.float64, rng_seed: 
                       degree_offset=1.0 if degree_smoothing else 0.0)
     if name == GRAPHSAGE:  # :131-141
         return Bundle(name, tuple(layers), dt, tuple(dims[:-1]), "count")
-    if name == GIN:  # :191-200
+    if name in GIN_FAMILY:  # :191-200
         return Bundle(name, tuple(layers), dt, tuple(dims[:-1]), "none")
     return Bundle(name, tuple(layers), dt, tuple(dims[1:]), "sum", dest_dependent=True, heads=int(heads))
 

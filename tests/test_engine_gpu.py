@@ -100,7 +100,7 @@ def _run_vs_oracle(P, model, dims, n, m, B, nb, seed, heads=1, smoothing=True, u
 
 
 @pytest.mark.parametrize("model,dims", [("gcn", [32, 64, 32]), ("graphsage", [48, 64, 32]), ("gin", [32, 32, 32]),
-                                        ("gat", [40, 32, 32])])
+                                        ("gat", [40, 32, 32]), ("gin_max", [32, 48, 32])])
 def test_engine_vs_oracle(P, model, dims):
     _run_vs_oracle(P, model, dims, n=4000, m=60000, B=400, nb=4, seed=3)
 
@@ -131,6 +131,29 @@ def test_engine_large_batch_radix_path(P):
 
 def test_engine_three_layers_gin(P):
     _run_vs_oracle(P, "gin", [16, 16, 16, 16], n=3000, m=30000, B=200, nb=3, seed=9)
+
+
+def test_gin_max_retract_paths(P):
+    # 3 layers, many batches with deletes (retract -> re-max) and the SIMT update path
+    _run_vs_oracle(P, "gin_max", [16, 16, 16, 16], n=2000, m=16000, B=300, nb=6, seed=14)
+    _run_vs_oracle(P, "gin_max", [20, 36, 8], n=1500, m=12000, B=150, nb=3, seed=15, update="simt")
+
+
+def test_gin_max_bit_exact_vs_full_recompute(P):
+    # max is exact: the incremental cached maxima equal a fresh fp32 bootstrap bit for bit
+    from paper_2603_20622_b200.workload import UpdateStream, chung_lu_edges, features
+
+    n = 3000
+    s, d = chung_lu_edges(n, 30000, seed=16)
+    stream = UpdateStream(s, d, holdout=0.1, seed=16)
+    bs, bd, bt = stream.base()
+    X = features(n, 32, seed=3)
+    eng = P.RTECEngine(P.make_bundle("gin_max", [32, 32, 32]), P.DynamicGraph.from_edges(n, (bs, bd, bt)), X)
+    for _ in range(4):
+        eng.step(*stream.next_batch(400))
+    src, dst, ts = eng.g.edges()
+    fresh = P.RTECEngine(P.make_bundle("gin_max", [32, 32, 32]), P.DynamicGraph.from_edges(n, (src, dst, ts)), X)
+    assert np.array_equal(eng.S[0].cpu().numpy(), fresh.S[0].cpu().numpy())
 
 
 def test_drift_many_batches(P):

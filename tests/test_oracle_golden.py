@@ -207,3 +207,31 @@ def test_deletion_round_trip_oracle():
         eng.step(op, bs, bd, bt)
         eng.step(*invert_batch(op, bs, bd, bt))
         assert np.abs(eng.H[-1] - H0).max() <= 1e-7, model
+
+
+def test_gin_max_oracle_brute_force():
+    """GIN-max (no reference counterpart) pinned by a per-vertex loop: a_v is
+    the elementwise max of the in-neighbours' rows, 0 for an empty
+    neighbourhood; update W2 relu(W (h_v + a_v)) (models.py:187-189)."""
+    from oracle import models as M
+    from oracle.graph import OracleGraph
+
+    rng = np.random.default_rng(5)
+    n = 60
+    s = rng.integers(0, n, 400)
+    d = rng.integers(0, n, 400)
+    key = np.unique(s * n + d)
+    g = OracleGraph.from_edges(n, key // n, key % n)
+    b = M.make_bundle("gin_max", [5, 6, 4])
+    gin = M.make_bundle("gin", [5, 6, 4])
+    for l in range(2):  # same weight draws as GIN
+        assert np.array_equal(b.layers[l]["W"], gin.layers[l]["W"])
+    X = rng.uniform(-1, 1, (n, 5))
+    H1, A, C = M.layer_full(b, 0, g, X)
+    indptr, srcs = g.in_csr()
+    for v in range(n):
+        nb = srcs[indptr[v]:indptr[v + 1]]
+        a = X[nb].max(axis=0) if nb.size else np.zeros(5)
+        assert np.array_equal(A[v], a)
+        h = np.maximum((X[v] + a) @ b.layers[0]["W"].T, 0) @ b.layers[0]["W2"].T
+        assert np.allclose(H1[v], h, rtol=1e-12, atol=1e-12)
