@@ -13,12 +13,13 @@
 // Each K-block is therefore one contiguous chunk fetched with a single 1-D
 // bulk async copy (cp.async.bulk -> UBLKCP) completing on an mbarrier.
 //
-// Persistent CTAs (one per SM, 128 threads), 2-stage smem ring:
-//   stage = A (raw -> lo in place, 16 KB) + A_hi (16 KB) + Bhi + Blo (Npad*128 B each)
-// thread 0 issues the bulk copies one step ahead and the 12 MMAs per K-block
-// (4 k-steps x 3 products, tcgen05.mma.cta_group::1.kind::tf32, M=128, N=Npad),
-// tcgen05.commit frees the stage; all 128 threads split hi/lo and run the
-// epilogue (tcgen05.ld 32x32b.x32 -> act -> scatter rows + DeltaLog capture).
+// Persistent CTAs (one per SM, 16 warps, see k_gemm_tc): an A ring (raw -> lo
+// in place + hi, 32 KB per K-block) and a B ring of (K-block, N-half) stages,
+// one producer lane issuing the bulk copies, one MMA lane issuing 12
+// tcgen05.mma per (K-block, N-half) into a double-buffered TMEM accumulator,
+// six splitter warps and eight epilogue warps (tcgen05.ld -> act -> rows
+// staged through swizzled shared memory -> float4 stores; the DeltaLog copy of
+// the old rows runs before the accumulator is ready).
 #include "prims.cuh"
 #include "gemm_tc.cuh"
 
@@ -106,17 +107,42 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Warp-specialised persistent kernel (256 threads):
-//   warp 0      producer: bulk-copies A / Bhi / Blo of each K-block into a ring of S stages
-//   warp 1      MMA issuer: 12 tcgen05.mma per K-block into one of two TMEM accumulators
-//   warps 2-3   splitters: A -> (hi, lo) in shared memory, fence.proxy.async, arrive
-//   warps 4-7   epilogue: tcgen05.ld -> act -> global rows (+ DeltaLog), overlapping the
+// Warp-specialised persistent kernel (512 threads), separate operand rings:
+//   warp 0      producer: bulk-copies each A K-block (16 KB) into the A ring and each
+//               (K-block, N-half) of Bhi/Blo into the B ring
+//   warp 1      MMA issuer: per (K-block, N-half) 12 tcgen05.mma into one of two TMEM
+//               accumulators (columns [half0, npad) of buffer t&1)
+//   warps 2-7   splitters: A -> (hi, lo) in shared memory, fence.proxy.async, arrive
+//   warps 8-15  epilogue: tcgen05.ld -> act -> global rows (+ DeltaLog), overlapping the
 //               next tile's main loop thanks to the double-buffered accumulator
-// mbarriers: full[s] (tx), split[s] (64 arrivals), empty[s] (tcgen05.commit),
-//            tfull[2] (tcgen05.commit), tempty[2] (128 arrivals)
-constexpr int kMaxStages = 4;
+// Splitting B by N-halves keeps the B stage at 32 KB for N = 256, so the rings
+// are 3 A stages + 4 B stages deep instead of 2 monolithic 96 KB stages.
+// mbarriers: a_full (tx), a_split (192 arrivals), a_empty (tcgen05.commit),
+//            b_full (tx), b_empty (commit), tfull[2] (commit), tempty[2] (256 arrivals)
+constexpr int kMaxA = 6, kMaxB = 8;
+constexpr int kSplitThreads = 192;
+constexpr int kEpiBytes = 8 * 32 * 32 * 4;              // 8 epilogue warps x 32 rows x 32 cols
 
-__global__ void __launch_bounds__(256, 1) k_gemm_tc(TcArgs g, int S) {
+struct TcShape {
+  int SA, SB;       // ring depths
+  int nh;           // N halves (1 or 2)
+  int h0;           // width of half 0 (multiple of 16); half 1 = npad - h0
+  uint32_t bstage;  // bytes of one B stage (hi + lo of the wider half)
+};
+
+static TcShape tc_shape(int npad) {
+  TcShape sh;
+  sh.nh = npad > 128 ? 2 : 1;
+  sh.h0 = sh.nh == 2 ? ((npad / 2 + 15) / 16) * 16 : npad;
+  sh.bstage = 2u * static_cast<uint32_t>(sh.h0) * kTK * 4;
+  const int budget = 227 * 1024 - 1024 - 512 - kEpiBytes;
+  sh.SA = 3;  // measured: 2..4 A stages perform alike; the B ring gets the rest
+  sh.SB = (budget - sh.SA * 2 * kABlockBytes) / static_cast<int>(sh.bstage);
+  if (sh.SB > kMaxB) sh.SB = kMaxB;
+  return sh;
+}
+
+__global__ void __launch_bounds__(512, 1) k_gemm_tc(TcArgs g, TcShape sh) {
   extern __shared__ uint8_t smem_raw[];
   if (g.err && err_set(g.err)) return;
   const int64_t nrows = g.n_rows ? *g.n_rows : g.max_rows;
@@ -124,28 +150,35 @@ __global__ void __launch_bounds__(256, 1) k_gemm_tc(TcArgs g, int S) {
   if (static_cast<int64_t>(blockIdx.x) >= ntiles) return;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t bbytes = static_cast<uint32_t>(g.npad) * kTK * 4;
-  const uint32_t stage_bytes = 2 * kABlockBytes + 2 * bbytes;
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(base + S * stage_bytes);
-  uint64_t* full = bars;
-  uint64_t* split = bars + kMaxStages;
-  uint64_t* empty = bars + 2 * kMaxStages;
-  uint64_t* tfull = bars + 3 * kMaxStages;
+  uint8_t* aring = base;                                      // SA x (lo 16 KB | hi 16 KB)
+  uint8_t* bring = base + sh.SA * 2 * kABlockBytes;           // SB x (hi | lo)
+  float* epi = reinterpret_cast<float*>(bring + sh.SB * sh.bstage);   // epilogue transpose staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(epi) + kEpiBytes);
+  uint64_t* a_full = bars;
+  uint64_t* a_split = a_full + kMaxA;
+  uint64_t* a_empty = a_split + kMaxA;
+  uint64_t* b_full = a_empty + kMaxA;
+  uint64_t* b_empty = b_full + kMaxB;
+  uint64_t* tfull = b_empty + kMaxB;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   uint32_t ncols = 32;
   while (ncols < static_cast<uint32_t>(2 * g.npad)) ncols <<= 1;
 
   if (tid == 0) {
-    for (int i = 0; i < S; ++i) {
-      mbar_init(full + i, 1);
-      mbar_init(split + i, 64);
-      mbar_init(empty + i, 1);
+    for (int i = 0; i < sh.SA; ++i) {
+      mbar_init(a_full + i, 1);
+      mbar_init(a_split + i, kSplitThreads);
+      mbar_init(a_empty + i, 1);
+    }
+    for (int i = 0; i < sh.SB; ++i) {
+      mbar_init(b_full + i, 1);
+      mbar_init(b_empty + i, 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(tfull + i, 1);
-      mbar_init(tempty + i, 128);
+      mbar_init(tempty + i, 256);
     }
     fence_barrier_init();
   }
@@ -159,90 +192,140 @@ __global__ void __launch_bounds__(256, 1) k_gemm_tc(TcArgs g, int S) {
   tc_fence_after();
   const uint32_t taddr = *tmem_slot;
   const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
-  const int64_t J = my_tiles * g.nkb;
+  const int64_t J = my_tiles * g.nkb;  // A stages consumed by this CTA
 
   if (warp == 0) {
     if (lane == 0) {
+      int64_t jb = 0;
       for (int64_t j = 0; j < J; ++j) {
-        const int s = static_cast<int>(j % S);
-        const int64_t u = j / S;
-        if (u > 0) mbar_wait(empty + s, static_cast<uint32_t>((u - 1) & 1));
+        const int sa = static_cast<int>(j % sh.SA);
+        if (j >= sh.SA) mbar_wait(a_empty + sa, static_cast<uint32_t>(((j / sh.SA) - 1) & 1));
         const int64_t tile = blockIdx.x + (j / g.nkb) * gridDim.x;
         const int kb = static_cast<int>(j % g.nkb);
-        uint8_t* st = base + s * stage_bytes;
-        mbar_expect_tx(full + s, kABlockBytes + 2 * bbytes);
-        bulk_g2s(st, g.A + (tile * g.nkb + kb) * (kABlockBytes / 4), kABlockBytes, full + s);
-        bulk_g2s(st + 2 * kABlockBytes, g.Bhi + static_cast<int64_t>(kb) * g.npad * kTK, bbytes, full + s);
-        bulk_g2s(st + 2 * kABlockBytes + bbytes, g.Blo + static_cast<int64_t>(kb) * g.npad * kTK, bbytes, full + s);
+        mbar_expect_tx(a_full + sa, kABlockBytes);
+        bulk_g2s(aring + sa * 2 * kABlockBytes, g.A + (tile * g.nkb + kb) * (kABlockBytes / 4), kABlockBytes,
+                 a_full + sa);
+        for (int h = 0; h < sh.nh; ++h, ++jb) {
+          const int sb = static_cast<int>(jb % sh.SB);
+          if (jb >= sh.SB) mbar_wait(b_empty + sb, static_cast<uint32_t>(((jb / sh.SB) - 1) & 1));
+          const int n0 = h == 0 ? 0 : sh.h0;
+          const int nw = h == 0 ? sh.h0 : g.npad - sh.h0;
+          const uint32_t hb = static_cast<uint32_t>(nw) * kTK * 4;
+          uint8_t* st = bring + sb * sh.bstage;
+          const int64_t off = (static_cast<int64_t>(kb) * g.npad + n0) * kTK;
+          mbar_expect_tx(b_full + sb, 2 * hb);
+          bulk_g2s(st, g.Bhi + off, hb, b_full + sb);
+          bulk_g2s(st + sh.bstage / 2, g.Blo + off, hb, b_full + sb);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(g.npad >> 3) << 17) |
-                             (static_cast<uint32_t>(kTM >> 4) << 24);
+      int64_t j = 0, jb = 0;
       for (int64_t t = 0; t < my_tiles; ++t) {
         const int b = static_cast<int>(t & 1);
         const int64_t ub = t >> 1;
         if (ub > 0) mbar_wait(tempty + b, static_cast<uint32_t>((ub - 1) & 1));
         tc_fence_after();
-        const uint32_t acc_addr = taddr + static_cast<uint32_t>(b * g.npad);
-        for (int kb = 0; kb < g.nkb; ++kb) {
-          const int64_t j = t * g.nkb + kb;
-          const int s = static_cast<int>(j % S);
-          mbar_wait(split + s, static_cast<uint32_t>((j / S) & 1));
+        for (int kb = 0; kb < g.nkb; ++kb, ++j) {
+          const int sa = static_cast<int>(j % sh.SA);
+          mbar_wait(a_split + sa, static_cast<uint32_t>((j / sh.SA) & 1));
           tc_fence_after();
-          const uint32_t a_lo = smem_u32(base + s * stage_bytes);
+          const uint32_t a_lo = smem_u32(aring + sa * 2 * kABlockBytes);
           const uint32_t a_hi = a_lo + kABlockBytes;
-          const uint32_t b_hi = a_lo + 2 * kABlockBytes;
-          const uint32_t b_lo = b_hi + bbytes;
+          for (int h = 0; h < sh.nh; ++h, ++jb) {
+            const int sb = static_cast<int>(jb % sh.SB);
+            mbar_wait(b_full + sb, static_cast<uint32_t>((jb / sh.SB) & 1));
+            tc_fence_after();
+            const int n0 = h == 0 ? 0 : sh.h0;
+            const int nw = h == 0 ? sh.h0 : g.npad - sh.h0;
+            const uint32_t b_hi = smem_u32(bring + sb * sh.bstage);
+            const uint32_t b_lo = b_hi + sh.bstage / 2;
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(nw >> 3) << 17) |
+                                   (static_cast<uint32_t>(kTM >> 4) << 24);
+            const uint32_t acc_addr = taddr + static_cast<uint32_t>(b * g.npad + n0);
 #pragma unroll
-          for (int k = 0; k < kTK / 8; ++k) {
-            const uint32_t off = k * 32;
-            const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
-            mma_tf32(acc_addr, sw128_desc(a_hi + off), sw128_desc(b_hi + off), idesc, acc);
-            mma_tf32(acc_addr, sw128_desc(a_hi + off), sw128_desc(b_lo + off), idesc, 1u);
-            mma_tf32(acc_addr, sw128_desc(a_lo + off), sw128_desc(b_hi + off), idesc, 1u);
+            for (int k = 0; k < kTK / 8; ++k) {
+              const uint32_t off = k * 32;
+              const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+              mma_tf32(acc_addr, sw128_desc(a_hi + off), sw128_desc(b_hi + off), idesc, acc);
+              mma_tf32(acc_addr, sw128_desc(a_hi + off), sw128_desc(b_lo + off), idesc, 1u);
+              mma_tf32(acc_addr, sw128_desc(a_lo + off), sw128_desc(b_hi + off), idesc, 1u);
+            }
+            mma_commit(b_empty + sb);  // B stage reusable once these MMAs retire
           }
-          mma_commit(empty + s);  // smem stage reusable once these MMAs retire
+          mma_commit(a_empty + sa);
         }
-        mma_commit(tfull + b);    // accumulator b complete
+        mma_commit(tfull + b);  // accumulator b complete
       }
     }
-  } else if (warp < 4) {
-    const int st_id = tid - 64;  // 0..63
+  } else if (warp < 8) {
+    const int st_id = tid - 64;  // 0..191
     for (int64_t j = 0; j < J; ++j) {
-      const int s = static_cast<int>(j % S);
-      mbar_wait(full + s, static_cast<uint32_t>((j / S) & 1));
-      float4* raw = reinterpret_cast<float4*>(base + s * stage_bytes);
-      float4* hi = reinterpret_cast<float4*>(base + s * stage_bytes + kABlockBytes);
-#pragma unroll 4
-      for (int q = 0; q < kABlockBytes / 16 / 64; ++q) {
-        const int idx = st_id + 64 * q;
+      const int sa = static_cast<int>(j % sh.SA);
+      mbar_wait(a_full + sa, static_cast<uint32_t>((j / sh.SA) & 1));
+      float4* raw = reinterpret_cast<float4*>(aring + sa * 2 * kABlockBytes);
+      float4* hi = reinterpret_cast<float4*>(aring + sa * 2 * kABlockBytes + kABlockBytes);
+      for (int idx = st_id; idx < kABlockBytes / 16; idx += kSplitThreads) {
         float4 x = raw[idx];
-        float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
-        hi[idx] = h;
-        raw[idx] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+        float4 hv = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
+        hi[idx] = hv;
+        raw[idx] = make_float4(x.x - hv.x, x.y - hv.y, x.z - hv.z, x.w - hv.w);
       }
       fence_proxy_async();
-      mbar_arrive(split + s);
+      mbar_arrive(a_split + sa);
     }
   } else {
-    // epilogue: thread owns accumulator row r = tid - 128 (TMEM lane r; warp w%4 -> lanes 32*(w%4))
-    const int r = tid - 128;
-    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    // epilogue (warps 8-15): warp w reads TMEM lanes 32*(w%4).. (its 32 rows) and the
+    // column half (w-8)/4 of the accumulator.  Row-major outputs are staged through
+    // shared memory (16-byte chunks XOR-swizzled by row) so each float4 store
+    // instruction writes 4 rows x 128 contiguous bytes.
+    const int wq = warp & 3;
+    const int half = (warp - 8) >> 2;
+    const int r = wq * 32 + lane;
+    const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
+    float* stg = epi + (warp - 8) * 32 * 32;
+    const int nchunk = g.npad / 32 + (g.npad % 32 ? 1 : 0);
+    const int cbeg = half == 0 ? 0 : (nchunk / 2), cend = half == 0 ? (nchunk / 2) : nchunk;
     for (int64_t t = 0; t < my_tiles; ++t) {
       const int b = static_cast<int>(t & 1);
-      mbar_wait(tfull + b, static_cast<uint32_t>((t >> 1) & 1));
-      tc_fence_after();
       const int64_t tile = blockIdx.x + t * gridDim.x;
       const int64_t i = tile * kTM + r;
       const bool valid = i < nrows;
-      const int64_t dst = valid ? (g.y_rows ? static_cast<int64_t>(g.y_rows[i]) : i) : 0;
-      for (int c0 = 0; c0 < g.npad; c0 += 32) {
+      const int64_t dst = valid ? (g.y_rows ? static_cast<int64_t>(g.y_rows[i]) : i) : -1;
+      const int64_t row0 = tile * kTM + wq * 32;  // first row of this warp
+      if (g.log && !g.Yt) {
+        // DeltaLog capture of this tile's rows (this warp's column half) does not
+        // depend on the MMA: copy the pre-batch rows while the tile accumulates
+        const int c_lo = cbeg * 32, c_hi = min(cend * 32, g.d_out);
+        for (int q0 = 0; q0 < 32; q0 += 4) {
+          float v[4][4];
+          int64_t dq[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            dq[u] = __shfl_sync(0xffffffffu, dst, q0 + u);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int c = c_lo + lane + 32 * k;
+              v[u][k] = (dq[u] >= 0 && c < c_hi) ? __ldcg(g.Y + dq[u] * g.ldy + c) : 0.f;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int c = c_lo + lane + 32 * k;
+              if (dq[u] >= 0 && c < c_hi) __stcs(g.log + (row0 + q0 + u) * g.d_out + c, v[u][k]);
+            }
+        }
+      }
+      mbar_wait(tfull + b, static_cast<uint32_t>((t >> 1) & 1));
+      tc_fence_after();
+      for (int cc = cbeg; cc < cend; ++cc) {
+        const int c0 = cc * 32;
         uint32_t rr[32];
         RTEC_TMEM_LD32(taddr + lane_base + static_cast<uint32_t>(b * g.npad + c0), rr);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (!valid) continue;
         float y[32];
 #pragma unroll
         for (int q = 0; q < 32; ++q) {
@@ -250,6 +333,7 @@ __global__ void __launch_bounds__(256, 1) k_gemm_tc(TcArgs g, int S) {
           y[q] = g.act == 1 ? fmaxf(v, 0.f) : v;
         }
         if (g.Yt) {  // chained GEMM input: SW128 tile image (zero padding beyond d_out)
+          if (!valid) continue;
           float* blk = g.Yt + ((tile * g.nkb_out + c0 / 32) * kTM) * kTK;
 #pragma unroll
           for (int q = 0; q < 32; q += 4) {
@@ -257,27 +341,32 @@ __global__ void __launch_bounds__(256, 1) k_gemm_tc(TcArgs g, int S) {
                                     c0 + q + 2 < g.d_out ? y[q + 2] : 0.f, c0 + q + 3 < g.d_out ? y[q + 3] : 0.f);
             *reinterpret_cast<float4*>(blk + sw128_off(r, q)) = v4;
           }
-        } else {
-          float* yrow = g.Y + dst * g.ldy;
-          if ((g.d_out & 3) == 0 && c0 + 32 <= g.d_out && (g.ldy & 3) == 0) {
-            float4* y4 = reinterpret_cast<float4*>(yrow + c0);
-            if (g.log) {
-              float4 old[8];
+          continue;
+        }
+        // stage: row `lane`, chunk c at 16-byte slot (c ^ (lane & 7))
 #pragma unroll
-              for (int q = 0; q < 8; ++q) old[q] = y4[q];
-              float4* l4 = reinterpret_cast<float4*>(g.log + i * g.d_out + c0);
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<float4*>(stg + lane * 32 + ((c ^ (lane & 7)) << 2)) =
+              make_float4(y[4 * c], y[4 * c + 1], y[4 * c + 2], y[4 * c + 3]);
+        __syncwarp();
+        const int sub = lane >> 3, ch = lane & 7;  // 4 rows per instruction, 8 lanes per row
+        const int col = c0 + ch * 4;
+        const bool full4 = (g.d_out & 3) == 0 && (g.ldy & 3) == 0;
 #pragma unroll
-              for (int q = 0; q < 8; ++q) l4[q] = old[q];
-            }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) y4[q] = make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+        for (int q0 = 0; q0 < 32; q0 += 4) {
+          const int q = q0 + sub;
+          const int64_t dq = __shfl_sync(0xffffffffu, dst, q);
+          const float4 v4 = *reinterpret_cast<const float4*>(stg + q * 32 + ((ch ^ (q & 7)) << 2));
+          if (dq < 0) continue;
+          float* yp = g.Y + dq * g.ldy + col;
+          if (full4 && col + 4 <= g.d_out) {
+            *reinterpret_cast<float4*>(yp) = v4;
           } else {
-            for (int q = 0; q < 32 && c0 + q < g.d_out; ++q) {
-              if (g.log) g.log[i * g.d_out + c0 + q] = yrow[c0 + q];
-              yrow[c0 + q] = y[q];
-            }
+            const float e[4] = {v4.x, v4.y, v4.z, v4.w};
+            for (int k = 0; k < 4 && col + k < g.d_out; ++k) yp[k] = e[k];
           }
         }
+        __syncwarp();
       }
       tc_fence_before();
       mbar_arrive(tempty + b);
@@ -307,13 +396,10 @@ __global__ void k_prep_b(const float* __restrict__ W, int d_in, int d_out, int n
   }
 }
 
-static int gemm_tc_stages(int npad) {
-  size_t stage = 2 * kABlockBytes + 2 * static_cast<size_t>(npad) * kTK * 4;
-  int S = static_cast<int>((227 * 1024 - 1024 - 256) / stage);
-  return S < kMaxStages ? S : kMaxStages;
-}
 size_t gemm_tc_smem(int npad) {
-  return gemm_tc_stages(npad) * (2 * kABlockBytes + 2 * static_cast<size_t>(npad) * kTK * 4) + 1024 + 256;
+  TcShape sh = tc_shape(npad);
+  return static_cast<size_t>(sh.SA) * 2 * kABlockBytes + static_cast<size_t>(sh.SB) * sh.bstage + kEpiBytes + 1024 +
+         512;
 }
 
 int gemm_tc_launch(const TcArgs& g, cudaStream_t s) {
@@ -327,7 +413,7 @@ int gemm_tc_launch(const TcArgs& g, cudaStream_t s) {
   int64_t tiles = (g.max_rows + kTM - 1) / kTM;
   int grid = static_cast<int>(tiles < kSMs ? tiles : kSMs);
   RTEC_PROF("k_gemm_tc", s);
-  k_gemm_tc<<<grid, 256, smem, s>>>(g, gemm_tc_stages(g.npad));
+  k_gemm_tc<<<grid, 512, smem, s>>>(g, tc_shape(g.npad));
   RTEC_LAUNCH_CHECK("k_gemm_tc");
   return RTEC_OK;
 }

@@ -308,6 +308,7 @@ struct MergePlan {
   int32_t* newlen;    // [maxK]
   int32_t* newcap;    // [maxK]
   uint8_t* inplace;   // [maxK]
+  int32_t* first;     // [maxK] in-place groups: run prefix [0, first) below every update stays put
   int64_t* totals;    // [4]: work, scratch, arena demand, base(top before)
   int32_t* scr_nbr;   // [scr_cap]
   int64_t* scr_ts;    // [scr_cap] or null
@@ -358,6 +359,9 @@ __global__ void k_group_info(MergeIn in, MergePlan p, rtec_adj_t a, float slack,
     p.newlen[g] = nl;
     p.inplace[g] = inpl ? 1 : 0;
     p.newcap[g] = inpl ? a.cap[v] : cap_for(nl, slack, min_slack);
+    // updates are sorted by neighbour: nothing below the smallest one moves
+    const int64_t b = a.beg[v];
+    p.first[g] = inpl ? static_cast<int32_t>(lower_bound_dev(a.nbr, b, b + L, in.nbr[s]) - b) : 0;
   }
 }
 
@@ -365,12 +369,12 @@ struct WorkOf {
   MergePlan p;
   const int32_t* len;
   __device__ __forceinline__ int64_t operator()(int64_t g) const {
-    return static_cast<int64_t>(len[p.gv[g]]) + (p.gstart[g + 1] - p.gstart[g]);
+    return static_cast<int64_t>(len[p.gv[g]]) - p.first[g] + (p.gstart[g + 1] - p.gstart[g]);
   }
 };
 struct ScrOf {
   MergePlan p;
-  __device__ __forceinline__ int64_t operator()(int64_t g) const { return p.inplace[g] ? p.newlen[g] : 0; }
+  __device__ __forceinline__ int64_t operator()(int64_t g) const { return p.inplace[g] ? p.newlen[g] - p.first[g] : 0; }
 };
 struct ArenaOf {
   MergePlan p;
@@ -440,10 +444,12 @@ __global__ void k_merge_items(MergeIn in, MergePlan p, rtec_adj_t a, const uint6
     int64_t s = p.gstart[g], e = p.gstart[g + 1];
     int64_t b = a.beg[v];
     int32_t L = a.len[v];
+    const int32_t f0 = p.first[g];
     int32_t w;
     int64_t tsv = 0;
     int64_t out;
-    if (t < L) {
+    if (t < L - f0) {
+      t += f0;
       w = a.nbr[b + t];
       int64_t q = lower_bound_dev(in.nbr, s, e, w);
       if (q < e && in.nbr[q] == w) continue;  // deleted (an applied insert never hits an existing key)
@@ -452,7 +458,7 @@ __global__ void k_merge_items(MergeIn in, MergePlan p, rtec_adj_t a, const uint6
       out = t - del_before + ins_before;
       if (a.ts) tsv = a.ts[b + t];
     } else {
-      int64_t k = s + (t - L);
+      int64_t k = s + (t - (L - f0));
       if (in.op[k] != RTEC_OP_INSERT) continue;
       w = in.nbr[k];
       int64_t pos = lower_bound_dev(a.nbr, b, b + L, w) - b;
@@ -463,7 +469,7 @@ __global__ void k_merge_items(MergeIn in, MergePlan p, rtec_adj_t a, const uint6
     }
     int64_t dst = p.inplace[g] ? -1 : p.dest[g] + out;
     if (dst < 0) {
-      int64_t so = p.scr_off[g] + out;
+      int64_t so = p.scr_off[g] + out - f0;
       p.scr_nbr[so] = w;
       if (p.scr_ts) p.scr_ts[so] = tsv;
     } else {
@@ -482,7 +488,7 @@ __global__ void k_merge_copyback(MergePlan p, rtec_adj_t a, const uint64_t* err)
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t g = upper_bound_dev<int64_t>(p.scr_off, 0, G, i) - 1;
     int32_t v = p.gv[g];
-    int64_t t = i - p.scr_off[g];
+    int64_t t = i - p.scr_off[g] + p.first[g];
     a.nbr[a.beg[v] + t] = p.scr_nbr[i];
     if (a.ts) a.ts[a.beg[v] + t] = p.scr_ts[i];
   }
@@ -513,6 +519,7 @@ static int plan_alloc(MergePlan& p, int64_t maxK, int64_t scr_cap, bool with_ts,
   p.newlen = ws.alloc<int32_t>(maxK + 1);
   p.newcap = ws.alloc<int32_t>(maxK + 1);
   p.inplace = ws.alloc<uint8_t>(maxK + 1);
+  p.first = ws.alloc<int32_t>(maxK + 1);
   p.totals = ws.alloc<int64_t>(4);
   p.scr_cap = scr_cap;
   p.scr_nbr = ws.alloc<int32_t>(scr_cap);
@@ -651,7 +658,7 @@ size_t batch_ws_bytes(int64_t n, int64_t B, int64_t scr_cap) {
   add(sizeof(int64_t) * 8);
   for (int d = 0; d < 2; ++d) {  // two merge plans
     add(sizeof(int64_t) * (B + 2) * 6);
-    add(sizeof(int32_t) * (B + 2) * 3);
+    add(sizeof(int32_t) * (B + 2) * 4);
     add(B + 2);
     add(sizeof(int64_t) * 8);
     add(sizeof(int32_t) * scr_cap);
@@ -793,7 +800,7 @@ int rtec_batch_apply_phase(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src,
   int64_t* cnt2 = w.alloc<int64_t>(2);
   // scratch capacity for in-place run merges: whatever workspace remains, split over 2 plans
   MergePlan po, pi;
-  size_t plan_fixed = sizeof(int64_t) * (B + 2) * 7 + sizeof(int32_t) * (B + 2) * 3 + (B + 2) + 4096;
+  size_t plan_fixed = sizeof(int64_t) * (B + 2) * 7 + sizeof(int32_t) * (B + 2) * 4 + (B + 2) + 4096 + 256;
   size_t sort_reserve = sort_ws_bytes(B2) + sizeof(int64_t) * (scan_blocks_for(B2) + 2) * 16 + (1 << 16);
   size_t used = w.off + 2 * plan_fixed + sort_reserve;
   int64_t scr_cap = used < w.bytes ? static_cast<int64_t>((w.bytes - used) / 2 / (sizeof(int32_t) + sizeof(int64_t) + 1)) : 0;

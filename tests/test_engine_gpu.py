@@ -114,6 +114,8 @@ def test_engine_simt_update_path(P, model):
 def test_tc_gemm_wide_and_padded(P):
     # d_in not a multiple of 32 (K padding), d_out not a multiple of 16 (N padding), 256-wide N
     _run_vs_oracle(P, "graphsage", [100, 256, 40], n=3000, m=30000, B=300, nb=2, seed=13)
+    # N split into uneven halves (npad 208 -> 112 + 96 columns)
+    _run_vs_oracle(P, "gcn", [72, 200, 144], n=2500, m=25000, B=250, nb=2, seed=17)
 
 
 def test_engine_vs_oracle_gat_heads(P):
