@@ -49,6 +49,14 @@ WORKLOADS = {
                     n=2449029, m=61859140, model="graphsage", dims=[100, 256, 256], batch=61859, heads=1),
     "c1-gcn": dict(desc="configs[0]: 2-layer GCN 128 hidden, 100K/2M power-law, 1,000-update batches",
                    n=100000, m=2000000, model="gcn", dims=[128, 128, 128], batch=1000, heads=1),
+    "c3-gat": dict(desc="configs[2]: 2-layer GAT, 4 heads, Reddit shape (232,965 V / 114.6M E, 602-dim), 0.1% batches",
+                   n=232965, m=114615892, model="gat", dims=[602, 256, 256], batch=114616, heads=4),
+    "c4-gin": dict(desc="configs[3]: 3-layer GIN (sum), R-MAT 10M V / 500M E, 128-dim, 0.1% batches",
+                   n=10000000, m=500000000, model="gin", dims=[128, 128, 128, 128], batch=500000, heads=1,
+                   gen="rmat"),
+    "c4-gin-max": dict(desc="configs[3]: 3-layer GIN (max), R-MAT 10M V / 500M E, 128-dim, 0.1% batches",
+                       n=10000000, m=500000000, model="gin_max", dims=[128, 128, 128, 128], batch=500000,
+                       heads=1, gen="rmat"),
 }
 
 
@@ -163,9 +171,10 @@ class Clocks:
 # ---------------------------------------------------------------- workload
 def make_workload(wl: dict, steps_total: int, device):
     """Graph on the GPU (bit-identical to the CPU generator), stream on the host."""
-    from paper_2603_20622_b200.workload import UpdateStream, chung_lu_edges, features
+    from paper_2603_20622_b200.workload import UpdateStream, chung_lu_edges, features, rmat_edges
 
-    s, d = chung_lu_edges(wl["n"], wl["m"], seed=0, device=device)
+    gen = rmat_edges if wl.get("gen") == "rmat" else chung_lu_edges
+    s, d = gen(wl["n"], wl["m"], seed=0, device=device)
     stream = UpdateStream(s, d, holdout=0.1, seed=0)
     batches = [stream.next_batch(wl["batch"]) for _ in range(steps_total)]
     X = features(wl["n"], wl["dims"][0], seed=1)

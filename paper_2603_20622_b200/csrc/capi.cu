@@ -26,7 +26,7 @@ size_t rtec_workspace_bytes(int64_t n, int64_t max_batch, int64_t m_slots, int32
   // layer: δ rows [n, d] + heavy-destination plan (lists, chunk map, partial rows)
   int64_t chunks = m_slots / 512 + 2 + n / 64;
   size_t l = static_cast<size_t>(n) * static_cast<size_t>(max_dim) * sizeof(float) +
-             static_cast<size_t>(n) * 40 + static_cast<size_t>(chunks) * (4 + 4 * static_cast<size_t>(max_dim)) +
+             static_cast<size_t>(n) * 40 + static_cast<size_t>(chunks) * (4 + 4 * static_cast<size_t>(max_dim + 8)) +
              sizeof(int64_t) * (scan_blocks_for(n) + 2) * 4 + (1 << 20);
   size_t r = b > f ? b : f;
   return (r > l ? r : l) + (1 << 20);

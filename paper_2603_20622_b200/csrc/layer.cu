@@ -361,19 +361,17 @@ static int agg_slice_width() {
   return w;
 }
 
-// plan + light + heavy launches for one aggregation
+// heavy-destination plan (list, chunk offsets, chunk -> heavy map); partial rows of `pw` floats
 template <bool FULL>
-static int launch_aggregation(LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_edges, Ws& w,
-                              cudaStream_t s) {
-  const int d = a.d_agg;
-  HeavyPlan hp{};
+static int plan_heavy(const LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_edges, int pw, Ws& w,
+                      cudaStream_t s, HeavyPlan& hp) {
   hp.heavy = w.alloc<int32_t>(max_rows + 1);
   hp.n_heavy = w.alloc<int64_t>(2);
   hp.hoff = w.alloc<int64_t>(max_rows + 2);
   int64_t max_chunks = max_edges / kChunk + 2 + max_rows / 64;
   hp.cmap = w.alloc<int32_t>(max_chunks);
   hp.arrive = w.alloc<int32_t>(max_rows + 1);
-  hp.part = w.alloc<float>(max_chunks * static_cast<int64_t>(d));
+  hp.part = w.alloc<float>(max_chunks * static_cast<int64_t>(pw));
   RTEC_WS_CHECK(w);
   RTEC_CUDA(cudaMemsetAsync(hp.n_heavy, 0, sizeof(int64_t) * 2, s));
   RTEC_CUDA(cudaMemsetAsync(hp.hoff, 0, sizeof(int64_t), s));
@@ -384,6 +382,17 @@ static int launch_aggregation(LayerArgs& a, AggRows rows, int64_t max_rows, int6
   RTEC_TRY(exclusive_scan(HeavyChunks{rows, a.g.in.len, hp.heavy}, Count{hp.n_heavy, max_rows}, max_rows,
                           StoreOffTailL{hp.hoff, hp.n_heavy}, nullptr, w, s));
   k_chunk_map<<<kSMs * 4, kLBlk, 0, s>>>(hp);
+  RTEC_LAUNCH_CHECK("k_chunk_map");
+  return RTEC_OK;
+}
+
+// plan + light + heavy launches for one aggregation
+template <bool FULL>
+static int launch_aggregation(LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_edges, Ws& w,
+                              cudaStream_t s) {
+  const int d = a.d_agg;
+  HeavyPlan hp{};
+  RTEC_TRY(plan_heavy<FULL>(a, rows, max_rows, max_edges, d, w, s, hp));
   const int grid = kSMs * 8;
   // Feature slicing: one pass per `sw`-column slice keeps the gathered rows'
   // working set (|S| x sw x 4 B) small enough for the hot sources to stay in
@@ -568,165 +577,340 @@ static int launch_max(LayerArgs& a, AggRows rows, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ GAT (K13-K15)
-// attention of edge (u -> v) for the head of chunk k
+// Alg. 3 for v in V_dst(l) \ R(l): per ValueChange edge
+// + a_new Z_new(u) - a_old Z_old(u) with a = exp(leaky_0.2(el_v + er_u)) per head
+// (dst half first, models.py:266-271), per structural edge +/- a Z; the
+// attention sums are the context.  v in R(l) (and every vertex at bootstrap):
+// full edge softmax over the post-batch in-run (models.py:431-458).  Gathers
+// run 2-4 rows deep per warp like the sum aggregation; destinations with more
+// than kChunk scanned edges are split into chunks reduced in chunk order.
+constexpr int kHMax = 8;
+
 template <int VEC>
 __device__ __forceinline__ int chunk_head(int k, int dh) {
   return ((lane_id() + 32 * k) * VEC) / dh;
 }
 
+struct GatEdgeState {
+  float elh[kHMax];  // el_v per head (destination half of the logit)
+};
+
+// contributions of in-run positions [e0, e1) of v: all edges (recompute) or the
+// ValueChange edges (sources in S(l), edge not inserted) -> acc, cacc
 template <int VEC, int K>
-__global__ void __launch_bounds__(kLBlk) k_gat_layer(LayerArgs a, int recompute_all) {
+__device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState& es, int64_t beg, int32_t e0,
+                                          int32_t e1, int64_t p, int64_t q, bool all, RowAcc<VEC, K>& acc,
+                                          float (&cacc)[K]) {
   using R = RowAcc<VEC, K>;
-  if (err_set(a.err)) return;
-  const int d = a.L.d_out;
+  const int d = a.L.d_out, H = a.L.heads, dh = d / H;
+  const int lane = lane_id();
+  int hk[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) hk[k] = R::has(k, d) ? chunk_head<VEC>(k, dh) : 0;
+  for (int32_t c0 = e0; c0 < e1; c0 += 32) {
+    const int32_t j = c0 + lane;
+    int32_t u = 0, sl = 0;
+    bool hit = false;
+    if (j < e1) {
+      u = a.g.in.nbr[beg + j];
+      hit = all || (bm_test(a.f.bm_src, u) && !in_range_has(a.b.i_src, p, q, u));
+    }
+    float an[kHMax], ao[kHMax];
+#pragma unroll
+    for (int h = 0; h < kHMax; ++h) an[h] = ao[h] = 0.f;
+    if (hit) {
+      if (!all) sl = a.prev_slot[u];
+#pragma unroll
+      for (int h = 0; h < kHMax; ++h)
+        if (h < H) {
+          an[h] = expf(leaky02(es.elh[h] + __ldg(a.st.er + static_cast<int64_t>(u) * H + h)));
+          if (!all) ao[h] = expf(leaky02(es.elh[h] + __ldg(a.st.er_log + static_cast<int64_t>(sl) * H + h)));
+        }
+    }
+    unsigned m = __ballot_sync(0xffffffffu, hit);
+    while (m) {
+      constexpr int UNR = 2;
+      int32_t uu[UNR], ss[UNR];
+      float wn[UNR][K], wo[UNR][K];
+      int cnt = 0;
+#pragma unroll
+      for (int t = 0; t < UNR; ++t) {
+        int src = m ? __ffs(m) - 1 : 0;
+        if (m) {
+          m &= m - 1;
+          cnt = t + 1;
+        }
+        uu[t] = __shfl_sync(0xffffffffu, u, src);
+        ss[t] = __shfl_sync(0xffffffffu, sl, src);
+#pragma unroll
+        for (int k = 0; k < K; ++k) wn[t][k] = wo[t][k] = 0.f;
+#pragma unroll
+        for (int h = 0; h < kHMax; ++h) {
+          if (h >= H) break;
+          float x = __shfl_sync(0xffffffffu, an[h], src);
+          float y = all ? 0.f : __shfl_sync(0xffffffffu, ao[h], src);
+#pragma unroll
+          for (int k = 0; k < K; ++k)
+            if (hk[k] == h) {
+              wn[t][k] = x;
+              wo[t][k] = y;
+            }
+        }
+      }
+      float zn[UNR][K][VEC], zo[UNR][K][VEC];
+#pragma unroll
+      for (int t = 0; t < UNR; ++t)
+        if (t < cnt) {
+          R::load(a.st.Z + static_cast<int64_t>(uu[t]) * d, d, zn[t]);
+          if (!all) R::load(a.st.Z_log + static_cast<int64_t>(ss[t]) * d, d, zo[t]);
+        }
+#pragma unroll
+      for (int t = 0; t < UNR; ++t)
+        if (t < cnt) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            cacc[k] += all ? wn[t][k] : wn[t][k] - wo[t][k];
+#pragma unroll
+            for (int jj = 0; jj < VEC; ++jj) {
+              float x = wn[t][k] * zn[t][k][jj];
+              if (!all) x = fmaf(-wo[t][k], zo[t][k][jj], x);
+              acc.v[k][jj] += x;
+            }
+          }
+        }
+    }
+  }
+}
+
+// structural edges of v (applied inserts / deletes), Alg. 3 with signed attention
+template <int VEC, int K>
+__device__ __forceinline__ void gat_struct(const LayerArgs& a, const GatEdgeState& es, int64_t p, int64_t q,
+                                           RowAcc<VEC, K>& acc, float (&cacc)[K]) {
+  using R = RowAcc<VEC, K>;
+  const int d = a.L.d_out, H = a.L.heads, dh = d / H;
+  for (int64_t kk = p; kk < q; ++kk) {
+    int32_t u = a.b.i_src[kk];
+    bool ins = a.b.i_op[kk] == RTEC_OP_INSERT;
+    const float* zrow = a.st.Z + static_cast<int64_t>(u) * d;
+    const float* errow = a.st.er + static_cast<int64_t>(u) * H;
+    if (!ins && a.prev_bm_dst && bm_test(a.prev_bm_dst, u)) {
+      int32_t sl = a.prev_slot[u];
+      zrow = a.st.Z_log + static_cast<int64_t>(sl) * d;
+      errow = a.st.er_log + static_cast<int64_t>(sl) * H;
+    }
+    float z[K][VEC];
+    R::load(zrow, d, z);
+    float sgn = ins ? 1.f : -1.f;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      float at = 0.f;
+      if (R::has(k, d)) {
+        int h = chunk_head<VEC>(k, dh);
+        at = expf(leaky02(es.elh[h] + errow[h]));
+      }
+      cacc[k] += sgn * at;
+#pragma unroll
+      for (int jj = 0; jj < VEC; ++jj) acc.v[k][jj] = fmaf(sgn * at, z[k][jj], acc.v[k][jj]);
+    }
+  }
+}
+
+template <int VEC, int K>
+__device__ __forceinline__ void gat_state(const LayerArgs& a, int32_t v, GatEdgeState& es) {
   const int H = a.L.heads;
-  const int dh = d / H;
-  const int64_t nd = recompute_all ? a.g.n : *a.f.n_dst;
-  const int64_t ns = recompute_all ? 0 : *a.f.n_src;
+#pragma unroll
+  for (int h = 0; h < kHMax; ++h) es.elh[h] = h < H ? __ldg(a.st.el + static_cast<int64_t>(v) * H + h) : 0.f;
+}
+
+// S / ctx update, zero-in-degree rule, DeltaLog, h = elu(S / ctx) (models.py:280-282)
+template <int VEC, int K, bool FULL>
+__device__ __forceinline__ void gat_finalize(const LayerArgs& a, int64_t i, int32_t v, int32_t len, bool recompute,
+                                             RowAcc<VEC, K>& acc, float (&cacc)[K]) {
+  using R = RowAcc<VEC, K>;
+  const int d = a.L.d_out, H = a.L.heads, dh = d / H;
+  const int lane = lane_id();
+  if (!recompute && a.g.in_deg_prev[v] > 0 && a.g.in_deg[v] > 0) {
+    float sv[K][VEC];
+    R::load_rw(a.st.S + static_cast<int64_t>(v) * d, d, sv);
+    acc.add(sv);
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (R::has(k, d)) cacc[k] += a.st.ctx[static_cast<int64_t>(v) * H + chunk_head<VEC>(k, dh)];
+  }
+  int32_t indeg = recompute ? len : a.g.in_deg[v];
+  if (indeg == 0) {
+    acc.zero();
+#pragma unroll
+    for (int k = 0; k < K; ++k) cacc[k] = 0.f;
+  }
+  acc.store(a.st.S + static_cast<int64_t>(v) * d, d);
+#pragma unroll
+  for (int k = 0; k < K; ++k) {  // ctx per head: written by the lane holding the head's first chunk
+    int c = lane + 32 * k;
+    if (c * VEC < d && (c * VEC) % dh == 0)
+      for (int hh = 0; hh < (VEC > dh ? VEC / dh : 1); ++hh) a.st.ctx[static_cast<int64_t>(v) * H + (c * VEC) / dh + hh] = cacc[k];
+  }
+  float* hrow = a.st.H_out + static_cast<int64_t>(v) * d;
+  if (!FULL && a.st.log_out) {
+    float old[K][VEC];
+    R::load_rw(hrow, d, old);
+    R o;
+    o.zero();
+    o.add(old);
+    o.store(a.st.log_out + i * d, d);
+  }
+  R o;
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int jj = 0; jj < VEC; ++jj) o.v[k][jj] = indeg > 0 ? elu1(acc.v[k][jj] / cacc[k]) : 0.f;
+  o.store(hrow, d);
+}
+
+template <int VEC, int K, bool FULL>
+__global__ void __launch_bounds__(kLBlk, 4) k_gat_light(LayerArgs a, AggRows rows) {
+  using R = RowAcc<VEC, K>;
+  if (!FULL && err_set(a.err)) return;
+  const int64_t nr = rows.count();
+  const bool scan = FULL || *a.f.n_src > 0;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int lane = lane_id();
-  for (int64_t i = warp; i < nd; i += nw) {
-    int32_t v = recompute_all ? static_cast<int32_t>(i) : a.f.dst_list[i];
-    bool recompute = recompute_all || (a.prev_bm_dst && bm_test(a.prev_bm_dst, v));
-    float elv[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) elv[k] = R::has(k, d) ? a.st.el[static_cast<int64_t>(v) * H + chunk_head<VEC>(k, dh)] : 0.f;
+  for (int64_t i = warp; i < nr; i += nw) {
+    int32_t v = rows.at(i);
+    int32_t len = a.g.in.len[v];
+    if (scan && len > kChunk) continue;  // heavy pass
+    const bool recompute = FULL || (a.prev_bm_dst && bm_test(a.prev_bm_dst, v));
+    int64_t p = 0, q = 0;
+    if (!FULL) {
+      int2 rg = reinterpret_cast<const int2*>(a.b.irange)[v];
+      if (rg.x >= 0) {
+        p = rg.x;
+        q = rg.x + rg.y;
+      }
+    }
+    GatEdgeState es;
+    gat_state<VEC, K>(a, v, es);
     R acc;
     acc.zero();
     float cacc[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) cacc[k] = 0.f;
-    int64_t beg = a.g.in.beg[v];
+    if (scan) gat_edges<VEC, K>(a, es, a.g.in.beg[v], 0, len, p, q, recompute, acc, cacc);
+    if (!recompute) gat_struct<VEC, K>(a, es, p, q, acc, cacc);
+    gat_finalize<VEC, K, FULL>(a, i, v, len, recompute, acc, cacc);
+  }
+}
+
+template <int VEC, int K, bool FULL>
+__global__ void __launch_bounds__(kLBlk, 4) k_gat_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
+  using R = RowAcc<VEC, K>;
+  if (!FULL && err_set(a.err)) return;
+  const int64_t nh = *hp.n_heavy;
+  if (nh == 0) return;
+  const int64_t T = hp.hoff[nh];
+  const int d = a.L.d_out, H = a.L.heads, dh = d / H;
+  const int pw = (d + H + 3) & ~3;  // partial row: d floats + H attention sums, 16-byte aligned
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = warp; t < T; t += nw) {
+    int32_t j = hp.cmap[t];
+    int64_t c0 = hp.hoff[j];
+    int32_t nch = static_cast<int32_t>(hp.hoff[j + 1] - c0);
+    int32_t c = static_cast<int32_t>(t - c0);
+    int64_t i = hp.heavy[j];
+    int32_t v = rows.at(i);
     int32_t len = a.g.in.len[v];
-    if (recompute) {
-      // full edge softmax over the post-batch in-run (vertex_aggregate models.py:444-458)
-      for (int32_t c0 = 0; c0 < len; c0 += 32) {
-        int32_t j = c0 + lane;
-        int32_t u = j < len ? a.g.in.nbr[beg + j] : 0;
-        int cnt_all = min(32, len - c0);
-        for (int t = 0; t < cnt_all; ++t) {
-          int32_t uu = __shfl_sync(0xffffffffu, u, t);
-          float z[K][VEC];
-          R::load(a.st.Z + static_cast<int64_t>(uu) * d, d, z);
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            float at = 0.f;
-            if (R::has(k, d)) at = expf(leaky02(elv[k] + a.st.er[static_cast<int64_t>(uu) * H + chunk_head<VEC>(k, dh)]));
-            cacc[k] += at;
-#pragma unroll
-            for (int jj = 0; jj < VEC; ++jj) acc.v[k][jj] = fmaf(at, z[k][jj], acc.v[k][jj]);
-          }
-        }
-      }
-    } else {
-      int64_t p = 0, q = 0;
-      {
-        int2 rg = reinterpret_cast<const int2*>(a.b.irange)[v];
-        if (rg.x >= 0) {
-          p = rg.x;
-          q = rg.x + rg.y;
-        }
-      }
-      if (ns > 0) {  // ValueChange edges: sources whose h^{l-1} changed
-        for (int32_t c0 = 0; c0 < len; c0 += 32) {
-          int32_t j = c0 + lane;
-          int32_t u = 0;
-          bool hit = false;
-          if (j < len) {
-            u = a.g.in.nbr[beg + j];
-            hit = bm_test(a.f.bm_src, u) && !in_range_has(a.b.i_src, p, q, u);
-          }
-          unsigned m = __ballot_sync(0xffffffffu, hit);
-          while (m) {
-            int src = __ffs(m) - 1;
-            m &= m - 1;
-            int32_t uu = __shfl_sync(0xffffffffu, u, src);
-            int32_t sl = a.prev_slot[uu];
-            float zn[K][VEC], zo[K][VEC];
-            R::load(a.st.Z + static_cast<int64_t>(uu) * d, d, zn);
-            R::load(a.st.Z_log + static_cast<int64_t>(sl) * d, d, zo);
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-              float an = 0.f, ao = 0.f;
-              if (R::has(k, d)) {
-                int h = chunk_head<VEC>(k, dh);
-                an = expf(leaky02(elv[k] + a.st.er[static_cast<int64_t>(uu) * H + h]));
-                ao = expf(leaky02(elv[k] + a.st.er_log[static_cast<int64_t>(sl) * H + h]));
-              }
-              cacc[k] += an - ao;
-#pragma unroll
-              for (int jj = 0; jj < VEC; ++jj) acc.v[k][jj] += an * zn[k][jj] - ao * zo[k][jj];
-            }
-          }
-        }
-      }
-      for (int64_t kk = p; kk < q; ++kk) {
-        int32_t u = a.b.i_src[kk];
-        bool ins = a.b.i_op[kk] == RTEC_OP_INSERT;
-        const float* zrow = a.st.Z + static_cast<int64_t>(u) * d;
-        const float* errow = a.st.er + static_cast<int64_t>(u) * H;
-        if (!ins && a.prev_bm_dst && bm_test(a.prev_bm_dst, u)) {
-          int32_t sl = a.prev_slot[u];
-          zrow = a.st.Z_log + static_cast<int64_t>(sl) * d;
-          errow = a.st.er_log + static_cast<int64_t>(sl) * H;
-        }
-        float z[K][VEC];
-        R::load(zrow, d, z);
-        float sgn = ins ? 1.f : -1.f;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          float at = 0.f;
-          if (R::has(k, d)) at = expf(leaky02(elv[k] + errow[chunk_head<VEC>(k, dh)]));
-          cacc[k] += sgn * at;
-#pragma unroll
-          for (int jj = 0; jj < VEC; ++jj) acc.v[k][jj] = fmaf(sgn * at, z[k][jj], acc.v[k][jj]);
-        }
-      }
-      // add the cached state (Alg. 3 lines 5-7: strip with the old sum = keep S un-normalised)
-      if (a.g.in_deg_prev[v] > 0 && a.g.in_deg[v] > 0) {
-        float sv[K][VEC];
-        R::load_rw(a.st.S + static_cast<int64_t>(v) * d, d, sv);
-        acc.add(sv);
-#pragma unroll
-        for (int k = 0; k < K; ++k)
-          if (R::has(k, d)) cacc[k] += a.st.ctx[static_cast<int64_t>(v) * H + chunk_head<VEC>(k, dh)];
+    const bool recompute = FULL || (a.prev_bm_dst && bm_test(a.prev_bm_dst, v));
+    int64_t p = 0, q = 0;
+    if (!FULL) {
+      int2 rg = reinterpret_cast<const int2*>(a.b.irange)[v];
+      if (rg.x >= 0) {
+        p = rg.x;
+        q = rg.x + rg.y;
       }
     }
-    int32_t indeg = recompute ? len : a.g.in_deg[v];
-    if (indeg == 0) {
-      acc.zero();
+    GatEdgeState es;
+    gat_state<VEC, K>(a, v, es);
+    R acc;
+    acc.zero();
+    float cacc[K];
 #pragma unroll
-      for (int k = 0; k < K; ++k) cacc[k] = 0.f;
-    }
-    acc.store(a.st.S + static_cast<int64_t>(v) * d, d);
-    // ctx per head: written by the lane holding the head's first chunk
+    for (int k = 0; k < K; ++k) cacc[k] = 0.f;
+    int32_t e0 = c * kChunk, e1 = min(len, e0 + kChunk);
+    gat_edges<VEC, K>(a, es, a.g.in.beg[v], e0, e1, p, q, recompute, acc, cacc);
+    if (!recompute && c == 0) gat_struct<VEC, K>(a, es, p, q, acc, cacc);
+    float* part = hp.part + t * pw;
+    acc.store(part, d);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      int c = lane + 32 * k;
-      if (c * VEC < d && (c * VEC) % dh == 0)
-        for (int hh = 0; hh < (VEC > dh ? VEC / dh : 1); ++hh) {
-          int h = (c * VEC) / dh + hh;
-          a.st.ctx[static_cast<int64_t>(v) * H + h] = cacc[k];
+      int cc = lane_id() + 32 * k;
+      if (cc * VEC < d && (cc * VEC) % dh == 0)
+        for (int hh = 0; hh < (VEC > dh ? VEC / dh : 1); ++hh) part[d + (cc * VEC) / dh + hh] = cacc[k];
+    }
+    __threadfence();
+    int old = 0;
+    if (lane_id() == 0) old = atomicAdd(hp.arrive + j, 1);
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old != nch - 1) continue;
+    __threadfence();
+    acc.zero();
+#pragma unroll
+    for (int k = 0; k < K; ++k) cacc[k] = 0.f;
+    for (int32_t cc = 0; cc < nch; ++cc) {  // chunk order: deterministic sum
+      const float* src = hp.part + (c0 + cc) * pw;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        int col = lane_id() + 32 * k;
+        if (col * VEC < d) {
+#pragma unroll
+          for (int jj = 0; jj < VEC; ++jj) acc.v[k][jj] += __ldcg(src + col * VEC + jj);
+          cacc[k] += __ldcg(src + d + chunk_head<VEC>(k, dh));
         }
+      }
     }
-    // a = S / ctx (models.py:280), h = elu(a) (models.py:282); DeltaLog capture
-    float* hrow = a.st.H_out + static_cast<int64_t>(v) * d;
-    if (!recompute_all && a.st.log_out) {
-      float old[K][VEC];
-      R::load_rw(hrow, d, old);
-      R o;
-      o.zero();
-      o.add(old);
-      o.store(a.st.log_out + i * d, d);
-    }
-    R o;
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-#pragma unroll
-      for (int jj = 0; jj < VEC; ++jj) o.v[k][jj] = indeg > 0 ? elu1(acc.v[k][jj] / cacc[k]) : 0.f;
-    o.store(hrow, d);
+    gat_finalize<VEC, K, FULL>(a, i, v, len, recompute, acc, cacc);
   }
+}
+
+template <bool FULL>
+static int launch_gat(LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_edges, Ws& w, cudaStream_t s) {
+  const int d = a.L.d_out;
+  if (a.L.heads > kHMax) {
+    set_error("GAT supports up to %d heads (got %d)", kHMax, a.L.heads);
+    return RTEC_SHAPE_ERROR;
+  }
+  a.d_agg = d;
+  HeavyPlan hp{};
+  RTEC_TRY(plan_heavy<FULL>(a, rows, max_rows, max_edges, (d + a.L.heads + 3) & ~3, w, s, hp));
+  const int grid = kSMs * 8;
+  const int dh = d / a.L.heads;
+  bool ok;
+  RTEC_PROF(FULL ? "k_gat_full" : "k_gat_layer", s);
+  if (d % 4 == 0 && dh % 4 == 0) {
+    ok = RTEC_ROW_DISPATCH(d, (k_gat_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows),
+                               k_gat_heavy<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows, hp)));
+  } else {
+    int kk = (d + 31) / 32;
+    ok = true;
+    if (kk <= 1) {
+      k_gat_light<1, 1, FULL><<<grid, kLBlk, 0, s>>>(a, rows);
+      k_gat_heavy<1, 1, FULL><<<grid, kLBlk, 0, s>>>(a, rows, hp);
+    } else if (kk <= 4) {
+      k_gat_light<1, 4, FULL><<<grid, kLBlk, 0, s>>>(a, rows);
+      k_gat_heavy<1, 4, FULL><<<grid, kLBlk, 0, s>>>(a, rows, hp);
+    } else if (kk <= 8) {
+      k_gat_light<1, 8, FULL><<<grid, kLBlk, 0, s>>>(a, rows);
+      k_gat_heavy<1, 8, FULL><<<grid, kLBlk, 0, s>>>(a, rows, hp);
+    } else {
+      ok = false;
+    }
+  }
+  if (!ok) {
+    set_error("row width %d unsupported", d);
+    return RTEC_SHAPE_ERROR;
+  }
+  RTEC_LAUNCH_CHECK("k_gat");
+  return RTEC_OK;
 }
 
 // el / er for projected rows: el = a[:dh]·z_h, er = a[dh:]·z_h per head
@@ -940,28 +1124,8 @@ int rtec_layer_incremental(const rtec_graph_t* g, const rtec_batch_t* b, const r
   a.prev_slot = prev ? (prev->chg_slot ? prev->chg_slot : prev->dst_slot) : nullptr;
   a.err = err;
   const int grid = kSMs * 8;
-  if (L->model == RTEC_MODEL_GAT) {
-    a.d_agg = L->d_out;
-    int dh = L->d_out / L->heads;
-    bool ok;
-    RTEC_PROF("k_gat_layer", s);
-    if (L->d_out % 4 == 0 && dh % 4 == 0) {
-      ok = RTEC_ROW_DISPATCH(L->d_out, (k_gat_layer<VEC, K><<<grid, kLBlk, 0, s>>>(a, 0)));
-    } else {
-      int kk = (L->d_out + 31) / 32;
-      ok = true;
-      if (kk <= 1) k_gat_layer<1, 1><<<grid, kLBlk, 0, s>>>(a, 0);
-      else if (kk <= 4) k_gat_layer<1, 4><<<grid, kLBlk, 0, s>>>(a, 0);
-      else if (kk <= 8) k_gat_layer<1, 8><<<grid, kLBlk, 0, s>>>(a, 0);
-      else ok = false;
-    }
-    if (!ok) {
-      set_error("row width %d unsupported", L->d_out);
-      return RTEC_SHAPE_ERROR;
-    }
-    RTEC_LAUNCH_CHECK("k_gat_layer");
-    return RTEC_OK;
-  }
+  if (L->model == RTEC_MODEL_GAT)
+    return launch_gat<false>(a, AggRows{f->dst_list, f->n_dst, n}, n, g->in.slots, w, s);
   a.d_agg = L->d_in;
   if (L->model == RTEC_MODEL_GIN_MAX) {
     a.tc_nkb = L->Wt_hi ? tc_nkb_of(L->d_in) : 0;
@@ -1009,25 +1173,8 @@ int rtec_layer_full(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* 
     RTEC_TRY(gemm_launch(gz, s));
     k_gat_logits<<<grid, kLBlk, 0, s>>>(st->Z, nullptr, nullptr, n, L->d_out, L->heads, L->att, st->el, st->er,
                                         nullptr, nullptr);
-    a.d_agg = L->d_out;
-    int dh = L->d_out / L->heads;
-    bool ok;
-    if (L->d_out % 4 == 0 && dh % 4 == 0) {
-      ok = RTEC_ROW_DISPATCH(L->d_out, (k_gat_layer<VEC, K><<<grid, kLBlk, 0, s>>>(a, 1)));
-    } else {
-      int kk = (L->d_out + 31) / 32;
-      ok = true;
-      if (kk <= 1) k_gat_layer<1, 1><<<grid, kLBlk, 0, s>>>(a, 1);
-      else if (kk <= 4) k_gat_layer<1, 4><<<grid, kLBlk, 0, s>>>(a, 1);
-      else if (kk <= 8) k_gat_layer<1, 8><<<grid, kLBlk, 0, s>>>(a, 1);
-      else ok = false;
-    }
-    if (!ok) {
-      set_error("row width %d unsupported", L->d_out);
-      return RTEC_SHAPE_ERROR;
-    }
-    RTEC_LAUNCH_CHECK("k_gat_layer(full)");
-    return RTEC_OK;
+    Ws w(ws, ws_bytes);
+    return launch_gat<true>(a, AggRows{nullptr, nullptr, n}, n, g->in.slots, w, s);
   }
   a.d_agg = L->d_in;
   a.tc_nkb = L->Wt_hi ? tc_nkb_of(L->d_in) : 0;
