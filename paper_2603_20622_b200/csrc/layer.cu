@@ -364,7 +364,7 @@ static int agg_slice_width() {
 // heavy-destination plan (list, chunk offsets, chunk -> heavy map); partial rows of `pw` floats
 template <bool FULL>
 static int plan_heavy(const LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_edges, int pw, Ws& w,
-                      cudaStream_t s, HeavyPlan& hp) {
+                      cudaStream_t s, HeavyPlan& hp, bool every_long_run = false) {
   hp.heavy = w.alloc<int32_t>(max_rows + 1);
   hp.n_heavy = w.alloc<int64_t>(2);
   hp.hoff = w.alloc<int64_t>(max_rows + 2);
@@ -375,7 +375,7 @@ static int plan_heavy(const LayerArgs& a, AggRows rows, int64_t max_rows, int64_
   RTEC_WS_CHECK(w);
   RTEC_CUDA(cudaMemsetAsync(hp.n_heavy, 0, sizeof(int64_t) * 2, s));
   RTEC_CUDA(cudaMemsetAsync(hp.hoff, 0, sizeof(int64_t), s));
-  HeavyFlagF hf{rows, a.g.in.len, FULL ? nullptr : a.f.n_src};
+  HeavyFlagF hf{rows, a.g.in.len, (FULL || every_long_run) ? nullptr : a.f.n_src};
   Count cnt{rows.n_dev, max_rows};
   if (!rows.n_dev) cnt = Count{nullptr, rows.n_all};
   RTEC_TRY(exclusive_scan(hf, cnt, max_rows, HeavyStore{hf, hp.heavy}, hp.n_heavy, w, s));
@@ -441,14 +441,24 @@ __device__ __forceinline__ void max_row(const float (&r)[K][VEC], RowAcc<VEC, K>
 }
 
 template <int VEC, int K>
-__device__ __forceinline__ void max_full_run(const LayerArgs& a, int64_t beg, int32_t len, RowAcc<VEC, K>& acc) {
+__device__ __forceinline__ void max_neg_inf(RowAcc<VEC, K>& acc) {
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) acc.v[k][j] = -INFINITY;
+}
+
+// max over the current rows of in-run positions [e0, e1), 4 rows in flight
+template <int VEC, int K>
+__device__ __forceinline__ void max_run(const LayerArgs& a, int64_t beg, int32_t e0, int32_t e1,
+                                        RowAcc<VEC, K>& acc) {
   using R = RowAcc<VEC, K>;
   const int d = a.d_agg;
   const int lane = lane_id();
-  for (int32_t c0 = 0; c0 < len; c0 += 32) {
+  for (int32_t c0 = e0; c0 < e1; c0 += 32) {
     int32_t j = c0 + lane;
-    int32_t u = j < len ? a.g.in.nbr[beg + j] : 0;
-    int cnt = min(32, len - c0);
+    int32_t u = j < e1 ? a.g.in.nbr[beg + j] : 0;
+    int cnt = min(32, e1 - c0);
     for (int t = 0; t < cnt; t += 4) {
       float r[4][K][VEC];
 #pragma unroll
@@ -462,117 +472,309 @@ __device__ __forceinline__ void max_full_run(const LayerArgs& a, int64_t beg, in
   }
 }
 
+// incremental candidates of in-run positions [e0, e1) (+ structural edges when
+// p < q): new rows of value-changed / inserted sources raise the max; returns
+// whether a retracted old value attained the cached max sv in some column
+template <int VEC, int K>
+__device__ __forceinline__ bool max_incremental(const LayerArgs& a, int64_t beg, int32_t e0, int32_t e1, int64_t p,
+                                                int64_t q, bool with_struct, const float (&sv)[K][VEC],
+                                                RowAcc<VEC, K>& acc) {
+  using R = RowAcc<VEC, K>;
+  const int d = a.d_agg;
+  const int lane = lane_id();
+  bool retract = false;
+  if (*a.f.n_src > 0) {
+    for (int32_t c0 = e0; c0 < e1; c0 += 32) {
+      int32_t j = c0 + lane;
+      int32_t u = 0;
+      bool hit = false;
+      if (j < e1) {
+        u = a.g.in.nbr[beg + j];
+        hit = bm_test(a.f.bm_src, u) && !in_range_has(a.b.i_src, p, q, u);
+      }
+      unsigned m = __ballot_sync(0xffffffffu, hit);
+      while (m) {
+        int32_t uu[2];
+        int cnt = 0;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          int src = m ? __ffs(m) - 1 : 0;
+          if (m) {
+            m &= m - 1;
+            cnt = t + 1;
+          }
+          uu[t] = __shfl_sync(0xffffffffu, u, src);
+        }
+        float hn[2][K][VEC], ho[2][K][VEC];
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+          if (t < cnt) {
+            R::load(a.st.H_in + static_cast<int64_t>(uu[t]) * d, d, hn[t]);
+            const float* orow = a.st.H_in + static_cast<int64_t>(uu[t]) * d;
+            if (a.prev_bm_dst && bm_test(a.prev_bm_dst, uu[t]))
+              orow = a.st.log_in + static_cast<int64_t>(a.prev_slot[uu[t]]) * d;
+            R::load(orow, d, ho[t]);
+          }
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+          if (t < cnt) {
+            max_row<VEC, K>(hn[t], acc);
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+#pragma unroll
+              for (int jj = 0; jj < VEC; ++jj)
+                retract |= R::has(k, d) && ho[t][k][jj] >= sv[k][jj] && hn[t][k][jj] < ho[t][k][jj];
+          }
+      }
+    }
+  }
+  if (with_struct) {
+    for (int64_t kk = p; kk < q; ++kk) {
+      int32_t u = a.b.i_src[kk];
+      float r[K][VEC];
+      if (a.b.i_op[kk] == RTEC_OP_INSERT) {
+        R::load(a.st.H_in + static_cast<int64_t>(u) * d, d, r);
+        max_row<VEC, K>(r, acc);
+      } else {
+        const float* orow = a.st.H_in + static_cast<int64_t>(u) * d;
+        if (a.prev_bm_dst && bm_test(a.prev_bm_dst, u)) orow = a.st.log_in + static_cast<int64_t>(a.prev_slot[u]) * d;
+        R::load(orow, d, r);
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+#pragma unroll
+          for (int jj = 0; jj < VEC; ++jj) retract |= R::has(k, d) && r[k][jj] >= sv[k][jj];
+      }
+    }
+  }
+  return __any_sync(0xffffffffu, retract);
+}
+
+// S = a_v, GEMM input h_v + a_v (models.py:187-189); empty neighbourhood -> 0
+template <int VEC, int K>
+__device__ __forceinline__ void max_finalize(const LayerArgs& a, int64_t i, int32_t v, int32_t len,
+                                             RowAcc<VEC, K>& acc) {
+  using R = RowAcc<VEC, K>;
+  const int d = a.d_agg;
+  if (len == 0) acc.zero();
+  acc.store(a.st.S + static_cast<int64_t>(v) * d, d);
+  R out;
+  out.zero();
+  out.add(acc.v);
+  float h[K][VEC];
+  R::load(a.st.H_in + static_cast<int64_t>(v) * d, d, h);
+  out.add(h);
+  if (a.tc_nkb > 0) out.store_tiled(a.st.gemm_in, i, 0, d, d, a.tc_nkb);
+  else out.store(a.st.gemm_in + i * d, d);
+}
+
+__device__ __forceinline__ int2 irange_of(const LayerArgs& a, int32_t v) {
+  int2 rg = reinterpret_cast<const int2*>(a.b.irange)[v];
+  return rg.x >= 0 ? make_int2(rg.x, rg.x + rg.y) : make_int2(0, 0);
+}
+
+// When most sources changed (|S(l)| > n/8), nearly every cached max is retracted
+// in some column; re-maxing every affected destination directly (1 row gather per
+// in-edge) then beats the incremental pass (2 per changed edge) plus rescans.
+template <bool FULL>
+__device__ __forceinline__ bool max_direct(const LayerArgs& a) {
+  return !FULL && (*a.f.n_src) * 8 > a.g.n;
+}
+
+// destinations with <= kChunk scanned edges: one warp each, re-max in place on retract
 template <int VEC, int K, bool FULL>
-__global__ void __launch_bounds__(kLBlk) k_max_layer(LayerArgs a, AggRows rows) {
+__global__ void __launch_bounds__(kLBlk) k_max_light(LayerArgs a, AggRows rows) {
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
   const int d = a.d_agg;
   const int64_t nr = rows.count();
-  const int lane = lane_id();
+  const bool direct = max_direct<FULL>(a);
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = warp; i < nr; i += nw) {
     int32_t v = rows.at(i);
     int64_t beg = a.g.in.beg[v];
     int32_t len = a.g.in.len[v];
-    float* srow = a.st.S + static_cast<int64_t>(v) * d;
+    if (len > kChunk) continue;  // heavy pass
     R acc;
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-#pragma unroll
-      for (int j = 0; j < VEC; ++j) acc.v[k][j] = -INFINITY;
-    bool rescan = FULL;
-    if (!FULL && len > 0) {
-      int64_t p = 0, q = 0;
-      int2 rg = reinterpret_cast<const int2*>(a.b.irange)[v];
-      if (rg.x >= 0) {
-        p = rg.x;
-        q = rg.x + rg.y;
-      }
+    max_neg_inf<VEC, K>(acc);
+    bool rescan = FULL || direct;
+    if (!rescan && len > 0) {
+      int2 pq = irange_of(a, v);
       const bool had = a.g.in_deg_prev[v] > 0;
       float sv[K][VEC];
-      R::load_rw(srow, d, sv);
-      bool retract = false;
-      // value-changed sources (u in S(l), edge not inserted)
-      if (*a.f.n_src > 0) {
-        for (int32_t c0 = 0; c0 < len; c0 += 32) {
-          int32_t j = c0 + lane;
-          int32_t u = 0;
-          bool hit = false;
-          if (j < len) {
-            u = a.g.in.nbr[beg + j];
-            hit = bm_test(a.f.bm_src, u) && !in_range_has(a.b.i_src, p, q, u);
-          }
-          unsigned m = __ballot_sync(0xffffffffu, hit);
-          while (m) {
-            int src = __ffs(m) - 1;
-            m &= m - 1;
-            int32_t uu = __shfl_sync(0xffffffffu, u, src);
-            float hn[K][VEC], ho[K][VEC];
-            R::load(a.st.H_in + static_cast<int64_t>(uu) * d, d, hn);
-            const float* orow = a.st.H_in + static_cast<int64_t>(uu) * d;
-            if (a.prev_bm_dst && bm_test(a.prev_bm_dst, uu))
-              orow = a.st.log_in + static_cast<int64_t>(a.prev_slot[uu]) * d;
-            R::load(orow, d, ho);
-            max_row<VEC, K>(hn, acc);
-#pragma unroll
-            for (int k = 0; k < K; ++k)
-#pragma unroll
-              for (int jj = 0; jj < VEC; ++jj)
-                retract |= R::has(k, d) && ho[k][jj] >= sv[k][jj] && hn[k][jj] < ho[k][jj];
-          }
-        }
-      }
-      // structural edges: inserts raise, deletes may retract the max
-      for (int64_t kk = p; kk < q; ++kk) {
-        int32_t u = a.b.i_src[kk];
-        float r[K][VEC];
-        if (a.b.i_op[kk] == RTEC_OP_INSERT) {
-          R::load(a.st.H_in + static_cast<int64_t>(u) * d, d, r);
-          max_row<VEC, K>(r, acc);
-        } else {
-          const float* orow = a.st.H_in + static_cast<int64_t>(u) * d;
-          if (a.prev_bm_dst && bm_test(a.prev_bm_dst, u)) orow = a.st.log_in + static_cast<int64_t>(a.prev_slot[u]) * d;
-          R::load(orow, d, r);
-#pragma unroll
-          for (int k = 0; k < K; ++k)
-#pragma unroll
-            for (int jj = 0; jj < VEC; ++jj) retract |= R::has(k, d) && r[k][jj] >= sv[k][jj];
-        }
-      }
-      rescan = had && __any_sync(0xffffffffu, retract);
+      R::load_rw(a.st.S + static_cast<int64_t>(v) * d, d, sv);
+      bool retract = max_incremental<VEC, K>(a, beg, 0, len, pq.x, pq.y, true, sv, acc);
+      rescan = had && retract;
       if (!rescan && had) max_row<VEC, K>(sv, acc);
     }
     if (rescan) {
-#pragma unroll
-      for (int k = 0; k < K; ++k)
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) acc.v[k][j] = -INFINITY;
-      max_full_run<VEC, K>(a, beg, len, acc);
+      max_neg_inf<VEC, K>(acc);
+      max_run<VEC, K>(a, beg, 0, len, acc);
     }
-    if (len == 0) acc.zero();  // empty neighbourhood -> zero aggregate
-    acc.store(srow, d);
-    R out;
-    out.zero();
-    out.add(acc.v);
-    float h[K][VEC];
-    R::load(a.st.H_in + static_cast<int64_t>(v) * d, d, h);
-    out.add(h);  // GIN update input h_v + a_v (models.py:187-189)
-    if (a.tc_nkb > 0) out.store_tiled(a.st.gemm_in, i, 0, d, d, a.tc_nkb);
-    else out.store(a.st.gemm_in + i * d, d);
+    max_finalize<VEC, K>(a, i, v, len, acc);
+  }
+}
+
+// Rescan queue of heavy destinations whose cached max was retracted
+struct MaxRescan {
+  int64_t* n;       // [1] queued destinations
+  int64_t* total;   // [1] queued chunks
+  int32_t* dest;    // [max_rows] heavy index j of each queued destination
+  int64_t* off;     // [max_rows] first chunk of each queued destination
+  int32_t* cmap;    // [max_chunks] chunk -> queue entry
+  int32_t* arrive;  // [max_rows]
+  int32_t* flag;    // [max_rows] per heavy destination: retract seen by some chunk
+  float* part;      // [max_chunks, d]
+};
+
+// heavy destinations, pass 1: chunked incremental candidates (FULL: chunked max);
+// the last chunk to arrive finalizes, or queues the destination for a rescan
+template <int VEC, int K, bool FULL>
+__global__ void __launch_bounds__(kLBlk) k_max_heavy(LayerArgs a, AggRows rows, HeavyPlan hp, MaxRescan rq) {
+  using R = RowAcc<VEC, K>;
+  if (!FULL && err_set(a.err)) return;
+  const int64_t nh = *hp.n_heavy;
+  if (nh == 0) return;
+  const int64_t T = hp.hoff[nh];
+  const int d = a.d_agg;
+  const bool direct = max_direct<FULL>(a);
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = warp; t < T; t += nw) {
+    int32_t j = hp.cmap[t];
+    int64_t c0 = hp.hoff[j];
+    int32_t nch = static_cast<int32_t>(hp.hoff[j + 1] - c0);
+    int32_t c = static_cast<int32_t>(t - c0);
+    int64_t i = hp.heavy[j];
+    int32_t v = rows.at(i);
+    int64_t beg = a.g.in.beg[v];
+    int32_t len = a.g.in.len[v];
+    int32_t e0 = c * kChunk, e1 = min(len, e0 + kChunk);
+    R acc;
+    max_neg_inf<VEC, K>(acc);
+    float sv[K][VEC];
+    bool had = false;
+    if (FULL || direct) {
+      max_run<VEC, K>(a, beg, e0, e1, acc);
+    } else {
+      int2 pq = irange_of(a, v);
+      had = a.g.in_deg_prev[v] > 0;
+      R::load_rw(a.st.S + static_cast<int64_t>(v) * d, d, sv);
+      bool retract = max_incremental<VEC, K>(a, beg, e0, e1, pq.x, pq.y, c == 0, sv, acc);
+      if (retract && had && lane_id() == 0) atomicOr(rq.flag + j, 1);
+    }
+    acc.store(hp.part + t * d, d);
+    __threadfence();
+    int old = 0;
+    if (lane_id() == 0) old = atomicAdd(hp.arrive + j, 1);
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old != nch - 1) continue;
+    __threadfence();
+    if (!FULL && *reinterpret_cast<volatile int32_t*>(rq.flag + j)) {
+      // queue a chunked re-max over the whole post-batch in-run (pass 2)
+      int64_t e = 0, base = 0;
+      if (lane_id() == 0) {
+        e = atomicAdd(reinterpret_cast<unsigned long long*>(rq.n), 1ull);
+        base = atomicAdd(reinterpret_cast<unsigned long long*>(rq.total), static_cast<unsigned long long>(nch));
+        rq.dest[e] = j;
+        rq.off[e] = base;
+        rq.arrive[e] = 0;
+      }
+      e = __shfl_sync(0xffffffffu, e, 0);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      for (int32_t cc = lane_id(); cc < nch; cc += 32) rq.cmap[base + cc] = static_cast<int32_t>(e);
+      continue;
+    }
+    max_neg_inf<VEC, K>(acc);
+    for (int32_t cc = 0; cc < nch; ++cc) {
+      float r[K][VEC];
+      const float* src = hp.part + (c0 + cc) * d;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        int col = lane_id() + 32 * k;
+#pragma unroll
+        for (int jj = 0; jj < VEC; ++jj) r[k][jj] = (col * VEC < d) ? __ldcg(src + col * VEC + jj) : -INFINITY;
+      }
+      max_row<VEC, K>(r, acc);
+    }
+    if (!FULL && had) max_row<VEC, K>(sv, acc);
+    max_finalize<VEC, K>(a, i, v, len, acc);
+  }
+}
+
+// heavy destinations, pass 2: chunked re-max of the queued destinations
+template <int VEC, int K>
+__global__ void __launch_bounds__(kLBlk) k_max_rescan(LayerArgs a, AggRows rows, HeavyPlan hp, MaxRescan rq) {
+  using R = RowAcc<VEC, K>;
+  if (err_set(a.err)) return;
+  const int64_t T = *rq.total;
+  const int d = a.d_agg;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = warp; t < T; t += nw) {
+    int32_t e = rq.cmap[t];
+    int32_t j = rq.dest[e];
+    int64_t c0 = rq.off[e];
+    int32_t nch = static_cast<int32_t>(hp.hoff[j + 1] - hp.hoff[j]);
+    int32_t c = static_cast<int32_t>(t - c0);
+    int64_t i = hp.heavy[j];
+    int32_t v = rows.at(i);
+    int64_t beg = a.g.in.beg[v];
+    int32_t len = a.g.in.len[v];
+    R acc;
+    max_neg_inf<VEC, K>(acc);
+    max_run<VEC, K>(a, beg, c * kChunk, min(len, (c + 1) * kChunk), acc);
+    acc.store(rq.part + t * d, d);
+    __threadfence();
+    int old = 0;
+    if (lane_id() == 0) old = atomicAdd(rq.arrive + e, 1);
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old != nch - 1) continue;
+    __threadfence();
+    max_neg_inf<VEC, K>(acc);
+    for (int32_t cc = 0; cc < nch; ++cc) {
+      float r[K][VEC];
+      const float* src = rq.part + (c0 + cc) * d;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        int col = lane_id() + 32 * k;
+#pragma unroll
+        for (int jj = 0; jj < VEC; ++jj) r[k][jj] = (col * VEC < d) ? __ldcg(src + col * VEC + jj) : -INFINITY;
+      }
+      max_row<VEC, K>(r, acc);
+    }
+    max_finalize<VEC, K>(a, i, v, len, acc);
   }
 }
 
 template <bool FULL>
-static int launch_max(LayerArgs& a, AggRows rows, cudaStream_t s) {
+static int launch_max(LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_edges, Ws& w, cudaStream_t s) {
+  const int d = a.d_agg;
   const int grid = kSMs * 8;
+  HeavyPlan hp{};
+  RTEC_TRY(plan_heavy<FULL>(a, rows, max_rows, max_edges, d, w, s, hp, true));
+  MaxRescan rq{};
+  int64_t max_chunks = max_edges / kChunk + 2 + max_rows / 64;
+  rq.n = w.alloc<int64_t>(2);
+  rq.total = rq.n + 1;
+  rq.dest = w.alloc<int32_t>(max_rows + 1);
+  rq.off = w.alloc<int64_t>(max_rows + 1);
+  rq.cmap = w.alloc<int32_t>(max_chunks);
+  rq.arrive = w.alloc<int32_t>(max_rows + 1);
+  rq.flag = w.alloc<int32_t>(max_rows + 1);
+  rq.part = FULL ? nullptr : w.alloc<float>(max_chunks * static_cast<int64_t>(d));
+  RTEC_WS_CHECK(w);
+  RTEC_CUDA(cudaMemsetAsync(rq.n, 0, sizeof(int64_t) * 2, s));
+  RTEC_CUDA(cudaMemsetAsync(rq.flag, 0, sizeof(int32_t) * (max_rows + 1), s));
   RTEC_PROF(FULL ? "k_max_full" : "k_max_inc", s);
-  bool ok = RTEC_ROW_DISPATCH(a.d_agg, (k_max_layer<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows)));
+  bool ok = RTEC_ROW_DISPATCH(d, (k_max_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows),
+                                  k_max_heavy<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows, hp, rq)));
+  if (ok && !FULL) ok = RTEC_ROW_DISPATCH(d, (k_max_rescan<VEC, K><<<grid, kLBlk, 0, s>>>(a, rows, hp, rq)));
   if (!ok) {
-    set_error("row width %d unsupported", a.d_agg);
+    set_error("row width %d unsupported", d);
     return RTEC_SHAPE_ERROR;
   }
-  RTEC_LAUNCH_CHECK("k_max_layer");
+  RTEC_LAUNCH_CHECK("k_max");
   return RTEC_OK;
 }
 
@@ -1129,7 +1331,7 @@ int rtec_layer_incremental(const rtec_graph_t* g, const rtec_batch_t* b, const r
   a.d_agg = L->d_in;
   if (L->model == RTEC_MODEL_GIN_MAX) {
     a.tc_nkb = L->Wt_hi ? tc_nkb_of(L->d_in) : 0;
-    RTEC_TRY(launch_max<false>(a, AggRows{f->dst_list, f->n_dst, n}, s));
+    RTEC_TRY(launch_max<false>(a, AggRows{f->dst_list, f->n_dst, n}, n, g->in.slots, w, s));
     return run_update(L, st, f->n_dst, n, f->dst_list, st->log_out, err, s);
   }
   float* delta = w.alloc<float>(n * static_cast<int64_t>(L->d_in));
@@ -1180,7 +1382,8 @@ int rtec_layer_full(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* 
   a.tc_nkb = L->Wt_hi ? tc_nkb_of(L->d_in) : 0;
   int64_t mr = rows ? max_rows : n;
   if (L->model == RTEC_MODEL_GIN_MAX) {
-    RTEC_TRY(launch_max<true>(a, AggRows{rows, rows ? n_rows : nullptr, n}, s));
+    Ws w(ws, ws_bytes);
+    RTEC_TRY(launch_max<true>(a, AggRows{rows, rows ? n_rows : nullptr, n}, mr, g->in.slots, w, s));
     return run_update(L, st, rows ? n_rows : nullptr, mr, rows, nullptr, nullptr, s);
   }
   {
