@@ -431,66 +431,115 @@ __device__ __forceinline__ int64_t upper_bound_dev(const T* a, int64_t lo, int64
   return lo;
 }
 
-// element-parallel merge: old elements and update items of every group
-__global__ void k_merge_items(MergeIn in, MergePlan p, rtec_adj_t a, const uint64_t* err) {
+// Work positions are processed in tiles of kMT consecutive positions per block:
+// two threads locate the groups of the tile's first / last position (one global
+// binary search each), the groups' offsets in between are staged in shared memory
+// and every thread finds its group there -- instead of a ~20-step dependent
+// binary search over the global offsets per element.
+constexpr int kMT = 1024;
+
+struct TileGroups {
+  int64_t g0, ng;  // first group of the tile, number of groups staged (0: fall back to global search)
+};
+
+__device__ __forceinline__ TileGroups tile_groups(const int64_t* off, int64_t G, int64_t t0, int64_t t1,
+                                                  int64_t* s_off, int64_t* s_g) {
+  if (threadIdx.x == 0) s_g[0] = upper_bound_dev<int64_t>(off, 0, G, t0) - 1;
+  if (threadIdx.x == 1) s_g[1] = upper_bound_dev<int64_t>(off, 0, G, t1 - 1) - 1;
+  __syncthreads();
+  TileGroups tg{s_g[0], s_g[1] - s_g[0] + 1};
+  if (tg.ng > kMT) tg.ng = 0;
+  for (int64_t k = threadIdx.x; k < tg.ng; k += blockDim.x) s_off[k] = off[tg.g0 + k + 1];  // group ends
+  __syncthreads();
+  return tg;
+}
+
+__device__ __forceinline__ int64_t group_of(const TileGroups& tg, const int64_t* s_off, const int64_t* off, int64_t G,
+                                            int64_t i) {
+  if (tg.ng == 0) return upper_bound_dev<int64_t>(off, 0, G, i) - 1;
+  int64_t lo = 0, hi = tg.ng - 1;  // first staged group whose end is > i
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (s_off[mid] <= i) lo = mid + 1;
+    else hi = mid;
+  }
+  return tg.g0 + lo;
+}
+
+// element-parallel merge: old elements (from the first changed position) and update items of every group
+__global__ void __launch_bounds__(kBlk) k_merge_items(MergeIn in, MergePlan p, rtec_adj_t a, const uint64_t* err) {
+  __shared__ int64_t s_off[kMT];
+  __shared__ int64_t s_g[2];
   if (err_set(err)) return;
   int64_t G = *p.G;
   if (G == 0) return;
   int64_t W = p.work_off[G];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < W; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t g = upper_bound_dev<int64_t>(p.work_off, 0, G, i) - 1;
-    int64_t t = i - p.work_off[g];
-    int32_t v = p.gv[g];
-    int64_t s = p.gstart[g], e = p.gstart[g + 1];
-    int64_t b = a.beg[v];
-    int32_t L = a.len[v];
-    const int32_t f0 = p.first[g];
-    int32_t w;
-    int64_t tsv = 0;
-    int64_t out;
-    if (t < L - f0) {
-      t += f0;
-      w = a.nbr[b + t];
-      int64_t q = lower_bound_dev(in.nbr, s, e, w);
-      if (q < e && in.nbr[q] == w) continue;  // deleted (an applied insert never hits an existing key)
-      int64_t ins_before = p.pre_ins[q] - p.pre_ins[s];
-      int64_t del_before = (q - s) - ins_before;
-      out = t - del_before + ins_before;
-      if (a.ts) tsv = a.ts[b + t];
-    } else {
-      int64_t k = s + (t - (L - f0));
-      if (in.op[k] != RTEC_OP_INSERT) continue;
-      w = in.nbr[k];
-      int64_t pos = lower_bound_dev(a.nbr, b, b + L, w) - b;
-      int64_t ins_before = p.pre_ins[k] - p.pre_ins[s];
-      int64_t del_before = (k - s) - ins_before;
-      out = pos - del_before + ins_before;
-      if (in.ts) tsv = in.ts[k];
+  for (int64_t t0 = static_cast<int64_t>(blockIdx.x) * kMT; t0 < W; t0 += static_cast<int64_t>(gridDim.x) * kMT) {
+    const int64_t t1 = t0 + kMT < W ? t0 + kMT : W;
+    TileGroups tg = tile_groups(p.work_off, G, t0, t1, s_off, s_g);
+    for (int64_t i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
+      int64_t g = group_of(tg, s_off, p.work_off, G, i);
+      int64_t t = i - p.work_off[g];
+      int32_t v = p.gv[g];
+      int64_t s = p.gstart[g], e = p.gstart[g + 1];
+      int64_t b = a.beg[v];
+      int32_t L = a.len[v];
+      const int32_t f0 = p.first[g];
+      int32_t w;
+      int64_t tsv = 0;
+      int64_t out;
+      if (t < L - f0) {
+        t += f0;
+        w = a.nbr[b + t];
+        int64_t q = lower_bound_dev(in.nbr, s, e, w);
+        if (q < e && in.nbr[q] == w) continue;  // deleted (an applied insert never hits an existing key)
+        int64_t ins_before = p.pre_ins[q] - p.pre_ins[s];
+        int64_t del_before = (q - s) - ins_before;
+        out = t - del_before + ins_before;
+        if (a.ts) tsv = a.ts[b + t];
+      } else {
+        int64_t k = s + (t - (L - f0));
+        if (in.op[k] != RTEC_OP_INSERT) continue;
+        w = in.nbr[k];
+        int64_t pos = lower_bound_dev(a.nbr, b, b + L, w) - b;
+        int64_t ins_before = p.pre_ins[k] - p.pre_ins[s];
+        int64_t del_before = (k - s) - ins_before;
+        out = pos - del_before + ins_before;
+        if (in.ts) tsv = in.ts[k];
+      }
+      int64_t dst = p.inplace[g] ? -1 : p.dest[g] + out;
+      if (dst < 0) {
+        int64_t so = p.scr_off[g] + out - f0;
+        p.scr_nbr[so] = w;
+        if (p.scr_ts) p.scr_ts[so] = tsv;
+      } else {
+        a.nbr[dst] = w;
+        if (a.ts) a.ts[dst] = tsv;
+      }
     }
-    int64_t dst = p.inplace[g] ? -1 : p.dest[g] + out;
-    if (dst < 0) {
-      int64_t so = p.scr_off[g] + out - f0;
-      p.scr_nbr[so] = w;
-      if (p.scr_ts) p.scr_ts[so] = tsv;
-    } else {
-      a.nbr[dst] = w;
-      if (a.ts) a.ts[dst] = tsv;
-    }
+    __syncthreads();  // s_off reused by the next tile
   }
 }
 
 // copy in-place runs back from scratch (after all reads of the old runs)
-__global__ void k_merge_copyback(MergePlan p, rtec_adj_t a, const uint64_t* err) {
+__global__ void __launch_bounds__(kBlk) k_merge_copyback(MergePlan p, rtec_adj_t a, const uint64_t* err) {
+  __shared__ int64_t s_off[kMT];
+  __shared__ int64_t s_g[2];
   if (err_set(err)) return;
   int64_t G = *p.G;
   if (G == 0) return;
   int64_t S = p.scr_off[G];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t g = upper_bound_dev<int64_t>(p.scr_off, 0, G, i) - 1;
-    int32_t v = p.gv[g];
-    int64_t t = i - p.scr_off[g] + p.first[g];
-    a.nbr[a.beg[v] + t] = p.scr_nbr[i];
-    if (a.ts) a.ts[a.beg[v] + t] = p.scr_ts[i];
+  for (int64_t t0 = static_cast<int64_t>(blockIdx.x) * kMT; t0 < S; t0 += static_cast<int64_t>(gridDim.x) * kMT) {
+    const int64_t t1 = t0 + kMT < S ? t0 + kMT : S;
+    TileGroups tg = tile_groups(p.scr_off, G, t0, t1, s_off, s_g);
+    for (int64_t i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
+      int64_t g = group_of(tg, s_off, p.scr_off, G, i);
+      int32_t v = p.gv[g];
+      int64_t t = i - p.scr_off[g] + p.first[g];
+      a.nbr[a.beg[v] + t] = p.scr_nbr[i];
+      if (a.ts) a.ts[a.beg[v] + t] = p.scr_ts[i];
+    }
+    __syncthreads();
   }
 }
 
@@ -554,8 +603,8 @@ static int merge_plan(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, floa
 static int merge_exec(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, int64_t work_bound, uint64_t* err,
                       cudaStream_t s) {
   RTEC_PROF("adj_merge", s);
-  k_merge_items<<<grid_for(work_bound, kBlk, kSMs * 32), kBlk, 0, s>>>(in, p, a, err);
-  k_merge_copyback<<<grid_for(work_bound, kBlk, kSMs * 32), kBlk, 0, s>>>(p, a, err);
+  k_merge_items<<<grid_for(work_bound, kMT, kSMs * 8), kBlk, 0, s>>>(in, p, a, err);
+  k_merge_copyback<<<grid_for(work_bound, kMT, kSMs * 8), kBlk, 0, s>>>(p, a, err);
   k_merge_commit<<<grid_for(in.maxK, kBlk), kBlk, 0, s>>>(p, a, err);
   k_commit_reserve<<<1, 32, 0, s>>>(p, a, err);
   RTEC_LAUNCH_CHECK("merge_exec");
