@@ -300,6 +300,7 @@ void rtec_prof_enable(int on);  /* bracket kernels with CUDA events (bench / pro
 size_t rtec_prof_report(char* buf, size_t len, int reset); /* "name count total_ms" lines */
 void rtec_struct_sizes(int64_t* out6); /* sizeof adj, graph, batch, frontier, layer, state */
 const char* rtec_last_error(void);
+int64_t rtec_graph_kernel_nodes(void* graph); /* kernel nodes of a captured cudaGraph_t (launch census) */
 const char* rtec_version(void);
 int rtec_device_sm_count(void);
 

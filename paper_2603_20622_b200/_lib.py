@@ -101,6 +101,7 @@ _SIGS = {
     "rtec_prof_enable": (None, [C.c_int]),
     "rtec_prof_report": (SZ, [C.c_char_p, SZ, C.c_int]),
     "rtec_last_error": (C.c_char_p, []),
+    "rtec_graph_kernel_nodes": (I64, [P]),
     "rtec_version": (C.c_char_p, []),
     "rtec_device_sm_count": (C.c_int, []),
 }
@@ -171,6 +172,20 @@ def stream_handle():
     import torch
 
     return torch.cuda.current_stream().cuda_stream
+
+
+_prof_on = False
+
+
+def prof_enable(on: bool) -> None:
+    """Toggle the library's per-kernel CUDA-event hook (bench / profiling only)."""
+    global _prof_on
+    _prof_on = bool(on)
+    load().rtec_prof_enable(1 if on else 0)
+
+
+def prof_enabled() -> bool:
+    return _prof_on
 
 
 def prof_report(reset: bool = True) -> dict:

@@ -1,3 +1,4 @@
+#include <vector>
 // capi.cu -- library-level C entry points (workspace sizing, diagnostics).
 #include <string.h>
 
@@ -50,6 +51,21 @@ void rtec_struct_sizes(int64_t* out6) {
 }
 
 const char* rtec_last_error(void) { return last_error_cstr(); }
+
+// kernel nodes of a captured CUDA graph (the per-batch launch census of a captured step)
+int64_t rtec_graph_kernel_nodes(void* graph) {
+  cudaGraph_t gr = static_cast<cudaGraph_t>(graph);
+  size_t n = 0;
+  if (cudaGraphGetNodes(gr, nullptr, &n) != cudaSuccess) return -1;
+  std::vector<cudaGraphNode_t> nodes(n);
+  if (n && cudaGraphGetNodes(gr, nodes.data(), &n) != cudaSuccess) return -1;
+  int64_t k = 0;
+  for (size_t i = 0; i < n; ++i) {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(nodes[i], &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++k;
+  }
+  return k;
+}
 
 void rtec_prof_enable(int on) { g_prof_on = on != 0; }
 

@@ -46,12 +46,14 @@ struct WordPop {
   __device__ __forceinline__ uint32_t word(int64_t i) const { return a[i] & (b ? ~b[i] : 0xffffffffu); }
   __device__ __forceinline__ int64_t operator()(int64_t i) const { return __popc(word(i)); }
 };
-struct WordList {
-  WordPop f;
-  int32_t* list;
-  int32_t* slot;  // may be null
-  __device__ __forceinline__ void operator()(int64_t i, int64_t off, int64_t) const {
+
+// bitmap -> ascending list: per-word offsets from a popcount scan, then one
+// thread per word writes its bits (many CTAs; the scan's out-functor stays cheap)
+__global__ void __launch_bounds__(kFBlk) k_word_list(WordPop f, const int64_t* __restrict__ woff, int64_t words,
+                                                     int32_t* list, int32_t* slot) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < words; i += (int64_t)gridDim.x * blockDim.x) {
     uint32_t w = f.word(i);
+    int64_t off = woff[i];
     while (w) {
       int bit = __ffs(w) - 1;
       w &= w - 1;
@@ -61,7 +63,15 @@ struct WordList {
       ++off;
     }
   }
-};
+}
+
+static int bitmap_to_list(WordPop f, int64_t words, int32_t* list, int32_t* slot, int64_t* count, int64_t* woff,
+                          Ws& w, cudaStream_t s) {
+  RTEC_TRY(exclusive_scan(f, Count{nullptr, words}, words, StorePrefix{woff}, count, w, s));
+  k_word_list<<<grid_for(words, kFBlk), kFBlk, 0, s>>>(f, woff, words, list, slot);
+  RTEC_LAUNCH_CHECK("k_word_list");
+  return RTEC_OK;
+}
 
 struct OutLenOf {
   const int32_t* list;
@@ -172,7 +182,7 @@ __global__ void k_counters(const int32_t* __restrict__ slist, const int64_t* n_s
 
 size_t frontier_ws_bytes(int64_t n) {
   int64_t words = (n + 31) / 32;
-  return sizeof(int32_t) * (n + 1) + sizeof(int64_t) * (n + 2) + 256 * 4 +
+  return sizeof(int32_t) * (n + 1) + sizeof(int64_t) * (n + 2) + sizeof(int64_t) * (words + 1) + 256 * 5 +
          sizeof(int64_t) * (scan_blocks_for(n > words ? n : words) + 2) * 4 + 8192;
 }
 
@@ -195,6 +205,7 @@ extern "C" int rtec_frontier_layer(const rtec_graph_t* g, const rtec_batch_t* b,
   int32_t* nlist = w.alloc<int32_t>(n + 1);
   int64_t* noff = w.alloc<int64_t>(n + 2);
   int64_t* n_new = w.alloc<int64_t>(4);
+  int64_t* woff = w.alloc<int64_t>(words + 1);
   RTEC_WS_CHECK(w);
   RTEC_CUDA(cudaMemsetAsync(f->counters, 0, sizeof(int64_t) * 8, s));
   RTEC_CUDA(cudaMemsetAsync(n_new, 0, sizeof(int64_t) * 4, s));
@@ -217,7 +228,7 @@ extern "C" int rtec_frontier_layer(const rtec_graph_t* g, const rtec_batch_t* b,
   }
   // new sources N = S(l) \ S(l-1)
   WordPop np{f->bm_src, prev_src};
-  RTEC_TRY(exclusive_scan(np, Count{nullptr, words}, words, WordList{np, nlist, nullptr}, n_new, w, s));
+  RTEC_TRY(bitmap_to_list(np, words, nlist, nullptr, n_new, woff, w, s));
   RTEC_TRY(exclusive_scan(OutLenOf{nlist, g->out.len}, Count{n_new, n}, n, StoreOffTailF{noff, n_new}, nullptr, w, s));
   {
     RTEC_PROF("k_expand", s);
@@ -227,9 +238,9 @@ extern "C" int rtec_frontier_layer(const rtec_graph_t* g, const rtec_batch_t* b,
   RTEC_LAUNCH_CHECK("k_expand");
   // lists + slots
   WordPop sp{f->bm_src, nullptr};
-  RTEC_TRY(exclusive_scan(sp, Count{nullptr, words}, words, WordList{sp, f->src_list, f->src_slot}, f->n_src, w, s));
+  RTEC_TRY(bitmap_to_list(sp, words, f->src_list, f->src_slot, f->n_src, woff, w, s));
   WordPop dp{f->bm_dst, nullptr};
-  RTEC_TRY(exclusive_scan(dp, Count{nullptr, words}, words, WordList{dp, f->dst_list, f->dst_slot}, f->n_dst, w, s));
+  RTEC_TRY(bitmap_to_list(dp, words, f->dst_list, f->dst_slot, f->n_dst, woff, w, s));
   k_counters<<<kSMs * 2, kFBlk, 0, s>>>(f->src_list, f->n_src, f->n_dst, g->out.len, g->in.len, f->dst_list, *b,
                                         f->bm_src, f->counters);
   RTEC_LAUNCH_CHECK("k_counters");

@@ -95,12 +95,40 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_down(F f, Count cnt, const 
 
 inline int64_t scan_blocks_for(int64_t max_n) { return (max_n + kScanTile - 1) / kScanTile; }
 
+// whole scan in one CTA when the (host-side) bound fits one tile: one launch instead of three
+template <typename F, typename O>
+__global__ void __launch_bounds__(kScanBlock) k_scan_one(F f, Count cnt, O out, int64_t* total) {
+  __shared__ int64_t sw[kScanBlock / 32];
+  int64_t n = cnt.get();
+  int64_t vals[kScanItems];
+  int64_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    int64_t i = static_cast<int64_t>(threadIdx.x) * kScanItems + k;
+    vals[k] = (i < n) ? f(i) : 0;
+    s += vals[k];
+  }
+  int64_t tot;
+  int64_t off = block_exclusive_scan<int64_t>(s, sw, &tot);
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    int64_t i = static_cast<int64_t>(threadIdx.x) * kScanItems + k;
+    if (i < n) out(i, off, vals[k]);
+    off += vals[k];
+  }
+  if (threadIdx.x == 0 && total) *total = tot;
+}
+
 // Exclusive scan: out(i, prefix, value) is called for every i < count; *total
 // (device, may be null) receives the sum.  ws needs scan_blocks_for(max)+1 int64.
 template <typename F, typename O>
 int exclusive_scan_bs(F f, Count cnt, int64_t max_n, O out, int64_t* total, int64_t* bs, cudaStream_t s) {
   int64_t nb = scan_blocks_for(max_n);
-  if (nb < 1) nb = 1;
+  if (nb <= 1) {
+    k_scan_one<F, O><<<1, kScanBlock, 0, s>>>(f, cnt, out, total);
+    RTEC_LAUNCH_CHECK("exclusive_scan");
+    return RTEC_OK;
+  }
   k_scan_reduce<F><<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(f, cnt, bs);
   k_scan_blocks<<<1, kScanBlock, 0, s>>>(bs, nb, total);
   k_scan_down<F, O><<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(f, cnt, bs, out);

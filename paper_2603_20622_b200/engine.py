@@ -76,11 +76,15 @@ class RTECEngine:
     """B200 incremental engine over a DynamicGraph and an operator Bundle."""
 
     def __init__(self, bundle: Bundle, graph: DynamicGraph, features, *, max_batch: int | None = None,
-                 update: str = "tc"):
+                 update: str = "tc", use_graphs: bool = True):
         if not isinstance(bundle, Bundle) or bundle.model not in MODELS:
             raise E.UnsupportedModel("engine needs a bundle from paper_2603_20622_b200.models")
         self.b = bundle
         self.g = graph
+        self.use_graphs = bool(use_graphs)
+        self._graphs: dict = {}
+        self._seen: dict = {}
+        self.graph_kernels: dict = {}  # batch size -> kernel nodes of the captured step
         self.lib = graph.lib
         self.dev = graph.dev
         n = graph.n
@@ -178,10 +182,45 @@ class RTECEngine:
     run_full = bootstrap
 
     # ---------------------------------------------------------------- incremental step
-    def enqueue_step(self, B: int) -> None:
-        """Enqueue the whole incremental pipeline for the staged batch (no sync)."""
+    def _graph_key(self, B: int):
+        """Everything a captured step bakes in: the batch size and every buffer address."""
         gr = self.g
-        self._ensure_ws(gr.batch.cap)
+        return (B, gr.ws.data_ptr(), gr.ws.numel(), gr.out.nbr.data_ptr(), gr.inn.nbr.data_ptr(),
+                gr.batch.err.data_ptr(), gr.batch.cap)
+
+    def enqueue_step(self, B: int) -> None:
+        """Enqueue the whole incremental pipeline for the staged batch (no sync).
+
+        With `use_graphs`, the pipeline (~100-200 launches) is captured into a CUDA
+        graph on the second batch of a given size and replayed afterwards; any
+        reallocation (workspace growth, compaction, larger batch buffers) changes
+        the key and triggers a fresh capture."""
+        self._ensure_ws(self.g.batch.cap)
+        if not self.use_graphs:
+            self._enqueue_eager(B)
+            return
+        key = self._graph_key(B)
+        cg = self._graphs.get(key)
+        if cg is None:
+            if self._seen.get(key, 0) < 1:  # first batch of this shape runs eagerly (lazy init, warm-up)
+                self._seen[key] = self._seen.get(key, 0) + 1
+                self._enqueue_eager(B)
+                return
+            prof = _lib.prof_enabled()
+            self.lib.rtec_prof_enable(0)
+            cg = torch.cuda.CUDAGraph(keep_graph=True)
+            with torch.cuda.graph(cg):
+                self._enqueue_eager(B)
+            cg.instantiate()
+            self.lib.rtec_prof_enable(1 if prof else 0)
+            self.graph_kernels[B] = int(self.lib.rtec_graph_kernel_nodes(cg.raw_cuda_graph()))
+            if len(self._graphs) >= 4:
+                self._graphs.pop(next(iter(self._graphs)))
+            self._graphs[key] = cg
+        cg.replay()
+
+    def _enqueue_eager(self, B: int) -> None:
+        gr = self.g
         gr.apply_staged(B)
         g, b = gr._gc, gr._bc
         st = _lib.stream_handle()

@@ -13,7 +13,7 @@ HEADER = os.path.join(ROOT, "include", "rtec.h")
 
 def declared_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|void|const char\*)\s+(rtec_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|size_t|void|const char\*)\s+(rtec_\w+)\s*\(", text, re.M)))
 
 
 @pytest.fixture(scope="module")

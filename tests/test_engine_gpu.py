@@ -198,3 +198,27 @@ def test_query_and_errors(P):
         eng.step(np.array([0], np.uint8), np.array([0]), np.array([n]), np.array([0]))
     with pytest.raises(P.UnsupportedModel):
         P.make_bundle("monet", [4, 4])
+
+
+def test_cuda_graph_replay_matches_eager(P):
+    # the captured per-batch pipeline (replayed from the second batch of a size on)
+    # is bit-identical to eager launches, across a compaction-triggered recapture
+    from paper_2603_20622_b200.workload import UpdateStream, chung_lu_edges, features
+
+    n = 3000
+    s, d = chung_lu_edges(n, 30000, seed=18)
+    X = features(n, 32, seed=4)
+    outs = []
+    for graphs in (False, True):
+        stream = UpdateStream(s, d, holdout=0.2, seed=18)
+        bs, bd, bt = stream.base()
+        g = P.DynamicGraph.from_edges(n, (bs, bd, bt), reserve=256)  # small arena: compaction mid-stream
+        eng = P.RTECEngine(P.make_bundle("gcn", [32, 32, 32]), g, X, use_graphs=graphs)
+        for _ in range(6):
+            eng.step(*stream.next_batch(500))
+        outs.append((eng.embeddings(2), eng.g.edges()))
+        if graphs:
+            assert eng.graph_kernels.get(500, 0) > 20  # kernel nodes of the captured step
+    assert np.array_equal(outs[0][0], outs[1][0])
+    for a, b in zip(outs[0][1], outs[1][1]):
+        assert np.array_equal(a, b)
