@@ -222,8 +222,14 @@ struct HeavyPlan {
   float* part;      // [chunks, d] partial rows
 };
 
+// resident CTAs per SM: wide rows need the registers (no spills)
+template <int VEC, int K>
+struct AggOcc {
+  static constexpr int value = (VEC * K <= 8) ? 4 : 2;
+};
+
 template <int VEC, int K, bool FULL>
-__global__ void __launch_bounds__(kLBlk, 4) k_agg_light(LayerArgs a, AggRows rows) {
+__global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_light(LayerArgs a, AggRows rows) {
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
   const int64_t nr = rows.count();
@@ -251,7 +257,7 @@ __global__ void __launch_bounds__(kLBlk, 4) k_agg_light(LayerArgs a, AggRows row
 }
 
 template <int VEC, int K, bool FULL>
-__global__ void __launch_bounds__(kLBlk, 4) k_agg_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
+__global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
   const int64_t nh = *hp.n_heavy;

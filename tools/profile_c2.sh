@@ -1,6 +1,8 @@
-# ncu evidence for the c2-gcn bench step (run under gpurun from the repo root)
+# ncu evidence for the c2-gcn bench step (run under gpurun from the repo root; eager launches)
 set -x
-ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches_c2gcn.csv python bench.py --profile --steps 1 --warmup 1 --e2e-steps 0 > gpurun_out/p_list.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_gemm_tc -s 4 -c 2 -o gpurun_out/r01b_gemm python bench.py --profile --steps 1 --warmup 1 --e2e-steps 0 > gpurun_out/p_gemm.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_agg -s 8 -c 4 -o gpurun_out/r01b_agg python bench.py --profile --steps 1 --warmup 1 --e2e-steps 0 > gpurun_out/p_agg.log 2>&1
+B="python bench.py --profile --no-graphs --steps 1 --warmup 1 --e2e-steps 0"
+ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches_c2gcn.csv $B > gpurun_out/p_list.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_gemm_tc -s 4 -c 2 -o gpurun_out/r01c_gemm $B > gpurun_out/p_gemm.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_agg -s 8 -c 4 -o gpurun_out/r01c_agg $B > gpurun_out/p_agg.log 2>&1
+ncu --set full --clock-control none -k regex:k_src_delta -s 2 -c 2 -o gpurun_out/r01c_delta $B > gpurun_out/p_delta.log 2>&1
 ls -la gpurun_out
