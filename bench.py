@@ -375,6 +375,12 @@ def run_ours(args, world, rank, local):
         tr = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tr):
             roof["traffic"] = json.load(open(tr)).get(args.workload, {}).get(dom)
+        if roof["traffic"]:
+            # the same launch against its measured DRAM traffic (ncu): how close the kernel runs to
+            # the HBM roof for the bytes it actually moves (re-gathers included)
+            dram = roof["traffic"] / (kernels[dom]["ms_per_launch"] * 1e6)
+            roof["dram_achieved"] = round(dram, 1)
+            roof["dram_frac"] = round(dram / hbm_peak, 4)
         if dom in ("k_gemm_update", "k_gemm_tc"):
             fl = sum(gemm_flops(wl, C[k, l]) for k in range(PROF) for l in range(L)) / max(kernels[dom]["launches"], 1)
             roof["tflops"] = round(fl / (kernels[dom]["ms_per_launch"] * 1e9), 2)
