@@ -52,7 +52,9 @@ def _rank_main(rank, world, port, cfg, out_dir):
     import torch.distributed as dist
 
     torch.cuda.set_device(0)
-    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    backend = cfg.get("backend", "gloo")
+    kw = {"device_id": torch.device("cuda", 0)} if backend == "nccl" else {}
+    dist.init_process_group(backend, init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world, **kw)
     import paper_2603_20622_b200 as P
     from paper_2603_20622_b200.shard import Comm, ShardedRTECEngine
 
@@ -127,3 +129,9 @@ def test_sharded_three_layers_arena_replay():
 
 def test_sharded_gat_heads_three_ranks():
     _run(dict(model="gat", dims=[24, 64, 64], n=2500, m=30000, B=250, nb=2, seed=23, heads=4), world=3)
+
+
+def test_sharded_nccl_single_rank():
+    # one rank over NCCL: the device-tensor collective path the multi-GPU bench runs
+    # (all_gather_into_tensor of ids / rows, uint8 MAX and int32 SUM all-reduces)
+    _run(dict(model="gcn", dims=[32, 48, 32], n=3000, m=40000, B=300, nb=3, seed=24, backend="nccl"), world=1)
