@@ -329,7 +329,8 @@ def run_ours(args, world, rank, local):
         e2e_ms.append(a_ev.elapsed_time(b_ev))
         e2e_upd += int(r.status.sum())
         h2d += sum(x.numel() * x.element_size() for x in hb)
-        d2h += r.status.nbytes + r.deltas.shape[0] * 5 * 4 + 8 + 8 + 8
+        # RTECEngine._readback: status (B), 5 DegreeDelta columns (2B int32 each), err, n_delta, counters
+        d2h += len(r.status) + 5 * 4 * 2 * len(r.status) + 8 + 8 + 64 * L
     e2e_val = None
     if E2E:
         e2e_s = max_over_ranks(sum(e2e_ms) / 1e3, world)

@@ -103,24 +103,30 @@ __host__ __device__ __forceinline__ int64_t sw128_off(int r, int c) {
 
 
 
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 // Warp-specialised persistent kernel (512 threads), separate operand rings:
-//   warp 0      producer: bulk-copies each A K-block (16 KB) into the A ring and each
-//               (K-block, N-half) of Bhi/Blo into the B ring
+//   warp 0      A producer: bulk-copies each A K-block (16 KB) into the A ring
+//   warp 2      B producer: each (K-block, N-half) of Bhi/Blo into the B ring
 //   warp 1      MMA issuer: per (K-block, N-half) 12 tcgen05.mma into one of two TMEM
 //               accumulators (columns [half0, npad) of buffer t&1)
-//   warps 2-7   splitters: A -> (hi, lo) in shared memory, fence.proxy.async, arrive
+//   warps 3-7   splitters: A -> (hi, lo) in shared memory, fence.proxy.async, arrive
 //   warps 8-15  epilogue: tcgen05.ld -> act -> global rows (+ DeltaLog), overlapping the
 //               next tile's main loop thanks to the double-buffered accumulator
 // Splitting B by N-halves keeps the B stage at 32 KB for N = 256, so the rings
 // are 3 A stages + 4 B stages deep instead of 2 monolithic 96 KB stages.
-// mbarriers: a_full (tx), a_split (192 arrivals), a_empty (tcgen05.commit),
+// mbarriers: a_full (tx), a_split (160 arrivals), a_empty (tcgen05.commit),
 //            b_full (tx), b_empty (commit), tfull[2] (commit), tempty[2] (256 arrivals)
 constexpr int kMaxA = 6, kMaxB = 8;
-constexpr int kSplitThreads = 192;
+constexpr int kSplitThreads = 160;
 constexpr int kEpiBytes = 8 * 32 * 32 * 4;              // 8 epilogue warps x 32 rows x 32 cols
 
 struct TcShape {
@@ -195,8 +201,7 @@ __global__ void __launch_bounds__(512, 1) k_gemm_tc(TcArgs g, TcShape sh) {
   const int64_t J = my_tiles * g.nkb;  // A stages consumed by this CTA
 
   if (warp == 0) {
-    if (lane == 0) {
-      int64_t jb = 0;
+    if (lane == 0) {  // A producer: one 16 KB K-block of the tile image per stage
       for (int64_t j = 0; j < J; ++j) {
         const int sa = static_cast<int>(j % sh.SA);
         if (j >= sh.SA) mbar_wait(a_empty + sa, static_cast<uint32_t>(((j / sh.SA) - 1) & 1));
@@ -205,62 +210,73 @@ __global__ void __launch_bounds__(512, 1) k_gemm_tc(TcArgs g, TcShape sh) {
         mbar_expect_tx(a_full + sa, kABlockBytes);
         bulk_g2s(aring + sa * 2 * kABlockBytes, g.A + (tile * g.nkb + kb) * (kABlockBytes / 4), kABlockBytes,
                  a_full + sa);
-        for (int h = 0; h < sh.nh; ++h, ++jb) {
-          const int sb = static_cast<int>(jb % sh.SB);
-          if (jb >= sh.SB) mbar_wait(b_empty + sb, static_cast<uint32_t>(((jb / sh.SB) - 1) & 1));
-          const int n0 = h == 0 ? 0 : sh.h0;
-          const int nw = h == 0 ? sh.h0 : g.npad - sh.h0;
-          const uint32_t hb = static_cast<uint32_t>(nw) * kTK * 4;
-          uint8_t* st = bring + sb * sh.bstage;
-          const int64_t off = (static_cast<int64_t>(kb) * g.npad + n0) * kTK;
-          mbar_expect_tx(b_full + sb, 2 * hb);
-          bulk_g2s(st, g.Bhi + off, hb, b_full + sb);
-          bulk_g2s(st + sh.bstage / 2, g.Blo + off, hb, b_full + sb);
-        }
+      }
+    }
+  } else if (warp == 2) {
+    if (lane == 0) {  // B producer (its own lane, so a full B ring never stalls the A loads)
+      const int64_t JB = J * sh.nh;
+      for (int64_t jb = 0; jb < JB; ++jb) {
+        const int kb = static_cast<int>((jb / sh.nh) % g.nkb);
+        const int h = static_cast<int>(jb % sh.nh);
+        const int sb = static_cast<int>(jb % sh.SB);
+        if (jb >= sh.SB) mbar_wait(b_empty + sb, static_cast<uint32_t>(((jb / sh.SB) - 1) & 1));
+        const int n0 = h == 0 ? 0 : sh.h0;
+        const int nw = h == 0 ? sh.h0 : g.npad - sh.h0;
+        const uint32_t hb = static_cast<uint32_t>(nw) * kTK * 4;
+        uint8_t* st = bring + sb * sh.bstage;
+        const int64_t off = (static_cast<int64_t>(kb) * g.npad + n0) * kTK;
+        mbar_expect_tx(b_full + sb, 2 * hb);
+        bulk_g2s(st, g.Bhi + off, hb, b_full + sb);
+        bulk_g2s(st + sh.bstage / 2, g.Blo + off, hb, b_full + sb);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      int64_t j = 0, jb = 0;
-      for (int64_t t = 0; t < my_tiles; ++t) {
-        const int b = static_cast<int>(t & 1);
-        const int64_t ub = t >> 1;
-        if (ub > 0) mbar_wait(tempty + b, static_cast<uint32_t>((ub - 1) & 1));
+    // MMA warp: all lanes walk the (uniform) schedule so descriptors live in uniform
+    // registers; one elected lane issues each tcgen05.mma / commit
+    int64_t j = 0, jb = 0;
+    for (int64_t t = 0; t < my_tiles; ++t) {
+      const int b = static_cast<int>(t & 1);
+      const int64_t ub = t >> 1;
+      if (ub > 0) mbar_wait(tempty + b, static_cast<uint32_t>((ub - 1) & 1));
+      tc_fence_after();
+      for (int kb = 0; kb < g.nkb; ++kb, ++j) {
+        const int sa = static_cast<int>(j % sh.SA);
+        mbar_wait(a_split + sa, static_cast<uint32_t>((j / sh.SA) & 1));
         tc_fence_after();
-        for (int kb = 0; kb < g.nkb; ++kb, ++j) {
-          const int sa = static_cast<int>(j % sh.SA);
-          mbar_wait(a_split + sa, static_cast<uint32_t>((j / sh.SA) & 1));
+        const uint64_t dalo = sw128_desc(smem_u32(aring + sa * 2 * kABlockBytes));
+        const uint64_t dahi = dalo + (kABlockBytes >> 4);
+        for (int h = 0; h < sh.nh; ++h, ++jb) {
+          const int sb = static_cast<int>(jb % sh.SB);
+          mbar_wait(b_full + sb, static_cast<uint32_t>((jb / sh.SB) & 1));
           tc_fence_after();
-          const uint32_t a_lo = smem_u32(aring + sa * 2 * kABlockBytes);
-          const uint32_t a_hi = a_lo + kABlockBytes;
-          for (int h = 0; h < sh.nh; ++h, ++jb) {
-            const int sb = static_cast<int>(jb % sh.SB);
-            mbar_wait(b_full + sb, static_cast<uint32_t>((jb / sh.SB) & 1));
-            tc_fence_after();
-            const int n0 = h == 0 ? 0 : sh.h0;
-            const int nw = h == 0 ? sh.h0 : g.npad - sh.h0;
-            const uint32_t b_hi = smem_u32(bring + sb * sh.bstage);
-            const uint32_t b_lo = b_hi + sh.bstage / 2;
-            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(nw >> 3) << 17) |
-                                   (static_cast<uint32_t>(kTM >> 4) << 24);
-            const uint32_t acc_addr = taddr + static_cast<uint32_t>(b * g.npad + n0);
+          const int n0 = h == 0 ? 0 : sh.h0;
+          const int nw = h == 0 ? sh.h0 : g.npad - sh.h0;
+          const uint64_t dbhi = sw128_desc(smem_u32(bring + sb * sh.bstage));
+          const uint64_t dblo = dbhi + ((sh.bstage / 2) >> 4);
+          const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(nw >> 3) << 17) |
+                                 (static_cast<uint32_t>(kTM >> 4) << 24);
+          const uint32_t acc_addr = taddr + static_cast<uint32_t>(b * g.npad + n0);
+          if (elect_one()) {
 #pragma unroll
             for (int k = 0; k < kTK / 8; ++k) {
-              const uint32_t off = k * 32;
+              const uint64_t off = static_cast<uint64_t>(k * 32) >> 4;  // +32 B along K per k-step
               const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
-              mma_tf32(acc_addr, sw128_desc(a_hi + off), sw128_desc(b_hi + off), idesc, acc);
-              mma_tf32(acc_addr, sw128_desc(a_hi + off), sw128_desc(b_lo + off), idesc, 1u);
-              mma_tf32(acc_addr, sw128_desc(a_lo + off), sw128_desc(b_hi + off), idesc, 1u);
+              mma_tf32(acc_addr, dahi + off, dbhi + off, idesc, acc);
+              mma_tf32(acc_addr, dahi + off, dblo + off, idesc, 1u);
+              mma_tf32(acc_addr, dalo + off, dbhi + off, idesc, 1u);
             }
             mma_commit(b_empty + sb);  // B stage reusable once these MMAs retire
           }
-          mma_commit(a_empty + sa);
+          __syncwarp();
         }
-        mma_commit(tfull + b);  // accumulator b complete
+        if (elect_one()) mma_commit(a_empty + sa);
+        __syncwarp();
       }
+      if (elect_one()) mma_commit(tfull + b);  // accumulator b complete
+      __syncwarp();
     }
   } else if (warp < 8) {
-    const int st_id = tid - 64;  // 0..191
+    const int st_id = tid - 96;  // warps 3-7: 0..159
     for (int64_t j = 0; j < J; ++j) {
       const int sa = static_cast<int>(j % sh.SA);
       mbar_wait(a_full + sa, static_cast<uint32_t>((j / sh.SA) & 1));

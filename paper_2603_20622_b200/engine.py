@@ -85,6 +85,7 @@ class RTECEngine:
         self._graphs: dict = {}
         self._seen: dict = {}
         self.graph_kernels: dict = {}  # batch size -> kernel nodes of the captured step
+        self._host = None  # pinned result buffers of step()
         self.lib = graph.lib
         self.dev = graph.dev
         n = graph.n
@@ -244,12 +245,45 @@ class RTECEngine:
                                                        st), "layer")
         _lib.check(self.lib.rtec_batch_commit(C.byref(g), C.byref(b), st), "commit")
 
+    def _readback(self, B: int):
+        """Queue the batch's results into pinned host buffers (one sync for all of them)."""
+        b = self.g.batch
+        cap = b.cap
+        hb = self._host
+        if hb is None or hb["cap"] < cap:
+            pin = lambda t, k: torch.empty(k, dtype=t, pin_memory=True)  # noqa: E731
+            hb = self._host = {"cap": cap, "err": pin(torch.int64, 1), "nd": pin(torch.int64, 1),
+                               "status": pin(torch.uint8, cap), "d": [pin(torch.int32, 2 * cap) for _ in range(5)],
+                               "ctr": pin(torch.int64, 8 * self.L)}
+        hb["err"].copy_(b.err, non_blocking=True)
+        hb["nd"].copy_(b.n_delta, non_blocking=True)
+        if B:
+            hb["status"][:B].copy_(b.status[:B], non_blocking=True)
+            for h, t in zip(hb["d"], b.d):  # DegreeDelta rows: at most 2B
+                h[: 2 * B].copy_(t[: 2 * B], non_blocking=True)
+        for l, f in enumerate(self.fr):
+            hb["ctr"][8 * l: 8 * l + 8].copy_(f.counters, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return hb
+
+    def _metrics_from(self, ctr) -> Metrics:
+        m = Metrics()
+        c = ctr.numpy().reshape(self.L, 8)
+        for l in range(self.L):
+            m.e_curr.append(int(c[l, 0]))
+            m.v_dst.append(int(c[l, 1]))
+            m.n_src.append(int(c[l, 2]))
+            m.in_edges_vdst.append(int(c[l, 5]))
+        return m
+
     def step(self, op, src, dst, ts) -> RunResult:
-        """run_incremental on array inputs; syncs once at the end to read the result."""
+        """run_incremental on array inputs; one host synchronisation at the end reads
+        the per-update status, DegreeDelta rows and counters from pinned buffers."""
         B = self.g.stage(op, src, dst, ts)
         for attempt in range(4):
             self.enqueue_step(B)
-            word = self.g.batch_error()
+            hb = self._readback(B)
+            word = int(hb["err"][0]) & _lib.ERR_OK
             d = _lib.decode_err(word)
             if d is not None and d[0] == _lib.ARENA_FULL:
                 # nothing was mutated (validation-before-mutation); make room and replay
@@ -261,8 +295,11 @@ class RTECEngine:
             break
         else:
             raise E.NativeError("run_incremental: arena still full after compaction")
-        status, deltas = self.g.read_result(B)
-        return RunResult(status, deltas, None, self.metrics())
+        status = hb["status"][:B].numpy().copy()
+        k = int(hb["nd"][0])
+        # DegreeDelta rows (vertex, old_in, new_in, old_out, new_out) as int32 [k, 5]
+        deltas = np.stack([h[:k].numpy() for h in hb["d"]], axis=1) if k else np.zeros((0, 5), np.int32)
+        return RunResult(status, deltas, None, self._metrics_from(hb["ctr"]))
 
     def run_incremental(self, batch) -> RunResult:
         """SPEC run_incremental on a coalesced EdgeUpdate list."""
