@@ -170,6 +170,18 @@ typedef struct {
   float* Z_log; float* er_log;              /* GAT DeltaLog of Z/er rows of V_chg(l-1) */
   float* gemm_in;      /* [n_dst cap, max(d_agg,d_in)] scratch: composed rows fed to the update GEMM */
   float* gemm_mid;     /* [n_dst cap, d_out] GIN hidden */
+  /* Source deltas of the sum aggregators (GCN / SAGE / GIN), vertex-indexed:
+   *   delta       [n, d_in]  δ_u = c_new(u) h_new(u) - c_old(u) h_old(u) of this layer's
+   *               sources S(l) (NULL: computed into the workspace);
+   *   delta_ready  rows of V_chg(l-1) were written by the previous layer's update, so only
+   *               the other sources (Dg) are computed here, and a deleted edge of a changed
+   *               source contributes -c_old h_old = δ - c_new h_new (no DeltaLog needed);
+   *   delta_next  [n, d_out] set (tcgen05 update, d_out % 4 == 0): this layer's update
+   *               writes δ_v of every updated row for the next layer instead of log_out. */
+  float* delta;
+  float* delta_next;
+  int32_t delta_ready;
+  int32_t pad_;
 } rtec_state_t;
 
 /* ---- workspace ---- */

@@ -103,6 +103,13 @@ __host__ __device__ __forceinline__ int64_t sw128_off(int r, int c) {
 
 
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
@@ -134,15 +141,19 @@ struct TcShape {
   int nh;           // N halves (1 or 2)
   int h0;           // width of half 0 (multiple of 16); half 1 = npad - h0
   uint32_t bstage;  // bytes of one B stage (hi + lo of the wider half)
+  uint32_t oldb;    // fused deltas: per-warp double-buffered old-row staging (bytes, all warps)
 };
 
-static TcShape tc_shape(int npad) {
+constexpr int kOldBytes = 8 * 2 * 32 * 32 * 4;  // 8 epilogue warps x 2 buffers x 32 rows x 32 cols
+
+static TcShape tc_shape(int npad, bool fused) {
   TcShape sh;
   sh.nh = npad > 128 ? 2 : 1;
   sh.h0 = sh.nh == 2 ? ((npad / 2 + 15) / 16) * 16 : npad;
   sh.bstage = 2u * static_cast<uint32_t>(sh.h0) * kTK * 4;
-  const int budget = 227 * 1024 - 1024 - 512 - kEpiBytes;
-  sh.SA = 3;  // measured: 2..4 A stages perform alike; the B ring gets the rest
+  sh.oldb = fused ? kOldBytes : 0;
+  const int budget = 227 * 1024 - 1024 - 512 - kEpiBytes - static_cast<int>(sh.oldb);
+  sh.SA = fused ? 2 : 3;  // measured: 2..4 A stages perform alike; the B ring gets the rest
   sh.SB = (budget - sh.SA * 2 * kABlockBytes) / static_cast<int>(sh.bstage);
   if (sh.SB > kMaxB) sh.SB = kMaxB;
   return sh;
@@ -160,7 +171,8 @@ __global__ void __launch_bounds__(512, 1) k_gemm_tc(TcArgs g, TcShape sh) {
   uint8_t* aring = base;                                      // SA x (lo 16 KB | hi 16 KB)
   uint8_t* bring = base + sh.SA * 2 * kABlockBytes;           // SB x (hi | lo)
   float* epi = reinterpret_cast<float*>(bring + sh.SB * sh.bstage);   // epilogue transpose staging
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(epi) + kEpiBytes);
+  float* olds = epi + kEpiBytes / 4;                                    // fused deltas: old rows
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(olds) + sh.oldb);
   uint64_t* a_full = bars;
   uint64_t* a_split = a_full + kMaxA;
   uint64_t* a_empty = a_split + kMaxA;
@@ -335,10 +347,43 @@ __global__ void __launch_bounds__(512, 1) k_gemm_tc(TcArgs g, TcShape sh) {
             }
         }
       }
+      // fused deltas: pre-batch rows of this warp's 32 rows, one 32-column chunk at a
+      // time, copied asynchronously into shared memory one chunk ahead
+      const bool fused = g.delta_next != nullptr && !g.Yt;
+      float c_new = 1.f, c_old = 1.f;
+      float* oldw = olds + (warp - 8) * 2 * 32 * 32;
+      const int sub = lane >> 3, ch = lane & 7;  // 4 rows per instruction, 8 lanes x 16 B per row
+      auto prefetch_old = [&](int cc) {
+        float* ob = oldw + ((cc - cbeg) & 1) * 32 * 32;
+        const int col = cc * 32 + ch * 4;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int q = 4 * u + sub;
+          const int64_t dq = __shfl_sync(0xffffffffu, dst, q);
+          if (dq >= 0 && col + 4 <= g.d_out) cp_async16(ob + q * 32 + ch * 4, g.Y + dq * g.ldy + col);
+        }
+        cp_async_commit();
+      };
+      if (fused) {
+        if (dst >= 0) {
+          const int32_t dn = g.deg_new[dst], dp = g.deg_old[dst];
+          c_new = dn > 0 ? (g.coeff_gcn ? 1.0f / sqrtf(static_cast<float>(dn) + g.deg_off) : 1.f) : 0.f;
+          c_old = dp > 0 ? (g.coeff_gcn ? 1.0f / sqrtf(static_cast<float>(dp) + g.deg_off) : 1.f) : 0.f;
+        }
+        if (cbeg < cend) prefetch_old(cbeg);  // independent of the MMA: overlaps the wait below
+      }
       mbar_wait(tfull + b, static_cast<uint32_t>((t >> 1) & 1));
       tc_fence_after();
       for (int cc = cbeg; cc < cend; ++cc) {
         const int c0 = cc * 32;
+        if (fused) {
+          if (cc + 1 < cend) {
+            prefetch_old(cc + 1);
+            cp_async_wait<1>();
+          } else {
+            cp_async_wait<0>();
+          }
+        }
         uint32_t rr[32];
         RTEC_TMEM_LD32(taddr + lane_base + static_cast<uint32_t>(b * g.npad + c0), rr);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -365,8 +410,26 @@ __global__ void __launch_bounds__(512, 1) k_gemm_tc(TcArgs g, TcShape sh) {
           *reinterpret_cast<float4*>(stg + lane * 32 + ((c ^ (lane & 7)) << 2)) =
               make_float4(y[4 * c], y[4 * c + 1], y[4 * c + 2], y[4 * c + 3]);
         __syncwarp();
-        const int sub = lane >> 3, ch = lane & 7;  // 4 rows per instruction, 8 lanes per row
         const int col = c0 + ch * 4;
+        if (fused) {
+          const float* ob = oldw + ((cc - cbeg) & 1) * 32 * 32;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int q = 4 * u + sub;
+            const int64_t dq = __shfl_sync(0xffffffffu, dst, q);
+            const float cn = __shfl_sync(0xffffffffu, c_new, q);
+            const float co = __shfl_sync(0xffffffffu, c_old, q);
+            const float4 v4 = *reinterpret_cast<const float4*>(stg + q * 32 + ((ch ^ (q & 7)) << 2));
+            if (dq < 0 || col + 4 > g.d_out) continue;
+            const float4 o4 = *reinterpret_cast<const float4*>(ob + q * 32 + ch * 4);
+            *reinterpret_cast<float4*>(g.Y + dq * g.ldy + col) = v4;
+            __stcg(reinterpret_cast<float4*>(g.delta_next + dq * g.d_out + col),
+                   make_float4(cn * v4.x - co * o4.x, cn * v4.y - co * o4.y, cn * v4.z - co * o4.z,
+                               cn * v4.w - co * o4.w));
+          }
+          __syncwarp();
+          continue;
+        }
         const bool full4 = (g.d_out & 3) == 0 && (g.ldy & 3) == 0;
 #pragma unroll
         for (int q0 = 0; q0 < 32; q0 += 4) {
@@ -412,15 +475,16 @@ __global__ void k_prep_b(const float* __restrict__ W, int d_in, int d_out, int n
   }
 }
 
-size_t gemm_tc_smem(int npad) {
-  TcShape sh = tc_shape(npad);
-  return static_cast<size_t>(sh.SA) * 2 * kABlockBytes + static_cast<size_t>(sh.SB) * sh.bstage + kEpiBytes + 1024 +
-         512;
+size_t gemm_tc_smem(int npad, bool fused) {
+  TcShape sh = tc_shape(npad, fused);
+  return static_cast<size_t>(sh.SA) * 2 * kABlockBytes + static_cast<size_t>(sh.SB) * sh.bstage + kEpiBytes +
+         sh.oldb + 1024 + 512;
 }
 
 int gemm_tc_launch(const TcArgs& g, cudaStream_t s) {
   if (g.max_rows <= 0) return RTEC_OK;
-  size_t smem = gemm_tc_smem(g.npad);
+  const bool fused = g.delta_next && !g.Yt;
+  size_t smem = gemm_tc_smem(g.npad, fused);
   static int configured = 0;
   if (!configured) {
     RTEC_CUDA(cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -429,7 +493,7 @@ int gemm_tc_launch(const TcArgs& g, cudaStream_t s) {
   int64_t tiles = (g.max_rows + kTM - 1) / kTM;
   int grid = static_cast<int>(tiles < kSMs ? tiles : kSMs);
   RTEC_PROF("k_gemm_tc", s);
-  k_gemm_tc<<<grid, 512, smem, s>>>(g, tc_shape(g.npad));
+  k_gemm_tc<<<grid, 512, smem, s>>>(g, tc_shape(g.npad, fused));
   RTEC_LAUNCH_CHECK("k_gemm_tc");
   return RTEC_OK;
 }

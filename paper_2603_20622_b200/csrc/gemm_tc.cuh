@@ -19,6 +19,14 @@ struct TcArgs {
   float* Yt;              // ... or a tile-layout output feeding a chained GEMM
   int nkb_out;
   const uint64_t* err;
+  // fused source deltas of the next layer (sum aggregators): instead of the DeltaLog,
+  // delta_next[y_rows[i]] = c_new * h_new - c_old * h_old with c from the out-degrees
+  // (GCN 1/sqrt(deg + off), others 1; 0 for a vertex without out-edges)
+  float* delta_next;
+  const int32_t* deg_new;
+  const int32_t* deg_old;
+  int coeff_gcn;
+  float deg_off;
 };
 
 int gemm_tc_launch(const TcArgs& g, cudaStream_t s);

@@ -30,6 +30,12 @@ __device__ __forceinline__ float src_coeff(int model, int32_t deg, float off) {
   return model == RTEC_MODEL_GCN ? 1.0f / sqrtf(static_cast<float>(deg) + off) : 1.0f;
 }
 
+// source coefficient of the fused deltas (update epilogue): 0 for a vertex without
+// out-edges, which never contributes (keeps raw-degree GCN finite)
+__device__ __forceinline__ float fused_coeff(int model, int32_t deg, float off) {
+  return deg > 0 ? src_coeff(model, deg, off) : 0.f;
+}
+
 __host__ __device__ __forceinline__ bool is_gin(int model) {
   return model == RTEC_MODEL_GIN || model == RTEC_MODEL_GIN_MAX;
 }
@@ -63,6 +69,8 @@ __global__ void __launch_bounds__(kLBlk) k_src_delta(LayerArgs a, float* delta) 
   const int d = a.d_agg;
   for (int64_t i = warp; i < ns; i += nw) {
     int32_t u = a.f.src_list[i];
+    // rows of V_chg(l-1) were written by the previous layer's update epilogue
+    if (a.st.delta_ready && a.prev_bm_dst && bm_test(a.prev_bm_dst, u)) continue;
     int32_t dn = a.g.out_deg[u], dp = a.g.out_deg_prev[u];
     R acc;
     acc.zero();
@@ -161,6 +169,12 @@ __device__ __forceinline__ void agg_struct(const LayerArgs& a, int64_t p, int64_
     if (a.b.i_op[k] == RTEC_OP_INSERT) {
       R::load(a.st.H_in + static_cast<int64_t>(u) * d + a.c0, cw, r);
       acc.fma(r, src_coeff(a.L.model, a.g.out_deg[u], a.L.degree_offset));
+    } else if (a.st.delta_ready && a.prev_bm_dst && bm_test(a.prev_bm_dst, u)) {
+      // -c_old h_old(u) = δ_u - c_new h_new(u)  (fused deltas: no DeltaLog)
+      R::load(a.delta + static_cast<int64_t>(u) * d + a.c0, cw, r);
+      acc.add(r);
+      R::load(a.st.H_in + static_cast<int64_t>(u) * d + a.c0, cw, r);
+      acc.fma(r, -fused_coeff(a.L.model, a.g.out_deg[u], a.L.degree_offset));
     } else {
       const float* orow = a.st.H_in + static_cast<int64_t>(u) * d;
       if (a.prev_bm_dst && bm_test(a.prev_bm_dst, u)) orow = a.st.log_in + static_cast<int64_t>(a.prev_slot[u]) * d;
@@ -1259,8 +1273,8 @@ using namespace rtec;
 
 // update (and GIN's chained MLP) on rows of gemm_in: tcgen05 3xTF32 when the
 // layer carries prepared weights, SIMT fp32 otherwise
-static int run_update(const rtec_layer_t* L, rtec_state_t* st, const int64_t* n_rows, int64_t max_rows,
-                      const int32_t* y_rows, float* log, const uint64_t* err, cudaStream_t s);
+static int run_update(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* st, const int64_t* n_rows,
+                      int64_t max_rows, const int32_t* y_rows, float* log, const uint64_t* err, cudaStream_t s);
 
 static int layer_dims_ok(const rtec_layer_t* L) {
   if (L->model < 0 || L->model > RTEC_MODEL_GIN_MAX) {
@@ -1274,8 +1288,17 @@ static int layer_dims_ok(const rtec_layer_t* L) {
   return RTEC_OK;
 }
 
-static int run_update(const rtec_layer_t* L, rtec_state_t* st, const int64_t* n_rows, int64_t max_rows,
-                      const int32_t* y_rows, float* log, const uint64_t* err, cudaStream_t s) {
+static int run_update(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* st, const int64_t* n_rows,
+                      int64_t max_rows, const int32_t* y_rows, float* log, const uint64_t* err, cudaStream_t s) {
+  auto fuse = [&](TcArgs& t) {  // the next layer's source deltas from this update's epilogue
+    if (!st->delta_next || !y_rows || (L->d_out & 3)) return;
+    t.delta_next = st->delta_next;
+    t.deg_new = g->out_deg;
+    t.deg_old = g->out_deg_prev;
+    t.coeff_gcn = L->model == RTEC_MODEL_GCN;
+    t.deg_off = L->degree_offset;
+    t.log = nullptr;
+  };
   if (L->Wt_hi) {
     const int nkb = tc_nkb_of(L->d_in);
     if (is_gin(L->model)) {  // W2 relu(W (h + a)) (models.py:187-189), hidden kept in tile layout
@@ -1285,10 +1308,12 @@ static int run_update(const rtec_layer_t* L, rtec_state_t* st, const int64_t* n_
       RTEC_TRY(gemm_tc_launch(t1, s));
       TcArgs t2{st->gemm_mid, L->W2t_hi, L->W2t_lo, nkb2, tc_npad_of(L->d_out), L->d_out, n_rows, max_rows, 0,
                 st->H_out, L->d_out, y_rows, log, nullptr, 0, err};
+      fuse(t2);
       return gemm_tc_launch(t2, s);
     }
     TcArgs t{st->gemm_in, L->Wt_hi, L->Wt_lo, nkb, tc_npad_of(L->d_out), L->d_out, n_rows, max_rows, 1,
              st->H_out, L->d_out, y_rows, log, nullptr, 0, err};
+    fuse(t);
     return gemm_tc_launch(t, s);
   }
   if (is_gin(L->model)) {
@@ -1338,9 +1363,9 @@ int rtec_layer_incremental(const rtec_graph_t* g, const rtec_batch_t* b, const r
   if (L->model == RTEC_MODEL_GIN_MAX) {
     a.tc_nkb = L->Wt_hi ? tc_nkb_of(L->d_in) : 0;
     RTEC_TRY(launch_max<false>(a, AggRows{f->dst_list, f->n_dst, n}, n, g->in.slots, w, s));
-    return run_update(L, st, f->n_dst, n, f->dst_list, st->log_out, err, s);
+    return run_update(g, L, st, f->n_dst, n, f->dst_list, st->log_out, err, s);
   }
-  float* delta = w.alloc<float>(n * static_cast<int64_t>(L->d_in));
+  float* delta = st->delta ? st->delta : w.alloc<float>(n * static_cast<int64_t>(L->d_in));
   RTEC_WS_CHECK(w);
   a.delta = delta;
   bool ok;
@@ -1355,7 +1380,7 @@ int rtec_layer_incremental(const rtec_graph_t* g, const rtec_batch_t* b, const r
   a.tc_nkb = L->Wt_hi ? tc_nkb_of(L->d_in) : 0;
   RTEC_TRY(launch_aggregation<false>(a, AggRows{f->dst_list, f->n_dst, n}, n, g->in.slots, w, s));
   // update on V_dst(l) rows with DeltaLog capture (operators.py:180)
-  return run_update(L, st, f->n_dst, n, f->dst_list, st->log_out, err, s);
+  return run_update(g, L, st, f->n_dst, n, f->dst_list, st->log_out, err, s);
 }
 
 
@@ -1390,13 +1415,13 @@ int rtec_layer_full(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* 
   if (L->model == RTEC_MODEL_GIN_MAX) {
     Ws w(ws, ws_bytes);
     RTEC_TRY(launch_max<true>(a, AggRows{rows, rows ? n_rows : nullptr, n}, mr, g->in.slots, w, s));
-    return run_update(L, st, rows ? n_rows : nullptr, mr, rows, nullptr, nullptr, s);
+    return run_update(g, L, st, rows ? n_rows : nullptr, mr, rows, nullptr, nullptr, s);
   }
   {
     Ws w(ws, ws_bytes);
     RTEC_TRY(launch_aggregation<true>(a, AggRows{rows, rows ? n_rows : nullptr, n}, mr, g->in.slots, w, s));
   }
-  return run_update(L, st, rows ? n_rows : nullptr, mr, rows, nullptr, nullptr, s);
+  return run_update(g, L, st, rows ? n_rows : nullptr, mr, rows, nullptr, nullptr, s);
 }
 
 int rtec_gat_project(const rtec_layer_t* L, const float* H, const int32_t* rows, const int64_t* n_rows,

@@ -30,7 +30,7 @@ import torch
 from . import _lib
 from . import errors as E
 from .graph import DynamicGraph, EdgeUpdate, updates_to_arrays
-from .models import GAT, GIN_FAMILY, Bundle, MODELS
+from .models import GAT, GCN, GIN, GIN_FAMILY, GRAPHSAGE, Bundle, MODELS
 
 _MODEL_ID = _lib.MODEL_IDS
 
@@ -75,6 +75,8 @@ class _Frontier:
 class RTECEngine:
     """B200 incremental engine over a DynamicGraph and an operator Bundle."""
 
+    FUSED_DELTA = True
+
     def __init__(self, bundle: Bundle, graph: DynamicGraph, features, *, max_batch: int | None = None,
                  update: str = "tc", use_graphs: bool = True):
         if not isinstance(bundle, Bundle) or bundle.model not in MODELS:
@@ -103,6 +105,11 @@ class RTECEngine:
         heads = bundle.heads
         # tcgen05 3xTF32 update (gemm_tc.cu) for every dense update with d_out <= 256
         self.tc = update == "tc" and bundle.model != GAT and max(dims[1:]) <= 256
+        # sum aggregators on the tcgen05 path: the update epilogue of layer l writes the source
+        # deltas of layer l+1 (no DeltaLog, no per-source delta pass over V_chg(l))
+        self.fused = (self.FUSED_DELTA and self.tc and bundle.model in (GCN, GRAPHSAGE, GIN)
+                      and all(d % 4 == 0 for d in dims[1:-1]))
+        self.delta = [z(n, bundle.agg_dims[l]) if self.fused else None for l in range(bundle.num_layers)]
         for l, w in enumerate(bundle.layers):
             d_in, d_out = w.in_dim, w.out_dim
             W = torch.as_tensor(np.asarray(w.tensors["W"], np.float32), device=self.dev).contiguous()
@@ -122,7 +129,7 @@ class RTECEngine:
             self.H.append(z(n, d_out))
             self.S.append(z(n, d_agg))
             # DeltaLog of this layer's output; the final layer's is never read (no layer L+1)
-            self.log.append(z(n, d_out) if l + 1 < bundle.num_layers else None)
+            self.log.append(z(n, d_out) if l + 1 < bundle.num_layers and not self.fused else None)
             if bundle.model == GAT:
                 self.ctx.append(z(n, heads))
                 self.Z.append(z(n, d_out))
@@ -162,11 +169,16 @@ class RTECEngine:
         if self.g.ws.numel() < need:
             self.g.ws = torch.empty(need, dtype=torch.uint8, device=self.dev)
 
-    def _state(self, l):
+    def _state(self, l, incremental: bool = False):
         p = _lib.ptr
-        return _lib.State(p(self.H[l]), p(self.H[l + 1]), p(self.S[l]), p(self.ctx[l]), p(self.log[l]),
-                          p(self.log[l - 1]) if l > 0 else None, p(self.Z[l]), p(self.el[l]), p(self.er[l]),
-                          p(self.Zlog[l]), p(self.erlog[l]), p(self.gemm_in), p(self.gemm_mid))
+        st = _lib.State(p(self.H[l]), p(self.H[l + 1]), p(self.S[l]), p(self.ctx[l]), p(self.log[l]),
+                        p(self.log[l - 1]) if l > 0 else None, p(self.Z[l]), p(self.el[l]), p(self.er[l]),
+                        p(self.Zlog[l]), p(self.erlog[l]), p(self.gemm_in), p(self.gemm_mid))
+        if incremental and self.fused:
+            st.delta = p(self.delta[l])
+            st.delta_next = p(self.delta[l + 1]) if l + 1 < self.L else None
+            st.delta_ready = 1 if l > 0 else 0
+        return st
 
     # ---------------------------------------------------------------- SPEC bootstrap / run_full
     def bootstrap(self):
@@ -229,7 +241,7 @@ class RTECEngine:
         errp = _lib.ptr(gr.batch.err)
         sdd = 1 if self.b.src_degree_dependent else 0
         self._fc = [f.c() for f in self.fr]
-        self._sc = [self._state(l) for l in range(self.L)]
+        self._sc = [self._state(l, incremental=True) for l in range(self.L)]
         for l in range(self.L):
             prev = C.byref(self._fc[l - 1]) if l > 0 else None
             _lib.check(self.lib.rtec_frontier_layer(C.byref(g), C.byref(b), l, sdd, prev, C.byref(self._fc[l]), ws, wsb,

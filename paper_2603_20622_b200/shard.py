@@ -101,6 +101,8 @@ def combine_err_words(words) -> int:
 class ShardedRTECEngine(RTECEngine):
     """RTECEngine over this rank's shard; same step()/query() API."""
 
+    FUSED_DELTA = False  # the halo exchange ships new rows and rebuilds the DeltaLog on receipt
+
     def __init__(self, bundle, num_vertices: int, edges, features, comm: Comm, *, max_batch: int | None = None,
                  update: str = "tc", reserve: int | None = None, device=None, exchange_chunk: int = 1 << 20):
         self.comm = comm
@@ -139,8 +141,8 @@ class ShardedRTECEngine(RTECEngine):
         g.out_deg, g.out_deg_prev = _lib.ptr(self.gout), _lib.ptr(self.gout_prev)
         return g
 
-    def _state(self, l):
-        s = super()._state(l)
+    def _state(self, l, incremental: bool = False):
+        s = super()._state(l, incremental)
         if l > 0:
             s.log_in = _lib.ptr(self.glog[l - 1]) if len(self.glog) >= l else None
         return s
