@@ -184,17 +184,21 @@ __device__ __forceinline__ void agg_struct(const LayerArgs& a, int64_t p, int64_
   }
 }
 
-// S_v update (INC: S += Σ, zero-in-degree rule; FULL: S = Σ), compose, GEMM input row i
+// S_v update (INC: S += Σ, zero-in-degree rule; FULL: S = Σ), compose, GEMM input row i.
+// `pre`: the caller already loaded indeg and the cached row (sv, zero when not to be added).
 template <int VEC, int K, bool FULL>
 __device__ __forceinline__ void agg_finalize(const LayerArgs& a, int64_t i, int32_t v, int32_t len,
-                                             RowAcc<VEC, K>& acc) {
+                                             RowAcc<VEC, K>& acc, const RowAcc<VEC, K>* pre = nullptr,
+                                             int32_t pre_indeg = 0) {
   using R = RowAcc<VEC, K>;
   const int d = a.d_agg, cw = a.cw;
   float* srow = a.st.S + static_cast<int64_t>(v) * d + a.c0;
-  int32_t indeg = FULL ? len : a.g.in_deg[v];
+  int32_t indeg = FULL ? len : (pre ? pre_indeg : a.g.in_deg[v]);
   if (!FULL) {
     if (indeg == 0) {
       acc.zero();  // empty neighbourhood -> zero aggregate
+    } else if (pre) {
+      acc.add(pre->v);
     } else if (a.g.in_deg_prev[v] > 0) {
       float sv[K][VEC];
       R::load_stream(srow, cw, sv, l2_evict_first_policy());
@@ -252,21 +256,32 @@ __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_light(Laye
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = warp; i < nr; i += nw) {
     int32_t v = rows.at(i);
-    int32_t len = a.g.in.len[v];
+    // independent per-destination loads issued together (the chain below is latency-bound)
+    const int32_t len = a.g.in.len[v];
+    const int64_t beg = a.g.in.beg[v];
+    int2 rg = make_int2(-1, 0);
+    int32_t indeg = len, had = 0;
+    if (!FULL) {
+      rg = reinterpret_cast<const int2*>(a.b.irange)[v];
+      indeg = a.g.in_deg[v];
+      had = a.g.in_deg_prev[v];
+    }
     if (scan && len > kChunk) continue;  // heavy pass
     int64_t p = 0, q = 0;
-    if (!FULL) {
-      int2 rg = reinterpret_cast<const int2*>(a.b.irange)[v];
-      if (rg.x >= 0) {
-        p = rg.x;
-        q = rg.x + rg.y;
-      }
+    if (rg.x >= 0) {
+      p = rg.x;
+      q = rg.x + rg.y;
     }
+    // the cached aggregate row, requested before the edge scan so its latency overlaps it
+    R sv;
+    sv.zero();
+    if (!FULL && indeg > 0 && had > 0)
+      R::load_stream(a.st.S + static_cast<int64_t>(v) * a.d_agg + a.c0, a.cw, sv.v, l2_evict_first_policy());
     R acc;
     acc.zero();
-    if (scan) agg_edges<VEC, K, FULL>(a, a.g.in.beg[v], 0, len, p, q, acc);
+    if (scan) agg_edges<VEC, K, FULL>(a, beg, 0, len, p, q, acc);
     if (!FULL) agg_struct<VEC, K>(a, p, q, acc);
-    agg_finalize<VEC, K, FULL>(a, i, v, len, acc);
+    agg_finalize<VEC, K, FULL>(a, i, v, len, acc, FULL ? nullptr : &sv, indeg);
   }
 }
 
