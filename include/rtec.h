@@ -252,7 +252,9 @@ int rtec_layer_incremental(const rtec_graph_t* g, const rtec_batch_t* b, const r
                            rtec_state_t* st, const rtec_frontier_t* prev, const rtec_frontier_t* f,
                            uint64_t* err, void* ws, size_t ws_bytes, rtec_stream_t stream);
 /* layer_embeddings (models.py:461-477) for all vertices (rows == NULL) or the
- * listed rows: bootstrap, refresh and dense fallback. */
+ * listed rows: bootstrap, refresh, dense fallback and the UER baseline (SPEC.md:455:
+ * affected rows over their full in-neighbourhoods).  GAT with rows expects Z / el / er
+ * of the changed sources to be current (rtec_gat_project). */
 int rtec_layer_full(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* st,
                     const int32_t* rows, const int64_t* n_rows, int64_t max_rows, uint64_t* err,
                     void* ws, size_t ws_bytes, rtec_stream_t stream);

@@ -14,6 +14,6 @@ from .graph import (  # noqa: F401
     write_stream,
 )
 from .models import MODELS, Bundle, LayerWeights, from_reference, make_bundle  # noqa: F401
-from .engine import Metrics, RTECEngine, RunResult  # noqa: F401
+from .engine import Metrics, RTECEngine, RunResult, redundancy  # noqa: F401
 
 __version__ = "0.1.0"

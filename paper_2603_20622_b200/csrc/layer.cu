@@ -1412,16 +1412,14 @@ int rtec_layer_full(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* 
   a.err = err;
   const int grid = kSMs * 8;
   if (L->model == RTEC_MODEL_GAT) {
-    if (rows) {
-      set_error("GAT full layer supports all rows only");
-      return RTEC_CONFIG_ERROR;
-    }
+    Ws w(ws, ws_bytes);
+    if (rows)  // listed rows (UER): the caller keeps Z / el / er current for the changed sources
+      return launch_gat<true>(a, AggRows{rows, n_rows, n}, max_rows, g->in.slots, w, s);
     // Z = W H (all rows), logits, then the full softmax aggregation
     GemmArgs gz{st->H_in, L->d_in, nullptr, L->W, L->d_in, L->d_out, nullptr, n, 0, st->Z, L->d_out, nullptr, nullptr, nullptr};
     RTEC_TRY(gemm_launch(gz, s));
     k_gat_logits<<<grid, kLBlk, 0, s>>>(st->Z, nullptr, nullptr, n, L->d_out, L->heads, L->att, st->el, st->er,
                                         nullptr, nullptr);
-    Ws w(ws, ws_bytes);
     return launch_gat<true>(a, AggRows{nullptr, nullptr, n}, n, g->in.slots, w, s);
   }
   a.d_agg = L->d_in;

@@ -43,6 +43,23 @@ class Metrics:
     v_dst: list = field(default_factory=list)    # |V_dst(l)|
     n_src: list = field(default_factory=list)    # |S(l)|
     in_edges_vdst: list = field(default_factory=list)  # Σ indeg(V_dst(l)) (scanned in-runs)
+    mode: str = "inc"                            # inc | uer | full
+    edge_accesses: list = field(default_factory=list)    # per layer, for `mode`
+    vertex_accesses: list = field(default_factory=list)
+    as_edges: int = 0                            # affected subgraph: Σ_l |E_curr(l)|
+    as_vertices: int = 0                         # Σ_l |V_dst(l)|
+
+
+def redundancy(m: Metrics, num_edges: int, num_vertices: int) -> dict:
+    """Access volume of each strategy relative to the affected subgraph (PAPER.md:165-191,
+    Fig. 2 / Table V): FN = full-neighbour recompute of every layer, UER = affected rows over
+    their full in-neighbourhoods, Inc = the incremental engine (exactly the affected edges)."""
+    L = len(m.e_curr)
+    a = max(m.as_edges, 1)
+    return {"as_edges": m.as_edges, "as_vertices": m.as_vertices,
+            "fn_edges": L * int(num_edges), "uer_edges": sum(m.in_edges_vdst), "inc_edges": sum(m.e_curr),
+            "fn_over_as": L * int(num_edges) / a, "uer_over_as": sum(m.in_edges_vdst) / a,
+            "inc_over_as": sum(m.e_curr) / a, "fn_vertices": L * int(num_vertices)}
 
 
 @dataclass
@@ -181,8 +198,9 @@ class RTECEngine:
         return st
 
     # ---------------------------------------------------------------- SPEC bootstrap / run_full
-    def bootstrap(self):
-        """Full forward populating every layer's state (models.py:461-477)."""
+    def bootstrap(self, sync: bool = True):
+        """Full forward populating every layer's state (SPEC.md:370; models.py:461-477);
+        also SPEC run_full on the current graph."""
         err = torch.full((1,), -1, dtype=torch.int64, device=self.dev)
         g = self.g.c()
         st = _lib.stream_handle()
@@ -190,9 +208,16 @@ class RTECEngine:
             s = self._state(l)
             _lib.check(self.lib.rtec_layer_full(C.byref(g), C.byref(self.layers[l]), C.byref(s), None, None, self.n,
                                                 _lib.ptr(err), _lib.ptr(self.g.ws), self.g.ws.numel(), st), "bootstrap")
-        _lib.raise_err(err.item(), "bootstrap")
+        if sync:
+            _lib.raise_err(err.item(), "bootstrap")
 
-    run_full = bootstrap
+    def run_full(self, batch=None) -> RunResult | None:
+        """SPEC run_full: without a batch, recompute every layer on the
+        current graph; with one, apply it and recompute everything (the RTEC-Full baseline)."""
+        if batch is None:
+            self.bootstrap()
+            return None
+        return self.step(*updates_to_arrays(list(batch)), mode="full")
 
     # ---------------------------------------------------------------- incremental step
     def _graph_key(self, B: int):
@@ -232,7 +257,9 @@ class RTECEngine:
             self._graphs[key] = cg
         cg.replay()
 
-    def _enqueue_eager(self, B: int) -> None:
+    def _enqueue_eager(self, B: int, mode: str = "inc") -> None:
+        """mode 'inc': Alg. 1 / Alg. 3 (run_incremental); 'uer': the same affected rows
+        recomputed over their full in-neighbourhoods (SPEC.md:455 run_uer)."""
         gr = self.g
         gr.apply_staged(B)
         g, b = gr._gc, gr._bc
@@ -246,15 +273,24 @@ class RTECEngine:
             prev = C.byref(self._fc[l - 1]) if l > 0 else None
             _lib.check(self.lib.rtec_frontier_layer(C.byref(g), C.byref(b), l, sdd, prev, C.byref(self._fc[l]), ws, wsb,
                                                     st), "frontier")
+            if mode == "frontier":
+                continue
             if self.b.model == GAT and l > 0:
                 pf = self.fr[l - 1]
                 _lib.check(self.lib.rtec_gat_project(C.byref(self.layers[l]), _lib.ptr(self.H[l]), _lib.ptr(pf.dst_list),
                                                      _lib.ptr(pf.n_dst), self.n, _lib.ptr(self.Z[l]), _lib.ptr(self.el[l]),
                                                      _lib.ptr(self.er[l]), _lib.ptr(self.Zlog[l]), _lib.ptr(self.erlog[l]),
                                                      errp, st), "gat_project")
-            _lib.check(self.lib.rtec_layer_incremental(C.byref(g), C.byref(b), C.byref(self.layers[l]),
-                                                       C.byref(self._sc[l]), prev, C.byref(self._fc[l]), errp, ws, wsb,
-                                                       st), "layer")
+            if mode == "uer":
+                f = self.fr[l]
+                s_full = self._state(l)
+                _lib.check(self.lib.rtec_layer_full(C.byref(g), C.byref(self.layers[l]), C.byref(s_full),
+                                                    _lib.ptr(f.dst_list), _lib.ptr(f.n_dst), self.n, errp, ws, wsb,
+                                                    st), "layer (uer)")
+            else:
+                _lib.check(self.lib.rtec_layer_incremental(C.byref(g), C.byref(b), C.byref(self.layers[l]),
+                                                           C.byref(self._sc[l]), prev, C.byref(self._fc[l]), errp, ws,
+                                                           wsb, st), "layer")
         _lib.check(self.lib.rtec_batch_commit(C.byref(g), C.byref(b), st), "commit")
 
     def _readback(self, B: int):
@@ -278,22 +314,51 @@ class RTECEngine:
         torch.cuda.current_stream().synchronize()
         return hb
 
-    def _metrics_from(self, ctr) -> Metrics:
-        m = Metrics()
+    def _metrics_from(self, ctr, mode: str = "inc") -> Metrics:
+        m = Metrics(mode=mode)
         c = ctr.numpy().reshape(self.L, 8)
+        m_edges = self.g.num_edges if mode == "full" else 0
         for l in range(self.L):
             m.e_curr.append(int(c[l, 0]))
             m.v_dst.append(int(c[l, 1]))
             m.n_src.append(int(c[l, 2]))
             m.in_edges_vdst.append(int(c[l, 5]))
+            # access counters: one edge access per processed (edge, layer),
+            # one vertex access per recomputed destination
+            if mode == "inc":
+                m.edge_accesses.append(int(c[l, 0]))
+                m.vertex_accesses.append(int(c[l, 1]))
+            elif mode == "uer":
+                m.edge_accesses.append(int(c[l, 5]))
+                m.vertex_accesses.append(int(c[l, 1]))
+            else:
+                m.edge_accesses.append(int(m_edges))
+                m.vertex_accesses.append(int(self.n))
+        m.as_edges = sum(m.e_curr)
+        m.as_vertices = sum(m.v_dst)
         return m
 
-    def step(self, op, src, dst, ts) -> RunResult:
-        """run_incremental on array inputs; one host synchronisation at the end reads
-        the per-update status, DegreeDelta rows and counters from pinned buffers."""
+    def run_uer(self, batch) -> RunResult:
+        """SPEC run_uer: affected rows over their full in-neighbourhoods."""
+        return self.step(*updates_to_arrays(list(batch)), mode="uer")
+
+    def step(self, op, src, dst, ts, mode: str = "inc") -> RunResult:
+        """One batch on array inputs: mode 'inc' = run_incremental, 'uer' =
+        run_uer, 'full' = apply + run_full.  One host
+        synchronisation at the end reads the per-update status, DegreeDelta rows and
+        counters from pinned buffers."""
+        if mode not in ("inc", "uer", "full"):
+            raise E.ConfigError(f"unknown engine mode {mode!r} (inc, uer, full)")
         B = self.g.stage(op, src, dst, ts)
         for attempt in range(4):
-            self.enqueue_step(B)
+            if mode == "inc":
+                self.enqueue_step(B)
+            else:
+                self._ensure_ws(self.g.batch.cap)
+                # 'full': apply + the frontier (for the access counters), then every layer
+                self._enqueue_eager(B, mode="uer" if mode == "uer" else "frontier")
+                if mode == "full":
+                    self.bootstrap(sync=False)
             hb = self._readback(B)
             word = int(hb["err"][0]) & _lib.ERR_OK
             d = _lib.decode_err(word)
@@ -311,7 +376,7 @@ class RTECEngine:
         k = int(hb["nd"][0])
         # DegreeDelta rows (vertex, old_in, new_in, old_out, new_out) as int32 [k, 5]
         deltas = np.stack([h[:k].numpy() for h in hb["d"]], axis=1) if k else np.zeros((0, 5), np.int32)
-        return RunResult(status, deltas, None, self._metrics_from(hb["ctr"]))
+        return RunResult(status, deltas, None, self._metrics_from(hb["ctr"], mode))
 
     def run_incremental(self, batch) -> RunResult:
         """SPEC run_incremental on a coalesced EdgeUpdate list."""

@@ -222,3 +222,37 @@ def test_cuda_graph_replay_matches_eager(P):
     assert np.array_equal(outs[0][0], outs[1][0])
     for a, b in zip(outs[0][1], outs[1][1]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("model,dims", [("gcn", [24, 32, 16]), ("gat", [24, 32, 32]), ("gin_max", [16, 24, 16])])
+def test_uer_and_full_modes_match_oracle(P, model, dims):
+    # SPEC run_uer / run_full on the same stream: both equal the
+    # reference recompute; access counters obey Inc <= UER <= FN (SPEC.md:601 ordering)
+    from oracle import models as OM
+    from oracle.engine import OracleEngine
+    from oracle.graph import OracleGraph
+    from paper_2603_20622_b200.workload import UpdateStream, chung_lu_edges, features
+
+    n, m = 2500, 25000
+    s, d = chung_lu_edges(n, m, seed=19)
+    X = features(n, dims[0], seed=5)
+    runs = {}
+    for mode in ("inc", "uer", "full"):
+        stream = UpdateStream(s, d, holdout=0.1, seed=19)
+        bs, bd, bt = stream.base()
+        eng = P.RTECEngine(P.make_bundle(model, dims), P.DynamicGraph.from_edges(n, (bs, bd, bt)), X)
+        oe = OracleEngine(OM.make_bundle(model, dims), OracleGraph.from_edges(n, bs, bd, bt), X.astype(np.float64))
+        for _ in range(3):
+            batch = stream.next_batch(150)
+            r = eng.step(*batch, mode=mode)
+            o = oe.step(*batch)
+            assert np.array_equal(r.status, o["status"])
+        for l in range(1, len(dims)):
+            assert rowwise_rel(eng.embeddings(l), oe.H[l]) <= TOL, (mode, l)
+        runs[mode] = r.metrics
+    inc, uer, full = runs["inc"], runs["uer"], runs["full"]
+    assert inc.e_curr == uer.e_curr == full.e_curr  # same affected subgraph
+    for l in range(len(dims) - 1):
+        assert inc.edge_accesses[l] <= uer.edge_accesses[l] <= full.edge_accesses[l]
+    rep = P.redundancy(inc, full.edge_accesses[0], n)
+    assert rep["inc_over_as"] == 1.0 and rep["fn_over_as"] >= rep["uer_over_as"] >= 1.0
