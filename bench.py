@@ -72,6 +72,7 @@ def parse():
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks / cpu baseline)")
     ap.add_argument("--no-graphs", action="store_true", help="launch the per-batch pipeline eagerly (no CUDA graph)")
+    ap.add_argument("--no-baselines", action="store_true", help="skip the UER / RTEC-Full GPU baseline batches")
     return ap.parse_args()
 
 
@@ -224,8 +225,9 @@ def run_ours(args, world, rank, local):
     K, W = args.steps, args.warmup
     E2E = args.e2e_steps if args.e2e_steps is not None else min(K, 10)
     PROF = min(K, 10)  # eager profiled pass after the timed region (per-kernel CUDA events)
+    NB = 0 if (world > 1 or args.no_baselines) else 3  # batches per GPU baseline mode (UER, Full)
     t0 = time.time()
-    stream, batches, X = make_workload(wl, W + K + PROF + E2E, dev)
+    stream, batches, X = make_workload(wl, W + K + PROF + E2E + 2 * NB, dev)
     bs, bd, bt = stream.base()
     bundle = P.make_bundle(wl["model"], wl["dims"], heads=wl["heads"])
     sharded = world > 1
@@ -335,6 +337,32 @@ def run_ours(args, world, rank, local):
     if E2E:
         e2e_s = max_over_ranks(sum(e2e_ms) / 1e3, world)
         e2e_val = sum_over_ranks(e2e_upd, world) / e2e_s
+    # --- the paper's comparison set on the same GPU and stream: the same
+    # public step() with the affected rows recomputed over full in-neighbourhoods (UER) and
+    # every layer recomputed (RTEC-Full); per-batch time incl. H2D / D2H like `e2e`
+    baselines = {}
+    for bi, mode in enumerate(("uer", "full")[: 2 if NB else 0]):
+        ms, ups, acc = [], 0, 0
+        for j in range(NB):
+            op, s, d, t = batches[W + K + PROF + E2E + bi * NB + j]
+            hb = [torch.from_numpy(np.ascontiguousarray(a, dt)).pin_memory()
+                  for a, dt in ((op, np.uint8), (s, np.int32), (d, np.int32), (t, np.int64))]
+            torch.cuda.synchronize()
+            a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_ev.record()
+            r = eng.step(*hb, mode=mode)
+            b_ev.record()
+            torch.cuda.synchronize()
+            ms.append(a_ev.elapsed_time(b_ev))
+            ups += int(r.status.sum())
+            acc += sum(r.metrics.edge_accesses)
+        baselines[mode] = {"p50_batch_ms": round(statistics.median(ms), 3),
+                           "value": round(ups / (sum(ms) / 1e3), 1), "unit": "edge updates/s", "batches": NB,
+                           "edge_accesses_per_batch": acc // NB}
+    if baselines and e2e_ms:
+        for mode in baselines:
+            baselines[mode]["incremental_speedup"] = round(baselines[mode]["p50_batch_ms"] /
+                                                           statistics.median(e2e_ms), 2)
     # --- roofline of the dominant kernel
     from_peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
@@ -411,6 +439,7 @@ def run_ours(args, world, rank, local):
                 "p50_batch_ms": round(statistics.median(e2e_ms), 4) if e2e_ms else None},
         "gpu_launches": None,
         "roofline": roof,
+        "gpu_baselines": baselines or None,
         "kernels": kernels,
         "frontier": {"e_curr": [int(np.mean(C[:, l, 0])) for l in range(L)],
                      "v_dst": [int(np.mean(C[:, l, 1])) for l in range(L)],
