@@ -151,18 +151,20 @@ __global__ void __launch_bounds__(1024) k_sort_small(const uint64_t* __restrict_
 // ---------------------------------------------------------------- radix sort
 constexpr int kRxBlock = 256;
 constexpr int kRxItems = 8;
-constexpr int kRxTile = kRxBlock * kRxItems;
 constexpr int kRxBins = 256;
+// items per thread: fewer for mid-size sorts (a batch of ~10^5 updates) so >100 CTAs take part
+inline int rx_items_for(int64_t max_n) { return max_n <= 131072 ? 1 : (max_n <= 524288 ? 4 : kRxItems); }
 
+template <int ITEMS>
 __global__ void __launch_bounds__(kRxBlock) k_rx_hist(const uint64_t* __restrict__ keys, Count cnt, int shift,
                                                       int64_t ntiles, uint32_t* __restrict__ counts) {
   __shared__ uint32_t hist[kRxBins];
   hist[threadIdx.x] = 0;
   __syncthreads();
   int64_t n = cnt.get();
-  int64_t base = static_cast<int64_t>(blockIdx.x) * kRxTile;
+  int64_t base = static_cast<int64_t>(blockIdx.x) * kRxBlock * ITEMS;
 #pragma unroll
-  for (int k = 0; k < kRxItems; ++k) {
+  for (int k = 0; k < ITEMS; ++k) {
     int64_t i = base + k * kRxBlock + threadIdx.x;
     if (i < n) atomicAdd(&hist[(keys[i] >> shift) & 0xff], 1u);
   }
@@ -170,6 +172,7 @@ __global__ void __launch_bounds__(kRxBlock) k_rx_hist(const uint64_t* __restrict
   counts[static_cast<int64_t>(threadIdx.x) * ntiles + blockIdx.x] = hist[threadIdx.x];
 }
 
+template <int ITEMS>
 __global__ void __launch_bounds__(kRxBlock) k_rx_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                          uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                          Count cnt, int shift, int64_t ntiles,
@@ -184,9 +187,9 @@ __global__ void __launch_bounds__(kRxBlock) k_rx_scatter(const uint64_t* __restr
   goff[t] = offsets[static_cast<int64_t>(t) * ntiles + blockIdx.x];
   __syncthreads();
   int64_t n = cnt.get();
-  int64_t base = static_cast<int64_t>(blockIdx.x) * kRxTile;
+  int64_t base = static_cast<int64_t>(blockIdx.x) * kRxBlock * ITEMS;
   unsigned lt_mask = (1u << lane) - 1u;
-  for (int k = 0; k < kRxItems; ++k) {
+  for (int k = 0; k < ITEMS; ++k) {
     int64_t i = base + k * kRxBlock + t;
     bool valid = i < n;
     uint64_t key = valid ? kin[i] : 0;
@@ -220,7 +223,8 @@ __global__ void __launch_bounds__(kRxBlock) k_rx_scatter(const uint64_t* __restr
 }
 
 size_t sort_ws_bytes(int64_t max_n) {
-  int64_t ntiles = (max_n + kRxTile - 1) / kRxTile;
+  const int64_t tile = static_cast<int64_t>(kRxBlock) * rx_items_for(max_n);
+  int64_t ntiles = (max_n + tile - 1) / tile;
   if (ntiles < 1) ntiles = 1;
   size_t b = 0;
   auto add = [&](size_t x) { b += (x + 255) & ~size_t(255); };
@@ -247,7 +251,8 @@ int sort_pairs(const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* keys_
     RTEC_LAUNCH_CHECK("k_sort_small");
     return RTEC_OK;
   }
-  int64_t ntiles = (max_n + kRxTile - 1) / kRxTile;
+  const int items = rx_items_for(max_n);
+  const int64_t ntiles = (max_n + static_cast<int64_t>(kRxBlock) * items - 1) / (static_cast<int64_t>(kRxBlock) * items);
   uint64_t* ka = ws.alloc<uint64_t>(max_n);
   uint32_t* va = ws.alloc<uint32_t>(max_n);
   uint64_t* kb = ws.alloc<uint64_t>(max_n);
@@ -264,10 +269,15 @@ int sort_pairs(const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* keys_
     uint64_t* ko = last ? keys_out : ((p & 1) ? kb : ka);
     uint32_t* vo = last ? vals_out : ((p & 1) ? vb : va);
     int shift = 8 * p;
-    k_rx_hist<<<static_cast<unsigned>(ntiles), kRxBlock, 0, s>>>(ki, cnt, shift, ntiles, counts);
+    const unsigned grid = static_cast<unsigned>(ntiles);
+    if (items == 1) k_rx_hist<1><<<grid, kRxBlock, 0, s>>>(ki, cnt, shift, ntiles, counts);
+    else if (items == 4) k_rx_hist<4><<<grid, kRxBlock, 0, s>>>(ki, cnt, shift, ntiles, counts);
+    else k_rx_hist<kRxItems><<<grid, kRxBlock, 0, s>>>(ki, cnt, shift, ntiles, counts);
     RTEC_TRY(exclusive_scan_bs(U32At{counts}, Count{nullptr, kRxBins * ntiles}, kRxBins * ntiles,
                                StorePrefix{offs}, nullptr, bs, s));
-    k_rx_scatter<<<static_cast<unsigned>(ntiles), kRxBlock, 0, s>>>(ki, vi, ko, vo, cnt, shift, ntiles, offs);
+    if (items == 1) k_rx_scatter<1><<<grid, kRxBlock, 0, s>>>(ki, vi, ko, vo, cnt, shift, ntiles, offs);
+    else if (items == 4) k_rx_scatter<4><<<grid, kRxBlock, 0, s>>>(ki, vi, ko, vo, cnt, shift, ntiles, offs);
+    else k_rx_scatter<kRxItems><<<grid, kRxBlock, 0, s>>>(ki, vi, ko, vo, cnt, shift, ntiles, offs);
     RTEC_LAUNCH_CHECK("k_rx_scatter");
     ki = ko;
     vi = vo;

@@ -49,16 +49,21 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T* smem_warp, T* total) {
   return r;
 }
 
-template <typename F>
+// items per thread: 8 for large inputs; 1 below kScanSmall so mid-size scans (a batch of
+// ~10^5 updates) still spread over >100 CTAs instead of a latency-bound handful
+constexpr int64_t kScanSmall = 262144;
+inline int scan_items_for(int64_t max_n) { return max_n <= kScanSmall ? 1 : kScanItems; }
+
+template <typename F, int ITEMS = kScanItems>
 __global__ void __launch_bounds__(kScanBlock) k_scan_reduce(F f, Count cnt, int64_t* block_sums) {
   __shared__ int64_t sw[kScanBlock / 32];
   int64_t n = cnt.get();
-  int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile;
+  int64_t base = static_cast<int64_t>(blockIdx.x) * kScanBlock * ITEMS;
   int64_t s = 0;
   if (base < n) {
 #pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-      int64_t i = base + static_cast<int64_t>(threadIdx.x) * kScanItems + k;
+    for (int k = 0; k < ITEMS; ++k) {
+      int64_t i = base + static_cast<int64_t>(threadIdx.x) * ITEMS + k;
       if (i < n) s += f(i);
     }
   }
@@ -70,30 +75,33 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_reduce(F f, Count cnt, int6
 // single CTA: exclusive scan of block_sums in place; total -> *total
 __global__ void __launch_bounds__(kScanBlock) k_scan_blocks(int64_t* block_sums, int64_t nb, int64_t* total);
 
-template <typename F, typename O>
+template <typename F, typename O, int ITEMS = kScanItems>
 __global__ void __launch_bounds__(kScanBlock) k_scan_down(F f, Count cnt, const int64_t* block_sums, O out) {
   __shared__ int64_t sw[kScanBlock / 32];
   int64_t n = cnt.get();
-  int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile;
+  int64_t base = static_cast<int64_t>(blockIdx.x) * kScanBlock * ITEMS;
   if (base >= n) return;
-  int64_t vals[kScanItems];
+  int64_t vals[ITEMS];
   int64_t s = 0;
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    int64_t i = base + static_cast<int64_t>(threadIdx.x) * kScanItems + k;
+  for (int k = 0; k < ITEMS; ++k) {
+    int64_t i = base + static_cast<int64_t>(threadIdx.x) * ITEMS + k;
     vals[k] = (i < n) ? f(i) : 0;
     s += vals[k];
   }
   int64_t off = block_exclusive_scan<int64_t>(s, sw, nullptr) + block_sums[blockIdx.x];
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    int64_t i = base + static_cast<int64_t>(threadIdx.x) * kScanItems + k;
+  for (int k = 0; k < ITEMS; ++k) {
+    int64_t i = base + static_cast<int64_t>(threadIdx.x) * ITEMS + k;
     if (i < n) out(i, off, vals[k]);
     off += vals[k];
   }
 }
 
-inline int64_t scan_blocks_for(int64_t max_n) { return (max_n + kScanTile - 1) / kScanTile; }
+inline int64_t scan_blocks_for(int64_t max_n) {
+  const int64_t tile = static_cast<int64_t>(kScanBlock) * scan_items_for(max_n);
+  return (max_n + tile - 1) / tile;
+}
 
 // whole scan in one CTA when the (host-side) bound fits one tile: one launch instead of three
 template <typename F, typename O>
@@ -123,15 +131,21 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_one(F f, Count cnt, O out, 
 // (device, may be null) receives the sum.  ws needs scan_blocks_for(max)+1 int64.
 template <typename F, typename O>
 int exclusive_scan_bs(F f, Count cnt, int64_t max_n, O out, int64_t* total, int64_t* bs, cudaStream_t s) {
-  int64_t nb = scan_blocks_for(max_n);
-  if (nb <= 1) {
+  if (max_n <= kScanTile) {
     k_scan_one<F, O><<<1, kScanBlock, 0, s>>>(f, cnt, out, total);
     RTEC_LAUNCH_CHECK("exclusive_scan");
     return RTEC_OK;
   }
-  k_scan_reduce<F><<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(f, cnt, bs);
-  k_scan_blocks<<<1, kScanBlock, 0, s>>>(bs, nb, total);
-  k_scan_down<F, O><<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(f, cnt, bs, out);
+  int64_t nb = scan_blocks_for(max_n);
+  if (scan_items_for(max_n) == 1) {
+    k_scan_reduce<F, 1><<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(f, cnt, bs);
+    k_scan_blocks<<<1, kScanBlock, 0, s>>>(bs, nb, total);
+    k_scan_down<F, O, 1><<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(f, cnt, bs, out);
+  } else {
+    k_scan_reduce<F><<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(f, cnt, bs);
+    k_scan_blocks<<<1, kScanBlock, 0, s>>>(bs, nb, total);
+    k_scan_down<F, O><<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(f, cnt, bs, out);
+  }
   RTEC_LAUNCH_CHECK("exclusive_scan");
   return RTEC_OK;
 }
