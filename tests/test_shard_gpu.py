@@ -117,7 +117,7 @@ def _run(cfg, world=2):
 
 
 @pytest.mark.parametrize("model,dims", [("gcn", [32, 64, 32]), ("graphsage", [48, 64, 32]), ("gin", [32, 32, 32]),
-                                        ("gat", [40, 32, 32])])
+                                        ("gat", [40, 32, 32]), ("gin_max", [32, 32, 32])])
 def test_sharded_matches_unsharded(model, dims):
     _run(dict(model=model, dims=dims, n=3000, m=40000, B=300, nb=3, seed=21))
 
