@@ -305,6 +305,18 @@ int rtec_halo_unpack(const rtec_graph_t* g, int32_t d, const int32_t* recv_ids, 
                      const int32_t* dst_slot, float* glog, uint32_t* bm_chg, int32_t* chg_slot, int32_t* chg_list,
                      int64_t* n_chg, rtec_stream_t stream);
 
+/* ---- NS baseline (SPEC.md:464 run_ns) ---- */
+/* Seeded sampling without replacement of min(len, fanout) in-neighbours (ascending) of
+ * every listed row into `sampled` (beg/len set for the rows, nbr filled, *top = total);
+ * bm_next <- rows ∪ sampled neighbours (the rows the hop below must provide).
+ * fanout in [1, 32]; deterministic in (seed, hop). */
+int rtec_ns_sample(const rtec_adj_t* in, const int32_t* rows, const int64_t* n_rows, int64_t max_rows,
+                   int32_t fanout, uint64_t seed, int32_t hop, rtec_adj_t* sampled, uint32_t* bm_next,
+                   int64_t n, void* ws, size_t ws_bytes, rtec_stream_t stream);
+/* ascending id list of the set bits of an n-bit bitmap; *count on device */
+int rtec_bitmap_to_list(const uint32_t* bm, int64_t n, int32_t* list, int64_t* count, void* ws, size_t ws_bytes,
+                        rtec_stream_t stream);
+
 /* materialize / query final-layer rows (SPEC materialize_h SPEC.md:379). */
 int rtec_query(const float* H, int64_t d, const int32_t* ids, int64_t k, float* out, int32_t n,
                uint64_t* err, rtec_stream_t stream);

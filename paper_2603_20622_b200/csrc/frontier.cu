@@ -246,3 +246,111 @@ extern "C" int rtec_frontier_layer(const rtec_graph_t* g, const rtec_batch_t* b,
   RTEC_LAUNCH_CHECK("k_counters");
   return RTEC_OK;
 }
+
+// ------------------------------------------------------------------ NS baseline (SPEC.md:464 run_ns)
+// Seeded neighbour sampling without replacement: row v keeps min(len, fanout) of its
+// in-neighbours, chosen by Floyd's algorithm over a counter-hash RNG (seed, hop, v, j),
+// written in ascending order; every kept neighbour and v itself are marked in bm_next
+// (the rows whose embeddings the hop below must provide).
+namespace rtec {
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+struct SampleCount {
+  const int32_t* rows;
+  const int32_t* len;
+  int32_t fanout;
+  __device__ __forceinline__ int64_t operator()(int64_t i) const {
+    int32_t L = len[rows[i]];
+    return L < fanout ? L : fanout;
+  }
+};
+struct SampleBeg {
+  const int32_t* rows;
+  int64_t* beg;
+  int32_t* len;
+  __device__ __forceinline__ void operator()(int64_t i, int64_t off, int64_t v) const {
+    beg[rows[i]] = off;
+    len[rows[i]] = static_cast<int32_t>(v);
+  }
+};
+
+__global__ void __launch_bounds__(kFBlk) k_ns_sample(rtec_adj_t in, const int32_t* __restrict__ rows,
+                                                     const int64_t* n_rows, int64_t max_rows, int32_t fanout,
+                                                     uint64_t seed, int32_t hop, rtec_adj_t smp, uint32_t* bm_next) {
+  const int64_t nr = n_rows ? *n_rows : max_rows;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = lane_id();
+  for (int64_t i = warp; i < nr; i += nw) {
+    const int32_t v = rows[i];
+    const int32_t L = in.len[v];
+    const int64_t b = in.beg[v];
+    const int32_t k = L < fanout ? L : fanout;
+    const int64_t o = smp.beg[v];
+    if (lane == 0) atomicOr(bm_next + (v >> 5), 1u << (v & 31));
+    if (k == L) {  // keep every neighbour
+      for (int32_t j = lane; j < L; j += 32) {
+        int32_t u = in.nbr[b + j];
+        smp.nbr[o + j] = u;
+        atomicOr(bm_next + (u >> 5), 1u << (u & 31));
+      }
+      continue;
+    }
+    // Floyd: for j = L-k .. L-1 draw t in [0, j]; take t unless taken, else j.  Lane q keeps pick q.
+    int32_t pick = -1;
+    for (int32_t q = 0; q < k; ++q) {
+      const int32_t j = L - k + q;
+      const uint64_t h = mix64(seed ^ mix64((static_cast<uint64_t>(hop) << 56) ^ (static_cast<uint64_t>(v) << 24) ^
+                                            static_cast<uint64_t>(j)));
+      const int32_t t = static_cast<int32_t>(h % static_cast<uint64_t>(j + 1));
+      const bool taken = __any_sync(0xffffffffu, lane < q && pick == t);
+      if (lane == q) pick = taken ? j : t;
+    }
+    // ascending order of the picked positions (k <= 32: rank by comparison)
+    int32_t rank = 0;
+    for (int32_t q = 0; q < k; ++q) {
+      int32_t other = __shfl_sync(0xffffffffu, pick, q);
+      if (lane < k && other < pick) ++rank;
+    }
+    if (lane < k) {
+      int32_t u = in.nbr[b + pick];
+      smp.nbr[o + rank] = u;
+      atomicOr(bm_next + (u >> 5), 1u << (u & 31));
+    }
+  }
+}
+
+}  // namespace rtec
+
+extern "C" int rtec_ns_sample(const rtec_adj_t* in, const int32_t* rows, const int64_t* n_rows, int64_t max_rows,
+                              int32_t fanout, uint64_t seed, int32_t hop, rtec_adj_t* sampled, uint32_t* bm_next,
+                              int64_t n, void* ws, size_t ws_bytes, rtec_stream_t stream) {
+  if (fanout < 1 || fanout > 32) {
+    set_error("NS fanout %d outside [1, 32]", fanout);
+    return RTEC_CONFIG_ERROR;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Ws w(ws, ws_bytes);
+  RTEC_CUDA(cudaMemsetAsync(bm_next, 0, sizeof(uint32_t) * ((n + 31) / 32), s));
+  RTEC_TRY(exclusive_scan(SampleCount{rows, in->len, fanout}, Count{n_rows, max_rows}, max_rows,
+                          SampleBeg{rows, sampled->beg, sampled->len}, sampled->top, w, s));
+  k_ns_sample<<<kSMs * 8, kFBlk, 0, s>>>(*in, rows, n_rows, max_rows, fanout, seed, hop, *sampled, bm_next);
+  RTEC_LAUNCH_CHECK("k_ns_sample");
+  return RTEC_OK;
+}
+
+extern "C" int rtec_bitmap_to_list(const uint32_t* bm, int64_t n, int32_t* list, int64_t* count, void* ws,
+                                   size_t ws_bytes, rtec_stream_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Ws w(ws, ws_bytes);
+  const int64_t words = (n + 31) / 32;
+  int64_t* woff = w.alloc<int64_t>(words + 1);
+  RTEC_WS_CHECK(w);
+  return bitmap_to_list(WordPop{bm, nullptr}, words, list, nullptr, count, woff, w, s);
+}

@@ -328,6 +328,9 @@ class RTECEngine:
             if mode == "inc":
                 m.edge_accesses.append(int(c[l, 0]))
                 m.vertex_accesses.append(int(c[l, 1]))
+            elif mode == "ns":  # sampled edges / rows of hop l
+                m.edge_accesses.append(int(self._ns["adj"][l]["top"].item()))
+                m.vertex_accesses.append(int(self._ns["cnt"][l + 1].item()) if l + 1 < self.L else int(c[l, 1]))
             elif mode == "uer":
                 m.edge_accesses.append(int(c[l, 5]))
                 m.vertex_accesses.append(int(c[l, 1]))
@@ -338,27 +341,102 @@ class RTECEngine:
         m.as_vertices = sum(m.v_dst)
         return m
 
+    # ---------------------------------------------------------------- NS baseline
+    def _ns_buffers(self, fanout: int):
+        nb = getattr(self, "_ns", None)
+        if nb is not None and nb["fanout"] >= fanout:
+            return nb
+        n, dev, L = self.n, self.dev, self.L
+        words = (n + 31) // 32
+        zi = lambda k, dt=torch.int32: torch.zeros(max(k, 1), dtype=dt, device=dev)  # noqa: E731
+        zf = lambda *sh: torch.zeros(*sh, dtype=torch.float32, device=dev)  # noqa: E731
+        nb = {"fanout": fanout,
+              "bm": [zi(words) for _ in range(L)], "T": [zi(n) for _ in range(L)],
+              "cnt": [zi(1, torch.int64) for _ in range(L)],
+              "adj": [{"beg": zi(n, torch.int64), "len": zi(n), "nbr": zi(n * fanout), "top": zi(1, torch.int64)}
+                      for _ in range(L)],
+              "H": [None] + [zf(n, d) for d in self.b.dims[1:]],
+              "S": zf(n, max(self.b.agg_dims)),
+              "Z": zf(n, max(self.b.dims[1:])) if self.b.model == GAT else None,
+              "el": zf(n, self.b.heads) if self.b.model == GAT else None,
+              "er": zf(n, self.b.heads) if self.b.model == GAT else None,
+              "ctx": zf(n, self.b.heads) if self.b.model == GAT else None}
+        self._ns = nb
+        return nb
+
+    def _ns_enqueue(self, fanout: int, seed: int) -> None:
+        """SPEC run_ns (§III-B): the final-layer affected vertices of the
+        batch (V_dst(L-1)) recomputed over L-hop in-neighbourhoods sampled without
+        replacement, at most `fanout` per vertex per hop, seeded; approximate by design.  The
+        result overwrites those rows of the final embeddings only (the exact caches are not
+        maintained: run NS on its own engine)."""
+        nb = self._ns_buffers(fanout)
+        lib, p, st = self.lib, _lib.ptr, _lib.stream_handle()
+        gr = self.g
+        ws, wsb = p(gr.ws), gr.ws.numel()
+        n, L = self.n, self.L
+        rows, cnt = self.fr[L - 1].dst_list, self.fr[L - 1].n_dst  # T_L
+        T, C_ = [None] * (L + 1), [None] * (L + 1)
+        T[L], C_[L] = rows, cnt
+        adjs = []
+        for l in range(L - 1, -1, -1):  # sample downwards: T_l = T_{l+1} ∪ sampled in-neighbours
+            a = nb["adj"][l]
+            smp = _lib.Adj(a["nbr"].numel(), p(a["beg"]), p(a["len"]), None, p(a["nbr"]), None, p(a["top"]))
+            inn = gr.inn.c()
+            _lib.check(lib.rtec_ns_sample(C.byref(inn), p(T[l + 1]), p(C_[l + 1]), n, int(fanout),
+                                          C.c_uint64(int(seed) & ((1 << 64) - 1)), l, C.byref(smp), p(nb["bm"][l]),
+                                          n, ws, wsb, st), "ns_sample")
+            _lib.check(lib.rtec_bitmap_to_list(p(nb["bm"][l]), n, p(nb["T"][l]), p(nb["cnt"][l]), ws, wsb, st),
+                       "ns_rows")
+            T[l], C_[l] = nb["T"][l], nb["cnt"][l]
+            adjs.append(smp)
+        adjs.reverse()  # adjs[l] = sampled in-neighbours of T_{l+1}
+        err = torch.full((1,), -1, dtype=torch.int64, device=self.dev)
+        H = [self.H[0]] + nb["H"][1:]
+        for l in range(L):
+            g = gr.c()
+            g.inn = adjs[l]
+            s = self._state(l)
+            s.H_in, s.H_out, s.S = p(H[l]), p(H[l + 1]), p(nb["S"])
+            s.log_out = s.log_in = None
+            if self.b.model == GAT:
+                s.Z, s.el, s.er, s.ctx = p(nb["Z"]), p(nb["el"]), p(nb["er"]), p(nb["ctx"])
+                _lib.check(lib.rtec_gat_project(C.byref(self.layers[l]), p(H[l]), p(T[l]), p(C_[l]), n, p(nb["Z"]),
+                                                p(nb["el"]), p(nb["er"]), None, None, p(err), st), "ns_project")
+            _lib.check(lib.rtec_layer_full(C.byref(g), C.byref(self.layers[l]), C.byref(s), p(T[l + 1]),
+                                           p(C_[l + 1]), n, p(err), ws, wsb, st), "ns_layer")
+        k = int(cnt.item())
+        if k:
+            idx = rows[:k].to(torch.int64)
+            self.H[L][idx] = H[L][idx]
+
+    def run_ns(self, batch, fanout: int = 10, seed: int = 0) -> RunResult:
+        """SPEC run_ns on a coalesced EdgeUpdate list."""
+        return self.step(*updates_to_arrays(list(batch)), mode="ns", fanout=fanout, seed=seed)
+
     def run_uer(self, batch) -> RunResult:
         """SPEC run_uer: affected rows over their full in-neighbourhoods."""
         return self.step(*updates_to_arrays(list(batch)), mode="uer")
 
-    def step(self, op, src, dst, ts, mode: str = "inc") -> RunResult:
+    def step(self, op, src, dst, ts, mode: str = "inc", fanout: int = 10, seed: int = 0) -> RunResult:
         """One batch on array inputs: mode 'inc' = run_incremental, 'uer' =
         run_uer, 'full' = apply + run_full.  One host
         synchronisation at the end reads the per-update status, DegreeDelta rows and
         counters from pinned buffers."""
-        if mode not in ("inc", "uer", "full"):
-            raise E.ConfigError(f"unknown engine mode {mode!r} (inc, uer, full)")
+        if mode not in ("inc", "uer", "full", "ns"):
+            raise E.ConfigError(f"unknown engine mode {mode!r} (inc, uer, full, ns)")
         B = self.g.stage(op, src, dst, ts)
         for attempt in range(4):
             if mode == "inc":
                 self.enqueue_step(B)
             else:
                 self._ensure_ws(self.g.batch.cap)
-                # 'full': apply + the frontier (for the access counters), then every layer
+                # 'full' / 'ns': apply + the frontier (access counters, affected final rows)
                 self._enqueue_eager(B, mode="uer" if mode == "uer" else "frontier")
                 if mode == "full":
                     self.bootstrap(sync=False)
+                elif mode == "ns":
+                    self._ns_enqueue(fanout, seed)
             hb = self._readback(B)
             word = int(hb["err"][0]) & _lib.ERR_OK
             d = _lib.decode_err(word)

@@ -256,3 +256,39 @@ def test_uer_and_full_modes_match_oracle(P, model, dims):
         assert inc.edge_accesses[l] <= uer.edge_accesses[l] <= full.edge_accesses[l]
     rep = P.redundancy(inc, full.edge_accesses[0], n)
     assert rep["inc_over_as"] == 1.0 and rep["fn_over_as"] >= rep["uer_over_as"] >= 1.0
+
+
+def test_ns_baseline(P):
+    # SPEC run_ns: fanout >= max in-degree reproduces the exact recompute of
+    # the affected final rows; a small fanout is approximate but bit-stable under a seed
+    from oracle import models as OM
+    from oracle.engine import OracleEngine
+    from oracle.graph import OracleGraph
+    from paper_2603_20622_b200.workload import UpdateStream, chung_lu_edges, features
+
+    n, m = 600, 2400
+    s, d = chung_lu_edges(n, m, alpha=0.0, seed=20)  # uniform: in-degrees well below the fanout
+    X = features(n, 16, seed=6)
+    stream = UpdateStream(s, d, holdout=0.1, seed=20)
+    bs, bd, bt = stream.base()
+    batch = stream.next_batch(40)
+    maxdeg = int(np.bincount(np.concatenate([bd, batch[2]]), minlength=n).max())
+    assert maxdeg <= 32
+    for model in ("gcn", "graphsage", "gin", "gat"):
+        eng = P.RTECEngine(P.make_bundle(model, [16, 16, 8]), P.DynamicGraph.from_edges(n, (bs, bd, bt)), X)
+        oe = OracleEngine(OM.make_bundle(model, [16, 16, 8]), OracleGraph.from_edges(n, bs, bd, bt),
+                          X.astype(np.float64))
+        r = eng.step(*batch, mode="ns", fanout=32)
+        oe.step(*batch)
+        rows = eng.frontier(1)[0]
+        assert rowwise_rel(eng.embeddings(2)[rows], oe.H[2][rows]) <= TOL, model
+        assert r.metrics.edge_accesses[1] > 0
+    # determinism and fanout bound
+    outs = []
+    for _ in range(2):
+        eng = P.RTECEngine(P.make_bundle("gcn", [16, 16, 8]), P.DynamicGraph.from_edges(n, (bs, bd, bt)), X)
+        eng.step(*batch, mode="ns", fanout=2, seed=7)
+        outs.append(eng.embeddings(2))
+        lens = eng._ns["adj"][1]["len"].cpu().numpy()
+        assert lens.max() <= 2
+    assert np.array_equal(outs[0], outs[1])
