@@ -225,9 +225,9 @@ def run_ours(args, world, rank, local):
     K, W = args.steps, args.warmup
     E2E = args.e2e_steps if args.e2e_steps is not None else min(K, 10)
     PROF = min(K, 10)  # eager profiled pass after the timed region (per-kernel CUDA events)
-    NB = 0 if (world > 1 or args.no_baselines) else 3  # batches per GPU baseline mode (UER, Full)
+    NB = 0 if (world > 1 or args.no_baselines) else 3  # batches per GPU baseline mode (UER, Full, NS)
     t0 = time.time()
-    stream, batches, X = make_workload(wl, W + K + PROF + E2E + 2 * NB, dev)
+    stream, batches, X = make_workload(wl, W + K + PROF + E2E + 3 * NB, dev)
     bs, bd, bt = stream.base()
     bundle = P.make_bundle(wl["model"], wl["dims"], heads=wl["heads"])
     sharded = world > 1
@@ -339,9 +339,10 @@ def run_ours(args, world, rank, local):
         e2e_val = sum_over_ranks(e2e_upd, world) / e2e_s
     # --- the paper's comparison set on the same GPU and stream: the same
     # public step() with the affected rows recomputed over full in-neighbourhoods (UER) and
-    # every layer recomputed (RTEC-Full); per-batch time incl. H2D / D2H like `e2e`
+    # every layer recomputed (RTEC-Full), and NS (fanout 10, approximate); per-batch time incl.
+    # H2D / D2H like `e2e`.  NS runs last: it leaves the exact caches stale by design.
     baselines = {}
-    for bi, mode in enumerate(("uer", "full")[: 2 if NB else 0]):
+    for bi, mode in enumerate(("uer", "full", "ns")[: 3 if NB else 0]):
         ms, ups, acc = [], 0, 0
         for j in range(NB):
             op, s, d, t = batches[W + K + PROF + E2E + bi * NB + j]
@@ -350,7 +351,7 @@ def run_ours(args, world, rank, local):
             torch.cuda.synchronize()
             a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a_ev.record()
-            r = eng.step(*hb, mode=mode)
+            r = eng.step(*hb, mode=mode, fanout=10)
             b_ev.record()
             torch.cuda.synchronize()
             ms.append(a_ev.elapsed_time(b_ev))
