@@ -246,6 +246,38 @@ struct AggOcc {
   static constexpr int value = (VEC * K <= 8) ? 4 : 2;
 };
 
+// acc += rows 0..nch-1 (stride `stride` floats, width w) in row order, 4 rows in flight:
+// the last-arriving warp of a hub reduces up to ~10^3 chunk partials
+template <int VEC, int K>
+__device__ __forceinline__ void sum_partials(const float* part, int64_t stride, int w, int32_t nch,
+                                             RowAcc<VEC, K>& acc) {
+  int32_t cc = 0;
+  for (; cc + 4 <= nch; cc += 4) {
+    float r[4][K][VEC];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int col = lane_id() + 32 * k;
+#pragma unroll
+        for (int jj = 0; jj < VEC; ++jj)
+          r[u][k][jj] = (col * VEC < w) ? __ldcg(part + (cc + u) * stride + col * VEC + jj) : 0.f;
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc.add(r[u]);
+  }
+  for (; cc < nch; ++cc) {
+    float r[K][VEC];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int col = lane_id() + 32 * k;
+#pragma unroll
+      for (int jj = 0; jj < VEC; ++jj) r[k][jj] = (col * VEC < w) ? __ldcg(part + cc * stride + col * VEC + jj) : 0.f;
+    }
+    acc.add(r);
+  }
+}
+
 template <int VEC, int K, bool FULL>
 __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_light(LayerArgs a, AggRows rows) {
   using R = RowAcc<VEC, K>;
@@ -324,17 +356,7 @@ __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_heavy(Laye
     if (old != nch - 1) continue;
     __threadfence();
     acc.zero();
-    for (int32_t cc = 0; cc < nch; ++cc) {  // chunk order: deterministic sum
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        int col = lane_id() + 32 * k;
-        if (col * VEC < cw) {
-          const float* src = hp.part + (c0 + cc) * cw + col * VEC;
-#pragma unroll
-          for (int jj = 0; jj < VEC; ++jj) acc.v[k][jj] += __ldcg(src + jj);
-        }
-      }
-    }
+    sum_partials<VEC, K>(hp.part + c0 * cw, cw, cw, nch, acc);  // chunk order: deterministic sum
     agg_finalize<VEC, K, FULL>(a, i, v, len, acc);
   }
 }
@@ -481,6 +503,25 @@ __device__ __forceinline__ void max_neg_inf(RowAcc<VEC, K>& acc) {
   for (int k = 0; k < K; ++k)
 #pragma unroll
     for (int j = 0; j < VEC; ++j) acc.v[k][j] = -INFINITY;
+}
+
+// acc = max(acc, chunk partial rows 0..nch-1), 4 rows in flight
+template <int VEC, int K>
+__device__ __forceinline__ void max_partials(const float* part, int d, int32_t nch, RowAcc<VEC, K>& acc) {
+  for (int32_t cc = 0; cc < nch; cc += 4) {
+    float r[4][K][VEC];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int col = lane_id() + 32 * k;
+#pragma unroll
+        for (int jj = 0; jj < VEC; ++jj)
+          r[u][k][jj] = (cc + u < nch && col * VEC < d) ? __ldcg(part + (cc + u) * d + col * VEC + jj) : -INFINITY;
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) max_row<VEC, K>(r[u], acc);
+  }
 }
 
 // max over the current rows of in-run positions [e0, e1), 4 rows in flight
@@ -721,17 +762,7 @@ __global__ void __launch_bounds__(kLBlk) k_max_heavy(LayerArgs a, AggRows rows, 
       continue;
     }
     max_neg_inf<VEC, K>(acc);
-    for (int32_t cc = 0; cc < nch; ++cc) {
-      float r[K][VEC];
-      const float* src = hp.part + (c0 + cc) * d;
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        int col = lane_id() + 32 * k;
-#pragma unroll
-        for (int jj = 0; jj < VEC; ++jj) r[k][jj] = (col * VEC < d) ? __ldcg(src + col * VEC + jj) : -INFINITY;
-      }
-      max_row<VEC, K>(r, acc);
-    }
+    max_partials<VEC, K>(hp.part + c0 * d, d, nch, acc);
     if (!FULL && had) max_row<VEC, K>(sv, acc);
     max_finalize<VEC, K>(a, i, v, len, acc);
   }
@@ -767,17 +798,7 @@ __global__ void __launch_bounds__(kLBlk) k_max_rescan(LayerArgs a, AggRows rows,
     if (old != nch - 1) continue;
     __threadfence();
     max_neg_inf<VEC, K>(acc);
-    for (int32_t cc = 0; cc < nch; ++cc) {
-      float r[K][VEC];
-      const float* src = rq.part + (c0 + cc) * d;
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        int col = lane_id() + 32 * k;
-#pragma unroll
-        for (int jj = 0; jj < VEC; ++jj) r[k][jj] = (col * VEC < d) ? __ldcg(src + col * VEC + jj) : -INFINITY;
-      }
-      max_row<VEC, K>(r, acc);
-    }
+    max_partials<VEC, K>(rq.part + c0 * d, d, nch, acc);
     max_finalize<VEC, K>(a, i, v, len, acc);
   }
 }
@@ -1093,17 +1114,13 @@ __global__ void __launch_bounds__(kLBlk, 4) k_gat_heavy(LayerArgs a, AggRows row
     acc.zero();
 #pragma unroll
     for (int k = 0; k < K; ++k) cacc[k] = 0.f;
-    for (int32_t cc = 0; cc < nch; ++cc) {  // chunk order: deterministic sum
-      const float* src = hp.part + (c0 + cc) * pw;
+    sum_partials<VEC, K>(hp.part + c0 * pw, pw, d, nch, acc);  // chunk order: deterministic sum
+#pragma unroll 4
+    for (int32_t cc = 0; cc < nch; ++cc) {
+      const float* src = hp.part + (c0 + cc) * pw + d;
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        int col = lane_id() + 32 * k;
-        if (col * VEC < d) {
-#pragma unroll
-          for (int jj = 0; jj < VEC; ++jj) acc.v[k][jj] += __ldcg(src + col * VEC + jj);
-          cacc[k] += __ldcg(src + d + chunk_head<VEC>(k, dh));
-        }
-      }
+      for (int k = 0; k < K; ++k)
+        if (R::has(k, d)) cacc[k] += __ldcg(src + chunk_head<VEC>(k, dh));
     }
     gat_finalize<VEC, K, FULL>(a, i, v, len, recompute, acc, cacc);
   }
