@@ -95,7 +95,7 @@ class RTECEngine:
     FUSED_DELTA = True
 
     def __init__(self, bundle: Bundle, graph: DynamicGraph, features, *, max_batch: int | None = None,
-                 update: str = "tc", use_graphs: bool = True):
+                 update: str = "tc", use_graphs: bool = True, bootstrap: bool = True):
         if not isinstance(bundle, Bundle) or bundle.model not in MODELS:
             raise E.UnsupportedModel("engine needs a bundle from paper_2603_20622_b200.models")
         self.b = bundle
@@ -169,7 +169,8 @@ class RTECEngine:
             self.gemm_mid = z(n, max(dims[1:])) if bundle.model in GIN_FAMILY else None
         self.fr = [_Frontier(n, self.dev) for _ in range(self.L)]
         self._ensure_ws(max_batch or graph.batch.cap)
-        self.bootstrap()
+        if bootstrap:  # (formats.load_checkpoint restores the state instead)
+            self.bootstrap()
 
     # ---------------------------------------------------------------- plumbing
     def _prep_weights(self, W, d_in, d_out):
@@ -210,6 +211,28 @@ class RTECEngine:
                                                 _lib.ptr(err), _lib.ptr(self.g.ws), self.g.ws.numel(), st), "bootstrap")
         if sync:
             _lib.raise_err(err.item(), "bootstrap")
+
+    def refresh_projection(self, l: int) -> None:
+        """GAT: Z = W h, el, er of every vertex of layer l from H^l (after a restore)."""
+        if self.b.model != GAT:
+            return
+        p = _lib.ptr
+        _lib.check(self.lib.rtec_gat_project(C.byref(self.layers[l]), p(self.H[l]), None, None, self.n, p(self.Z[l]),
+                                             p(self.el[l]), p(self.er[l]), None, None, None, _lib.stream_handle()),
+                   "gat_project")
+
+    def save(self, directory: str) -> None:
+        """Checkpoint between batches (formats.save_checkpoint)."""
+        from .formats import save_checkpoint
+
+        save_checkpoint(self, directory)
+
+    @staticmethod
+    def load(directory: str, **kw) -> "RTECEngine":
+        """Resume from a checkpoint without a bootstrap (formats.load_checkpoint)."""
+        from .formats import load_checkpoint
+
+        return load_checkpoint(directory, **kw)
 
     def run_full(self, batch=None) -> RunResult | None:
         """SPEC run_full: without a batch, recompute every layer on the

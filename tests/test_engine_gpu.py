@@ -292,3 +292,29 @@ def test_ns_baseline(P):
         lens = eng._ns["adj"][1]["len"].cpu().numpy()
         assert lens.max() <= 2
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("model,heads", [("gcn", 1), ("gat", 2)])
+def test_checkpoint_resume(P, model, heads, tmp_path):
+    # save between batches, resume without a bootstrap, continue: identical to never stopping
+    from paper_2603_20622_b200.workload import UpdateStream, chung_lu_edges, features
+
+    n = 2000
+    s, d = chung_lu_edges(n, 20000, seed=25)
+    stream = UpdateStream(s, d, holdout=0.2, seed=25)
+    bs, bd, bt = stream.base()
+    X = features(n, 16, seed=7)
+    eng = P.RTECEngine(P.make_bundle(model, [16, 16, 16], heads=heads), P.DynamicGraph.from_edges(n, (bs, bd, bt)), X)
+    for _ in range(2):
+        eng.step(*stream.next_batch(200))
+    eng.save(str(tmp_path / "ck"))
+    eng2 = P.RTECEngine.load(str(tmp_path / "ck"))
+    assert np.array_equal(eng.embeddings(2), eng2.embeddings(2))
+    for _ in range(2):
+        b = stream.next_batch(200)
+        r1, r2 = eng.step(*b), eng2.step(*b)
+        assert np.array_equal(r1.status, r2.status)
+    assert rowwise_rel(eng2.embeddings(2), eng.embeddings(2)) <= 1e-6
+    s1, s2 = eng.g.edges(), eng2.g.edges()
+    for a, b in zip(s1, s2):
+        assert np.array_equal(a, b)
