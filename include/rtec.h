@@ -181,12 +181,20 @@ typedef struct {
   float* delta;
   float* delta_next;
   int32_t delta_ready;
-  int32_t pad_;
+  /* Sharded state: rows of S / ctx (and of H_out when out_local) are
+   * stored per owned vertex at v / row_div (owner(v) = v mod row_div); delta_slot: δ rows
+   * indexed by the source's slot in S(l) (frontier src_slot) instead of by vertex, so the
+   * δ buffer holds |S(l)| rows.  0 / 0 / 0: unsharded, vertex-indexed. */
+  int32_t row_div;
+  int32_t out_local;
+  int32_t delta_slot;
 } rtec_state_t;
 
 /* ---- workspace ---- */
 /* per-batch calls (apply / frontier / layers); m_slots bounds the in-place merge scratch */
 size_t rtec_workspace_bytes(int64_t n, int64_t max_batch, int64_t m_slots, int32_t max_dim);
+/* the same without the [n, max_dim] δ region (callers that pass state.delta) */
+size_t rtec_workspace_bytes_ext(int64_t n, int64_t max_batch, int64_t m_slots, int32_t max_dim);
 /* bulk build / compaction of m edges */
 size_t rtec_build_workspace_bytes(int64_t n, int64_t m);
 

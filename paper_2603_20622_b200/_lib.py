@@ -69,12 +69,14 @@ class State(C.Structure):
     _fields_ = [
         ("H_in", P), ("H_out", P), ("S", P), ("ctx", P), ("log_out", P), ("log_in", P),
         ("Z", P), ("el", P), ("er", P), ("Z_log", P), ("er_log", P), ("gemm_in", P), ("gemm_mid", P),
-        ("delta", P), ("delta_next", P), ("delta_ready", I32), ("pad_", I32),
+        ("delta", P), ("delta_next", P), ("delta_ready", I32), ("row_div", I32), ("out_local", I32),
+        ("delta_slot", I32),
     ]
 
 
 _SIGS = {
     "rtec_workspace_bytes": (SZ, [I64, I64, I64, I32]),
+    "rtec_workspace_bytes_ext": (SZ, [I64, I64, I64, I32]),
     "rtec_build_workspace_bytes": (SZ, [I64, I64]),
     "rtec_graph_count": (C.c_int, [P, P, I64, I64, P, P, P, P]),
     "rtec_graph_slots_needed": (C.c_int, [P, I64, F32, I32, P, P, SZ, P]),

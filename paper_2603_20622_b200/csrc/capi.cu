@@ -18,7 +18,17 @@ extern "C" {
 // Workspace for every per-batch call: max over batch apply (sorts + merge
 // plans + in-place merge scratch), frontier (lists) and layer (δ rows).
 // `m_slots` bounds the in-place merge scratch (touched run lengths).
+static size_t workspace_bytes(int64_t n, int64_t max_batch, int64_t m_slots, int32_t max_dim, bool delta_in_ws);
+
 size_t rtec_workspace_bytes(int64_t n, int64_t max_batch, int64_t m_slots, int32_t max_dim) {
+  return workspace_bytes(n, max_batch, m_slots, max_dim, true);
+}
+
+size_t rtec_workspace_bytes_ext(int64_t n, int64_t max_batch, int64_t m_slots, int32_t max_dim) {
+  return workspace_bytes(n, max_batch, m_slots, max_dim, false);
+}
+
+static size_t workspace_bytes(int64_t n, int64_t max_batch, int64_t m_slots, int32_t max_dim, bool delta_in_ws) {
   int64_t scr = 64 * max_batch + (1 << 20);
   if (scr > m_slots + max_batch) scr = m_slots + max_batch;
   if (scr < (1 << 16)) scr = 1 << 16;
@@ -26,7 +36,7 @@ size_t rtec_workspace_bytes(int64_t n, int64_t max_batch, int64_t m_slots, int32
   size_t f = frontier_ws_bytes(n);
   // layer: δ rows [n, d] + heavy-destination plan (lists, chunk map, partial rows)
   int64_t chunks = m_slots / 512 + 2 + n / 64;
-  size_t l = static_cast<size_t>(n) * static_cast<size_t>(max_dim) * sizeof(float) +
+  size_t l = (delta_in_ws ? static_cast<size_t>(n) * static_cast<size_t>(max_dim) * sizeof(float) : 0) +
              static_cast<size_t>(n) * 40 + static_cast<size_t>(chunks) * (4 + 4 * static_cast<size_t>(max_dim + 8)) +
              sizeof(int64_t) * (scan_blocks_for(n) + 2) * 4 + (1 << 20);
   size_t r = b > f ? b : f;

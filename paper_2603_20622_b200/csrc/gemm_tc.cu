@@ -320,7 +320,8 @@ __global__ void __launch_bounds__(512, 1) k_gemm_tc(TcArgs g, TcShape sh) {
       const int64_t tile = blockIdx.x + t * gridDim.x;
       const int64_t i = tile * kTM + r;
       const bool valid = i < nrows;
-      const int64_t dst = valid ? (g.y_rows ? static_cast<int64_t>(g.y_rows[i]) : i) : -1;
+      const int64_t dst =
+          valid ? (g.y_rows ? static_cast<int64_t>(g.y_rows[i]) : i) / (g.ydiv > 1 ? g.ydiv : 1) : -1;
       const int64_t row0 = tile * kTM + wq * 32;  // first row of this warp
       if (g.log && !g.Yt) {
         // DeltaLog capture of this tile's rows (this warp's column half) does not

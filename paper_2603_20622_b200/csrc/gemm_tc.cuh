@@ -27,6 +27,7 @@ struct TcArgs {
   const int32_t* deg_old;
   int coeff_gcn;
   float deg_off;
+  int ydiv;  // > 1: Y rows stored per owned vertex at y_rows[i] / ydiv (sharded final layer)
 };
 
 int gemm_tc_launch(const TcArgs& g, cudaStream_t s);

@@ -59,6 +59,18 @@ struct LayerArgs {
   uint64_t* err;
 };
 
+// row of v in S / ctx (and in H_out when out_local): per owned vertex when sharded
+__device__ __forceinline__ int64_t srow(const LayerArgs& a, int32_t v) {
+  return a.st.row_div > 1 ? static_cast<int64_t>(v / a.st.row_div) : static_cast<int64_t>(v);
+}
+__device__ __forceinline__ int64_t hrow(const LayerArgs& a, int32_t v) {
+  return (a.st.out_local && a.st.row_div > 1) ? static_cast<int64_t>(v / a.st.row_div) : static_cast<int64_t>(v);
+}
+// row of source u in the δ buffer: its S(l) slot when slot-indexed
+__device__ __forceinline__ int64_t drow(const LayerArgs& a, int32_t u) {
+  return a.st.delta_slot ? static_cast<int64_t>(a.f.src_slot[u]) : static_cast<int64_t>(u);
+}
+
 // ------------------------------------------------------------------ δ rows (K10)
 template <int VEC, int K>
 __global__ void __launch_bounds__(kLBlk) k_src_delta(LayerArgs a, float* delta) {
@@ -85,7 +97,8 @@ __global__ void __launch_bounds__(kLBlk) k_src_delta(LayerArgs a, float* delta) 
       acc.fma(hn, cn);
       acc.fma(ho, -co);
     }
-    acc.store(delta + static_cast<int64_t>(u) * d, d);  // indexed by vertex: no slot gather per edge
+    // indexed by vertex (no slot gather per edge) unless the sharded δ buffer is slot-indexed
+    acc.store(delta + (a.st.delta_slot ? i : static_cast<int64_t>(u)) * d, d);
   }
 }
 
@@ -128,7 +141,8 @@ __device__ __forceinline__ void agg_edges(const LayerArgs& a, int64_t beg, int32
     }
     unsigned m = __ballot_sync(0xffffffffu, hit);
     const float* base = (FULL ? a.st.H_in : a.delta) + a.c0;
-    int32_t row = u;
+    // gathered row: the source's own row (H_in, vertex-indexed δ) or its δ slot
+    int32_t row = (!FULL && hit && a.st.delta_slot) ? a.f.src_slot[u] : u;
     while (m) {
       int32_t rw[UNR];
       float cs[UNR];
@@ -171,7 +185,7 @@ __device__ __forceinline__ void agg_struct(const LayerArgs& a, int64_t p, int64_
       acc.fma(r, src_coeff(a.L.model, a.g.out_deg[u], a.L.degree_offset));
     } else if (a.st.delta_ready && a.prev_bm_dst && bm_test(a.prev_bm_dst, u)) {
       // -c_old h_old(u) = δ_u - c_new h_new(u)  (fused deltas: no DeltaLog)
-      R::load(a.delta + static_cast<int64_t>(u) * d + a.c0, cw, r);
+      R::load(a.delta + drow(a, u) * d + a.c0, cw, r);
       acc.add(r);
       R::load(a.st.H_in + static_cast<int64_t>(u) * d + a.c0, cw, r);
       acc.fma(r, -fused_coeff(a.L.model, a.g.out_deg[u], a.L.degree_offset));
@@ -192,7 +206,7 @@ __device__ __forceinline__ void agg_finalize(const LayerArgs& a, int64_t i, int3
                                              int32_t pre_indeg = 0) {
   using R = RowAcc<VEC, K>;
   const int d = a.d_agg, cw = a.cw;
-  float* srow = a.st.S + static_cast<int64_t>(v) * d + a.c0;
+  float* sp = a.st.S + srow(a, v) * d + a.c0;
   int32_t indeg = FULL ? len : (pre ? pre_indeg : a.g.in_deg[v]);
   if (!FULL) {
     if (indeg == 0) {
@@ -201,11 +215,11 @@ __device__ __forceinline__ void agg_finalize(const LayerArgs& a, int64_t i, int3
       acc.add(pre->v);
     } else if (a.g.in_deg_prev[v] > 0) {
       float sv[K][VEC];
-      R::load_stream(srow, cw, sv, l2_evict_first_policy());
+      R::load_stream(sp, cw, sv, l2_evict_first_policy());
       acc.add(sv);
     }
   }
-  acc.store_stream(srow, cw, l2_evict_first_policy());
+  acc.store_stream(sp, cw, l2_evict_first_policy());
   float scale = 1.f;
   if (indeg > 0) {
     if (a.L.model == RTEC_MODEL_GCN) scale = 1.0f / sqrtf(static_cast<float>(indeg) + a.L.degree_offset);
@@ -308,7 +322,7 @@ __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_light(Laye
     R sv;
     sv.zero();
     if (!FULL && indeg > 0 && had > 0)
-      R::load_stream(a.st.S + static_cast<int64_t>(v) * a.d_agg + a.c0, a.cw, sv.v, l2_evict_first_policy());
+      R::load_stream(a.st.S + srow(a, v) * a.d_agg + a.c0, a.cw, sv.v, l2_evict_first_policy());
     R acc;
     acc.zero();
     if (scan) agg_edges<VEC, K, FULL>(a, beg, 0, len, p, q, acc);
@@ -632,7 +646,7 @@ __device__ __forceinline__ void max_finalize(const LayerArgs& a, int64_t i, int3
   using R = RowAcc<VEC, K>;
   const int d = a.d_agg;
   if (len == 0) acc.zero();
-  acc.store(a.st.S + static_cast<int64_t>(v) * d, d);
+  acc.store(a.st.S + srow(a, v) * d, d);
   R out;
   out.zero();
   out.add(acc.v);
@@ -678,7 +692,7 @@ __global__ void __launch_bounds__(kLBlk) k_max_light(LayerArgs a, AggRows rows) 
       int2 pq = irange_of(a, v);
       const bool had = a.g.in_deg_prev[v] > 0;
       float sv[K][VEC];
-      R::load_rw(a.st.S + static_cast<int64_t>(v) * d, d, sv);
+      R::load_rw(a.st.S + srow(a, v) * d, d, sv);
       bool retract = max_incremental<VEC, K>(a, beg, 0, len, pq.x, pq.y, true, sv, acc);
       rescan = had && retract;
       if (!rescan && had) max_row<VEC, K>(sv, acc);
@@ -735,7 +749,7 @@ __global__ void __launch_bounds__(kLBlk) k_max_heavy(LayerArgs a, AggRows rows, 
     } else {
       int2 pq = irange_of(a, v);
       had = a.g.in_deg_prev[v] > 0;
-      R::load_rw(a.st.S + static_cast<int64_t>(v) * d, d, sv);
+      R::load_rw(a.st.S + srow(a, v) * d, d, sv);
       bool retract = max_incremental<VEC, K>(a, beg, e0, e1, pq.x, pq.y, c == 0, sv, acc);
       if (retract && had && lane_id() == 0) atomicOr(rq.flag + j, 1);
     }
@@ -989,11 +1003,11 @@ __device__ __forceinline__ void gat_finalize(const LayerArgs& a, int64_t i, int3
   const int lane = lane_id();
   if (!recompute && a.g.in_deg_prev[v] > 0 && a.g.in_deg[v] > 0) {
     float sv[K][VEC];
-    R::load_rw(a.st.S + static_cast<int64_t>(v) * d, d, sv);
+    R::load_rw(a.st.S + srow(a, v) * d, d, sv);
     acc.add(sv);
 #pragma unroll
     for (int k = 0; k < K; ++k)
-      if (R::has(k, d)) cacc[k] += a.st.ctx[static_cast<int64_t>(v) * H + chunk_head<VEC>(k, dh)];
+      if (R::has(k, d)) cacc[k] += a.st.ctx[srow(a, v) * H + chunk_head<VEC>(k, dh)];
   }
   int32_t indeg = recompute ? len : a.g.in_deg[v];
   if (indeg == 0) {
@@ -1001,14 +1015,14 @@ __device__ __forceinline__ void gat_finalize(const LayerArgs& a, int64_t i, int3
 #pragma unroll
     for (int k = 0; k < K; ++k) cacc[k] = 0.f;
   }
-  acc.store(a.st.S + static_cast<int64_t>(v) * d, d);
+  acc.store(a.st.S + srow(a, v) * d, d);
 #pragma unroll
   for (int k = 0; k < K; ++k) {  // ctx per head: written by the lane holding the head's first chunk
     int c = lane + 32 * k;
     if (c * VEC < d && (c * VEC) % dh == 0)
-      for (int hh = 0; hh < (VEC > dh ? VEC / dh : 1); ++hh) a.st.ctx[static_cast<int64_t>(v) * H + (c * VEC) / dh + hh] = cacc[k];
+      for (int hh = 0; hh < (VEC > dh ? VEC / dh : 1); ++hh) a.st.ctx[srow(a, v) * H + (c * VEC) / dh + hh] = cacc[k];
   }
-  float* hrow = a.st.H_out + static_cast<int64_t>(v) * d;
+  float* hrow = a.st.H_out + ::rtec::hrow(a, v) * d;
   if (!FULL && a.st.log_out) {
     float old[K][VEC];
     R::load_rw(hrow, d, old);
@@ -1208,6 +1222,7 @@ struct GemmArgs {
   float* Y; int64_t ldy; const int32_t* y_rows;
   float* log;
   const uint64_t* err;  // skip when the batch failed validation / reservation
+  int ydiv;             // > 1: Y row of y_rows[i] is y_rows[i] / ydiv (sharded final layer)
 };
 
 constexpr int kGM = 64, kGN = 64, kGK = 16;
@@ -1259,7 +1274,7 @@ __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs g) {
   for (int r = 0; r < 4; ++r) {
     int64_t gr = row0 + ty * 4 + r;
     if (gr >= nr) continue;
-    int64_t dst = g.y_rows ? g.y_rows[gr] : gr;
+    int64_t dst = (g.y_rows ? g.y_rows[gr] : gr) / (g.ydiv > 1 ? g.ydiv : 1);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       int col = col0 + tx * 4 + c;
@@ -1322,6 +1337,7 @@ static int layer_dims_ok(const rtec_layer_t* L) {
 
 static int run_update(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* st, const int64_t* n_rows,
                       int64_t max_rows, const int32_t* y_rows, float* log, const uint64_t* err, cudaStream_t s) {
+  const int ydiv = (st->out_local && st->row_div > 1) ? st->row_div : 1;
   auto fuse = [&](TcArgs& t) {  // the next layer's source deltas from this update's epilogue
     if (!st->delta_next || !y_rows || (L->d_out & 3)) return;
     t.delta_next = st->delta_next;
@@ -1340,11 +1356,13 @@ static int run_update(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t
       RTEC_TRY(gemm_tc_launch(t1, s));
       TcArgs t2{st->gemm_mid, L->W2t_hi, L->W2t_lo, nkb2, tc_npad_of(L->d_out), L->d_out, n_rows, max_rows, 0,
                 st->H_out, L->d_out, y_rows, log, nullptr, 0, err};
+      t2.ydiv = ydiv;
       fuse(t2);
       return gemm_tc_launch(t2, s);
     }
     TcArgs t{st->gemm_in, L->Wt_hi, L->Wt_lo, nkb, tc_npad_of(L->d_out), L->d_out, n_rows, max_rows, 1,
              st->H_out, L->d_out, y_rows, log, nullptr, 0, err};
+    t.ydiv = ydiv;
     fuse(t);
     return gemm_tc_launch(t, s);
   }
@@ -1353,11 +1371,11 @@ static int run_update(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t
                 st->gemm_mid, L->d_out, nullptr, nullptr, err};
     RTEC_TRY(gemm_launch(g1, s));
     GemmArgs g2{st->gemm_mid, L->d_out, nullptr, L->W2, L->d_out, L->d_out, n_rows, max_rows, 0,
-                st->H_out, L->d_out, y_rows, log, err};
+                st->H_out, L->d_out, y_rows, log, err, ydiv};
     return gemm_launch(g2, s);
   }
   GemmArgs g1{st->gemm_in, L->d_in, nullptr, L->W, L->d_in, L->d_out, n_rows, max_rows, 1,
-              st->H_out, L->d_out, y_rows, log, err};
+              st->H_out, L->d_out, y_rows, log, err, ydiv};
   return gemm_launch(g1, s);
 }
 

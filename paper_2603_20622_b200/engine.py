@@ -120,6 +120,7 @@ class RTECEngine:
         self.S, self.ctx, self.log = [], [], []
         self.Z, self.el, self.er, self.Zlog, self.erlog = [], [], [], [], []
         heads = bundle.heads
+        no = self._rows_owned()  # rows of the destination-side state (all n unless sharded)
         # tcgen05 3xTF32 update (gemm_tc.cu) for every dense update with d_out <= 256
         self.tc = update == "tc" and bundle.model != GAT and max(dims[1:]) <= 256
         # sum aggregators on the tcgen05 path: the update epilogue of layer l writes the source
@@ -143,12 +144,13 @@ class RTECEngine:
                                           float(bundle.degree_offset), 0, p(W), p(W2), p(att),
                                           p(tcw[0]), p(tcw[1]), p(tcw[2]), p(tcw[3])))
             d_agg = bundle.agg_dims[l]
-            self.H.append(z(n, d_out))
-            self.S.append(z(n, d_agg))
-            # DeltaLog of this layer's output; the final layer's is never read (no layer L+1)
-            self.log.append(z(n, d_out) if l + 1 < bundle.num_layers and not self.fused else None)
+            # layer inputs are read for every source: full rows; the final output only per owner
+            self.H.append(z(n if l + 1 < bundle.num_layers else no, d_out))
+            self.S.append(z(no, d_agg))
+            # DeltaLog of this layer's output (rows = V_dst slots); the final layer's is never read
+            self.log.append(z(no, d_out) if l + 1 < bundle.num_layers and not self.fused else None)
             if bundle.model == GAT:
-                self.ctx.append(z(n, heads))
+                self.ctx.append(z(no, heads))
                 self.Z.append(z(n, d_out))
                 self.el.append(z(n, heads))
                 self.er.append(z(n, heads))
@@ -159,20 +161,24 @@ class RTECEngine:
                 for lst in (self.Z, self.el, self.er, self.Zlog, self.erlog):
                     lst.append(None)
         self.max_dim = max(max(dims), 1)
-        if self.tc:  # SW128 tile image: ceil(n/128)*128 rows x ceil(d/32)*32 columns
-            rows = (n + 127) // 128 * 128
+        if self.tc:  # SW128 tile image: ceil(rows/128)*128 rows x ceil(d/32)*32 columns
+            rows = (no + 127) // 128 * 128
             pad = lambda d: (d + 31) // 32 * 32  # noqa: E731
             self.gemm_in = z(rows * pad(max(bundle.agg_dims)))
             self.gemm_mid = z(rows * pad(max(dims[1:]))) if bundle.model in GIN_FAMILY else None
         else:
-            self.gemm_in = z(n, max(bundle.agg_dims)) if bundle.model != GAT else None
-            self.gemm_mid = z(n, max(dims[1:])) if bundle.model in GIN_FAMILY else None
+            self.gemm_in = z(no, max(bundle.agg_dims)) if bundle.model != GAT else None
+            self.gemm_mid = z(no, max(dims[1:])) if bundle.model in GIN_FAMILY else None
         self.fr = [_Frontier(n, self.dev) for _ in range(self.L)]
         self._ensure_ws(max_batch or graph.batch.cap)
         if bootstrap:  # (formats.load_checkpoint restores the state instead)
             self.bootstrap()
 
     # ---------------------------------------------------------------- plumbing
+    def _rows_owned(self) -> int:
+        """Rows of the destination-side state (S, ctx, final H, DeltaLog, GEMM input)."""
+        return self.n
+
     def _prep_weights(self, W, d_in, d_out):
         nkb, npad = (d_in + 31) // 32, (d_out + 15) // 16 * 16
         hi = torch.zeros(nkb * npad * 32, dtype=torch.float32, device=self.dev)

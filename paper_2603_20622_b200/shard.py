@@ -141,10 +141,34 @@ class ShardedRTECEngine(RTECEngine):
         g.out_deg, g.out_deg_prev = _lib.ptr(self.gout), _lib.ptr(self.gout_prev)
         return g
 
+    def _rows_owned(self) -> int:
+        # owner(v) = v mod P: rank r owns r, r + P, ...; its rows sit at v // P
+        P, r = self.comm.world, self.comm.rank
+        return max((self.n - r + P - 1) // P, 0)
+
+    def _ensure_ws(self, B):
+        # the δ rows live in per-layer buffers sized |S(l)| (slot-indexed), not in the workspace
+        need = int(self.lib.rtec_workspace_bytes_ext(self.n, max(int(B), 1),
+                                                     max(self.g.out.slots, self.g.inn.slots), self.max_dim))
+        if self.g.ws.numel() < need:
+            self.g.ws = torch.empty(need, dtype=torch.uint8, device=self.dev)
+
+    def _delta_buffer(self, l: int, rows: int) -> torch.Tensor:
+        if not hasattr(self, "_dbuf"):
+            self._dbuf = [torch.zeros(1, dtype=torch.float32, device=self.dev) for _ in range(self.L)]
+        need = max(rows, 1) * int(self.b.agg_dims[l])
+        if self._dbuf[l].numel() < need:
+            self._dbuf[l] = torch.zeros(int(need * 1.25), dtype=torch.float32, device=self.dev)
+        return self._dbuf[l]
+
     def _state(self, l, incremental: bool = False):
         s = super()._state(l, incremental)
         if l > 0:
             s.log_in = _lib.ptr(self.glog[l - 1]) if len(self.glog) >= l else None
+        # destination-side rows per owned vertex (v // P); δ rows per S(l) slot
+        s.row_div = self.comm.world
+        s.out_local = 1 if l + 1 == self.L else 0
+        s.delta_slot = 1
         return s
 
     def _chg_buffers(self, l):
@@ -199,16 +223,22 @@ class ShardedRTECEngine(RTECEngine):
                                         p(f.chg_list), p(f.n_chg), st), "halo_unpack")
 
     # ---------------------------------------------------------------- bootstrap
-    def bootstrap(self):
-        """Full forward (models.py:461-477): every rank evaluates all rows over its
-        shard (owned rows are exact), then the owners' rows refresh the replicas."""
+    def bootstrap(self, sync: bool = True):
+        """Full forward (models.py:461-477) of the owned rows over this rank's shard,
+        then the owners' rows refresh the replicas."""
         err = torch.full((1,), -1, dtype=torch.int64, device=self.dev)
         st = _lib.stream_handle()
+        p = _lib.ptr
         for l in range(self.L):
             g = self._mg()
             s = self._state(l)
-            _lib.check(self.lib.rtec_layer_full(C.byref(g), C.byref(self.layers[l]), C.byref(s), None, None, self.n,
-                                                _lib.ptr(err), _lib.ptr(self.g.ws), self.g.ws.numel(), st), "bootstrap")
+            if self.b.model == GAT:  # Z / el / er of every (replica) row feed the owned rows' softmax
+                _lib.check(self.lib.rtec_gat_project(C.byref(self.layers[l]), p(self.H[l]), None, None, self.n,
+                                                     p(self.Z[l]), p(self.el[l]), p(self.er[l]), None, None, None,
+                                                     st), "bootstrap")
+            _lib.check(self.lib.rtec_layer_full(C.byref(g), C.byref(self.layers[l]), C.byref(s), p(self.owned),
+                                                p(self.n_owned), self.owned.numel(), p(err), p(self.g.ws),
+                                                self.g.ws.numel(), st), "bootstrap")
             if l + 1 < self.L:
                 self._exchange(self.H[l + 1], self.b.dims[l + 1], self.owned, self.owned.numel())
         _lib.raise_err(err.item(), "bootstrap")
@@ -274,6 +304,7 @@ class ShardedRTECEngine(RTECEngine):
                                                 self.n, p(self.Z[l]), p(self.el[l]), p(self.er[l]), p(self.Zlog[l]),
                                                 p(self.erlog[l]), p(bb.err), st), "gat_project")
             s = self._state(l)
+            s.delta = p(self._delta_buffer(l, int(self.fr[l].n_src.item())))  # |S(l)| δ rows
             _lib.check(lib.rtec_layer_incremental(C.byref(g), C.byref(b), C.byref(self.layers[l]), C.byref(s), prev,
                                                   C.byref(fc[l]), p(bb.err), ws, wsb, st), "layer")
             if l + 1 < self.L:
@@ -316,7 +347,8 @@ class ShardedRTECEngine(RTECEngine):
         d = self.H[l].shape[1]
         full = torch.zeros(self.n, d, dtype=torch.float32, device=self.dev)
         idx = self.owned.to(torch.int64)
-        full[idx] = self.H[l][idx]
+        # the final layer is stored per owned vertex (row v // P); inputs are full replicas
+        full[idx] = self.H[l][: idx.numel()] if l == self.L else self.H[l][idx]
         self.comm.all_reduce_(full)
         return full.cpu().numpy()
 
@@ -336,8 +368,11 @@ class ShardedRTECEngine(RTECEngine):
         if ids_np.size and (ids_np.min() < 0 or ids_np.max() >= self.n):
             raise E.InvalidVertex("query vertex outside the vertex range")
         ids_t = torch.as_tensor(ids_np, device=self.dev)
-        out = self.H[-1][ids_t].clone() if ids_np.size else torch.zeros(0, self.b.dims[-1], device=self.dev)
-        out[owner_of(ids_t, self.comm.world) != self.comm.rank] = 0
+        P = self.comm.world
+        mine = owner_of(ids_t, P) == self.comm.rank
+        out = torch.zeros(ids_np.size, self.b.dims[-1], dtype=torch.float32, device=self.dev)
+        if ids_np.size:
+            out[mine] = self.H[-1][ids_t[mine] // P]  # owned rows at v // P
         self.comm.all_reduce_(out)
         return out.cpu().numpy()
 
