@@ -432,6 +432,24 @@ static int agg_slice_width() {
   return w;
 }
 
+// library-owned side stream + fork/join events for independent passes of one layer
+// (created once per process; used on the current device)
+static cudaStream_t side_stream() {
+  static cudaStream_t st = nullptr;
+  if (!st) cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  return st;
+}
+static cudaEvent_t side_fork() {
+  static cudaEvent_t e = nullptr;
+  if (!e) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  return e;
+}
+static cudaEvent_t side_join() {
+  static cudaEvent_t e = nullptr;
+  if (!e) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  return e;
+}
+
 // heavy-destination plan (list, chunk offsets, chunk -> heavy map); partial rows of `pw` floats
 template <bool FULL>
 static int plan_heavy(const LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_edges, int pw, Ws& w,
@@ -475,15 +493,27 @@ static int launch_aggregation(LayerArgs& a, AggRows rows, int64_t max_rows, int6
     a.cw = sw > 0 ? (d - c0 < sw ? d - c0 : sw) : d;
     if (c0 > 0) RTEC_CUDA(cudaMemsetAsync(hp.arrive, 0, sizeof(int32_t) * (max_rows + 1), s));
     const bool sliced = a.cw <= 64;
-    {
-      RTEC_PROF(FULL ? "k_agg_full_light" : "k_agg_inc", s);
-      ok = sliced ? RTEC_SLICE_DISPATCH(a.cw, (k_agg_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows)))
-                  : RTEC_ROW_DISPATCH(a.cw, (k_agg_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows)));
+    // The hub chunks (heavy) touch other destinations than the light pass: run them on a
+    // side stream so each pass fills the other's tail (a fork / join the CUDA graph keeps).
+    // Not while profiling (per-kernel events need the passes apart).
+    cudaStream_t hs = g_prof_on ? s : side_stream();
+    if (hs != s) {
+      RTEC_CUDA(cudaEventRecord(side_fork(), s));
+      RTEC_CUDA(cudaStreamWaitEvent(hs, side_fork(), 0));
     }
     {
-      RTEC_PROF(FULL ? "k_agg_full_heavy" : "k_agg_inc_heavy", s);
-      ok = ok && (sliced ? RTEC_SLICE_DISPATCH(a.cw, (k_agg_heavy<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows, hp)))
-                         : RTEC_ROW_DISPATCH(a.cw, (k_agg_heavy<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows, hp))));
+      RTEC_PROF(FULL ? "k_agg_full_heavy" : "k_agg_inc_heavy", hs);
+      ok = (sliced ? RTEC_SLICE_DISPATCH(a.cw, (k_agg_heavy<VEC, K, FULL><<<grid, kLBlk, 0, hs>>>(a, rows, hp)))
+                   : RTEC_ROW_DISPATCH(a.cw, (k_agg_heavy<VEC, K, FULL><<<grid, kLBlk, 0, hs>>>(a, rows, hp))));
+    }
+    {
+      RTEC_PROF(FULL ? "k_agg_full_light" : "k_agg_inc", s);
+      ok = ok && (sliced ? RTEC_SLICE_DISPATCH(a.cw, (k_agg_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows)))
+                         : RTEC_ROW_DISPATCH(a.cw, (k_agg_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows))));
+    }
+    if (hs != s) {
+      RTEC_CUDA(cudaEventRecord(side_join(), hs));
+      RTEC_CUDA(cudaStreamWaitEvent(s, side_join(), 0));
     }
   }
   if (!ok) {
