@@ -298,10 +298,31 @@ class RTECEngine:
         sdd = 1 if self.b.src_degree_dependent else 0
         self._fc = [f.c() for f in self.fr]
         self._sc = [self._state(l, incremental=True) for l in range(self.L)]
+        # The frontier of layer l+1 needs only layer l's frontier, not its embeddings: layers
+        # 1..L-1's frontiers run on a side stream (own workspace) under layer 0's compute and
+        # each layer waits for its frontier (a fork / join the CUDA graph keeps).
+        overlap = mode != "frontier" and self.L > 1
+        main = torch.cuda.current_stream()
+        _lib.check(self.lib.rtec_frontier_layer(C.byref(g), C.byref(b), 0, sdd, None, C.byref(self._fc[0]), ws, wsb,
+                                                st), "frontier")
+        if overlap:  # fork after layer 0's frontier
+            fws = self._frontier_ws()
+            side, evs = self._side()
+            evs[0].record(main)
+            side.wait_event(evs[0])
+            with torch.cuda.stream(side):
+                for l in range(1, self.L):
+                    _lib.check(self.lib.rtec_frontier_layer(C.byref(g), C.byref(b), l, sdd, C.byref(self._fc[l - 1]),
+                                                            C.byref(self._fc[l]), _lib.ptr(fws), fws.numel(),
+                                                            side.cuda_stream), "frontier")
+                    evs[l].record(side)
         for l in range(self.L):
             prev = C.byref(self._fc[l - 1]) if l > 0 else None
-            _lib.check(self.lib.rtec_frontier_layer(C.byref(g), C.byref(b), l, sdd, prev, C.byref(self._fc[l]), ws, wsb,
-                                                    st), "frontier")
+            if l > 0 and not overlap:
+                _lib.check(self.lib.rtec_frontier_layer(C.byref(g), C.byref(b), l, sdd, prev, C.byref(self._fc[l]), ws,
+                                                        wsb, st), "frontier")
+            elif l > 0:
+                main.wait_event(self._side()[1][l])
             if mode == "frontier":
                 continue
             if self.b.model == GAT and l > 0:
@@ -321,6 +342,18 @@ class RTECEngine:
                                                            C.byref(self._sc[l]), prev, C.byref(self._fc[l]), errp, ws,
                                                            wsb, st), "layer")
         _lib.check(self.lib.rtec_batch_commit(C.byref(g), C.byref(b), st), "commit")
+
+    def _side(self):
+        if getattr(self, "_side_stream", None) is None:
+            self._side_stream = torch.cuda.Stream(device=self.dev)
+            self._side_events = [torch.cuda.Event() for _ in range(self.L)]
+        return self._side_stream, self._side_events
+
+    def _frontier_ws(self) -> torch.Tensor:
+        need = int(self.n) * 24 + (1 << 20)  # list + offsets + word offsets + scan partials
+        if getattr(self, "_fws", None) is None or self._fws.numel() < need:
+            self._fws = torch.empty(need, dtype=torch.uint8, device=self.dev)
+        return self._fws
 
     def _readback(self, B: int):
         """Queue the batch's results into pinned host buffers (one sync for all of them)."""
