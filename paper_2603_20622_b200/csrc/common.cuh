@@ -50,6 +50,14 @@ struct ProfScope {
 };
 #define RTEC_PROF(name, stream) ::rtec::ProfScope _rtec_prof_scope_##__LINE__(name, stream)
 
+// ---------------------------------------------------------------- side stream
+// Library-owned side stream + fork / join events for independent passes inside one
+// call (created once per process, on the device current at first use).  Fork and join
+// are event records / waits, so a CUDA-graph capture of the caller's stream keeps them.
+cudaStream_t side_stream();
+cudaEvent_t side_fork();
+cudaEvent_t side_join();
+
 // ---------------------------------------------------------------- workspace
 // Bump allocator over the caller's workspace; every chunk 256-B aligned.
 struct Ws {

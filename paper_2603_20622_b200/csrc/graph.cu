@@ -893,8 +893,18 @@ int rtec_batch_apply_phase(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src,
   k_apply_degrees<<<grid, kBlk, 0, s>>>(b->a_src, b->a_dst, b->a_op, b->n_applied, g->out_deg, g->in_deg,
                                         g->num_edges, b->err);
   int64_t work_bound = g->out.slots + B;  // grid-stride loops read the real totals on device
-  RTEC_TRY(merge_exec(mo, po, g->out, work_bound, b->err, s));
+  // the two directions touch disjoint arrays (own plans and scratch): merge them concurrently
+  cudaStream_t ms = g_prof_on ? s : side_stream();
+  if (ms != s) {
+    RTEC_CUDA(cudaEventRecord(side_fork(), s));
+    RTEC_CUDA(cudaStreamWaitEvent(ms, side_fork(), 0));
+  }
+  RTEC_TRY(merge_exec(mo, po, g->out, work_bound, b->err, ms));
   RTEC_TRY(merge_exec(mi, pi, g->in, work_bound, b->err, s));
+  if (ms != s) {
+    RTEC_CUDA(cudaEventRecord(side_join(), ms));
+    RTEC_CUDA(cudaStreamWaitEvent(s, side_join(), 0));
+  }
   // 9. DegreeDelta rows: unique endpoints of applied updates whose degrees changed
   k_touched_keys<<<grid, kBlk, 0, s>>>(b->a_src, b->a_dst, b->n_applied, keys, vals, cnt2);
   RTEC_TRY(sort_pairs(keys, vals, sk, sv, Count{cnt2, B2}, B2, bits_for(static_cast<uint64_t>(n)), w, s));

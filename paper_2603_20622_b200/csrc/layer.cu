@@ -432,24 +432,6 @@ static int agg_slice_width() {
   return w;
 }
 
-// library-owned side stream + fork/join events for independent passes of one layer
-// (created once per process; used on the current device)
-static cudaStream_t side_stream() {
-  static cudaStream_t st = nullptr;
-  if (!st) cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-  return st;
-}
-static cudaEvent_t side_fork() {
-  static cudaEvent_t e = nullptr;
-  if (!e) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-  return e;
-}
-static cudaEvent_t side_join() {
-  static cudaEvent_t e = nullptr;
-  if (!e) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-  return e;
-}
-
 // heavy-destination plan (list, chunk offsets, chunk -> heavy map); partial rows of `pw` floats
 template <bool FULL>
 static int plan_heavy(const LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_edges, int pw, Ws& w,

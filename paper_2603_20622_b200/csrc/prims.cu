@@ -80,6 +80,23 @@ std::string prof_report(bool reset) {
   return out;
 }
 
+// ---------------------------------------------------------------- side stream
+cudaStream_t side_stream() {
+  static cudaStream_t st = nullptr;
+  if (!st) cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  return st;
+}
+cudaEvent_t side_fork() {
+  static cudaEvent_t e = nullptr;
+  if (!e) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  return e;
+}
+cudaEvent_t side_join() {
+  static cudaEvent_t e = nullptr;
+  if (!e) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  return e;
+}
+
 // ---------------------------------------------------------------- scan
 __global__ void __launch_bounds__(kScanBlock) k_scan_blocks(int64_t* bs, int64_t nb, int64_t* total) {
   __shared__ int64_t sw[kScanBlock / 32];
