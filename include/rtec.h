@@ -321,6 +321,10 @@ int rtec_halo_unpack(const rtec_graph_t* g, int32_t d, const int32_t* recv_ids, 
 int rtec_ns_sample(const rtec_adj_t* in, const int32_t* rows, const int64_t* n_rows, int64_t max_rows,
                    int32_t fanout, uint64_t seed, int32_t hop, rtec_adj_t* sampled, uint32_t* bm_next,
                    int64_t n, void* ws, size_t ws_bytes, rtec_stream_t stream);
+/* ODEC: bm |= rows ∪ in-neighbours(rows) -- one level of the queries'
+ * L-hop in-subgraph */
+int rtec_in_expand(const rtec_adj_t* in, const int32_t* rows, const int64_t* n_rows, int64_t max_rows, uint32_t* bm,
+                   rtec_stream_t stream);
 /* ascending id list of the set bits of an n-bit bitmap; *count on device */
 int rtec_bitmap_to_list(const uint32_t* bm, int64_t n, int32_t* list, int64_t* count, void* ws, size_t ws_bytes,
                         rtec_stream_t stream);

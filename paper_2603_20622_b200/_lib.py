@@ -101,6 +101,7 @@ _SIGS = {
     "rtec_query": (C.c_int, [P, I64, P, I64, P, I32, P, P]),
     "rtec_ns_sample": (C.c_int, [C.POINTER(Adj), P, P, I64, I32, C.c_uint64, I32, C.POINTER(Adj), P, I64, P, SZ, P]),
     "rtec_bitmap_to_list": (C.c_int, [P, I64, P, P, P, SZ, P]),
+    "rtec_in_expand": (C.c_int, [C.POINTER(Adj), P, P, I64, P, P]),
     "rtec_gemm_prepare_weights": (C.c_int, [P, I32, I32, P, P, P]),
     "rtec_struct_sizes": (None, [C.POINTER(I64)]),
     "rtec_prof_enable": (None, [C.c_int]),

@@ -354,3 +354,34 @@ extern "C" int rtec_bitmap_to_list(const uint32_t* bm, int64_t n, int32_t* list,
   RTEC_WS_CHECK(w);
   return bitmap_to_list(WordPop{bm, nullptr}, words, list, nullptr, count, woff, w, s);
 }
+
+// ------------------------------------------------------------------ ODEC (SPEC.md:473 run_odec)
+// bm_out |= rows ∪ in-neighbours(rows): one level of the queries' L-hop in-subgraph.
+namespace rtec {
+__global__ void __launch_bounds__(kFBlk) k_in_expand(rtec_adj_t in, const int32_t* __restrict__ rows,
+                                                     const int64_t* n_rows, int64_t max_rows, uint32_t* bm) {
+  const int64_t nr = n_rows ? *n_rows : max_rows;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < nr; i += nw) {
+    const int32_t v = rows[i];
+    if (lane_id() == 0) atomicOr(bm + (v >> 5), 1u << (v & 31));
+    const int64_t b = in.beg[v];
+    const int32_t L = in.len[v];
+    for (int32_t j0 = 0; j0 < L; j0 += 32) {
+      const int32_t j = j0 + lane_id();
+      const bool act = j < L;
+      bm_set_warp(bm, act ? in.nbr[b + j] : 0, act);
+    }
+  }
+}
+}  // namespace rtec
+
+extern "C" int rtec_in_expand(const rtec_adj_t* in, const int32_t* rows, const int64_t* n_rows, int64_t max_rows,
+                              uint32_t* bm, rtec_stream_t stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (max_rows <= 0) return RTEC_OK;
+  k_in_expand<<<kSMs * 8, kFBlk, 0, s>>>(*in, rows, n_rows, max_rows, bm);
+  RTEC_LAUNCH_CHECK("k_in_expand");
+  return RTEC_OK;
+}

@@ -390,6 +390,9 @@ class RTECEngine:
             if mode == "inc":
                 m.edge_accesses.append(int(c[l, 0]))
                 m.vertex_accesses.append(int(c[l, 1]))
+            elif mode == "odec":  # deferred: no layer work at batch time
+                m.edge_accesses.append(0)
+                m.vertex_accesses.append(0)
             elif mode == "ns":  # sampled edges / rows of hop l
                 m.edge_accesses.append(int(self._ns["adj"][l]["top"].item()))
                 m.vertex_accesses.append(int(self._ns["cnt"][l + 1].item()) if l + 1 < self.L else int(c[l, 1]))
@@ -476,6 +479,98 @@ class RTECEngine:
         """SPEC run_ns on a coalesced EdgeUpdate list."""
         return self.step(*updates_to_arrays(list(batch)), mode="ns", fanout=fanout, seed=seed)
 
+    # ---------------------------------------------------------------- ODEC (query-driven)
+    def _odec_state(self):
+        if getattr(self, "_stale", None) is None:
+            words = (self.n + 31) // 32
+            z = lambda: torch.zeros(max(words, 1), dtype=torch.int32, device=self.dev)  # noqa: E731
+            self._stale = [z() for _ in range(self.L)]  # rows of H^{l+1} / S^l whose cache is out of date
+            self._need = [z() for _ in range(self.L)]
+            self._rows = torch.zeros(max(self.n, 1), dtype=torch.int32, device=self.dev)
+            self._nrows = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        return self._stale
+
+    def odec_flush(self) -> None:
+        """Recompute every deferred row (then any engine mode may follow)."""
+        if getattr(self, "_stale", None) is None:
+            return
+        lib, p, st = self.lib, _lib.ptr, _lib.stream_handle()
+        gr = self.g
+        err = torch.full((1,), -1, dtype=torch.int64, device=self.dev)
+        prev = None
+        for l in range(self.L):
+            if self.b.model == GAT and l > 0 and prev is not None:
+                _lib.check(lib.rtec_gat_project(C.byref(self.layers[l]), p(self.H[l]), p(prev[0]), p(prev[1]),
+                                                self.n, p(self.Z[l]), p(self.el[l]), p(self.er[l]), None, None, None,
+                                                st), "odec")
+            rows = torch.empty(max(self.n, 1), dtype=torch.int32, device=self.dev)
+            nrows = torch.zeros(1, dtype=torch.int64, device=self.dev)
+            _lib.check(lib.rtec_bitmap_to_list(p(self._stale[l]), self.n, p(rows), p(nrows), p(gr.ws), gr.ws.numel(),
+                                               st), "odec")
+            _lib.check(lib.rtec_layer_full(C.byref(gr.c()), C.byref(self.layers[l]), C.byref(self._state(l)), p(rows),
+                                           p(nrows), self.n, p(err), p(gr.ws), gr.ws.numel(), st), "odec")
+            self._stale[l].zero_()
+            prev = (rows, nrows)
+        _lib.raise_err(err.item(), "odec_flush")
+
+    def stale_rows(self, l: int) -> int:
+        """ODEC: vertices whose layer-l output is deferred (cache out of date)."""
+        st = self._odec_state()[l]
+        return int(torch.bitwise_count(st.view(torch.int32)).sum().item()) if hasattr(torch, "bitwise_count") \
+            else int(sum(bin(int(w) & 0xFFFFFFFF).count("1") for w in st.cpu().tolist()))
+
+    def _mark(self, bm: torch.Tensor, ids: torch.Tensor) -> None:
+        """bm |= bits of the (device) ids."""
+        u = torch.unique(ids.to(torch.int64))
+        w = torch.zeros(bm.numel(), dtype=torch.int64, device=self.dev)
+        w.index_add_(0, u >> 5, torch.ones_like(u) << (u & 31))  # distinct bits: add == or
+        bm |= w.to(torch.int32)
+
+    def odec_query(self, ids) -> np.ndarray:
+        """SPEC run_odec (§V-D): fresh final-layer rows of `ids`.
+        Batches applied with mode 'odec' only mark the affected rows of every layer as
+        deferred; a query recomputes, bottom-up, the deferred rows inside the queries' L-hop
+        in-subgraph over their full post-batch in-neighbourhoods, clears their staleness and
+        returns H^L[ids] -- equal to a full recomputation on the current graph."""
+        stale = self._odec_state()
+        ids_np = np.asarray(ids, np.int64).reshape(-1)
+        if ids_np.size and (ids_np.min() < 0 or ids_np.max() >= self.n):
+            raise E.InvalidVertex("query vertex outside the vertex range")
+        if ids_np.size == 0:
+            return np.zeros((0, self.b.dims[-1]), np.float32)
+        lib, p, st = self.lib, _lib.ptr, _lib.stream_handle()
+        gr = self.g
+        inn = gr.inn.c()
+        L, n = self.L, self.n
+        q = torch.as_tensor(ids_np.astype(np.int32), device=self.dev)
+        # need[l]: rows whose layer-l output the queries depend on; need[l-1] = need[l] ∪ in-nbrs
+        for b in self._need:
+            b.zero_()
+        self._mark(self._need[L - 1], q)
+        for l in range(L - 1, 0, -1):
+            _lib.check(lib.rtec_bitmap_to_list(p(self._need[l]), n, p(self._rows), p(self._nrows), p(gr.ws),
+                                               gr.ws.numel(), st), "odec")
+            _lib.check(lib.rtec_in_expand(C.byref(inn), p(self._rows), p(self._nrows), n, p(self._need[l - 1]), st),
+                       "odec")
+        err = torch.full((1,), -1, dtype=torch.int64, device=self.dev)
+        prev_rows = None
+        for l in range(L):  # bottom-up over the deferred rows the queries need
+            if self.b.model == GAT and l > 0 and prev_rows is not None:  # fresh H^l rows: fresh projections
+                _lib.check(lib.rtec_gat_project(C.byref(self.layers[l]), p(self.H[l]), p(prev_rows[0]),
+                                                p(prev_rows[1]), n, p(self.Z[l]), p(self.el[l]), p(self.er[l]), None,
+                                                None, None, st), "odec")
+            todo = stale[l] & self._need[l]
+            rows = torch.empty(max(n, 1), dtype=torch.int32, device=self.dev)
+            nrows = torch.zeros(1, dtype=torch.int64, device=self.dev)
+            _lib.check(lib.rtec_bitmap_to_list(p(todo), n, p(rows), p(nrows), p(gr.ws), gr.ws.numel(), st), "odec")
+            s_full = self._state(l)
+            _lib.check(lib.rtec_layer_full(C.byref(gr.c()), C.byref(self.layers[l]), C.byref(s_full), p(rows),
+                                           p(nrows), n, p(err), p(gr.ws), gr.ws.numel(), st), "odec")
+            stale[l] &= ~todo
+            prev_rows = (rows, nrows)
+        _lib.raise_err(err.item(), "odec_query")
+        return self.H[L][q.to(torch.int64)].cpu().numpy()
+
     def run_uer(self, batch) -> RunResult:
         """SPEC run_uer: affected rows over their full in-neighbourhoods."""
         return self.step(*updates_to_arrays(list(batch)), mode="uer")
@@ -485,8 +580,10 @@ class RTECEngine:
         run_uer, 'full' = apply + run_full.  One host
         synchronisation at the end reads the per-update status, DegreeDelta rows and
         counters from pinned buffers."""
-        if mode not in ("inc", "uer", "full", "ns"):
-            raise E.ConfigError(f"unknown engine mode {mode!r} (inc, uer, full, ns)")
+        if mode not in ("inc", "uer", "full", "ns", "odec"):
+            raise E.ConfigError(f"unknown engine mode {mode!r} (inc, uer, full, ns, odec)")
+        if mode != "odec" and getattr(self, "_stale", None) is not None and any(int(b.any()) for b in self._stale):
+            raise E.StaleState("deferred (ODEC) rows pending: call odec_flush() before another mode")
         B = self.g.stage(op, src, dst, ts)
         for attempt in range(4):
             if mode == "inc":
@@ -499,6 +596,10 @@ class RTECEngine:
                     self.bootstrap(sync=False)
                 elif mode == "ns":
                     self._ns_enqueue(fanout, seed)
+                elif mode == "odec":  # defer: the affected rows of every layer become stale
+                    stale = self._odec_state()
+                    for l in range(self.L):
+                        stale[l] |= self.fr[l].bm_dst
             hb = self._readback(B)
             word = int(hb["err"][0]) & _lib.ERR_OK
             d = _lib.decode_err(word)

@@ -318,3 +318,48 @@ def test_checkpoint_resume(P, model, heads, tmp_path):
     s1, s2 = eng.g.edges(), eng2.g.edges()
     for a, b in zip(s1, s2):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("model,dims,heads", [("gcn", [24, 32, 16], 1), ("graphsage", [24, 32, 16], 1),
+                                              ("gin", [16, 16, 16, 16], 1), ("gat", [24, 32, 32], 2),
+                                              ("gin_max", [16, 24, 16], 1)])
+def test_odec_queries_match_full_recompute(P, model, dims, heads):
+    # SPEC run_odec: batches only mark deferred rows; a query recomputes the
+    # deferred part of its L-hop in-subgraph and returns rows equal to a full recompute;
+    # interleaved queries leave partially fresh caches that later queries must respect
+    from oracle import models as OM
+    from oracle.engine import OracleEngine
+    from oracle.graph import OracleGraph
+    from paper_2603_20622_b200.workload import UpdateStream, chung_lu_edges, features
+
+    n = 2500
+    s, d = chung_lu_edges(n, 25000, seed=31)
+    stream = UpdateStream(s, d, holdout=0.15, seed=31)
+    bs, bd, bt = stream.base()
+    X = features(n, dims[0], seed=9)
+    L = len(dims) - 1
+    eng = P.RTECEngine(P.make_bundle(model, dims, heads=heads), P.DynamicGraph.from_edges(n, (bs, bd, bt)), X)
+    oe = OracleEngine(OM.make_bundle(model, dims, heads=heads), OracleGraph.from_edges(n, bs, bd, bt),
+                      X.astype(np.float64))
+    rng = np.random.default_rng(3)
+    for i in range(4):
+        batch = stream.next_batch(200)
+        r = eng.step(*batch, mode="odec")
+        o = oe.step(*batch)
+        assert np.array_equal(r.status, o["status"])
+        assert sum(r.metrics.edge_accesses) == 0
+        assert eng.stale_rows(L - 1) > 0
+        ids = np.concatenate([rng.integers(0, n, 40), o["frontier"][L - 1]["vdst"][:20]])
+        got = eng.odec_query(ids)
+        assert rowwise_rel(got, oe.H[L][ids]) <= TOL, (i, model)
+        assert np.array_equal(eng.odec_query(ids), got)  # now fresh: a second query is a no-op
+    eng.odec_flush()
+    assert all(eng.stale_rows(l) == 0 for l in range(L))
+    for l in range(1, L + 1):
+        assert rowwise_rel(eng.embeddings(l), oe.H[l]) <= TOL, l
+    batch = stream.next_batch(200)  # incremental mode resumes from the flushed caches
+    eng.step(*batch)
+    oe.step(*batch)
+    assert rowwise_rel(eng.embeddings(L), oe.H[L]) <= TOL
+    with pytest.raises(P.InvalidVertex):
+        eng.odec_query([n])
