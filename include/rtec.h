@@ -52,7 +52,15 @@ enum { RTEC_OP_INSERT = 0, RTEC_OP_DELETE = 1 };
 /* models (models.py:42-52); the hot-path four, plus GIN with an elementwise
  * max aggregator (configs[3]; no reference counterpart -- retract-and-recompute
  * per destination) */
-enum { RTEC_MODEL_GCN = 0, RTEC_MODEL_SAGE = 1, RTEC_MODEL_GIN = 2, RTEC_MODEL_GAT = 3, RTEC_MODEL_GIN_MAX = 4 };
+enum { RTEC_MODEL_GCN = 0, RTEC_MODEL_SAGE = 1, RTEC_MODEL_GIN = 2, RTEC_MODEL_GAT = 3, RTEC_MODEL_GIN_MAX = 4,
+       /* the rest of Table II (models.py:144-348):
+        *   PINSAGE  payload alpha relu(Q h_u + q), mean, update relu(W [h_v ; a_v])
+        *   MONET    scalar payload exp(0.5 (h_u-mu)^T Wq (h_u-mu)), sum, update relu(W a)
+        *   COMMNET  sum of h_u, update W h_v + W2 a_v
+        *   GGCN     dest-dependent sigmoid(Wg_src h_u + Wg_dst h_v) * h_u, sum, relu(W a)
+        *   AGNN     dest-dependent beta cos(h_u, h_v) h_u, sum, relu(W a) */
+       RTEC_MODEL_PINSAGE = 5, RTEC_MODEL_MONET = 6, RTEC_MODEL_COMMNET = 7, RTEC_MODEL_GGCN = 8,
+       RTEC_MODEL_AGNN = 9 };
 
 /* One direction of the adjacency: gapped per-vertex runs.  Run of v is
  * nbr[beg[v] .. beg[v]+len[v]) ascending, with cap[v] >= len[v] slots reserved.
@@ -151,6 +159,14 @@ typedef struct {
    * the SW128 tile image: ceil(rows/128)*128 x ceil(d/32)*32 floats. */
   const float* Wt_hi; const float* Wt_lo;
   const float* W2t_hi; const float* W2t_lo;
+  /* per-source projection of the payload / gate models (rtec_project):
+   *   PINSAGE Q [d_in, d_in] + bias q;  MONET symmetrised Wq [d_in, d_in] + mean mu;
+   *   GGCN [Wg_src ; Wg_dst] [2 d_in, d_in] (no bias).  NULL for the other models. */
+  const float* Wp;
+  const float* bp;
+  float scalar;        /* PINSAGE alpha (models.py:151), AGNN beta (models.py:322) */
+  int32_t d_k;         /* update GEMM input width: 2 d_in for PINSAGE / COMMNET ([h_v ; a_v]), 1 for
+                          MONET, d_in otherwise (0 = d_in).  W is [d_out, d_k]; COMMNET W = [W | W2]. */
 } rtec_layer_t;
 
 /* Per-layer cached state (SPEC.md:355-419 state_cache; stored un-normalised):
@@ -159,14 +175,16 @@ typedef struct {
  *   H_out [n, d_out] layer output; H_in = previous layer's output (or X)
  *   log_out [n_dst cap, d_out] DeltaLog: pre-batch H_out rows of V_dst(l),
  *            indexed by frontier.dst_slot
- *   GAT caches for the layer: Z [n, d_out] = W h, el/er [n, heads]. */
+ *   GAT caches for the layer: Z [n, d_out] = W h, el/er [n, heads].
+ *   PINSAGE / MONET / GGCN: Z = the rtec_project payload rows, Z_log their
+ *   pre-batch values for V_chg(l-1) (indexed by the previous dst_slot). */
 typedef struct {
   const float* H_in;   float* H_out;
   float* S;            float* ctx;
   float* log_out;      /* DeltaLog rows of this layer's output */
   const float* log_in; /* previous layer's DeltaLog (NULL for layer 0); rows indexed by
                           the previous frontier's dst_slot, membership = its bm_dst */
-  float* Z; float* el; float* er;           /* GAT caches */
+  float* Z; float* el; float* er;           /* GAT caches (Z: projected payloads of the Table II models) */
   float* Z_log; float* er_log;              /* GAT DeltaLog of Z/er rows of V_chg(l-1) */
   float* gemm_in;      /* [n_dst cap, max(d_agg,d_in)] scratch: composed rows fed to the update GEMM */
   float* gemm_mid;     /* [n_dst cap, d_out] GIN hidden */
@@ -270,6 +288,16 @@ int rtec_layer_full(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* 
 int rtec_gat_project(const rtec_layer_t* L, const float* H, const int32_t* rows, const int64_t* n_rows,
                      int64_t n_or_max_rows, float* Z, float* el, float* er,
                      float* Z_log, float* er_log, const uint64_t* err, rtec_stream_t stream);
+
+/* Per-source projections of the payload / gate models for all vertices
+ * (rows == NULL) or the listed rows (V_chg(l-1) before layer l):
+ *   PINSAGE P = alpha relu(Q h + q)             [n, d_in]   (models.py:157-159)
+ *   MONET   P = exp(0.5 (h-mu)^T Wq (h-mu))     [n, 1]      (models.py:211-213)
+ *   GGCN    P = [Wg_src h ; Wg_dst h]           [n, 2 d_in] (models.py:301-305)
+ * P_log (optional) receives the overwritten rows, indexed like the rows list
+ * (the old payloads the incremental retraction reads).  Other models: no-op. */
+int rtec_project(const rtec_layer_t* L, const float* H, const int32_t* rows, const int64_t* n_rows,
+                 int64_t n_or_max_rows, float* P, float* P_log, const uint64_t* err, rtec_stream_t stream);
 
 /* Dense update GEMM on gathered rows (operators.py:180; linalg.py:22):
  * Y[i] = act(X[i] · W^T) (act: 0 none, 1 relu).  Rows i < *n_rows. */

@@ -158,6 +158,19 @@ class OracleEngine:
             A[rows] = a_new.reshape(R, heads * dh)
             C[rows] = ctx_new[:, 0] if heads == 1 else ctx_new
             return
+        if b.model in M.EDGE_MODELS:  # dest-dependent, no context: v ∉ R keeps h_v
+            dS = np.zeros((R, h_new.shape[1]))
+            for s, u, d, h in ((+1, vcs, vcd, h_new), (-1, vcs, vcd, h_old), (+1, Is, Id, h_new), (-1, Ds, Dd, h_old)):
+                if u.size:
+                    np.add.at(dS, pos[d], s * M.edge_message(b, l, h[u], h_new[d]))
+            had = old_in[rows] > 0
+            has = new_in[rows] > 0
+            a_new = np.where(had[:, None], A[rows], 0.0) + dS
+            A[rows] = np.where(has[:, None], a_new, 0.0)
+            C[rows] = 1.0
+            return
+        if b.model in M.PAYLOAD_MODELS:  # messages are per-source payload rows
+            h_new, h_old = M.payload(b, l, h_new), M.payload(b, l, h_old)
         with np.errstate(divide="ignore"):
             c_new = M.src_coeff(b, g.out_deg)
             c_old = M.src_coeff(b, old_out)

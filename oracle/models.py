@@ -1,7 +1,8 @@
 """Oracle restatement of the reference model zoo -- TEST INFRASTRUCTURE ONLY.
 
 Restates `streamgnn/models.py` for the four hot-path models (gcn, graphsage,
-gin, gat):
+gin, gat) and the rest of Table II (pinsage,
+monet, commnet, ggcn, agnn; models.py:144-348):
 
 - `make_bundle` draws weights with the reference's RNG sequence
   (models.py:56-63 `_mat`/`_vec`, builders :88-287, `make_bundle` :364-384),
@@ -31,7 +32,10 @@ GCN, SAGE, GIN, GAT = "gcn", "graphsage", "gin", "gat"
 # aggregator exists in models.py); restated here as the full recompute
 # a_v = max_{u in N_in(v)} h_u (0 for an empty neighbourhood), GIN update.
 GIN_MAX = "gin_max"
-MODELS = (GCN, SAGE, GIN, GAT, GIN_MAX)
+PINSAGE, MONET, COMMNET, GGCN, AGNN = "pinsage", "monet", "commnet", "ggcn", "agnn"
+MODELS = (GCN, SAGE, GIN, GAT, GIN_MAX, PINSAGE, MONET, COMMNET, GGCN, AGNN)
+PAYLOAD_MODELS = (PINSAGE, MONET)  # message = a function of h_u alone (per-source payload row)
+EDGE_MODELS = (GGCN, AGNN)  # message reads both endpoints (dest-dependent, no context)
 
 
 def _mat(rng, rows, cols):  # models.py:56-58
@@ -52,7 +56,7 @@ def head_seed(seed: int, layer: int, head: int, heads: int) -> int:
 class OracleBundle:
     model: str
     dims: tuple
-    layers: list  # per layer: dict of f64 arrays (W, W2, a[heads, 2*dh], Wh[heads, dh, din])
+    layers: list  # per layer: dict of f64 arrays (W, W2, a[heads, 2*dh], Wh[heads, dh, din], ...) + scalars
     degree_offset: float = 1.0
     heads: int = 1
     ctx_kind: str = "none"
@@ -86,6 +90,30 @@ def make_bundle(model, dims, *, rng_seed=0, degree_smoothing=True, heads=1) -> O
             W = _mat(rng, o, i)
             W2 = _mat(rng, o, o)
             layers.append({"W": W, "W2": W2})
+    elif model == PINSAGE:  # models.py:144-155: W [o, 2i], Q [i, i], q [i]; alpha = 1
+        for i, o in pairs:
+            W = _mat(rng, o, 2 * i)
+            Q = _mat(rng, i, i)
+            layers.append({"W": W, "Q": Q, "q": _vec(rng, i, i), "alpha": 1.0})
+    elif model == MONET:  # models.py:203-216: negative-definite kernel, W [o, 1], mu [i]
+        for i, o in pairs:
+            seed_mat = rng.uniform(-1.0, 1.0, (i, i)) / math.sqrt(i)
+            Wq = -(seed_mat @ seed_mat.T) / i
+            W = _mat(rng, o, 1)
+            layers.append({"W": W, "Wq": Wq, "mu": rng.uniform(-1.0, 1.0, i)})
+    elif model == COMMNET:  # models.py:235-239: W [o, i], W2 [o, i]
+        for i, o in pairs:
+            W = _mat(rng, o, i)
+            layers.append({"W": W, "W2": _mat(rng, o, i)})
+    elif model == GGCN:  # models.py:290-299: W [o, i], Wg_src [i, i], Wg_dst [i, i]
+        for i, o in pairs:
+            W = _mat(rng, o, i)
+            Ws = _mat(rng, i, i)
+            layers.append({"W": W, "Wg_src": Ws, "Wg_dst": _mat(rng, i, i)})
+    elif model == AGNN:  # models.py:320-324: W [o, i], beta ~ U(0.5, 1.5)
+        for i, o in pairs:
+            W = _mat(rng, o, i)
+            layers.append({"W": W, "beta": float(rng.uniform(0.5, 1.5))})
     else:  # GAT models.py:256-260
         if heads == 1:
             for i, o in pairs:
@@ -111,8 +139,17 @@ def make_bundle(model, dims, *, rng_seed=0, degree_smoothing=True, heads=1) -> O
     elif model == SAGE:  # :131-141
         b.ctx_kind = "count"
         b.agg_dims = dims[:-1]
-    elif model in (GIN, GIN_MAX):  # :191-200
+    elif model in (GIN, GIN_MAX, COMMNET):  # :191-200, :240-249
         b.ctx_kind = "none"
+        b.agg_dims = dims[:-1]
+    elif model == PINSAGE:  # :165-175
+        b.ctx_kind = "count"
+        b.agg_dims = dims[:-1]
+    elif model == MONET:  # :218-227 (scalar aggregate)
+        b.ctx_kind = "none"
+        b.agg_dims = (1,) * (len(dims) - 1)
+    elif model in EDGE_MODELS:  # :307-317, :337-347
+        b.ctx_kind, b.dest_dependent = "none", True
         b.agg_dims = dims[:-1]
     else:  # GAT :276-287
         b.ctx_kind, b.dest_dependent = "sum", True
@@ -141,11 +178,46 @@ def gat_project(b: OracleBundle, l: int, H):
     return z, el, er
 
 
+def sigmoid(x):  # linalg.py:46-52 (two-branch form)
+    pos = 1.0 / (1.0 + np.exp(-np.maximum(x, 0)))
+    ex = np.exp(np.minimum(x, 0))
+    return np.where(x >= 0, pos, ex / (1.0 + ex))
+
+
+def payload(b: OracleBundle, l: int, H):
+    """Per-source payload of the source-only models (ms_local * f_nn):
+    PinSAGE alpha relu(Q h + q) (models.py:157-159), MoNet exp(0.5 d^T Wq d),
+    d = h - mu, as a width-1 row (models.py:211-213)."""
+    L = b.layers[l]
+    if b.model == PINSAGE:
+        return L["alpha"] * np.maximum(H @ L["Q"].T + L["q"], 0.0)
+    diff = H - L["mu"]
+    return np.exp(0.5 * np.einsum("ri,ri->r", diff, diff @ L["Wq"].T))[:, None]
+
+
+def edge_message(b: OracleBundle, l: int, Hu, Hv):
+    """Dest-dependent payload rows for edges (u, v): G-GCN sigmoid(Wg_src h_u +
+    Wg_dst h_v) * h_u (models.py:301-305); A-GNN beta cos(h_u, h_v) h_u, zero
+    when either norm is zero (models.py:326-331)."""
+    L = b.layers[l]
+    if b.model == GGCN:
+        return sigmoid(Hu @ L["Wg_src"].T + Hv @ L["Wg_dst"].T) * Hu
+    nu = np.linalg.norm(Hu, axis=1)
+    nv = np.linalg.norm(Hv, axis=1)
+    ok = (nu > 0) & (nv > 0)
+    cos = np.where(ok, np.einsum("ri,ri->r", Hu, Hv) / np.where(ok, nu * nv, 1.0), 0.0)
+    return (L["beta"] * cos)[:, None] * Hu
+
+
 def update(b: OracleBundle, l: int, h_v, a_v):
     """apply_update (operators.py:180) for the builders' `update`."""
     L = b.layers[l]
-    if b.model in (GCN, SAGE):  # models.py:107-108, :137: relu(W a)
+    if b.model in (GCN, SAGE, MONET, GGCN, AGNN):  # models.py:107-108, :137, :225, :315, :345: relu(W a)
         return np.maximum(a_v @ L["W"].T, 0.0)
+    if b.model == PINSAGE:  # models.py:161-162: relu(W [h_v ; a_v])
+        return np.maximum(np.concatenate([h_v, a_v], 1) @ L["W"].T, 0.0)
+    if b.model == COMMNET:  # models.py:247: W h_v + W2 a_v (no activation)
+        return h_v @ L["W"].T + a_v @ L["W2"].T
     if b.model in (GIN, GIN_MAX):  # models.py:187-189: W2 relu(W (h_v + a_v))
         return np.maximum((h_v + a_v) @ L["W"].T, 0.0) @ L["W2"].T
     # GAT models.py:282: elu(a) (linalg.py:41-43)
@@ -156,7 +228,7 @@ def compose(b: OracleBundle, ctx, x):
     """ms_cbn (operators.py:135-144), row-wise; ctx broadcast per row(/head)."""
     if b.model == GCN:  # models.py:101-102
         return x / np.sqrt(ctx + b.degree_offset)[..., None]
-    if b.model in (SAGE, GAT):  # models.py:135, :280
+    if b.model in (SAGE, GAT, PINSAGE):  # models.py:135, :280, :169
         return x / ctx[..., None]
     return x
 
@@ -165,7 +237,7 @@ def strip(b: OracleBundle, ctx, x):
     """ms_cbn_inv (operators.py:146-155)."""
     if b.model == GCN:  # models.py:104-105
         return x * np.sqrt(ctx + b.degree_offset)[..., None]
-    if b.model in (SAGE, GAT):
+    if b.model in (SAGE, GAT, PINSAGE):
         return x * ctx[..., None]
     return x
 
@@ -218,11 +290,22 @@ def layer_full(b: OracleBundle, l: int, g, H_prev, rows=None):
         S[empty] = 0.0
         A = S
         C = np.ones(rows.size)
+    elif b.model in EDGE_MODELS:
+        msg = edge_message(b, l, H_prev[e_src], H_prev[rows][e_row])
+        S = np.zeros((rows.size, H_prev.shape[1]))
+        np.add.at(S, e_row, msg)
+        A = S
+        C = np.ones(rows.size)
+        A[cnt == 0] = 0.0
     else:
+        if b.model in PAYLOAD_MODELS:
+            H_msg = payload(b, l, H_prev)
+        else:
+            H_msg = H_prev
         with np.errstate(divide="ignore"):  # raw GCN: sources with no out-edges never appear
             c = src_coeff(b, g.out_deg)
         M = sp.csr_matrix((c[e_src], (e_row, e_src)), shape=(rows.size, n))
-        S = M @ H_prev
+        S = M @ H_msg
         empty = cnt == 0
         if b.ctx_kind == "count":
             C = cnt.astype(np.float64)

@@ -17,7 +17,8 @@ LIB_PATH = os.path.join(_HERE, "librtec.so")
 
 OP_INSERT = 0
 OP_DELETE = 1
-MODEL_IDS = {"gcn": 0, "graphsage": 1, "gin": 2, "gat": 3, "gin_max": 4}
+MODEL_IDS = {"gcn": 0, "graphsage": 1, "gin": 2, "gat": 3, "gin_max": 4, "pinsage": 5, "monet": 6, "commnet": 7,
+             "ggcn": 8, "agnn": 9}
 ARENA_FULL = 8
 ERR_OK = (1 << 64) - 1
 
@@ -61,7 +62,8 @@ class Layer(C.Structure):
     _fields_ = [
         ("model", I32), ("d_in", I32), ("d_out", I32), ("heads", I32),
         ("degree_offset", F32), ("pad", I32), ("W", P), ("W2", P), ("att", P),
-        ("Wt_hi", P), ("Wt_lo", P), ("W2t_hi", P), ("W2t_lo", P),
+        ("Wt_hi", P), ("Wt_lo", P), ("W2t_hi", P), ("W2t_lo", P), ("Wp", P), ("bp", P), ("scalar", F32),
+        ("d_k", I32),
     ]
 
 
@@ -97,6 +99,7 @@ _SIGS = {
                                          C.POINTER(Frontier), C.POINTER(Frontier), P, P, SZ, P]),
     "rtec_layer_full": (C.c_int, [C.POINTER(Graph), C.POINTER(Layer), C.POINTER(State), P, P, I64, P, P, SZ, P]),
     "rtec_gat_project": (C.c_int, [C.POINTER(Layer), P, P, P, I64, P, P, P, P, P, P, P]),
+    "rtec_project": (C.c_int, [C.POINTER(Layer), P, P, P, I64, P, P, P, P]),
     "rtec_update_gemm": (C.c_int, [P, I64, P, I32, I32, P, I64, I32, P, I64, P, P, P, P]),
     "rtec_query": (C.c_int, [P, I64, P, I64, P, I32, P, P]),
     "rtec_ns_sample": (C.c_int, [C.POINTER(Adj), P, P, I64, I32, C.c_uint64, I32, C.POINTER(Adj), P, I64, P, SZ, P]),

@@ -40,6 +40,18 @@ __host__ __device__ __forceinline__ bool is_gin(int model) {
   return model == RTEC_MODEL_GIN || model == RTEC_MODEL_GIN_MAX;
 }
 
+// Table II model classes (models.py:144-348)
+__host__ __device__ __forceinline__ bool self_concat(int model) {  // update reads [h_v ; a_v]
+  return model == RTEC_MODEL_PINSAGE || model == RTEC_MODEL_COMMNET;
+}
+__host__ __device__ __forceinline__ bool payload_model(int model) {  // message = projected payload of h_u
+  return model == RTEC_MODEL_PINSAGE || model == RTEC_MODEL_MONET;
+}
+__host__ __device__ __forceinline__ bool edge_model(int model) {  // message reads h_u and h_v
+  return model == RTEC_MODEL_GGCN || model == RTEC_MODEL_AGNN;
+}
+__host__ __device__ __forceinline__ int upd_k(const rtec_layer_t& L) { return L.d_k > 0 ? L.d_k : L.d_in; }
+
 __device__ __forceinline__ float leaky02(float x) { return x < 0.f ? 0.2f * x : x; }  // models.py:272-273
 __device__ __forceinline__ float elu1(float x) { return x >= 0.f ? x : expm1f(x); }   // linalg.py:41-43
 
@@ -55,6 +67,8 @@ struct LayerArgs {
   int d_agg;
   int tc_nkb;                   // > 0: gemm_in is the tcgen05 A image with tc_nkb K-blocks
   int c0, cw;                   // feature slice [c0, c0 + cw) of the d_agg-wide rows (aggregation)
+  int gcol, gk;                 // aggregate columns start at gcol of the gk-wide update input
+  const float* self_in;         // H^l (st.H_in is redirected to the payload rows for PinSAGE / MoNet)
   int layer;
   uint64_t* err;
 };
@@ -223,18 +237,23 @@ __device__ __forceinline__ void agg_finalize(const LayerArgs& a, int64_t i, int3
   float scale = 1.f;
   if (indeg > 0) {
     if (a.L.model == RTEC_MODEL_GCN) scale = 1.0f / sqrtf(static_cast<float>(indeg) + a.L.degree_offset);
-    else if (a.L.model == RTEC_MODEL_SAGE) scale = 1.0f / static_cast<float>(indeg);
+    else if (a.L.model == RTEC_MODEL_SAGE || a.L.model == RTEC_MODEL_PINSAGE) scale = 1.0f / static_cast<float>(indeg);
   }
   R out;
   out.zero();
   out.fma(acc.v, scale);
   if (is_gin(a.L.model)) {  // update input h_v + a_v (models.py:187-189)
     float h[K][VEC];
-    R::load(a.st.H_in + static_cast<int64_t>(v) * d + a.c0, cw, h);
+    R::load(a.self_in + static_cast<int64_t>(v) * d + a.c0, cw, h);
     out.add(h);
+  } else if (self_concat(a.L.model)) {  // update input [h_v ; a_v] (models.py:161-162, :247)
+    R hv;
+    R::load(a.self_in + static_cast<int64_t>(v) * d + a.c0, cw, hv.v);
+    if (a.tc_nkb > 0) hv.store_tiled(a.st.gemm_in, i, a.c0, cw, a.gk, a.tc_nkb);
+    else hv.store(a.st.gemm_in + i * a.gk + a.c0, cw);
   }
-  if (a.tc_nkb > 0) out.store_tiled(a.st.gemm_in, i, a.c0, cw, d, a.tc_nkb);
-  else out.store_stream(a.st.gemm_in + i * d + a.c0, cw, l2_evict_first_policy());
+  if (a.tc_nkb > 0) out.store_tiled(a.st.gemm_in, i, a.gcol + a.c0, cw, a.gk, a.tc_nkb);
+  else out.store_stream(a.st.gemm_in + i * a.gk + a.gcol + a.c0, cw, l2_evict_first_policy());
 }
 
 struct AggRows {
@@ -503,6 +522,247 @@ static int launch_aggregation(LayerArgs& a, AggRows rows, int64_t max_rows, int6
     return RTEC_SHAPE_ERROR;
   }
   RTEC_LAUNCH_CHECK("aggregation");
+  return RTEC_OK;
+}
+
+// ------------------------------------------------------------------ dest-dependent sums (G-GCN, A-GNN)
+// m(u, v) reads both endpoints (models.py:301-305, :326-331), so a destination
+// whose own h_v changed (R(l) = V_dst(l) ∩ V_chg(l-1)) is summed
+// over its whole post-batch in-run; every other destination keeps h_v and adds
+//   ValueChange (u,v), u ∈ S(l), not inserted :  m(u_new, v) - m(u_old, v)
+//   insert (u,v) :  + m(u_new, v)        delete (u,v) :  - m(u_old, v)
+// to its cached sum.  Old rows of V_chg(l-1) sources come from the previous
+// layer's DeltaLog (h) and the projection log (G-GCN gates), both by prev_slot.
+template <int VEC, int K>
+struct DstRow {
+  float hv[K][VEC];  // h_v
+  float pv[K][VEC];  // G-GCN: Wg_dst h_v
+  float nv;          // A-GNN: |h_v|
+};
+
+__device__ __forceinline__ float sigmoid_ref(float x) {  // linalg.py:46-52 two-branch form
+  if (x >= 0.f) return 1.f / (1.f + expf(-x));
+  const float e = expf(x);
+  return e / (1.f + e);
+}
+
+template <int VEC, int K>
+__device__ __forceinline__ void dd_load_dst(const LayerArgs& a, int32_t v, DstRow<VEC, K>& D) {
+  using R = RowAcc<VEC, K>;
+  const int d = a.d_agg;
+  R::load(a.st.H_in + static_cast<int64_t>(v) * d, d, D.hv);
+  D.nv = 0.f;
+  if (a.L.model == RTEC_MODEL_GGCN) {
+    R::load(a.st.Z + static_cast<int64_t>(v) * 2 * d + d, d, D.pv);
+  } else {
+    float s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) s2 = fmaf(D.hv[k][j], D.hv[k][j], s2);
+    D.nv = sqrtf(warp_sum(s2));
+  }
+}
+
+// acc += sign * m(u, v) for the source row hu (and its gate projection ps)
+template <int VEC, int K>
+__device__ __forceinline__ void dd_msg(const LayerArgs& a, const DstRow<VEC, K>& D, const float (&hu)[K][VEC],
+                                       const float (&ps)[K][VEC], float sign, RowAcc<VEC, K>& acc) {
+  if (a.L.model == RTEC_MODEL_GGCN) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) acc.v[k][j] = fmaf(sign * sigmoid_ref(ps[k][j] + D.pv[k][j]), hu[k][j], acc.v[k][j]);
+  } else {
+    float dot = 0.f, n2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        dot = fmaf(hu[k][j], D.hv[k][j], dot);
+        n2 = fmaf(hu[k][j], hu[k][j], n2);
+      }
+    dot = warp_sum(dot);
+    const float nu = sqrtf(warp_sum(n2));
+    const float c = (nu > 0.f && D.nv > 0.f) ? a.L.scalar * dot / (nu * D.nv) : 0.f;  // models.py:327-331
+    acc.fma(hu, sign * c);
+  }
+}
+
+// new (or old) rows of source u: h and, for G-GCN, the source gate projection
+template <int VEC, int K>
+__device__ __forceinline__ void dd_src(const LayerArgs& a, int32_t u, bool old, float (&h)[K][VEC],
+                                       float (&ps)[K][VEC]) {
+  using R = RowAcc<VEC, K>;
+  const int d = a.d_agg;
+  const bool logged = old && a.prev_bm_dst && bm_test(a.prev_bm_dst, u);
+  const int64_t slot = logged ? static_cast<int64_t>(a.prev_slot[u]) : 0;
+  R::load(logged ? a.st.log_in + slot * d : a.st.H_in + static_cast<int64_t>(u) * d, d, h);
+  if (a.L.model == RTEC_MODEL_GGCN)
+    R::load(logged ? a.st.Z_log + slot * 2 * d : a.st.Z + static_cast<int64_t>(u) * 2 * d, d, ps);
+}
+
+// in-run edges [e0, e1) of v: every edge when `full`, else the ValueChange ones (new - old)
+template <int VEC, int K>
+__device__ __forceinline__ void dd_edges(const LayerArgs& a, const DstRow<VEC, K>& D, int64_t beg, int32_t e0,
+                                         int32_t e1, int64_t p, int64_t q, bool full, RowAcc<VEC, K>& acc) {
+  for (int32_t c0 = e0; c0 < e1; c0 += 32) {
+    const int32_t j = c0 + lane_id();
+    int32_t u = 0;
+    bool hit = false;
+    if (j < e1) {
+      u = a.g.in.nbr[beg + j];
+      hit = full || (bm_test(a.f.bm_src, u) && !in_range_has(a.b.i_src, p, q, u) && a.prev_bm_dst &&
+                     bm_test(a.prev_bm_dst, u));  // S(l) sources whose row changed (Dg is empty here)
+    }
+    unsigned m = __ballot_sync(0xffffffffu, hit);
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      const int32_t uu = __shfl_sync(0xffffffffu, u, src);
+      float h[K][VEC], ps[K][VEC];
+      dd_src<VEC, K>(a, uu, false, h, ps);
+      dd_msg<VEC, K>(a, D, h, ps, 1.f, acc);
+      if (!full) {
+        dd_src<VEC, K>(a, uu, true, h, ps);
+        dd_msg<VEC, K>(a, D, h, ps, -1.f, acc);
+      }
+    }
+  }
+}
+
+template <int VEC, int K>
+__device__ __forceinline__ void dd_struct(const LayerArgs& a, const DstRow<VEC, K>& D, int64_t p, int64_t q,
+                                          RowAcc<VEC, K>& acc) {
+  for (int64_t k = p; k < q; ++k) {
+    const int32_t u = a.b.i_src[k];
+    const bool ins = a.b.i_op[k] == RTEC_OP_INSERT;
+    float h[K][VEC], ps[K][VEC];
+    dd_src<VEC, K>(a, u, !ins, h, ps);
+    dd_msg<VEC, K>(a, D, h, ps, ins ? 1.f : -1.f, acc);
+  }
+}
+
+// per-destination setup shared by the light / heavy kernels
+struct DdRow {
+  int64_t beg, p, q;
+  int32_t len, indeg, had;
+  bool full;
+};
+template <bool FULL>
+__device__ __forceinline__ DdRow dd_row(const LayerArgs& a, int32_t v) {
+  DdRow r{a.g.in.beg[v], 0, 0, a.g.in.len[v], 0, 0, true};
+  r.indeg = r.len;
+  if (!FULL) {
+    const int2 rg = reinterpret_cast<const int2*>(a.b.irange)[v];
+    if (rg.x >= 0) {
+      r.p = rg.x;
+      r.q = rg.x + rg.y;
+    }
+    r.indeg = a.g.in_deg[v];
+    r.had = a.g.in_deg_prev[v];
+    r.full = a.prev_bm_dst && bm_test(a.prev_bm_dst, v);  // v ∈ R(l)
+  }
+  return r;
+}
+
+// S_v: the new sum (R(l) / FULL) or the cached sum plus the signed changes
+template <int VEC, int K, bool FULL>
+__device__ __forceinline__ void dd_finalize(const LayerArgs& a, int64_t i, int32_t v, const DdRow& r,
+                                            RowAcc<VEC, K>& acc) {
+  using R = RowAcc<VEC, K>;
+  if (FULL) {
+    agg_finalize<VEC, K, true>(a, i, v, r.len, acc);
+    return;
+  }
+  R pre;
+  pre.zero();
+  if (!r.full && r.indeg > 0 && r.had > 0) R::load(a.st.S + srow(a, v) * a.d_agg, a.d_agg, pre.v);
+  agg_finalize<VEC, K, false>(a, i, v, r.len, acc, &pre, r.indeg);
+}
+
+template <int VEC, int K, bool FULL>
+__global__ void __launch_bounds__(kLBlk) k_dd_light(LayerArgs a, AggRows rows) {
+  using R = RowAcc<VEC, K>;
+  if (!FULL && err_set(a.err)) return;
+  const int64_t nr = rows.count();
+  const bool scan = FULL || *a.f.n_src > 0;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < nr; i += nw) {
+    const int32_t v = rows.at(i);
+    const DdRow r = dd_row<FULL>(a, v);
+    if (scan && r.len > kChunk) continue;  // heavy pass
+    DstRow<VEC, K> D;
+    dd_load_dst<VEC, K>(a, v, D);
+    R acc;
+    acc.zero();
+    if (scan) dd_edges<VEC, K>(a, D, r.beg, 0, r.len, r.p, r.q, r.full, acc);
+    if (!FULL && !r.full) dd_struct<VEC, K>(a, D, r.p, r.q, acc);
+    dd_finalize<VEC, K, FULL>(a, i, v, r, acc);
+  }
+}
+
+template <int VEC, int K, bool FULL>
+__global__ void __launch_bounds__(kLBlk) k_dd_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
+  using R = RowAcc<VEC, K>;
+  if (!FULL && err_set(a.err)) return;
+  const int64_t nh = *hp.n_heavy;
+  if (nh == 0) return;
+  const int64_t T = hp.hoff[nh];
+  const int d = a.d_agg;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = warp; t < T; t += nw) {
+    const int32_t j = hp.cmap[t];
+    const int64_t c0 = hp.hoff[j];
+    const int32_t nch = static_cast<int32_t>(hp.hoff[j + 1] - c0);
+    const int32_t c = static_cast<int32_t>(t - c0);
+    const int64_t i = hp.heavy[j];
+    const int32_t v = rows.at(i);
+    const DdRow r = dd_row<FULL>(a, v);
+    DstRow<VEC, K> D;
+    dd_load_dst<VEC, K>(a, v, D);
+    R acc;
+    acc.zero();
+    const int32_t e0 = c * kChunk, e1 = min(r.len, e0 + kChunk);
+    dd_edges<VEC, K>(a, D, r.beg, e0, e1, r.p, r.q, r.full, acc);
+    if (!FULL && !r.full && c == 0) dd_struct<VEC, K>(a, D, r.p, r.q, acc);
+    acc.store(hp.part + t * d, d);
+    __threadfence();
+    int old = 0;
+    if (lane_id() == 0) old = atomicAdd(hp.arrive + j, 1);
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old != nch - 1) continue;
+    __threadfence();
+    acc.zero();
+    sum_partials<VEC, K>(hp.part + c0 * d, d, d, nch, acc);  // chunk order: deterministic
+    dd_finalize<VEC, K, FULL>(a, i, v, r, acc);
+  }
+}
+
+template <bool FULL>
+static int launch_dd(LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_edges, Ws& w, cudaStream_t s) {
+  const int d = a.d_agg;
+  a.c0 = 0;
+  a.cw = d;
+  HeavyPlan hp{};
+  RTEC_TRY(plan_heavy<FULL>(a, rows, max_rows, max_edges, d, w, s, hp));
+  const int grid = kSMs * 8;
+  bool ok;
+  {
+    RTEC_PROF(FULL ? "k_dd_full_heavy" : "k_dd_inc_heavy", s);
+    ok = RTEC_ROW_DISPATCH(d, (k_dd_heavy<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows, hp)));
+  }
+  {
+    RTEC_PROF(FULL ? "k_dd_full_light" : "k_dd_inc", s);
+    ok = ok && RTEC_ROW_DISPATCH(d, (k_dd_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows)));
+  }
+  if (!ok) {
+    set_error("row width %d unsupported", d);
+    return RTEC_SHAPE_ERROR;
+  }
+  RTEC_LAUNCH_CHECK("k_dd");
   return RTEC_OK;
 }
 
@@ -1235,6 +1495,9 @@ struct GemmArgs {
   float* log;
   const uint64_t* err;  // skip when the batch failed validation / reservation
   int ydiv;             // > 1: Y row of y_rows[i] is y_rows[i] / ydiv (sharded final layer)
+  const float* bias;    // Y = scale * act(X W^T + bias) (PinSAGE payload, models.py:159)
+  float scale;
+  int has_scale;
 };
 
 constexpr int kGM = 64, kGN = 64, kGK = 16;
@@ -1292,7 +1555,9 @@ __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs g) {
       int col = col0 + tx * 4 + c;
       if (col >= g.d_out) continue;
       float y = acc[r][c];
+      if (g.bias) y += g.bias[col];
       if (g.act == 1) y = fmaxf(y, 0.f);
+      if (g.has_scale) y *= g.scale;
       float* yp = g.Y + dst * g.ldy + col;
       if (g.log) g.log[gr * g.d_out + col] = *yp;
       *yp = y;
@@ -1309,6 +1574,52 @@ int gemm_launch(const GemmArgs& g, cudaStream_t s) {
   k_gemm_simt<<<grid, 256, 0, s>>>(g);
   RTEC_LAUNCH_CHECK("k_gemm_simt");
   return RTEC_OK;
+}
+
+// ------------------------------------------------------------------ MoNet payload (models.py:211-213)
+// P[v] = exp(0.5 (h_v - mu)^T Wq (h_v - mu)); Wq symmetrised on the host so the
+// lane-strided reads of row k are coalesced.  One warp per row, d <= 256.
+constexpr int kQuadM = 8;
+__global__ void __launch_bounds__(256) k_quadform(const float* __restrict__ H, const int32_t* rows,
+                                                  const int64_t* n_rows, int64_t n_all, int d,
+                                                  const float* __restrict__ Wq, const float* __restrict__ mu,
+                                                  float* P, float* P_log, const uint64_t* err) {
+  if (err && err_set(err)) return;
+  const int64_t nr = rows ? *n_rows : n_all;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = lane_id();
+  for (int64_t i = warp; i < nr; i += nw) {
+    const int32_t v = rows ? rows[i] : static_cast<int32_t>(i);
+    float df[kQuadM], t[kQuadM];
+#pragma unroll
+    for (int m = 0; m < kQuadM; ++m) {
+      const int k = lane + 32 * m;
+      df[m] = k < d ? H[static_cast<int64_t>(v) * d + k] - mu[k] : 0.f;
+      t[m] = 0.f;
+    }
+#pragma unroll
+    for (int m = 0; m < kQuadM; ++m) {
+      if (32 * m >= d) break;
+      for (int kk = 0; kk < 32 && 32 * m + kk < d; ++kk) {
+        const float dk = __shfl_sync(0xffffffffu, df[m], kk);
+        const float* wr = Wq + static_cast<int64_t>(32 * m + kk) * d;
+#pragma unroll
+        for (int mm = 0; mm < kQuadM; ++mm) {
+          const int j = lane + 32 * mm;
+          if (j < d) t[mm] = fmaf(__ldg(wr + j), dk, t[mm]);
+        }
+      }
+    }
+    float q = 0.f;
+#pragma unroll
+    for (int m = 0; m < kQuadM; ++m) q = fmaf(df[m], t[m], q);
+    q = warp_sum(q);
+    if (lane == 0) {
+      if (P_log) P_log[i] = P[v];
+      P[v] = expf(0.5f * q);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ query (K18)
@@ -1336,7 +1647,7 @@ static int run_update(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t
                       int64_t max_rows, const int32_t* y_rows, float* log, const uint64_t* err, cudaStream_t s);
 
 static int layer_dims_ok(const rtec_layer_t* L) {
-  if (L->model < 0 || L->model > RTEC_MODEL_GIN_MAX) {
+  if (L->model < 0 || L->model > RTEC_MODEL_AGNN) {
     set_error("unsupported model id %d", L->model);
     return RTEC_UNSUPPORTED_MODEL;
   }
@@ -1359,8 +1670,10 @@ static int run_update(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t
     t.deg_off = L->degree_offset;
     t.log = nullptr;
   };
+  const int dk = upd_k(*L);
+  const int act = L->model == RTEC_MODEL_COMMNET ? 0 : 1;  // CommNet: W h_v + W2 a_v (models.py:247)
   if (L->Wt_hi) {
-    const int nkb = tc_nkb_of(L->d_in);
+    const int nkb = tc_nkb_of(dk);
     if (is_gin(L->model)) {  // W2 relu(W (h + a)) (models.py:187-189), hidden kept in tile layout
       const int nkb2 = tc_nkb_of(L->d_out);
       TcArgs t1{st->gemm_in, L->Wt_hi, L->Wt_lo, nkb, tc_npad_of(L->d_out), L->d_out, n_rows, max_rows, 1,
@@ -1372,7 +1685,7 @@ static int run_update(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t
       fuse(t2);
       return gemm_tc_launch(t2, s);
     }
-    TcArgs t{st->gemm_in, L->Wt_hi, L->Wt_lo, nkb, tc_npad_of(L->d_out), L->d_out, n_rows, max_rows, 1,
+    TcArgs t{st->gemm_in, L->Wt_hi, L->Wt_lo, nkb, tc_npad_of(L->d_out), L->d_out, n_rows, max_rows, act,
              st->H_out, L->d_out, y_rows, log, nullptr, 0, err};
     t.ydiv = ydiv;
     fuse(t);
@@ -1386,9 +1699,22 @@ static int run_update(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t
                 st->H_out, L->d_out, y_rows, log, err, ydiv};
     return gemm_launch(g2, s);
   }
-  GemmArgs g1{st->gemm_in, L->d_in, nullptr, L->W, L->d_in, L->d_out, n_rows, max_rows, 1,
+  GemmArgs g1{st->gemm_in, dk, nullptr, L->W, dk, L->d_out, n_rows, max_rows, act,
               st->H_out, L->d_out, y_rows, log, err, ydiv};
   return gemm_launch(g1, s);
+}
+
+// LayerArgs common to the incremental and full layer passes
+static void layer_args_init(LayerArgs& a, const rtec_layer_t* L, const rtec_state_t* st) {
+  a.self_in = st->H_in;
+  a.gk = upd_k(*L);
+  a.gcol = self_concat(L->model) ? L->d_in : 0;
+  a.d_agg = L->model == RTEC_MODEL_MONET ? 1 : L->d_in;
+  if (payload_model(L->model)) {  // messages are the projected payload rows (and their log)
+    a.st.H_in = st->Z;
+    a.st.log_in = st->Z_log;
+  }
+  a.tc_nkb = L->Wt_hi ? tc_nkb_of(a.gk) : 0;
 }
 
 extern "C" {
@@ -1421,25 +1747,27 @@ int rtec_layer_incremental(const rtec_graph_t* g, const rtec_batch_t* b, const r
   const int grid = kSMs * 8;
   if (L->model == RTEC_MODEL_GAT)
     return launch_gat<false>(a, AggRows{f->dst_list, f->n_dst, n}, n, g->in.slots, w, s);
-  a.d_agg = L->d_in;
+  layer_args_init(a, L, st);
   if (L->model == RTEC_MODEL_GIN_MAX) {
-    a.tc_nkb = L->Wt_hi ? tc_nkb_of(L->d_in) : 0;
     RTEC_TRY(launch_max<false>(a, AggRows{f->dst_list, f->n_dst, n}, n, g->in.slots, w, s));
     return run_update(g, L, st, f->n_dst, n, f->dst_list, st->log_out, err, s);
   }
-  float* delta = st->delta ? st->delta : w.alloc<float>(n * static_cast<int64_t>(L->d_in));
+  if (edge_model(L->model)) {
+    RTEC_TRY(launch_dd<false>(a, AggRows{f->dst_list, f->n_dst, n}, n, g->in.slots, w, s));
+    return run_update(g, L, st, f->n_dst, n, f->dst_list, st->log_out, err, s);
+  }
+  float* delta = st->delta ? st->delta : w.alloc<float>(n * static_cast<int64_t>(a.d_agg));
   RTEC_WS_CHECK(w);
   a.delta = delta;
   bool ok;
   {
     RTEC_PROF("k_src_delta", s);
-    ok = RTEC_ROW_DISPATCH(L->d_in, (k_src_delta<VEC, K><<<grid, kLBlk, 0, s>>>(a, delta)));
+    ok = RTEC_ROW_DISPATCH(a.d_agg, (k_src_delta<VEC, K><<<grid, kLBlk, 0, s>>>(a, delta)));
   }
   if (!ok) {
-    set_error("row width %d unsupported", L->d_in);
+    set_error("row width %d unsupported", a.d_agg);
     return RTEC_SHAPE_ERROR;
   }
-  a.tc_nkb = L->Wt_hi ? tc_nkb_of(L->d_in) : 0;
   RTEC_TRY(launch_aggregation<false>(a, AggRows{f->dst_list, f->n_dst, n}, n, g->in.slots, w, s));
   // update on V_dst(l) rows with DeltaLog capture (operators.py:180)
   return run_update(g, L, st, f->n_dst, n, f->dst_list, st->log_out, err, s);
@@ -1469,8 +1797,8 @@ int rtec_layer_full(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* 
                                         nullptr, nullptr);
     return launch_gat<true>(a, AggRows{nullptr, nullptr, n}, n, g->in.slots, w, s);
   }
-  a.d_agg = L->d_in;
-  a.tc_nkb = L->Wt_hi ? tc_nkb_of(L->d_in) : 0;
+  if (!rows) RTEC_TRY(rtec_project(L, st->H_in, nullptr, nullptr, n, st->Z, nullptr, nullptr, stream));
+  layer_args_init(a, L, st);
   int64_t mr = rows ? max_rows : n;
   if (L->model == RTEC_MODEL_GIN_MAX) {
     Ws w(ws, ws_bytes);
@@ -1479,7 +1807,10 @@ int rtec_layer_full(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* 
   }
   {
     Ws w(ws, ws_bytes);
-    RTEC_TRY(launch_aggregation<true>(a, AggRows{rows, rows ? n_rows : nullptr, n}, mr, g->in.slots, w, s));
+    if (edge_model(L->model))
+      RTEC_TRY(launch_dd<true>(a, AggRows{rows, rows ? n_rows : nullptr, n}, mr, g->in.slots, w, s));
+    else
+      RTEC_TRY(launch_aggregation<true>(a, AggRows{rows, rows ? n_rows : nullptr, n}, mr, g->in.slots, w, s));
   }
   return run_update(g, L, st, rows ? n_rows : nullptr, mr, rows, nullptr, nullptr, s);
 }
@@ -1497,6 +1828,40 @@ int rtec_gat_project(const rtec_layer_t* L, const float* H, const int32_t* rows,
                                           err);
   RTEC_LAUNCH_CHECK("k_gat_logits");
   return RTEC_OK;
+}
+
+int rtec_project(const rtec_layer_t* L, const float* H, const int32_t* rows, const int64_t* n_rows,
+                 int64_t n_or_max_rows, float* P, float* P_log, const uint64_t* err, rtec_stream_t stream) {
+  RTEC_TRY(layer_dims_ok(L));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (n_or_max_rows <= 0) return RTEC_OK;
+  const int d = L->d_in;
+  const int64_t* nr = rows ? n_rows : nullptr;
+  switch (L->model) {
+    case RTEC_MODEL_PINSAGE: {  // alpha relu(Q h + q)
+      GemmArgs g{H, d, rows, L->Wp, d, d, nr, n_or_max_rows, 1, P, d, rows, P_log, err};
+      g.bias = L->bp;
+      g.scale = L->scalar;
+      g.has_scale = 1;
+      return gemm_launch(g, s);
+    }
+    case RTEC_MODEL_GGCN: {  // [Wg_src h ; Wg_dst h]
+      GemmArgs g{H, d, rows, L->Wp, d, 2 * d, nr, n_or_max_rows, 0, P, 2 * d, rows, P_log, err};
+      return gemm_launch(g, s);
+    }
+    case RTEC_MODEL_MONET: {
+      if (d > 32 * kQuadM) {
+        set_error("MoNet input width %d > %d", d, 32 * kQuadM);
+        return RTEC_SHAPE_ERROR;
+      }
+      RTEC_PROF("k_quadform", s);
+      k_quadform<<<kSMs * 8, 256, 0, s>>>(H, rows, nr, n_or_max_rows, d, L->Wp, L->bp, P, P_log, err);
+      RTEC_LAUNCH_CHECK("k_quadform");
+      return RTEC_OK;
+    }
+    default:
+      return RTEC_OK;
+  }
 }
 
 int rtec_query(const float* H, int64_t d, const int32_t* ids, int64_t k, float* out, int32_t n, uint64_t* err,

@@ -30,7 +30,7 @@ import torch
 from . import _lib
 from . import errors as E
 from .graph import DynamicGraph, EdgeUpdate, updates_to_arrays
-from .models import GAT, GCN, GIN, GIN_FAMILY, GRAPHSAGE, Bundle, MODELS
+from .models import AGNN, COMMNET, GAT, GCN, GGCN, GIN, GIN_FAMILY, GRAPHSAGE, MONET, PINSAGE, Bundle, MODELS
 
 _MODEL_ID = _lib.MODEL_IDS
 
@@ -130,19 +130,36 @@ class RTECEngine:
         self.delta = [z(n, bundle.agg_dims[l]) if self.fused else None for l in range(bundle.num_layers)]
         for l, w in enumerate(bundle.layers):
             d_in, d_out = w.in_dim, w.out_dim
-            W = torch.as_tensor(np.asarray(w.tensors["W"], np.float32), device=self.dev).contiguous()
-            W2 = torch.as_tensor(np.asarray(w.tensors["W2"], np.float32), device=self.dev).contiguous() if bundle.model in GIN_FAMILY else None
-            att = torch.as_tensor(np.asarray(w.tensors["a"], np.float32).reshape(heads, -1), device=self.dev).contiguous() if bundle.model == GAT else None
+            dev32 = lambda a: torch.as_tensor(np.ascontiguousarray(a, np.float32), device=self.dev)  # noqa: E731
+            t = w.tensors
+            Wnp = np.asarray(t["W"], np.float64)
+            if bundle.model == COMMNET:  # W h_v + W2 a_v == [W | W2] [h_v ; a_v]
+                Wnp = np.concatenate([Wnp, np.asarray(t["W2"], np.float64)], 1)
+            W = dev32(Wnp)
+            W2 = dev32(t["W2"]) if bundle.model in GIN_FAMILY else None
+            att = dev32(np.asarray(t["a"]).reshape(heads, -1)) if bundle.model == GAT else None
+            Wp = bp = None
+            scalar = 0.0
+            if bundle.model == PINSAGE:  # alpha relu(Q h + q)
+                Wp, bp, scalar = dev32(t["Q"]), dev32(t["q"]), float(w.scalars.get("alpha", 1.0))
+            elif bundle.model == MONET:  # the quadratic form only sees the symmetric part of Wq
+                Wq = np.asarray(t["Wq"], np.float64)
+                Wp, bp = dev32(0.5 * (Wq + Wq.T)), dev32(t["mu"])
+            elif bundle.model == GGCN:
+                Wp = dev32(np.concatenate([np.asarray(t["Wg_src"]), np.asarray(t["Wg_dst"])], 0))
+            elif bundle.model == AGNN:
+                scalar = float(w.scalars["beta"])
+            d_k = bundle.update_width(l)
             tcw = [None, None, None, None]
             if self.tc:
-                tcw[0], tcw[1] = self._prep_weights(W, d_in, d_out)
+                tcw[0], tcw[1] = self._prep_weights(W, d_k, d_out)
                 if W2 is not None:
                     tcw[2], tcw[3] = self._prep_weights(W2, d_out, d_out)
-            self.wt.append((W, W2, att, *tcw))
+            self.wt.append((W, W2, att, *tcw, Wp, bp))
             p = _lib.ptr
             self.layers.append(_lib.Layer(_MODEL_ID[bundle.model], d_in, d_out, heads if bundle.model == GAT else 1,
                                           float(bundle.degree_offset), 0, p(W), p(W2), p(att),
-                                          p(tcw[0]), p(tcw[1]), p(tcw[2]), p(tcw[3])))
+                                          p(tcw[0]), p(tcw[1]), p(tcw[2]), p(tcw[3]), p(Wp), p(bp), scalar, d_k))
             d_agg = bundle.agg_dims[l]
             # layer inputs are read for every source: full rows; the final output only per owner
             self.H.append(z(n if l + 1 < bundle.num_layers else no, d_out))
@@ -156,6 +173,13 @@ class RTECEngine:
                 self.er.append(z(n, heads))
                 self.Zlog.append(z(n, d_out))
                 self.erlog.append(z(n, heads))
+            elif bundle.projected:  # payload / gate projections of every vertex + their batch log
+                pw = bundle.proj_width(l)
+                self.ctx.append(None)
+                self.Z.append(z(n, pw))
+                self.Zlog.append(z(n, pw))
+                for lst in (self.el, self.er, self.erlog):
+                    lst.append(None)
             else:
                 self.ctx.append(None)
                 for lst in (self.Z, self.el, self.er, self.Zlog, self.erlog):
@@ -164,10 +188,10 @@ class RTECEngine:
         if self.tc:  # SW128 tile image: ceil(rows/128)*128 rows x ceil(d/32)*32 columns
             rows = (no + 127) // 128 * 128
             pad = lambda d: (d + 31) // 32 * 32  # noqa: E731
-            self.gemm_in = z(rows * pad(max(bundle.agg_dims)))
+            self.gemm_in = z(rows * pad(max(bundle.update_width(l) for l in range(self.L))))
             self.gemm_mid = z(rows * pad(max(dims[1:]))) if bundle.model in GIN_FAMILY else None
         else:
-            self.gemm_in = z(no, max(bundle.agg_dims)) if bundle.model != GAT else None
+            self.gemm_in = z(no, max(bundle.update_width(l) for l in range(self.L))) if bundle.model != GAT else None
             self.gemm_mid = z(no, max(dims[1:])) if bundle.model in GIN_FAMILY else None
         self.fr = [_Frontier(n, self.dev) for _ in range(self.L)]
         self._ensure_ws(max_batch or graph.batch.cap)
@@ -218,14 +242,22 @@ class RTECEngine:
         if sync:
             _lib.raise_err(err.item(), "bootstrap")
 
-    def refresh_projection(self, l: int) -> None:
-        """GAT: Z = W h, el, er of every vertex of layer l from H^l (after a restore)."""
-        if self.b.model != GAT:
-            return
+    def _project(self, l, H, rows, n_rows, Z, el=None, er=None, Zlog=None, erlog=None, err=None, stream=None):
+        """Per-vertex projections of layer l for `rows` (all when None) from H: GAT Z / el / er
+        (rtec_gat_project), PinSAGE / MoNet payloads and G-GCN gates (rtec_project)."""
         p = _lib.ptr
-        _lib.check(self.lib.rtec_gat_project(C.byref(self.layers[l]), p(self.H[l]), None, None, self.n, p(self.Z[l]),
-                                             p(self.el[l]), p(self.er[l]), None, None, None, _lib.stream_handle()),
-                   "gat_project")
+        st = stream if stream is not None else _lib.stream_handle()
+        if self.b.model == GAT:
+            _lib.check(self.lib.rtec_gat_project(C.byref(self.layers[l]), p(H), p(rows), p(n_rows), self.n, p(Z),
+                                                 p(el), p(er), p(Zlog), p(erlog), p(err), st), "gat_project")
+        elif self.b.projected:
+            _lib.check(self.lib.rtec_project(C.byref(self.layers[l]), p(H), p(rows), p(n_rows), self.n, p(Z),
+                                             p(Zlog), p(err), st), "project")
+
+    def refresh_projection(self, l: int) -> None:
+        """Projections of every vertex of layer l from H^l (after a restore)."""
+        if self.b.projected:
+            self._project(l, self.H[l], None, None, self.Z[l], self.el[l], self.er[l])
 
     def save(self, directory: str) -> None:
         """Checkpoint between batches (formats.save_checkpoint)."""
@@ -325,12 +357,10 @@ class RTECEngine:
                 main.wait_event(self._side()[1][l])
             if mode == "frontier":
                 continue
-            if self.b.model == GAT and l > 0:
+            if self.b.projected and l > 0:  # projections of the rows V_chg(l-1) rewrote (+ their log)
                 pf = self.fr[l - 1]
-                _lib.check(self.lib.rtec_gat_project(C.byref(self.layers[l]), _lib.ptr(self.H[l]), _lib.ptr(pf.dst_list),
-                                                     _lib.ptr(pf.n_dst), self.n, _lib.ptr(self.Z[l]), _lib.ptr(self.el[l]),
-                                                     _lib.ptr(self.er[l]), _lib.ptr(self.Zlog[l]), _lib.ptr(self.erlog[l]),
-                                                     errp, st), "gat_project")
+                self._project(l, self.H[l], pf.dst_list, pf.n_dst, self.Z[l], self.el[l], self.er[l], self.Zlog[l],
+                              self.erlog[l], gr.batch.err, st)
             if mode == "uer":
                 f = self.fr[l]
                 s_full = self._state(l)
@@ -422,7 +452,8 @@ class RTECEngine:
                       for _ in range(L)],
               "H": [None] + [zf(n, d) for d in self.b.dims[1:]],
               "S": zf(n, max(self.b.agg_dims)),
-              "Z": zf(n, max(self.b.dims[1:])) if self.b.model == GAT else None,
+              "Z": (zf(n, max(self.b.dims[1:])) if self.b.model == GAT else
+                    zf(n, max(self.b.proj_width(l) for l in range(L))) if self.b.projected else None),
               "el": zf(n, self.b.heads) if self.b.model == GAT else None,
               "er": zf(n, self.b.heads) if self.b.model == GAT else None,
               "ctx": zf(n, self.b.heads) if self.b.model == GAT else None}
@@ -464,10 +495,10 @@ class RTECEngine:
             s = self._state(l)
             s.H_in, s.H_out, s.S = p(H[l]), p(H[l + 1]), p(nb["S"])
             s.log_out = s.log_in = None
-            if self.b.model == GAT:
+            if self.b.projected:  # projections of the sampled rows T_l
                 s.Z, s.el, s.er, s.ctx = p(nb["Z"]), p(nb["el"]), p(nb["er"]), p(nb["ctx"])
-                _lib.check(lib.rtec_gat_project(C.byref(self.layers[l]), p(H[l]), p(T[l]), p(C_[l]), n, p(nb["Z"]),
-                                                p(nb["el"]), p(nb["er"]), None, None, p(err), st), "ns_project")
+                s.Z_log = s.er_log = None
+                self._project(l, H[l], T[l], C_[l], nb["Z"], nb["el"], nb["er"], err=err, stream=st)
             _lib.check(lib.rtec_layer_full(C.byref(g), C.byref(self.layers[l]), C.byref(s), p(T[l + 1]),
                                            p(C_[l + 1]), n, p(err), ws, wsb, st), "ns_layer")
         k = int(cnt.item())
@@ -499,10 +530,8 @@ class RTECEngine:
         err = torch.full((1,), -1, dtype=torch.int64, device=self.dev)
         prev = None
         for l in range(self.L):
-            if self.b.model == GAT and l > 0 and prev is not None:
-                _lib.check(lib.rtec_gat_project(C.byref(self.layers[l]), p(self.H[l]), p(prev[0]), p(prev[1]),
-                                                self.n, p(self.Z[l]), p(self.el[l]), p(self.er[l]), None, None, None,
-                                                st), "odec")
+            if self.b.projected and l > 0 and prev is not None:
+                self._project(l, self.H[l], prev[0], prev[1], self.Z[l], self.el[l], self.er[l])
             rows = torch.empty(max(self.n, 1), dtype=torch.int32, device=self.dev)
             nrows = torch.zeros(1, dtype=torch.int64, device=self.dev)
             _lib.check(lib.rtec_bitmap_to_list(p(self._stale[l]), self.n, p(rows), p(nrows), p(gr.ws), gr.ws.numel(),
@@ -555,10 +584,8 @@ class RTECEngine:
         err = torch.full((1,), -1, dtype=torch.int64, device=self.dev)
         prev_rows = None
         for l in range(L):  # bottom-up over the deferred rows the queries need
-            if self.b.model == GAT and l > 0 and prev_rows is not None:  # fresh H^l rows: fresh projections
-                _lib.check(lib.rtec_gat_project(C.byref(self.layers[l]), p(self.H[l]), p(prev_rows[0]),
-                                                p(prev_rows[1]), n, p(self.Z[l]), p(self.el[l]), p(self.er[l]), None,
-                                                None, None, st), "odec")
+            if self.b.projected and l > 0 and prev_rows is not None:  # fresh H^l rows: fresh projections
+                self._project(l, self.H[l], prev_rows[0], prev_rows[1], self.Z[l], self.el[l], self.er[l])
             todo = stale[l] & self._need[l]
             rows = torch.empty(max(n, 1), dtype=torch.int32, device=self.dev)
             nrows = torch.zeros(1, dtype=torch.int64, device=self.dev)
@@ -655,7 +682,7 @@ class RTECEngine:
             A = (S.view(self.n, h, -1) / safe[:, :, None]).reshape(self.n, -1)
         elif self.b.model == "gcn":
             A = S / torch.sqrt(indeg + self.b.degree_offset)[:, None]
-        elif self.b.model == "graphsage":
+        elif self.b.model in (GRAPHSAGE, PINSAGE):
             A = S / torch.clamp(indeg, min=1.0)[:, None]
         else:
             A = S

@@ -1,7 +1,8 @@
-"""Operator bundles for the hot-path models (gcn, graphsage, gin, gat).
+"""Operator bundles for the reference model zoo (Table II).
 
-Mirrors the reference model zoo (`streamgnn/models.py`) for the four models
-on the north-star path: `make_bundle(model, dims, *, dtype, rng_seed,
+Mirrors `streamgnn/models.py`: the four north-star models (gcn, graphsage,
+gin, gat) and the rest of Table II (pinsage, monet, commnet, ggcn, agnn;
+models.py:144-348).  `make_bundle(model, dims, *, dtype, rng_seed,
 weights, degree_smoothing)` draws weights with the same RNG sequence as
 models.py:56-63 / :88-287 / :364-384, so a given seed produces bit-identical
 f64 weights; the engine uploads fp32 copies.  A reference `OperatorBundle`
@@ -32,9 +33,11 @@ GCN, GRAPHSAGE, GIN, GAT = "gcn", "graphsage", "gin", "gat"
 # reference has no max aggregator, so this one is pinned only by the oracle's
 # restated full recompute (SURVEY §8(c) "Unpinned by the reference").
 GIN_MAX = "gin_max"
-MODELS = (GCN, GRAPHSAGE, GIN, GAT, GIN_MAX)
+PINSAGE, MONET, COMMNET, GGCN, AGNN = "pinsage", "monet", "commnet", "ggcn", "agnn"
+MODELS = (GCN, GRAPHSAGE, GIN, GAT, GIN_MAX, PINSAGE, MONET, COMMNET, GGCN, AGNN)
 GIN_FAMILY = (GIN, GIN_MAX)
-REFERENCE_ONLY = ("pinsage", "monet", "commnet", "ggcn", "agnn")
+PROJECTED = (PINSAGE, MONET, GGCN)  # per-source projection cache (rtec_project) besides GAT's
+REFERENCE_ONLY = ()
 
 
 @dataclass(frozen=True)
@@ -71,6 +74,22 @@ class Bundle:
 
     def empty_context(self) -> float:  # operators.py:99-100
         return 0.0 if self.has_nbr_ctx else 1.0
+
+    @property
+    def projected(self) -> bool:
+        """Layers keep a per-vertex projection of H^l (GAT Z/el/er, PinSAGE / MoNet
+        payloads, G-GCN gates) that must follow every changed row."""
+        return self.model == GAT or self.model in PROJECTED
+
+    def proj_width(self, l: int) -> int:
+        d = self.layers[l].in_dim
+        return {PINSAGE: d, MONET: 1, GGCN: 2 * d}.get(self.model, 0)
+
+    def update_width(self, l: int) -> int:
+        """Columns of the update input: [h_v ; a_v] for PinSAGE / CommNet, the scalar
+        aggregate for MoNet, a_v otherwise (rtec_layer_t.d_k)."""
+        d = self.layers[l].in_dim
+        return {PINSAGE: 2 * d, COMMNET: 2 * d, MONET: 1}.get(self.model, self.agg_dims[l])
 
 
 def _mat(rng, rows, cols, dtype):  # models.py:56-58
@@ -120,6 +139,35 @@ def make_bundle(model: str, dims: Sequence[int], *, dtype=np.float64, rng_seed: 
         for i, o in pairs:
             W = _mat(rng, o, i, dt)
             layers.append(LayerWeights(i, o, {"W": W, "W2": _mat(rng, o, o, dt)}))
+    elif name == PINSAGE:  # models.py:144-155
+        layers = []
+        for i, o in pairs:
+            W = _mat(rng, o, 2 * i, dt)
+            Q = _mat(rng, i, i, dt)
+            layers.append(LayerWeights(i, o, {"W": W, "Q": Q, "q": _vec(rng, i, i, dt)}, {"alpha": 1.0}))
+    elif name == MONET:  # models.py:203-216
+        layers = []
+        for i, o in pairs:
+            seed_mat = rng.uniform(-1.0, 1.0, (i, i)) / math.sqrt(i)
+            kernel = (-(seed_mat @ seed_mat.T) / i).astype(dt)
+            W = _mat(rng, o, 1, dt)
+            layers.append(LayerWeights(i, o, {"W": W, "Wq": kernel, "mu": rng.uniform(-1.0, 1.0, i).astype(dt)}))
+    elif name == COMMNET:  # models.py:235-239
+        layers = []
+        for i, o in pairs:
+            W = _mat(rng, o, i, dt)
+            layers.append(LayerWeights(i, o, {"W": W, "W2": _mat(rng, o, i, dt)}))
+    elif name == GGCN:  # models.py:290-299
+        layers = []
+        for i, o in pairs:
+            W = _mat(rng, o, i, dt)
+            Ws = _mat(rng, i, i, dt)
+            layers.append(LayerWeights(i, o, {"W": W, "Wg_src": Ws, "Wg_dst": _mat(rng, i, i, dt)}))
+    elif name == AGNN:  # models.py:320-324
+        layers = []
+        for i, o in pairs:
+            W = _mat(rng, o, i, dt)
+            layers.append(LayerWeights(i, o, {"W": W}, {"beta": float(rng.uniform(0.5, 1.5))}))
     else:  # GAT models.py:256-260
         layers = []
         for li, (i, o) in enumerate(pairs):
@@ -138,8 +186,14 @@ def make_bundle(model: str, dims: Sequence[int], *, dtype=np.float64, rng_seed: 
                       degree_offset=1.0 if degree_smoothing else 0.0)
     if name == GRAPHSAGE:  # :131-141
         return Bundle(name, tuple(layers), dt, tuple(dims[:-1]), "count")
-    if name in GIN_FAMILY:  # :191-200
+    if name in GIN_FAMILY or name == COMMNET:  # :191-200, :240-249
         return Bundle(name, tuple(layers), dt, tuple(dims[:-1]), "none")
+    if name == PINSAGE:  # :165-175
+        return Bundle(name, tuple(layers), dt, tuple(dims[:-1]), "count")
+    if name == MONET:  # :218-227 (scalar aggregate)
+        return Bundle(name, tuple(layers), dt, (1,) * len(pairs), "none")
+    if name in (GGCN, AGNN):  # :307-317, :337-347
+        return Bundle(name, tuple(layers), dt, tuple(dims[:-1]), "none", dest_dependent=True)
     return Bundle(name, tuple(layers), dt, tuple(dims[1:]), "sum", dest_dependent=True, heads=int(heads))
 
 

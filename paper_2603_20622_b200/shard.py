@@ -39,7 +39,7 @@ from . import _lib
 from . import errors as E
 from .engine import Metrics, RTECEngine, RunResult
 from .graph import DynamicGraph
-from .models import GAT
+from .models import GAT, PROJECTED
 
 _U64 = (1 << 64) - 1
 
@@ -105,6 +105,8 @@ class ShardedRTECEngine(RTECEngine):
 
     def __init__(self, bundle, num_vertices: int, edges, features, comm: Comm, *, max_batch: int | None = None,
                  update: str = "tc", reserve: int | None = None, device=None, exchange_chunk: int = 1 << 20):
+        if bundle.model in PROJECTED:  # payload / gate caches are not exchanged between shards
+            raise E.UnsupportedModel(f"sharded engine: model {bundle.model!r} not supported")
         self.comm = comm
         P, r = comm.world, comm.rank
         n = int(num_vertices)

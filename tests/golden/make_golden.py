@@ -192,6 +192,8 @@ def model_case(name, model, dims, smoothing=True, heads=1, n=100, m=600, nb=6, B
         for l, w in enumerate(bundles[0].layers):
             for k, t in w.tensors.items():
                 out[f"w{l}_{k}"] = t
+            for k, v in w.scalars.items():
+                out[f"w{l}_{k}"] = np.float64(v)
     else:
         bundles = None
         hb = {}
@@ -227,7 +229,14 @@ def model_case(name, model, dims, smoothing=True, heads=1, n=100, m=600, nb=6, B
     print(f"models_{name}.npz written")
 
 
+TABLE2 = (("pinsage", [12, 16, 8]), ("monet", [8, 12, 6]), ("commnet", [12, 16, 8]), ("ggcn", [12, 16, 8]),
+          ("agnn", [12, 16, 8]))
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["table2"]:  # only the remaining Table II models (models.py:144-348)
+        for name, dims in TABLE2:
+            model_case(name, name, dims)
+        sys.exit(0)
     graph_streams()
     coalesce_cases()
     model_case("gcn", "gcn", [16, 16, 8])
@@ -236,3 +245,5 @@ if __name__ == "__main__":
     model_case("gin", "gin", [16, 16, 8])
     model_case("gat", "gat", [16, 16, 8])
     model_case("gat_h4", "gat", [16, 16, 8], heads=4)
+    for name, dims in TABLE2:
+        model_case(name, name, dims)

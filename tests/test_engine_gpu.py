@@ -105,6 +105,26 @@ def test_engine_vs_oracle(P, model, dims):
     _run_vs_oracle(P, model, dims, n=4000, m=60000, B=400, nb=4, seed=3)
 
 
+TABLE2 = [("pinsage", [32, 48, 32]), ("monet", [32, 48, 16]), ("commnet", [32, 32, 32]), ("ggcn", [32, 48, 32]),
+          ("agnn", [32, 48, 32])]
+
+
+@pytest.mark.parametrize("model,dims", TABLE2)
+def test_table2_models_vs_oracle(P, model, dims):
+    # the rest of Table II (models.py:144-348) through the same frontier / delta / recompute
+    # kernels: payload models (PinSAGE, MoNet) via the projection cache and its log,
+    # dest-dependent G-GCN / A-GNN via per-edge retraction and R(l) recompute
+    _run_vs_oracle(P, model, dims, n=4000, m=60000, B=400, nb=4, seed=5)
+
+
+@pytest.mark.parametrize("model,dims", [("pinsage", [6, 10, 6]), ("ggcn", [6, 10, 6]), ("agnn", [5, 7, 3]),
+                                        ("commnet", [6, 10, 6]), ("monet", [6, 10, 6])])
+@pytest.mark.parametrize("update", ["tc", "simt"])
+def test_table2_odd_widths(P, model, dims, update):
+    # widths off the 128-bit lane layout (scalar lanes) and both update GEMMs
+    _run_vs_oracle(P, model, dims, n=1500, m=20000, B=200, nb=3, seed=6, update=update)
+
+
 @pytest.mark.parametrize("model", ["gcn", "gin"])
 def test_engine_simt_update_path(P, model):
     # the SIMT fp32 update (used for d_out > 256 and GAT projections) stays parity-green
@@ -197,7 +217,7 @@ def test_query_and_errors(P):
     with pytest.raises(P.InvalidVertex):
         eng.step(np.array([0], np.uint8), np.array([0]), np.array([n]), np.array([0]))
     with pytest.raises(P.UnsupportedModel):
-        P.make_bundle("monet", [4, 4])
+        P.make_bundle("broken-mean", [4, 4])
 
 
 def test_cuda_graph_replay_matches_eager(P):
@@ -322,7 +342,8 @@ def test_checkpoint_resume(P, model, heads, tmp_path):
 
 @pytest.mark.parametrize("model,dims,heads", [("gcn", [24, 32, 16], 1), ("graphsage", [24, 32, 16], 1),
                                               ("gin", [16, 16, 16, 16], 1), ("gat", [24, 32, 32], 2),
-                                              ("gin_max", [16, 24, 16], 1)])
+                                              ("gin_max", [16, 24, 16], 1), ("pinsage", [16, 24, 16], 1),
+                                              ("ggcn", [16, 24, 16], 1)])
 def test_odec_queries_match_full_recompute(P, model, dims, heads):
     # SPEC run_odec: batches only mark deferred rows; a query recomputes the
     # deferred part of its L-hop in-subgraph and returns rows equal to a full recompute;

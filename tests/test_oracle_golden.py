@@ -17,8 +17,7 @@ from oracle.graph import OracleError, OracleGraph, coalesce_batch, invert_batch
 
 
 def _model_of(case):
-    return {"gcn": "gcn", "gcn_raw": "gcn", "graphsage": "graphsage", "gin": "gin",
-            "gat": "gat", "gat_h4": "gat"}[case]
+    return {"gcn_raw": "gcn", "gat_h4": "gat"}.get(case, case)
 
 
 def _bundle(case, z):
@@ -109,6 +108,8 @@ def test_weights_bit_identical(case):
             else:
                 for k in b.layers[l]:
                     assert np.array_equal(b.layers[l][k], z[f"w{l}_{k}"]), (l, k)
+                assert sorted(b.layers[l]) == sorted(k[len(f"w{l}_"):] for k in z.files
+                                                     if k.startswith(f"w{l}_") and "degree_offset" not in k), l
         else:
             for h in range(int(z["heads"])):
                 assert np.array_equal(b.layers[l]["Wh"][h], z[f"w{l}_h{h}_W"])
