@@ -16,6 +16,9 @@ from .graph import (  # noqa: F401
 from .models import MODELS, Bundle, LayerWeights, from_reference, make_bundle  # noqa: F401
 from .engine import Metrics, RTECEngine, RunResult, redundancy  # noqa: F401
 
-from .formats import load_checkpoint, load_weights, read_tensor, save_checkpoint, save_weights, write_tensor  # noqa: F401
+from .formats import (  # noqa: F401
+    load_checkpoint, load_sharded_checkpoint, load_weights, read_tensor, save_checkpoint, save_sharded_checkpoint,
+    save_weights, write_tensor,
+)
 
 __version__ = "0.1.0"

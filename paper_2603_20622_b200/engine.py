@@ -50,16 +50,24 @@ class Metrics:
     as_vertices: int = 0                         # Σ_l |V_dst(l)|
 
 
-def redundancy(m: Metrics, num_edges: int, num_vertices: int) -> dict:
-    """Access volume of each strategy relative to the affected subgraph (PAPER.md:165-191,
-    Fig. 2 / Table V): FN = full-neighbour recompute of every layer, UER = affected rows over
-    their full in-neighbourhoods, Inc = the incremental engine (exactly the affected edges)."""
+def redundancy(m: Metrics, num_edges: int, num_vertices: int, breakdown: dict | None = None) -> dict:
+    """SPEC cmd_redundancy_report: access volume of each strategy relative to
+    the affected subgraph (Fig. 2 / Table V): FN = full-neighbour recompute of
+    every layer, UER = affected rows over their full in-neighbourhoods, Inc = the incremental
+    engine (exactly the affected edges); `redundant_share` = the part of FN's accesses outside
+    the affected subgraph.  `breakdown` (RTECEngine.degree_breakdown) adds the per
+    degree-class volumes."""
     L = len(m.e_curr)
     a = max(m.as_edges, 1)
-    return {"as_edges": m.as_edges, "as_vertices": m.as_vertices,
-            "fn_edges": L * int(num_edges), "uer_edges": sum(m.in_edges_vdst), "inc_edges": sum(m.e_curr),
-            "fn_over_as": L * int(num_edges) / a, "uer_over_as": sum(m.in_edges_vdst) / a,
-            "inc_over_as": sum(m.e_curr) / a, "fn_vertices": L * int(num_vertices)}
+    fn = L * int(num_edges)
+    out = {"as_edges": m.as_edges, "as_vertices": m.as_vertices,
+           "fn_edges": fn, "uer_edges": sum(m.in_edges_vdst), "inc_edges": sum(m.e_curr),
+           "fn_over_as": fn / a, "uer_over_as": sum(m.in_edges_vdst) / a,
+           "inc_over_as": sum(m.e_curr) / a, "fn_vertices": L * int(num_vertices),
+           "redundant_share": (fn - m.as_edges) / fn if fn else 0.0}
+    if breakdown is not None:
+        out["degree_classes"] = breakdown
+    return out
 
 
 @dataclass
@@ -660,6 +668,54 @@ class RTECEngine:
             m.n_src.append(int(c[2]))
             m.in_edges_vdst.append(int(c[5]))
         return m
+
+    def degree_breakdown(self, shares=(0.2, 0.3, 0.5)) -> dict:
+        """Table V / SPEC.md:564 degree-percentile breakdown of the LAST batch's edge accesses:
+        vertices ranked by in-degree (descending, ties by id) into top 20 % / mid 30 % /
+        bottom 50 %; each edge access is charged to its destination's class.  FN = every
+        in-edge at every layer, UER = in-runs of V_dst(l), Inc = E_curr(l) (G_post out-edges of
+        S(l), plus applied inserts from other sources and deletes).  Device torch ops over
+        the frontier lists and adjacency; Σ over classes of `inc` equals Σ_l |E_curr(l)|."""
+        n, L, dev = self.n, self.L, self.dev
+        gr = self.g
+        indeg = gr.in_deg[:n].to(torch.int64)
+        order = torch.argsort(-indeg, stable=True)
+        cls = torch.empty(n, dtype=torch.int64, device=dev)
+        cuts = np.ceil(np.cumsum(shares) * n).astype(np.int64).tolist()
+        lo = 0
+        for c, hi in enumerate(cuts):
+            cls[order[lo:min(hi, n)]] = c
+            lo = min(hi, n)
+        nc = len(shares)
+        cnt = lambda idx, w=None: torch.bincount(cls[idx], weights=w, minlength=nc)  # noqa: E731
+        fn = L * torch.bincount(cls, weights=indeg.to(torch.float64), minlength=nc)
+        uer = torch.zeros(nc, dtype=torch.float64, device=dev)
+        inc = torch.zeros(nc, dtype=torch.float64, device=dev)
+        b = gr.batch
+        na = int(b.n_applied.item())
+        a_src, a_dst = b.a_src[:na].to(torch.int64), b.a_dst[:na].to(torch.int64)
+        ins = b.a_op[:na] == _lib.OP_INSERT
+        for l in range(L):
+            f = self.fr[l]
+            ns, nd = int(f.n_src.item()), int(f.n_dst.item())
+            S = f.src_list[:ns].to(torch.int64)
+            V = f.dst_list[:nd].to(torch.int64)
+            uer += cnt(V, indeg[V].to(torch.float64))
+            lens = gr.out.len[S].to(torch.int64)
+            tot = int(lens.sum().item()) if ns else 0
+            if tot:
+                start = torch.repeat_interleave(gr.out.beg[S] - (torch.cumsum(lens, 0) - lens), lens)
+                w = gr.out.nbr[start + torch.arange(tot, device=dev)].to(torch.int64)
+                inc += cnt(w).to(torch.float64)
+            in_s = torch.zeros(n, dtype=torch.bool, device=dev)
+            in_s[S] = True
+            inc += cnt(a_dst[ins & ~in_s[a_src]]).to(torch.float64)
+            inc += cnt(a_dst[~ins]).to(torch.float64)
+        names = [f"{'top' if i == 0 else 'bottom' if i == nc - 1 else 'mid'}{round(100 * x)}" for i, x in enumerate(shares)]
+        fn_, uer_, inc_ = (x.cpu().numpy() for x in (fn, uer, inc))
+        return {"classes": names, "fn_edges": fn_.astype(np.int64).tolist(), "uer_edges": uer_.astype(np.int64).tolist(),
+                "inc_edges": inc_.astype(np.int64).tolist(),
+                "fn_over_inc": [float(a / c) if c else None for a, c in zip(fn_, inc_)]}
 
     def frontier(self, l: int):
         """(V_dst(l), S(l)) ascending id arrays of the last batch."""

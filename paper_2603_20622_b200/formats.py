@@ -10,6 +10,10 @@
   JSON sidecar): the edge list, every layer's embeddings and un-normalised
   aggregates (and GAT attention sums), the weights, and the model config, so a
   long stream can restart without a bootstrap.
+- Sharded checkpoint: one `rank<r>/` directory per rank
+  holding that rank's edge shard, its replica layer inputs, its owned rows of
+  the final layer / aggregates / contexts, and the same sidecar plus the world
+  size; every rank writes and reads only its own directory (no collective).
 
 Host-side IO only; nothing here is on the timed path.
 """
@@ -157,4 +161,65 @@ def load_checkpoint(directory: str, **engine_kw):
             eng.ctx[l].copy_(torch.from_numpy(read_tensor(os.path.join(directory, f"ctx{l}.nrtf"))))
         if eng.Z[l] is not None:  # GAT projections are a function of H: recompute them
             eng.refresh_projection(l)
+    return eng
+
+
+# ---------------------------------------------------------------- sharded checkpoint
+def _rank_dir(directory: str, rank: int) -> str:
+    return os.path.join(directory, f"rank{rank:04d}")
+
+
+def save_sharded_checkpoint(engine, directory: str) -> None:
+    """Per-rank snapshot of a ShardedRTECEngine between batches (call on every rank)."""
+    r, P = engine.comm.rank, engine.comm.world
+    d = _rank_dir(directory, r)
+    os.makedirs(d, exist_ok=True)
+    src, dst, ts = engine.g.edges()  # this rank's shard: the edges whose destination it owns
+    write_tensor(os.path.join(d, "edges.nrtf"), np.stack([src, dst, ts], 1).astype(np.float64))
+    for l in range(engine.L + 1):  # inputs are full replicas, the final layer per owned vertex
+        write_tensor(os.path.join(d, f"H{l}.nrtf"), engine.H[l].cpu().numpy())
+    for l in range(engine.L):
+        write_tensor(os.path.join(d, f"S{l}.nrtf"), engine.S[l].cpu().numpy())
+        if engine.ctx[l] is not None:
+            write_tensor(os.path.join(d, f"ctx{l}.nrtf"), engine.ctx[l].cpu().numpy())
+    b = engine.b
+    save_weights(b, os.path.join(d, "weights.json"))
+    side = {"format": "rtec-b200-sharded-checkpoint", "version": 1, "model": b.model, "dims": list(b.dims),
+            "heads": int(b.heads), "degree_offset": float(b.degree_offset), "num_vertices": int(engine.n),
+            "world_size": int(P), "rank": int(r), "num_edges_shard": int(len(src))}
+    with open(os.path.join(d, "checkpoint.json"), "w", encoding="ascii") as fh:
+        json.dump(side, fh, indent=1)
+        fh.write("\n")
+
+
+def load_sharded_checkpoint(directory: str, comm, **engine_kw):
+    """Rebuild this rank's ShardedRTECEngine from `save_sharded_checkpoint` (collective:
+    the constructor all-reduces the global degrees).  The world size must match."""
+    import torch
+
+    from .models import make_bundle
+    from .shard import ShardedRTECEngine
+
+    d = _rank_dir(directory, comm.rank)
+    with open(os.path.join(d, "checkpoint.json"), "r", encoding="ascii") as fh:
+        side = json.load(fh)
+    if side.get("format") != "rtec-b200-sharded-checkpoint":
+        raise E.ConfigError(f"{d}: not an rtec-b200 sharded checkpoint")
+    if int(side["world_size"]) != comm.world or int(side["rank"]) != comm.rank:
+        raise E.ConfigError(f"{d}: saved by rank {side['rank']} of {side['world_size']}, "
+                            f"loading on rank {comm.rank} of {comm.world}")
+    w = load_weights(os.path.join(d, "weights.json"))
+    bundle = make_bundle(side["model"], side["dims"], weights=w["layers"], heads=side["heads"],
+                         degree_smoothing=side["degree_offset"] != 0.0)
+    e = read_tensor(os.path.join(d, "edges.nrtf")).astype(np.int64)
+    X = read_tensor(os.path.join(d, "H0.nrtf"))
+    eng = ShardedRTECEngine(bundle, side["num_vertices"], (e[:, 0], e[:, 1], e[:, 2]), X, comm, bootstrap=False,
+                            **engine_kw)
+    for l in range(1, eng.L + 1):
+        eng.H[l].copy_(torch.from_numpy(read_tensor(os.path.join(d, f"H{l}.nrtf"))))
+    for l in range(eng.L):
+        eng.S[l].copy_(torch.from_numpy(read_tensor(os.path.join(d, f"S{l}.nrtf"))))
+        if eng.ctx[l] is not None:
+            eng.ctx[l].copy_(torch.from_numpy(read_tensor(os.path.join(d, f"ctx{l}.nrtf"))))
+        eng.refresh_projection(l)  # GAT Z / el / er of every replica row from H^l
     return eng

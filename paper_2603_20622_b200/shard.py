@@ -104,7 +104,8 @@ class ShardedRTECEngine(RTECEngine):
     FUSED_DELTA = False  # the halo exchange ships new rows and rebuilds the DeltaLog on receipt
 
     def __init__(self, bundle, num_vertices: int, edges, features, comm: Comm, *, max_batch: int | None = None,
-                 update: str = "tc", reserve: int | None = None, device=None, exchange_chunk: int = 1 << 20):
+                 update: str = "tc", reserve: int | None = None, device=None, exchange_chunk: int = 1 << 20,
+                 bootstrap: bool = True):
         if bundle.model in PROJECTED:  # payload / gate caches are not exchanged between shards
             raise E.UnsupportedModel(f"sharded engine: model {bundle.model!r} not supported")
         self.comm = comm
@@ -134,7 +135,7 @@ class ShardedRTECEngine(RTECEngine):
         self.owned = torch.arange(r, n, P, dtype=torch.int32, device=dev)
         self.n_owned = torch.tensor([self.owned.numel()], dtype=torch.int64, device=dev)
         self.glog = []  # per exchanged layer: DeltaLog rows of V_chg(l) in exchange order
-        super().__init__(bundle, g, features, max_batch=max_batch, update=update)
+        super().__init__(bundle, g, features, max_batch=max_batch, update=update, bootstrap=bootstrap)
 
     # ---------------------------------------------------------------- plumbing
     def _mg(self) -> _lib.Graph:
@@ -379,6 +380,19 @@ class ShardedRTECEngine(RTECEngine):
         return out.cpu().numpy()
 
     materialize_h = query
+
+    def save(self, directory: str) -> None:
+        """Per-rank checkpoint (formats.save_sharded_checkpoint); call on every rank."""
+        from .formats import save_sharded_checkpoint
+
+        save_sharded_checkpoint(self, directory)
+
+    @staticmethod
+    def load(directory: str, comm: Comm | None = None, **kw) -> "ShardedRTECEngine":
+        """Resume this rank's shard (formats.load_sharded_checkpoint); collective."""
+        from .formats import load_sharded_checkpoint
+
+        return load_sharded_checkpoint(directory, comm if comm is not None else Comm(), **kw)
 
     def aggregates(self, l: int):
         raise E.ConfigError("aggregates() of a sharded engine: read owned rows of S[l] on each rank")

@@ -384,3 +384,45 @@ def test_odec_queries_match_full_recompute(P, model, dims, heads):
     assert rowwise_rel(eng.embeddings(L), oe.H[L]) <= TOL
     with pytest.raises(P.InvalidVertex):
         eng.odec_query([n])
+
+
+def test_redundancy_degree_breakdown(P):
+    # SPEC cmd_redundancy_report (Table V): per degree-class FN / UER / Inc
+    # volumes sum to the global counters, obey Inc <= UER <= FN per class, and match a
+    # host recount from the frontier lists and the post-batch edge list
+    from paper_2603_20622_b200.workload import UpdateStream, chung_lu_edges, features
+
+    n = 3000
+    s, d = chung_lu_edges(n, 40000, seed=41)
+    stream = UpdateStream(s, d, holdout=0.1, seed=41)
+    bs, bd, bt = stream.base()
+    eng = P.RTECEngine(P.make_bundle("gcn", [16, 16, 16]), P.DynamicGraph.from_edges(n, (bs, bd, bt)),
+                       features(n, 16, seed=2))
+    for _ in range(2):
+        op, s1, d1, t1 = stream.next_batch(300)
+        r = eng.step(op, s1, d1, t1)
+        br = eng.degree_breakdown()
+        rep = P.redundancy(r.metrics, eng.g.num_edges, n, br)
+        assert sum(br["inc_edges"]) == sum(r.metrics.e_curr)
+        assert sum(br["uer_edges"]) == sum(r.metrics.in_edges_vdst)
+        assert sum(br["fn_edges"]) == 2 * eng.g.num_edges
+        for c in range(3):
+            assert br["inc_edges"][c] <= br["uer_edges"][c] <= br["fn_edges"][c]
+        assert 0.0 < rep["redundant_share"] < 1.0
+        # host recount
+        es, ed, _ = eng.g.edges()
+        indeg = np.bincount(ed, minlength=n)
+        order = np.lexsort((np.arange(n), -indeg))
+        cls = np.empty(n, np.int64)
+        cls[order[:600]], cls[order[600:1500]], cls[order[1500:]] = 0, 1, 2
+        st = r.status.astype(bool)
+        ins = st & (op == 0)
+        dele = st & (op == 1)
+        inc = np.zeros(3, np.int64)
+        for l in range(2):
+            _, S = eng.frontier(l)
+            ins_S = np.isin(es, S)
+            inc += np.bincount(cls[ed[ins_S]], minlength=3)
+            inc += np.bincount(cls[d1[ins & ~np.isin(s1, S)]], minlength=3)
+            inc += np.bincount(cls[d1[dele]], minlength=3)
+        assert inc.tolist() == br["inc_edges"]

@@ -69,6 +69,11 @@ def _rank_main(rank, world, port, cfg, out_dir):
         for l in range(L):
             res[f"vdst{i}_{l}"] = eng.frontier(l)[0]
             res[f"ecurr{i}_{l}"] = np.array(r.metrics.e_curr[l])
+        if cfg.get("ckpt") and i == 0:  # per-rank checkpoint, then resume without a bootstrap
+            ck = os.path.join(out_dir, "ck")
+            eng.save(ck)
+            dist.barrier()
+            eng = ShardedRTECEngine.load(ck, Comm(), max_batch=cfg["B"])
     for l in range(L + 1):
         res[f"H{l}"] = eng.embeddings(l)
     ids = np.arange(0, cfg["n"], 7)
@@ -135,3 +140,9 @@ def test_sharded_nccl_single_rank():
     # one rank over NCCL: the device-tensor collective path the multi-GPU bench runs
     # (all_gather_into_tensor of ids / rows, uint8 MAX and int32 SUM all-reduces)
     _run(dict(model="gcn", dims=[32, 48, 32], n=3000, m=40000, B=300, nb=3, seed=24, backend="nccl"), world=1)
+
+
+@pytest.mark.parametrize("model,heads", [("gcn", 1), ("gat", 2)])
+def test_sharded_checkpoint_resume(model, heads):
+    # each rank saves / restores its own shard between batches
+    _run(dict(model=model, dims=[24, 32, 16], n=2500, m=30000, B=250, nb=3, seed=26, heads=heads, ckpt=True))
