@@ -350,6 +350,143 @@ __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_light(Laye
   }
 }
 
+// Warp-batched incremental light pass: a warp takes 32 consecutive destinations
+// (one per lane for the metadata loads, all issued together), scans the in-runs
+// of a run of them as ONE flattened edge sequence (lane e finds its
+// destination by a shuffle binary search over the run offsets) and compacts
+// the ValueChange hits, in order, into a per-warp shared-memory window with
+// per-destination counts; then, destination by destination, gathers its hit
+// rows UNR at a time (the cached S row prefetched first), adds the structural
+// edges and finalises.  Per destination this replaces the dependent chain
+// metadata -> run -> bitmap -> rows of k_agg_light by batched loads, for the
+// scan-heavy layers (few hits among many scanned edges).  Summation order per
+// destination (run order, then structural edges) matches k_agg_light.
+constexpr int kBatchWin = kChunk;  // flattened edges per window: any light run fits one window
+
+template <int VEC, int K>
+__global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_batch(LayerArgs a, AggRows rows) {
+  using R = RowAcc<VEC, K>;
+  constexpr int UNR = (VEC * K <= 4) ? 8 : kUnroll;
+  __shared__ int32_t s_u[kLBlk / 32][kBatchWin];
+  __shared__ int32_t s_c[kLBlk / 32][32];
+  if (err_set(a.err)) return;
+  const int64_t nr = rows.count();
+  const bool scan = *a.f.n_src > 0;
+  const int lane = lane_id();
+  const int wib = threadIdx.x >> 5;
+  int32_t* hu = s_u[wib];
+  int32_t* hc = s_c[wib];
+  const int d = a.d_agg, cw = a.cw;
+  const float* base = a.delta + a.c0;
+  const int64_t ngroups = (nr + 31) >> 5;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t grp = warp; grp < ngroups; grp += nw) {
+    const int64_t i0 = grp << 5;
+    const int nd = static_cast<int>(nr - i0 < 32 ? nr - i0 : 32);
+    int32_t v = 0, len = 0, indeg = 0, had = 0, p = 0, q = 0;
+    int64_t beg = 0;
+    bool live = lane < nd;
+    if (live) {
+      v = rows.at(i0 + lane);
+      len = a.g.in.len[v];
+      beg = a.g.in.beg[v];
+      const int2 rg = reinterpret_cast<const int2*>(a.b.irange)[v];
+      indeg = a.g.in_deg[v];
+      had = a.g.in_deg_prev[v];
+      if (rg.x >= 0) {
+        p = rg.x;
+        q = rg.x + rg.y;
+      }
+      if (scan && len > kChunk) live = false;  // heavy pass owns it
+    }
+    const int32_t slen = (live && scan) ? len : 0;
+    int32_t end = slen;  // inclusive scan: end of this lane's run in the flattened sequence
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t t = __shfl_up_sync(0xffffffffu, end, o);
+      if (lane >= o) end += t;
+    }
+    const int32_t off = end - slen;
+    const unsigned live_mask = __ballot_sync(0xffffffffu, live);
+    int j0 = 0;
+    while (j0 < nd) {
+      // window [j0, j1): the longest run of destinations whose edges fit kBatchWin
+      const int32_t w0 = __shfl_sync(0xffffffffu, off, j0);
+      const unsigned fit = __ballot_sync(0xffffffffu, lane >= j0 && lane < nd && end - w0 <= kBatchWin);
+      const int j1 = max(j0 + 1, 32 - __clz(fit));  // fit is a prefix of [j0, nd) (ends grow)
+      const int32_t w1 = __shfl_sync(0xffffffffu, end, j1 - 1);
+      hc[lane] = 0;
+      __syncwarp();
+      int nh = 0;
+      for (int32_t e0 = w0; e0 < w1; e0 += 32) {
+        const int32_t e = e0 + lane;
+        int lo = j0;  // last destination j in [j0, j1) with off_j <= e
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const int cand = lo + step;
+          const int32_t oc = __shfl_sync(0xffffffffu, off, cand & 31);
+          if (cand < j1 && oc <= e) lo = cand;
+        }
+        const int64_t bj = __shfl_sync(0xffffffffu, beg, lo);
+        const int32_t oj = __shfl_sync(0xffffffffu, off, lo);
+        const int32_t pj = __shfl_sync(0xffffffffu, p, lo);
+        const int32_t qj = __shfl_sync(0xffffffffu, q, lo);
+        bool hit = false;
+        int32_t u = 0;
+        if (e < w1) {
+          u = a.g.in.nbr[bj + (e - oj)];
+          hit = bm_test(a.f.bm_src, u) && !in_range_has(a.b.i_src, pj, qj, u);
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+          hu[nh + __popc(m & ((1u << lane) - 1u))] = a.st.delta_slot ? a.f.src_slot[u] : u;
+          atomicAdd(hc + lo, 1);
+        }
+        nh += __popc(m);
+      }
+      __syncwarp();
+      int32_t hs = hc[lane];  // exclusive scan of the per-destination hit counts
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t t = __shfl_up_sync(0xffffffffu, hs, o);
+        if (lane >= o) hs += t;
+      }
+      hs -= hc[lane];
+      for (int j = j0; j < j1; ++j) {
+        if (!((live_mask >> j) & 1u)) continue;
+        const int32_t vj = __shfl_sync(0xffffffffu, v, j);
+        const int32_t lj = __shfl_sync(0xffffffffu, len, j);
+        const int32_t ij = __shfl_sync(0xffffffffu, indeg, j);
+        const int32_t dj = __shfl_sync(0xffffffffu, had, j);
+        const int32_t pj = __shfl_sync(0xffffffffu, p, j);
+        const int32_t qj = __shfl_sync(0xffffffffu, q, j);
+        const int32_t h0 = __shfl_sync(0xffffffffu, hs, j);
+        const int32_t h1 = h0 + hc[j];
+        R sv;
+        sv.zero();
+        if (ij > 0 && dj > 0) R::load_stream(a.st.S + srow(a, vj) * d + a.c0, cw, sv.v, l2_evict_first_policy());
+        R acc;
+        acc.zero();
+        for (int32_t k0 = h0; k0 < h1; k0 += UNR) {
+          const int cnt = min(UNR, h1 - k0);
+          float r[UNR][K][VEC];
+#pragma unroll
+          for (int t = 0; t < UNR; ++t)
+            if (t < cnt) R::load(base + static_cast<int64_t>(hu[k0 + t]) * d, cw, r[t]);
+#pragma unroll
+          for (int t = 0; t < UNR; ++t)
+            if (t < cnt) acc.add(r[t]);
+        }
+        agg_struct<VEC, K>(a, pj, qj, acc);
+        agg_finalize<VEC, K, false>(a, i0 + j, vj, lj, acc, &sv, ij);
+      }
+      __syncwarp();
+      j0 = j1;
+    }
+  }
+}
+
 template <int VEC, int K, bool FULL>
 __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
   using R = RowAcc<VEC, K>;
@@ -451,6 +588,16 @@ static int agg_slice_width() {
   return w;
 }
 
+// RTEC_AGG_BATCH env: rows up to this width use the warp-batched light pass (0: never)
+static bool agg_batched(int d) {
+  static int b = -1;
+  if (b < 0) {
+    const char* e = getenv("RTEC_AGG_BATCH");
+    b = e ? atoi(e) : 128;
+  }
+  return d <= b;
+}
+
 // heavy-destination plan (list, chunk offsets, chunk -> heavy map); partial rows of `pw` floats
 template <bool FULL>
 static int plan_heavy(const LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_edges, int pw, Ws& w,
@@ -509,8 +656,11 @@ static int launch_aggregation(LayerArgs& a, AggRows rows, int64_t max_rows, int6
     }
     {
       RTEC_PROF(FULL ? "k_agg_full_light" : "k_agg_inc", s);
-      ok = ok && (sliced ? RTEC_SLICE_DISPATCH(a.cw, (k_agg_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows)))
-                         : RTEC_ROW_DISPATCH(a.cw, (k_agg_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows))));
+      if (!FULL && !sliced && agg_batched(a.cw))
+        ok = ok && RTEC_ROW_DISPATCH(a.cw, (k_agg_batch<VEC, K><<<grid, kLBlk, 0, s>>>(a, rows)));
+      else
+        ok = ok && (sliced ? RTEC_SLICE_DISPATCH(a.cw, (k_agg_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows)))
+                           : RTEC_ROW_DISPATCH(a.cw, (k_agg_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows))));
     }
     if (hs != s) {
       RTEC_CUDA(cudaEventRecord(side_join(), hs));

@@ -426,3 +426,20 @@ def test_redundancy_degree_breakdown(P):
             inc += np.bincount(cls[d1[ins & ~np.isin(s1, S)]], minlength=3)
             inc += np.bincount(cls[d1[dele]], minlength=3)
         assert inc.tolist() == br["inc_edges"]
+
+
+@pytest.mark.parametrize("batch", ["0", "4096"])
+def test_light_pass_variants(P, batch):
+    # the one-destination-per-warp light pass (RTEC_AGG_BATCH=0) and the warp-batched pass
+    # for every width (4096) stay parity-green; the env is read once per process
+    import os
+    import subprocess
+    import sys
+
+    code = ("import sys; sys.path.insert(0, 'tests'); import test_engine_gpu as t, paper_2603_20622_b200 as P; "
+            "t._run_vs_oracle(P, 'gcn', [48, 256, 32], n=3000, m=40000, B=300, nb=3, seed=8); "
+            "t._run_vs_oracle(P, 'graphsage', [24, 40, 16], n=3000, m=40000, B=300, nb=3, seed=9); print('ok')")
+    root = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, "RTEC_AGG_BATCH": batch},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
