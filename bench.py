@@ -192,7 +192,7 @@ def algorithmic_bytes(name: str, wl: dict, layer_counters, n: int) -> float:
     d_a = wl["dims"][int(l)]
     d_o = wl["dims"][int(l) + 1]
     f = 4.0
-    if name == "k_agg_inc":
+    if name == "aggregation":
         # in-run ids of V_dst + S-bitmap + δ rows once + S read/write + composed row write + list/offsets
         return 4 * sum_in + n / 8 + f * d_a * n_src + 3 * f * d_a * v_dst + 16 * v_dst
     if name == "k_src_delta":
@@ -371,28 +371,22 @@ def run_ours(args, world, rank, local):
     peak_src = "measured" if from_peaks else "fallback"
     C = ctrs.cpu().numpy()
     # the eager profiled pass: total of the bracketed library scopes (nested scopes excluded)
-    prof_step_ms = sum(ms for name, (cnt, ms) in prof.items() if name not in ("adj_merge", "k_expand"))
+    nested = ("adj_merge", "k_expand", "k_agg_inc", "k_agg_inc_heavy", "k_hit_compact", "k_agg_sliced")
+    prof_step_ms = sum(ms for name, (cnt, ms) in prof.items() if name not in nested)
     for l in range(L):
         C[:, l, 7] = l
     kernels = {}
     for name, (cnt, ms) in prof.items():
         per_launch_ms = ms / max(cnt, 1)
         byts = 0.0
-        if name in ("k_agg_inc", "k_src_delta", "k_gemm_update", "k_gemm_tc", "k_expand"):
+        if name in ("aggregation", "k_src_delta", "k_gemm_update", "k_gemm_tc", "k_expand"):
             byts = sum(algorithmic_bytes(name, wl, C[k, l], wl["n"]) for k in range(PROF) for l in range(L)) / max(cnt, 1)
         kernels[name] = {"launches": cnt, "total_ms": round(ms, 4), "ms_per_launch": round(per_launch_ms, 5),
                          "share": round(ms / max(prof_step_ms, 1e-9), 4),
                          "algo_GBps": round(byts / (per_launch_ms * 1e6), 1) if byts else None}
-    # the aggregation stage is two launches (light + heavy destinations): account them together
-    if "k_agg_inc" in kernels and "k_agg_inc_heavy" in kernels:
-        a, h = kernels["k_agg_inc"], kernels["k_agg_inc_heavy"]
-        tot = a["total_ms"] + h["total_ms"]
-        byts = (a["algo_GBps"] or 0) * a["ms_per_launch"] * 1e6
-        kernels["aggregation"] = {"launches": a["launches"], "total_ms": round(tot, 4),
-                                  "ms_per_launch": round(tot / a["launches"], 5),
-                                  "share": round(a["share"] + h["share"], 4),
-                                  "algo_GBps": round(byts / (tot / a["launches"] * 1e6), 1),
-                                  "kernels": "k_agg_inc (light) + k_agg_inc_heavy (hub chunks)"}
+    if "aggregation" in kernels:
+        kernels["aggregation"]["kernels"] = ("one scope per layer around the whole stage: k_agg_inc (light) + "
+                                             "k_agg_inc_heavy (hub chunks), or k_hit_compact + k_agg_sliced passes")
     hot = [k for k in ("aggregation", "k_gemm_tc", "k_gemm_update", "k_src_delta", "k_expand") if k in kernels]
     dom = max(hot, key=lambda k: kernels[k]["total_ms"]) if hot else None
     roof = None

@@ -1918,7 +1918,10 @@ int rtec_layer_incremental(const rtec_graph_t* g, const rtec_batch_t* b, const r
     set_error("row width %d unsupported", a.d_agg);
     return RTEC_SHAPE_ERROR;
   }
-  RTEC_TRY(launch_aggregation<false>(a, AggRows{f->dst_list, f->n_dst, n}, n, g->in.slots, w, s));
+  {
+    RTEC_PROF("aggregation", s);  // the whole stage (plan + light / heavy, or compaction + slice passes)
+    RTEC_TRY(launch_aggregation<false>(a, AggRows{f->dst_list, f->n_dst, n}, n, g->in.slots, w, s));
+  }
   // update on V_dst(l) rows with DeltaLog capture (operators.py:180)
   return run_update(g, L, st, f->n_dst, n, f->dst_list, st->log_out, err, s);
 }

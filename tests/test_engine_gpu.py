@@ -443,3 +443,4 @@ def test_light_pass_variants(P, batch):
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, "RTEC_AGG_BATCH": batch},
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
