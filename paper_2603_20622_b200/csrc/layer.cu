@@ -276,7 +276,7 @@ struct HeavyPlan {
 // resident CTAs per SM: wide rows need the registers (no spills)
 template <int VEC, int K>
 struct AggOcc {
-  static constexpr int value = (VEC * K <= 8) ? 4 : 2;
+  static constexpr int value = (VEC * K <= 8) ? 4 : 2;  // measured: 3 CTAs for VEC*K = 8 (no spills) is slower
 };
 
 // acc += rows 0..nch-1 (stride `stride` floats, width w) in row order, 4 rows in flight:
@@ -366,7 +366,7 @@ constexpr int kBatchWin = kChunk;  // flattened edges per window: any light run 
 template <int VEC, int K>
 __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_batch(LayerArgs a, AggRows rows) {
   using R = RowAcc<VEC, K>;
-  constexpr int UNR = (VEC * K <= 4) ? 8 : kUnroll;
+  constexpr int UNR = kUnroll;  // measured: 8 rows in flight spill next to the prefetched S row
   __shared__ int32_t s_u[kLBlk / 32][kBatchWin];
   __shared__ int32_t s_c[kLBlk / 32][32];
   if (err_set(a.err)) return;
@@ -453,19 +453,35 @@ __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_batch(Laye
         if (lane >= o) hs += t;
       }
       hs -= hc[lane];
-      for (int j = j0; j < j1; ++j) {
-        if (!((live_mask >> j) & 1u)) continue;
+      // destinations of the window in order; the cached S row of the next one is
+      // requested before this one's gathers (one DRAM latency hidden per destination)
+      const unsigned wm = live_mask & (j1 >= 32 ? 0xffffffffu : ((1u << j1) - 1u)) & ~((1u << j0) - 1u);
+      int jn = wm ? __ffs(wm) - 1 : 32;
+      R svn;
+      svn.zero();
+      if (jn < 32) {
+        const int32_t vn = __shfl_sync(0xffffffffu, v, jn);
+        if (__shfl_sync(0xffffffffu, indeg, jn) > 0 && __shfl_sync(0xffffffffu, had, jn) > 0)
+          R::load_stream(a.st.S + srow(a, vn) * d + a.c0, cw, svn.v, l2_evict_first_policy());
+      }
+      while (jn < 32) {
+        const int j = jn;
+        R sv = svn;
+        const unsigned rest = wm & ~(j >= 31 ? 0xffffffffu : ((2u << j) - 1u));
+        jn = rest ? __ffs(rest) - 1 : 32;
+        svn.zero();
+        if (jn < 32) {
+          const int32_t vn = __shfl_sync(0xffffffffu, v, jn);
+          if (__shfl_sync(0xffffffffu, indeg, jn) > 0 && __shfl_sync(0xffffffffu, had, jn) > 0)
+            R::load_stream(a.st.S + srow(a, vn) * d + a.c0, cw, svn.v, l2_evict_first_policy());
+        }
         const int32_t vj = __shfl_sync(0xffffffffu, v, j);
         const int32_t lj = __shfl_sync(0xffffffffu, len, j);
         const int32_t ij = __shfl_sync(0xffffffffu, indeg, j);
-        const int32_t dj = __shfl_sync(0xffffffffu, had, j);
         const int32_t pj = __shfl_sync(0xffffffffu, p, j);
         const int32_t qj = __shfl_sync(0xffffffffu, q, j);
         const int32_t h0 = __shfl_sync(0xffffffffu, hs, j);
         const int32_t h1 = h0 + hc[j];
-        R sv;
-        sv.zero();
-        if (ij > 0 && dj > 0) R::load_stream(a.st.S + srow(a, vj) * d + a.c0, cw, sv.v, l2_evict_first_policy());
         R acc;
         acc.zero();
         for (int32_t k0 = h0; k0 < h1; k0 += UNR) {
