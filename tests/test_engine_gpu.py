@@ -444,3 +444,54 @@ def test_light_pass_variants(P, batch):
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
+
+
+@pytest.mark.parametrize("model", ["gcn", "graphsage", "gin", "gat", "gin_max"])
+def test_edge_case_batches(P, model):
+    # empty batch, a batch whose updates are all rejected (duplicate inserts / absent
+    # deletes), deleting every in-edge of a vertex (zero in-degree rule)
+    # and re-inserting them, and self-loop insert / delete -- status, DegreeDelta,
+    # frontiers and embeddings vs the oracle after every batch
+    from oracle import models as OM
+    from oracle.engine import OracleEngine
+    from oracle.graph import OracleGraph
+    from paper_2603_20622_b200.workload import chung_lu_edges, features
+
+    n = 1000
+    s, d = chung_lu_edges(n, 30000, seed=21)  # hub in-degree 727: its deletion runs the chunked pass
+    dims = [16, 24, 16]
+    X = features(n, dims[0], seed=22)
+    eng = P.RTECEngine(P.make_bundle(model, dims), P.DynamicGraph.from_edges(n, (s, d)), X)
+    oe = OracleEngine(OM.make_bundle(model, dims), OracleGraph.from_edges(n, s, d), X.astype(np.float64))
+    ins, dele = 0, 1
+    v = int(np.bincount(d, minlength=n).argmax())  # the hub destination
+    hub_src = s[d == v]
+    absent = [(u, w) for u, w in zip(range(n), range(n - 1, -1, -1)) if u != w][:50]
+    eset = set(zip(s.tolist(), d.tolist()))
+    absent = [e for e in absent if e not in eset][:20]
+    loops = [u for u in range(0, n, 37) if (u, u) not in eset][:8]
+    batches = [
+        (np.zeros(0, np.uint8), np.zeros(0, np.int64), np.zeros(0, np.int64)),
+        (np.array([ins] * 10 + [dele] * len(absent), np.uint8),
+         np.concatenate([s[:10], [a for a, _ in absent]]), np.concatenate([d[:10], [b for _, b in absent]])),
+        (np.full(hub_src.size, dele, np.uint8), hub_src, np.full(hub_src.size, v)),
+        (np.full(hub_src.size, ins, np.uint8), hub_src, np.full(hub_src.size, v)),
+        (np.full(len(loops), ins, np.uint8), np.array(loops), np.array(loops)),
+        (np.full(len(loops), dele, np.uint8), np.array(loops), np.array(loops)),
+    ]
+    for bi, (op, bs, bd) in enumerate(batches):
+        ts = np.arange(op.size, dtype=np.int64) + 1000 * (bi + 1)
+        r = eng.step(op, bs, bd, ts)
+        o = oe.step(op, bs, bd, ts)
+        assert np.array_equal(r.status, o["status"]), bi
+        assert np.array_equal(r.deltas, o["deltas"]), bi
+        for l in range(len(dims) - 1):
+            vdst, _ = eng.frontier(l)
+            assert np.array_equal(vdst, o["frontier"][l]["vdst"]), (bi, l)
+            assert rowwise_rel(eng.embeddings(l + 1), oe.H[l + 1]) <= TOL, (bi, l)
+    if model != "gat":
+        # v has no in-edges after batch 2 in the oracle's replay too; its aggregate is exactly zero
+        eng2 = P.RTECEngine(P.make_bundle(model, dims), P.DynamicGraph.from_edges(n, (s, d)), X)
+        op, bs, bd = batches[2]
+        eng2.step(op, bs, bd, np.arange(op.size, dtype=np.int64))
+        assert not np.any(eng2.aggregates(0)[v])
