@@ -314,6 +314,7 @@ __device__ __forceinline__ void sum_partials(const float* part, int64_t stride, 
 template <int VEC, int K, bool FULL>
 __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_light(LayerArgs a, AggRows rows) {
   using R = RowAcc<VEC, K>;
+  __shared__ __align__(16) float s_sv[kLBlk / 32][(!FULL && VEC == 4) ? 32 * VEC * K : 4];
   if (!FULL && err_set(a.err)) return;
   const int64_t nr = rows.count();
   const bool scan = FULL || *a.f.n_src > 0;
@@ -338,14 +339,23 @@ __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_light(Laye
       q = rg.x + rg.y;
     }
     // the cached aggregate row, requested before the edge scan so its latency overlaps it
+    // (16-byte rows: staged in shared memory by cp.async, so it holds no registers --
+    // and is not spilled -- across the gather loop)
+    const bool pre = !FULL && indeg > 0 && had > 0;
     R sv;
     sv.zero();
-    if (!FULL && indeg > 0 && had > 0)
-      R::load_stream(a.st.S + srow(a, v) * a.d_agg + a.c0, a.cw, sv.v, l2_evict_first_policy());
+    if constexpr (VEC == 4) {
+      if (pre) R::stage_async(s_sv[threadIdx.x >> 5], a.st.S + srow(a, v) * a.d_agg + a.c0, a.cw, l2_evict_first_policy());
+    } else {
+      if (pre) R::load_stream(a.st.S + srow(a, v) * a.d_agg + a.c0, a.cw, sv.v, l2_evict_first_policy());
+    }
     R acc;
     acc.zero();
     if (scan) agg_edges<VEC, K, FULL>(a, beg, 0, len, p, q, acc);
     if (!FULL) agg_struct<VEC, K>(a, p, q, acc);
+    if constexpr (VEC == 4) {
+      if (pre) R::from_stage(s_sv[threadIdx.x >> 5], a.cw, sv.v);
+    }
     agg_finalize<VEC, K, FULL>(a, i, v, len, acc, FULL ? nullptr : &sv, indeg);
   }
 }

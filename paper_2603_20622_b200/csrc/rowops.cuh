@@ -45,6 +45,15 @@ __device__ __forceinline__ int32_t ld_stream_i32(const int32_t* a, uint64_t pol)
   return v;
 }
 
+// 16-byte global -> shared async copy with an L2 eviction-priority hint; completion
+// (cp_async_wait_all) makes it visible to the issuing thread
+__device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, uint64_t pol) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 template <int VEC, int K>
 struct RowAcc {
   float v[K][VEC];
@@ -72,6 +81,29 @@ struct RowAcc {
       } else {
 #pragma unroll
         for (int j = 0; j < VEC; ++j) r[k][j] = 0.f;
+      }
+    }
+  }
+  // row -> this lane's chunks of a shared-memory stage, asynchronously (VEC == 4): keeps a
+  // prefetched row out of registers across a gather loop; read back with from_stage
+  __device__ __forceinline__ static void stage_async(float* stage, const float* row, int d, uint64_t pol) {
+    static_assert(VEC == 4, "stage_async needs 16-byte chunks");
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      int c = lane_id() + 32 * k;
+      if (c * VEC < d) cp_async16_hint(stage + c * VEC, row + c * VEC, pol);
+    }
+  }
+  __device__ __forceinline__ static void from_stage(const float* stage, int d, float (&r)[K][VEC]) {
+    cp_async_wait_all();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      int c = lane_id() + 32 * k;
+      if (c * VEC < d) {
+        float4 x = *reinterpret_cast<const float4*>(stage + c * VEC);
+        r[k][0] = x.x; r[k][1] = x.y; r[k][2] = x.z; r[k][3] = x.w;
+      } else {
+        r[k][0] = r[k][1] = r[k][2] = r[k][3] = 0.f;
       }
     }
   }
