@@ -1324,9 +1324,19 @@ __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState
   using R = RowAcc<VEC, K>;
   const int d = a.L.d_out, H = a.L.heads, dh = d / H;
   const int lane = lane_id();
+  // every lane evaluates the attention of a gathered edge for the head(s) of its own
+  // columns (same inputs, same expf as the edge's owner lane): no per-head arrays and
+  // shuffles, which kept the kernel spilling at 4 CTAs / SM
   int hk[K];
+  float el[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k) hk[k] = R::has(k, d) ? chunk_head<VEC>(k, dh) : 0;
+  for (int k = 0; k < K; ++k) {
+    hk[k] = R::has(k, d) ? chunk_head<VEC>(k, dh) : 0;
+    el[k] = 0.f;
+#pragma unroll
+    for (int h = 0; h < kHMax; ++h)
+      if (hk[k] == h) el[k] = es.elh[h];
+  }
   for (int32_t c0 = e0; c0 < e1; c0 += 32) {
     const int32_t j = c0 + lane;
     int32_t u = 0, sl = 0;
@@ -1335,23 +1345,11 @@ __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState
       u = a.g.in.nbr[beg + j];
       hit = all || (bm_test(a.f.bm_src, u) && !in_range_has(a.b.i_src, p, q, u));
     }
-    float an[kHMax], ao[kHMax];
-#pragma unroll
-    for (int h = 0; h < kHMax; ++h) an[h] = ao[h] = 0.f;
-    if (hit) {
-      if (!all) sl = a.prev_slot[u];
-#pragma unroll
-      for (int h = 0; h < kHMax; ++h)
-        if (h < H) {
-          an[h] = expf(leaky02(es.elh[h] + __ldg(a.st.er + static_cast<int64_t>(u) * H + h)));
-          if (!all) ao[h] = expf(leaky02(es.elh[h] + __ldg(a.st.er_log + static_cast<int64_t>(sl) * H + h)));
-        }
-    }
+    if (hit && !all) sl = a.prev_slot[u];
     unsigned m = __ballot_sync(0xffffffffu, hit);
     while (m) {
       constexpr int UNR = 2;
       int32_t uu[UNR], ss[UNR];
-      float wn[UNR][K], wo[UNR][K];
       int cnt = 0;
 #pragma unroll
       for (int t = 0; t < UNR; ++t) {
@@ -1362,38 +1360,32 @@ __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState
         }
         uu[t] = __shfl_sync(0xffffffffu, u, src);
         ss[t] = __shfl_sync(0xffffffffu, sl, src);
-#pragma unroll
-        for (int k = 0; k < K; ++k) wn[t][k] = wo[t][k] = 0.f;
-#pragma unroll
-        for (int h = 0; h < kHMax; ++h) {
-          if (h >= H) break;
-          float x = __shfl_sync(0xffffffffu, an[h], src);
-          float y = all ? 0.f : __shfl_sync(0xffffffffu, ao[h], src);
-#pragma unroll
-          for (int k = 0; k < K; ++k)
-            if (hk[k] == h) {
-              wn[t][k] = x;
-              wo[t][k] = y;
-            }
-        }
       }
       float zn[UNR][K][VEC], zo[UNR][K][VEC];
+      float rn[UNR][K], ro[UNR][K];
 #pragma unroll
       for (int t = 0; t < UNR; ++t)
         if (t < cnt) {
           R::load(a.st.Z + static_cast<int64_t>(uu[t]) * d, d, zn[t]);
           if (!all) R::load(a.st.Z_log + static_cast<int64_t>(ss[t]) * d, d, zo[t]);
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            rn[t][k] = __ldg(a.st.er + static_cast<int64_t>(uu[t]) * H + hk[k]);
+            ro[t][k] = all ? 0.f : __ldg(a.st.er_log + static_cast<int64_t>(ss[t]) * H + hk[k]);
+          }
         }
 #pragma unroll
       for (int t = 0; t < UNR; ++t)
         if (t < cnt) {
 #pragma unroll
           for (int k = 0; k < K; ++k) {
-            cacc[k] += all ? wn[t][k] : wn[t][k] - wo[t][k];
+            const float wn = expf(leaky02(el[k] + rn[t][k]));
+            const float wo = all ? 0.f : expf(leaky02(el[k] + ro[t][k]));
+            cacc[k] += all ? wn : wn - wo;
 #pragma unroll
             for (int jj = 0; jj < VEC; ++jj) {
-              float x = wn[t][k] * zn[t][k][jj];
-              if (!all) x = fmaf(-wo[t][k], zo[t][k][jj], x);
+              float x = wn * zn[t][k][jj];
+              if (!all) x = fmaf(-wo, zo[t][k][jj], x);
               acc.v[k][jj] += x;
             }
           }
@@ -1425,8 +1417,12 @@ __device__ __forceinline__ void gat_struct(const LayerArgs& a, const GatEdgeStat
     for (int k = 0; k < K; ++k) {
       float at = 0.f;
       if (R::has(k, d)) {
-        int h = chunk_head<VEC>(k, dh);
-        at = expf(leaky02(es.elh[h] + errow[h]));
+        const int h = chunk_head<VEC>(k, dh);
+        float elv = 0.f;
+#pragma unroll
+        for (int hh = 0; hh < kHMax; ++hh)  // static index: keeps es.elh in registers
+          if (hh == h) elv = es.elh[hh];
+        at = expf(leaky02(elv + errow[h]));
       }
       cacc[k] += sgn * at;
 #pragma unroll
