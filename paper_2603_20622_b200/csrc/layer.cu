@@ -1348,7 +1348,7 @@ __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState
     if (hit && !all) sl = a.prev_slot[u];
     unsigned m = __ballot_sync(0xffffffffu, hit);
     while (m) {
-      constexpr int UNR = 2;
+      constexpr int UNR = 1;  // measured (c3-gat): 1 > 2 > 3 -- deeper unrolls spill at 4 CTAs / SM
       int32_t uu[UNR], ss[UNR];
       int cnt = 0;
 #pragma unroll
