@@ -195,6 +195,15 @@ def algorithmic_bytes(name: str, wl: dict, layer_counters, n: int) -> float:
     if name == "aggregation":
         # in-run ids of V_dst + S-bitmap + δ rows once + S read/write + composed row write + list/offsets
         return 4 * sum_in + n / 8 + f * d_a * n_src + 3 * f * d_a * v_dst + 16 * v_dst
+    if name == "k_gat_layer":
+        # GAT (transform, then aggregate: rows of width d_o): in-run ids of V_dst + S-bitmap,
+        # each gathered source row once (new Z rows, plus the logged old rows of S(l)),
+        # S read + write, H write, DeltaLog write, el / er / ctx per head
+        h = wl.get("heads", 1)
+        new_rows = min(n, e_curr if layer_counters[3] == 0 else n)
+        old_rows = min(n_src, e_curr)
+        return (4 * sum_in + n / 8 + f * d_o * (new_rows + old_rows) + 4 * f * d_o * v_dst
+                + 8 * h * (new_rows + old_rows) + 8 * h * v_dst)
     if name == "k_src_delta":
         return f * d_a * 3 * n_src + 12 * n_src
     if name in ("k_gemm_update", "k_gemm_tc"):
@@ -379,7 +388,7 @@ def run_ours(args, world, rank, local):
     for name, (cnt, ms) in prof.items():
         per_launch_ms = ms / max(cnt, 1)
         byts = 0.0
-        if name in ("aggregation", "k_src_delta", "k_gemm_update", "k_gemm_tc", "k_expand"):
+        if name in ("aggregation", "k_gat_layer", "k_src_delta", "k_gemm_update", "k_gemm_tc", "k_expand"):
             byts = sum(algorithmic_bytes(name, wl, C[k, l], wl["n"]) for k in range(PROF) for l in range(L)) / max(cnt, 1)
         kernels[name] = {"launches": cnt, "total_ms": round(ms, 4), "ms_per_launch": round(per_launch_ms, 5),
                          "share": round(ms / max(prof_step_ms, 1e-9), 4),
@@ -387,7 +396,7 @@ def run_ours(args, world, rank, local):
     if "aggregation" in kernels:
         kernels["aggregation"]["kernels"] = ("one scope per layer around the whole stage: k_agg_inc (light) + "
                                              "k_agg_inc_heavy (hub chunks), or k_hit_compact + k_agg_sliced passes")
-    hot = [k for k in ("aggregation", "k_gemm_tc", "k_gemm_update", "k_src_delta", "k_expand") if k in kernels]
+    hot = [k for k in ("aggregation", "k_gat_layer", "k_gemm_tc", "k_gemm_update", "k_src_delta", "k_expand") if k in kernels]
     dom = max(hot, key=lambda k: kernels[k]["total_ms"]) if hot else None
     roof = None
     if dom:

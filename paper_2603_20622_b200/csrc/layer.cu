@@ -1324,19 +1324,16 @@ __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState
   using R = RowAcc<VEC, K>;
   const int d = a.L.d_out, H = a.L.heads, dh = d / H;
   const int lane = lane_id();
-  // every lane evaluates the attention of a gathered edge for the head(s) of its own
-  // columns (same inputs, same expf as the edge's owner lane): no per-head arrays and
-  // shuffles, which kept the kernel spilling at 4 CTAs / SM
+  // The attention of a 32-edge window is evaluated once per edge, lane j for edge j,
+  // all heads (same inputs and expf as before), into a per-warp shared-memory table;
+  // the gather loop then reads the head of its own columns from it (one LDS per chunk
+  // instead of an er load + expf per lane per edge, no per-head register arrays).
+  __shared__ float s_att[kLBlk / 32][2][32][kHMax + 1];
+  float(*an)[kHMax + 1] = s_att[threadIdx.x >> 5][0];
+  float(*ao)[kHMax + 1] = s_att[threadIdx.x >> 5][1];
   int hk[K];
-  float el[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    hk[k] = R::has(k, d) ? chunk_head<VEC>(k, dh) : 0;
-    el[k] = 0.f;
-#pragma unroll
-    for (int h = 0; h < kHMax; ++h)
-      if (hk[k] == h) el[k] = es.elh[h];
-  }
+  for (int k = 0; k < K; ++k) hk[k] = R::has(k, d) ? chunk_head<VEC>(k, dh) : 0;
   for (int32_t c0 = e0; c0 < e1; c0 += 32) {
     const int32_t j = c0 + lane;
     int32_t u = 0, sl = 0;
@@ -1347,50 +1344,38 @@ __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState
     }
     if (hit && !all) sl = a.prev_slot[u];
     unsigned m = __ballot_sync(0xffffffffu, hit);
-    while (m) {
-      constexpr int UNR = 1;  // measured (c3-gat): 1 > 2 > 3 -- deeper unrolls spill at 4 CTAs / SM
-      int32_t uu[UNR], ss[UNR];
-      int cnt = 0;
+    if (!m) continue;
+    if (hit) {
 #pragma unroll
-      for (int t = 0; t < UNR; ++t) {
-        int src = m ? __ffs(m) - 1 : 0;
-        if (m) {
-          m &= m - 1;
-          cnt = t + 1;
-        }
-        uu[t] = __shfl_sync(0xffffffffu, u, src);
-        ss[t] = __shfl_sync(0xffffffffu, sl, src);
-      }
-      float zn[UNR][K][VEC], zo[UNR][K][VEC];
-      float rn[UNR][K], ro[UNR][K];
-#pragma unroll
-      for (int t = 0; t < UNR; ++t)
-        if (t < cnt) {
-          R::load(a.st.Z + static_cast<int64_t>(uu[t]) * d, d, zn[t]);
-          if (!all) R::load(a.st.Z_log + static_cast<int64_t>(ss[t]) * d, d, zo[t]);
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            rn[t][k] = __ldg(a.st.er + static_cast<int64_t>(uu[t]) * H + hk[k]);
-            ro[t][k] = all ? 0.f : __ldg(a.st.er_log + static_cast<int64_t>(ss[t]) * H + hk[k]);
-          }
-        }
-#pragma unroll
-      for (int t = 0; t < UNR; ++t)
-        if (t < cnt) {
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            const float wn = expf(leaky02(el[k] + rn[t][k]));
-            const float wo = all ? 0.f : expf(leaky02(el[k] + ro[t][k]));
-            cacc[k] += all ? wn : wn - wo;
-#pragma unroll
-            for (int jj = 0; jj < VEC; ++jj) {
-              float x = wn * zn[t][k][jj];
-              if (!all) x = fmaf(-wo, zo[t][k][jj], x);
-              acc.v[k][jj] += x;
-            }
-          }
+      for (int h = 0; h < kHMax; ++h)
+        if (h < H) {
+          an[lane][h] = expf(leaky02(es.elh[h] + __ldg(a.st.er + static_cast<int64_t>(u) * H + h)));
+          if (!all) ao[lane][h] = expf(leaky02(es.elh[h] + __ldg(a.st.er_log + static_cast<int64_t>(sl) * H + h)));
         }
     }
+    __syncwarp();
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      const int32_t uu = __shfl_sync(0xffffffffu, u, src);
+      const int32_t ss = __shfl_sync(0xffffffffu, sl, src);
+      float zn[K][VEC], zo[K][VEC];
+      R::load(a.st.Z + static_cast<int64_t>(uu) * d, d, zn);
+      if (!all) R::load(a.st.Z_log + static_cast<int64_t>(ss) * d, d, zo);
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const float wn = an[src][hk[k]];
+        const float wo = all ? 0.f : ao[src][hk[k]];
+        cacc[k] += all ? wn : wn - wo;
+#pragma unroll
+        for (int jj = 0; jj < VEC; ++jj) {
+          float x = wn * zn[k][jj];
+          if (!all) x = fmaf(-wo, zo[k][jj], x);
+          acc.v[k][jj] += x;
+        }
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -1599,8 +1584,19 @@ static int launch_gat(LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_
   bool ok;
   RTEC_PROF(FULL ? "k_gat_full" : "k_gat_layer", s);
   if (d % 4 == 0 && dh % 4 == 0) {
-    ok = RTEC_ROW_DISPATCH(d, (k_gat_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows),
-                               k_gat_heavy<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows, hp)));
+    // hub chunks on the side stream, as in launch_aggregation: the two passes write
+    // disjoint destinations and fill each other's tails (not while profiling)
+    cudaStream_t hs = g_prof_on ? s : side_stream();
+    if (hs != s) {
+      RTEC_CUDA(cudaEventRecord(side_fork(), s));
+      RTEC_CUDA(cudaStreamWaitEvent(hs, side_fork(), 0));
+    }
+    ok = RTEC_ROW_DISPATCH(d, (k_gat_heavy<VEC, K, FULL><<<grid, kLBlk, 0, hs>>>(a, rows, hp),
+                               k_gat_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows)));
+    if (hs != s) {
+      RTEC_CUDA(cudaEventRecord(side_join(), hs));
+      RTEC_CUDA(cudaStreamWaitEvent(s, side_join(), 0));
+    }
   } else {
     int kk = (d + 31) / 32;
     ok = true;
