@@ -1334,12 +1334,14 @@ __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState
   int hk[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) hk[k] = R::has(k, d) ? chunk_head<VEC>(k, dh) : 0;
+  // the next window's source ids are requested before this window's gathers
+  int32_t u_nx = e0 + lane < e1 ? a.g.in.nbr[beg + e0 + lane] : 0;
   for (int32_t c0 = e0; c0 < e1; c0 += 32) {
     const int32_t j = c0 + lane;
-    int32_t u = 0, sl = 0;
+    int32_t u = u_nx, sl = 0;
+    if (j + 32 < e1) u_nx = a.g.in.nbr[beg + j + 32];
     bool hit = false;
     if (j < e1) {
-      u = a.g.in.nbr[beg + j];
       hit = all || (bm_test(a.f.bm_src, u) && !in_range_has(a.b.i_src, p, q, u));
     }
     if (hit && !all) sl = a.prev_slot[u];
