@@ -271,6 +271,14 @@ struct HeavyPlan {
   int32_t* cmap;    // chunk -> heavy index j
   int32_t* arrive;  // [n_heavy] arrival counters (zeroed per launch)
   float* part;      // [chunks, d] partial rows
+  // chunk visit order: chunks sorted (stably) by their relative position c / nch in
+  // their destination's in-run, so the warps resident at one time gather from the
+  // same band of (ascending) source ids of every hub -- an L2-sized working set.
+  // nullptr: destination-major.  Execution order only: partials are still reduced
+  // in chunk order (results identical).
+  const uint32_t* order;
+  uint64_t* okey;   // sort keys (position << 32 | 0) written by k_chunk_map
+  uint32_t* oval;   // chunk ids
 };
 
 // resident CTAs per SM: wide rows need the registers (no spills)
@@ -523,7 +531,8 @@ __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_heavy(Laye
   const int cw = a.cw;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t t = warp; t < T; t += nw) {
+  for (int64_t tt = warp; tt < T; tt += nw) {
+    const int64_t t = hp.order ? static_cast<int64_t>(hp.order[tt]) : tt;
     int32_t j = hp.cmap[t];
     int64_t c0 = hp.hoff[j];
     int32_t nch = static_cast<int32_t>(hp.hoff[j + 1] - c0);
@@ -593,11 +602,18 @@ struct StoreOffTailL {
 
 __global__ void k_chunk_map(HeavyPlan hp) {
   int64_t nh = *hp.n_heavy;
+  if (blockIdx.x == 0 && threadIdx.x == 0) hp.n_heavy[1] = hp.hoff[nh];  // total chunks (sort count)
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t j = warp; j < nh; j += nw) {
     int64_t c0 = hp.hoff[j], c1 = hp.hoff[j + 1];
-    for (int64_t c = c0 + lane_id(); c < c1; c += 32) hp.cmap[c] = static_cast<int32_t>(j);
+    for (int64_t c = c0 + lane_id(); c < c1; c += 32) {
+      hp.cmap[c] = static_cast<int32_t>(j);
+      if (hp.okey) {
+        hp.okey[c] = static_cast<uint64_t>(((c - c0) << 16) / (c1 - c0));
+        hp.oval[c] = static_cast<uint32_t>(c);
+      }
+    }
     if (lane_id() == 0) hp.arrive[j] = 0;
   }
 }
@@ -624,6 +640,16 @@ static bool agg_batched(int d) {
   return d <= b;
 }
 
+// RTEC_HEAVY_ORDER env: visit hub chunks in relative-position order (default 1; 0: destination-major)
+static bool heavy_order() {
+  static int o = -1;
+  if (o < 0) {
+    const char* e = getenv("RTEC_HEAVY_ORDER");
+    o = e ? atoi(e) : 1;
+  }
+  return o != 0;
+}
+
 // heavy-destination plan (list, chunk offsets, chunk -> heavy map); partial rows of `pw` floats
 template <bool FULL>
 static int plan_heavy(const LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_edges, int pw, Ws& w,
@@ -644,8 +670,20 @@ static int plan_heavy(const LayerArgs& a, AggRows rows, int64_t max_rows, int64_
   RTEC_TRY(exclusive_scan(hf, cnt, max_rows, HeavyStore{hf, hp.heavy}, hp.n_heavy, w, s));
   RTEC_TRY(exclusive_scan(HeavyChunks{rows, a.g.in.len, hp.heavy}, Count{hp.n_heavy, max_rows}, max_rows,
                           StoreOffTailL{hp.hoff, hp.n_heavy}, nullptr, w, s));
+  if (heavy_order()) {
+    hp.okey = w.alloc<uint64_t>(max_chunks);
+    hp.oval = w.alloc<uint32_t>(max_chunks);
+    RTEC_WS_CHECK(w);
+  }
   k_chunk_map<<<kSMs * 4, kLBlk, 0, s>>>(hp);
   RTEC_LAUNCH_CHECK("k_chunk_map");
+  if (hp.okey) {
+    uint64_t* kout = w.alloc<uint64_t>(max_chunks);
+    uint32_t* order = w.alloc<uint32_t>(max_chunks);
+    RTEC_WS_CHECK(w);
+    RTEC_TRY(sort_pairs(hp.okey, hp.oval, kout, order, Count{hp.n_heavy + 1, max_chunks}, max_chunks, 16, w, s));
+    hp.order = order;
+  }
   return RTEC_OK;
 }
 
@@ -889,7 +927,8 @@ __global__ void __launch_bounds__(kLBlk) k_dd_heavy(LayerArgs a, AggRows rows, H
   const int d = a.d_agg;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t t = warp; t < T; t += nw) {
+  for (int64_t tt = warp; tt < T; tt += nw) {
+    const int64_t t = hp.order ? static_cast<int64_t>(hp.order[tt]) : tt;
     const int32_t j = hp.cmap[t];
     const int64_t c0 = hp.hoff[j];
     const int32_t nch = static_cast<int32_t>(hp.hoff[j + 1] - c0);
@@ -1178,7 +1217,8 @@ __global__ void __launch_bounds__(kLBlk) k_max_heavy(LayerArgs a, AggRows rows, 
   const bool direct = max_direct<FULL>(a);
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t t = warp; t < T; t += nw) {
+  for (int64_t tt = warp; tt < T; tt += nw) {
+    const int64_t t = hp.order ? static_cast<int64_t>(hp.order[tt]) : tt;
     int32_t j = hp.cmap[t];
     int64_t c0 = hp.hoff[j];
     int32_t nch = static_cast<int32_t>(hp.hoff[j + 1] - c0);
@@ -1515,7 +1555,8 @@ __global__ void __launch_bounds__(kLBlk, 4) k_gat_heavy(LayerArgs a, AggRows row
   const int pw = (d + H + 3) & ~3;  // partial row: d floats + H attention sums, 16-byte aligned
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t t = warp; t < T; t += nw) {
+  for (int64_t tt = warp; tt < T; tt += nw) {
+    const int64_t t = hp.order ? static_cast<int64_t>(hp.order[tt]) : tt;
     int32_t j = hp.cmap[t];
     int64_t c0 = hp.hoff[j];
     int32_t nch = static_cast<int32_t>(hp.hoff[j + 1] - c0);
