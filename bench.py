@@ -470,11 +470,12 @@ def launches_per_step(prof, K):
 
 
 # ---------------------------------------------------------------- reference (CPU) arm
-def cpu_sample(wl_name: str, budget_s: float, max_steps: int):
+def cpu_sample(wl_name: str, budget_s: float, max_steps: int, warmup: int = 1):
     """The reference's CPU path on the same workload: the C/OpenMP oracle port
     (oracle/rtec_cpu.c, pinned to the numpy oracle which is pinned to the
-    reference), f64, every host thread.  Bounded sample: one untimed warm-up
-    batch, then timed batches until `budget_s` of CPU work or `max_steps`."""
+    reference), f64, every host thread.  Bounded sample: `warmup` untimed warm-up
+    batches (at most 3: ~7 s each at c2), then timed batches until `budget_s` of
+    CPU work or `max_steps`."""
     import os as _os
 
     from oracle import cport
@@ -492,7 +493,8 @@ def cpu_sample(wl_name: str, budget_s: float, max_steps: int):
     eng = cport.CPortEngine(wl["model"], wl["n"], bs, bd, bt, W, W2, wl["dims"],
                             features(wl["n"], wl["dims"][0], 1).astype(np.float64), degree_offset=b.degree_offset)
     setup = time.time() - t0
-    eng.step(*stream.next_batch(wl["batch"]))  # warm-up
+    for _ in range(max(1, min(3, warmup))):  # untimed warm-up
+        eng.step(*stream.next_batch(wl["batch"]))
     times, ups = [], 0
     while len(times) < max(1, max_steps):
         op, s1, d1, t1 = stream.next_batch(wl["batch"])
@@ -515,15 +517,16 @@ def main():
         if rank != 0:
             return
         wl = args.workload
-        r = cpu_sample(wl, budget_s=150.0, max_steps=args.steps)
+        wu = max(1, min(3, args.warmup))
+        r = cpu_sample(wl, budget_s=150.0, max_steps=args.steps, warmup=wu)
         v = r["value"]
         out = {"impl": "reference", "metric": METRIC, "value": round(v, 1), "unit": "edge updates/s", "n_gpus": world,
-               "steps": r["steps"], "warmup": 1, "ms_per_step": round(r["p50_s"] * 1e3, 2),
+               "steps": r["steps"], "warmup": wu, "ms_per_step": round(r["p50_s"] * 1e3, 2),
                "p50_batch_ms": round(r["p50_s"] * 1e3, 2), "higher_is_better": True, "scaling": "weak",
                "vs_baseline": None, "dtype": "f64", "data": "synthetic (same seeded workload as the GPU arm)",
                "config": {"workload": wl, "desc": WORKLOADS[wl]["desc"], "setup_s": round(r["setup_s"], 1)},
                "cpu_baseline": {"value": round(v, 1), "unit": "edge updates/s", "cores": r["threads"], "kind": "port",
-                                "sample": f"{r['steps']} timed batches (after 1 warm-up) of the {wl} workload, "
+                                "sample": f"{r['steps']} timed batches (after {wu} warm-up) of the {wl} workload, "
                                           f"C/OpenMP oracle port, f64, {r['threads']} threads of {r['host_cpus']} host CPUs"},
                "e2e": {"value": round(v, 1), "unit": "edge updates/s", "h2d_bytes_per_step": 0,
                        "d2h_bytes_per_step": 0}}
