@@ -1510,10 +1510,11 @@ __device__ __forceinline__ void gat_finalize(const LayerArgs& a, int64_t i, int3
   o.store(hrow, d);
 }
 
-// 5 CTAs / SM (51 registers, small spills): the GAT passes are latency-bound on their row
-// gathers, occupancy wins -- measured c3-gat p50 3 CTAs 16.4 ms, 4 CTAs 14.7, 5 CTAs 14.55
+// 6 CTAs / SM (42 registers, spills): the GAT passes are latency-bound on their row
+// gathers and the two streams' passes co-reside, so occupancy wins -- measured c3-gat
+// p50 3 CTAs 16.4 ms, 4 CTAs 14.7, 5 CTAs 14.55, 6 CTAs 14.1
 template <int VEC, int K, bool FULL>
-__global__ void __launch_bounds__(kLBlk, 5) k_gat_light(LayerArgs a, AggRows rows) {
+__global__ void __launch_bounds__(kLBlk, 6) k_gat_light(LayerArgs a, AggRows rows) {
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
   const int64_t nr = rows.count();
@@ -1547,7 +1548,7 @@ __global__ void __launch_bounds__(kLBlk, 5) k_gat_light(LayerArgs a, AggRows row
 }
 
 template <int VEC, int K, bool FULL>
-__global__ void __launch_bounds__(kLBlk, 5) k_gat_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
+__global__ void __launch_bounds__(kLBlk, 6) k_gat_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
   const int64_t nh = *hp.n_heavy;
