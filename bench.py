@@ -73,6 +73,7 @@ def parse():
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks / cpu baseline)")
     ap.add_argument("--no-graphs", action="store_true", help="launch the per-batch pipeline eagerly (no CUDA graph)")
     ap.add_argument("--no-baselines", action="store_true", help="skip the UER / RTEC-Full GPU baseline batches")
+    ap.add_argument("--no-parity", action="store_true", help="skip the full-scale GPU-vs-CPU-port parity check")
     return ap.parse_args()
 
 
@@ -183,10 +184,11 @@ def make_workload(wl: dict, steps_total: int, device):
     return stream, batches, X
 
 
-def algorithmic_bytes(name: str, wl: dict, layer_counters, n: int) -> float:
+def algorithmic_bytes(name: str, wl: dict, layer_counters, n: int, prev_counters=None, fused: bool = False) -> float:
     """Algorithmic (compulsory) HBM bytes of one launch.
 
-    layer_counters: [|E_curr|, |V_dst|, |S|, |R|, -, Σindeg(V_dst), -, -] of the layer."""
+    layer_counters: [|E_curr|, |V_dst|, |S|, |R|, -, Σindeg(V_dst), -, layer] of the layer;
+    prev_counters: the previous layer's (None for layer 0)."""
     e_curr, v_dst, n_src, _, _, sum_in = [float(x) for x in layer_counters[:6]]
     l = layer_counters[7]
     d_a = wl["dims"][int(l)]
@@ -205,7 +207,10 @@ def algorithmic_bytes(name: str, wl: dict, layer_counters, n: int) -> float:
         return (4 * sum_in + n / 8 + f * d_o * (new_rows + old_rows) + 4 * f * d_o * v_dst
                 + 8 * h * (new_rows + old_rows) + 8 * h * v_dst)
     if name == "k_src_delta":
-        return f * d_a * 3 * n_src + 12 * n_src
+        # rows the kernel processes: all of S(l), or -- with the fused update epilogue writing
+        # the δ rows of V_chg(l-1) -- only S(l) \ V_chg(l-1) = |S(l)| - |V_dst(l-1)|
+        rows = n_src - (float(prev_counters[1]) if (fused and prev_counters is not None) else 0.0)
+        return f * d_a * 3 * rows + 12 * rows
     if name in ("k_gemm_update", "k_gemm_tc"):
         # composed rows in (K padded to 32), H rows out (+ old H rows into the DeltaLog for
         # every layer but the last), 3xTF32 weight images
@@ -215,6 +220,27 @@ def algorithmic_bytes(name: str, wl: dict, layer_counters, n: int) -> float:
     if name == "k_expand":
         return 4 * e_curr + n / 8
     return 0.0
+
+
+def apply_bytes(B: int, apply_ctr) -> float:
+    """Algorithmic bytes of one batch_apply (SURVEY §8(d) "Structure"): the batch (op u8 +
+    src/dst i32 + ts i64 = 17 B per update) read, the applied updates' ts (8 B), and the
+    touched run suffixes moved by the merges: the old suffix + update items read and the
+    new suffix written (out-runs 12 B per element with ts, in-runs 4 B), plus the in-place
+    scratch staged and copied back."""
+    w_out, s_out, w_in, s_in = [float(x) for x in apply_ctr]
+    return 25.0 * B + 12.0 * (2 * w_out + 2 * s_out) + 4.0 * (2 * w_in + 2 * s_in)
+
+
+def bench_config(args, wl: dict, world: int) -> dict:
+    """The workload dict both arms print (same_config)."""
+    sharded = world > 1
+    return {"workload": args.workload, "desc": wl["desc"], "vertices": wl["n"], "edges": wl["m"],
+            "model": wl["model"], "dims": wl["dims"], "batch_updates": wl["batch"],
+            "batch_fraction": round(wl["batch"] / wl["m"], 6),
+            "parallelism": f"vertex-sharded x{world} (owner = v mod {world}, halo all-gather per layer)"
+            if sharded else "single GPU",
+            "l2": "flushed between timed steps (256 MiB write)"}
 
 
 def gemm_flops(wl, layer_counters):
@@ -262,6 +288,8 @@ def run_ours(args, world, rank, local):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     errs = torch.zeros(K + PROF, dtype=torch.int64, device=dev)
     ctrs = torch.zeros(PROF, L, 8, dtype=torch.int64, device=dev)
+    actr = torch.zeros(PROF, 4, dtype=torch.int64, device=dev)
+    bsz = []
     napp = torch.zeros(K, dtype=torch.int64, device=dev)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
 
@@ -305,8 +333,9 @@ def run_ours(args, world, rank, local):
     _lib.prof_report(reset=True)
     for k in range(PROF):
         flush.zero_()
-        run_step(W + K + k)
+        bsz.append(run_step(W + K + k))
         errs[K + k : K + k + 1].copy_(g.batch.err)
+        actr[k].copy_(g.batch.apply_ctr)
         for l in range(L):
             ctrs[k, l].copy_(eng.fr[l].counters)
     torch.cuda.synchronize()
@@ -385,11 +414,16 @@ def run_ours(args, world, rank, local):
     for l in range(L):
         C[:, l, 7] = l
     kernels = {}
+    fused = bool(getattr(eng, "fused", False))
+    AC = actr.cpu().numpy()
     for name, (cnt, ms) in prof.items():
         per_launch_ms = ms / max(cnt, 1)
         byts = 0.0
         if name in ("aggregation", "k_gat_layer", "k_src_delta", "k_gemm_update", "k_gemm_tc", "k_expand"):
-            byts = sum(algorithmic_bytes(name, wl, C[k, l], wl["n"]) for k in range(PROF) for l in range(L)) / max(cnt, 1)
+            byts = sum(algorithmic_bytes(name, wl, C[k, l], wl["n"], C[k, l - 1] if l else None, fused)
+                       for k in range(PROF) for l in range(L)) / max(cnt, 1)
+        elif name == "batch_apply" and not sharded:
+            byts = sum(apply_bytes(bsz[k], AC[k]) for k in range(PROF)) / max(cnt, 1)
         kernels[name] = {"launches": cnt, "total_ms": round(ms, 4), "ms_per_launch": round(per_launch_ms, 5),
                          "share": round(ms / max(prof_step_ms, 1e-9), 4),
                          "algo_GBps": round(byts / (per_launch_ms * 1e6), 1) if byts else None}
@@ -432,12 +466,7 @@ def run_ours(args, world, rank, local):
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (seeded Chung-Lu graph, U(-1,1) features, make_bundle seed-0 weights)",
-        "config": {"workload": args.workload, "desc": wl["desc"], "vertices": wl["n"], "edges": wl["m"],
-                   "model": wl["model"], "dims": wl["dims"], "batch_updates": wl["batch"],
-                   "batch_fraction": round(wl["batch"] / wl["m"], 6),
-                   "parallelism": f"vertex-sharded x{world} (owner = v mod {world}, halo all-gather per layer)"
-                   if sharded else "single GPU",
-                   "l2": "flushed between timed steps (256 MiB write)"},
+        "config": bench_config(args, wl, world),
         "e2e": {"value": round(e2e_val, 1) if e2e_val else None, "unit": "edge updates/s", "steps": E2E,
                 "h2d_bytes_per_step": h2d // max(E2E, 1), "d2h_bytes_per_step": d2h // max(E2E, 1),
                 "p50_batch_ms": round(statistics.median(e2e_ms), 4) if e2e_ms else None},
@@ -455,7 +484,7 @@ def run_ours(args, world, rank, local):
     nodes = getattr(eng, "graph_kernels", {}).get(wl["batch"])
     # captured step: every kernel node is one of ours; eager (sharded / --no-graphs): the scope count
     res["gpu_launches"] = (nodes if nodes and nodes > 0 else launches_per_step(prof, PROF)) * K
-    res["config"]["cuda_graph"] = bool(graphs_on and nodes)
+    res["cuda_graph"] = bool(graphs_on and nodes)
     return res, g, eng
 
 
@@ -469,8 +498,74 @@ def launches_per_step(prof, K):
     return int(round(n / max(K, 1)))
 
 
+# ---------------------------------------------------------------- full-scale parity (GPU twin vs the CPU port)
+def _rowwise(x, y):
+    """(floored, strict) row-wise relative error (tests/helpers.py rowwise_rel / _strict)."""
+    num = np.abs(x - y).max(axis=1)
+    den = np.abs(y).max(axis=1)
+    floored = float((num / np.maximum(den, max(1e-2 * float(den.max()), 1e-6))).max())
+    nz = den > 0
+    strict = float((num[nz] / den[nz]).max()) if nz.any() else 0.0
+    zero_abs = float(num[~nz].max()) if (~nz).any() else 0.0
+    return floored, strict, zero_abs
+
+
+class GpuTwin:
+    """A fresh GPU engine on the CPU leg's base graph that steps through the same batches;
+    per batch the per-update status, DegreeDelta rows and frontier sizes must equal the
+    C port's bit for bit, and after the last batch sampled rows of every H^l and S^l are
+    compared (SURVEY §8(c) row-wise metric, fp32 vs f64) -- parity at the bench's own
+    configuration, outside every timed region."""
+
+    ROWS = 1 << 17
+
+    def __init__(self, wl, bs, bd, bt, X):
+        import torch
+
+        import paper_2603_20622_b200 as P
+
+        dev = torch.device("cuda", torch.cuda.current_device())
+        t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)  # noqa: E731
+        self.g = P.DynamicGraph.from_tensors(wl["n"], t(bs), t(bd), t(bt), reserve=max(1 << 20, wl["m"] // 2))
+        self.eng = P.RTECEngine(P.make_bundle(wl["model"], wl["dims"]), self.g, X, max_batch=wl["batch"])
+        self.wl, self.batches, self.exact = wl, 0, True
+        self.mismatch = []
+
+    def step(self, batch, c_status, c_deltas, cport):
+        r = self.eng.step(*batch)
+        self.batches += 1
+        ok = np.array_equal(r.status, c_status) and np.array_equal(r.deltas.astype(np.int64), c_deltas)
+        for l in range(len(self.wl["dims"]) - 1):
+            nv, ne = cport.frontier(l)
+            ok = ok and (nv, ne) == (r.metrics.v_dst[l], r.metrics.e_curr[l])
+        if not ok:
+            self.mismatch.append(self.batches)
+        self.exact = self.exact and ok
+
+    def compare(self, cport) -> dict:
+        import torch
+
+        n = self.wl["n"]
+        rng = np.random.default_rng(12345)
+        indeg = self.g.in_deg[:n].cpu().numpy()
+        ids = np.union1d(rng.choice(n, min(self.ROWS, n), replace=False), np.argsort(-indeg, kind="stable")[:1024])
+        it = torch.as_tensor(ids, device=self.eng.dev)
+        worst = {}
+        L = len(self.wl["dims"]) - 1
+        for kind, l in [("H", l) for l in range(1, L + 1)] + [("S", l) for l in range(L)]:
+            mine = (self.eng.H[l] if kind == "H" else self.eng.S[l])[it].double().cpu().numpy()
+            fl, st, za = _rowwise(mine, cport.rows(kind, l, ids))
+            worst[f"{kind}{l}"] = {"rowwise_rel": fl, "strict_rel": st, "zero_rows_abs": za}
+        return {"batches": self.batches, "rows": int(ids.size),
+                "status_deltas_frontier_bit_exact": bool(self.exact), "mismatched_batches": self.mismatch,
+                "max_rowwise_rel": max(v["rowwise_rel"] for v in worst.values()),
+                "max_strict_rel": max(v["strict_rel"] for v in worst.values()), "tolerance": 1e-4,
+                "per_tensor": worst,
+                "against": "oracle/rtec_cpu.c f64 (C/OpenMP port of the oracle, pinned to the reference goldens)"}
+
+
 # ---------------------------------------------------------------- reference (CPU) arm
-def cpu_sample(wl_name: str, budget_s: float, max_steps: int, warmup: int = 1):
+def cpu_sample(wl_name: str, budget_s: float, max_steps: int, warmup: int = 1, twin: bool = False):
     """The reference's CPU path on the same workload: the C/OpenMP oracle port
     (oracle/rtec_cpu.c, pinned to the numpy oracle which is pinned to the
     reference), f64, every host thread.  Bounded sample: `warmup` untimed warm-up
@@ -490,24 +585,32 @@ def cpu_sample(wl_name: str, budget_s: float, max_steps: int, warmup: int = 1):
     b = OM.make_bundle(wl["model"], wl["dims"])
     W = [L["W"] for L in b.layers]
     W2 = [L["W2"] for L in b.layers] if wl["model"] == "gin" else None
-    eng = cport.CPortEngine(wl["model"], wl["n"], bs, bd, bt, W, W2, wl["dims"],
-                            features(wl["n"], wl["dims"][0], 1).astype(np.float64), degree_offset=b.degree_offset)
+    X = features(wl["n"], wl["dims"][0], 1)
+    eng = cport.CPortEngine(wl["model"], wl["n"], bs, bd, bt, W, W2, wl["dims"], X.astype(np.float64),
+                            degree_offset=b.degree_offset)
     setup = time.time() - t0
+    tw = GpuTwin(wl, bs, bd, bt, X) if twin else None
     for _ in range(max(1, min(3, warmup))):  # untimed warm-up
-        eng.step(*stream.next_batch(wl["batch"]))
+        batch = stream.next_batch(wl["batch"])
+        st, dl = eng.step(*batch)
+        if tw:
+            tw.step(batch, st, dl, eng)
     times, ups = [], 0
     while len(times) < max(1, max_steps):
         op, s1, d1, t1 = stream.next_batch(wl["batch"])
         t = time.time()
-        st, _ = eng.step(op, s1, d1, t1)
+        st, dl = eng.step(op, s1, d1, t1)
         times.append(time.time() - t)
         ups += int(st.sum())
+        if tw:
+            tw.step((op, s1, d1, t1), st, dl, eng)
         if sum(times) > budget_s:
             break
     threads = eng.threads
+    parity = tw.compare(eng) if tw else None
     eng.close()
     return {"value": ups / sum(times), "steps": len(times), "p50_s": statistics.median(times), "threads": threads,
-            "setup_s": setup, "host_cpus": _os.cpu_count()}
+            "setup_s": setup, "host_cpus": _os.cpu_count(), "parity": parity}
 
 
 def main():
@@ -524,7 +627,7 @@ def main():
                "steps": r["steps"], "warmup": wu, "ms_per_step": round(r["p50_s"] * 1e3, 2),
                "p50_batch_ms": round(r["p50_s"] * 1e3, 2), "higher_is_better": True, "scaling": "weak",
                "vs_baseline": None, "dtype": "f64", "data": "synthetic (same seeded workload as the GPU arm)",
-               "config": {"workload": wl, "desc": WORKLOADS[wl]["desc"], "setup_s": round(r["setup_s"], 1)},
+               "config": bench_config(args, WORKLOADS[wl], world), "setup_s": round(r["setup_s"], 1),
                "cpu_baseline": {"value": round(v, 1), "unit": "edge updates/s", "cores": r["threads"], "kind": "port",
                                 "sample": f"{r['steps']} timed batches (after {wu} warm-up) of the {wl} workload, "
                                           f"C/OpenMP oracle port, f64, {r['threads']} threads of {r['host_cpus']} host CPUs"},
@@ -533,9 +636,13 @@ def main():
         print(json.dumps(out))
         return
     res, g, eng = run_ours(args, world, rank, local)
-    if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.profile):
+    from oracle.cport import MODELS as PORT_MODELS
+
+    if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.profile) and \
+            WORKLOADS[args.workload]["model"] in PORT_MODELS:
         del eng, g  # free HBM-side host references before the CPU run
-        r = cpu_sample(args.workload, budget_s=30.0, max_steps=2)
+        r = cpu_sample(args.workload, budget_s=30.0, max_steps=2, twin=not args.no_parity)
+        res["parity"] = r["parity"]
         res["cpu_baseline"] = {"value": round(r["value"], 1), "unit": "edge updates/s", "cores": r["threads"],
                                "kind": "port",
                                "sample": f"{r['steps']} timed batch(es) after 1 warm-up of the same {args.workload} "

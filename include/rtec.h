@@ -122,6 +122,10 @@ typedef struct {
    * batch (rtec_shard_degrees); the frontier seeds Dg from it instead of the
    * shard-local DegreeDelta.  NULL when unsharded. */
   const uint32_t* dg_bm;
+  /* [4] or NULL: run-merge volume of the last apply, in elements -- out-runs: old
+   * suffix + update items read, in-place new suffix staged; in-runs: the same two.
+   * The bench turns them into the apply chain's algorithmic bytes. */
+  int64_t* apply_ctr;
 } rtec_batch_t;
 
 /* Per-layer frontier (Alg. 4).  Bitmaps

@@ -46,6 +46,7 @@ def lib():
         L.rc_num_edges.argtypes = [P]
         L.rc_frontier.argtypes = [P, C.c_int, P, P]
         L.rc_threads.restype = C.c_int
+        L.rc_get_rows.argtypes = [P, C.c_int, C.c_int, P, C.c_int64, P]
         _lib = L
     return _lib
 
@@ -92,6 +93,13 @@ class CPortEngine:
     def H(self, l):
         out = np.empty((self.n, self.dims[l]), np.float64)
         lib().rc_get_h(self.h, l, _p(out))
+        return out
+
+    def rows(self, kind: str, l: int, ids) -> np.ndarray:
+        """Rows `ids` of H^l (kind 'H') or of the un-normalised aggregate S^l (kind 'S')."""
+        ids = np.ascontiguousarray(ids, np.int64)
+        out = np.empty((ids.size, self.dims[l]), np.float64)
+        lib().rc_get_rows(self.h, 0 if kind == "H" else 1, l, _p(ids), ids.size, _p(out))
         return out
 
     def frontier(self, l):

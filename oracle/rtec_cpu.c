@@ -477,6 +477,13 @@ int rc_step(eng_t* e, int64_t B, const uint8_t* op, const int32_t* src, const in
 void rc_get_h(const eng_t* e, int l, double* out) {
   memcpy(out, e->H[l], sizeof(double) * e->g.n * e->dims[l]);
 }
+/* rows ids[0..k) of H[l] (kind 0, width dims[l]) or of the un-normalised aggregate S[l]
+ * (kind 1, width dims[l]) -- the bench's sampled parity check */
+void rc_get_rows(const eng_t* e, int kind, int l, const int64_t* ids, int64_t k, double* out) {
+  const int d = e->dims[l];
+  const double* src = kind == 0 ? e->H[l] : e->S[l];
+  for (int64_t i = 0; i < k; ++i) memcpy(out + i * d, src + ids[i] * d, sizeof(double) * d);
+}
 int64_t rc_num_edges(const eng_t* e) { return e->g.m; }
 void rc_frontier(const eng_t* e, int l, int64_t* n_vdst, int64_t* n_ecurr) {
   *n_vdst = e->nvdst[l];

@@ -14,7 +14,9 @@ from .graph import (  # noqa: F401
     write_stream,
 )
 from .models import MODELS, Bundle, LayerWeights, from_reference, make_bundle  # noqa: F401
-from .engine import Metrics, RTECEngine, RunResult, redundancy  # noqa: F401
+from .engine import (  # noqa: F401
+    Metrics, RTECEngine, RunResult, forward_layer_reference, layer_embeddings, redundancy, reference_embeddings,
+)
 
 from .formats import (  # noqa: F401
     load_checkpoint, load_sharded_checkpoint, load_weights, read_tensor, save_checkpoint, save_sharded_checkpoint,

@@ -47,7 +47,7 @@ class Batch(C.Structure):
         ("a_src", P), ("a_dst", P), ("a_op", P), ("a_ts", P), ("n_applied", P),
         ("i_src", P), ("i_dst", P), ("i_op", P),
         ("d_vertex", P), ("d_old_in", P), ("d_new_in", P), ("d_old_out", P), ("d_new_out", P),
-        ("n_delta", P), ("irange", P), ("dg_bm", P),
+        ("n_delta", P), ("irange", P), ("dg_bm", P), ("apply_ctr", P),
     ]
 
 

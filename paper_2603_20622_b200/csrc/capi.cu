@@ -35,9 +35,9 @@ static size_t workspace_bytes(int64_t n, int64_t max_batch, int64_t m_slots, int
   size_t b = batch_ws_bytes(n, max_batch, scr) + static_cast<size_t>(scr) * 13 * 2;
   size_t f = frontier_ws_bytes(n);
   // layer: δ rows [n, d] + heavy-destination plan (lists, chunk map, partial rows)
-  int64_t chunks = m_slots / 512 + 2 + n / 64;
+  int64_t chunks = 2 * m_slots / 512 + 2;  // layer.cu heavy_chunk_bound
   size_t l = (delta_in_ws ? static_cast<size_t>(n) * static_cast<size_t>(max_dim) * sizeof(float) : 0) +
-             static_cast<size_t>(n) * 40 + static_cast<size_t>(chunks) * (4 + 4 * static_cast<size_t>(max_dim + 8)) +
+             static_cast<size_t>(n) * 40 + static_cast<size_t>(chunks) * 2 * (4 + 4 * static_cast<size_t>(max_dim + 8))  /* heavy partials + GIN-max rescan partials */ +
              sizeof(int64_t) * (scan_blocks_for(n) + 2) * 4 + (1 << 20) +
              static_cast<size_t>(chunks) * 24 + sort_ws_bytes(chunks) + (1 << 12);  // chunk visit order
   size_t r = b > f ? b : f;

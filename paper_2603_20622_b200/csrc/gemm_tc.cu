@@ -389,11 +389,15 @@ __global__ void __launch_bounds__(512, 1) k_gemm_tc(TcArgs g, TcShape sh) {
         RTEC_TMEM_LD32(taddr + lane_base + static_cast<uint32_t>(b * g.npad + c0), rr);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         float y[32];
+        bool finite = true;
 #pragma unroll
         for (int q = 0; q < 32; ++q) {
           float v = __uint_as_float(rr[q]);
+          finite = finite && isfinite(v);  // padding columns accumulate zeros
           y[q] = g.act == 1 ? fmaxf(v, 0.f) : v;
         }
+        if (!finite && valid && g.nerr)
+          report_error(g.nerr, RTEC_NUMERIC_ERROR, g.y_rows ? static_cast<int64_t>(g.y_rows[i]) : i);
         if (g.Yt) {  // chained GEMM input: SW128 tile image (zero padding beyond d_out)
           if (!valid) continue;
           float* blk = g.Yt + ((tile * g.nkb_out + c0 / 32) * kTM) * kTK;

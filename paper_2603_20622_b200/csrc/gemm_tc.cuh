@@ -28,6 +28,9 @@ struct TcArgs {
   int coeff_gcn;
   float deg_off;
   int ydiv;  // > 1: Y rows stored per owned vertex at y_rows[i] / ydiv (sharded final layer)
+  // non-finite pre-activation output -> NumericError at the row's vertex id (linalg.py:22-29
+  // matvec "non-finite result"); null: not checked
+  uint64_t* nerr;
 };
 
 int gemm_tc_launch(const TcArgs& g, cudaStream_t s);

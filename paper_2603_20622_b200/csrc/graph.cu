@@ -390,7 +390,7 @@ struct StoreOffTail {
 };
 
 // reserve arena space for relocated runs (single thread): all-or-nothing
-__global__ void k_reserve(MergePlan p, rtec_adj_t a, uint64_t* err) {
+__global__ void k_reserve(MergePlan p, rtec_adj_t a, uint64_t* err, int64_t* ctr) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   int64_t G = *p.G;
   int64_t demand = G > 0 ? p.arena_off[G] : 0;
@@ -398,6 +398,10 @@ __global__ void k_reserve(MergePlan p, rtec_adj_t a, uint64_t* err) {
   int64_t top = *a.top;
   p.totals[0] = G > 0 ? p.work_off[G] : 0;
   p.totals[1] = scr;
+  if (ctr) {  // merge volume (elements) for the bench's algorithmic bytes
+    ctr[0] = p.totals[0];
+    ctr[1] = scr;
+  }
   p.totals[2] = demand;
   p.totals[3] = top;
   if (err_set(err)) return;
@@ -579,7 +583,7 @@ static int plan_alloc(MergePlan& p, int64_t maxK, int64_t scr_cap, bool with_ts,
 
 // plan: groups, new lengths, offsets, arena reservation; no mutation
 static int merge_plan(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, float slack, int32_t min_slack,
-                      uint64_t* err, Ws& ws, cudaStream_t s) {
+                      uint64_t* err, Ws& ws, cudaStream_t s, int64_t* ctr) {
   RTEC_CUDA(cudaMemsetAsync(p.G, 0, sizeof(int64_t), s));
   RTEC_CUDA(cudaMemsetAsync(p.pre_ins, 0, sizeof(int64_t), s));
   RTEC_CUDA(cudaMemsetAsync(p.gstart, 0, sizeof(int64_t), s));
@@ -594,7 +598,7 @@ static int merge_plan(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, floa
   RTEC_TRY(exclusive_scan(WorkOf{p, a.len}, G, in.maxK, StoreOffTail{p.work_off, p.G}, nullptr, ws, s));
   RTEC_TRY(exclusive_scan(ScrOf{p}, G, in.maxK, StoreOffTail{p.scr_off, p.G}, nullptr, ws, s));
   RTEC_TRY(exclusive_scan(ArenaOf{p}, G, in.maxK, StoreOffTail{p.arena_off, p.G}, nullptr, ws, s));
-  k_reserve<<<1, 32, 0, s>>>(p, a, err);
+  k_reserve<<<1, 32, 0, s>>>(p, a, err, ctr);
   k_set_dest<<<grid_for(in.maxK, kBlk), kBlk, 0, s>>>(p, err);
   RTEC_LAUNCH_CHECK("merge_plan");
   return RTEC_OK;
@@ -882,9 +886,10 @@ int rtec_batch_apply_phase(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src,
   w.off = mark;
   k_in_gather<<<grid, kBlk, 0, s>>>(sv, b->n_applied, b->a_src, b->a_dst, b->a_op, b->i_src, b->i_dst, b->i_op);
   // 7. plan both merges (no mutation; all-or-nothing arena reservation)
-  RTEC_TRY(merge_plan(mo, po, g->out, g->slack, g->min_slack, b->err, w, s));
+  RTEC_TRY(merge_plan(mo, po, g->out, g->slack, g->min_slack, b->err, w, s, b->apply_ctr));
   w.off = mark;
-  RTEC_TRY(merge_plan(mi, pi, g->in, g->slack, g->min_slack, b->err, w, s));
+  RTEC_TRY(merge_plan(mi, pi, g->in, g->slack, g->min_slack, b->err, w, s,
+                      b->apply_ctr ? b->apply_ctr + 2 : nullptr));
   w.off = mark;
   }
   if (!exec) return RTEC_OK;

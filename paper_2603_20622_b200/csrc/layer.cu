@@ -131,6 +131,10 @@ __device__ __forceinline__ bool in_range_has(const int32_t* __restrict__ is, int
 // last-arriving warp (deterministic; threadfence + per-vertex arrival counter).
 constexpr int kChunk = 512;
 
+// chunks of all heavy runs (len > kChunk) within `max_edges` slots: ceil(len / kChunk) <=
+// 2 len / kChunk for len > kChunk, so the sum is at most 2 max_edges / kChunk
+__host__ __device__ constexpr int64_t heavy_chunk_bound(int64_t max_edges) { return 2 * max_edges / kChunk + 2; }
+
 template <int VEC, int K, bool FULL>
 __device__ __forceinline__ void agg_edges(const LayerArgs& a, int64_t beg, int32_t e0, int32_t e1, int64_t p,
                                           int64_t q, RowAcc<VEC, K>& acc) {
@@ -277,7 +281,7 @@ struct HeavyPlan {
   // nullptr: destination-major.  Execution order only: partials are still reduced
   // in chunk order (results identical).
   const uint32_t* order;
-  uint64_t* okey;   // sort keys (position << 32 | 0) written by k_chunk_map
+  uint64_t* okey;   // 16-bit sort keys (c << 16) / nch written by k_chunk_map
   uint32_t* oval;   // chunk ids
 };
 
@@ -555,6 +559,7 @@ __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_heavy(Laye
     if (!FULL && c == 0) agg_struct<VEC, K>(a, p, q, acc);
     acc.store(hp.part + t * cw, cw);
     __threadfence();
+    __syncwarp();  // every lane's partial is fenced before the arrival is published
     int old = 0;
     if (lane_id() == 0) old = atomicAdd(hp.arrive + j, 1);
     old = __shfl_sync(0xffffffffu, old, 0);
@@ -657,7 +662,7 @@ static int plan_heavy(const LayerArgs& a, AggRows rows, int64_t max_rows, int64_
   hp.heavy = w.alloc<int32_t>(max_rows + 1);
   hp.n_heavy = w.alloc<int64_t>(2);
   hp.hoff = w.alloc<int64_t>(max_rows + 2);
-  int64_t max_chunks = max_edges / kChunk + 2 + max_rows / 64;
+  int64_t max_chunks = heavy_chunk_bound(max_edges);
   hp.cmap = w.alloc<int32_t>(max_chunks);
   hp.arrive = w.alloc<int32_t>(max_rows + 1);
   hp.part = w.alloc<float>(max_chunks * static_cast<int64_t>(pw));
@@ -945,6 +950,7 @@ __global__ void __launch_bounds__(kLBlk) k_dd_heavy(LayerArgs a, AggRows rows, H
     if (!FULL && !r.full && c == 0) dd_struct<VEC, K>(a, D, r.p, r.q, acc);
     acc.store(hp.part + t * d, d);
     __threadfence();
+    __syncwarp();  // every lane's partial is fenced before the arrival is published
     int old = 0;
     if (lane_id() == 0) old = atomicAdd(hp.arrive + j, 1);
     old = __shfl_sync(0xffffffffu, old, 0);
@@ -1243,6 +1249,7 @@ __global__ void __launch_bounds__(kLBlk) k_max_heavy(LayerArgs a, AggRows rows, 
     }
     acc.store(hp.part + t * d, d);
     __threadfence();
+    __syncwarp();  // every lane's partial is fenced before the arrival is published
     int old = 0;
     if (lane_id() == 0) old = atomicAdd(hp.arrive + j, 1);
     old = __shfl_sync(0xffffffffu, old, 0);
@@ -1294,6 +1301,7 @@ __global__ void __launch_bounds__(kLBlk) k_max_rescan(LayerArgs a, AggRows rows,
     max_run<VEC, K>(a, beg, c * kChunk, min(len, (c + 1) * kChunk), acc);
     acc.store(rq.part + t * d, d);
     __threadfence();
+    __syncwarp();  // every lane's partial is fenced before the arrival is published
     int old = 0;
     if (lane_id() == 0) old = atomicAdd(rq.arrive + e, 1);
     old = __shfl_sync(0xffffffffu, old, 0);
@@ -1312,7 +1320,7 @@ static int launch_max(LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_
   HeavyPlan hp{};
   RTEC_TRY(plan_heavy<FULL>(a, rows, max_rows, max_edges, d, w, s, hp, true));
   MaxRescan rq{};
-  int64_t max_chunks = max_edges / kChunk + 2 + max_rows / 64;
+  int64_t max_chunks = heavy_chunk_bound(max_edges);
   rq.n = w.alloc<int64_t>(2);
   rq.total = rq.n + 1;
   rq.dest = w.alloc<int32_t>(max_rows + 1);
@@ -1503,11 +1511,20 @@ __device__ __forceinline__ void gat_finalize(const LayerArgs& a, int64_t i, int3
     o.store(a.st.log_out + i * d, d);
   }
   R o;
+  bool finite = true;
 #pragma unroll
   for (int k = 0; k < K; ++k)
 #pragma unroll
-    for (int jj = 0; jj < VEC; ++jj) o.v[k][jj] = indeg > 0 ? elu1(acc.v[k][jj] / cacc[k]) : 0.f;
+    for (int jj = 0; jj < VEC; ++jj) {
+      const float x = indeg > 0 ? acc.v[k][jj] / cacc[k] : 0.f;
+      finite = finite && isfinite(x);
+      o.v[k][jj] = elu1(x);
+    }
   o.store(hrow, d);
+  // an attention weight or sum that overflowed fp32 (exp of a logit above ~88.7; the f64
+  // reference's math.exp overflows above ~709.8) or a non-finite aggregate: NumericError
+  // at the destination (linalg.py:55-60 exp overflow, :22-29 non-finite result)
+  if (__any_sync(0xffffffffu, !finite) && lane_id() == 0) report_error(a.err, RTEC_NUMERIC_ERROR, v);
 }
 
 // 6 CTAs / SM (42 registers, spills): the GAT passes are latency-bound on their row
@@ -1595,6 +1612,7 @@ __global__ void __launch_bounds__(kLBlk, 6) k_gat_heavy(LayerArgs a, AggRows row
         for (int hh = 0; hh < (VEC > dh ? VEC / dh : 1); ++hh) part[d + (cc * VEC) / dh + hh] = cacc[k];
     }
     __threadfence();
+    __syncwarp();  // every lane's partial is fenced before the arrival is published
     int old = 0;
     if (lane_id() == 0) old = atomicAdd(hp.arrive + j, 1);
     old = __shfl_sync(0xffffffffu, old, 0);
@@ -1712,6 +1730,7 @@ struct GemmArgs {
   const float* bias;    // Y = scale * act(X W^T + bias) (PinSAGE payload, models.py:159)
   float scale;
   int has_scale;
+  uint64_t* nerr;       // non-finite output -> NumericError at the row's vertex (linalg.py:22-29)
 };
 
 constexpr int kGM = 64, kGN = 64, kGK = 16;
@@ -1770,6 +1789,7 @@ __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs g) {
       if (col >= g.d_out) continue;
       float y = acc[r][c];
       if (g.bias) y += g.bias[col];
+      if (g.nerr && !isfinite(y)) report_error(g.nerr, RTEC_NUMERIC_ERROR, g.y_rows ? g.y_rows[gr] : gr);
       if (g.act == 1) y = fmaxf(y, 0.f);
       if (g.has_scale) y *= g.scale;
       float* yp = g.Y + dst * g.ldy + col;
@@ -1858,7 +1878,8 @@ using namespace rtec;
 // update (and GIN's chained MLP) on rows of gemm_in: tcgen05 3xTF32 when the
 // layer carries prepared weights, SIMT fp32 otherwise
 static int run_update(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* st, const int64_t* n_rows,
-                      int64_t max_rows, const int32_t* y_rows, float* log, const uint64_t* err, cudaStream_t s);
+                      int64_t max_rows, const int32_t* y_rows, float* log, const uint64_t* err, cudaStream_t s,
+                      uint64_t* nerr);
 
 static int layer_dims_ok(const rtec_layer_t* L) {
   if (L->model < 0 || L->model > RTEC_MODEL_AGNN) {
@@ -1872,8 +1893,10 @@ static int layer_dims_ok(const rtec_layer_t* L) {
   return RTEC_OK;
 }
 
+// err: skip when set (the batch failed); nerr: where non-finite outputs are reported
 static int run_update(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* st, const int64_t* n_rows,
-                      int64_t max_rows, const int32_t* y_rows, float* log, const uint64_t* err, cudaStream_t s) {
+                      int64_t max_rows, const int32_t* y_rows, float* log, const uint64_t* err, cudaStream_t s,
+                      uint64_t* nerr) {
   const int ydiv = (st->out_local && st->row_div > 1) ? st->row_div : 1;
   auto fuse = [&](TcArgs& t) {  // the next layer's source deltas from this update's epilogue
     if (!st->delta_next || !y_rows || (L->d_out & 3)) return;
@@ -1892,29 +1915,35 @@ static int run_update(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t
       const int nkb2 = tc_nkb_of(L->d_out);
       TcArgs t1{st->gemm_in, L->Wt_hi, L->Wt_lo, nkb, tc_npad_of(L->d_out), L->d_out, n_rows, max_rows, 1,
                 nullptr, 0, nullptr, nullptr, st->gemm_mid, nkb2, err};
+      t1.nerr = nerr;
       RTEC_TRY(gemm_tc_launch(t1, s));
       TcArgs t2{st->gemm_mid, L->W2t_hi, L->W2t_lo, nkb2, tc_npad_of(L->d_out), L->d_out, n_rows, max_rows, 0,
                 st->H_out, L->d_out, y_rows, log, nullptr, 0, err};
       t2.ydiv = ydiv;
+      t2.nerr = nerr;
       fuse(t2);
       return gemm_tc_launch(t2, s);
     }
     TcArgs t{st->gemm_in, L->Wt_hi, L->Wt_lo, nkb, tc_npad_of(L->d_out), L->d_out, n_rows, max_rows, act,
              st->H_out, L->d_out, y_rows, log, nullptr, 0, err};
     t.ydiv = ydiv;
+    t.nerr = nerr;
     fuse(t);
     return gemm_tc_launch(t, s);
   }
   if (is_gin(L->model)) {
     GemmArgs g1{st->gemm_in, L->d_in, nullptr, L->W, L->d_in, L->d_out, n_rows, max_rows, 1,
                 st->gemm_mid, L->d_out, nullptr, nullptr, err};
+    g1.nerr = nerr;
     RTEC_TRY(gemm_launch(g1, s));
     GemmArgs g2{st->gemm_mid, L->d_out, nullptr, L->W2, L->d_out, L->d_out, n_rows, max_rows, 0,
                 st->H_out, L->d_out, y_rows, log, err, ydiv};
+    g2.nerr = nerr;
     return gemm_launch(g2, s);
   }
   GemmArgs g1{st->gemm_in, dk, nullptr, L->W, dk, L->d_out, n_rows, max_rows, act,
               st->H_out, L->d_out, y_rows, log, err, ydiv};
+  g1.nerr = nerr;
   return gemm_launch(g1, s);
 }
 
@@ -1964,11 +1993,11 @@ int rtec_layer_incremental(const rtec_graph_t* g, const rtec_batch_t* b, const r
   layer_args_init(a, L, st);
   if (L->model == RTEC_MODEL_GIN_MAX) {
     RTEC_TRY(launch_max<false>(a, AggRows{f->dst_list, f->n_dst, n}, n, g->in.slots, w, s));
-    return run_update(g, L, st, f->n_dst, n, f->dst_list, st->log_out, err, s);
+    return run_update(g, L, st, f->n_dst, n, f->dst_list, st->log_out, err, s, err);
   }
   if (edge_model(L->model)) {
     RTEC_TRY(launch_dd<false>(a, AggRows{f->dst_list, f->n_dst, n}, n, g->in.slots, w, s));
-    return run_update(g, L, st, f->n_dst, n, f->dst_list, st->log_out, err, s);
+    return run_update(g, L, st, f->n_dst, n, f->dst_list, st->log_out, err, s, err);
   }
   float* delta = st->delta ? st->delta : w.alloc<float>(n * static_cast<int64_t>(a.d_agg));
   RTEC_WS_CHECK(w);
@@ -1987,7 +2016,7 @@ int rtec_layer_incremental(const rtec_graph_t* g, const rtec_batch_t* b, const r
     RTEC_TRY(launch_aggregation<false>(a, AggRows{f->dst_list, f->n_dst, n}, n, g->in.slots, w, s));
   }
   // update on V_dst(l) rows with DeltaLog capture (operators.py:180)
-  return run_update(g, L, st, f->n_dst, n, f->dst_list, st->log_out, err, s);
+  return run_update(g, L, st, f->n_dst, n, f->dst_list, st->log_out, err, s, err);
 }
 
 
@@ -2009,6 +2038,7 @@ int rtec_layer_full(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* 
       return launch_gat<true>(a, AggRows{rows, n_rows, n}, max_rows, g->in.slots, w, s);
     // Z = W H (all rows), logits, then the full softmax aggregation
     GemmArgs gz{st->H_in, L->d_in, nullptr, L->W, L->d_in, L->d_out, nullptr, n, 0, st->Z, L->d_out, nullptr, nullptr, nullptr};
+    gz.nerr = err;
     RTEC_TRY(gemm_launch(gz, s));
     k_gat_logits<<<grid, kLBlk, 0, s>>>(st->Z, nullptr, nullptr, n, L->d_out, L->heads, L->att, st->el, st->er,
                                         nullptr, nullptr);
@@ -2020,7 +2050,7 @@ int rtec_layer_full(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* 
   if (L->model == RTEC_MODEL_GIN_MAX) {
     Ws w(ws, ws_bytes);
     RTEC_TRY(launch_max<true>(a, AggRows{rows, rows ? n_rows : nullptr, n}, mr, g->in.slots, w, s));
-    return run_update(g, L, st, rows ? n_rows : nullptr, mr, rows, nullptr, nullptr, s);
+    return run_update(g, L, st, rows ? n_rows : nullptr, mr, rows, nullptr, nullptr, s, err);
   }
   {
     Ws w(ws, ws_bytes);
@@ -2029,7 +2059,7 @@ int rtec_layer_full(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* 
     else
       RTEC_TRY(launch_aggregation<true>(a, AggRows{rows, rows ? n_rows : nullptr, n}, mr, g->in.slots, w, s));
   }
-  return run_update(g, L, st, rows ? n_rows : nullptr, mr, rows, nullptr, nullptr, s);
+  return run_update(g, L, st, rows ? n_rows : nullptr, mr, rows, nullptr, nullptr, s, err);
 }
 
 int rtec_gat_project(const rtec_layer_t* L, const float* H, const int32_t* rows, const int64_t* n_rows,
@@ -2039,6 +2069,7 @@ int rtec_gat_project(const rtec_layer_t* L, const float* H, const int32_t* rows,
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   GemmArgs gz{H, L->d_in, rows, L->W, L->d_in, L->d_out, rows ? n_rows : nullptr, n_or_max_rows, 0,
               Z, L->d_out, rows, Z_log, err};
+  gz.nerr = const_cast<uint64_t*>(err);
   RTEC_TRY(gemm_launch(gz, s));
   RTEC_PROF("k_gat_logits", s);
   k_gat_logits<<<kSMs * 8, kLBlk, 0, s>>>(Z, rows, n_rows, n_or_max_rows, L->d_out, L->heads, L->att, el, er, er_log,

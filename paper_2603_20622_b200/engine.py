@@ -22,6 +22,7 @@ device), so the whole step can be captured in a CUDA graph (`capture()`).
 from __future__ import annotations
 
 import ctypes as C
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -48,6 +49,8 @@ class Metrics:
     vertex_accesses: list = field(default_factory=list)
     as_edges: int = 0                            # affected subgraph: Σ_l |E_curr(l)|
     as_vertices: int = 0                         # Σ_l |V_dst(l)|
+    wall_time: float = 0.0                       # host seconds of the step, sync included
+    refreshed: bool = False                      # refresh_every fired after this batch (full bootstrap)
 
 
 def redundancy(m: Metrics, num_edges: int, num_vertices: int, breakdown: dict | None = None) -> dict:
@@ -70,12 +73,25 @@ def redundancy(m: Metrics, num_edges: int, num_vertices: int, breakdown: dict | 
     return out
 
 
-@dataclass
 class RunResult:
-    status: np.ndarray
-    deltas: np.ndarray
-    changed_final: np.ndarray | None
-    metrics: Metrics
+    """status u8[B] (1 applied), deltas int32[k, 5] DegreeDelta rows, metrics, and
+    `changed_final`: ascending ids of the vertices whose final-layer embedding was
+    recomputed (inc / uer / ns: V_dst(L-1) of the batch; full: every vertex; odec: none,
+    the rows are deferred).  The id list is snapshotted on the device at the end of the
+    step and copied to the host on first access."""
+
+    __slots__ = ("status", "deltas", "metrics", "_changed")
+
+    def __init__(self, status, deltas, changed_final, metrics):
+        self.status, self.deltas, self.metrics = status, deltas, metrics
+        self._changed = changed_final
+
+    @property
+    def changed_final(self) -> np.ndarray:
+        c = self._changed
+        if isinstance(c, torch.Tensor):
+            c = self._changed = c.cpu().numpy().astype(np.int64)
+        return c
 
 
 class _Frontier:
@@ -103,9 +119,16 @@ class RTECEngine:
     FUSED_DELTA = True
 
     def __init__(self, bundle: Bundle, graph: DynamicGraph, features, *, max_batch: int | None = None,
-                 update: str = "tc", use_graphs: bool = True, bootstrap: bool = True):
+                 update: str = "tc", use_graphs: bool = True, bootstrap: bool = True,
+                 refresh_every: int | None = None):
+        """refresh_every = R: after every R-th incremental batch the caches are rebuilt by a
+        full bootstrap (SPEC.md:494 drift control; default off)."""
         if not isinstance(bundle, Bundle) or bundle.model not in MODELS:
             raise E.UnsupportedModel("engine needs a bundle from paper_2603_20622_b200.models")
+        if refresh_every is not None and int(refresh_every) < 1:
+            raise E.ConfigError(f"refresh_every must be >= 1, got {refresh_every}")
+        self.refresh_every = None if refresh_every is None else int(refresh_every)
+        self._since_refresh = 0
         self.b = bundle
         self.g = graph
         self.use_graphs = bool(use_graphs)
@@ -290,10 +313,12 @@ class RTECEngine:
 
     # ---------------------------------------------------------------- incremental step
     def _graph_key(self, B: int):
-        """Everything a captured step bakes in: the batch size and every buffer address."""
+        """Everything a captured step bakes in: the batch size, the workspace and the raw
+        bytes of the graph / batch descriptors (every run-array pointer, slot count and
+        degree array), so a compaction or a batch-buffer reallocation can never replay a
+        graph against moved or freed buffers."""
         gr = self.g
-        return (B, gr.ws.data_ptr(), gr.ws.numel(), gr.out.nbr.data_ptr(), gr.inn.nbr.data_ptr(),
-                gr.batch.err.data_ptr(), gr.batch.cap)
+        return (B, gr.ws.data_ptr(), gr.ws.numel(), bytes(gr.c()), bytes(gr.batch.c()))
 
     def enqueue_step(self, B: int) -> None:
         """Enqueue the whole incremental pipeline for the staged batch (no sync).
@@ -617,6 +642,7 @@ class RTECEngine:
         counters from pinned buffers."""
         if mode not in ("inc", "uer", "full", "ns", "odec"):
             raise E.ConfigError(f"unknown engine mode {mode!r} (inc, uer, full, ns, odec)")
+        t0 = time.perf_counter()
         if mode != "odec" and getattr(self, "_stale", None) is not None and any(int(b.any()) for b in self._stale):
             raise E.StaleState("deferred (ODEC) rows pending: call odec_flush() before another mode")
         B = self.g.stage(op, src, dst, ts)
@@ -652,7 +678,27 @@ class RTECEngine:
         k = int(hb["nd"][0])
         # DegreeDelta rows (vertex, old_in, new_in, old_out, new_out) as int32 [k, 5]
         deltas = np.stack([h[:k].numpy() for h in hb["d"]], axis=1) if k else np.zeros((0, 5), np.int32)
-        return RunResult(status, deltas, None, self._metrics_from(hb["ctr"], mode))
+        m = self._metrics_from(hb["ctr"], mode)
+        changed = self._changed_final(mode, m)
+        if mode in ("inc", "uer") and self.refresh_every:
+            self._since_refresh += 1
+            if self._since_refresh >= self.refresh_every:  # SPEC.md:494 drift control
+                self.bootstrap()
+                self._since_refresh = 0
+                m.refreshed = True
+        elif mode == "full":
+            self._since_refresh = 0
+        m.wall_time = time.perf_counter() - t0
+        return RunResult(status, deltas, changed, m)
+
+    def _changed_final(self, mode: str, m: Metrics):
+        """Device snapshot of the ids whose final-layer rows this step recomputed."""
+        if mode == "odec":
+            return np.zeros(0, np.int64)
+        if mode == "full":
+            return torch.arange(self.n, dtype=torch.int64, device=self.dev)
+        k = m.v_dst[-1] if m.v_dst else 0
+        return self.fr[-1].dst_list[:k].clone()
 
     def run_incremental(self, batch) -> RunResult:
         """SPEC run_incremental on a coalesced EdgeUpdate list."""
@@ -769,3 +815,45 @@ class RTECEngine:
         return out[: ids_t.numel()].cpu().numpy()
 
     materialize_h = query
+
+
+# ---------------------------------------------------------------- full-recompute API (models.py:461-492)
+def _as_bundle(bundle) -> Bundle:
+    if isinstance(bundle, Bundle):
+        return bundle
+    from .models import from_reference
+
+    return from_reference(bundle)
+
+
+def layer_embeddings(bundle, layer: int, graph: DynamicGraph, H_prev):
+    """models.py:461-477 on the GPU: one full layer pass over `graph` from `H_prev`,
+    returning (H_next f32[n, out], aggregates f32[n, agg], contexts f64[n]) -- the
+    aggregates composed with the context (ms_cbn) exactly as the reference stores them.
+    `bundle` may be ours or a reference OperatorBundle (adopted by value)."""
+    b = _as_bundle(bundle)
+    n = graph.num_vertices
+    if not 0 <= int(layer) < b.num_layers:
+        raise E.ConfigError(f"layer {layer} outside [0, {b.num_layers})")
+    w = b.layers[layer]
+    shape = tuple(H_prev.shape)
+    if shape != (n, w.in_dim):
+        raise E.ConfigError(f"layer {layer}: embeddings shape {shape} unexpected")
+    from dataclasses import replace
+
+    sub = replace(b, layers=(w,), agg_dims=(b.agg_dims[layer],))
+    eng = RTECEngine(sub, graph, H_prev, use_graphs=False)
+    return eng.embeddings(1), eng.aggregates(0), eng.contexts(0)
+
+
+def forward_layer_reference(bundle, graph: DynamicGraph, H_prev, layer: int) -> np.ndarray:
+    """models.py:480-484: H_next of one full layer."""
+    return layer_embeddings(bundle, layer, graph, H_prev)[0]
+
+
+def reference_embeddings(bundle, graph: DynamicGraph, features) -> np.ndarray:
+    """models.py:487-492: final-layer embeddings from scratch (every layer recomputed on
+    the GPU by the same full-layer kernels the engine bootstraps with)."""
+    b = _as_bundle(bundle)
+    eng = RTECEngine(b, graph, features, use_graphs=False)
+    return eng.embeddings(b.num_layers)

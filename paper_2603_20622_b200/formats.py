@@ -112,12 +112,43 @@ def load_weights(path: str) -> dict:
 
 
 # ---------------------------------------------------------------- checkpoint / resume
+def _edges_table(src, dst, ts) -> np.ndarray:
+    """Edge list as an exact float64 NRTF table [src, dst, ts_hi, ts_lo]: ts = ts_hi * 2^32 +
+    ts_lo with ts_hi the arithmetic high word and ts_lo in [0, 2^32), both exact in f64, so
+    int64 timestamps (the reference keeps them as PMA uint64 payloads) survive any magnitude."""
+    ts = np.asarray(ts, np.int64)
+    return np.stack([np.asarray(src, np.float64), np.asarray(dst, np.float64),
+                     (ts >> 32).astype(np.float64), (ts & 0xFFFFFFFF).astype(np.float64)], 1)
+
+
+def _edges_from_table(e: np.ndarray):
+    """Inverse of _edges_table (also reads the 3-column version-1 layout)."""
+    src, dst = e[:, 0].astype(np.int64), e[:, 1].astype(np.int64)
+    if e.shape[1] == 3:
+        return src, dst, e[:, 2].astype(np.int64)
+    return src, dst, (e[:, 2].astype(np.int64) << 32) | e[:, 3].astype(np.int64)
+
+
+def _graph_knobs(g) -> dict:
+    return {"slack": float(g.slack), "min_slack": int(g.min_slack),
+            "reserve": None if g.reserve is None else int(g.reserve),
+            "segment_slots": int(g.segment_slots), "density_bounds": list(g.density_bounds)}
+
+
+def _graph_kw(side: dict) -> dict:
+    kw = {k: side["graph"][k] for k in ("slack", "min_slack", "reserve", "segment_slots") if "graph" in side}
+    if "graph" in side:
+        kw["density_bounds"] = tuple(side["graph"]["density_bounds"])
+    return kw
+
+
 def save_checkpoint(engine, directory: str) -> None:
-    """Snapshot an RTECEngine between batches: edges (src, dst, ts as float64 NRTF),
-    per-layer H / S (/ GAT ctx) as float32 NRTF, weights JSON and a JSON sidecar."""
+    """Snapshot an RTECEngine between batches: edges (exact float64 NRTF table, see
+    _edges_table), per-layer H / S (/ GAT ctx) as float32 NRTF, weights JSON and a JSON
+    sidecar (model config and the graph's slack / reserve knobs)."""
     os.makedirs(directory, exist_ok=True)
     src, dst, ts = engine.g.edges()
-    write_tensor(os.path.join(directory, "edges.nrtf"), np.stack([src, dst, ts], 1).astype(np.float64))
+    write_tensor(os.path.join(directory, "edges.nrtf"), _edges_table(src, dst, ts))
     for l in range(engine.L + 1):
         write_tensor(os.path.join(directory, f"H{l}.nrtf"), engine.H[l].cpu().numpy())
     for l in range(engine.L):
@@ -126,9 +157,9 @@ def save_checkpoint(engine, directory: str) -> None:
             write_tensor(os.path.join(directory, f"ctx{l}.nrtf"), engine.ctx[l].cpu().numpy())
     b = engine.b
     save_weights(b, os.path.join(directory, "weights.json"))
-    side = {"format": "rtec-b200-checkpoint", "version": 1, "model": b.model, "dims": list(b.dims),
+    side = {"format": "rtec-b200-checkpoint", "version": 2, "model": b.model, "dims": list(b.dims),
             "heads": int(b.heads), "degree_offset": float(b.degree_offset), "num_vertices": int(engine.n),
-            "num_edges": int(len(src))}
+            "num_edges": int(len(src)), "graph": _graph_knobs(engine.g)}
     with open(os.path.join(directory, "checkpoint.json"), "w", encoding="ascii") as fh:
         json.dump(side, fh, indent=1)
         fh.write("\n")
@@ -149,8 +180,8 @@ def load_checkpoint(directory: str, **engine_kw):
     w = load_weights(os.path.join(directory, "weights.json"))
     bundle = make_bundle(side["model"], side["dims"], weights=w["layers"], heads=side["heads"],
                          degree_smoothing=side["degree_offset"] != 0.0)
-    e = read_tensor(os.path.join(directory, "edges.nrtf")).astype(np.int64)
-    g = DynamicGraph.from_edges(side["num_vertices"], (e[:, 0], e[:, 1], e[:, 2]))
+    e = _edges_from_table(read_tensor(os.path.join(directory, "edges.nrtf")))
+    g = DynamicGraph.from_edges(side["num_vertices"], e, **_graph_kw(side))
     X = read_tensor(os.path.join(directory, "H0.nrtf"))
     eng = RTECEngine(bundle, g, X, bootstrap=False, **engine_kw)
     for l in range(1, eng.L + 1):
@@ -175,7 +206,7 @@ def save_sharded_checkpoint(engine, directory: str) -> None:
     d = _rank_dir(directory, r)
     os.makedirs(d, exist_ok=True)
     src, dst, ts = engine.g.edges()  # this rank's shard: the edges whose destination it owns
-    write_tensor(os.path.join(d, "edges.nrtf"), np.stack([src, dst, ts], 1).astype(np.float64))
+    write_tensor(os.path.join(d, "edges.nrtf"), _edges_table(src, dst, ts))
     for l in range(engine.L + 1):  # inputs are full replicas, the final layer per owned vertex
         write_tensor(os.path.join(d, f"H{l}.nrtf"), engine.H[l].cpu().numpy())
     for l in range(engine.L):
@@ -184,7 +215,7 @@ def save_sharded_checkpoint(engine, directory: str) -> None:
             write_tensor(os.path.join(d, f"ctx{l}.nrtf"), engine.ctx[l].cpu().numpy())
     b = engine.b
     save_weights(b, os.path.join(d, "weights.json"))
-    side = {"format": "rtec-b200-sharded-checkpoint", "version": 1, "model": b.model, "dims": list(b.dims),
+    side = {"format": "rtec-b200-sharded-checkpoint", "version": 2, "model": b.model, "dims": list(b.dims),
             "heads": int(b.heads), "degree_offset": float(b.degree_offset), "num_vertices": int(engine.n),
             "world_size": int(P), "rank": int(r), "num_edges_shard": int(len(src))}
     with open(os.path.join(d, "checkpoint.json"), "w", encoding="ascii") as fh:
@@ -211,9 +242,9 @@ def load_sharded_checkpoint(directory: str, comm, **engine_kw):
     w = load_weights(os.path.join(d, "weights.json"))
     bundle = make_bundle(side["model"], side["dims"], weights=w["layers"], heads=side["heads"],
                          degree_smoothing=side["degree_offset"] != 0.0)
-    e = read_tensor(os.path.join(d, "edges.nrtf")).astype(np.int64)
+    e = _edges_from_table(read_tensor(os.path.join(d, "edges.nrtf")))
     X = read_tensor(os.path.join(d, "H0.nrtf"))
-    eng = ShardedRTECEngine(bundle, side["num_vertices"], (e[:, 0], e[:, 1], e[:, 2]), X, comm, bootstrap=False,
+    eng = ShardedRTECEngine(bundle, side["num_vertices"], e, X, comm, bootstrap=False,
                             **engine_kw)
     for l in range(1, eng.L + 1):
         eng.H[l].copy_(torch.from_numpy(read_tensor(os.path.join(d, f"H{l}.nrtf"))))

@@ -109,6 +109,7 @@ class DeviceBatch:
         self.i_src, self.i_dst, self.i_op = z(cap, torch.int32), z(cap, torch.int32), z(cap, torch.uint8)
         self.d = [z(2 * cap, torch.int32) for _ in range(5)]
         self.n_delta = z(1, torch.int64)
+        self.apply_ctr = z(4, torch.int64)  # run-merge volume of the last apply (rtec_batch_t.apply_ctr)
         # staging of the batch itself
         self.src, self.dst = z(cap, torch.int32), z(cap, torch.int32)
         self.op, self.ts = z(cap, torch.uint8), z(cap, torch.int64)
@@ -118,17 +119,33 @@ class DeviceBatch:
         d = self.d
         return _lib.Batch(self.cap, p(self.err), p(self.status), p(self.a_src), p(self.a_dst), p(self.a_op),
                           p(self.a_ts), p(self.n_applied), p(self.i_src), p(self.i_dst), p(self.i_op),
-                          p(d[0]), p(d[1]), p(d[2]), p(d[3]), p(d[4]), p(self.n_delta), p(self.irange))
+                          p(d[0]), p(d[1]), p(d[2]), p(d[3]), p(d[4]), p(self.n_delta), p(self.irange), None,
+                          p(self.apply_ctr))
 
 
 class DynamicGraph:
     """Directed graph over [0, n) in B200 HBM (graph.py:59-235 semantics)."""
 
-    def __init__(self, num_vertices: int, *, device=None, slack: float = 0.25, min_slack: int = 4,
-                 reserve: int | None = None):
+    def __init__(self, num_vertices: int, *, segment_slots: int = 64,
+                 density_bounds: tuple[float, float] = (0.25, 0.875), device=None, slack: float | None = None,
+                 min_slack: int = 4, reserve: int | None = None):
+        """`segment_slots` / `density_bounds` are the reference's PMA knobs (graph.py:62-68,
+        pma.py:40-57), validated with the same rules.  Here every vertex run is its own
+        gapped segment: a run of length k gets max(min_slack, ceil(slack * k)) free slots,
+        and `slack` defaults to the free fraction the upper density bound leaves
+        (1/hi - 1, at least 0.25)."""
         n = int(num_vertices)
         if n < 0 or n * n >= _MAX_KEY or n >= (1 << 31):  # graph.py:69-71
             raise E.ConfigError(f"unsupported vertex count {num_vertices}")
+        lo, hi = (float(x) for x in density_bounds)
+        if not 0.0 < lo < hi <= 1.0:
+            raise E.ConfigError(f"density bounds must satisfy 0 < lo < hi <= 1, got {density_bounds}")
+        seg = int(segment_slots)
+        if seg < 2 or int(hi * seg) < 1 or int(hi * seg) >= seg:
+            raise E.ConfigError(f"segment_slots={segment_slots} does not fit density bounds {density_bounds}")
+        self.segment_slots, self.density_bounds = seg, (lo, hi)
+        if slack is None:
+            slack = max(0.25, 1.0 / hi - 1.0)
         self.lib = _lib.load()
         self.dev = _device(device)
         self.n = n
@@ -299,7 +316,8 @@ class DynamicGraph:
 
     def copy(self) -> "DynamicGraph":  # graph.py:172-180
         s, d, t = self.edges()
-        g = DynamicGraph(self.n, device=self.dev, slack=self.slack, min_slack=self.min_slack, reserve=self.reserve)
+        g = DynamicGraph(self.n, segment_slots=self.segment_slots, density_bounds=self.density_bounds, device=self.dev,
+                         slack=self.slack, min_slack=self.min_slack, reserve=self.reserve)
         g._build(s, d, t)
         return g
 
@@ -444,26 +462,29 @@ def invert_batch(batch: Sequence[EdgeUpdate]) -> list:
     return [EdgeUpdate(flip[u.op], u.src, u.dst, u.ts) for u in batch]
 
 
+def _parse_update(path: str, lineno: int, text: str) -> EdgeUpdate:
+    """One 'op,src,dst,ts' record of an edge-stream file (graph.py:269-293 format)."""
+    fields = text.split(",")
+    op = {"+": UpdateOp.INSERT, "-": UpdateOp.DELETE}.get(fields[0]) if len(fields) == 4 else None
+    if op is None:
+        raise E.ConfigError(f"{path}:{lineno}: malformed update line {text!r}")
+    try:
+        ids = [int(f) for f in fields[1:]]
+    except ValueError as exc:
+        raise E.ConfigError(f"{path}:{lineno}: non-integer field in {text!r}") from exc
+    return EdgeUpdate(op, *ids)
+
+
 def read_stream(path: str) -> list:
-    """Edge-stream text file (graph.py:269-293): one 'op,src,dst,ts' line per update."""
-    out: list = []
+    """Edge-stream text file: one 'op,src,dst,ts' update per line; blank lines and
+    '#' comments skipped; a malformed record raises ConfigError naming path:line."""
     with open(path, "r", encoding="ascii") as fh:
-        for lineno, line in enumerate(fh, start=1):
-            line = line.strip()
-            if not line or line.startswith("#"):
-                continue
-            parts = line.split(",")
-            if len(parts) != 4 or parts[0] not in ("+", "-"):
-                raise E.ConfigError(f"{path}:{lineno}: malformed update line {line!r}")
-            try:
-                s, d, t = int(parts[1]), int(parts[2]), int(parts[3])
-            except ValueError as exc:
-                raise E.ConfigError(f"{path}:{lineno}: non-integer field in {line!r}") from exc
-            out.append(EdgeUpdate(UpdateOp(parts[0]), s, d, t))
-    return out
+        lines = [(k, ln.strip()) for k, ln in enumerate(fh, start=1)]
+    return [_parse_update(path, k, t) for k, t in lines if t and not t.startswith("#")]
 
 
 def write_stream(path: str, updates: Iterable[EdgeUpdate]) -> None:
+    """Inverse of read_stream (one record per line, ASCII)."""
+    recs = "".join("%s,%d,%d,%d\n" % (u.op.value, u.src, u.dst, u.ts) for u in updates)
     with open(path, "w", encoding="ascii") as fh:
-        for u in updates:
-            fh.write(f"{u.op.value},{u.src},{u.dst},{u.ts}\n")
+        fh.write(recs)

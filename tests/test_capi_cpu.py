@@ -59,7 +59,7 @@ def test_struct_layouts_match_header(lib):
     assert list(sizes) == [ctypes.sizeof(t) for t in mirror]
     assert ctypes.sizeof(_lib.Adj) == 8 * 7
     assert ctypes.sizeof(_lib.Graph) == 8 + 2 * 56 + 5 * 8 + 8 + 8  # + part_rank / part_count
-    assert ctypes.sizeof(_lib.Batch) == 8 * 19
+    assert ctypes.sizeof(_lib.Batch) == 8 * 20  # + apply_ctr
     assert ctypes.sizeof(_lib.Frontier) == 8 * 11
     assert ctypes.sizeof(_lib.Layer) == 6 * 4 + 9 * 8 + 8  # + Wp, bp, scalar, d_k
     assert ctypes.sizeof(_lib.State) == 15 * 8 + 16
