@@ -469,7 +469,8 @@ def run_ours(args, world, rank, local):
         "config": bench_config(args, wl, world),
         "e2e": {"value": round(e2e_val, 1) if e2e_val else None, "unit": "edge updates/s", "steps": E2E,
                 "h2d_bytes_per_step": h2d // max(E2E, 1), "d2h_bytes_per_step": d2h // max(E2E, 1),
-                "p50_batch_ms": round(statistics.median(e2e_ms), 4) if e2e_ms else None},
+                "p50_batch_ms": round(statistics.median(e2e_ms), 4) if e2e_ms else None,
+                "batch_ms": [round(x, 3) for x in e2e_ms]},
         "gpu_launches": None,
         "roofline": roof,
         "gpu_baselines": baselines or None,
@@ -485,6 +486,8 @@ def run_ours(args, world, rank, local):
     # captured step: every kernel node is one of ours; eager (sharded / --no-graphs): the scope count
     res["gpu_launches"] = (nodes if nodes and nodes > 0 else launches_per_step(prof, PROF)) * K
     res["cuda_graph"] = bool(graphs_on and nodes)
+    res["graph_captures"] = len(getattr(eng, "_graphs", {}))
+    res["compactions"] = int(getattr(g, "compactions", 0))
     return res, g, eng
 
 

@@ -69,6 +69,8 @@ struct LayerArgs {
   int c0, cw;                   // feature slice [c0, c0 + cw) of the d_agg-wide rows (aggregation)
   int gcol, gk;                 // aggregate columns start at gcol of the gk-wide update input
   const float* self_in;         // H^l (st.H_in is redirected to the payload rows for PinSAGE / MoNet)
+  int hot_deg;                  // > 0: gathered rows of sources with out-degree >= hot_deg are
+                                // loaded L2 evict_last, the rest evict_first (RTEC_HOT_DEG)
   int layer;
   uint64_t* err;
 };
@@ -143,31 +145,39 @@ __device__ __forceinline__ void agg_edges(const LayerArgs& a, int64_t beg, int32
   const int d = a.d_agg, cw = a.cw;
   const int lane = lane_id();
   const uint64_t pol = l2_evict_first_policy();
+  const uint64_t pol_hot = l2_evict_last_policy();
+  const bool hinted = a.hot_deg > 0;
   for (int32_t c0 = e0; c0 < e1; c0 += 32) {
     int32_t j = c0 + lane;
     int32_t u = 0;
-    bool hit = false;
+    bool hit = false, hot = false;
     float cu = 0.f;
     if (j < e1) {
       u = ld_stream_i32(a.g.in.nbr + beg + j, pol);
       if (FULL) {
         hit = true;
-        cu = src_coeff(a.L.model, a.g.out_deg[u], a.L.degree_offset);
+        const int32_t od = a.g.out_deg[u];
+        cu = src_coeff(a.L.model, od, a.L.degree_offset);
+        hot = od >= a.hot_deg;
       } else {
         hit = bm_test(a.f.bm_src, u) && !in_range_has(a.b.i_src, p, q, u);
+        if (hinted && hit) hot = a.g.out_deg[u] >= a.hot_deg;
       }
     }
     unsigned m = __ballot_sync(0xffffffffu, hit);
+    const unsigned hm = __ballot_sync(0xffffffffu, hot);
     const float* base = (FULL ? a.st.H_in : a.delta) + a.c0;
     // gathered row: the source's own row (H_in, vertex-indexed δ) or its δ slot
     int32_t row = (!FULL && hit && a.st.delta_slot) ? a.f.src_slot[u] : u;
     while (m) {
       int32_t rw[UNR];
       float cs[UNR];
+      bool hh[UNR];
       int cnt = 0;
 #pragma unroll
       for (int t = 0; t < UNR; ++t) {
         int src = m ? __ffs(m) - 1 : 0;
+        hh[t] = (hm >> src) & 1u;
         if (m) {
           m &= m - 1;
           cnt = t + 1;
@@ -178,7 +188,10 @@ __device__ __forceinline__ void agg_edges(const LayerArgs& a, int64_t beg, int32
       float r[UNR][K][VEC];
 #pragma unroll
       for (int t = 0; t < UNR; ++t)
-        if (t < cnt) R::load(base + static_cast<int64_t>(rw[t]) * d, cw, r[t]);
+        if (t < cnt) {
+          if (hinted) R::load_hint(base + static_cast<int64_t>(rw[t]) * d, cw, r[t], hh[t] ? pol_hot : pol);
+          else R::load(base + static_cast<int64_t>(rw[t]) * d, cw, r[t]);
+        }
 #pragma unroll
       for (int t = 0; t < UNR; ++t) {
         if (t < cnt) {
@@ -645,6 +658,26 @@ static bool agg_batched(int d) {
   return d <= b;
 }
 
+// RTEC_HOT_DEG env: out-degree threshold of the L2 evict_last gathers (0: off); RTEC_PERSIST_MB:
+// persisting-L2 set-aside (cudaLimitPersistingL2CacheSize) requested once per process
+static int hot_degree() {
+  static int h = -1;
+  if (h < 0) {
+    const char* e = getenv("RTEC_HOT_DEG");
+    h = e ? atoi(e) : 0;
+    if (h < 0) h = 0;
+    const char* pm = getenv("RTEC_PERSIST_MB");
+    if (pm && atoi(pm) > 0) {
+      int dev = 0, mx = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
+      size_t want = static_cast<size_t>(atoi(pm)) << 20;
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want < static_cast<size_t>(mx) ? want : static_cast<size_t>(mx));
+    }
+  }
+  return h;
+}
+
 // RTEC_HEAVY_ORDER env: visit hub chunks in relative-position order (default 1; 0: destination-major)
 static bool heavy_order() {
   static int o = -1;
@@ -700,6 +733,7 @@ static int launch_aggregation(LayerArgs& a, AggRows rows, int64_t max_rows, int6
   HeavyPlan hp{};
   RTEC_TRY(plan_heavy<FULL>(a, rows, max_rows, max_edges, d, w, s, hp));
   const int grid = kSMs * 8;
+  a.hot_deg = hot_degree();
   // Feature slicing: one pass per `sw`-column slice keeps the gathered rows'
   // working set (|S| x sw x 4 B) small enough for the hot sources to stay in
   // L2 (126 MB); the plan above is shared by all passes.
@@ -1517,7 +1551,7 @@ __device__ __forceinline__ void gat_finalize(const LayerArgs& a, int64_t i, int3
 #pragma unroll
     for (int jj = 0; jj < VEC; ++jj) {
       const float x = indeg > 0 ? acc.v[k][jj] / cacc[k] : 0.f;
-      finite = finite && isfinite(x);
+      finite = finite && (isfinite(x) || !R::has(k, d));  // chunks beyond d hold 0 / 0
       o.v[k][jj] = elu1(x);
     }
   o.store(hrow, d);

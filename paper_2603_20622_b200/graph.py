@@ -155,6 +155,7 @@ class DynamicGraph:
         self.ws = torch.empty(0, dtype=torch.uint8, device=self.dev)
         self.batch = DeviceBatch(1024, self.dev, n)
         self.m_hint = 0
+        self.compactions = 0  # rebuilds since construction (arena full / explicit)
         # vertex sharding (shard.py): this graph holds the edges whose dst it owns
         self.part_rank, self.part_count = 0, 1
         self._build(np.zeros(0, np.int32), np.zeros(0, np.int32), None)
@@ -334,6 +335,7 @@ class DynamicGraph:
             _lib.check(self.lib.rtec_adj_compact(self.n, C.byref(a_old), C.byref(a_new), self.slack, self.min_slack,
                                                  _lib.ptr(ws), ws.numel(), st), "compact")
             setattr(self, name, new)
+        self.compactions += 1
         self._ensure_ws(self.batch.cap)
 
     # ---------------------------------------------------------------- mutation
