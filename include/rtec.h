@@ -288,10 +288,14 @@ int rtec_layer_incremental(const rtec_graph_t* g, const rtec_batch_t* b, const r
 int rtec_layer_full(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* st,
                     const int32_t* rows, const int64_t* n_rows, int64_t max_rows, uint64_t* err,
                     void* ws, size_t ws_bytes, rtec_stream_t stream);
-/* GAT f_nn / logit halves for rows (models.py:265-279): Z = W h, el, er. */
+/* GAT f_nn / logit halves for rows (models.py:265-279): Z = W h, el, er.  With the
+ * layer's tcgen05 operand images (L->Wt_hi) and an A-image scratch `a_img` of
+ * ceil(rows/128)*128 x ceil(d_in/32)*32 floats, the rows are packed and Z runs on
+ * tcgen05 (3xTF32); a_img == NULL -> SIMT fp32.  A non-finite Z row -> NumericError
+ * (position = vertex) in *err. */
 int rtec_gat_project(const rtec_layer_t* L, const float* H, const int32_t* rows, const int64_t* n_rows,
                      int64_t n_or_max_rows, float* Z, float* el, float* er,
-                     float* Z_log, float* er_log, const uint64_t* err, rtec_stream_t stream);
+                     float* Z_log, float* er_log, const uint64_t* err, float* a_img, rtec_stream_t stream);
 
 /* Per-source projections of the payload / gate models for all vertices
  * (rows == NULL) or the listed rows (V_chg(l-1) before layer l):

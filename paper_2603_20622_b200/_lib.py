@@ -98,7 +98,7 @@ _SIGS = {
     "rtec_layer_incremental": (C.c_int, [C.POINTER(Graph), C.POINTER(Batch), C.POINTER(Layer), C.POINTER(State),
                                          C.POINTER(Frontier), C.POINTER(Frontier), P, P, SZ, P]),
     "rtec_layer_full": (C.c_int, [C.POINTER(Graph), C.POINTER(Layer), C.POINTER(State), P, P, I64, P, P, SZ, P]),
-    "rtec_gat_project": (C.c_int, [C.POINTER(Layer), P, P, P, I64, P, P, P, P, P, P, P]),
+    "rtec_gat_project": (C.c_int, [C.POINTER(Layer), P, P, P, I64, P, P, P, P, P, P, P, P]),
     "rtec_project": (C.c_int, [C.POINTER(Layer), P, P, P, I64, P, P, P, P]),
     "rtec_update_gemm": (C.c_int, [P, I64, P, I32, I32, P, I64, I32, P, I64, P, P, P, P]),
     "rtec_query": (C.c_int, [P, I64, P, I64, P, I32, P, P]),

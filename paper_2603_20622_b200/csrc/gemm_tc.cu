@@ -480,6 +480,43 @@ __global__ void k_prep_b(const float* __restrict__ W, int d_in, int d_out, int n
   }
 }
 
+// gathered rows -> SW128 A image: one warp per row, lane = 4 consecutive columns (scalar
+// loads: rows of odd 16-byte alignment such as d = 602 are read coalesced), one float4
+// store per lane into its swizzled 16-byte slot
+__global__ void k_pack_rows(const float* __restrict__ X, int64_t ld, int d, const int32_t* __restrict__ rows,
+                            const int64_t* n_rows, int64_t n_all, float* __restrict__ img, int nkb, const uint64_t* err) {
+  if (err && err_set(err)) return;
+  const int64_t nr = n_rows ? *n_rows : n_all;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int kw = nkb * kTK;
+  for (int64_t i = warp; i < nr; i += nw) {
+    const int64_t src = rows ? static_cast<int64_t>(rows[i]) : i;
+    const float* xr = X + src * ld;
+    const int64_t tile = i / kTM;
+    const int r = static_cast<int>(i % kTM);
+    for (int c = lane * 4; c < kw; c += 128) {
+      float4 v;
+      v.x = c < d ? __ldg(xr + c) : 0.f;
+      v.y = c + 1 < d ? __ldg(xr + c + 1) : 0.f;
+      v.z = c + 2 < d ? __ldg(xr + c + 2) : 0.f;
+      v.w = c + 3 < d ? __ldg(xr + c + 3) : 0.f;
+      const int kb = c / kTK, cc = c % kTK;
+      *reinterpret_cast<float4*>(img + ((tile * nkb + kb) * kTM) * kTK + sw128_off(r, cc)) = v;
+    }
+  }
+}
+
+int gemm_tc_pack_rows(const float* X, int64_t ld, int d, const int32_t* rows, const int64_t* n_rows, int64_t n_all,
+                      float* img, int nkb, const uint64_t* err, cudaStream_t s) {
+  if (n_all <= 0) return RTEC_OK;
+  RTEC_PROF("k_pack_rows", s);
+  k_pack_rows<<<grid_for(n_all * 32, 256, kSMs * 8), 256, 0, s>>>(X, ld, d, rows, n_rows, n_all, img, nkb, err);
+  RTEC_LAUNCH_CHECK("k_pack_rows");
+  return RTEC_OK;
+}
+
 size_t gemm_tc_smem(int npad, bool fused) {
   TcShape sh = tc_shape(npad, fused);
   return static_cast<size_t>(sh.SA) * 2 * kABlockBytes + static_cast<size_t>(sh.SB) * sh.bstage + kEpiBytes +

@@ -35,6 +35,11 @@ struct TcArgs {
 
 int gemm_tc_launch(const TcArgs& g, cudaStream_t s);
 
+// rows of a row-major [*, ld] matrix (rows[i], or i when rows is null; i < *n_rows or
+// n_all) -> the SW128 A image [tiles][nkb][128][32] with zero K padding beyond d
+int gemm_tc_pack_rows(const float* X, int64_t ld, int d, const int32_t* rows, const int64_t* n_rows, int64_t n_all,
+                      float* img, int nkb, const uint64_t* err, cudaStream_t s);
+
 __host__ __device__ __forceinline__ int tc_nkb_of(int d) { return (d + 31) / 32; }
 __host__ __device__ __forceinline__ int tc_npad_of(int d) { return (d + 15) / 16 * 16; }
 

@@ -69,8 +69,6 @@ struct LayerArgs {
   int c0, cw;                   // feature slice [c0, c0 + cw) of the d_agg-wide rows (aggregation)
   int gcol, gk;                 // aggregate columns start at gcol of the gk-wide update input
   const float* self_in;         // H^l (st.H_in is redirected to the payload rows for PinSAGE / MoNet)
-  int hot_deg;                  // > 0: gathered rows of sources with out-degree >= hot_deg are
-                                // loaded L2 evict_last, the rest evict_first (RTEC_HOT_DEG)
   int layer;
   uint64_t* err;
 };
@@ -145,39 +143,31 @@ __device__ __forceinline__ void agg_edges(const LayerArgs& a, int64_t beg, int32
   const int d = a.d_agg, cw = a.cw;
   const int lane = lane_id();
   const uint64_t pol = l2_evict_first_policy();
-  const uint64_t pol_hot = l2_evict_last_policy();
-  const bool hinted = a.hot_deg > 0;
   for (int32_t c0 = e0; c0 < e1; c0 += 32) {
     int32_t j = c0 + lane;
     int32_t u = 0;
-    bool hit = false, hot = false;
+    bool hit = false;
     float cu = 0.f;
     if (j < e1) {
       u = ld_stream_i32(a.g.in.nbr + beg + j, pol);
       if (FULL) {
         hit = true;
-        const int32_t od = a.g.out_deg[u];
-        cu = src_coeff(a.L.model, od, a.L.degree_offset);
-        hot = od >= a.hot_deg;
+        cu = src_coeff(a.L.model, a.g.out_deg[u], a.L.degree_offset);
       } else {
         hit = bm_test(a.f.bm_src, u) && !in_range_has(a.b.i_src, p, q, u);
-        if (hinted && hit) hot = a.g.out_deg[u] >= a.hot_deg;
       }
     }
     unsigned m = __ballot_sync(0xffffffffu, hit);
-    const unsigned hm = __ballot_sync(0xffffffffu, hot);
     const float* base = (FULL ? a.st.H_in : a.delta) + a.c0;
     // gathered row: the source's own row (H_in, vertex-indexed δ) or its δ slot
     int32_t row = (!FULL && hit && a.st.delta_slot) ? a.f.src_slot[u] : u;
     while (m) {
       int32_t rw[UNR];
       float cs[UNR];
-      bool hh[UNR];
       int cnt = 0;
 #pragma unroll
       for (int t = 0; t < UNR; ++t) {
         int src = m ? __ffs(m) - 1 : 0;
-        hh[t] = (hm >> src) & 1u;
         if (m) {
           m &= m - 1;
           cnt = t + 1;
@@ -188,10 +178,7 @@ __device__ __forceinline__ void agg_edges(const LayerArgs& a, int64_t beg, int32
       float r[UNR][K][VEC];
 #pragma unroll
       for (int t = 0; t < UNR; ++t)
-        if (t < cnt) {
-          if (hinted) R::load_hint(base + static_cast<int64_t>(rw[t]) * d, cw, r[t], hh[t] ? pol_hot : pol);
-          else R::load(base + static_cast<int64_t>(rw[t]) * d, cw, r[t]);
-        }
+        if (t < cnt) R::load(base + static_cast<int64_t>(rw[t]) * d, cw, r[t]);
 #pragma unroll
       for (int t = 0; t < UNR; ++t) {
         if (t < cnt) {
@@ -658,26 +645,6 @@ static bool agg_batched(int d) {
   return d <= b;
 }
 
-// RTEC_HOT_DEG env: out-degree threshold of the L2 evict_last gathers (0: off); RTEC_PERSIST_MB:
-// persisting-L2 set-aside (cudaLimitPersistingL2CacheSize) requested once per process
-static int hot_degree() {
-  static int h = -1;
-  if (h < 0) {
-    const char* e = getenv("RTEC_HOT_DEG");
-    h = e ? atoi(e) : 0;
-    if (h < 0) h = 0;
-    const char* pm = getenv("RTEC_PERSIST_MB");
-    if (pm && atoi(pm) > 0) {
-      int dev = 0, mx = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
-      size_t want = static_cast<size_t>(atoi(pm)) << 20;
-      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want < static_cast<size_t>(mx) ? want : static_cast<size_t>(mx));
-    }
-  }
-  return h;
-}
-
 // RTEC_HEAVY_ORDER env: visit hub chunks in relative-position order (default 1; 0: destination-major)
 static bool heavy_order() {
   static int o = -1;
@@ -733,7 +700,6 @@ static int launch_aggregation(LayerArgs& a, AggRows rows, int64_t max_rows, int6
   HeavyPlan hp{};
   RTEC_TRY(plan_heavy<FULL>(a, rows, max_rows, max_edges, d, w, s, hp));
   const int grid = kSMs * 8;
-  a.hot_deg = hot_degree();
   // Feature slicing: one pass per `sw`-column slice keeps the gathered rows'
   // working set (|S| x sw x 4 B) small enough for the hot sources to stay in
   // L2 (126 MB); the plan above is shared by all passes.
@@ -2065,17 +2031,14 @@ int rtec_layer_full(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* 
   a.L = *L;
   a.st = *st;
   a.err = err;
-  const int grid = kSMs * 8;
   if (L->model == RTEC_MODEL_GAT) {
     Ws w(ws, ws_bytes);
     if (rows)  // listed rows (UER): the caller keeps Z / el / er current for the changed sources
       return launch_gat<true>(a, AggRows{rows, n_rows, n}, max_rows, g->in.slots, w, s);
-    // Z = W H (all rows), logits, then the full softmax aggregation
-    GemmArgs gz{st->H_in, L->d_in, nullptr, L->W, L->d_in, L->d_out, nullptr, n, 0, st->Z, L->d_out, nullptr, nullptr, nullptr};
-    gz.nerr = err;
-    RTEC_TRY(gemm_launch(gz, s));
-    k_gat_logits<<<grid, kLBlk, 0, s>>>(st->Z, nullptr, nullptr, n, L->d_out, L->heads, L->att, st->el, st->er,
-                                        nullptr, nullptr);
+    // Z = W H (all rows; tcgen05 when the layer carries operand images), logits, then the
+    // full softmax aggregation
+    RTEC_TRY(rtec_gat_project(L, st->H_in, nullptr, nullptr, n, st->Z, st->el, st->er, nullptr, nullptr, err,
+                              st->gemm_in, stream));
     return launch_gat<true>(a, AggRows{nullptr, nullptr, n}, n, g->in.slots, w, s);
   }
   if (!rows) RTEC_TRY(rtec_project(L, st->H_in, nullptr, nullptr, n, st->Z, nullptr, nullptr, stream));
@@ -2098,16 +2061,30 @@ int rtec_layer_full(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t* 
 
 int rtec_gat_project(const rtec_layer_t* L, const float* H, const int32_t* rows, const int64_t* n_rows,
                      int64_t n_or_max_rows, float* Z, float* el, float* er, float* Z_log, float* er_log,
-                     const uint64_t* err, rtec_stream_t stream) {
+                     const uint64_t* err, float* a_img, rtec_stream_t stream) {
   RTEC_TRY(layer_dims_ok(L));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  GemmArgs gz{H, L->d_in, rows, L->W, L->d_in, L->d_out, rows ? n_rows : nullptr, n_or_max_rows, 0,
-              Z, L->d_out, rows, Z_log, err};
-  gz.nerr = const_cast<uint64_t*>(err);
-  RTEC_TRY(gemm_launch(gz, s));
+  const int64_t* nr = rows ? n_rows : nullptr;
+  uint64_t* nerr = const_cast<uint64_t*>(err);
+  if (L->Wt_hi && a_img) {
+    // K13 on tcgen05: the rows are gathered into the SW128 A image, then the 3xTF32
+    // GEMM scatters Z[rows] (old rows into Z_log) -- f_nn = W h_u (models.py:279)
+    const int nkb = tc_nkb_of(L->d_in);
+    const uint64_t* skip = rows ? err : nullptr;  // a failed batch skips; bootstrap always runs
+    RTEC_TRY(gemm_tc_pack_rows(H, L->d_in, L->d_in, rows, nr, n_or_max_rows, a_img, nkb, skip, s));
+    TcArgs t{a_img, L->Wt_hi, L->Wt_lo, nkb, tc_npad_of(L->d_out), L->d_out, nr, n_or_max_rows, 0,
+             Z, L->d_out, rows, Z_log, nullptr, 0, skip};
+    t.nerr = nerr;
+    RTEC_TRY(gemm_tc_launch(t, s));
+  } else {
+    GemmArgs gz{H, L->d_in, rows, L->W, L->d_in, L->d_out, nr, n_or_max_rows, 0,
+                Z, L->d_out, rows, Z_log, rows ? err : nullptr};
+    gz.nerr = nerr;
+    RTEC_TRY(gemm_launch(gz, s));
+  }
   RTEC_PROF("k_gat_logits", s);
   k_gat_logits<<<kSMs * 8, kLBlk, 0, s>>>(Z, rows, n_rows, n_or_max_rows, L->d_out, L->heads, L->att, el, er, er_log,
-                                          err);
+                                          rows ? err : nullptr);
   RTEC_LAUNCH_CHECK("k_gat_logits");
   return RTEC_OK;
 }

@@ -28,18 +28,6 @@ __device__ __forceinline__ uint64_t l2_evict_first_policy() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
-__device__ __forceinline__ uint64_t l2_evict_last_policy() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-// read-only gathered row chunk with an L2 eviction-priority hint
-__device__ __forceinline__ float4 ld_hint_f4(const float4* a, uint64_t pol) {
-  float4 v;
-  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(a), "l"(pol));
-  return v;
-}
 __device__ __forceinline__ float4 ld_stream_f4(const float4* a, uint64_t pol) {
   float4 v;
   asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
@@ -94,24 +82,6 @@ struct RowAcc {
 #pragma unroll
         for (int j = 0; j < VEC; ++j) r[k][j] = 0.f;
       }
-    }
-  }
-  // gathered row with an L2 priority hint (VEC == 4; plain __ldg otherwise)
-  __device__ __forceinline__ static void load_hint(const float* __restrict__ row, int d, float (&r)[K][VEC],
-                                                   uint64_t pol) {
-    if constexpr (VEC == 4) {
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        int c = lane_id() + 32 * k;
-        if (c * VEC < d) {
-          float4 x = ld_hint_f4(reinterpret_cast<const float4*>(row) + c, pol);
-          r[k][0] = x.x; r[k][1] = x.y; r[k][2] = x.z; r[k][3] = x.w;
-        } else {
-          r[k][0] = r[k][1] = r[k][2] = r[k][3] = 0.f;
-        }
-      }
-    } else {
-      load(row, d, r);
     }
   }
   // row -> this lane's chunks of a shared-memory stage, asynchronously (VEC == 4): keeps a

@@ -117,6 +117,7 @@ class RTECEngine:
     """B200 incremental engine over a DynamicGraph and an operator Bundle."""
 
     FUSED_DELTA = True
+    GAT_IMG_BUDGET = 8 << 30  # bytes of the GAT projection's tcgen05 A image (all n rows)
 
     def __init__(self, bundle: Bundle, graph: DynamicGraph, features, *, max_batch: int | None = None,
                  update: str = "tc", use_graphs: bool = True, bootstrap: bool = True,
@@ -152,8 +153,13 @@ class RTECEngine:
         self.Z, self.el, self.er, self.Zlog, self.erlog = [], [], [], [], []
         heads = bundle.heads
         no = self._rows_owned()  # rows of the destination-side state (all n unless sharded)
-        # tcgen05 3xTF32 update (gemm_tc.cu) for every dense update with d_out <= 256
-        self.tc = update == "tc" and bundle.model != GAT and max(dims[1:]) <= 256
+        # tcgen05 3xTF32 (gemm_tc.cu) for every dense contraction with d_out <= 256: the update
+        # GEMM, and GAT's projection Z = W h (K13; rows packed into an A image of n rows, kept
+        # under a memory budget -- beyond it the projection stays on the SIMT GEMM)
+        self.tc = update == "tc" and max(dims[1:]) <= 256
+        if self.tc and bundle.model == GAT:
+            img_bytes = (n + 127) // 128 * 128 * ((max(dims[:-1]) + 31) // 32 * 32) * 4
+            self.tc = img_bytes <= self.GAT_IMG_BUDGET
         # sum aggregators on the tcgen05 path: the update epilogue of layer l writes the source
         # deltas of layer l+1 (no DeltaLog, no per-source delta pass over V_chg(l))
         self.fused = (self.FUSED_DELTA and self.tc and bundle.model in (GCN, GRAPHSAGE, GIN)
@@ -182,8 +188,8 @@ class RTECEngine:
                 scalar = float(w.scalars["beta"])
             d_k = bundle.update_width(l)
             tcw = [None, None, None, None]
-            if self.tc:
-                tcw[0], tcw[1] = self._prep_weights(W, d_k, d_out)
+            if self.tc:  # GAT: the operand images of the projection W [d_out, d_in]
+                tcw[0], tcw[1] = self._prep_weights(W, d_in if bundle.model == GAT else d_k, d_out)
                 if W2 is not None:
                     tcw[2], tcw[3] = self._prep_weights(W2, d_out, d_out)
             self.wt.append((W, W2, att, *tcw, Wp, bp))
@@ -216,9 +222,12 @@ class RTECEngine:
                 for lst in (self.Z, self.el, self.er, self.Zlog, self.erlog):
                     lst.append(None)
         self.max_dim = max(max(dims), 1)
-        if self.tc:  # SW128 tile image: ceil(rows/128)*128 rows x ceil(d/32)*32 columns
+        pad = lambda d: (d + 31) // 32 * 32  # noqa: E731
+        if self.tc and bundle.model == GAT:  # projection A image over every row (bootstrap, replicas)
+            self.gemm_in = z((n + 127) // 128 * 128 * pad(max(dims[:-1])))
+            self.gemm_mid = None
+        elif self.tc:  # SW128 tile image: ceil(rows/128)*128 rows x ceil(d/32)*32 columns
             rows = (no + 127) // 128 * 128
-            pad = lambda d: (d + 31) // 32 * 32  # noqa: E731
             self.gemm_in = z(rows * pad(max(bundle.update_width(l) for l in range(self.L))))
             self.gemm_mid = z(rows * pad(max(dims[1:]))) if bundle.model in GIN_FAMILY else None
         else:
@@ -280,10 +289,15 @@ class RTECEngine:
         st = stream if stream is not None else _lib.stream_handle()
         if self.b.model == GAT:
             _lib.check(self.lib.rtec_gat_project(C.byref(self.layers[l]), p(H), p(rows), p(n_rows), self.n, p(Z),
-                                                 p(el), p(er), p(Zlog), p(erlog), p(err), st), "gat_project")
+                                                 p(el), p(er), p(Zlog), p(erlog), p(err), self._proj_img(), st),
+                       "gat_project")
         elif self.b.projected:
             _lib.check(self.lib.rtec_project(C.byref(self.layers[l]), p(H), p(rows), p(n_rows), self.n, p(Z),
                                              p(Zlog), p(err), st), "project")
+
+    def _proj_img(self):
+        """A-image scratch of the tcgen05 GAT projection (None: SIMT)."""
+        return _lib.ptr(self.gemm_in) if (self.tc and self.b.model == GAT) else None
 
     def refresh_projection(self, l: int) -> None:
         """Projections of every vertex of layer l from H^l (after a restore)."""

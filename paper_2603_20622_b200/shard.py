@@ -238,7 +238,7 @@ class ShardedRTECEngine(RTECEngine):
             if self.b.model == GAT:  # Z / el / er of every (replica) row feed the owned rows' softmax
                 _lib.check(self.lib.rtec_gat_project(C.byref(self.layers[l]), p(self.H[l]), None, None, self.n,
                                                      p(self.Z[l]), p(self.el[l]), p(self.er[l]), None, None, None,
-                                                     st), "bootstrap")
+                                                     self._proj_img(), st), "bootstrap")
             _lib.check(self.lib.rtec_layer_full(C.byref(g), C.byref(self.layers[l]), C.byref(s), p(self.owned),
                                                 p(self.n_owned), self.owned.numel(), p(err), p(self.g.ws),
                                                 self.g.ws.numel(), st), "bootstrap")
@@ -305,7 +305,7 @@ class ShardedRTECEngine(RTECEngine):
                 pf = self.fr[l - 1]
                 _lib.check(lib.rtec_gat_project(C.byref(self.layers[l]), p(self.H[l]), p(pf.chg_list), p(pf.n_chg),
                                                 self.n, p(self.Z[l]), p(self.el[l]), p(self.er[l]), p(self.Zlog[l]),
-                                                p(self.erlog[l]), p(bb.err), st), "gat_project")
+                                                p(self.erlog[l]), p(bb.err), self._proj_img(), st), "gat_project")
             s = self._state(l)
             s.delta = p(self._delta_buffer(l, int(self.fr[l].n_src.item())))  # |S(l)| δ rows
             _lib.check(lib.rtec_layer_incremental(C.byref(g), C.byref(b), C.byref(self.layers[l]), C.byref(s), prev,

@@ -23,7 +23,7 @@ from helpers import record, rowwise_rel, rowwise_rel_strict
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-4          # north star: fp32 engine vs the f64 reference, row-wise
-STRICT_TOL = 1e-3   # the same without the 1 % scale floor (rows that nearly cancel)
+STRICT_TOL = 1e-4   # the same without the 1 % scale floor: measured <= 5e-6 (profiles/r02_parity_report.jsonl)
 
 
 @pytest.fixture(scope="module")
