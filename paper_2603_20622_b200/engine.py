@@ -32,7 +32,7 @@ import torch
 from . import _lib
 from . import errors as E
 from .graph import DynamicGraph, EdgeUpdate, updates_to_arrays
-from .models import AGNN, COMMNET, GAT, GCN, GGCN, GIN, GIN_FAMILY, GRAPHSAGE, MONET, PINSAGE, Bundle, MODELS
+from .models import AGNN, COMMNET, GAT, GCN, GGCN, GIN, GIN_FAMILY, GIN_MAX, GRAPHSAGE, MONET, PINSAGE, Bundle, MODELS
 
 _MODEL_ID = _lib.MODEL_IDS
 
