@@ -154,11 +154,7 @@ typedef struct {
   int32_t d_out;       /* output width */
   int32_t heads;       /* GAT heads (1 for others) */
   float degree_offset; /* GCN: 1 if degree_smoothing else 0 (models.py:89) */
-  /* > 0: two-phase incremental sum aggregation for rows wider than 128 floats --
-   * first the δ rows of sources with out-degree >= hot_deg (an L2-sized band,
-   * reused by many destinations) into a partial row per destination, then the
-   * remaining sources.  0: one pass. */
-  int32_t hot_deg;
+  int32_t pad;
   const float* W;      /* [d_out, d_in] row-major (GAT: heads stacked [heads*dh, d_in]) */
   const float* W2;     /* GIN second matrix [d_out, d_out] (models.py:181) */
   const float* att;    /* GAT attention [heads, 2*dh] (dst half first, models.py:266-271) */

@@ -61,7 +61,7 @@ class Frontier(C.Structure):
 class Layer(C.Structure):
     _fields_ = [
         ("model", I32), ("d_in", I32), ("d_out", I32), ("heads", I32),
-        ("degree_offset", F32), ("hot_deg", I32), ("W", P), ("W2", P), ("att", P),
+        ("degree_offset", F32), ("pad", I32), ("W", P), ("W2", P), ("att", P),
         ("Wt_hi", P), ("Wt_lo", P), ("W2t_hi", P), ("W2t_lo", P), ("Wp", P), ("bp", P), ("scalar", F32),
         ("d_k", I32),
     ]

@@ -69,7 +69,6 @@ struct LayerArgs {
   int c0, cw;                   // feature slice [c0, c0 + cw) of the d_agg-wide rows (aggregation)
   int gcol, gk;                 // aggregate columns start at gcol of the gk-wide update input
   const float* self_in;         // H^l (st.H_in is redirected to the payload rows for PinSAGE / MoNet)
-  int phase;                    // incremental gathers: 0 all sources, 1 out_deg >= L.hot_deg only, 2 the rest
   int layer;
   uint64_t* err;
 };
@@ -136,15 +135,9 @@ constexpr int kChunk = 512;
 // 2 len / kChunk for len > kChunk, so the sum is at most 2 max_edges / kChunk
 __host__ __device__ constexpr int64_t heavy_chunk_bound(int64_t max_edges) { return 2 * max_edges / kChunk + 2; }
 
-// source u is gathered by this pass (two-phase: hot band first, then the rest)
-__device__ __forceinline__ bool phase_has(const LayerArgs& a, int32_t u) {
-  return a.phase == 0 || ((a.g.out_deg[u] >= a.L.hot_deg) == (a.phase == 1));
-}
-
 template <int VEC, int K, bool FULL>
-__device__ __forceinline__ int agg_edges(const LayerArgs& a, int64_t beg, int32_t e0, int32_t e1, int64_t p,
-                                         int64_t q, RowAcc<VEC, K>& acc) {
-  int hits = 0;
+__device__ __forceinline__ void agg_edges(const LayerArgs& a, int64_t beg, int32_t e0, int32_t e1, int64_t p,
+                                          int64_t q, RowAcc<VEC, K>& acc) {
   using R = RowAcc<VEC, K>;
   constexpr int UNR = (VEC * K <= 2) ? 8 : kUnroll;  // more rows in flight for thin slices
   const int d = a.d_agg, cw = a.cw;
@@ -161,11 +154,10 @@ __device__ __forceinline__ int agg_edges(const LayerArgs& a, int64_t beg, int32_
         hit = true;
         cu = src_coeff(a.L.model, a.g.out_deg[u], a.L.degree_offset);
       } else {
-        hit = bm_test(a.f.bm_src, u) && !in_range_has(a.b.i_src, p, q, u) && phase_has(a, u);
+        hit = bm_test(a.f.bm_src, u) && !in_range_has(a.b.i_src, p, q, u);
       }
     }
     unsigned m = __ballot_sync(0xffffffffu, hit);
-    hits += __popc(m);
     const float* base = (FULL ? a.st.H_in : a.delta) + a.c0;
     // gathered row: the source's own row (H_in, vertex-indexed δ) or its δ slot
     int32_t row = (!FULL && hit && a.st.delta_slot) ? a.f.src_slot[u] : u;
@@ -196,7 +188,6 @@ __device__ __forceinline__ int agg_edges(const LayerArgs& a, int64_t beg, int32_
       }
     }
   }
-  return hits;
 }
 
 // structural edges of v (graph.py:202-224 applied set): + c_new h_new for I, - c_old h_old for D
@@ -332,42 +323,8 @@ __device__ __forceinline__ void sum_partials(const float* part, int64_t stride, 
   }
 }
 
-// Two-phase incremental aggregation, phase 1 (L.hot_deg > 0, light destinations): the
-// ValueChange hits whose source has out-degree >= hot_deg -- a band of ~64 MB of δ rows
-// that every destination reuses -- summed into hp_part[i] while nothing else streams
-// through the L2; hp_flag[i] says whether the row holds anything.  Phase 2 (k_agg_light,
-// a.phase = 2) starts from it and adds the other sources.  Hub chunks stay one-phase.
-template <int VEC, int K>
-__global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_hot(LayerArgs a, AggRows rows, float* hp_part,
-                                                                          uint8_t* hp_flag) {
-  using R = RowAcc<VEC, K>;
-  if (err_set(a.err)) return;
-  const int64_t nr = rows.count();
-  if (*a.f.n_src == 0) return;
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp; i < nr; i += nw) {
-    const int32_t v = rows.at(i);
-    const int32_t len = a.g.in.len[v];
-    if (len > kChunk) continue;
-    const int2 rg = reinterpret_cast<const int2*>(a.b.irange)[v];
-    int64_t p = 0, q = 0;
-    if (rg.x >= 0) {
-      p = rg.x;
-      q = rg.x + rg.y;
-    }
-    R acc;
-    acc.zero();
-    const int h = agg_edges<VEC, K, false>(a, a.g.in.beg[v], 0, len, p, q, acc);
-    if (h) acc.store_stream(hp_part + i * a.d_agg + a.c0, a.cw, l2_evict_first_policy());
-    if (lane_id() == 0) hp_flag[i] = h ? 1 : 0;
-  }
-}
-
 template <int VEC, int K, bool FULL>
-__global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_light(LayerArgs a, AggRows rows,
-                                                                            const float* hp_part = nullptr,
-                                                                            const uint8_t* hp_flag = nullptr) {
+__global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_light(LayerArgs a, AggRows rows) {
   using R = RowAcc<VEC, K>;
   __shared__ __align__(16) float s_sv[kLBlk / 32][(!FULL && VEC == 4) ? 32 * VEC * K : 4];
   if (!FULL && err_set(a.err)) return;
@@ -406,7 +363,6 @@ __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_light(Laye
     }
     R acc;
     acc.zero();
-    if (!FULL && a.phase == 2 && hp_flag[i]) R::load(hp_part + i * a.d_agg + a.c0, a.cw, acc.v);  // hot band
     if (scan) agg_edges<VEC, K, FULL>(a, beg, 0, len, p, q, acc);
     if (!FULL) agg_struct<VEC, K>(a, p, q, acc);
     if constexpr (VEC == 4) {
@@ -758,38 +714,22 @@ static int launch_aggregation(LayerArgs& a, AggRows rows, int64_t max_rows, int6
     // side stream so each pass fills the other's tail (a fork / join the CUDA graph keeps).
     // Not while profiling (per-kernel events need the passes apart).
     cudaStream_t hs = g_prof_on ? s : side_stream();
-    // two-phase light pass (hot band first, L.hot_deg): wide rows on the one-destination pass only
-    const bool two = !FULL && !sliced && a.L.hot_deg > 0 && !agg_batched(a.cw);
-    float* hpart = nullptr;
-    uint8_t* hflag = nullptr;
-    if (two) {
-      hpart = w.alloc<float>(max_rows * static_cast<int64_t>(d));
-      hflag = w.alloc<uint8_t>(max_rows);
-      RTEC_WS_CHECK(w);
-      LayerArgs ah = a;
-      ah.phase = 1;
-      RTEC_PROF("k_agg_hot", s);
-      ok = RTEC_ROW_DISPATCH(a.cw, (k_agg_hot<VEC, K><<<grid, kLBlk, 0, s>>>(ah, rows, hpart, hflag)));
-    }
-    if (hs != s) {  // the hub chunks start after the hot-band pass (they would share its L2)
+    if (hs != s) {
       RTEC_CUDA(cudaEventRecord(side_fork(), s));
       RTEC_CUDA(cudaStreamWaitEvent(hs, side_fork(), 0));
     }
     {
       RTEC_PROF(FULL ? "k_agg_full_heavy" : "k_agg_inc_heavy", hs);
-      ok = ok && (sliced ? RTEC_SLICE_DISPATCH(a.cw, (k_agg_heavy<VEC, K, FULL><<<grid, kLBlk, 0, hs>>>(a, rows, hp)))
-                         : RTEC_ROW_DISPATCH(a.cw, (k_agg_heavy<VEC, K, FULL><<<grid, kLBlk, 0, hs>>>(a, rows, hp))));
+      ok = (sliced ? RTEC_SLICE_DISPATCH(a.cw, (k_agg_heavy<VEC, K, FULL><<<grid, kLBlk, 0, hs>>>(a, rows, hp)))
+                   : RTEC_ROW_DISPATCH(a.cw, (k_agg_heavy<VEC, K, FULL><<<grid, kLBlk, 0, hs>>>(a, rows, hp))));
     }
     {
       RTEC_PROF(FULL ? "k_agg_full_light" : "k_agg_inc", s);
-      LayerArgs al = a;
-      al.phase = two ? 2 : 0;
       if (!FULL && !sliced && agg_batched(a.cw))
         ok = ok && RTEC_ROW_DISPATCH(a.cw, (k_agg_batch<VEC, K><<<grid, kLBlk, 0, s>>>(a, rows)));
       else
-        ok = ok && (sliced ? RTEC_SLICE_DISPATCH(a.cw, (k_agg_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(al, rows)))
-                           : RTEC_ROW_DISPATCH(a.cw, (k_agg_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(
-                                                             al, rows, hpart, hflag))));
+        ok = ok && (sliced ? RTEC_SLICE_DISPATCH(a.cw, (k_agg_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows)))
+                           : RTEC_ROW_DISPATCH(a.cw, (k_agg_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows))));
     }
     if (hs != s) {
       RTEC_CUDA(cudaEventRecord(side_join(), hs));

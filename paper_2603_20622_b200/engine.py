@@ -22,7 +22,6 @@ device), so the whole step can be captured in a CUDA graph (`capture()`).
 from __future__ import annotations
 
 import ctypes as C
-import os
 import time
 from dataclasses import dataclass, field
 
@@ -235,35 +234,11 @@ class RTECEngine:
             self.gemm_in = z(no, max(bundle.update_width(l) for l in range(self.L))) if bundle.model != GAT else None
             self.gemm_mid = z(no, max(dims[1:])) if bundle.model in GIN_FAMILY else None
         self.fr = [_Frontier(n, self.dev) for _ in range(self.L)]
-        self.set_hot_band()
         self._ensure_ws(max_batch or graph.batch.cap)
         if bootstrap:  # (formats.load_checkpoint restores the state instead)
             self.bootstrap()
 
     # ---------------------------------------------------------------- plumbing
-    HOT_BAND_MB = float(os.environ.get("RTEC_HOT_MB", "0"))
-
-    def _out_degrees(self) -> torch.Tensor:
-        return self.g.out_deg[: self.n]
-
-    def set_hot_band(self, mb: float | None = None) -> None:
-        """Two-phase sum aggregation (rtec_layer_t.hot_deg) for layers whose aggregate is
-        wider than 128 floats: the δ rows of the highest out-degree sources, `mb` MB of
-        them, are summed in a first pass while they are L2-resident.  The out-degree
-        threshold comes from the current degree distribution; 0 MB turns it off."""
-        mb = self.HOT_BAND_MB if mb is None else float(mb)
-        deg = None
-        for l, lay in enumerate(self.layers):
-            d = int(self.b.agg_dims[l])
-            lay.hot_deg = 0
-            if mb <= 0 or d <= 128 or self.b.model in (GAT, GIN_MAX) or self.b.dest_dependent:
-                continue
-            if deg is None:
-                deg = torch.sort(self._out_degrees().to(torch.int32), descending=True).values
-            k = int(mb * (1 << 20)) // (4 * d)
-            if 0 < k < deg.numel():
-                lay.hot_deg = max(int(deg[k].item()) + 1, 2)
-
     def _rows_owned(self) -> int:
         """Rows of the destination-side state (S, ctx, final H, DeltaLog, GEMM input)."""
         return self.n

@@ -144,9 +144,6 @@ class ShardedRTECEngine(RTECEngine):
         g.out_deg, g.out_deg_prev = _lib.ptr(self.gout), _lib.ptr(self.gout_prev)
         return g
 
-    def _out_degrees(self) -> torch.Tensor:
-        return self.gout[: self.n]  # global out-degrees (the shard's are partial)
-
     def _rows_owned(self) -> int:
         # owner(v) = v mod P: rank r owns r, r + P, ...; its rows sit at v // P
         P, r = self.comm.world, self.comm.rank

@@ -495,29 +495,3 @@ def test_edge_case_batches(P, model):
         op, bs, bd = batches[2]
         eng2.step(op, bs, bd, np.arange(op.size, dtype=np.int64))
         assert not np.any(eng2.aggregates(0)[v])
-
-
-@pytest.mark.parametrize("update", ["tc", "simt"])
-def test_gat_projection_paths(P, update):
-    # K13: Z = W h of the 602-wide first layer and the 256-wide second layer on tcgen05 (rows
-    # packed into the SW128 A image) and on the SIMT fp32 GEMM, both against the oracle
-    eng, _, _ = _run_vs_oracle(P, "gat", [602, 256, 256], n=3000, m=60000, B=300, nb=2, seed=23, heads=4,
-                               update=update)
-    assert eng.tc == (update == "tc")
-    assert (eng.layers[0].Wt_hi is not None) == (update == "tc")
-
-
-@pytest.mark.parametrize("model", ["gcn", "graphsage", "gin"])
-def test_two_phase_hot_band(P, model):
-    # the hot-band-first incremental aggregation (rtec_layer_t.hot_deg) on 160-wide
-    # aggregates: a small band (0.25 MB -> ~400 sources) so both passes and the hub
-    # chunks all contribute; parity vs the oracle like the one-pass path
-    import paper_2603_20622_b200.engine as EM
-
-    old = EM.RTECEngine.HOT_BAND_MB
-    EM.RTECEngine.HOT_BAND_MB = 0.25
-    try:
-        eng, _, _ = _run_vs_oracle(P, model, [160, 160, 24], n=4000, m=80000, B=400, nb=3, seed=31)
-    finally:
-        EM.RTECEngine.HOT_BAND_MB = old
-    assert eng.layers[1].hot_deg > 1 and eng.layers[0].hot_deg > 1
