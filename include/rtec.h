@@ -139,7 +139,7 @@ typedef struct {
   int32_t* dst_slot;   /* [n] vertex -> index in dst_list (valid where bm_dst bit set) */
   int64_t* counters;   /* [8] |E_curr|, |V_dst|, |S|, |R|, Σ outdeg(new S), Σ indeg(V_dst), Σ indeg(R), reserved */
   /* Sharded runs: V_chg(l) over ALL ranks (union of every shard's V_dst(l),
-   * assembled by rtec_halo_unpack) and vertex -> row of the exchanged
+   * assembled by rtec_shard_unpack_changed) and vertex -> row of the exchanged
    * DeltaLog.  The next layer reads S(l+1) = S(l) ∪ bm_chg and old rows through
    * chg_slot.  NULL: bm_dst / dst_slot (unsharded). */
   uint32_t* bm_chg;
@@ -319,35 +319,90 @@ int rtec_update_gemm(const float* X, int64_t ldx, const float* W, int32_t d_in, 
 int rtec_gemm_prepare_weights(const float* W, int32_t d_in, int32_t d_out, float* Bhi, float* Blo,
                               rtec_stream_t stream);
 
-/* ---- vertex sharding (one process per GPU) ---- */
-/* Global degrees from the globally applied set of a batch: `gstatus` is the
- * per-update status after a MAX all-reduce over ranks (every update is owned
- * by exactly one rank).  Updates gout/gin (replicated [n] arrays), marks the
- * touched endpoints in bm_touch, writes dg_bm (global Dg: out-degree changed)
- * and the global DegreeDelta rows (graph.py:225-230, ascending vertex). */
-int rtec_shard_degrees(int64_t n, const int32_t* src, const int32_t* dst, const uint8_t* op,
-                       const uint8_t* gstatus, int64_t B, int32_t* gout, const int32_t* gout_prev,
-                       int32_t* gin, const int32_t* gin_prev, uint32_t* bm_touch, uint32_t* dg_bm,
-                       int32_t* d_vertex, int32_t* d_old_in, int32_t* d_new_in, int32_t* d_old_out,
-                       int32_t* d_new_out, int64_t* n_delta, void* ws, size_t ws_bytes, rtec_stream_t stream);
-/* Close the batch on the global degree arrays (prev catch-up, bitmaps cleared). */
-int rtec_shard_commit(const int32_t* src, const int32_t* dst, const uint8_t* gstatus, int64_t B,
-                      const int32_t* gout, int32_t* gout_prev, const int32_t* gin, int32_t* gin_prev,
-                      uint32_t* bm_touch, uint32_t* dg_bm, rtec_stream_t stream);
-/* Halo exchange of one layer's changed rows.  pack: rows H[list[i]] (i <
- * *n_list) -> send_rows[i], ids -> send_ids[i] (the collective itself is an
- * all-gather issued by the host over NCCL).  unpack: recv holds `world`
- * slots of `slot_cap` rows, counts[r] valid in slot r; for every received
- * (u, row) at global position k: bm_chg bit u, chg_slot[u] = k, and
- * glog[k] = pre-batch row (the replica's H[u] for remote u, which is then
- * overwritten; local_log[dst_slot[u]] for owned u).  glog == NULL: replica
- * refresh only (bootstrap).  *n_chg = Σ counts. */
-int rtec_halo_pack(const float* H, int32_t d, const int32_t* list, const int64_t* n_list, int64_t max_rows,
-                   int32_t* send_ids, float* send_rows, rtec_stream_t stream);
-int rtec_halo_unpack(const rtec_graph_t* g, int32_t d, const int32_t* recv_ids, const float* recv_rows,
-                     const int64_t* counts, int32_t world, int64_t slot_cap, float* H, const float* local_log,
-                     const int32_t* dst_slot, float* glog, uint32_t* bm_chg, int32_t* chg_slot, int32_t* chg_list,
-                     int64_t* n_chg, rtec_stream_t stream);
+/* ---- vertex sharding (one process per GPU) ----
+ * Rank p of P holds the edges whose dst it owns (owner(v) = v mod P) over LOCAL
+ * ids: [0, n_own) its owned vertices (local i <-> global p + P i), [n_own, n_loc)
+ * ghosts (sources with an out-edge into the shard).  The graph, frontier and
+ * layer calls above run unchanged on the local graph; the calls below keep the
+ * ghost rows coherent.  Replaces the paper's CPU-offloaded embedding store
+ * with destination-owned rows in HBM. */
+#define RTEC_SHARD_MAX_WORLD 32
+#define RTEC_SHARD_MAX_MATS 8
+typedef struct {
+  int32_t rank, world;
+  int64_t n;          /* global vertex count */
+  int64_t n_own;      /* owned vertices */
+  int64_t cap;        /* local id capacity (every per-vertex array of the shard) */
+  int32_t* g2l;       /* [n] global -> local id, -1: not on this rank */
+  int32_t* l2g;       /* [cap] local -> global id */
+  int64_t* n_loc;     /* [1] local ids in use (device) */
+  uint32_t* peers;    /* [n_own] bit q: rank q holds a ghost row of this owned vertex */
+  int32_t* gout;      /* [cap] global out-degree of every local vertex */
+  int32_t* gout_prev; /* [cap] its pre-batch value */
+} rtec_shard_t;
+
+/* Validation of a global batch without a graph (graph.py:192-198): range ->
+ * InvalidVertex, repeated (src, dst) -> ConfigError; first offender in batch
+ * order.  *err is reset first.  Identical on every rank. */
+int rtec_batch_validate(const int32_t* src, const int32_t* dst, int64_t B, int64_t n, uint64_t* err,
+                        void* ws, size_t ws_bytes, rtec_stream_t stream);
+/* Ghost admission for the inserts of a validated global batch (no-op when *err is
+ * set).  Receiver: every not-yet-local source of an insert into an owned
+ * destination gets the next local id (ascending global id; adm_list = their local
+ * ids, *n_adm; sh->n_loc advanced; bm_adm: an all-zero [n]-bit scratch, left
+ * zero).  Owner: every (owned source u, rank q) pair whose peers bit was clear is
+ * set and listed (send_u = local id of u, send_q, *n_send, peer_count[q]). */
+int rtec_shard_admit(const rtec_shard_t* sh, const int32_t* src, const int32_t* dst, const uint8_t* op,
+                     int64_t B, uint64_t* err, uint32_t* bm_adm, int32_t* adm_list, int64_t* n_adm,
+                     int32_t* send_u, int32_t* send_q, int64_t* n_send, int64_t* peer_count,
+                     void* ws, size_t ws_bytes, rtec_stream_t stream);
+/* The shard's part of a global batch in batch order, in local ids: updates whose
+ * dst this rank owns (l* arrays), lpos = their global position, *n_local. */
+int rtec_shard_localize(const rtec_shard_t* sh, const int32_t* src, const int32_t* dst, const uint8_t* op,
+                        const int64_t* ts, int64_t B, const uint64_t* err, int32_t* lsrc, int32_t* ldst,
+                        uint8_t* lop, int64_t* lts, int32_t* lpos, int64_t* n_local, void* ws, size_t ws_bytes,
+                        rtec_stream_t stream);
+/* Rows each peer receives from a list of owned local ids (list NULL: 0..max_list-1):
+ * peer_count[q] = #{i : peers[list[i]] has bit q}. */
+int rtec_shard_count_peers(const rtec_shard_t* sh, const int32_t* list, const int64_t* n_list, int64_t max_list,
+                           int64_t* peer_count, rtec_stream_t stream);
+/* Pack rows for an all-to-all: segment q starts at peer_off[q] (HOST array of
+ * world+1 offsets); each item writes its global id, optionally its global
+ * out-degree, and the concatenation of rows mats[j][v] (dims[j] floats; HOST
+ * arrays of nmat <= RTEC_SHARD_MAX_MATS device pointers / widths).  Items: list mode
+ * (every q in peers[v] of the listed owned v) or pair mode (pair_u / pair_q).
+ * cursor: [world] int64 scratch.  Order inside a segment is unspecified. */
+int rtec_shard_pack(const rtec_shard_t* sh, int32_t nmat, const float* const* mats, const int32_t* dims,
+                    const int64_t* peer_off, const int32_t* list, const int64_t* n_list, int64_t max_list,
+                    const int32_t* pair_u, const int32_t* pair_q, int64_t n_pairs, int64_t* cursor,
+                    int32_t* out_ids, int32_t* out_deg, float* out_rows, rtec_stream_t stream);
+/* k received (global id, rows) items into the ghost rows of mats[] (+ gout / gout_prev
+ * from degs when given); out_local[i] = local id (optional). */
+int rtec_shard_unpack_rows(const rtec_shard_t* sh, int32_t nmat, float* const* mats, const int32_t* dims,
+                           const int32_t* ids, const int32_t* degs, const float* rows, int64_t k,
+                           int32_t* out_local, rtec_stream_t stream);
+/* V_chg(l) of the shard after layer l: the k received changed rows overwrite their
+ * ghost rows of H (glog[p] = the overwritten pre-batch row, p < k), then the owned
+ * changed rows own_list[j] (glog[k + j] = own_log[own_slot[v]]); bm_chg (cleared
+ * first), chg_slot[v] = p, chg_list[p] = v, *n_chg = k + *n_own.  The next layer's
+ * frontier / retractions read them (rtec_frontier_t.bm_chg / chg_slot). */
+int rtec_shard_unpack_changed(const rtec_shard_t* sh, int32_t d, const int32_t* ids, const float* rows, int64_t k,
+                              float* H, const int32_t* own_list, const int64_t* n_own, int64_t max_own,
+                              const float* own_log, const int32_t* own_slot, float* glog, uint32_t* bm_chg,
+                              int32_t* chg_slot, int32_t* chg_list, int64_t* n_chg, rtec_stream_t stream);
+/* Global degrees from the globally applied set of a batch (gstatus = per-update
+ * status MAX-all-reduced over ranks): sh->gout of local sources, dg_bm (local ids
+ * whose global out-degree changed: the F1 Dg seed), bm_touch ([n_own] bits) and the
+ * DegreeDelta rows of the OWNED vertices (graph.py:225-230; global ids, ascending;
+ * in-degrees from the local graph, exact for owned vertices). */
+int rtec_shard_degrees(const rtec_shard_t* sh, const int32_t* src, const int32_t* dst, const uint8_t* op,
+                       const uint8_t* gstatus, int64_t B, const int32_t* in_deg, const int32_t* in_deg_prev,
+                       uint32_t* bm_touch, uint32_t* dg_bm, int32_t* d_vertex, int32_t* d_old_in,
+                       int32_t* d_new_in, int32_t* d_old_out, int32_t* d_new_out, int64_t* n_delta,
+                       void* ws, size_t ws_bytes, rtec_stream_t stream);
+/* Close the batch: gout_prev catches up, dg_bm / bm_touch cleared. */
+int rtec_shard_commit(const rtec_shard_t* sh, const int32_t* src, const int32_t* dst, const uint8_t* gstatus,
+                      int64_t B, uint32_t* dg_bm, uint32_t* bm_touch, rtec_stream_t stream);
 
 /* ---- NS baseline (SPEC.md:464 run_ns) ---- */
 /* Seeded sampling without replacement of min(len, fanout) in-neighbours (ascending) of
@@ -372,7 +427,7 @@ int rtec_query(const float* H, int64_t d, const int32_t* ids, int64_t k, float* 
 /* ---- diagnostics ---- */
 void rtec_prof_enable(int on);  /* bracket kernels with CUDA events (bench / profiling only) */
 size_t rtec_prof_report(char* buf, size_t len, int reset); /* "name count total_ms" lines */
-void rtec_struct_sizes(int64_t* out6); /* sizeof adj, graph, batch, frontier, layer, state */
+void rtec_struct_sizes(int64_t* out7); /* sizeof adj, graph, batch, frontier, layer, state, shard */
 const char* rtec_last_error(void);
 int64_t rtec_graph_kernel_nodes(void* graph); /* kernel nodes of a captured cudaGraph_t (launch census) */
 const char* rtec_version(void);

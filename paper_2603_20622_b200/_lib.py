@@ -76,6 +76,13 @@ class State(C.Structure):
     ]
 
 
+class Shard(C.Structure):
+    _fields_ = [
+        ("rank", I32), ("world", I32), ("n", I64), ("n_own", I64), ("cap", I64), ("g2l", P), ("l2g", P),
+        ("n_loc", P), ("peers", P), ("gout", P), ("gout_prev", P),
+    ]
+
+
 _SIGS = {
     "rtec_workspace_bytes": (SZ, [I64, I64, I64, I32]),
     "rtec_workspace_bytes_ext": (SZ, [I64, I64, I64, I32]),
@@ -89,10 +96,15 @@ _SIGS = {
     "rtec_batch_apply": (C.c_int, [C.POINTER(Graph), C.POINTER(Batch), P, P, P, P, I64, P, SZ, P]),
     "rtec_batch_apply_phase": (C.c_int, [C.POINTER(Graph), C.POINTER(Batch), P, P, P, P, I64, I32, P, SZ, P]),
     "rtec_batch_commit": (C.c_int, [C.POINTER(Graph), C.POINTER(Batch), P]),
-    "rtec_shard_degrees": (C.c_int, [I64, P, P, P, P, I64, P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
-    "rtec_shard_commit": (C.c_int, [P, P, P, I64, P, P, P, P, P, P, P]),
-    "rtec_halo_pack": (C.c_int, [P, I32, P, P, I64, P, P, P]),
-    "rtec_halo_unpack": (C.c_int, [C.POINTER(Graph), I32, P, P, P, I32, I64, P, P, P, P, P, P, P, P, P]),
+    "rtec_batch_validate": (C.c_int, [P, P, I64, I64, P, P, SZ, P]),
+    "rtec_shard_admit": (C.c_int, [C.POINTER(Shard), P, P, P, I64, P, P, P, P, P, P, P, P, P, SZ, P]),
+    "rtec_shard_localize": (C.c_int, [C.POINTER(Shard), P, P, P, P, I64, P, P, P, P, P, P, P, P, SZ, P]),
+    "rtec_shard_count_peers": (C.c_int, [C.POINTER(Shard), P, P, I64, P, P]),
+    "rtec_shard_pack": (C.c_int, [C.POINTER(Shard), I32, P, P, P, P, P, I64, P, P, I64, P, P, P, P, P]),
+    "rtec_shard_unpack_rows": (C.c_int, [C.POINTER(Shard), I32, P, P, P, P, P, I64, P, P]),
+    "rtec_shard_unpack_changed": (C.c_int, [C.POINTER(Shard), I32, P, P, I64, P, P, P, I64, P, P, P, P, P, P, P, P]),
+    "rtec_shard_degrees": (C.c_int, [C.POINTER(Shard), P, P, P, P, I64, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
+    "rtec_shard_commit": (C.c_int, [C.POINTER(Shard), P, P, P, I64, P, P, P]),
     "rtec_frontier_layer": (C.c_int, [C.POINTER(Graph), C.POINTER(Batch), I32, I32, C.POINTER(Frontier),
                                       C.POINTER(Frontier), P, SZ, P]),
     "rtec_layer_incremental": (C.c_int, [C.POINTER(Graph), C.POINTER(Batch), C.POINTER(Layer), C.POINTER(State),

@@ -52,13 +52,14 @@ size_t rtec_build_workspace_bytes(int64_t n, int64_t m) {
 }
 
 // sizeof of the ABI structs, for binding self-checks (ctypes / cgo / JNI mirrors)
-void rtec_struct_sizes(int64_t* out6) {
-  out6[0] = sizeof(rtec_adj_t);
-  out6[1] = sizeof(rtec_graph_t);
-  out6[2] = sizeof(rtec_batch_t);
-  out6[3] = sizeof(rtec_frontier_t);
-  out6[4] = sizeof(rtec_layer_t);
-  out6[5] = sizeof(rtec_state_t);
+void rtec_struct_sizes(int64_t* out7) {
+  out7[0] = sizeof(rtec_adj_t);
+  out7[1] = sizeof(rtec_graph_t);
+  out7[2] = sizeof(rtec_batch_t);
+  out7[3] = sizeof(rtec_frontier_t);
+  out7[4] = sizeof(rtec_layer_t);
+  out7[5] = sizeof(rtec_state_t);
+  out7[6] = sizeof(rtec_shard_t);
 }
 
 const char* rtec_last_error(void) { return last_error_cstr(); }

@@ -201,23 +201,26 @@ def _rank_dir(directory: str, rank: int) -> str:
 
 
 def save_sharded_checkpoint(engine, directory: str) -> None:
-    """Per-rank snapshot of a ShardedRTECEngine between batches (call on every rank)."""
+    """Per-rank snapshot of a ShardedRTECEngine between batches (call on every rank): the
+    shard's edges (global ids) and the OWNED rows of every layer; ghost rows are derived
+    (their owners refresh them on resume)."""
     r, P = engine.comm.rank, engine.comm.world
     d = _rank_dir(directory, r)
     os.makedirs(d, exist_ok=True)
-    src, dst, ts = engine.g.edges()  # this rank's shard: the edges whose destination it owns
+    src, dst, ts = engine.shard_edges()  # the edges whose destination this rank owns
     write_tensor(os.path.join(d, "edges.nrtf"), _edges_table(src, dst, ts))
-    for l in range(engine.L + 1):  # inputs are full replicas, the final layer per owned vertex
-        write_tensor(os.path.join(d, f"H{l}.nrtf"), engine.H[l].cpu().numpy())
+    no = engine.n_own
+    for l in range(engine.L + 1):
+        write_tensor(os.path.join(d, f"H{l}.nrtf"), engine.H[l][:no].cpu().numpy())
     for l in range(engine.L):
         write_tensor(os.path.join(d, f"S{l}.nrtf"), engine.S[l].cpu().numpy())
         if engine.ctx[l] is not None:
             write_tensor(os.path.join(d, f"ctx{l}.nrtf"), engine.ctx[l].cpu().numpy())
     b = engine.b
     save_weights(b, os.path.join(d, "weights.json"))
-    side = {"format": "rtec-b200-sharded-checkpoint", "version": 2, "model": b.model, "dims": list(b.dims),
-            "heads": int(b.heads), "degree_offset": float(b.degree_offset), "num_vertices": int(engine.n),
-            "world_size": int(P), "rank": int(r), "num_edges_shard": int(len(src))}
+    side = {"format": "rtec-b200-sharded-checkpoint", "version": 3, "model": b.model, "dims": list(b.dims),
+            "heads": int(b.heads), "degree_offset": float(b.degree_offset), "num_vertices": int(engine.n_glob),
+            "world_size": int(P), "rank": int(r), "num_edges_shard": int(len(src)), "owned_rows": int(no)}
     with open(os.path.join(d, "checkpoint.json"), "w", encoding="ascii") as fh:
         json.dump(side, fh, indent=1)
         fh.write("\n")
@@ -225,7 +228,8 @@ def save_sharded_checkpoint(engine, directory: str) -> None:
 
 def load_sharded_checkpoint(directory: str, comm, **engine_kw):
     """Rebuild this rank's ShardedRTECEngine from `save_sharded_checkpoint` (collective:
-    the constructor all-reduces the global degrees).  The world size must match."""
+    ghosts are announced to their owners, who refresh their rows and degrees).  The world
+    size must match."""
     import torch
 
     from .models import make_bundle
@@ -234,8 +238,8 @@ def load_sharded_checkpoint(directory: str, comm, **engine_kw):
     d = _rank_dir(directory, comm.rank)
     with open(os.path.join(d, "checkpoint.json"), "r", encoding="ascii") as fh:
         side = json.load(fh)
-    if side.get("format") != "rtec-b200-sharded-checkpoint":
-        raise E.ConfigError(f"{d}: not an rtec-b200 sharded checkpoint")
+    if side.get("format") != "rtec-b200-sharded-checkpoint" or int(side.get("version", 0)) < 3:
+        raise E.ConfigError(f"{d}: not an rtec-b200 sharded checkpoint (version 3)")
     if int(side["world_size"]) != comm.world or int(side["rank"]) != comm.rank:
         raise E.ConfigError(f"{d}: saved by rank {side['rank']} of {side['world_size']}, "
                             f"loading on rank {comm.rank} of {comm.world}")
@@ -244,13 +248,17 @@ def load_sharded_checkpoint(directory: str, comm, **engine_kw):
                          degree_smoothing=side["degree_offset"] != 0.0)
     e = _edges_from_table(read_tensor(os.path.join(d, "edges.nrtf")))
     X = read_tensor(os.path.join(d, "H0.nrtf"))
-    eng = ShardedRTECEngine(bundle, side["num_vertices"], e, X, comm, bootstrap=False,
+    eng = ShardedRTECEngine(bundle, side["num_vertices"], e, X, comm, bootstrap=False, shard_edges=True,
                             **engine_kw)
+    no = eng.n_own
     for l in range(1, eng.L + 1):
-        eng.H[l].copy_(torch.from_numpy(read_tensor(os.path.join(d, f"H{l}.nrtf"))))
+        eng.H[l][:no].copy_(torch.from_numpy(read_tensor(os.path.join(d, f"H{l}.nrtf"))))
     for l in range(eng.L):
         eng.S[l].copy_(torch.from_numpy(read_tensor(os.path.join(d, f"S{l}.nrtf"))))
         if eng.ctx[l] is not None:
             eng.ctx[l].copy_(torch.from_numpy(read_tensor(os.path.join(d, f"ctx{l}.nrtf"))))
-        eng.refresh_projection(l)  # GAT Z / el / er of every replica row from H^l
+    if eng.L > 1:
+        eng._refresh_ghosts(list(range(1, eng.L)))
+    for l in range(eng.L):
+        eng.refresh_projection(l)  # GAT Z / el / er of every local row from H^l
     return eng

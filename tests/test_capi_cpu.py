@@ -53,9 +53,9 @@ def test_pure_host_entry_points(lib):
 def test_struct_layouts_match_header(lib):
     from paper_2603_20622_b200 import _lib
 
-    sizes = (ctypes.c_int64 * 6)()
+    sizes = (ctypes.c_int64 * 7)()
     lib.rtec_struct_sizes(sizes)
-    mirror = [_lib.Adj, _lib.Graph, _lib.Batch, _lib.Frontier, _lib.Layer, _lib.State]
+    mirror = [_lib.Adj, _lib.Graph, _lib.Batch, _lib.Frontier, _lib.Layer, _lib.State, _lib.Shard]
     assert list(sizes) == [ctypes.sizeof(t) for t in mirror]
     assert ctypes.sizeof(_lib.Adj) == 8 * 7
     assert ctypes.sizeof(_lib.Graph) == 8 + 2 * 56 + 5 * 8 + 8 + 8  # + part_rank / part_count

@@ -48,18 +48,21 @@ def _comm_main(rank, world, port, td):
     c = Comm()
     assert c.staged and c.world == world and c.rank == rank
     ints = c.all_gather_ints([rank + 5, -1], torch.device("cpu"))
-    cap = 3
-    ids = torch.full((cap,), 100 + rank, dtype=torch.int32)
-    rows = torch.arange(cap * 4, dtype=torch.float32).reshape(cap, 4) + 1000 * rank
-    gi, gr = c.all_gather_rows(ids, rows)
+    # variable-length gather (DegreeDelta rows, frontier ids)
+    var = c.all_gather_var(torch.arange(3 + rank, dtype=torch.int32) + 10 * rank, 2 + rank)
+    # targeted exchange: rank r sends (r + 1) * (q + 1) rows of width 4 to rank q
+    sc = torch.tensor([(rank + 1) * (q + 1) for q in range(world)], dtype=torch.int64)
+    rc = c.all_to_all_counts(sc)
+    rows = torch.cat([torch.full(((rank + 1) * (q + 1), 4), 100.0 * rank + q) for q in range(world)])
+    got = c.all_to_all_rows(rows, sc.tolist(), rc.tolist())
     st = torch.tensor([rank, 1 - rank, 0], dtype=torch.uint8)
     c.all_reduce_(st, op=dist.ReduceOp.MAX)
     mine = (7 << 32) | 2 if rank == 0 else (3 << 32) | 8
     signed = mine - (1 << 64) if mine >= (1 << 63) else mine
     w = combine_err_words(c.all_gather_ints([signed], torch.device("cpu"))[:, 0])
     assert combine_err_words([-1, (5 << 32) | 1]) == (5 << 32) | 1  # all-ones (ok) never wins
-    np.savez(os.path.join(td, f"r{rank}.npz"), ints=ints, gi=gi.numpy(), gr=gr.numpy(), st=st.numpy(),
-             w=np.array([w], np.uint64))
+    np.savez(os.path.join(td, f"r{rank}.npz"), ints=ints, var=var.numpy(), rc=rc.numpy(), got=got.numpy(),
+             st=st.numpy(), w=np.array([w], np.uint64))
     dist.destroy_process_group()
 
 
@@ -68,8 +71,11 @@ def test_comm_collectives_gloo_world2():
     for r in (0, 1):
         z = out[f"r{r}.npz"]
         assert z["ints"].tolist() == [[5, -1], [6, -1]]
-        assert z["gi"].tolist() == [100] * 3 + [101] * 3
-        assert z["gr"].shape == (6, 4) and z["gr"][3, 0] == 1000.0 and z["gr"][2, 3] == 11.0
+        assert z["var"].tolist() == [0, 1, 10, 11, 12]
+        assert z["rc"].tolist() == [1 * (r + 1), 2 * (r + 1)]  # rank q sends (q + 1) * (r + 1) rows here
+        g = z["got"]
+        assert g.shape == ((r + 1) * 3, 4)
+        assert (g[: r + 1] == 100.0 * 0 + r).all() and (g[r + 1:] == 100.0 * 1 + r).all()
         assert z["st"].tolist() == [1, 1, 0]
         assert int(z["w"][0]) == (3 << 32) | 8  # smallest position wins across ranks
 

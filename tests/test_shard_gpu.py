@@ -51,17 +51,22 @@ def _rank_main(rank, world, port, cfg, out_dir):
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(0)
+    dev_i = rank if cfg.get("one_gpu_per_rank") else 0
+    torch.cuda.set_device(dev_i)
     backend = cfg.get("backend", "gloo")
-    kw = {"device_id": torch.device("cuda", 0)} if backend == "nccl" else {}
+    kw = {"device_id": torch.device("cuda", dev_i)} if backend == "nccl" else {}
     dist.init_process_group(backend, init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world, **kw)
     import paper_2603_20622_b200 as P
     from paper_2603_20622_b200.shard import Comm, ShardedRTECEngine
 
     (bs, bd, bt), X, batches = _workload(cfg)
     b = P.make_bundle(cfg["model"], cfg["dims"], heads=cfg.get("heads", 1))
-    eng = ShardedRTECEngine(b, cfg["n"], (bs, bd, bt), X, Comm(), max_batch=cfg["B"], reserve=cfg.get("reserve"))
+    eng = ShardedRTECEngine(b, cfg["n"], (bs, bd, bt), X, Comm(), max_batch=cfg["B"], reserve=cfg.get("reserve"),
+                            ghost_headroom=cfg.get("headroom", 0.25))
     res = {}
+    # the store is not replicated: layer-input rows = owned + ghosts (+ headroom), never all n
+    mem = eng.memory_bytes()
+    res["n_local0"] = np.array([mem["n_local"], mem["cap"], mem["n_own"]])
     L = len(cfg["dims"]) - 1
     for i, (op, s, d, t) in enumerate(batches):
         r = eng.step(op, s, d, t)
@@ -69,11 +74,14 @@ def _rank_main(rank, world, port, cfg, out_dir):
         for l in range(L):
             res[f"vdst{i}_{l}"] = eng.frontier(l)[0]
             res[f"ecurr{i}_{l}"] = np.array(r.metrics.e_curr[l])
+        res[f"sent{i}"] = np.array([x["rows_sent"] for x in eng.exchange_log[-1]] or [0])
+        res[f"adm{i}"] = np.array([eng.admitted])
         if cfg.get("ckpt") and i == 0:  # per-rank checkpoint, then resume without a bootstrap
             ck = os.path.join(out_dir, "ck")
             eng.save(ck)
             dist.barrier()
             eng = ShardedRTECEngine.load(ck, Comm(), max_batch=cfg["B"])
+    res["grown"] = np.array([getattr(eng, "grown", 0)])
     for l in range(L + 1):
         res[f"H{l}"] = eng.embeddings(l)
     ids = np.arange(0, cfg["n"], 7)
@@ -119,6 +127,7 @@ def _run(cfg, world=2):
         assert rowwise_rel(sh[f"H{l}"], oe.H[l]) <= 1e-4, l
     ids = np.arange(0, n, 7)
     assert np.array_equal(sh["query"], sh[f"H{L}"][ids])
+    return sh
 
 
 @pytest.mark.parametrize("model,dims", [("gcn", [32, 64, 32]), ("graphsage", [48, 64, 32]), ("gin", [32, 32, 32]),
@@ -134,6 +143,31 @@ def test_sharded_three_layers_arena_replay():
 
 def test_sharded_gat_heads_three_ranks():
     _run(dict(model="gat", dims=[24, 64, 64], n=2500, m=30000, B=250, nb=2, seed=23, heads=4), world=3)
+
+
+def test_sharded_store_has_no_replicas():
+    # rank 0's layer inputs hold its owned rows + ghosts, not all n vertices; rows are exchanged only
+    # to peers (fewer than V_dst x (P - 1)); inserts admit new ghosts
+    sh = _run(dict(model="graphsage", dims=[16, 32, 16], n=6000, m=9000, B=600, nb=3, seed=27), world=3)
+    n_local, cap, n_own = sh["n_local0"].tolist()
+    assert n_own == 2000 and n_local < 6000 and cap <= 6000
+    assert sum(int(sh[f"adm{i}"][0]) for i in range(3)) > 0
+
+
+def test_sharded_ghost_capacity_growth():
+    # zero headroom: the first batches' admissions need a larger local id space (rebuild, ids kept)
+    sh = _run(dict(model="gcn", dims=[16, 16, 16], n=20000, m=20000, B=1200, nb=3, seed=28, headroom=0.0))
+    assert int(sh["grown"][0]) >= 1
+
+
+def test_sharded_nccl_two_gpus():
+    # the multi-GPU path proper: one rank per GPU over NCCL (device all_to_all / all_gather)
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    _run(dict(model="gcn", dims=[32, 48, 32], n=3000, m=40000, B=300, nb=3, seed=29, backend="nccl",
+              one_gpu_per_rank=True), world=2)
 
 
 def test_sharded_nccl_single_rank():

@@ -1,10 +1,11 @@
-# compute-sanitizer memcheck / racecheck / synccheck over tools/sanitize_run.py (all models),
-# plus the two-phase hot band.  Logs -> gpurun_out/sanitize_*.log
+# compute-sanitizer memcheck / racecheck / synccheck over tools/sanitize_run.py (all ten models,
+# hub chunking, forced compaction), plus memcheck of the same run with the captured CUDA graph
+# (two-stream light / heavy passes).  Logs -> gpurun_out/sanitize_*.log, summary line per run.
 mkdir -p gpurun_out
 CS=/usr/local/cuda/bin/compute-sanitizer
 for tool in memcheck racecheck synccheck; do
   timeout 1500 $CS --tool $tool --error-exitcode 9 --print-limit 50 python tools/sanitize_run.py > gpurun_out/sanitize_$tool.log 2>&1
-  echo "$tool rc=$?" | tee -a gpurun_out/sanitize_summary.txt
-  RTEC_HOT_MB=1 timeout 900 $CS --tool $tool --error-exitcode 9 --print-limit 50 python tools/sanitize_run.py gcn graphsage > gpurun_out/sanitize_${tool}_hot.log 2>&1
-  echo "$tool hot-band rc=$?" | tee -a gpurun_out/sanitize_summary.txt
+  echo "$tool rc=$? $(grep -c ': ok' gpurun_out/sanitize_$tool.log) models ok; $(tail -1 gpurun_out/sanitize_$tool.log)" | tee -a gpurun_out/sanitize_summary.txt
 done
+RTEC_SAN_GRAPHS=1 timeout 1500 $CS --tool memcheck --error-exitcode 9 --print-limit 50 python tools/sanitize_run.py > gpurun_out/sanitize_memcheck_graphs.log 2>&1
+echo "memcheck (CUDA graphs) rc=$? $(grep -c ': ok' gpurun_out/sanitize_memcheck_graphs.log) models ok; $(tail -1 gpurun_out/sanitize_memcheck_graphs.log)" | tee -a gpurun_out/sanitize_summary.txt

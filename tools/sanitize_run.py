@@ -26,7 +26,8 @@ for model in models:
     dims = [64, 128, 64] if model != "gin" else [64, 128, 64, 64]
     g = P.DynamicGraph.from_edges(n, (bs, bd, bt), reserve=4096)
     X = features(n, dims[0], seed=1)
-    eng = P.RTECEngine(P.make_bundle(model, dims, heads=heads), g, X, use_graphs=False)
+    graphs = os.environ.get("RTEC_SAN_GRAPHS", "0") == "1"
+    eng = P.RTECEngine(P.make_bundle(model, dims, heads=heads), g, X, use_graphs=graphs)
     for k in range(3):
         op, s1, d1, t1 = stream.next_batch(600)
         r = eng.step(op, s1, d1, t1)
@@ -37,3 +38,4 @@ for model in models:
     H = eng.embeddings(len(dims) - 1)
     assert np.isfinite(H).all(), model
     print(f"{model}: ok, 4 batches, applied {int(r.status.sum())}", flush=True)
+print("sanitize_run: all models done", flush=True)
