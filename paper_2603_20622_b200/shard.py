@@ -368,13 +368,18 @@ class ShardedRTECEngine(RTECEngine):
         err = torch.full((1,), -1, dtype=torch.int64, device=self.dev)
         st = _lib.stream_handle()
         p = _lib.ptr
+        if getattr(self, "_own_ids", None) is None:
+            self._own_ids = torch.arange(max(self.n_own, 1), dtype=torch.int32, device=self.dev)
+            self._n_own_t = torch.tensor([self.n_own], dtype=torch.int64, device=self.dev)
         for l in range(self.L):
             g = self._mg()
             s = self._state(l)
             if self.b.model == GAT:  # Z / el / er of every local row feed the owned rows' softmax
                 self._project(l, self.H[l], None, None, self.Z[l], self.el[l], self.er[l])
-            _lib.check(self.lib.rtec_layer_full(C.byref(g), C.byref(self.layers[l]), C.byref(s), None, None,
-                                                self.n_own, p(err), p(self.g.ws), self.g.ws.numel(), st), "bootstrap")
+            # the owned rows only (local ids [0, n_own)): S / ctx / the final H hold n_own rows
+            _lib.check(self.lib.rtec_layer_full(C.byref(g), C.byref(self.layers[l]), C.byref(s), p(self._own_ids),
+                                                p(self._n_own_t), self.n_own, p(err), p(self.g.ws), self.g.ws.numel(),
+                                                st), "bootstrap")
             if l + 1 < self.L:
                 self._refresh_ghosts([l + 1])
         if sync:
