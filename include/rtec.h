@@ -381,14 +381,21 @@ int rtec_shard_pack(const rtec_shard_t* sh, int32_t nmat, const float* const* ma
 int rtec_shard_unpack_rows(const rtec_shard_t* sh, int32_t nmat, float* const* mats, const int32_t* dims,
                            const int32_t* ids, const int32_t* degs, const float* rows, int64_t k,
                            int32_t* out_local, rtec_stream_t stream);
-/* V_chg(l) of the shard after layer l: the k received changed rows overwrite their
- * ghost rows of H (glog[p] = the overwritten pre-batch row, p < k), then the owned
- * changed rows own_list[j] (glog[k + j] = own_log[own_slot[v]]); bm_chg (cleared
- * first), chg_slot[v] = p, chg_list[p] = v, *n_chg = k + *n_own.  The next layer's
- * frontier / retractions read them (rtec_frontier_t.bm_chg / chg_slot). */
+/* V_chg(l) of the shard after layer l, over one or more exchange rounds (clear != 0 on
+ * the first: bm_chg zeroed).  The k received changed rows of a round overwrite their
+ * ghost rows of H at positions pos_base + [0, k); the owned changed rows own_list[j]
+ * (given on the last round) follow; bm_chg, chg_slot[v] = pos, chg_list[pos] = v,
+ * *n_chg = total (last round).  Exactly one of
+ *   glog:  glog[pos] = the overwritten pre-batch row (owned: own_log[own_slot[v]]) --
+ *          the exchanged DeltaLog the next layer retracts with;
+ *   delta: delta[v] = c_new h_new - c_old h_old for received rows (c: GCN
+ *          1/sqrt(deg + deg_off) if coeff_gcn else 1, 0 for deg 0; global out-degrees),
+ *          the source deltas the update epilogue writes for owned rows.
+ * The next layer's frontier / retractions read them (rtec_frontier_t.bm_chg / chg_slot). */
 int rtec_shard_unpack_changed(const rtec_shard_t* sh, int32_t d, const int32_t* ids, const float* rows, int64_t k,
-                              float* H, const int32_t* own_list, const int64_t* n_own, int64_t max_own,
-                              const float* own_log, const int32_t* own_slot, float* glog, uint32_t* bm_chg,
+                              int64_t pos_base, int32_t clear, float* H, const int32_t* own_list,
+                              const int64_t* n_own, int64_t max_own, const float* own_log, const int32_t* own_slot,
+                              float* glog, float* delta, int32_t coeff_gcn, float deg_off, uint32_t* bm_chg,
                               int32_t* chg_slot, int32_t* chg_list, int64_t* n_chg, rtec_stream_t stream);
 /* Global degrees from the globally applied set of a batch (gstatus = per-update
  * status MAX-all-reduced over ranks): sh->gout of local sources, dg_bm (local ids

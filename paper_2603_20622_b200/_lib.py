@@ -102,7 +102,8 @@ _SIGS = {
     "rtec_shard_count_peers": (C.c_int, [C.POINTER(Shard), P, P, I64, P, P]),
     "rtec_shard_pack": (C.c_int, [C.POINTER(Shard), I32, P, P, P, P, P, I64, P, P, I64, P, P, P, P, P]),
     "rtec_shard_unpack_rows": (C.c_int, [C.POINTER(Shard), I32, P, P, P, P, P, I64, P, P]),
-    "rtec_shard_unpack_changed": (C.c_int, [C.POINTER(Shard), I32, P, P, I64, P, P, P, I64, P, P, P, P, P, P, P, P]),
+    "rtec_shard_unpack_changed": (C.c_int, [C.POINTER(Shard), I32, P, P, I64, I64, I32, P, P, P, I64, P, P, P, P,
+                                            I32, F32, P, P, P, P, P]),
     "rtec_shard_degrees": (C.c_int, [C.POINTER(Shard), P, P, P, P, I64, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
     "rtec_shard_commit": (C.c_int, [C.POINTER(Shard), P, P, P, I64, P, P, P]),
     "rtec_frontier_layer": (C.c_int, [C.POINTER(Graph), C.POINTER(Batch), I32, I32, C.POINTER(Frontier),

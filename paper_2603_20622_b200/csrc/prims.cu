@@ -97,28 +97,6 @@ cudaEvent_t side_join() {
   return e;
 }
 
-// ---------------------------------------------------------------- scan
-__global__ void __launch_bounds__(kScanBlock) k_scan_blocks(int64_t* bs, int64_t nb, int64_t* total) {
-  __shared__ int64_t sw[kScanBlock / 32];
-  __shared__ int64_t carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int64_t base = 0; base < nb; base += kScanBlock) {
-    int64_t i = base + threadIdx.x;
-    int64_t v = i < nb ? bs[i] : 0;
-    int64_t tot;
-    int64_t ex = block_exclusive_scan<int64_t>(v, sw, &tot);
-    if (i < nb) bs[i] = ex + carry;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += tot;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    bs[nb] = carry;
-    if (total) *total = carry;
-  }
-}
-
 // ---------------------------------------------------------------- small sort
 // One CTA of 1024 threads, bitonic over (key, val) lexicographic; N <= 2048.
 constexpr int kSmallSort = 2048;

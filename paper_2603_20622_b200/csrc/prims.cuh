@@ -54,50 +54,6 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T* smem_warp, T* total) {
 constexpr int64_t kScanSmall = 262144;
 inline int scan_items_for(int64_t max_n) { return max_n <= kScanSmall ? 1 : kScanItems; }
 
-template <typename F, int ITEMS = kScanItems>
-__global__ void __launch_bounds__(kScanBlock) k_scan_reduce(F f, Count cnt, int64_t* block_sums) {
-  __shared__ int64_t sw[kScanBlock / 32];
-  int64_t n = cnt.get();
-  int64_t base = static_cast<int64_t>(blockIdx.x) * kScanBlock * ITEMS;
-  int64_t s = 0;
-  if (base < n) {
-#pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-      int64_t i = base + static_cast<int64_t>(threadIdx.x) * ITEMS + k;
-      if (i < n) s += f(i);
-    }
-  }
-  int64_t tot;
-  block_exclusive_scan<int64_t>(s, sw, &tot);
-  if (threadIdx.x == 0) block_sums[blockIdx.x] = tot;
-}
-
-// single CTA: exclusive scan of block_sums in place; total -> *total
-__global__ void __launch_bounds__(kScanBlock) k_scan_blocks(int64_t* block_sums, int64_t nb, int64_t* total);
-
-template <typename F, typename O, int ITEMS = kScanItems>
-__global__ void __launch_bounds__(kScanBlock) k_scan_down(F f, Count cnt, const int64_t* block_sums, O out) {
-  __shared__ int64_t sw[kScanBlock / 32];
-  int64_t n = cnt.get();
-  int64_t base = static_cast<int64_t>(blockIdx.x) * kScanBlock * ITEMS;
-  if (base >= n) return;
-  int64_t vals[ITEMS];
-  int64_t s = 0;
-#pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {
-    int64_t i = base + static_cast<int64_t>(threadIdx.x) * ITEMS + k;
-    vals[k] = (i < n) ? f(i) : 0;
-    s += vals[k];
-  }
-  int64_t off = block_exclusive_scan<int64_t>(s, sw, nullptr) + block_sums[blockIdx.x];
-#pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {
-    int64_t i = base + static_cast<int64_t>(threadIdx.x) * ITEMS + k;
-    if (i < n) out(i, off, vals[k]);
-    off += vals[k];
-  }
-}
-
 inline int64_t scan_blocks_for(int64_t max_n) {
   const int64_t tile = static_cast<int64_t>(kScanBlock) * scan_items_for(max_n);
   return (max_n + tile - 1) / tile;
@@ -127,8 +83,70 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_one(F f, Count cnt, O out, 
   if (threadIdx.x == 0 && total) *total = tot;
 }
 
+// Single-pass scan with decoupled look-back: tiles are claimed in launch order from a
+// counter (so every tile's predecessors are running or done), each tile publishes its
+// aggregate, then walks back over its predecessors' published words until it meets an
+// inclusive prefix.  Word = flag (bits 62-63: 1 aggregate, 2 inclusive prefix) | value.
+// One kernel per scan instead of reduce + block-scan + down-sweep (the per-batch pipeline
+// runs ~40 scans, most of them latency-bound).
+constexpr unsigned long long kLbAgg = 1ull << 62, kLbPrefix = 2ull << 62, kLbMask = (1ull << 62) - 1;
+
+template <typename F, typename O, int ITEMS>
+__global__ void __launch_bounds__(kScanBlock) k_scan_1pass(F f, Count cnt, O out, int64_t* total,
+                                                           unsigned long long* st, unsigned int* tile_ctr) {
+  __shared__ int64_t sw[kScanBlock / 32];
+  __shared__ int64_t s_prefix;
+  __shared__ unsigned int s_tile;
+  const int64_t n = cnt.get();
+  constexpr int64_t kT = static_cast<int64_t>(kScanBlock) * ITEMS;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t ntiles = (n + kT - 1) / kT;
+  if (tile >= (ntiles > 0 ? ntiles : 1)) return;  // tile 0 runs for n == 0 (writes the total)
+  const int64_t base = tile * kT;
+  int64_t vals[ITEMS];
+  int64_t s = 0;
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const int64_t i = base + static_cast<int64_t>(threadIdx.x) * ITEMS + k;
+    vals[k] = (i < n) ? f(i) : 0;
+    s += vals[k];
+  }
+  int64_t tot;
+  int64_t off = block_exclusive_scan<int64_t>(s, sw, &tot);
+  if (threadIdx.x == 0) {
+    volatile unsigned long long* vst = st;
+    int64_t excl = 0;
+    if (tile == 0) {
+      atomicExch(st, kLbPrefix | static_cast<unsigned long long>(tot));
+    } else {
+      atomicExch(st + tile, kLbAgg | static_cast<unsigned long long>(tot));
+      for (int64_t j = tile - 1;;) {
+        const unsigned long long w = vst[j];
+        if (w == 0) continue;  // predecessor still scanning its tile
+        excl += static_cast<int64_t>(w & kLbMask);
+        if (w & kLbPrefix) break;
+        --j;
+      }
+      __threadfence();
+      atomicExch(st + tile, kLbPrefix | static_cast<unsigned long long>(excl + tot));
+    }
+    s_prefix = excl;
+    if (total && tile == (ntiles > 0 ? ntiles - 1 : 0)) *total = excl + tot;
+  }
+  __syncthreads();
+  off += s_prefix;
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const int64_t i = base + static_cast<int64_t>(threadIdx.x) * ITEMS + k;
+    if (i < n) out(i, off, vals[k]);
+    off += vals[k];
+  }
+}
+
 // Exclusive scan: out(i, prefix, value) is called for every i < count; *total
-// (device, may be null) receives the sum.  ws needs scan_blocks_for(max)+1 int64.
+// (device, may be null) receives the sum.  ws needs scan_blocks_for(max)+2 int64.
 template <typename F, typename O>
 int exclusive_scan_bs(F f, Count cnt, int64_t max_n, O out, int64_t* total, int64_t* bs, cudaStream_t s) {
   if (max_n <= kScanTile) {
@@ -136,16 +154,14 @@ int exclusive_scan_bs(F f, Count cnt, int64_t max_n, O out, int64_t* total, int6
     RTEC_LAUNCH_CHECK("exclusive_scan");
     return RTEC_OK;
   }
-  int64_t nb = scan_blocks_for(max_n);
-  if (scan_items_for(max_n) == 1) {
-    k_scan_reduce<F, 1><<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(f, cnt, bs);
-    k_scan_blocks<<<1, kScanBlock, 0, s>>>(bs, nb, total);
-    k_scan_down<F, O, 1><<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(f, cnt, bs, out);
-  } else {
-    k_scan_reduce<F><<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(f, cnt, bs);
-    k_scan_blocks<<<1, kScanBlock, 0, s>>>(bs, nb, total);
-    k_scan_down<F, O><<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(f, cnt, bs, out);
-  }
+  const int64_t nb = scan_blocks_for(max_n);
+  unsigned long long* st = reinterpret_cast<unsigned long long*>(bs);
+  unsigned int* ctr = reinterpret_cast<unsigned int*>(bs + nb);
+  RTEC_CUDA(cudaMemsetAsync(bs, 0, sizeof(int64_t) * (nb + 1), s));
+  if (scan_items_for(max_n) == 1)
+    k_scan_1pass<F, O, 1><<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(f, cnt, out, total, st, ctr);
+  else
+    k_scan_1pass<F, O, kScanItems><<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(f, cnt, out, total, st, ctr);
   RTEC_LAUNCH_CHECK("exclusive_scan");
   return RTEC_OK;
 }

@@ -237,46 +237,73 @@ __global__ void __launch_bounds__(kSBlk) k_unpack_rows(rtec_shard_t sh, PackSrc 
   }
 }
 
-// V_chg(l) of the shard: received ghost rows (positions [0, k)) then the owned changed
-// rows (positions k + j); glog[pos] = the pre-batch row the next layer retracts
+// V_chg(l) of the shard, assembled over one or more exchange rounds: the received ghost
+// rows of a round take positions pos_base + [0, k), the owned changed rows (own_list, last
+// round) the positions after them.  Per received row either
+//   glog mode:  glog[pos] = the overwritten pre-batch ghost row (the next layer retracts with it)
+//   delta mode: delta[u] = c_new h_new - c_old h_old, c from the global out-degrees (GCN
+//               1/sqrt(deg + off), else 1; 0 without out-edges) -- the next layer's source delta,
+//               as the update epilogue writes it for owned rows (no DeltaLog at all)
+struct ChgOut {
+  float* glog;
+  float* delta;
+  int32_t coeff_gcn;
+  float deg_off;
+};
+
+__device__ __forceinline__ float shard_coeff(const ChgOut& o, int32_t deg) {
+  return deg > 0 ? (o.coeff_gcn ? 1.0f / sqrtf(static_cast<float>(deg) + o.deg_off) : 1.f) : 0.f;
+}
+
 template <bool V4>
 __global__ void __launch_bounds__(kSBlk) k_unpack_changed(rtec_shard_t sh, int32_t d, const int32_t* __restrict__ ids,
-                                                          const float* __restrict__ rows, int64_t k, float* H,
-                                                          const int32_t* __restrict__ own_list, const int64_t* n_own,
-                                                          const float* __restrict__ own_log,
-                                                          const int32_t* __restrict__ own_slot, float* glog,
+                                                          const float* __restrict__ rows, int64_t k, int64_t pos_base,
+                                                          float* H, const int32_t* __restrict__ own_list,
+                                                          const int64_t* n_own, const float* __restrict__ own_log,
+                                                          const int32_t* __restrict__ own_slot, ChgOut o,
                                                           uint32_t* bm_chg, int32_t* chg_slot, int32_t* chg_list,
                                                           int64_t* n_chg) {
-  const int64_t no = *n_own;
+  const int64_t no = own_list ? *n_own : 0;
   const int64_t total = k + no;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *n_chg = total;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && own_list) *n_chg = pos_base + total;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t p = warp; p < total; p += nw) {
     const bool recv = p < k;
     const int32_t u = recv ? sh.g2l[ids[p]] : own_list[p - k];
     if (u < 0) continue;
+    const int64_t pos = pos_base + p;
     if (lane_id() == 0) {
       atomicOr(bm_chg + (u >> 5), 1u << (u & 31));
-      chg_slot[u] = static_cast<int32_t>(p);
-      chg_list[p] = u;
+      chg_slot[u] = static_cast<int32_t>(pos);
+      chg_list[pos] = u;
     }
-    float* lrow = glog + p * d;
     float* hrow = H + static_cast<int64_t>(u) * d;
     if (recv) {
       const float* nrow = rows + p * d;
-      if (V4) {
+      if (o.delta) {
+        const float cn = shard_coeff(o, sh.gout[u]), co = shard_coeff(o, sh.gout_prev[u]);
+        float* drow = o.delta + static_cast<int64_t>(u) * d;
+        for (int c = lane_id(); c < d; c += 32) {
+          const float nv = __ldg(nrow + c), ov = hrow[c];
+          drow[c] = cn * nv - co * ov;
+          hrow[c] = nv;
+        }
+      } else if (V4) {
+        float* lrow = o.glog + pos * d;
         for (int c = lane_id(); c < d / 4; c += 32) {
           reinterpret_cast<float4*>(lrow)[c] = reinterpret_cast<const float4*>(hrow)[c];
           reinterpret_cast<float4*>(hrow)[c] = __ldg(reinterpret_cast<const float4*>(nrow) + c);
         }
       } else {
+        float* lrow = o.glog + pos * d;
         for (int c = lane_id(); c < d; c += 32) {
           lrow[c] = hrow[c];
           hrow[c] = __ldg(nrow + c);
         }
       }
-    } else {
+    } else if (!o.delta) {  // owned: the local DeltaLog row (delta mode: the epilogue wrote δ)
+      float* lrow = o.glog + pos * d;
       const float* orow = own_log + static_cast<int64_t>(own_slot[u]) * d;
       if (V4) {
         for (int c = lane_id(); c < d / 4; c += 32)
@@ -508,20 +535,32 @@ int rtec_shard_unpack_rows(const rtec_shard_t* sh, int32_t nmat, float* const* m
 }
 
 int rtec_shard_unpack_changed(const rtec_shard_t* sh, int32_t d, const int32_t* ids, const float* rows, int64_t k,
-                              float* H, const int32_t* own_list, const int64_t* n_own, int64_t max_own,
-                              const float* own_log, const int32_t* own_slot, float* glog, uint32_t* bm_chg,
-                              int32_t* chg_slot, int32_t* chg_list, int64_t* n_chg, rtec_stream_t stream) {
+                              int64_t pos_base, int32_t clear, float* H, const int32_t* own_list, const int64_t* n_own,
+                              int64_t max_own, const float* own_log, const int32_t* own_slot, float* glog,
+                              float* delta, int32_t coeff_gcn, float deg_off, uint32_t* bm_chg, int32_t* chg_slot,
+                              int32_t* chg_list, int64_t* n_chg, rtec_stream_t stream) {
   RTEC_TRY(shard_ok(sh));
+  if (!glog == !delta) {
+    set_error("shard_unpack_changed: exactly one of glog / delta");
+    return RTEC_CONFIG_ERROR;
+  }
+  if (own_list && glog && (!own_log || !own_slot)) {
+    set_error("shard_unpack_changed: glog mode needs the owned DeltaLog rows");
+    return RTEC_CONFIG_ERROR;
+  }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   RTEC_PROF("shard_unpack", s);
-  RTEC_CUDA(cudaMemsetAsync(bm_chg, 0, sizeof(uint32_t) * ((sh->cap + 31) / 32), s));
-  const int grid = grid_for((k + max_own) * 32, kSBlk, kSMs * 8);
+  if (clear) RTEC_CUDA(cudaMemsetAsync(bm_chg, 0, sizeof(uint32_t) * ((sh->cap + 31) / 32), s));
+  const int64_t work = k + (own_list ? max_own : 0);
+  if (work <= 0 && !own_list) return RTEC_OK;
+  const int grid = grid_for((work > 0 ? work : 1) * 32, kSBlk, kSMs * 8);
+  const ChgOut o{glog, delta, coeff_gcn, deg_off};
   if (d % 4 == 0)
-    k_unpack_changed<true><<<grid, kSBlk, 0, s>>>(*sh, d, ids, rows, k, H, own_list, n_own, own_log, own_slot, glog,
-                                                  bm_chg, chg_slot, chg_list, n_chg);
+    k_unpack_changed<true><<<grid, kSBlk, 0, s>>>(*sh, d, ids, rows, k, pos_base, H, own_list, n_own, own_log, own_slot,
+                                                  o, bm_chg, chg_slot, chg_list, n_chg);
   else
-    k_unpack_changed<false><<<grid, kSBlk, 0, s>>>(*sh, d, ids, rows, k, H, own_list, n_own, own_log, own_slot, glog,
-                                                   bm_chg, chg_slot, chg_list, n_chg);
+    k_unpack_changed<false><<<grid, kSBlk, 0, s>>>(*sh, d, ids, rows, k, pos_base, H, own_list, n_own, own_log,
+                                                   own_slot, o, bm_chg, chg_slot, chg_list, n_chg);
   RTEC_LAUNCH_CHECK("k_unpack_changed");
   return RTEC_OK;
 }

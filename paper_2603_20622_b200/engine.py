@@ -164,7 +164,12 @@ class RTECEngine:
         # deltas of layer l+1 (no DeltaLog, no per-source delta pass over V_chg(l))
         self.fused = (self.FUSED_DELTA and self.tc and bundle.model in (GCN, GRAPHSAGE, GIN)
                       and all(d % 4 == 0 for d in dims[1:-1]))
-        self.delta = [z(n, bundle.agg_dims[l]) if self.fused else None for l in range(bundle.num_layers)]
+        # one vertex-indexed δ buffer shared by all layers: layer l's rows are dead once its
+        # aggregation has run, before the update epilogue writes layer l+1's (stream order)
+        self.delta = [None] * bundle.num_layers
+        if self.fused:
+            dbuf = z(n * max(bundle.agg_dims))
+            self.delta = [dbuf[: n * d].view(n, d) for d in bundle.agg_dims]
         for l, w in enumerate(bundle.layers):
             d_in, d_out = w.in_dim, w.out_dim
             dev32 = lambda a: torch.as_tensor(np.ascontiguousarray(a, np.float32), device=self.dev)  # noqa: E731

@@ -46,7 +46,9 @@ from . import _lib
 from . import errors as E
 from .engine import Metrics, RTECEngine, RunResult, _Frontier
 from .graph import DynamicGraph
-from .models import GAT, PROJECTED
+from .models import GAT, GCN, GIN, GRAPHSAGE, PROJECTED
+
+SUM_MODELS = (GCN, GRAPHSAGE, GIN)
 
 _U64 = (1 << 64) - 1
 MAX_WORLD = 32  # RTEC_SHARD_MAX_WORLD: peers masks are 32-bit
@@ -146,7 +148,9 @@ class ShardedRTECEngine(RTECEngine):
     """RTECEngine over this rank's shard of the graph; same step() /
     query() / embeddings() API, collective over the ranks of `comm`."""
 
-    FUSED_DELTA = False  # remotely changed ghosts arrive as rows; δ is rebuilt from the exchanged DeltaLog
+    # sum aggregators: the update epilogue writes δ of the owned changed rows and the exchange
+    # writes δ of the received ghost rows (no DeltaLog); GAT / GIN-max keep an exchanged DeltaLog
+    FUSED_DELTA = True
 
     def __init__(self, bundle, num_vertices: int, edges, features, comm: Comm, *, max_batch: int | None = None,
                  update: str = "tc", reserve: int | None = None, device=None, exchange_chunk: int = 1 << 20,
@@ -250,8 +254,10 @@ class ShardedRTECEngine(RTECEngine):
         return self.n_own
 
     def _ensure_ws(self, B):
-        need = int(self.lib.rtec_workspace_bytes(self.n, max(int(B), 1), max(self.g.out.slots, self.g.inn.slots),
-                                                 self.max_dim))
+        # the [n, d] δ region only when δ is not kept in self.delta (non-fused sum aggregators)
+        ws_fn = (self.lib.rtec_workspace_bytes if (not getattr(self, "fused", False) and self.b.model in SUM_MODELS)
+                 else self.lib.rtec_workspace_bytes_ext)
+        need = int(ws_fn(self.n, max(int(B), 1), max(self.g.out.slots, self.g.inn.slots), self.max_dim))
         # batch validation / ghost admission scan over the global id space
         need = max(need, int(self.lib.rtec_build_workspace_bytes(self.n_glob, max(int(B), 1))))
         if self.g.ws.numel() < need:
@@ -549,7 +555,7 @@ class ShardedRTECEngine(RTECEngine):
                 _lib.check(lib.rtec_gat_project(C.byref(self.layers[l]), p(self.H[l]), p(pf.chg_list), p(pf.n_chg),
                                                 self.n, p(self.Z[l]), p(self.el[l]), p(self.er[l]), p(self.Zlog[l]),
                                                 p(self.erlog[l]), p(bb.err), self._proj_img(), st), "gat_project")
-            s = self._state(l)
+            s = self._state(l, incremental=True)
             _lib.check(lib.rtec_layer_incremental(C.byref(g), C.byref(b), C.byref(self.layers[l]), C.byref(s), prev,
                                                   C.byref(fc[l]), p(bb.err), ws, wsb, st), "layer")
             if l + 1 < self.L:
@@ -573,28 +579,45 @@ class ShardedRTECEngine(RTECEngine):
 
     def _exchange_layer(self, l: int) -> None:
         """Targeted exchange of layer l's changed owned rows (H^{l+1}) to the ranks holding
-        ghosts of them; assembles V_chg(l) and the exchanged DeltaLog for layer l+1."""
+        ghosts of them, in rounds of at most `exchange_chunk` listed rows per rank (bounded
+        send / receive buffers); assembles V_chg(l) and, for the next layer, either the
+        received rows' source deltas (fused sum aggregators) or the exchanged DeltaLog."""
         lib, st, p = self.lib, _lib.stream_handle(), _lib.ptr
         f = self._chg_buffers(l)
-        pc = torch.zeros(self.comm.world, dtype=torch.int64, device=self.dev)
-        _lib.check(lib.rtec_shard_count_peers(C.byref(self._shard()), p(f.dst_list), p(f.n_dst), self.n_own, p(pc),
-                                              st), "count_peers")
-        sc, rc, ex = self._send_recv(pc, [f.n_dst])
-        n_dst = int(ex[0])
         H = self.H[l + 1]
         d = int(H.shape[1])
-        ids, _, rows = self._exchange_rows([H.data_ptr()], [d], sc, rc, list_=f.dst_list, n_list=f.n_dst,
-                                           max_list=n_dst)
-        k = int(np.sum(rc))
-        need = max(k + n_dst, 1) * d
-        if self.glog[l].numel() < need:
-            self.glog[l] = torch.zeros(int(need * 1.25), dtype=torch.float32, device=self.dev)
-        _lib.check(lib.rtec_shard_unpack_changed(C.byref(self._shard()), d, p(ids), p(rows), k, p(H), p(f.dst_list),
-                                                 p(f.n_dst), n_dst, p(self.log[l]), p(f.dst_slot), p(self.glog[l]),
-                                                 p(f.bm_chg), p(f.chg_slot), p(f.chg_list), p(f.n_chg), st),
-                   "shard_unpack")
-        sent = int(np.sum(sc))
-        self.exchange_log[-1].append({"layer": l, "rows_sent": sent, "rows_recv": k, "bytes_sent": sent * (4 * d + 4)})
+        fused = self.fused
+        pc = torch.zeros(self.comm.world, dtype=torch.int64, device=self.dev)
+        n_dst = int(f.n_dst.item())
+        rounds = int(self.comm.all_gather_ints([n_dst], self.dev)[:, 0].max(initial=0))
+        step = max(1, self.exchange_chunk)
+        rounds = max((rounds + step - 1) // step, 1)
+        sent = recv = 0
+        for rd in range(rounds):
+            c0 = min(rd * step, n_dst)
+            cnt = max(min(step, n_dst - c0), 0)
+            lst = f.dst_list[c0:c0 + cnt] if cnt else f.dst_list[:1]
+            _lib.check(lib.rtec_shard_count_peers(C.byref(self._shard()), p(lst), None, cnt, p(pc), st), "count_peers")
+            sc, rc, _ = self._send_recv(pc)
+            ids, _, rows = self._exchange_rows([H.data_ptr()], [d], sc, rc, list_=lst, max_list=cnt)
+            k = int(np.sum(rc))
+            last = rd == rounds - 1
+            if not fused:
+                need = max(recv + k + (n_dst if last else 0), 1) * d
+                if self.glog[l].numel() < need:  # grow, keeping the rows of earlier rounds
+                    g2 = torch.zeros(int(need * 1.25), dtype=torch.float32, device=self.dev)
+                    g2[: self.glog[l].numel()] = self.glog[l]
+                    self.glog[l] = g2
+            _lib.check(lib.rtec_shard_unpack_changed(
+                C.byref(self._shard()), d, p(ids), p(rows), k, recv, 1 if rd == 0 else 0, p(H),
+                p(f.dst_list) if last else None, p(f.n_dst), n_dst, p(self.log[l]), p(f.dst_slot),
+                None if fused else p(self.glog[l]), p(self.delta[l + 1]) if fused else None,
+                1 if self.b.model == GCN else 0, float(self.b.degree_offset), p(f.bm_chg), p(f.chg_slot),
+                p(f.chg_list), p(f.n_chg), st), "shard_unpack")
+            sent += int(np.sum(sc))
+            recv += k
+        self.exchange_log[-1].append({"layer": l, "rounds": rounds, "rows_sent": sent, "rows_recv": recv,
+                                      "bytes_sent": sent * (4 * d + 4)})
 
     # ---------------------------------------------------------------- reads
     def _owned_popcount(self, bm: torch.Tensor) -> int:
@@ -667,6 +690,8 @@ class ShardedRTECEngine(RTECEngine):
                 "layer_inputs": nb(self.H[: self.L]),
                 "owned_state": nb([self.H[self.L]] + self.S + self.ctx + self.log),
                 "gat_caches": nb(self.Z + self.el + self.er + self.Zlog + self.erlog),
+                "source_deltas": self.delta[0].untyped_storage().nbytes() if self.fused else 0,
+                "exchanged_log": nb(self.glog),
                 "graph": nb([gr.out.nbr, gr.out.ts, gr.inn.nbr, gr.out.beg, gr.inn.beg, gr.out.len, gr.inn.len,
                              gr.out.cap, gr.inn.cap]),
                 "maps": nb([self.g2l, self.l2g, self.peers, self.gout, self.gout_prev]),

@@ -9,8 +9,8 @@ CPU oracle and compares:
 
 - per-update status and DegreeDelta rows: bit-exact;
 - V_dst(l) assembled over the shards and |E_curr(l)| summed: bit-exact;
-- embeddings H^l assembled from the owners: within 1e-6 (row-wise) of the
-  unsharded engine and within 1e-4 of the oracle.
+- embeddings H^l assembled from the owners: within 1e-5 (row-wise; local-id
+  summation order) of the unsharded engine and within 1e-4 of the oracle.
 """
 
 import os
@@ -62,7 +62,7 @@ def _rank_main(rank, world, port, cfg, out_dir):
     (bs, bd, bt), X, batches = _workload(cfg)
     b = P.make_bundle(cfg["model"], cfg["dims"], heads=cfg.get("heads", 1))
     eng = ShardedRTECEngine(b, cfg["n"], (bs, bd, bt), X, Comm(), max_batch=cfg["B"], reserve=cfg.get("reserve"),
-                            ghost_headroom=cfg.get("headroom", 0.25))
+                            ghost_headroom=cfg.get("headroom", 0.25), exchange_chunk=cfg.get("chunk", 1 << 20))
     res = {}
     # the store is not replicated: layer-input rows = owned + ghosts (+ headroom), never all n
     mem = eng.memory_bytes()
@@ -123,7 +123,9 @@ def _run(cfg, world=2):
             assert np.array_equal(sh[f"vdst{i}_{l}"], o["frontier"][l]["vdst"]), (i, l)
             assert int(sh[f"ecurr{i}_{l}"]) == o["frontier"][l]["n_ecurr"], (i, l)
     for l in range(1, L + 1):
-        assert rowwise_rel(sh[f"H{l}"], eng.embeddings(l)) <= 1e-6, l
+        # shards sum each in-run in LOCAL source-id order (owned ids, then ghosts): fp32
+        # reassociation only, well inside the 1e-4 parity bound below
+        assert rowwise_rel(sh[f"H{l}"], eng.embeddings(l)) <= 1e-5, l
         assert rowwise_rel(sh[f"H{l}"], oe.H[l]) <= 1e-4, l
     ids = np.arange(0, n, 7)
     assert np.array_equal(sh["query"], sh[f"H{L}"][ids])
@@ -142,7 +144,13 @@ def test_sharded_three_layers_arena_replay():
 
 
 def test_sharded_gat_heads_three_ranks():
-    _run(dict(model="gat", dims=[24, 64, 64], n=2500, m=30000, B=250, nb=2, seed=23, heads=4), world=3)
+    # exchanged DeltaLog (GAT), several exchange rounds per layer
+    _run(dict(model="gat", dims=[24, 64, 64], n=2500, m=30000, B=250, nb=2, seed=23, heads=4, chunk=97), world=3)
+
+
+def test_sharded_fused_deltas_chunked_exchange():
+    # fused source deltas written on receipt (GCN coefficients), exchange in rounds of 64 rows
+    _run(dict(model="gcn", dims=[32, 64, 32], n=3000, m=40000, B=300, nb=3, seed=30, chunk=64), world=2)
 
 
 def test_sharded_store_has_no_replicas():
