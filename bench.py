@@ -238,7 +238,8 @@ def bench_config(args, wl: dict, world: int) -> dict:
     return {"workload": args.workload, "desc": wl["desc"], "vertices": wl["n"], "edges": wl["m"],
             "model": wl["model"], "dims": wl["dims"], "batch_updates": wl["batch"],
             "batch_fraction": round(wl["batch"] / wl["m"], 6),
-            "parallelism": f"vertex-sharded x{world} (owner = v mod {world}, halo all-gather per layer)"
+            "parallelism": f"vertex-sharded x{world} (owner = v mod {world}, owned + ghost rows, targeted "
+                           "all-to-all of changed rows per layer)"
             if sharded else "single GPU",
             "l2": "flushed between timed steps (256 MiB write)"}
 
@@ -320,8 +321,8 @@ def run_ours(args, world, rank, local):
         B = run_step(W + k)
         evs[k][1].record()
         total_updates += B
-        errs[k : k + 1].copy_(g.batch.err)
-        napp[k : k + 1].copy_(g.batch.n_applied)
+        errs[k : k + 1].copy_(eng.g.batch.err)  # (eng.g: a sharded engine may rebuild its shard graph)
+        napp[k : k + 1].copy_(eng.g.batch.n_applied)
     torch.cuda.synchronize()
     barrier(world)
     wall = time.time() - wall0
@@ -334,8 +335,8 @@ def run_ours(args, world, rank, local):
     for k in range(PROF):
         flush.zero_()
         bsz.append(run_step(W + K + k))
-        errs[K + k : K + k + 1].copy_(g.batch.err)
-        actr[k].copy_(g.batch.apply_ctr)
+        errs[K + k : K + k + 1].copy_(eng.g.batch.err)
+        actr[k].copy_(eng.g.batch.apply_ctr)
         for l in range(L):
             ctrs[k, l].copy_(eng.fr[l].counters)
     torch.cuda.synchronize()
@@ -487,8 +488,23 @@ def run_ours(args, world, rank, local):
     res["gpu_launches"] = (nodes if nodes and nodes > 0 else launches_per_step(prof, PROF)) * K
     res["cuda_graph"] = bool(graphs_on and nodes)
     res["graph_captures"] = len(getattr(eng, "_graphs", {}))
-    res["compactions"] = int(getattr(g, "compactions", 0))
-    return res, g, eng
+    res["compactions"] = int(getattr(eng.g, "compactions", 0))
+    if sharded:  # per-rank exchange volume of the timed batches and the replica-free store
+        import torch.distributed as dist
+
+        xl = eng.exchange_log[W:W + K]
+        mine = {"rank": rank, "exchange_rows_per_batch": sum(x["rows_sent"] for b in xl for x in b) / max(K, 1),
+                "exchange_bytes_per_batch": sum(x["bytes_sent"] for b in xl for x in b) / max(K, 1),
+                "exchange_rounds_per_batch": sum(x["rounds"] for b in xl for x in b) / max(K, 1),
+                "admitted_ghosts_last_batch": int(eng.admitted)}
+        mem = eng.memory_bytes()
+        mine.update({k: v for k, v in mem.items() if k in ("n_own", "n_local", "cap")})
+        mine["hbm_gb"] = round(sum(v for k, v in mem.items() if k not in ("n_own", "n_local", "cap")) / 1e9, 3)
+        allr = [None] * world
+        dist.all_gather_object(allr, mine)
+        res["shard"] = {"nranks": world, "backend": eng.comm.backend, "collective": "all_to_all_single",
+                        "per_rank": allr}
+    return res, eng.g, eng
 
 
 def launches_per_step(prof, K):

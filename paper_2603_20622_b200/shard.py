@@ -154,7 +154,7 @@ class ShardedRTECEngine(RTECEngine):
 
     def __init__(self, bundle, num_vertices: int, edges, features, comm: Comm, *, max_batch: int | None = None,
                  update: str = "tc", reserve: int | None = None, device=None, exchange_chunk: int = 1 << 20,
-                 bootstrap: bool = True, shard_edges: bool = False, ghost_headroom: float = 0.25):
+                 bootstrap: bool = True, shard_edges: bool = False, ghost_headroom: float = 0.10):
         """edges: (src, dst[, ts]) global edge list (every rank passes the same), or with
         shard_edges=True only this rank's edges (owner(dst) == rank; checkpoint resume).
         features: [n, d0] global, or [n_own, d0] owned rows in owner order."""
