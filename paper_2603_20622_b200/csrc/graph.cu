@@ -8,6 +8,8 @@
 // the reference.
 #include "prims.cuh"
 
+#include <stdlib.h>
+
 namespace rtec {
 
 constexpr int kBlk = 256;
@@ -525,6 +527,139 @@ __global__ void __launch_bounds__(kBlk) k_merge_items(MergeIn in, MergePlan p, r
   }
 }
 
+// Warp-per-chunk merge (default): a warp takes kWC consecutive work positions, finds its
+// first group once, and walks the groups of its range with their metadata in registers.
+// For a group of at most 32 updates the updates sit one per lane, and each old element's
+// rank among them (inserts / deletes before it, deleted or not) comes from a shuffle sweep
+// over the lanes instead of a per-element binary search in global memory; larger groups
+// fall back to the binary search.  Output positions and order are those of k_merge_items.
+constexpr int kWC = 512;
+
+__device__ __forceinline__ void merge_put(const MergePlan& p, const rtec_adj_t& a, int64_t g, int32_t f0, int64_t out,
+                                          int32_t w, int64_t tsv, bool inpl, int64_t dest, int64_t so0) {
+  if (inpl) {
+    const int64_t so = so0 + out - f0;
+    p.scr_nbr[so] = w;
+    if (p.scr_ts) p.scr_ts[so] = tsv;
+  } else {
+    a.nbr[dest + out] = w;
+    if (a.ts) a.ts[dest + out] = tsv;
+  }
+}
+
+__global__ void __launch_bounds__(kBlk) k_merge_items_warp(MergeIn in, MergePlan p, rtec_adj_t a,
+                                                           const uint64_t* err) {
+  if (err_set(err)) return;
+  const int64_t G = *p.G;
+  if (G == 0) return;
+  const int64_t W = p.work_off[G];
+  const int lane = lane_id();
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t0 = warp * kWC; t0 < W; t0 += nw * kWC) {
+    const int64_t t1 = t0 + kWC < W ? t0 + kWC : W;
+    int64_t g = 0;
+    if (lane == 0) g = upper_bound_dev<int64_t>(p.work_off, 0, G, t0) - 1;
+    g = __shfl_sync(0xffffffffu, g, 0);
+    for (; g < G; ++g) {
+      const int64_t wo = p.work_off[g], we = p.work_off[g + 1];
+      if (wo >= t1) break;
+      const int32_t v = p.gv[g];
+      const int64_t s = p.gstart[g], e = p.gstart[g + 1];
+      const int64_t b = a.beg[v];
+      const int32_t L = a.len[v];
+      const int32_t f0 = p.first[g];
+      const bool inpl = p.inplace[g] != 0;
+      const int64_t dest = inpl ? 0 : p.dest[g];
+      const int64_t so0 = inpl ? p.scr_off[g] : 0;
+      const int64_t pre_s = p.pre_ins[s];
+      const int64_t nu = e - s;
+      const bool small = nu <= 32;
+      // small groups: update j on lane j (neighbour, op)
+      int32_t un = 0x7fffffff;
+      int ui = 0;
+      if (small && lane < nu) {
+        un = in.nbr[s + lane];
+        ui = in.op[s + lane] == RTEC_OP_INSERT ? 1 : 0;
+      }
+      const int64_t lo = t0 > wo ? t0 : wo, hi = t1 < we ? t1 : we;
+      const int64_t nold = L - f0;  // work positions [0, nold) are old elements, then the updates
+      for (int64_t i0 = lo; i0 < hi; i0 += 32) {
+        const int64_t i = i0 + lane;
+        const bool act = i < hi;
+        const int64_t t = i - wo;
+        const bool old = act && t < nold;
+        int32_t w = 0;
+        if (old) w = a.nbr[b + f0 + t];
+        int64_t ib = 0, db = 0;
+        bool deleted = false;
+        if (small) {
+          // rank of w among the group's updates: every lane sweeps all of them (old lanes only)
+          const unsigned om = __ballot_sync(0xffffffffu, old);
+          if (om) {
+            for (int j = 0; j < static_cast<int>(nu); ++j) {
+              const int32_t uj = __shfl_sync(0xffffffffu, un, j);
+              const int ij = __shfl_sync(0xffffffffu, ui, j);
+              if (uj < w) {
+                ib += ij;
+                db += 1 - ij;
+              } else if (uj == w) {
+                deleted = true;  // an applied insert never hits an existing key
+              }
+            }
+          }
+        } else if (old) {
+          const int64_t q = lower_bound_dev(in.nbr, s, e, w);
+          deleted = q < e && in.nbr[q] == w;
+          ib = p.pre_ins[q] - pre_s;
+          db = (q - s) - ib;
+        }
+        if (old) {
+          if (!deleted)
+            merge_put(p, a, g, f0, f0 + t - db + ib, w, a.ts ? a.ts[b + f0 + t] : 0, inpl, dest, so0);
+        } else if (act) {
+          const int64_t k = s + (t - nold);
+          if (in.op[k] == RTEC_OP_INSERT) {
+            const int32_t wk = in.nbr[k];
+            const int64_t pos = lower_bound_dev(a.nbr, b, b + L, wk) - b;
+            const int64_t ibk = p.pre_ins[k] - pre_s;
+            const int64_t dbk = (k - s) - ibk;
+            merge_put(p, a, g, f0, pos - dbk + ibk, wk, in.ts ? in.ts[k] : 0, inpl, dest, so0);
+          }
+        }
+      }
+    }
+  }
+}
+
+// copy in-place runs back from scratch, a warp per kWC scratch positions walking its groups
+__global__ void __launch_bounds__(kBlk) k_merge_copyback_warp(MergePlan p, rtec_adj_t a, const uint64_t* err) {
+  if (err_set(err)) return;
+  const int64_t G = *p.G;
+  if (G == 0) return;
+  const int64_t S = p.scr_off[G];
+  const int lane = lane_id();
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t0 = warp * kWC; t0 < S; t0 += nw * kWC) {
+    const int64_t t1 = t0 + kWC < S ? t0 + kWC : S;
+    int64_t g = 0;
+    if (lane == 0) g = upper_bound_dev<int64_t>(p.scr_off, 0, G, t0) - 1;
+    g = __shfl_sync(0xffffffffu, g, 0);
+    for (; g < G; ++g) {
+      const int64_t so = p.scr_off[g], se = p.scr_off[g + 1];
+      if (so >= t1) break;
+      if (se == so) continue;
+      const int64_t base = a.beg[p.gv[g]] + p.first[g] - so;
+      const int64_t lo = t0 > so ? t0 : so, hi = t1 < se ? t1 : se;
+      for (int64_t i = lo + lane; i < hi; i += 32) {
+        a.nbr[base + i] = p.scr_nbr[i];
+        if (a.ts) a.ts[base + i] = p.scr_ts[i];
+      }
+    }
+  }
+}
+
 // copy in-place runs back from scratch (after all reads of the old runs)
 __global__ void __launch_bounds__(kBlk) k_merge_copyback(MergePlan p, rtec_adj_t a, const uint64_t* err) {
   __shared__ int64_t s_off[kMT];
@@ -604,11 +739,26 @@ static int merge_plan(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, floa
   return RTEC_OK;
 }
 
+// RTEC_MERGE_WARP env: 1 (default) warp-per-chunk merge kernels, 0 element-parallel (A/B)
+static bool merge_warp() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("RTEC_MERGE_WARP");
+    m = e ? atoi(e) : 1;
+  }
+  return m != 0;
+}
+
 static int merge_exec(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, int64_t work_bound, uint64_t* err,
                       cudaStream_t s) {
   RTEC_PROF("adj_merge", s);
-  k_merge_items<<<grid_for(work_bound, kMT, kSMs * 8), kBlk, 0, s>>>(in, p, a, err);
-  k_merge_copyback<<<grid_for(work_bound, kMT, kSMs * 8), kBlk, 0, s>>>(p, a, err);
+  if (merge_warp()) {
+    k_merge_items_warp<<<grid_for(work_bound, kWC * (kBlk / 32), kSMs * 8), kBlk, 0, s>>>(in, p, a, err);
+    k_merge_copyback_warp<<<grid_for(work_bound, kWC * (kBlk / 32), kSMs * 8), kBlk, 0, s>>>(p, a, err);
+  } else {
+    k_merge_items<<<grid_for(work_bound, kMT, kSMs * 8), kBlk, 0, s>>>(in, p, a, err);
+    k_merge_copyback<<<grid_for(work_bound, kMT, kSMs * 8), kBlk, 0, s>>>(p, a, err);
+  }
   k_merge_commit<<<grid_for(in.maxK, kBlk), kBlk, 0, s>>>(p, a, err);
   k_commit_reserve<<<1, 32, 0, s>>>(p, a, err);
   RTEC_LAUNCH_CHECK("merge_exec");
@@ -653,38 +803,52 @@ __global__ void k_apply_degrees(const int32_t* __restrict__ as, const int32_t* _
                                               static_cast<unsigned long long>(local));
 }
 
-__global__ void k_touched_keys(const int32_t* __restrict__ as, const int32_t* __restrict__ ad, const int64_t* cnt,
-                               uint64_t* keys, uint32_t* vals, int64_t* cnt2) {
-  int64_t K = *cnt;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *cnt2 = 2 * K;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x) {
-    keys[2 * i] = static_cast<uint64_t>(as[i]);
-    keys[2 * i + 1] = static_cast<uint64_t>(ad[i]);
-    vals[2 * i] = 0;
-    vals[2 * i + 1] = 0;
+// endpoints of the applied updates -> bits of a touched-vertex bitmap
+__global__ void k_touched_bits(const int32_t* __restrict__ as, const int32_t* __restrict__ ad, const int64_t* cnt,
+                               uint32_t* bm) {
+  const int64_t K = *cnt;
+  for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~int64_t(31); i0 < K;
+       i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + lane_id();
+    const bool act = i < K;
+    bm_set_warp(bm, act ? as[i] : 0, act);
+    bm_set_warp(bm, act ? ad[i] : 0, act);
   }
 }
 
-struct DeltaFlag {
-  const uint64_t* sk;
+// touched vertices whose (in, out) degree changed -> DegreeDelta rows, ascending
+// (graph.py:225-230): one bitmap word per scan item
+struct TouchedWord {
+  const uint32_t* bm;
   const int32_t* in_deg; const int32_t* out_deg; const int32_t* in_prev; const int32_t* out_prev;
-  __device__ __forceinline__ int64_t operator()(int64_t i) const {
-    if (i > 0 && sk[i] == sk[i - 1]) return 0;
-    int32_t v = static_cast<int32_t>(sk[i]);
-    return (in_deg[v] != in_prev[v] || out_deg[v] != out_prev[v]) ? 1 : 0;
+  __device__ __forceinline__ uint32_t changed(int64_t w) const {
+    uint32_t t = bm[w], c = 0;
+    while (t) {
+      const int b = __ffs(t) - 1;
+      t &= t - 1;
+      const int64_t v = w * 32 + b;
+      if (in_deg[v] != in_prev[v] || out_deg[v] != out_prev[v]) c |= 1u << b;
+    }
+    return c;
   }
+  __device__ __forceinline__ int64_t operator()(int64_t w) const { return __popc(changed(w)); }
 };
-struct DeltaOut {
-  DeltaFlag f;
+struct TouchedRows {
+  TouchedWord f;
   int32_t* dv; int32_t* doi; int32_t* dni; int32_t* doo; int32_t* dno;
-  __device__ __forceinline__ void operator()(int64_t i, int64_t off, int64_t v) const {
-    if (!v) return;
-    int32_t x = static_cast<int32_t>(f.sk[i]);
-    dv[off] = x;
-    doi[off] = f.in_prev[x];
-    dni[off] = f.in_deg[x];
-    doo[off] = f.out_prev[x];
-    dno[off] = f.out_deg[x];
+  __device__ __forceinline__ void operator()(int64_t w, int64_t off, int64_t) const {
+    uint32_t c = f.changed(w);
+    while (c) {
+      const int b = __ffs(c) - 1;
+      c &= c - 1;
+      const int32_t x = static_cast<int32_t>(w * 32 + b);
+      dv[off] = x;
+      doi[off] = f.in_prev[x];
+      dni[off] = f.in_deg[x];
+      doo[off] = f.out_prev[x];
+      dno[off] = f.out_deg[x];
+      ++off;
+    }
   }
 };
 
@@ -719,6 +883,8 @@ size_t batch_ws_bytes(int64_t n, int64_t B, int64_t scr_cap) {
   }
   add(sort_ws_bytes(B2));
   add(sizeof(int64_t) * (scan_blocks_for(B2) + 2) * 12);
+  add(sizeof(uint32_t) * ((n + 31) / 32));  // touched-vertex bitmap (DegreeDelta rows)
+  add(sizeof(int64_t) * (scan_blocks_for((n + 31) / 32) + 2));
   return b + (1 << 16);
 }
 
@@ -850,11 +1016,11 @@ int rtec_batch_apply_phase(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src,
   uint64_t* sk = w.alloc<uint64_t>(B2);
   uint32_t* sv = w.alloc<uint32_t>(B2);
   uint8_t* aflag = w.alloc<uint8_t>(B);
-  int64_t* cnt2 = w.alloc<int64_t>(2);
   // scratch capacity for in-place run merges: whatever workspace remains, split over 2 plans
   MergePlan po, pi;
   size_t plan_fixed = sizeof(int64_t) * (B + 2) * 7 + sizeof(int32_t) * (B + 2) * 4 + (B + 2) + 4096 + 256;
-  size_t sort_reserve = sort_ws_bytes(B2) + sizeof(int64_t) * (scan_blocks_for(B2) + 2) * 16 + (1 << 16);
+  size_t sort_reserve = sort_ws_bytes(B2) + sizeof(int64_t) * (scan_blocks_for(B2) + 2) * 16 + (1 << 16) +
+                        sizeof(uint32_t) * ((n + 31) / 32) + sizeof(int64_t) * (scan_blocks_for((n + 31) / 32) + 2) + 512;
   size_t used = w.off + 2 * plan_fixed + sort_reserve;
   int64_t scr_cap = used < w.bytes ? static_cast<int64_t>((w.bytes - used) / 2 / (sizeof(int32_t) + sizeof(int64_t) + 1)) : 0;
   RTEC_TRY(plan_alloc(po, B, scr_cap, true, w));
@@ -910,14 +1076,17 @@ int rtec_batch_apply_phase(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src,
     RTEC_CUDA(cudaEventRecord(side_join(), ms));
     RTEC_CUDA(cudaStreamWaitEvent(s, side_join(), 0));
   }
-  // 9. DegreeDelta rows: unique endpoints of applied updates whose degrees changed
-  k_touched_keys<<<grid, kBlk, 0, s>>>(b->a_src, b->a_dst, b->n_applied, keys, vals, cnt2);
-  RTEC_TRY(sort_pairs(keys, vals, sk, sv, Count{cnt2, B2}, B2, bits_for(static_cast<uint64_t>(n)), w, s));
-  w.off = mark;
-  DeltaFlag df{sk, g->in_deg, g->out_deg, g->in_deg_prev, g->out_deg_prev};
-  RTEC_TRY(exclusive_scan(df, Count{cnt2, B2}, B2,
-                          DeltaOut{df, b->d_vertex, b->d_old_in, b->d_new_in, b->d_old_out, b->d_new_out},
+  // 9. DegreeDelta rows: endpoints of applied updates (touched bitmap) whose degrees changed
+  const int64_t words = (n + 31) / 32;
+  uint32_t* tbm = w.alloc<uint32_t>(words);
+  RTEC_WS_CHECK(w);
+  RTEC_CUDA(cudaMemsetAsync(tbm, 0, sizeof(uint32_t) * words, s));
+  k_touched_bits<<<grid, kBlk, 0, s>>>(b->a_src, b->a_dst, b->n_applied, tbm);
+  TouchedWord tw{tbm, g->in_deg, g->out_deg, g->in_deg_prev, g->out_deg_prev};
+  RTEC_TRY(exclusive_scan(tw, Count{nullptr, words}, words,
+                          TouchedRows{tw, b->d_vertex, b->d_old_in, b->d_new_in, b->d_old_out, b->d_new_out},
                           b->n_delta, w, s));
+  w.off = mark;
   return RTEC_OK;
 }
 

@@ -629,7 +629,7 @@ static int agg_slice_width() {
   if (w < 0) {
     const char* e = getenv("RTEC_AGG_SLICE");
     w = e ? atoi(e) : 0;  // measured: slicing costs more per-edge work than it saves in L2 misses
-    if (w < 0 || w > 64) w = 64;
+    if (w < 0 || w > 256) w = 256;
     w &= ~1;
   }
   return w;
