@@ -535,6 +535,14 @@ __global__ void __launch_bounds__(kBlk) k_merge_items(MergeIn in, MergePlan p, r
 // fall back to the binary search.  Output positions and order are those of k_merge_items.
 constexpr int kWC = 512;
 
+// positions per warp: the work spread over every resident warp (small batches: one
+// 32-position step per warp, no serial walk), at most kWC
+__device__ __forceinline__ int64_t warp_chunk(int64_t W, int64_t nw) {
+  int64_t c = (W + nw - 1) / nw;
+  c = (c + 31) & ~int64_t(31);
+  return c < 32 ? 32 : (c > kWC ? kWC : c);
+}
+
 __device__ __forceinline__ void merge_put(const MergePlan& p, const rtec_adj_t& a, int64_t g, int32_t f0, int64_t out,
                                           int32_t w, int64_t tsv, bool inpl, int64_t dest, int64_t so0) {
   if (inpl) {
@@ -556,8 +564,9 @@ __global__ void __launch_bounds__(kBlk) k_merge_items_warp(MergeIn in, MergePlan
   const int lane = lane_id();
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t t0 = warp * kWC; t0 < W; t0 += nw * kWC) {
-    const int64_t t1 = t0 + kWC < W ? t0 + kWC : W;
+  const int64_t wc = warp_chunk(W, nw);
+  for (int64_t t0 = warp * wc; t0 < W; t0 += nw * wc) {
+    const int64_t t1 = t0 + wc < W ? t0 + wc : W;
     int64_t g = 0;
     if (lane == 0) g = upper_bound_dev<int64_t>(p.work_off, 0, G, t0) - 1;
     g = __shfl_sync(0xffffffffu, g, 0);
@@ -641,8 +650,9 @@ __global__ void __launch_bounds__(kBlk) k_merge_copyback_warp(MergePlan p, rtec_
   const int lane = lane_id();
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t t0 = warp * kWC; t0 < S; t0 += nw * kWC) {
-    const int64_t t1 = t0 + kWC < S ? t0 + kWC : S;
+  const int64_t wc = warp_chunk(S, nw);
+  for (int64_t t0 = warp * wc; t0 < S; t0 += nw * wc) {
+    const int64_t t1 = t0 + wc < S ? t0 + wc : S;
     int64_t g = 0;
     if (lane == 0) g = upper_bound_dev<int64_t>(p.scr_off, 0, G, t0) - 1;
     g = __shfl_sync(0xffffffffu, g, 0);

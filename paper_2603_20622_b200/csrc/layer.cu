@@ -18,6 +18,7 @@
 #include "prims.cuh"
 #include "rowops.cuh"
 #include "gemm_tc.cuh"
+#include "async.cuh"
 
 #include <stdlib.h>
 
@@ -1365,10 +1366,49 @@ struct GatEdgeState {
 
 // contributions of in-run positions [e0, e1) of v: all edges (recompute) or the
 // ValueChange edges (sources in S(l), edge not inserted) -> acc, cacc
+// Row ring of a warp (GAT passes on 16-byte rows of at most 256 floats): kGD slots of
+// (new, old) Z rows in shared memory, each filled by one lane with 1-D bulk copies
+// (cp.async.bulk, completion on the slot's mbarrier), so a warp keeps kGD edges' rows in
+// flight without holding them in registers; plus the warp's attention table.
+constexpr int kGD = 3;
+struct GatRing {
+  float* rows;     // [kGD][2][rw]
+  uint64_t* bar;   // [kGD]
+  float (*att)[32][kHMax + 1];  // [2][32][kHMax + 1]
+  int rw;
+  uint32_t ph;     // parity bit per slot
+};
 template <int VEC, int K>
+__host__ __device__ constexpr int gat_ring_rw() { return 32 * VEC * K; }
+template <int VEC, int K>
+constexpr size_t gat_ring_warp_bytes() {
+  return static_cast<size_t>(kGD) * 2 * gat_ring_rw<VEC, K>() * 4 + 2 * 32 * (kHMax + 1) * 4 + kGD * 8 + 64;
+}
+
+// warp's slice of the dynamic shared memory; mbarriers initialised by lane 0
+template <int VEC, int K>
+__device__ __forceinline__ GatRing gat_ring_init() {
+  extern __shared__ __align__(128) uint8_t s_dyn[];
+  const int wib = threadIdx.x >> 5;
+  uint8_t* base = s_dyn + static_cast<size_t>(wib) * ((gat_ring_warp_bytes<VEC, K>() + 127) & ~size_t(127));
+  GatRing r;
+  r.rw = gat_ring_rw<VEC, K>();
+  r.rows = reinterpret_cast<float*>(base);
+  r.att = reinterpret_cast<float(*)[32][kHMax + 1]>(base + static_cast<size_t>(kGD) * 2 * r.rw * 4);
+  r.bar = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(r.att) + 2 * 32 * (kHMax + 1) * 4 + 7) & ~uintptr_t(7));
+  r.ph = 0;
+  if (lane_id() == 0) {
+    for (int k = 0; k < kGD; ++k) mbar_init(r.bar + k, 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  return r;
+}
+
+template <int VEC, int K, bool RING>
 __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState& es, int64_t beg, int32_t e0,
                                           int32_t e1, int64_t p, int64_t q, bool all, RowAcc<VEC, K>& acc,
-                                          float (&cacc)[K]) {
+                                          float (&cacc)[K], GatRing* ring) {
   using R = RowAcc<VEC, K>;
   const int d = a.L.d_out, H = a.L.heads, dh = d / H;
   const int lane = lane_id();
@@ -1376,9 +1416,9 @@ __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState
   // all heads (same inputs and expf as before), into a per-warp shared-memory table;
   // the gather loop then reads the head of its own columns from it (one LDS per chunk
   // instead of an er load + expf per lane per edge, no per-head register arrays).
-  __shared__ float s_att[kLBlk / 32][2][32][kHMax + 1];
-  float(*an)[kHMax + 1] = s_att[threadIdx.x >> 5][0];
-  float(*ao)[kHMax + 1] = s_att[threadIdx.x >> 5][1];
+  __shared__ float s_att[RING ? 1 : kLBlk / 32][2][32][kHMax + 1];
+  float(*an)[kHMax + 1] = RING ? ring->att[0] : s_att[RING ? 0 : threadIdx.x >> 5][0];
+  float(*ao)[kHMax + 1] = RING ? ring->att[1] : s_att[RING ? 0 : threadIdx.x >> 5][1];
   int hk[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) hk[k] = R::has(k, d) ? chunk_head<VEC>(k, dh) : 0;
@@ -1404,24 +1444,76 @@ __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState
         }
     }
     __syncwarp();
-    while (m) {
-      const int src = __ffs(m) - 1;
-      m &= m - 1;
-      const int32_t uu = __shfl_sync(0xffffffffu, u, src);
-      const int32_t ss = __shfl_sync(0xffffffffu, sl, src);
-      float zn[K][VEC], zo[K][VEC];
-      R::load(a.st.Z + static_cast<int64_t>(uu) * d, d, zn);
-      if (!all) R::load(a.st.Z_log + static_cast<int64_t>(ss) * d, d, zo);
+    if constexpr (RING) {
+      static_assert(VEC == 4 && K <= 2, "ring rows are 16-byte chunks of at most 256 floats");
+      {
+        // pipelined: the rows of up to kGD hits are in flight (bulk copies into the ring);
+        // hits are consumed in edge order (same sums as the register path)
+        const uint32_t bytes = static_cast<uint32_t>(d) * 4u;
+        unsigned mi = m;  // hits still to issue
+        int slot_i = 0, slot_c = 0;
+        auto issue = [&]() {
+          const int src = __ffs(mi) - 1;
+          mi &= mi - 1;
+          const int32_t uu = __shfl_sync(0xffffffffu, u, src);
+          const int32_t ss = __shfl_sync(0xffffffffu, sl, src);
+          if (lane == 0) {
+            float* dst = ring->rows + static_cast<int64_t>(slot_i) * 2 * ring->rw;
+            mbar_expect_tx(ring->bar + slot_i, all ? bytes : 2u * bytes);
+            bulk_g2s(dst, a.st.Z + static_cast<int64_t>(uu) * d, bytes, ring->bar + slot_i);
+            if (!all) bulk_g2s(dst + ring->rw, a.st.Z_log + static_cast<int64_t>(ss) * d, bytes, ring->bar + slot_i);
+          }
+          slot_i = slot_i + 1 == kGD ? 0 : slot_i + 1;
+        };
+        for (int k = 0; k < kGD && mi; ++k) issue();
+        while (m) {
+          const int src = __ffs(m) - 1;
+          m &= m - 1;
+          mbar_wait(ring->bar + slot_c, (ring->ph >> slot_c) & 1u);
+          ring->ph ^= 1u << slot_c;
+          const float* zr = ring->rows + static_cast<int64_t>(slot_c) * 2 * ring->rw;
+          float zn[K][VEC], zo[K][VEC];
+          R::from_stage_sync(zr, d, zn);
+          if (!all) R::from_stage_sync(zr + ring->rw, d, zo);
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const float wn = an[src][hk[k]];
-        const float wo = all ? 0.f : ao[src][hk[k]];
-        cacc[k] += all ? wn : wn - wo;
+          for (int k = 0; k < K; ++k) {
+            const float wn = an[src][hk[k]];
+            const float wo = all ? 0.f : ao[src][hk[k]];
+            cacc[k] += all ? wn : wn - wo;
 #pragma unroll
-        for (int jj = 0; jj < VEC; ++jj) {
-          float x = wn * zn[k][jj];
-          if (!all) x = fmaf(-wo, zo[k][jj], x);
-          acc.v[k][jj] += x;
+            for (int jj = 0; jj < VEC; ++jj) {
+              float x = wn * zn[k][jj];
+              if (!all) x = fmaf(-wo, zo[k][jj], x);
+              acc.v[k][jj] += x;
+            }
+          }
+          // the slot's rows are consumed (the sums above used them): refill it with a later hit
+          __syncwarp();
+          fence_proxy_async();
+          if (mi) issue();
+          slot_c = slot_c + 1 == kGD ? 0 : slot_c + 1;
+        }
+      }
+    } else {
+      while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const int32_t uu = __shfl_sync(0xffffffffu, u, src);
+        const int32_t ss = __shfl_sync(0xffffffffu, sl, src);
+        float zn[K][VEC], zo[K][VEC];
+        R::load(a.st.Z + static_cast<int64_t>(uu) * d, d, zn);
+        if (!all) R::load(a.st.Z_log + static_cast<int64_t>(ss) * d, d, zo);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const float wn = an[src][hk[k]];
+          const float wo = all ? 0.f : ao[src][hk[k]];
+          cacc[k] += all ? wn : wn - wo;
+#pragma unroll
+          for (int jj = 0; jj < VEC; ++jj) {
+            float x = wn * zn[k][jj];
+            if (!all) x = fmaf(-wo, zo[k][jj], x);
+            acc.v[k][jj] += x;
+          }
         }
       }
     }
@@ -1530,10 +1622,16 @@ __device__ __forceinline__ void gat_finalize(const LayerArgs& a, int64_t i, int3
 // 6 CTAs / SM (42 registers, spills): the GAT passes are latency-bound on their row
 // gathers and the two streams' passes co-reside, so occupancy wins -- measured c3-gat
 // p50 3 CTAs 16.4 ms, 4 CTAs 14.7, 5 CTAs 14.55, 6 CTAs 14.1
-template <int VEC, int K, bool FULL>
-__global__ void __launch_bounds__(kLBlk, 6) k_gat_light(LayerArgs a, AggRows rows) {
+template <int VEC, int K, bool FULL, bool RING = false>
+__global__ void __launch_bounds__(kLBlk, RING ? 3 : 6) k_gat_light(LayerArgs a, AggRows rows) {
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
+  GatRing rg_{};
+  GatRing* ring = nullptr;
+  if constexpr (RING) {
+    rg_ = gat_ring_init<VEC, K>();
+    ring = &rg_;
+  }
   const int64_t nr = rows.count();
   const bool scan = FULL || *a.f.n_src > 0;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -1558,16 +1656,22 @@ __global__ void __launch_bounds__(kLBlk, 6) k_gat_light(LayerArgs a, AggRows row
     float cacc[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) cacc[k] = 0.f;
-    if (scan) gat_edges<VEC, K>(a, es, a.g.in.beg[v], 0, len, p, q, recompute, acc, cacc);
+    if (scan) gat_edges<VEC, K, RING>(a, es, a.g.in.beg[v], 0, len, p, q, recompute, acc, cacc, ring);
     if (!recompute) gat_struct<VEC, K>(a, es, p, q, acc, cacc);
     gat_finalize<VEC, K, FULL>(a, i, v, len, recompute, acc, cacc);
   }
 }
 
-template <int VEC, int K, bool FULL>
-__global__ void __launch_bounds__(kLBlk, 6) k_gat_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
+template <int VEC, int K, bool FULL, bool RING = false>
+__global__ void __launch_bounds__(kLBlk, RING ? 3 : 6) k_gat_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
+  GatRing rg_{};
+  GatRing* ring = nullptr;
+  if constexpr (RING) {
+    rg_ = gat_ring_init<VEC, K>();
+    ring = &rg_;
+  }
   const int64_t nh = *hp.n_heavy;
   if (nh == 0) return;
   const int64_t T = hp.hoff[nh];
@@ -1601,7 +1705,7 @@ __global__ void __launch_bounds__(kLBlk, 6) k_gat_heavy(LayerArgs a, AggRows row
 #pragma unroll
     for (int k = 0; k < K; ++k) cacc[k] = 0.f;
     int32_t e0 = c * kChunk, e1 = min(len, e0 + kChunk);
-    gat_edges<VEC, K>(a, es, a.g.in.beg[v], e0, e1, p, q, recompute, acc, cacc);
+    gat_edges<VEC, K, RING>(a, es, a.g.in.beg[v], e0, e1, p, q, recompute, acc, cacc, ring);
     if (!recompute && c == 0) gat_struct<VEC, K>(a, es, p, q, acc, cacc);
     float* part = hp.part + t * pw;
     acc.store(part, d);
@@ -1633,6 +1737,40 @@ __global__ void __launch_bounds__(kLBlk, 6) k_gat_heavy(LayerArgs a, AggRows row
   }
 }
 
+// RTEC_GAT_RING env: 1 (default) bulk-copy row ring for rows of <= 256 floats, 0 register path
+static bool gat_ring_on() {
+  static int r = -1;
+  if (r < 0) {
+    const char* e = getenv("RTEC_GAT_RING");
+    r = e ? atoi(e) : 1;
+  }
+  return r != 0;
+}
+
+template <int VEC, int K, bool FULL>
+static int launch_gat_passes(const LayerArgs& a, AggRows rows, const HeavyPlan& hp, int grid, cudaStream_t s,
+                             cudaStream_t hs) {
+  if constexpr (VEC == 4 && K <= 2) {
+    if (gat_ring_on()) {
+      const size_t smem = ((gat_ring_warp_bytes<VEC, K>() + 127) & ~size_t(127)) * (kLBlk / 32);
+      static bool attr = false;  // per process: the same two instantiations on every device
+      if (!attr) {
+        RTEC_CUDA(cudaFuncSetAttribute(k_gat_heavy<VEC, K, FULL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+        RTEC_CUDA(cudaFuncSetAttribute(k_gat_light<VEC, K, FULL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+        attr = true;
+      }
+      k_gat_heavy<VEC, K, FULL, true><<<grid, kLBlk, smem, hs>>>(a, rows, hp);
+      k_gat_light<VEC, K, FULL, true><<<grid, kLBlk, smem, s>>>(a, rows);
+      return RTEC_OK;
+    }
+  }
+  k_gat_heavy<VEC, K, FULL><<<grid, kLBlk, 0, hs>>>(a, rows, hp);
+  k_gat_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows);
+  return RTEC_OK;
+}
+
 template <bool FULL>
 static int launch_gat(LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_edges, Ws& w, cudaStream_t s) {
   const int d = a.L.d_out;
@@ -1655,8 +1793,9 @@ static int launch_gat(LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_
       RTEC_CUDA(cudaEventRecord(side_fork(), s));
       RTEC_CUDA(cudaStreamWaitEvent(hs, side_fork(), 0));
     }
-    ok = RTEC_ROW_DISPATCH(d, (k_gat_heavy<VEC, K, FULL><<<grid, kLBlk, 0, hs>>>(a, rows, hp),
-                               k_gat_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows)));
+    int grc = RTEC_OK;
+    ok = RTEC_ROW_DISPATCH(d, (grc = launch_gat_passes<VEC, K, FULL>(a, rows, hp, grid, s, hs)));
+    if (grc != RTEC_OK) return grc;
     if (hs != s) {
       RTEC_CUDA(cudaEventRecord(side_join(), hs));
       RTEC_CUDA(cudaStreamWaitEvent(s, side_join(), 0));

@@ -94,6 +94,20 @@ struct RowAcc {
       if (c * VEC < d) cp_async16_hint(stage + c * VEC, row + c * VEC, pol);
     }
   }
+  // row already resident in shared memory (e.g. completed bulk copy)
+  __device__ __forceinline__ static void from_stage_sync(const float* stage, int d, float (&r)[K][VEC]) {
+    static_assert(VEC == 4, "16-byte chunks");
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      int c = lane_id() + 32 * k;
+      if (c * VEC < d) {
+        float4 x = *reinterpret_cast<const float4*>(stage + c * VEC);
+        r[k][0] = x.x; r[k][1] = x.y; r[k][2] = x.z; r[k][3] = x.w;
+      } else {
+        r[k][0] = r[k][1] = r[k][2] = r[k][3] = 0.f;
+      }
+    }
+  }
   __device__ __forceinline__ static void from_stage(const float* stage, int d, float (&r)[K][VEC]) {
     cp_async_wait_all();
 #pragma unroll
