@@ -444,6 +444,10 @@ __device__ __forceinline__ int64_t upper_bound_dev(const T* a, int64_t lo, int64
 // binary search over the global offsets per element.
 constexpr int kMT = 1024;
 
+// merge regime: average work (run suffix + updates) per touched run above 64 positions
+__device__ __forceinline__ bool long_runs(int64_t W, int64_t G) { return W > 64 * G; }
+
+
 struct TileGroups {
   int64_t g0, ng;  // first group of the tile, number of groups staged (0: fall back to global search)
 };
@@ -473,12 +477,14 @@ __device__ __forceinline__ int64_t group_of(const TileGroups& tg, const int64_t*
 }
 
 // element-parallel merge: old elements (from the first changed position) and update items of every group
-__global__ void __launch_bounds__(kBlk) k_merge_items(MergeIn in, MergePlan p, rtec_adj_t a, const uint64_t* err) {
+__global__ void __launch_bounds__(kBlk) k_merge_items(MergeIn in, MergePlan p, rtec_adj_t a, const uint64_t* err,
+                                                      bool choose) {
   __shared__ int64_t s_off[kMT];
   __shared__ int64_t s_g[2];
   if (err_set(err)) return;
   int64_t G = *p.G;
   if (G == 0) return;
+  if (choose && long_runs(p.work_off[G], G)) return;
   int64_t W = p.work_off[G];
   for (int64_t t0 = static_cast<int64_t>(blockIdx.x) * kMT; t0 < W; t0 += static_cast<int64_t>(gridDim.x) * kMT) {
     const int64_t t1 = t0 + kMT < W ? t0 + kMT : W;
@@ -556,11 +562,12 @@ __device__ __forceinline__ void merge_put(const MergePlan& p, const rtec_adj_t& 
 }
 
 __global__ void __launch_bounds__(kBlk) k_merge_items_warp(MergeIn in, MergePlan p, rtec_adj_t a,
-                                                           const uint64_t* err) {
+                                                           const uint64_t* err, bool choose) {
   if (err_set(err)) return;
   const int64_t G = *p.G;
   if (G == 0) return;
   const int64_t W = p.work_off[G];
+  if (choose && !long_runs(W, G)) return;
   const int lane = lane_id();
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -642,10 +649,12 @@ __global__ void __launch_bounds__(kBlk) k_merge_items_warp(MergeIn in, MergePlan
 }
 
 // copy in-place runs back from scratch, a warp per kWC scratch positions walking its groups
-__global__ void __launch_bounds__(kBlk) k_merge_copyback_warp(MergePlan p, rtec_adj_t a, const uint64_t* err) {
+__global__ void __launch_bounds__(kBlk) k_merge_copyback_warp(MergePlan p, rtec_adj_t a, const uint64_t* err,
+                                                              bool choose) {
   if (err_set(err)) return;
   const int64_t G = *p.G;
   if (G == 0) return;
+  if (choose && !long_runs(p.work_off[G], G)) return;
   const int64_t S = p.scr_off[G];
   const int lane = lane_id();
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -671,12 +680,14 @@ __global__ void __launch_bounds__(kBlk) k_merge_copyback_warp(MergePlan p, rtec_
 }
 
 // copy in-place runs back from scratch (after all reads of the old runs)
-__global__ void __launch_bounds__(kBlk) k_merge_copyback(MergePlan p, rtec_adj_t a, const uint64_t* err) {
+__global__ void __launch_bounds__(kBlk) k_merge_copyback(MergePlan p, rtec_adj_t a, const uint64_t* err,
+                                                         bool choose) {
   __shared__ int64_t s_off[kMT];
   __shared__ int64_t s_g[2];
   if (err_set(err)) return;
   int64_t G = *p.G;
   if (G == 0) return;
+  if (choose && long_runs(p.work_off[G], G)) return;
   int64_t S = p.scr_off[G];
   for (int64_t t0 = static_cast<int64_t>(blockIdx.x) * kMT; t0 < S; t0 += static_cast<int64_t>(gridDim.x) * kMT) {
     const int64_t t1 = t0 + kMT < S ? t0 + kMT : S;
@@ -749,25 +760,32 @@ static int merge_plan(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, floa
   return RTEC_OK;
 }
 
-// RTEC_MERGE_WARP env: 1 (default) warp-per-chunk merge kernels, 0 element-parallel (A/B)
-static bool merge_warp() {
+// RTEC_MERGE_WARP env: 1 (default) choose on the device by work per run, 0 element-parallel
+// only, 2 warp-per-chunk only (A/B)
+static int merge_mode() {
   static int m = -1;
   if (m < 0) {
     const char* e = getenv("RTEC_MERGE_WARP");
     m = e ? atoi(e) : 1;
+    if (m < 0 || m > 2) m = 1;
   }
-  return m != 0;
+  return m;
 }
 
 static int merge_exec(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, int64_t work_bound, uint64_t* err,
                       cudaStream_t s) {
   RTEC_PROF("adj_merge", s);
-  if (merge_warp()) {
-    k_merge_items_warp<<<grid_for(work_bound, kWC * (kBlk / 32), kSMs * 8), kBlk, 0, s>>>(in, p, a, err);
-    k_merge_copyback_warp<<<grid_for(work_bound, kWC * (kBlk / 32), kSMs * 8), kBlk, 0, s>>>(p, a, err);
-  } else {
-    k_merge_items<<<grid_for(work_bound, kMT, kSMs * 8), kBlk, 0, s>>>(in, p, a, err);
-    k_merge_copyback<<<grid_for(work_bound, kMT, kSMs * 8), kBlk, 0, s>>>(p, a, err);
+  // both variants are enqueued; on the device each runs only for its own regime of the
+  // average merge work per touched run (warp-per-chunk for long runs, measured on c3-gat's
+  // ~490-edge runs; element-parallel for short ones, c2 / c1)
+  const int mode = merge_mode();
+  if (mode != 0) {
+    k_merge_items_warp<<<grid_for(work_bound, kWC * (kBlk / 32), kSMs * 8), kBlk, 0, s>>>(in, p, a, err, mode == 1);
+    k_merge_copyback_warp<<<grid_for(work_bound, kWC * (kBlk / 32), kSMs * 8), kBlk, 0, s>>>(p, a, err, mode == 1);
+  }
+  if (mode != 2) {
+    k_merge_items<<<grid_for(work_bound, kMT, kSMs * 8), kBlk, 0, s>>>(in, p, a, err, mode == 1);
+    k_merge_copyback<<<grid_for(work_bound, kMT, kSMs * 8), kBlk, 0, s>>>(p, a, err, mode == 1);
   }
   k_merge_commit<<<grid_for(in.maxK, kBlk), kBlk, 0, s>>>(p, a, err);
   k_commit_reserve<<<1, 32, 0, s>>>(p, a, err);

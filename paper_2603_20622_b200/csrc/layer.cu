@@ -1737,12 +1737,15 @@ __global__ void __launch_bounds__(kLBlk, RING ? 3 : 6) k_gat_heavy(LayerArgs a, 
   }
 }
 
-// RTEC_GAT_RING env: 1 (default) bulk-copy row ring for rows of <= 256 floats, 0 register path
+// RTEC_GAT_RING env: 1 bulk-copy row ring for rows of <= 256 floats, 0 (default) register
+// path.  Measured on c3-gat (profiles/r02g_gat_ring_ab.md): the ring runs the GAT stage at
+// 8.2 ms per layer launch against 6.2 ms -- one 1 KB bulk copy per gathered row at 3 CTAs / SM
+// loses to 6 CTAs / SM of register gathers
 static bool gat_ring_on() {
   static int r = -1;
   if (r < 0) {
     const char* e = getenv("RTEC_GAT_RING");
-    r = e ? atoi(e) : 1;
+    r = e ? atoi(e) : 0;
   }
   return r != 0;
 }
