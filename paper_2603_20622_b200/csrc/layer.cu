@@ -1367,25 +1367,24 @@ struct GatEdgeState {
 // contributions of in-run positions [e0, e1) of v: all edges (recompute) or the
 // ValueChange edges (sources in S(l), edge not inserted) -> acc, cacc
 // Row ring of a warp (GAT passes on 16-byte rows of at most 256 floats): kGD slots of
-// (new, old) Z rows in shared memory, each filled by one lane with 1-D bulk copies
-// (cp.async.bulk, completion on the slot's mbarrier), so a warp keeps kGD edges' rows in
-// flight without holding them in registers; plus the warp's attention table.
+// (new, old) Z rows in shared memory.  Every lane copies its own 16-byte chunks of a row
+// with cp.async (LDGSTS, one commit group per edge) and later reads back exactly those
+// chunks, so no cross-lane synchronisation is needed; a warp keeps kGD edges' rows in
+// flight without holding them in registers.  The ring also holds the warp's attention table.
 constexpr int kGD = 3;
 struct GatRing {
   float* rows;     // [kGD][2][rw]
-  uint64_t* bar;   // [kGD]
   float (*att)[32][kHMax + 1];  // [2][32][kHMax + 1]
   int rw;
-  uint32_t ph;     // parity bit per slot
 };
 template <int VEC, int K>
 __host__ __device__ constexpr int gat_ring_rw() { return 32 * VEC * K; }
 template <int VEC, int K>
 constexpr size_t gat_ring_warp_bytes() {
-  return static_cast<size_t>(kGD) * 2 * gat_ring_rw<VEC, K>() * 4 + 2 * 32 * (kHMax + 1) * 4 + kGD * 8 + 64;
+  return static_cast<size_t>(kGD) * 2 * gat_ring_rw<VEC, K>() * 4 + 2 * 32 * (kHMax + 1) * 4;
 }
 
-// warp's slice of the dynamic shared memory; mbarriers initialised by lane 0
+// warp's slice of the dynamic shared memory
 template <int VEC, int K>
 __device__ __forceinline__ GatRing gat_ring_init() {
   extern __shared__ __align__(128) uint8_t s_dyn[];
@@ -1395,14 +1394,14 @@ __device__ __forceinline__ GatRing gat_ring_init() {
   r.rw = gat_ring_rw<VEC, K>();
   r.rows = reinterpret_cast<float*>(base);
   r.att = reinterpret_cast<float(*)[32][kHMax + 1]>(base + static_cast<size_t>(kGD) * 2 * r.rw * 4);
-  r.bar = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(r.att) + 2 * 32 * (kHMax + 1) * 4 + 7) & ~uintptr_t(7));
-  r.ph = 0;
-  if (lane_id() == 0) {
-    for (int k = 0; k < kGD; ++k) mbar_init(r.bar + k, 1);
-    fence_barrier_init();
-  }
-  __syncwarp();
   return r;
+}
+
+// wait until at most `pending` of this thread's newest cp.async groups are in flight
+__device__ __forceinline__ void cp_async_wait_pending(int pending) {
+  if (pending <= 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
+  else if (pending == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
+  else asm volatile("cp.async.wait_group 2;" ::: "memory");
 }
 
 template <int VEC, int K, bool RING>
@@ -1447,30 +1446,37 @@ __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState
     if constexpr (RING) {
       static_assert(VEC == 4 && K <= 2, "ring rows are 16-byte chunks of at most 256 floats");
       {
-        // pipelined: the rows of up to kGD hits are in flight (bulk copies into the ring);
+        // pipelined: the rows of up to kGD hits are in flight (cp.async into the ring);
         // hits are consumed in edge order (same sums as the register path)
-        const uint32_t bytes = static_cast<uint32_t>(d) * 4u;
+        static_assert(kGD == 3, "cp_async_wait_pending covers up to 2 newer groups");
         unsigned mi = m;  // hits still to issue
-        int slot_i = 0, slot_c = 0;
+        int slot_i = 0, slot_c = 0, inflight = 0;
         auto issue = [&]() {
           const int src = __ffs(mi) - 1;
           mi &= mi - 1;
           const int32_t uu = __shfl_sync(0xffffffffu, u, src);
           const int32_t ss = __shfl_sync(0xffffffffu, sl, src);
-          if (lane == 0) {
-            float* dst = ring->rows + static_cast<int64_t>(slot_i) * 2 * ring->rw;
-            mbar_expect_tx(ring->bar + slot_i, all ? bytes : 2u * bytes);
-            bulk_g2s(dst, a.st.Z + static_cast<int64_t>(uu) * d, bytes, ring->bar + slot_i);
-            if (!all) bulk_g2s(dst + ring->rw, a.st.Z_log + static_cast<int64_t>(ss) * d, bytes, ring->bar + slot_i);
+          float* dst = ring->rows + static_cast<int64_t>(slot_i) * 2 * ring->rw;
+          const float* zr = a.st.Z + static_cast<int64_t>(uu) * d;
+          const float* zl = a.st.Z_log + static_cast<int64_t>(ss) * d;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const int c = (lane + 32 * k) * VEC;
+            if (c < d) {
+              cp_async16(dst + c, zr + c);
+              if (!all) cp_async16(dst + ring->rw + c, zl + c);
+            }
           }
+          cp_async_commit();
+          ++inflight;
           slot_i = slot_i + 1 == kGD ? 0 : slot_i + 1;
         };
         for (int k = 0; k < kGD && mi; ++k) issue();
         while (m) {
           const int src = __ffs(m) - 1;
           m &= m - 1;
-          mbar_wait(ring->bar + slot_c, (ring->ph >> slot_c) & 1u);
-          ring->ph ^= 1u << slot_c;
+          cp_async_wait_pending(inflight - 1);  // this hit's group (the oldest) has landed
+          --inflight;
           const float* zr = ring->rows + static_cast<int64_t>(slot_c) * 2 * ring->rw;
           float zn[K][VEC], zo[K][VEC];
           R::from_stage_sync(zr, d, zn);
@@ -1487,10 +1493,7 @@ __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState
               acc.v[k][jj] += x;
             }
           }
-          // the slot's rows are consumed (the sums above used them): refill it with a later hit
-          __syncwarp();
-          fence_proxy_async();
-          if (mi) issue();
+          if (mi) issue();  // refill the consumed slot (this lane's chunks only: no hazard)
           slot_c = slot_c + 1 == kGD ? 0 : slot_c + 1;
         }
       }
@@ -1737,10 +1740,10 @@ __global__ void __launch_bounds__(kLBlk, RING ? 3 : 6) k_gat_heavy(LayerArgs a, 
   }
 }
 
-// RTEC_GAT_RING env: 1 bulk-copy row ring for rows of <= 256 floats, 0 (default) register
-// path.  Measured on c3-gat (profiles/r02g_gat_ring_ab.md): the ring runs the GAT stage at
-// 8.2 ms per layer launch against 6.2 ms -- one 1 KB bulk copy per gathered row at 3 CTAs / SM
-// loses to 6 CTAs / SM of register gathers
+// RTEC_GAT_RING env: 1 cp.async row ring for rows of <= 256 floats, 0 (default) register
+// path.  Measured on c3-gat (profiles/r02g_gat_ring_ab.md): a ring filled by 1 KB bulk
+// copies (cp.async.bulk, one lane, mbarriers) ran the GAT stage at 8.2 ms per layer launch
+// against 6.2 ms for 6 CTAs / SM of register gathers
 static bool gat_ring_on() {
   static int r = -1;
   if (r < 0) {
