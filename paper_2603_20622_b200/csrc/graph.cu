@@ -760,8 +760,8 @@ static int merge_plan(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, floa
   return RTEC_OK;
 }
 
-// RTEC_MERGE_WARP env: 1 (default) choose on the device by work per run, 0 element-parallel
-// only, 2 warp-per-chunk only (A/B)
+// RTEC_MERGE_WARP env: 1 (default) choose by run slots per vertex, 0 element-parallel only,
+// 2 warp-per-chunk only (A/B)
 static int merge_mode() {
   static int m = -1;
   if (m < 0) {
@@ -772,20 +772,19 @@ static int merge_mode() {
   return m;
 }
 
-static int merge_exec(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, int64_t work_bound, uint64_t* err,
-                      cudaStream_t s) {
+static int merge_exec(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, int64_t n, int64_t work_bound,
+                      uint64_t* err, cudaStream_t s) {
   RTEC_PROF("adj_merge", s);
-  // both variants are enqueued; on the device each runs only for its own regime of the
-  // average merge work per touched run (warp-per-chunk for long runs, measured on c3-gat's
-  // ~490-edge runs; element-parallel for short ones, c2 / c1)
+  // warp-per-chunk merges for long runs (measured on c3-gat's ~490-edge runs), element-parallel
+  // ones for short runs (c2 / c1); the regime from the run slots per vertex (host-known)
   const int mode = merge_mode();
-  if (mode != 0) {
-    k_merge_items_warp<<<grid_for(work_bound, kWC * (kBlk / 32), kSMs * 8), kBlk, 0, s>>>(in, p, a, err, mode == 1);
-    k_merge_copyback_warp<<<grid_for(work_bound, kWC * (kBlk / 32), kSMs * 8), kBlk, 0, s>>>(p, a, err, mode == 1);
-  }
-  if (mode != 2) {
-    k_merge_items<<<grid_for(work_bound, kMT, kSMs * 8), kBlk, 0, s>>>(in, p, a, err, mode == 1);
-    k_merge_copyback<<<grid_for(work_bound, kMT, kSMs * 8), kBlk, 0, s>>>(p, a, err, mode == 1);
+  const bool warp = mode == 2 || (mode == 1 && a.slots > 96 * (n > 0 ? n : 1));
+  if (warp) {
+    k_merge_items_warp<<<grid_for(work_bound, kWC * (kBlk / 32), kSMs * 8), kBlk, 0, s>>>(in, p, a, err, false);
+    k_merge_copyback_warp<<<grid_for(work_bound, kWC * (kBlk / 32), kSMs * 8), kBlk, 0, s>>>(p, a, err, false);
+  } else {
+    k_merge_items<<<grid_for(work_bound, kMT, kSMs * 8), kBlk, 0, s>>>(in, p, a, err, false);
+    k_merge_copyback<<<grid_for(work_bound, kMT, kSMs * 8), kBlk, 0, s>>>(p, a, err, false);
   }
   k_merge_commit<<<grid_for(in.maxK, kBlk), kBlk, 0, s>>>(p, a, err);
   k_commit_reserve<<<1, 32, 0, s>>>(p, a, err);
@@ -1098,8 +1097,8 @@ int rtec_batch_apply_phase(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src,
     RTEC_CUDA(cudaEventRecord(side_fork(), s));
     RTEC_CUDA(cudaStreamWaitEvent(ms, side_fork(), 0));
   }
-  RTEC_TRY(merge_exec(mo, po, g->out, work_bound, b->err, ms));
-  RTEC_TRY(merge_exec(mi, pi, g->in, work_bound, b->err, s));
+  RTEC_TRY(merge_exec(mo, po, g->out, n, work_bound, b->err, ms));
+  RTEC_TRY(merge_exec(mi, pi, g->in, n, work_bound, b->err, s));
   if (ms != s) {
     RTEC_CUDA(cudaEventRecord(side_join(), ms));
     RTEC_CUDA(cudaStreamWaitEvent(s, side_join(), 0));
