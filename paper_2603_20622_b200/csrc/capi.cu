@@ -94,11 +94,6 @@ size_t rtec_prof_report(char* buf, size_t len, int reset) {
 }
 const char* rtec_version(void) { return "rtec-b200 0.1 (sm_100a)"; }
 
-int rtec_device_sm_count(void) {
-  int dev = 0, sms = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
-  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
-  return sms;
-}
+int rtec_device_sm_count(void) { return sm_count(); }
 
 }  // extern "C"

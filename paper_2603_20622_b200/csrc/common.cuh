@@ -11,7 +11,14 @@
 namespace rtec {
 
 constexpr int kWarp = 32;
-constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs
+constexpr int kMaxDevices = 64;
+
+// SM count of the current device (148 on B200: 2 dies x 74), queried once per device;
+// grids are sized in multiples of it
+int sm_count();
+#define kSMs (::rtec::sm_count())
+// current device ordinal (0..kMaxDevices-1) for per-device host state
+int cur_device();
 
 // ---------------------------------------------------------------- errors
 void set_error(const char* fmt, ...);

@@ -493,10 +493,11 @@ int gemm_tc_launch(const TcArgs& g, cudaStream_t s) {
   if (g.max_rows <= 0) return RTEC_OK;
   const bool fused = g.delta_next && !g.Yt;
   size_t smem = gemm_tc_smem(g.npad, fused);
-  static int configured = 0;
-  if (!configured) {
+  static bool configured[kMaxDevices] = {};  // a function attribute is per device
+  const int dev = cur_device();
+  if (!configured[dev]) {
     RTEC_CUDA(cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    configured = 1;
+    configured[dev] = true;
   }
   int64_t tiles = (g.max_rows + kTM - 1) / kTM;
   int grid = static_cast<int>(tiles < kSMs ? tiles : kSMs);

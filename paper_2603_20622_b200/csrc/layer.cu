@@ -72,7 +72,25 @@ struct LayerArgs {
   const float* self_in;         // H^l (st.H_in is redirected to the payload rows for PinSAGE / MoNet)
   int layer;
   uint64_t* err;
+  // light-pass kernel chosen on the device from the layer's scan size Σ indeg(V_dst) and hit
+  // density |E_curr| / Σ indeg(V_dst) (frontier counters 5 / 0): 0 always run, 1 run only on
+  // large sparse scans (warp-batched pass), 2 otherwise (one destination per warp)
+  int pick;
+  float pick_thr;
 };
+
+// the warp-batched pass pays off only on large, sparse scans (c2-gcn layer 1: 55M scanned
+// in-edges, 24 % hits); small layers (c1, c2-sage layer 1) and dense ones favour one
+// destination per warp (profiles/r02j_light_pick_ab.md)
+constexpr float kBatchMinScan = 8e6f;
+
+__device__ __forceinline__ bool pick_ok(const LayerArgs& a) {
+  if (a.pick == 0) return true;
+  const float e = static_cast<float>(a.f.counters[0]);
+  const float s = static_cast<float>(a.f.counters[5]);
+  const bool batched = s >= kBatchMinScan && e < a.pick_thr * s;
+  return a.pick == 1 ? batched : !batched;
+}
 
 // row of v in S / ctx (and in H_out when out_local): per owned vertex when sharded
 __device__ __forceinline__ int64_t srow(const LayerArgs& a, int32_t v) {
@@ -329,6 +347,7 @@ __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_light(Laye
   using R = RowAcc<VEC, K>;
   __shared__ __align__(16) float s_sv[kLBlk / 32][(!FULL && VEC == 4) ? 32 * VEC * K : 4];
   if (!FULL && err_set(a.err)) return;
+  if (!FULL && !pick_ok(a)) return;
   const int64_t nr = rows.count();
   const bool scan = FULL || *a.f.n_src > 0;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -393,6 +412,7 @@ __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_batch(Laye
   __shared__ int32_t s_u[kLBlk / 32][kBatchWin];
   __shared__ int32_t s_c[kLBlk / 32][32];
   if (err_set(a.err)) return;
+  if (!pick_ok(a)) return;
   const int64_t nr = rows.count();
   const bool scan = *a.f.n_src > 0;
   const int lane = lane_id();
@@ -646,6 +666,18 @@ static bool agg_batched(int d) {
   return d <= b;
 }
 
+// RTEC_AGG_DENSE env: hit density |E_curr| / Σ indeg(V_dst) below which a large scan of rows
+// <= 128 floats uses the warp-batched light pass instead of one destination per warp
+static float agg_dense_thr() {
+  static float t = -1.f;
+  if (t < 0.f) {
+    const char* e = getenv("RTEC_AGG_DENSE");
+    t = e ? static_cast<float>(atof(e)) : 0.3f;
+    if (t < 0.f) t = 0.f;
+  }
+  return t;
+}
+
 // RTEC_HEAVY_ORDER env: visit hub chunks in relative-position order (default 1; 0: destination-major)
 static bool heavy_order() {
   static int o = -1;
@@ -726,9 +758,15 @@ static int launch_aggregation(LayerArgs& a, AggRows rows, int64_t max_rows, int6
     }
     {
       RTEC_PROF(FULL ? "k_agg_full_light" : "k_agg_inc", s);
-      if (!FULL && !sliced && agg_batched(a.cw))
-        ok = ok && RTEC_ROW_DISPATCH(a.cw, (k_agg_batch<VEC, K><<<grid, kLBlk, 0, s>>>(a, rows)));
-      else
+      if (!FULL && !sliced && agg_batched(a.cw)) {
+        // both light-pass kernels are enqueued; each runs only in its hit-density regime
+        LayerArgs ab = a, al = a;
+        ab.pick = 1;
+        al.pick = 2;
+        ab.pick_thr = al.pick_thr = agg_dense_thr();
+        ok = ok && RTEC_ROW_DISPATCH(a.cw, (k_agg_batch<VEC, K><<<grid, kLBlk, 0, s>>>(ab, rows),
+                                            k_agg_light<VEC, K, false><<<grid, kLBlk, 0, s>>>(al, rows)));
+      } else
         ok = ok && (sliced ? RTEC_SLICE_DISPATCH(a.cw, (k_agg_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows)))
                            : RTEC_ROW_DISPATCH(a.cw, (k_agg_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows))));
     }
@@ -1759,13 +1797,14 @@ static int launch_gat_passes(const LayerArgs& a, AggRows rows, const HeavyPlan& 
   if constexpr (VEC == 4 && K <= 2) {
     if (gat_ring_on()) {
       const size_t smem = ((gat_ring_warp_bytes<VEC, K>() + 127) & ~size_t(127)) * (kLBlk / 32);
-      static bool attr = false;  // per process: the same two instantiations on every device
-      if (!attr) {
+      static bool attr[kMaxDevices] = {};  // a function attribute is per device
+      const int dev = cur_device();
+      if (!attr[dev]) {
         RTEC_CUDA(cudaFuncSetAttribute(k_gat_heavy<VEC, K, FULL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem)));
         RTEC_CUDA(cudaFuncSetAttribute(k_gat_light<VEC, K, FULL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem)));
-        attr = true;
+        attr[dev] = true;
       }
       k_gat_heavy<VEC, K, FULL, true><<<grid, kLBlk, smem, hs>>>(a, rows, hp);
       k_gat_light<VEC, K, FULL, true><<<grid, kLBlk, smem, s>>>(a, rows);

@@ -80,21 +80,42 @@ std::string prof_report(bool reset) {
   return out;
 }
 
-// ---------------------------------------------------------------- side stream
+// ---------------------------------------------------------------- per-device host state
+int cur_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+  return d;
+}
+
+int sm_count() {
+  static int cache[kMaxDevices] = {0};
+  const int d = cur_device();
+  if (!cache[d]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+    cache[d] = v > 0 ? v : 148;
+  }
+  return cache[d];
+}
+
+// side stream + fork / join events of the current device (the two-stream passes)
 cudaStream_t side_stream() {
-  static cudaStream_t st = nullptr;
-  if (!st) cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-  return st;
+  static cudaStream_t st[kMaxDevices] = {};
+  const int d = cur_device();
+  if (!st[d]) cudaStreamCreateWithFlags(&st[d], cudaStreamNonBlocking);
+  return st[d];
 }
 cudaEvent_t side_fork() {
-  static cudaEvent_t e = nullptr;
-  if (!e) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-  return e;
+  static cudaEvent_t e[kMaxDevices] = {};
+  const int d = cur_device();
+  if (!e[d]) cudaEventCreateWithFlags(&e[d], cudaEventDisableTiming);
+  return e[d];
 }
 cudaEvent_t side_join() {
-  static cudaEvent_t e = nullptr;
-  if (!e) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-  return e;
+  static cudaEvent_t e[kMaxDevices] = {};
+  const int d = cur_device();
+  if (!e[d]) cudaEventCreateWithFlags(&e[d], cudaEventDisableTiming);
+  return e[d];
 }
 
 // ---------------------------------------------------------------- small sort
