@@ -232,6 +232,14 @@ def apply_bytes(B: int, apply_ctr) -> float:
     return 25.0 * B + 12.0 * (2 * w_out + 2 * s_out) + 4.0 * (2 * w_in + 2 * s_in)
 
 
+def merge_bytes(apply_ctr) -> float:
+    """Algorithmic bytes of the two run merges of one batch (both directions): the old
+    suffix + update items read and the new suffix written, plus the in-place scratch staged
+    and copied back (out-runs 12 B per element with ts, in-runs 4 B)."""
+    w_out, s_out, w_in, s_in = [float(x) for x in apply_ctr]
+    return 12.0 * (2 * w_out + 2 * s_out) + 4.0 * (2 * w_in + 2 * s_in)
+
+
 def bench_config(args, wl: dict, world: int) -> dict:
     """The workload dict both arms print (same_config)."""
     sharded = world > 1
@@ -425,6 +433,8 @@ def run_ours(args, world, rank, local):
                        for k in range(PROF) for l in range(L)) / max(cnt, 1)
         elif name == "batch_apply" and not sharded:
             byts = sum(apply_bytes(bsz[k], AC[k]) for k in range(PROF)) / max(cnt, 1)
+        elif name == "adj_merge" and not sharded:
+            byts = sum(merge_bytes(AC[k]) for k in range(PROF)) / max(cnt, 1)
         kernels[name] = {"launches": cnt, "total_ms": round(ms, 4), "ms_per_launch": round(per_launch_ms, 5),
                          "share": round(ms / max(prof_step_ms, 1e-9), 4),
                          "algo_GBps": round(byts / (per_launch_ms * 1e6), 1) if byts else None}

@@ -24,6 +24,8 @@
 #include "gemm_tc.cuh"
 #include "async.cuh"
 
+#include <stdlib.h>
+
 namespace rtec {
 
 constexpr int kTM = 128;                    // UMMA M (rows per tile)
@@ -112,14 +114,29 @@ struct TcShape {
 
 constexpr int kOldBytes = 8 * 2 * 32 * 32 * 4;  // 8 epilogue warps x 2 buffers x 32 rows x 32 cols
 
+// RTEC_GEMM_NWIDE env: 1 (default) one N <= 256 MMA per (K-step, product) when the shared
+// memory leaves a double-buffered 64 KB B ring (no fused deltas), 0 always two N-halves
+static bool gemm_n_wide() {
+  static int w = -1;
+  if (w < 0) {
+    const char* e = getenv("RTEC_GEMM_NWIDE");
+    w = e ? atoi(e) : 1;
+  }
+  return w != 0;
+}
+
 static TcShape tc_shape(int npad, bool fused) {
   TcShape sh;
-  sh.nh = npad > 128 ? 2 : 1;
+  // N > 128 runs in two N-halves (32 KB B stages, deep rings) unless the whole N fits one
+  // MMA with a double-buffered B ring: half the MMA issues and ~25 % fewer shared-memory
+  // operand reads (A is read once per K-step instead of once per N-half)
+  const bool wide = gemm_n_wide() && !fused && npad > 128;
+  sh.nh = (npad > 128 && !wide) ? 2 : 1;
   sh.h0 = sh.nh == 2 ? ((npad / 2 + 15) / 16) * 16 : npad;
   sh.bstage = 2u * static_cast<uint32_t>(sh.h0) * kTK * 4;
   sh.oldb = fused ? kOldBytes : 0;
   const int budget = 227 * 1024 - 1024 - 512 - kEpiBytes - static_cast<int>(sh.oldb);
-  sh.SA = fused ? 2 : 3;  // measured: 2..4 A stages perform alike; the B ring gets the rest
+  sh.SA = (fused || wide) ? 2 : 3;  // measured: 2..4 A stages perform alike; the B ring gets the rest
   sh.SB = (budget - sh.SA * 2 * kABlockBytes) / static_cast<int>(sh.bstage);
   if (sh.SB > kMaxB) sh.SB = kMaxB;
   return sh;
