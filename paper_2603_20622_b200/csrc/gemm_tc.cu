@@ -114,13 +114,16 @@ struct TcShape {
 
 constexpr int kOldBytes = 8 * 2 * 32 * 32 * 4;  // 8 epilogue warps x 2 buffers x 32 rows x 32 cols
 
-// RTEC_GEMM_NWIDE env: 1 (default) one N <= 256 MMA per (K-step, product) when the shared
-// memory leaves a double-buffered 64 KB B ring (no fused deltas), 0 always two N-halves
+// RTEC_GEMM_NWIDE env: 1 one N <= 256 MMA per (K-step, product) when the shared memory leaves
+// a double-buffered 64 KB B ring (no fused deltas), 0 (default) two N-halves.  Measured on
+// c2-gcn layer 2 (profiles/r02k_gemm_wide.md): tensor pipe 30 -> 40 % active but 1.77 ->
+// 1.83 ms -- the shallower B ring (2 x 64 KB instead of 4 x 32 KB) costs more than the halved
+// MMA issues / A re-reads save
 static bool gemm_n_wide() {
   static int w = -1;
   if (w < 0) {
     const char* e = getenv("RTEC_GEMM_NWIDE");
-    w = e ? atoi(e) : 1;
+    w = e ? atoi(e) : 0;
   }
   return w != 0;
 }

@@ -1078,12 +1078,23 @@ int rtec_batch_apply_phase(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src,
   RTEC_TRY(sort_pairs(keys, vals, sk, sv, Count{b->n_applied, B}, B, bits, w, s));
   w.off = mark;
   k_in_gather<<<grid, kBlk, 0, s>>>(sv, b->n_applied, b->a_src, b->a_dst, b->a_op, b->i_src, b->i_dst, b->i_op);
-  // 7. plan both merges (no mutation; all-or-nothing arena reservation)
-  RTEC_TRY(merge_plan(mo, po, g->out, g->slack, g->min_slack, b->err, w, s, b->apply_ctr));
-  w.off = mark;
-  RTEC_TRY(merge_plan(mi, pi, g->in, g->slack, g->min_slack, b->err, w, s,
-                      b->apply_ctr ? b->apply_ctr + 2 : nullptr));
-  w.off = mark;
+  // 7. plan both merges (no mutation; all-or-nothing arena reservation) -- independent of
+  // each other: the in-run plan runs on the side stream with its own scratch
+  {
+    cudaStream_t ps = g_prof_on ? s : side_stream();
+    if (ps != s) {
+      RTEC_CUDA(cudaEventRecord(side_fork(), s));
+      RTEC_CUDA(cudaStreamWaitEvent(ps, side_fork(), 0));
+    }
+    RTEC_TRY(merge_plan(mo, po, g->out, g->slack, g->min_slack, b->err, w, s, b->apply_ctr));
+    RTEC_TRY(merge_plan(mi, pi, g->in, g->slack, g->min_slack, b->err, w, ps,
+                        b->apply_ctr ? b->apply_ctr + 2 : nullptr));
+    if (ps != s) {
+      RTEC_CUDA(cudaEventRecord(side_join(), ps));
+      RTEC_CUDA(cudaStreamWaitEvent(s, side_join(), 0));
+    }
+    w.off = mark;
+  }
   }
   if (!exec) return RTEC_OK;
   // 8. mutate: degrees, runs, per-destination ranges

@@ -164,6 +164,54 @@ __global__ void __launch_bounds__(1024) k_sort_small(const uint64_t* __restrict_
   }
 }
 
+// One CTA of 1024 threads, n <= 1024: bitonic network with one (key, val) per thread in
+// registers; pairs closer than a warp exchange by shuffles, farther ones through shared
+// memory (15 of the 55 compare stages of a 1024-sort need a block barrier).
+__global__ void __launch_bounds__(1024) k_sort_reg(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                   uint64_t* kout, uint32_t* vout, Count cnt) {
+  __shared__ uint64_t sk[1024];
+  __shared__ uint32_t sv[1024];
+  const int64_t n = cnt.get();
+  const int t = threadIdx.x;
+  int N = 32;
+  while (N < n) N <<= 1;
+  uint64_t key = t < n ? kin[t] : ~0ull;
+  uint32_t val = t < n ? vin[t] : 0xffffffffu;
+  for (int size = 2; size <= N; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      uint64_t pk;
+      uint32_t pv;
+      if (stride >= 32) {
+        __syncthreads();
+        if (t < N) {
+          sk[t] = key;
+          sv[t] = val;
+        }
+        __syncthreads();
+        pk = t < N ? sk[t ^ stride] : key;
+        pv = t < N ? sv[t ^ stride] : val;
+      } else {
+        pk = __shfl_xor_sync(0xffffffffu, key, stride);
+        pv = __shfl_xor_sync(0xffffffffu, val, stride);
+      }
+      if (t < N) {
+        const bool up = (t & size) == 0;
+        const bool lower = (t & stride) == 0;
+        const bool gt = key > pk || (key == pk && val > pv);  // self after partner
+        const bool take = lower ? (up ? gt : !gt) : (up ? !gt : gt);
+        if (take && !(key == pk && val == pv)) {
+          key = pk;
+          val = pv;
+        }
+      }
+    }
+  }
+  if (t < n) {
+    kout[t] = key;
+    vout[t] = val;
+  }
+}
+
 // ---------------------------------------------------------------- radix sort
 constexpr int kRxBlock = 256;
 constexpr int kRxItems = 8;
@@ -262,6 +310,11 @@ struct U32At {
 int sort_pairs(const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* keys_out, uint32_t* vals_out,
                Count cnt, int64_t max_n, int bits, Ws& ws, cudaStream_t s) {
   if (max_n <= 0) return RTEC_OK;
+  if (max_n <= 1024) {
+    k_sort_reg<<<1, 1024, 0, s>>>(keys_in, vals_in, keys_out, vals_out, cnt);
+    RTEC_LAUNCH_CHECK("k_sort_reg");
+    return RTEC_OK;
+  }
   if (max_n <= kSmallSort) {
     k_sort_small<<<1, 1024, 0, s>>>(keys_in, vals_in, keys_out, vals_out, cnt);
     RTEC_LAUNCH_CHECK("k_sort_small");
