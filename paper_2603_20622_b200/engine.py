@@ -445,14 +445,16 @@ class RTECEngine:
         if hb is None or hb["cap"] < cap:
             pin = lambda t, k: torch.empty(k, dtype=t, pin_memory=True)  # noqa: E731
             hb = self._host = {"cap": cap, "err": pin(torch.int64, 1), "nd": pin(torch.int64, 1),
-                               "status": pin(torch.uint8, cap), "d": [pin(torch.int32, 2 * cap) for _ in range(5)],
+                               "status": pin(torch.uint8, cap),
+                               "d": torch.empty((2 * cap, 5), dtype=torch.int32, pin_memory=True),
                                "ctr": pin(torch.int64, 8 * self.L)}
         hb["err"].copy_(b.err, non_blocking=True)
         hb["nd"].copy_(b.n_delta, non_blocking=True)
         if B:
             hb["status"][:B].copy_(b.status[:B], non_blocking=True)
-            for h, t in zip(hb["d"], b.d):  # DegreeDelta rows: at most 2B
-                h[: 2 * B].copy_(t[: 2 * B], non_blocking=True)
+            # DegreeDelta rows (at most 2B) interleaved into [rows, 5] on the device: one copy,
+            # and the host result is a slice instead of a stack of five columns
+            hb["d"][: 2 * B].copy_(torch.stack([t[: 2 * B] for t in b.d], dim=1), non_blocking=True)
         for l, f in enumerate(self.fr):
             hb["ctr"][8 * l: 8 * l + 8].copy_(f.counters, non_blocking=True)
         torch.cuda.current_stream().synchronize()
@@ -696,7 +698,7 @@ class RTECEngine:
         status = hb["status"][:B].numpy().copy()
         k = int(hb["nd"][0])
         # DegreeDelta rows (vertex, old_in, new_in, old_out, new_out) as int32 [k, 5]
-        deltas = np.stack([h[:k].numpy() for h in hb["d"]], axis=1) if k else np.zeros((0, 5), np.int32)
+        deltas = hb["d"][:k].numpy().copy() if k else np.zeros((0, 5), np.int32)
         m = self._metrics_from(hb["ctr"], mode)
         changed = self._changed_final(mode, m)
         if mode in ("inc", "uer") and self.refresh_every:
