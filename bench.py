@@ -268,10 +268,11 @@ def run_ours(args, world, rank, local):
     dev = torch.device("cuda", local)
     K, W = args.steps, args.warmup
     E2E = args.e2e_steps if args.e2e_steps is not None else min(K, 10)
+    E2W = 2 if E2E else 0  # untimed warm-up calls of the public step() (pinned result buffers, allocator)
     PROF = min(K, 10)  # eager profiled pass after the timed region (per-kernel CUDA events)
     NB = 0 if (world > 1 or args.no_baselines) else 3  # batches per GPU baseline mode (UER, Full, NS)
     t0 = time.time()
-    stream, batches, X = make_workload(wl, W + K + PROF + E2E + 3 * NB, dev)
+    stream, batches, X = make_workload(wl, W + K + PROF + E2W + E2E + 3 * NB, dev)
     bs, bd, bt = stream.base()
     bundle = P.make_bundle(wl["model"], wl["dims"], heads=wl["heads"])
     sharded = world > 1
@@ -365,8 +366,13 @@ def run_ours(args, world, rank, local):
     # --- e2e through the public API from pinned host memory
     e2e_ms, h2d, d2h = [], 0, 0
     e2e_upd = 0
-    for j in range(E2E):
+    for j in range(E2W):  # warm the public path once (first-call allocations), untimed
         op, s, d, t = batches[W + K + PROF + j]
+        eng.step(*[torch.from_numpy(np.ascontiguousarray(a, dt)).pin_memory()
+                   for a, dt in ((op, np.uint8), (s, np.int32), (d, np.int32), (t, np.int64))])
+    torch.cuda.synchronize()
+    for j in range(E2E):
+        op, s, d, t = batches[W + K + PROF + E2W + j]
         hb = [torch.from_numpy(np.ascontiguousarray(a, dt)).pin_memory()
               for a, dt in ((op, np.uint8), (s, np.int32), (d, np.int32), (t, np.int64))]
         torch.cuda.synchronize()
@@ -392,7 +398,7 @@ def run_ours(args, world, rank, local):
     for bi, mode in enumerate(("uer", "full", "ns")[: 3 if NB else 0]):
         ms, ups, acc = [], 0, 0
         for j in range(NB):
-            op, s, d, t = batches[W + K + PROF + E2E + bi * NB + j]
+            op, s, d, t = batches[W + K + PROF + E2W + E2E + bi * NB + j]
             hb = [torch.from_numpy(np.ascontiguousarray(a, dt)).pin_memory()
                   for a, dt in ((op, np.uint8), (s, np.int32), (d, np.int32), (t, np.int64))]
             torch.cuda.synchronize()
@@ -479,6 +485,7 @@ def run_ours(args, world, rank, local):
         "data": "synthetic (seeded Chung-Lu graph, U(-1,1) features, make_bundle seed-0 weights)",
         "config": bench_config(args, wl, world),
         "e2e": {"value": round(e2e_val, 1) if e2e_val else None, "unit": "edge updates/s", "steps": E2E,
+                "warmup": E2W,
                 "h2d_bytes_per_step": h2d // max(E2E, 1), "d2h_bytes_per_step": d2h // max(E2E, 1),
                 "p50_batch_ms": round(statistics.median(e2e_ms), 4) if e2e_ms else None,
                 "batch_ms": [round(x, 3) for x in e2e_ms]},
