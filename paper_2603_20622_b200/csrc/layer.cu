@@ -1400,52 +1400,18 @@ __device__ __forceinline__ int chunk_head(int k, int dh) {
 
 struct GatEdgeState {
   float elh[kHMax];  // el_v per head (destination half of the logit)
+  bool fa;           // factored attention deltas usable at this destination (|el_v| < kFaMax)
 };
+
+// factored path only where the split exponentials stay far from fp32 overflow
+constexpr float kFaMax = 40.f;
 
 // contributions of in-run positions [e0, e1) of v: all edges (recompute) or the
 // ValueChange edges (sources in S(l), edge not inserted) -> acc, cacc
-// Row ring of a warp (GAT passes on 16-byte rows of at most 256 floats): kGD slots of
-// (new, old) Z rows in shared memory.  Every lane copies its own 16-byte chunks of a row
-// with cp.async (LDGSTS, one commit group per edge) and later reads back exactly those
-// chunks, so no cross-lane synchronisation is needed; a warp keeps kGD edges' rows in
-// flight without holding them in registers.  The ring also holds the warp's attention table.
-constexpr int kGD = 3;
-struct GatRing {
-  float* rows;     // [kGD][2][rw]
-  float (*att)[32][kHMax + 1];  // [2][32][kHMax + 1]
-  int rw;
-};
 template <int VEC, int K>
-__host__ __device__ constexpr int gat_ring_rw() { return 32 * VEC * K; }
-template <int VEC, int K>
-constexpr size_t gat_ring_warp_bytes() {
-  return static_cast<size_t>(kGD) * 2 * gat_ring_rw<VEC, K>() * 4 + 2 * 32 * (kHMax + 1) * 4;
-}
-
-// warp's slice of the dynamic shared memory
-template <int VEC, int K>
-__device__ __forceinline__ GatRing gat_ring_init() {
-  extern __shared__ __align__(128) uint8_t s_dyn[];
-  const int wib = threadIdx.x >> 5;
-  uint8_t* base = s_dyn + static_cast<size_t>(wib) * ((gat_ring_warp_bytes<VEC, K>() + 127) & ~size_t(127));
-  GatRing r;
-  r.rw = gat_ring_rw<VEC, K>();
-  r.rows = reinterpret_cast<float*>(base);
-  r.att = reinterpret_cast<float(*)[32][kHMax + 1]>(base + static_cast<size_t>(kGD) * 2 * r.rw * 4);
-  return r;
-}
-
-// wait until at most `pending` of this thread's newest cp.async groups are in flight
-__device__ __forceinline__ void cp_async_wait_pending(int pending) {
-  if (pending <= 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
-  else if (pending == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
-  else asm volatile("cp.async.wait_group 2;" ::: "memory");
-}
-
-template <int VEC, int K, bool RING>
 __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState& es, int64_t beg, int32_t e0,
                                           int32_t e1, int64_t p, int64_t q, bool all, RowAcc<VEC, K>& acc,
-                                          float (&cacc)[K], GatRing* ring) {
+                                          float (&cacc)[K]) {
   using R = RowAcc<VEC, K>;
   const int d = a.L.d_out, H = a.L.heads, dh = d / H;
   const int lane = lane_id();
@@ -1453,9 +1419,9 @@ __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState
   // all heads (same inputs and expf as before), into a per-warp shared-memory table;
   // the gather loop then reads the head of its own columns from it (one LDS per chunk
   // instead of an er load + expf per lane per edge, no per-head register arrays).
-  __shared__ float s_att[RING ? 1 : kLBlk / 32][2][32][kHMax + 1];
-  float(*an)[kHMax + 1] = RING ? ring->att[0] : s_att[RING ? 0 : threadIdx.x >> 5][0];
-  float(*ao)[kHMax + 1] = RING ? ring->att[1] : s_att[RING ? 0 : threadIdx.x >> 5][1];
+  __shared__ float s_att[kLBlk / 32][2][32][kHMax + 1];
+  float(*an)[kHMax + 1] = s_att[threadIdx.x >> 5][0];
+  float(*ao)[kHMax + 1] = s_att[threadIdx.x >> 5][1];
   int hk[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) hk[k] = R::has(k, d) ? chunk_head<VEC>(k, dh) : 0;
@@ -1473,74 +1439,65 @@ __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState
     unsigned m = __ballot_sync(0xffffffffu, hit);
     if (!m) continue;
     if (hit) {
+      if (all) {
 #pragma unroll
-      for (int h = 0; h < kHMax; ++h)
-        if (h < H) {
-          an[lane][h] = expf(leaky02(es.elh[h] + __ldg(a.st.er + static_cast<int64_t>(u) * H + h)));
-          if (!all) ao[lane][h] = expf(leaky02(es.elh[h] + __ldg(a.st.er_log + static_cast<int64_t>(sl) * H + h)));
-        }
+        for (int h = 0; h < kHMax; ++h)
+          if (h < H) an[lane][h] = expf(leaky02(es.elh[h] + __ldg(a.st.er + static_cast<int64_t>(u) * H + h)));
+      } else {
+        const float* ernp = a.st.er + static_cast<int64_t>(u) * H;
+        const float* erop = a.st.er_log + static_cast<int64_t>(sl) * H;
+        bool fa = VEC == 4 && es.fa;
+        // same piece of leaky_0.2 for the new and the old logit, no overflow risk (the logits
+        // are re-read below instead of held in per-head registers)
+#pragma unroll
+        for (int h = 0; h < kHMax; ++h)
+          if (h < H) {
+            const float xn = __ldg(ernp + h), xo = __ldg(erop + h);
+            if (fabsf(xn) >= kFaMax || fabsf(xo) >= kFaMax || ((es.elh[h] + xn) < 0.f) != ((es.elh[h] + xo) < 0.f))
+              fa = false;
+          }
+#pragma unroll
+        for (int h = 0; h < kHMax; ++h)
+          if (h < H) {
+            const float xn = es.elh[h] + __ldg(ernp + h);
+            if (fa) {  // an = F_p(v), ao = p
+              const bool neg = xn < 0.f;
+              an[lane][h] = expf(neg ? 0.2f * es.elh[h] : es.elh[h]);
+              ao[lane][h] = neg ? 1.f : 0.f;
+            } else {
+              an[lane][h] = expf(leaky02(xn));
+              ao[lane][h] = expf(leaky02(es.elh[h] + __ldg(erop + h)));
+            }
+          }
+        ao[lane][kHMax] = fa ? 1.f : 0.f;
+      }
     }
     __syncwarp();
-    if constexpr (RING) {
-      static_assert(VEC == 4 && K <= 2, "ring rows are 16-byte chunks of at most 256 floats");
-      {
-        // pipelined: the rows of up to kGD hits are in flight (cp.async into the ring);
-        // hits are consumed in edge order (same sums as the register path)
-        static_assert(kGD == 3, "cp_async_wait_pending covers up to 2 newer groups");
-        unsigned mi = m;  // hits still to issue
-        int slot_i = 0, slot_c = 0, inflight = 0;
-        auto issue = [&]() {
-          const int src = __ffs(mi) - 1;
-          mi &= mi - 1;
-          const int32_t uu = __shfl_sync(0xffffffffu, u, src);
-          const int32_t ss = __shfl_sync(0xffffffffu, sl, src);
-          float* dst = ring->rows + static_cast<int64_t>(slot_i) * 2 * ring->rw;
-          const float* zr = a.st.Z + static_cast<int64_t>(uu) * d;
-          const float* zl = a.st.Z_log + static_cast<int64_t>(ss) * d;
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            const int c = (lane + 32 * k) * VEC;
-            if (c < d) {
-              cp_async16(dst + c, zr + c);
-              if (!all) cp_async16(dst + ring->rw + c, zl + c);
-            }
-          }
-          cp_async_commit();
-          ++inflight;
-          slot_i = slot_i + 1 == kGD ? 0 : slot_i + 1;
-        };
-        for (int k = 0; k < kGD && mi; ++k) issue();
-        while (m) {
-          const int src = __ffs(m) - 1;
-          m &= m - 1;
-          cp_async_wait_pending(inflight - 1);  // this hit's group (the oldest) has landed
-          --inflight;
-          const float* zr = ring->rows + static_cast<int64_t>(slot_c) * 2 * ring->rw;
-          float zn[K][VEC], zo[K][VEC];
-          R::from_stage_sync(zr, d, zn);
-          if (!all) R::from_stage_sync(zr + ring->rw, d, zo);
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            const float wn = an[src][hk[k]];
-            const float wo = all ? 0.f : ao[src][hk[k]];
-            cacc[k] += all ? wn : wn - wo;
-#pragma unroll
-            for (int jj = 0; jj < VEC; ++jj) {
-              float x = wn * zn[k][jj];
-              if (!all) x = fmaf(-wo, zo[k][jj], x);
-              acc.v[k][jj] += x;
-            }
-          }
-          if (mi) issue();  // refill the consumed slot (this lane's chunks only: no hazard)
-          slot_c = slot_c + 1 == kGD ? 0 : slot_c + 1;
-        }
-      }
-    } else {
+    {
       while (m) {
         const int src = __ffs(m) - 1;
         m &= m - 1;
         const int32_t uu = __shfl_sync(0xffffffffu, u, src);
         const int32_t ss = __shfl_sync(0xffffffffu, sl, src);
+        if constexpr (VEC == 4) {
+          if (!all && ao[src][kHMax] != 0.f) {
+            // factored: one row per edge, chunk k from its head's piece row of the source's slot
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              if (!R::has(k, d)) continue;
+              const int pc = static_cast<int>(ao[src][hk[k]]);
+              const float c = an[src][hk[k]];
+              const int64_t rw = static_cast<int64_t>(ss) * 2 + pc;
+              const float4 x = __ldg(reinterpret_cast<const float4*>(a.st.gat_drow + rw * d) + (lane + 32 * k));
+              cacc[k] = fmaf(c, __ldg(a.st.gat_da + rw * H + hk[k]), cacc[k]);
+              acc.v[k][0] = fmaf(c, x.x, acc.v[k][0]);
+              acc.v[k][1] = fmaf(c, x.y, acc.v[k][1]);
+              acc.v[k][2] = fmaf(c, x.z, acc.v[k][2]);
+              acc.v[k][3] = fmaf(c, x.w, acc.v[k][3]);
+            }
+            continue;
+          }
+        }
         float zn[K][VEC], zo[K][VEC];
         R::load(a.st.Z + static_cast<int64_t>(uu) * d, d, zn);
         if (!all) R::load(a.st.Z_log + static_cast<int64_t>(ss) * d, d, zo);
@@ -1602,8 +1559,12 @@ __device__ __forceinline__ void gat_struct(const LayerArgs& a, const GatEdgeStat
 template <int VEC, int K>
 __device__ __forceinline__ void gat_state(const LayerArgs& a, int32_t v, GatEdgeState& es) {
   const int H = a.L.heads;
+  es.fa = a.st.gat_drow != nullptr && a.prev_bm_dst != nullptr;
 #pragma unroll
-  for (int h = 0; h < kHMax; ++h) es.elh[h] = h < H ? __ldg(a.st.el + static_cast<int64_t>(v) * H + h) : 0.f;
+  for (int h = 0; h < kHMax; ++h) {
+    es.elh[h] = h < H ? __ldg(a.st.el + static_cast<int64_t>(v) * H + h) : 0.f;
+    if (fabsf(es.elh[h]) >= kFaMax) es.fa = false;
+  }
 }
 
 // S / ctx update, zero-in-degree rule, DeltaLog, h = elu(S / ctx) (models.py:280-282)
@@ -1663,16 +1624,10 @@ __device__ __forceinline__ void gat_finalize(const LayerArgs& a, int64_t i, int3
 // 6 CTAs / SM (42 registers, spills): the GAT passes are latency-bound on their row
 // gathers and the two streams' passes co-reside, so occupancy wins -- measured c3-gat
 // p50 3 CTAs 16.4 ms, 4 CTAs 14.7, 5 CTAs 14.55, 6 CTAs 14.1
-template <int VEC, int K, bool FULL, bool RING = false>
-__global__ void __launch_bounds__(kLBlk, RING ? 3 : 6) k_gat_light(LayerArgs a, AggRows rows) {
+template <int VEC, int K, bool FULL>
+__global__ void __launch_bounds__(kLBlk, 6) k_gat_light(LayerArgs a, AggRows rows) {
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
-  GatRing rg_{};
-  GatRing* ring = nullptr;
-  if constexpr (RING) {
-    rg_ = gat_ring_init<VEC, K>();
-    ring = &rg_;
-  }
   const int64_t nr = rows.count();
   const bool scan = FULL || *a.f.n_src > 0;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -1697,22 +1652,16 @@ __global__ void __launch_bounds__(kLBlk, RING ? 3 : 6) k_gat_light(LayerArgs a, 
     float cacc[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) cacc[k] = 0.f;
-    if (scan) gat_edges<VEC, K, RING>(a, es, a.g.in.beg[v], 0, len, p, q, recompute, acc, cacc, ring);
+    if (scan) gat_edges<VEC, K>(a, es, a.g.in.beg[v], 0, len, p, q, recompute, acc, cacc);
     if (!recompute) gat_struct<VEC, K>(a, es, p, q, acc, cacc);
     gat_finalize<VEC, K, FULL>(a, i, v, len, recompute, acc, cacc);
   }
 }
 
-template <int VEC, int K, bool FULL, bool RING = false>
-__global__ void __launch_bounds__(kLBlk, RING ? 3 : 6) k_gat_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
+template <int VEC, int K, bool FULL>
+__global__ void __launch_bounds__(kLBlk, 6) k_gat_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
-  GatRing rg_{};
-  GatRing* ring = nullptr;
-  if constexpr (RING) {
-    rg_ = gat_ring_init<VEC, K>();
-    ring = &rg_;
-  }
   const int64_t nh = *hp.n_heavy;
   if (nh == 0) return;
   const int64_t T = hp.hoff[nh];
@@ -1746,7 +1695,7 @@ __global__ void __launch_bounds__(kLBlk, RING ? 3 : 6) k_gat_heavy(LayerArgs a, 
 #pragma unroll
     for (int k = 0; k < K; ++k) cacc[k] = 0.f;
     int32_t e0 = c * kChunk, e1 = min(len, e0 + kChunk);
-    gat_edges<VEC, K, RING>(a, es, a.g.in.beg[v], e0, e1, p, q, recompute, acc, cacc, ring);
+    gat_edges<VEC, K>(a, es, a.g.in.beg[v], e0, e1, p, q, recompute, acc, cacc);
     if (!recompute && c == 0) gat_struct<VEC, K>(a, es, p, q, acc, cacc);
     float* part = hp.part + t * pw;
     acc.store(part, d);
@@ -1778,39 +1727,9 @@ __global__ void __launch_bounds__(kLBlk, RING ? 3 : 6) k_gat_heavy(LayerArgs a, 
   }
 }
 
-// RTEC_GAT_RING env: 1 cp.async row ring for rows of <= 256 floats, 0 (default) register
-// path.  Measured on c3-gat (profiles/r02g_gat_ring_ab.md): a ring filled by 1 KB bulk
-// copies (cp.async.bulk, one lane, mbarriers) ran the GAT stage at 8.2 ms per layer launch
-// against 6.2 ms for 6 CTAs / SM of register gathers
-static bool gat_ring_on() {
-  static int r = -1;
-  if (r < 0) {
-    const char* e = getenv("RTEC_GAT_RING");
-    r = e ? atoi(e) : 0;
-  }
-  return r != 0;
-}
-
 template <int VEC, int K, bool FULL>
 static int launch_gat_passes(const LayerArgs& a, AggRows rows, const HeavyPlan& hp, int grid, cudaStream_t s,
                              cudaStream_t hs) {
-  if constexpr (VEC == 4 && K <= 2) {
-    if (gat_ring_on()) {
-      const size_t smem = ((gat_ring_warp_bytes<VEC, K>() + 127) & ~size_t(127)) * (kLBlk / 32);
-      static bool attr[kMaxDevices] = {};  // a function attribute is per device
-      const int dev = cur_device();
-      if (!attr[dev]) {
-        RTEC_CUDA(cudaFuncSetAttribute(k_gat_heavy<VEC, K, FULL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem)));
-        RTEC_CUDA(cudaFuncSetAttribute(k_gat_light<VEC, K, FULL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem)));
-        attr[dev] = true;
-      }
-      k_gat_heavy<VEC, K, FULL, true><<<grid, kLBlk, smem, hs>>>(a, rows, hp);
-      k_gat_light<VEC, K, FULL, true><<<grid, kLBlk, smem, s>>>(a, rows);
-      return RTEC_OK;
-    }
-  }
   k_gat_heavy<VEC, K, FULL><<<grid, kLBlk, 0, hs>>>(a, rows, hp);
   k_gat_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows);
   return RTEC_OK;
@@ -1867,6 +1786,43 @@ static int launch_gat(LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_
   }
   RTEC_LAUNCH_CHECK("k_gat");
   return RTEC_OK;
+}
+
+// factored attention deltas of the V_chg(l-1) slots (rtec_state_t.gat_drow / gat_da): per
+// slot i (source u = rows[i]) and piece p (exponent slope 1 or 0.2), per head h:
+//   drow[i][p] = e^{s_p er_new(u)_h} Z_new(u) - e^{s_p er_old_h} Z_old(u),  da[i][p][h] = the two exps' difference
+__global__ void k_gat_delta(const float* __restrict__ Z, const float* __restrict__ Z_log, const float* __restrict__ er,
+                            const float* __restrict__ er_log, const int32_t* __restrict__ rows, const int64_t* n_rows,
+                            int d, int H, float* drow, float* da, const uint64_t* err) {
+  if (err_set(err)) return;
+  const int64_t nr = *n_rows;
+  const int dh = d / H;
+  const int lane = lane_id();
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < nr; i += nw) {
+    const int32_t u = rows[i];
+    const float* zn = Z + static_cast<int64_t>(u) * d;
+    const float* zo = Z_log + i * d;
+    float* d0 = drow + (i * 2) * d;
+    float* d1 = d0 + d;
+    for (int c = lane * 4; c < d; c += 128) {
+      const int h = c / dh;
+      const float ern = __ldg(er + static_cast<int64_t>(u) * H + h), ero = __ldg(er_log + i * H + h);
+      const float a0n = expf(ern), a0o = expf(ero), a1n = expf(0.2f * ern), a1o = expf(0.2f * ero);
+      const float4 n4 = __ldg(reinterpret_cast<const float4*>(zn + c));
+      const float4 o4 = __ldg(reinterpret_cast<const float4*>(zo + c));
+      *reinterpret_cast<float4*>(d0 + c) = make_float4(a0n * n4.x - a0o * o4.x, a0n * n4.y - a0o * o4.y,
+                                                       a0n * n4.z - a0o * o4.z, a0n * n4.w - a0o * o4.w);
+      *reinterpret_cast<float4*>(d1 + c) = make_float4(a1n * n4.x - a1o * o4.x, a1n * n4.y - a1o * o4.y,
+                                                       a1n * n4.z - a1o * o4.z, a1n * n4.w - a1o * o4.w);
+    }
+    if (lane < H) {
+      const float ern = __ldg(er + static_cast<int64_t>(u) * H + lane), ero = __ldg(er_log + i * H + lane);
+      da[(i * 2) * H + lane] = expf(ern) - expf(ero);
+      da[(i * 2 + 1) * H + lane] = expf(0.2f * ern) - expf(0.2f * ero);
+    }
+  }
 }
 
 // el / er for projected rows: el = a[:dh]·z_h, er = a[dh:]·z_h per head
@@ -2172,8 +2128,21 @@ int rtec_layer_incremental(const rtec_graph_t* g, const rtec_batch_t* b, const r
   a.prev_slot = prev ? (prev->chg_slot ? prev->chg_slot : prev->dst_slot) : nullptr;
   a.err = err;
   const int grid = kSMs * 8;
-  if (L->model == RTEC_MODEL_GAT)
+  if (L->model == RTEC_MODEL_GAT) {
+    // factored attention deltas of the changed sources (unsharded, 16-byte rows)
+    const bool fa = st->gat_drow && st->gat_da && prev && !prev->bm_chg && st->Z_log && st->er_log &&
+                    L->d_out % 4 == 0 && (L->d_out / L->heads) % 4 == 0;
+    if (fa) {
+      RTEC_PROF("k_gat_delta", s);
+      k_gat_delta<<<kSMs * 8, kLBlk, 0, s>>>(st->Z, st->Z_log, st->er, st->er_log, prev->dst_list, prev->n_dst,
+                                             L->d_out, L->heads, st->gat_drow, st->gat_da, err);
+      RTEC_LAUNCH_CHECK("k_gat_delta");
+    } else {
+      a.st.gat_drow = nullptr;
+      a.st.gat_da = nullptr;
+    }
     return launch_gat<false>(a, AggRows{f->dst_list, f->n_dst, n}, n, g->in.slots, w, s);
+  }
   layer_args_init(a, L, st);
   if (L->model == RTEC_MODEL_GIN_MAX) {
     RTEC_TRY(launch_max<false>(a, AggRows{f->dst_list, f->n_dst, n}, n, g->in.slots, w, s));
