@@ -1,0 +1,10 @@
+# factored GAT deltas (RTEC_GAT_FA): parity tests, then A/B on c3-gat
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_engine_gpu.py tests/test_parity_configs_gpu.py tests/test_api_gpu.py -q -x -k "gat or golden or drift or edge" > gpurun_out/pytest_fa.log 2>&1; echo "pytest_rc=$?"; tail -3 gpurun_out/pytest_fa.log
+grep -h "gat" gpurun_out/parity_report.jsonl 2>/dev/null | head -5
+rm -f gpurun_out/ab_fa.txt
+for x in 1 0 1 0; do
+  RTEC_GAT_FA=$x timeout 400 python bench.py --workload c3-gat --steps 10 --warmup 3 --no-cpu-baseline --no-baselines --no-parity --e2e-steps 3 > gpurun_out/ab_fa_$x.json 2>/dev/null
+  python -c "import json;r=json.load(open('gpurun_out/ab_fa_$x.json'));k=r['kernels'];g=lambda n: k.get(n,{}).get('ms_per_launch');print('c3-gat fa=$x', r['p50_batch_ms'], 'gat', g('k_gat_layer'), 'delta', g('k_gat_delta'))" >> gpurun_out/ab_fa.txt
+done
+cat gpurun_out/ab_fa.txt
