@@ -1408,7 +1408,7 @@ constexpr float kFaMax = 40.f;
 
 // contributions of in-run positions [e0, e1) of v: all edges (recompute) or the
 // ValueChange edges (sources in S(l), edge not inserted) -> acc, cacc
-template <int VEC, int K>
+template <int VEC, int K, bool FA>
 __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState& es, int64_t beg, int32_t e0,
                                           int32_t e1, int64_t p, int64_t q, bool all, RowAcc<VEC, K>& acc,
                                           float (&cacc)[K]) {
@@ -1439,14 +1439,21 @@ __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState
     unsigned m = __ballot_sync(0xffffffffu, hit);
     if (!m) continue;
     if (hit) {
-      if (all) {
+      if (!FA) {
+#pragma unroll
+        for (int h = 0; h < kHMax; ++h)
+          if (h < H) {
+            an[lane][h] = expf(leaky02(es.elh[h] + __ldg(a.st.er + static_cast<int64_t>(u) * H + h)));
+            if (!all) ao[lane][h] = expf(leaky02(es.elh[h] + __ldg(a.st.er_log + static_cast<int64_t>(sl) * H + h)));
+          }
+      } else if (all) {
 #pragma unroll
         for (int h = 0; h < kHMax; ++h)
           if (h < H) an[lane][h] = expf(leaky02(es.elh[h] + __ldg(a.st.er + static_cast<int64_t>(u) * H + h)));
       } else {
         const float* ernp = a.st.er + static_cast<int64_t>(u) * H;
         const float* erop = a.st.er_log + static_cast<int64_t>(sl) * H;
-        bool fa = VEC == 4 && es.fa;
+        bool fa = es.fa;
         // same piece of leaky_0.2 for the new and the old logit, no overflow risk (the logits
         // are re-read below instead of held in per-head registers)
 #pragma unroll
@@ -1479,7 +1486,7 @@ __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState
         m &= m - 1;
         const int32_t uu = __shfl_sync(0xffffffffu, u, src);
         const int32_t ss = __shfl_sync(0xffffffffu, sl, src);
-        if constexpr (VEC == 4) {
+        if constexpr (FA && VEC == 4) {
           if (!all && ao[src][kHMax] != 0.f) {
             // factored: one row per edge, chunk k from its head's piece row of the source's slot
 #pragma unroll
@@ -1624,7 +1631,7 @@ __device__ __forceinline__ void gat_finalize(const LayerArgs& a, int64_t i, int3
 // 6 CTAs / SM (42 registers, spills): the GAT passes are latency-bound on their row
 // gathers and the two streams' passes co-reside, so occupancy wins -- measured c3-gat
 // p50 3 CTAs 16.4 ms, 4 CTAs 14.7, 5 CTAs 14.55, 6 CTAs 14.1
-template <int VEC, int K, bool FULL>
+template <int VEC, int K, bool FULL, bool FA = false>
 __global__ void __launch_bounds__(kLBlk, 6) k_gat_light(LayerArgs a, AggRows rows) {
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
@@ -1652,13 +1659,13 @@ __global__ void __launch_bounds__(kLBlk, 6) k_gat_light(LayerArgs a, AggRows row
     float cacc[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) cacc[k] = 0.f;
-    if (scan) gat_edges<VEC, K>(a, es, a.g.in.beg[v], 0, len, p, q, recompute, acc, cacc);
+    if (scan) gat_edges<VEC, K, FA>(a, es, a.g.in.beg[v], 0, len, p, q, recompute, acc, cacc);
     if (!recompute) gat_struct<VEC, K>(a, es, p, q, acc, cacc);
     gat_finalize<VEC, K, FULL>(a, i, v, len, recompute, acc, cacc);
   }
 }
 
-template <int VEC, int K, bool FULL>
+template <int VEC, int K, bool FULL, bool FA = false>
 __global__ void __launch_bounds__(kLBlk, 6) k_gat_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
@@ -1695,7 +1702,7 @@ __global__ void __launch_bounds__(kLBlk, 6) k_gat_heavy(LayerArgs a, AggRows row
 #pragma unroll
     for (int k = 0; k < K; ++k) cacc[k] = 0.f;
     int32_t e0 = c * kChunk, e1 = min(len, e0 + kChunk);
-    gat_edges<VEC, K>(a, es, a.g.in.beg[v], e0, e1, p, q, recompute, acc, cacc);
+    gat_edges<VEC, K, FA>(a, es, a.g.in.beg[v], e0, e1, p, q, recompute, acc, cacc);
     if (!recompute && c == 0) gat_struct<VEC, K>(a, es, p, q, acc, cacc);
     float* part = hp.part + t * pw;
     acc.store(part, d);
@@ -1730,6 +1737,11 @@ __global__ void __launch_bounds__(kLBlk, 6) k_gat_heavy(LayerArgs a, AggRows row
 template <int VEC, int K, bool FULL>
 static int launch_gat_passes(const LayerArgs& a, AggRows rows, const HeavyPlan& hp, int grid, cudaStream_t s,
                              cudaStream_t hs) {
+  if (!FULL && VEC == 4 && a.st.gat_drow) {  // factored attention deltas of this layer
+    k_gat_heavy<VEC, K, FULL, true><<<grid, kLBlk, 0, hs>>>(a, rows, hp);
+    k_gat_light<VEC, K, FULL, true><<<grid, kLBlk, 0, s>>>(a, rows);
+    return RTEC_OK;
+  }
   k_gat_heavy<VEC, K, FULL><<<grid, kLBlk, 0, hs>>>(a, rows, hp);
   k_gat_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows);
   return RTEC_OK;

@@ -1,7 +1,11 @@
-# factored GAT deltas (RTEC_GAT_FA): parity tests, then A/B on c3-gat
+# factored GAT deltas (RTEC_GAT_FA): parity tests with it off and on (report lines), then A/B on c3-gat
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_engine_gpu.py tests/test_parity_configs_gpu.py tests/test_api_gpu.py -q -x -k "gat or golden or drift or edge" > gpurun_out/pytest_fa.log 2>&1; echo "pytest_rc=$?"; tail -3 gpurun_out/pytest_fa.log
-grep -h "gat" gpurun_out/parity_report.jsonl 2>/dev/null | head -5
+for x in 0 1; do
+  rm -f gpurun_out/parity_report.jsonl
+  RTEC_GAT_FA=$x timeout 900 python -m pytest tests/test_parity_configs_gpu.py -q -x -k "gat" > gpurun_out/pytest_fa_$x.log 2>&1; echo "pytest_fa$x rc=$?"; tail -1 gpurun_out/pytest_fa_$x.log
+  grep -h '"c3-gat-shape"' gpurun_out/parity_report.jsonl | python -c "import json,sys;[print('fa=$x', json.loads(l)['worst']) for l in sys.stdin]"
+done
+timeout 900 python -m pytest tests/test_engine_gpu.py tests/test_api_gpu.py -q -x -k "gat or golden or drift or edge" > gpurun_out/pytest_fa.log 2>&1; echo "pytest_rc=$?"; tail -1 gpurun_out/pytest_fa.log
 rm -f gpurun_out/ab_fa.txt
 for x in 1 0 1 0; do
   RTEC_GAT_FA=$x timeout 400 python bench.py --workload c3-gat --steps 10 --warmup 3 --no-cpu-baseline --no-baselines --no-parity --e2e-steps 3 > gpurun_out/ab_fa_$x.json 2>/dev/null
