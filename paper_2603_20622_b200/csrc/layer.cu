@@ -1463,20 +1463,23 @@ __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState
             if (fabsf(xn) >= kFaMax || fabsf(xo) >= kFaMax || ((es.elh[h] + xn) < 0.f) != ((es.elh[h] + xo) < 0.f))
               fa = false;
           }
+        int pmask = 0;
 #pragma unroll
         for (int h = 0; h < kHMax; ++h)
           if (h < H) {
             const float xn = es.elh[h] + __ldg(ernp + h);
-            if (fa) {  // an = F_p(v), ao = p
-              const bool neg = xn < 0.f;
-              an[lane][h] = expf(neg ? 0.2f * es.elh[h] : es.elh[h]);
-              ao[lane][h] = neg ? 1.f : 0.f;
+            if (fa) {  // an = F_p(v), ao = F_p(v) (A_p(new) - A_p(old)): the context increment
+              const int pc = xn < 0.f ? 1 : 0;
+              const float c = expf(pc ? 0.2f * es.elh[h] : es.elh[h]);
+              an[lane][h] = c;
+              ao[lane][h] = c * __ldg(a.st.gat_da + (static_cast<int64_t>(sl) * 2 + pc) * H + h);
+              pmask |= pc << h;
             } else {
               an[lane][h] = expf(leaky02(xn));
               ao[lane][h] = expf(leaky02(es.elh[h] + __ldg(erop + h)));
             }
           }
-        ao[lane][kHMax] = fa ? 1.f : 0.f;
+        ao[lane][kHMax] = fa ? static_cast<float>(1 + pmask) : 0.f;  // 0: two-row edge; else 1 + piece mask
       }
     }
     __syncwarp();
@@ -1487,16 +1490,18 @@ __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState
         const int32_t uu = __shfl_sync(0xffffffffu, u, src);
         const int32_t ss = __shfl_sync(0xffffffffu, sl, src);
         if constexpr (FA && VEC == 4) {
-          if (!all && ao[src][kHMax] != 0.f) {
+          const float fm = ao[src][kHMax];
+          if (!all && fm != 0.f) {
             // factored: one row per edge, chunk k from its head's piece row of the source's slot
+            const int pmask = static_cast<int>(fm) - 1;
 #pragma unroll
             for (int k = 0; k < K; ++k) {
               if (!R::has(k, d)) continue;
-              const int pc = static_cast<int>(ao[src][hk[k]]);
+              const int pc = (pmask >> hk[k]) & 1;
               const float c = an[src][hk[k]];
               const int64_t rw = static_cast<int64_t>(ss) * 2 + pc;
               const float4 x = __ldg(reinterpret_cast<const float4*>(a.st.gat_drow + rw * d) + (lane + 32 * k));
-              cacc[k] = fmaf(c, __ldg(a.st.gat_da + rw * H + hk[k]), cacc[k]);
+              cacc[k] += ao[src][hk[k]];
               acc.v[k][0] = fmaf(c, x.x, acc.v[k][0]);
               acc.v[k][1] = fmaf(c, x.y, acc.v[k][1]);
               acc.v[k][2] = fmaf(c, x.z, acc.v[k][2]);
