@@ -284,7 +284,9 @@ __global__ void __launch_bounds__(512, 1) k_gemm_tc(TcArgs g, TcShape sh) {
         float4 x = raw[idx];
         float4 hv = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
         hi[idx] = hv;
-        raw[idx] = make_float4(x.x - hv.x, x.y - hv.y, x.z - hv.z, x.w - hv.w);
+        // lo rounded to tf32 too (the MMA would truncate it): half an ulp of the residual
+        raw[idx] = make_float4(tf32_rna(x.x - hv.x), tf32_rna(x.y - hv.y), tf32_rna(x.z - hv.z),
+                               tf32_rna(x.w - hv.w));
       }
       fence_proxy_async();
       mbar_arrive(a_split + sa);

@@ -1405,6 +1405,11 @@ struct GatEdgeState {
 
 // factored path only where the split exponentials stay far from fp32 overflow
 constexpr float kFaMax = 40.f;
+// resident CTAs per SM of the factored instantiation (RTEC_GAT_FA_CTAS at build time)
+#ifndef RTEC_GAT_FA_CTAS
+#define RTEC_GAT_FA_CTAS 5
+#endif
+constexpr int kGatFaCtas = RTEC_GAT_FA_CTAS;
 
 // contributions of in-run positions [e0, e1) of v: all edges (recompute) or the
 // ValueChange edges (sources in S(l), edge not inserted) -> acc, cacc
@@ -1637,7 +1642,7 @@ __device__ __forceinline__ void gat_finalize(const LayerArgs& a, int64_t i, int3
 // gathers and the two streams' passes co-reside, so occupancy wins -- measured c3-gat
 // p50 3 CTAs 16.4 ms, 4 CTAs 14.7, 5 CTAs 14.55, 6 CTAs 14.1
 template <int VEC, int K, bool FULL, bool FA = false>
-__global__ void __launch_bounds__(kLBlk, 6) k_gat_light(LayerArgs a, AggRows rows) {
+__global__ void __launch_bounds__(kLBlk, FA ? kGatFaCtas : 6) k_gat_light(LayerArgs a, AggRows rows) {
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
   const int64_t nr = rows.count();
@@ -1671,7 +1676,7 @@ __global__ void __launch_bounds__(kLBlk, 6) k_gat_light(LayerArgs a, AggRows row
 }
 
 template <int VEC, int K, bool FULL, bool FA = false>
-__global__ void __launch_bounds__(kLBlk, 6) k_gat_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
+__global__ void __launch_bounds__(kLBlk, FA ? kGatFaCtas : 6) k_gat_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
   const int64_t nh = *hp.n_heavy;
