@@ -210,15 +210,6 @@ typedef struct {
   int32_t row_div;
   int32_t out_local;
   int32_t delta_slot;
-  /* GAT factored attention deltas (layers >= 1, optional): leaky_0.2 makes the edge weight
-   * exp(leaky(el_v + er_u)) = F_p(v) A_p(u) with p = [el_v + er_u < 0], F_0 = e^el, A_0 = e^er,
-   * F_1 = e^{0.2 el}, A_1 = e^{0.2 er}.  For every V_chg(l-1) slot i (source u = previous
-   * dst_list[i]): gat_drow[i][p] = A_p(u_new) Z_new(u) - A_p(u_old) Z_old(u) per head
-   * ([slots][2][d_out]) and gat_da[i][p][h] = A_p(u_new) - A_p(u_old) ([slots][2][heads]).  A
-   * ValueChange edge whose new and old logits fall in the same piece for every head then
-   * gathers ONE row (F_p(v) * gat_drow) instead of Z_new and Z_old.  NULL: off. */
-  float* gat_drow;
-  float* gat_da;
 } rtec_state_t;
 
 /* ---- workspace ---- */

@@ -1400,20 +1400,12 @@ __device__ __forceinline__ int chunk_head(int k, int dh) {
 
 struct GatEdgeState {
   float elh[kHMax];  // el_v per head (destination half of the logit)
-  bool fa;           // factored attention deltas usable at this destination (|el_v| < kFaMax)
 };
 
-// factored path only where the split exponentials stay far from fp32 overflow
-constexpr float kFaMax = 40.f;
-// resident CTAs per SM of the factored instantiation (RTEC_GAT_FA_CTAS at build time)
-#ifndef RTEC_GAT_FA_CTAS
-#define RTEC_GAT_FA_CTAS 5
-#endif
-constexpr int kGatFaCtas = RTEC_GAT_FA_CTAS;
 
 // contributions of in-run positions [e0, e1) of v: all edges (recompute) or the
 // ValueChange edges (sources in S(l), edge not inserted) -> acc, cacc
-template <int VEC, int K, bool FA>
+template <int VEC, int K>
 __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState& es, int64_t beg, int32_t e0,
                                           int32_t e1, int64_t p, int64_t q, bool all, RowAcc<VEC, K>& acc,
                                           float (&cacc)[K]) {
@@ -1444,48 +1436,12 @@ __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState
     unsigned m = __ballot_sync(0xffffffffu, hit);
     if (!m) continue;
     if (hit) {
-      if (!FA) {
 #pragma unroll
-        for (int h = 0; h < kHMax; ++h)
-          if (h < H) {
-            an[lane][h] = expf(leaky02(es.elh[h] + __ldg(a.st.er + static_cast<int64_t>(u) * H + h)));
-            if (!all) ao[lane][h] = expf(leaky02(es.elh[h] + __ldg(a.st.er_log + static_cast<int64_t>(sl) * H + h)));
-          }
-      } else if (all) {
-#pragma unroll
-        for (int h = 0; h < kHMax; ++h)
-          if (h < H) an[lane][h] = expf(leaky02(es.elh[h] + __ldg(a.st.er + static_cast<int64_t>(u) * H + h)));
-      } else {
-        const float* ernp = a.st.er + static_cast<int64_t>(u) * H;
-        const float* erop = a.st.er_log + static_cast<int64_t>(sl) * H;
-        bool fa = es.fa;
-        // same piece of leaky_0.2 for the new and the old logit, no overflow risk (the logits
-        // are re-read below instead of held in per-head registers)
-#pragma unroll
-        for (int h = 0; h < kHMax; ++h)
-          if (h < H) {
-            const float xn = __ldg(ernp + h), xo = __ldg(erop + h);
-            if (fabsf(xn) >= kFaMax || fabsf(xo) >= kFaMax || ((es.elh[h] + xn) < 0.f) != ((es.elh[h] + xo) < 0.f))
-              fa = false;
-          }
-        int pmask = 0;
-#pragma unroll
-        for (int h = 0; h < kHMax; ++h)
-          if (h < H) {
-            const float xn = es.elh[h] + __ldg(ernp + h);
-            if (fa) {  // an = F_p(v), ao = F_p(v) (A_p(new) - A_p(old)): the context increment
-              const int pc = xn < 0.f ? 1 : 0;
-              const float c = expf(pc ? 0.2f * es.elh[h] : es.elh[h]);
-              an[lane][h] = c;
-              ao[lane][h] = c * __ldg(a.st.gat_da + (static_cast<int64_t>(sl) * 2 + pc) * H + h);
-              pmask |= pc << h;
-            } else {
-              an[lane][h] = expf(leaky02(xn));
-              ao[lane][h] = expf(leaky02(es.elh[h] + __ldg(erop + h)));
-            }
-          }
-        ao[lane][kHMax] = fa ? static_cast<float>(1 + pmask) : 0.f;  // 0: two-row edge; else 1 + piece mask
-      }
+      for (int h = 0; h < kHMax; ++h)
+        if (h < H) {
+          an[lane][h] = expf(leaky02(es.elh[h] + __ldg(a.st.er + static_cast<int64_t>(u) * H + h)));
+          if (!all) ao[lane][h] = expf(leaky02(es.elh[h] + __ldg(a.st.er_log + static_cast<int64_t>(sl) * H + h)));
+        }
     }
     __syncwarp();
     {
@@ -1494,27 +1450,6 @@ __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState
         m &= m - 1;
         const int32_t uu = __shfl_sync(0xffffffffu, u, src);
         const int32_t ss = __shfl_sync(0xffffffffu, sl, src);
-        if constexpr (FA && VEC == 4) {
-          const float fm = ao[src][kHMax];
-          if (!all && fm != 0.f) {
-            // factored: one row per edge, chunk k from its head's piece row of the source's slot
-            const int pmask = static_cast<int>(fm) - 1;
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-              if (!R::has(k, d)) continue;
-              const int pc = (pmask >> hk[k]) & 1;
-              const float c = an[src][hk[k]];
-              const int64_t rw = static_cast<int64_t>(ss) * 2 + pc;
-              const float4 x = __ldg(reinterpret_cast<const float4*>(a.st.gat_drow + rw * d) + (lane + 32 * k));
-              cacc[k] += ao[src][hk[k]];
-              acc.v[k][0] = fmaf(c, x.x, acc.v[k][0]);
-              acc.v[k][1] = fmaf(c, x.y, acc.v[k][1]);
-              acc.v[k][2] = fmaf(c, x.z, acc.v[k][2]);
-              acc.v[k][3] = fmaf(c, x.w, acc.v[k][3]);
-            }
-            continue;
-          }
-        }
         float zn[K][VEC], zo[K][VEC];
         R::load(a.st.Z + static_cast<int64_t>(uu) * d, d, zn);
         if (!all) R::load(a.st.Z_log + static_cast<int64_t>(ss) * d, d, zo);
@@ -1576,11 +1511,9 @@ __device__ __forceinline__ void gat_struct(const LayerArgs& a, const GatEdgeStat
 template <int VEC, int K>
 __device__ __forceinline__ void gat_state(const LayerArgs& a, int32_t v, GatEdgeState& es) {
   const int H = a.L.heads;
-  es.fa = a.st.gat_drow != nullptr && a.prev_bm_dst != nullptr;
 #pragma unroll
   for (int h = 0; h < kHMax; ++h) {
     es.elh[h] = h < H ? __ldg(a.st.el + static_cast<int64_t>(v) * H + h) : 0.f;
-    if (fabsf(es.elh[h]) >= kFaMax) es.fa = false;
   }
 }
 
@@ -1641,8 +1574,8 @@ __device__ __forceinline__ void gat_finalize(const LayerArgs& a, int64_t i, int3
 // 6 CTAs / SM (42 registers, spills): the GAT passes are latency-bound on their row
 // gathers and the two streams' passes co-reside, so occupancy wins -- measured c3-gat
 // p50 3 CTAs 16.4 ms, 4 CTAs 14.7, 5 CTAs 14.55, 6 CTAs 14.1
-template <int VEC, int K, bool FULL, bool FA = false>
-__global__ void __launch_bounds__(kLBlk, FA ? kGatFaCtas : 6) k_gat_light(LayerArgs a, AggRows rows) {
+template <int VEC, int K, bool FULL>
+__global__ void __launch_bounds__(kLBlk, 6) k_gat_light(LayerArgs a, AggRows rows) {
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
   const int64_t nr = rows.count();
@@ -1669,14 +1602,14 @@ __global__ void __launch_bounds__(kLBlk, FA ? kGatFaCtas : 6) k_gat_light(LayerA
     float cacc[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) cacc[k] = 0.f;
-    if (scan) gat_edges<VEC, K, FA>(a, es, a.g.in.beg[v], 0, len, p, q, recompute, acc, cacc);
+    if (scan) gat_edges<VEC, K>(a, es, a.g.in.beg[v], 0, len, p, q, recompute, acc, cacc);
     if (!recompute) gat_struct<VEC, K>(a, es, p, q, acc, cacc);
     gat_finalize<VEC, K, FULL>(a, i, v, len, recompute, acc, cacc);
   }
 }
 
-template <int VEC, int K, bool FULL, bool FA = false>
-__global__ void __launch_bounds__(kLBlk, FA ? kGatFaCtas : 6) k_gat_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
+template <int VEC, int K, bool FULL>
+__global__ void __launch_bounds__(kLBlk, 6) k_gat_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
   const int64_t nh = *hp.n_heavy;
@@ -1712,7 +1645,7 @@ __global__ void __launch_bounds__(kLBlk, FA ? kGatFaCtas : 6) k_gat_heavy(LayerA
 #pragma unroll
     for (int k = 0; k < K; ++k) cacc[k] = 0.f;
     int32_t e0 = c * kChunk, e1 = min(len, e0 + kChunk);
-    gat_edges<VEC, K, FA>(a, es, a.g.in.beg[v], e0, e1, p, q, recompute, acc, cacc);
+    gat_edges<VEC, K>(a, es, a.g.in.beg[v], e0, e1, p, q, recompute, acc, cacc);
     if (!recompute && c == 0) gat_struct<VEC, K>(a, es, p, q, acc, cacc);
     float* part = hp.part + t * pw;
     acc.store(part, d);
@@ -1747,11 +1680,6 @@ __global__ void __launch_bounds__(kLBlk, FA ? kGatFaCtas : 6) k_gat_heavy(LayerA
 template <int VEC, int K, bool FULL>
 static int launch_gat_passes(const LayerArgs& a, AggRows rows, const HeavyPlan& hp, int grid, cudaStream_t s,
                              cudaStream_t hs) {
-  if (!FULL && VEC == 4 && a.st.gat_drow) {  // factored attention deltas of this layer
-    k_gat_heavy<VEC, K, FULL, true><<<grid, kLBlk, 0, hs>>>(a, rows, hp);
-    k_gat_light<VEC, K, FULL, true><<<grid, kLBlk, 0, s>>>(a, rows);
-    return RTEC_OK;
-  }
   k_gat_heavy<VEC, K, FULL><<<grid, kLBlk, 0, hs>>>(a, rows, hp);
   k_gat_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows);
   return RTEC_OK;
@@ -1808,43 +1736,6 @@ static int launch_gat(LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_
   }
   RTEC_LAUNCH_CHECK("k_gat");
   return RTEC_OK;
-}
-
-// factored attention deltas of the V_chg(l-1) slots (rtec_state_t.gat_drow / gat_da): per
-// slot i (source u = rows[i]) and piece p (exponent slope 1 or 0.2), per head h:
-//   drow[i][p] = e^{s_p er_new(u)_h} Z_new(u) - e^{s_p er_old_h} Z_old(u),  da[i][p][h] = the two exps' difference
-__global__ void k_gat_delta(const float* __restrict__ Z, const float* __restrict__ Z_log, const float* __restrict__ er,
-                            const float* __restrict__ er_log, const int32_t* __restrict__ rows, const int64_t* n_rows,
-                            int d, int H, float* drow, float* da, const uint64_t* err) {
-  if (err_set(err)) return;
-  const int64_t nr = *n_rows;
-  const int dh = d / H;
-  const int lane = lane_id();
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp; i < nr; i += nw) {
-    const int32_t u = rows[i];
-    const float* zn = Z + static_cast<int64_t>(u) * d;
-    const float* zo = Z_log + i * d;
-    float* d0 = drow + (i * 2) * d;
-    float* d1 = d0 + d;
-    for (int c = lane * 4; c < d; c += 128) {
-      const int h = c / dh;
-      const float ern = __ldg(er + static_cast<int64_t>(u) * H + h), ero = __ldg(er_log + i * H + h);
-      const float a0n = expf(ern), a0o = expf(ero), a1n = expf(0.2f * ern), a1o = expf(0.2f * ero);
-      const float4 n4 = __ldg(reinterpret_cast<const float4*>(zn + c));
-      const float4 o4 = __ldg(reinterpret_cast<const float4*>(zo + c));
-      *reinterpret_cast<float4*>(d0 + c) = make_float4(a0n * n4.x - a0o * o4.x, a0n * n4.y - a0o * o4.y,
-                                                       a0n * n4.z - a0o * o4.z, a0n * n4.w - a0o * o4.w);
-      *reinterpret_cast<float4*>(d1 + c) = make_float4(a1n * n4.x - a1o * o4.x, a1n * n4.y - a1o * o4.y,
-                                                       a1n * n4.z - a1o * o4.z, a1n * n4.w - a1o * o4.w);
-    }
-    if (lane < H) {
-      const float ern = __ldg(er + static_cast<int64_t>(u) * H + lane), ero = __ldg(er_log + i * H + lane);
-      da[(i * 2) * H + lane] = expf(ern) - expf(ero);
-      da[(i * 2 + 1) * H + lane] = expf(0.2f * ern) - expf(0.2f * ero);
-    }
-  }
 }
 
 // el / er for projected rows: el = a[:dh]·z_h, er = a[dh:]·z_h per head
@@ -2150,21 +2041,8 @@ int rtec_layer_incremental(const rtec_graph_t* g, const rtec_batch_t* b, const r
   a.prev_slot = prev ? (prev->chg_slot ? prev->chg_slot : prev->dst_slot) : nullptr;
   a.err = err;
   const int grid = kSMs * 8;
-  if (L->model == RTEC_MODEL_GAT) {
-    // factored attention deltas of the changed sources (unsharded, 16-byte rows)
-    const bool fa = st->gat_drow && st->gat_da && prev && !prev->bm_chg && st->Z_log && st->er_log &&
-                    L->d_out % 4 == 0 && (L->d_out / L->heads) % 4 == 0;
-    if (fa) {
-      RTEC_PROF("k_gat_delta", s);
-      k_gat_delta<<<kSMs * 8, kLBlk, 0, s>>>(st->Z, st->Z_log, st->er, st->er_log, prev->dst_list, prev->n_dst,
-                                             L->d_out, L->heads, st->gat_drow, st->gat_da, err);
-      RTEC_LAUNCH_CHECK("k_gat_delta");
-    } else {
-      a.st.gat_drow = nullptr;
-      a.st.gat_da = nullptr;
-    }
+  if (L->model == RTEC_MODEL_GAT)
     return launch_gat<false>(a, AggRows{f->dst_list, f->n_dst, n}, n, g->in.slots, w, s);
-  }
   layer_args_init(a, L, st);
   if (L->model == RTEC_MODEL_GIN_MAX) {
     RTEC_TRY(launch_max<false>(a, AggRows{f->dst_list, f->n_dst, n}, n, g->in.slots, w, s));

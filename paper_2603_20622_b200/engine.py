@@ -22,7 +22,6 @@ device), so the whole step can be captured in a CUDA graph (`capture()`).
 from __future__ import annotations
 
 import ctypes as C
-import os
 import time
 from dataclasses import dataclass, field
 
@@ -119,8 +118,6 @@ class RTECEngine:
 
     FUSED_DELTA = True
     GAT_IMG_BUDGET = 8 << 30  # bytes of the GAT projection's tcgen05 A image (all n rows)
-    GAT_FA = True             # factored attention deltas (one gathered row per ValueChange edge)
-    GAT_FA_BUDGET = 8 << 30
 
     def __init__(self, bundle: Bundle, graph: DynamicGraph, features, *, max_batch: int | None = None,
                  update: str = "tc", use_graphs: bool = True, bootstrap: bool = True,
@@ -230,14 +227,6 @@ class RTECEngine:
                 for lst in (self.Z, self.el, self.er, self.Zlog, self.erlog):
                     lst.append(None)
         self.max_dim = max(max(dims), 1)
-        # GAT factored attention deltas of the changed sources (rtec_state_t.gat_drow / gat_da):
-        # [slots][2][d_out] + [slots][2][heads] per layer >= 1, slots <= n
-        self.gat_fa = [None] * self.L
-        if bundle.model == GAT and self.GAT_FA and os.environ.get("RTEC_GAT_FA", "1") != "0":
-            need = sum(n * 2 * (dims[l + 1] + heads) * 4 for l in range(1, self.L))
-            if need <= self.GAT_FA_BUDGET:
-                for l in range(1, self.L):
-                    self.gat_fa[l] = (z(n * 2 * dims[l + 1]), z(n * 2 * heads))
         pad = lambda d: (d + 31) // 32 * 32  # noqa: E731
         if self.tc and bundle.model == GAT:  # projection A image over every row (bootstrap, replicas)
             self.gemm_in = z((n + 127) // 128 * 128 * pad(max(dims[:-1])))
@@ -278,8 +267,6 @@ class RTECEngine:
         st = _lib.State(p(self.H[l]), p(self.H[l + 1]), p(self.S[l]), p(self.ctx[l]), p(self.log[l]),
                         p(self.log[l - 1]) if l > 0 else None, p(self.Z[l]), p(self.el[l]), p(self.er[l]),
                         p(self.Zlog[l]), p(self.erlog[l]), p(self.gemm_in), p(self.gemm_mid))
-        if incremental and self.gat_fa[l] is not None:
-            st.gat_drow, st.gat_da = p(self.gat_fa[l][0]), p(self.gat_fa[l][1])
         if incremental and self.fused:
             st.delta = p(self.delta[l])
             st.delta_next = p(self.delta[l + 1]) if l + 1 < self.L else None

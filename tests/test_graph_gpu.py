@@ -92,11 +92,22 @@ def test_golden_coalesce(P):
 def test_random_stream_vs_oracle(P, B, reserve):
     """Mixed streams incl. rejects/self-loops, small and radix-sort batch sizes,
     and a tiny arena (forces relocation overflow -> compaction -> replay)."""
+    _stream_vs_oracle(P, B, reserve, n=3000, m=40000)
+
+
+@pytest.mark.parametrize("B", [800, 6000])
+def test_long_runs_stream_vs_oracle(P, B):
+    """~200 edges per vertex: the warp-per-chunk run merges (more than 96 slots per vertex),
+    small update groups ranked by shuffles and hub groups of more than 32 updates by binary
+    search; bit-exact against the oracle graph."""
+    _stream_vs_oracle(P, B, None, n=600, m=120000)
+
+
+def _stream_vs_oracle(P, B, reserve, n, m):
     from oracle.graph import OracleGraph
     from paper_2603_20622_b200.workload import chung_lu_edges
 
     rng = np.random.default_rng(B + (reserve or 0))
-    n, m = 3000, 40000
     s, d = chung_lu_edges(n, m, seed=7)
     ts = rng.permutation(m)
     g = P.DynamicGraph.from_edges(n, (s, d, ts), reserve=reserve)
