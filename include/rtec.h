@@ -210,13 +210,6 @@ typedef struct {
   int32_t row_div;
   int32_t out_local;
   int32_t delta_slot;
-  /* Packed source-delta rows (d_agg = 128 S, S >= 2; fused sum aggregators): δ rows after a
-   * ReLU are half exact zeros, so a row is stored as d/32 mask words + per 128-column segment
-   * its nonzeros (row stride d + d/32 floats).  delta_packed: this layer's δ rows (read by the
-   * aggregation, written by its source-delta pass); delta_next_packed: the update epilogue
-   * writes the next layer's rows packed.  Lossless: the same values, summed in the same order. */
-  int32_t delta_packed;
-  int32_t delta_next_packed;
 } rtec_state_t;
 
 /* ---- workspace ---- */

@@ -72,7 +72,7 @@ class State(C.Structure):
         ("H_in", P), ("H_out", P), ("S", P), ("ctx", P), ("log_out", P), ("log_in", P),
         ("Z", P), ("el", P), ("er", P), ("Z_log", P), ("er_log", P), ("gemm_in", P), ("gemm_mid", P),
         ("delta", P), ("delta_next", P), ("delta_ready", I32), ("row_div", I32), ("out_local", I32),
-        ("delta_slot", I32), ("delta_packed", I32), ("delta_next_packed", I32),
+        ("delta_slot", I32),
     ]
 
 

@@ -339,7 +339,6 @@ __global__ void __launch_bounds__(512, 1) k_gemm_tc(TcArgs g, TcShape sh) {
       // fused deltas: pre-batch rows of this warp's 32 rows, one 32-column chunk at a
       // time, copied asynchronously into shared memory one chunk ahead
       const bool fused = g.delta_next != nullptr && !g.Yt;
-      int segoff[8];  // packed δ rows: nonzeros written so far in the current segment, per row group
       float c_new = 1.f, c_old = 1.f;
       float* oldw = olds + (warp - 8) * 2 * 32 * 32;
       const int sub = lane >> 3, ch = lane & 7;  // 4 rows per instruction, 8 lanes x 16 B per row
@@ -407,10 +406,6 @@ __global__ void __launch_bounds__(512, 1) k_gemm_tc(TcArgs g, TcShape sh) {
         const int col = c0 + ch * 4;
         if (fused) {
           const float* ob = oldw + ((cc - cbeg) & 1) * 32 * 32;
-          if (g.delta_pk && (cc & 3) == 0) {
-#pragma unroll
-            for (int u = 0; u < 8; ++u) segoff[u] = 0;  // a new 128-column segment of the packed rows
-          }
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const int q = 4 * u + sub;
@@ -418,29 +413,12 @@ __global__ void __launch_bounds__(512, 1) k_gemm_tc(TcArgs g, TcShape sh) {
             const float cn = __shfl_sync(0xffffffffu, c_new, q);
             const float co = __shfl_sync(0xffffffffu, c_old, q);
             const float4 v4 = *reinterpret_cast<const float4*>(stg + q * 32 + ((ch ^ (q & 7)) << 2));
-            if (dq < 0 || col + 4 > g.d_out) continue;  // uniform over the row's 8 lanes
+            if (dq < 0 || col + 4 > g.d_out) continue;
             const float4 o4 = *reinterpret_cast<const float4*>(ob + q * 32 + ch * 4);
             *reinterpret_cast<float4*>(g.Y + dq * g.ldy + col) = v4;
-            const float4 dd = make_float4(cn * v4.x - co * o4.x, cn * v4.y - co * o4.y, cn * v4.z - co * o4.z,
-                                          cn * v4.w - co * o4.w);
-            if (g.delta_pk) {
-              // packed row: this 32-column block's mask word, then its nonzeros after the
-              // segment's earlier ones (the 8 lanes of row q hold the block's 32 columns)
-              const uint32_t nib = (dd.x != 0.f ? 1u : 0u) | (dd.y != 0.f ? 2u : 0u) | (dd.z != 0.f ? 4u : 0u) |
-                                   (dd.w != 0.f ? 8u : 0u);
-              const uint32_t word = __reduce_or_sync(0xFFu << (lane & ~7), nib << (ch * 4));
-              float* prow = g.delta_next + dq * g.delta_ld;
-              if (ch == 0) __stcg(reinterpret_cast<uint32_t*>(prow) + cc, word);
-              int pp = segoff[u] + __popc(word & ((1u << (ch * 4)) - 1u));
-              float* vals = prow + (g.d_out >> 5) + (cc >> 2) * 128;
-              if (nib & 1u) __stcg(vals + pp++, dd.x);
-              if (nib & 2u) __stcg(vals + pp++, dd.y);
-              if (nib & 4u) __stcg(vals + pp++, dd.z);
-              if (nib & 8u) __stcg(vals + pp++, dd.w);
-              segoff[u] += __popc(word);
-            } else {
-              __stcg(reinterpret_cast<float4*>(g.delta_next + dq * g.delta_ld + col), dd);
-            }
+            __stcg(reinterpret_cast<float4*>(g.delta_next + dq * g.d_out + col),
+                   make_float4(cn * v4.x - co * o4.x, cn * v4.y - co * o4.y, cn * v4.z - co * o4.z,
+                               cn * v4.w - co * o4.w));
           }
           __syncwarp();
           continue;

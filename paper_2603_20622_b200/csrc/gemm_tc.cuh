@@ -23,8 +23,6 @@ struct TcArgs {
   // delta_next[y_rows[i]] = c_new * h_new - c_old * h_old with c from the out-degrees
   // (GCN 1/sqrt(deg + off), others 1; 0 for a vertex without out-edges)
   float* delta_next;
-  int delta_pk;      // delta_next rows packed (rowops.cuh pk_stride layout)
-  int64_t delta_ld;  // row stride of delta_next (d_out, or pk_stride(d_out) when packed)
   const int32_t* deg_new;
   const int32_t* deg_old;
   int coeff_gcn;

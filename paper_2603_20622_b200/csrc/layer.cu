@@ -131,12 +131,6 @@ __global__ void __launch_bounds__(kLBlk) k_src_delta(LayerArgs a, float* delta) 
       acc.fma(ho, -co);
     }
     // indexed by vertex (no slot gather per edge) unless the sharded δ buffer is slot-indexed
-    if constexpr (VEC == 4) {
-      if (a.st.delta_packed) {
-        acc.store_packed(delta + static_cast<int64_t>(u) * pk_stride(d), d);
-        continue;
-      }
-    }
     acc.store(delta + (a.st.delta_slot ? i : static_cast<int64_t>(u)) * d, d);
   }
 }
@@ -160,7 +154,7 @@ constexpr int kChunk = 512;
 // 2 len / kChunk for len > kChunk, so the sum is at most 2 max_edges / kChunk
 __host__ __device__ constexpr int64_t heavy_chunk_bound(int64_t max_edges) { return 2 * max_edges / kChunk + 2; }
 
-template <int VEC, int K, bool FULL, bool PK = false>
+template <int VEC, int K, bool FULL>
 __device__ __forceinline__ void agg_edges(const LayerArgs& a, int64_t beg, int32_t e0, int32_t e1, int64_t p,
                                           int64_t q, RowAcc<VEC, K>& acc) {
   using R = RowAcc<VEC, K>;
@@ -168,11 +162,6 @@ __device__ __forceinline__ void agg_edges(const LayerArgs& a, int64_t beg, int32
   const int d = a.d_agg, cw = a.cw;
   const int lane = lane_id();
   const uint64_t pol = l2_evict_first_policy();
-  // packed δ rows: the window's hits' mask words are staged once (lane j: hit j), so each
-  // gather reads its mask from shared memory and only the nonzero values from L2 / HBM
-  constexpr bool kPk = PK && !FULL && VEC == 4;
-  __shared__ uint4 s_pm[kPk ? kLBlk / 32 : 1][kPk ? 32 : 1][kPk ? K : 1];
-  const int64_t pks = pk_stride(d);
   for (int32_t c0 = e0; c0 < e1; c0 += 32) {
     int32_t j = c0 + lane;
     int32_t u = 0;
@@ -191,48 +180,6 @@ __device__ __forceinline__ void agg_edges(const LayerArgs& a, int64_t beg, int32
     const float* base = (FULL ? a.st.H_in : a.delta) + a.c0;
     // gathered row: the source's own row (H_in, vertex-indexed δ) or its δ slot
     int32_t row = (!FULL && hit && a.st.delta_slot) ? a.f.src_slot[u] : u;
-    if constexpr (kPk) {
-      if (hit) {
-        const uint4* mw = reinterpret_cast<const uint4*>(a.delta + static_cast<int64_t>(row) * pks);
-#pragma unroll
-        for (int k = 0; k < K; ++k) s_pm[threadIdx.x >> 5][lane][k] = __ldg(mw + k);
-      }
-      __syncwarp();
-      while (m) {
-        int32_t rw[UNR];
-        int sr[UNR];
-        int cnt = 0;
-#pragma unroll
-        for (int t = 0; t < UNR; ++t) {
-          const int src = m ? __ffs(m) - 1 : 0;
-          if (m) {
-            m &= m - 1;
-            cnt = t + 1;
-          }
-          rw[t] = __shfl_sync(0xffffffffu, row, src);
-          sr[t] = src;
-        }
-        float r[UNR][K][VEC];
-#pragma unroll
-        for (int t = 0; t < UNR; ++t)
-          if (t < cnt) {
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-              float x[4];
-              pk_load4(a.delta + static_cast<int64_t>(rw[t]) * pks + d / 32 + k * 128,
-                       pk_lane_from_words(s_pm[threadIdx.x >> 5][sr[t]][k]), x);
-              r[t][k][0] = x[0];
-              r[t][k][1] = x[1];
-              r[t][k][2] = x[2];
-              r[t][k][3] = x[3];
-            }
-          }
-#pragma unroll
-        for (int t = 0; t < UNR; ++t)
-          if (t < cnt) acc.add(r[t]);
-      }
-      __syncwarp();
-    } else {
     while (m) {
       int32_t rw[UNR];
       float cs[UNR];
@@ -259,7 +206,6 @@ __device__ __forceinline__ void agg_edges(const LayerArgs& a, int64_t beg, int32
         }
       }
     }
-    }
   }
 }
 
@@ -276,14 +222,7 @@ __device__ __forceinline__ void agg_struct(const LayerArgs& a, int64_t p, int64_
       acc.fma(r, src_coeff(a.L.model, a.g.out_deg[u], a.L.degree_offset));
     } else if (a.st.delta_ready && a.prev_bm_dst && bm_test(a.prev_bm_dst, u)) {
       // -c_old h_old(u) = δ_u - c_new h_new(u)  (fused deltas: no DeltaLog)
-      bool done = false;
-      if constexpr (VEC == 4) {
-        if (a.st.delta_packed) {
-          R::load_packed(a.delta + static_cast<int64_t>(u) * pk_stride(d), d, r);
-          done = true;
-        }
-      }
-      if (!done) R::load(a.delta + drow(a, u) * d + a.c0, cw, r);
+      R::load(a.delta + drow(a, u) * d + a.c0, cw, r);
       acc.add(r);
       R::load(a.st.H_in + static_cast<int64_t>(u) * d + a.c0, cw, r);
       acc.fma(r, -fused_coeff(a.L.model, a.g.out_deg[u], a.L.degree_offset));
@@ -403,7 +342,7 @@ __device__ __forceinline__ void sum_partials(const float* part, int64_t stride, 
   }
 }
 
-template <int VEC, int K, bool FULL, bool PK = false>
+template <int VEC, int K, bool FULL>
 __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_light(LayerArgs a, AggRows rows) {
   using R = RowAcc<VEC, K>;
   __shared__ __align__(16) float s_sv[kLBlk / 32][(!FULL && VEC == 4) ? 32 * VEC * K : 4];
@@ -444,7 +383,7 @@ __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_light(Laye
     }
     R acc;
     acc.zero();
-    if (scan) agg_edges<VEC, K, FULL, PK>(a, beg, 0, len, p, q, acc);
+    if (scan) agg_edges<VEC, K, FULL>(a, beg, 0, len, p, q, acc);
     if (!FULL) agg_struct<VEC, K>(a, p, q, acc);
     if constexpr (VEC == 4) {
       if (pre) R::from_stage(s_sv[threadIdx.x >> 5], a.cw, sv.v);
@@ -607,7 +546,7 @@ __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_batch(Laye
   }
 }
 
-template <int VEC, int K, bool FULL, bool PK = false>
+template <int VEC, int K, bool FULL>
 __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
@@ -637,7 +576,7 @@ __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_heavy(Laye
     R acc;
     acc.zero();
     int32_t e0 = c * kChunk, e1 = min(len, e0 + kChunk);
-    agg_edges<VEC, K, FULL, PK>(a, a.g.in.beg[v], e0, e1, p, q, acc);
+    agg_edges<VEC, K, FULL>(a, a.g.in.beg[v], e0, e1, p, q, acc);
     if (!FULL && c == 0) agg_struct<VEC, K>(a, p, q, acc);
     acc.store(hp.part + t * cw, cw);
     __threadfence();
@@ -812,25 +751,14 @@ static int launch_aggregation(LayerArgs& a, AggRows rows, int64_t max_rows, int6
       RTEC_CUDA(cudaEventRecord(side_fork(), s));
       RTEC_CUDA(cudaStreamWaitEvent(hs, side_fork(), 0));
     }
-    // packed δ rows (whole-row passes over d = 128 S, S >= 2; the batched pass is for d <= 128)
-    const bool pk = !FULL && a.st.delta_packed && !sliced && a.cw == d && pk_width_ok(d) && !agg_batched(a.cw);
-    if (!FULL && a.st.delta_packed && !pk) {
-      set_error("packed source deltas need whole-row passes over d = 128 S (d = %d, slice %d)", d, a.cw);
-      return RTEC_CONFIG_ERROR;
-    }
     {
       RTEC_PROF(FULL ? "k_agg_full_heavy" : "k_agg_inc_heavy", hs);
-      if (pk)
-        ok = RTEC_ROW_DISPATCH(a.cw, (k_agg_heavy<VEC, K, FULL, true><<<grid, kLBlk, 0, hs>>>(a, rows, hp)));
-      else
-        ok = (sliced ? RTEC_SLICE_DISPATCH(a.cw, (k_agg_heavy<VEC, K, FULL><<<grid, kLBlk, 0, hs>>>(a, rows, hp)))
-                     : RTEC_ROW_DISPATCH(a.cw, (k_agg_heavy<VEC, K, FULL><<<grid, kLBlk, 0, hs>>>(a, rows, hp))));
+      ok = (sliced ? RTEC_SLICE_DISPATCH(a.cw, (k_agg_heavy<VEC, K, FULL><<<grid, kLBlk, 0, hs>>>(a, rows, hp)))
+                   : RTEC_ROW_DISPATCH(a.cw, (k_agg_heavy<VEC, K, FULL><<<grid, kLBlk, 0, hs>>>(a, rows, hp))));
     }
     {
       RTEC_PROF(FULL ? "k_agg_full_light" : "k_agg_inc", s);
-      if (pk) {
-        ok = ok && RTEC_ROW_DISPATCH(a.cw, (k_agg_light<VEC, K, FULL, true><<<grid, kLBlk, 0, s>>>(a, rows)));
-      } else if (!FULL && !sliced && agg_batched(a.cw)) {
+      if (!FULL && !sliced && agg_batched(a.cw)) {
         // both light-pass kernels are enqueued; each runs only in its hit-density regime
         LayerArgs ab = a, al = a;
         ab.pick = 1;
@@ -2026,8 +1954,6 @@ static int run_update(const rtec_graph_t* g, const rtec_layer_t* L, rtec_state_t
   auto fuse = [&](TcArgs& t) {  // the next layer's source deltas from this update's epilogue
     if (!st->delta_next || !y_rows || (L->d_out & 3)) return;
     t.delta_next = st->delta_next;
-    t.delta_pk = st->delta_next_packed && pk_width_ok(L->d_out) ? 1 : 0;
-    t.delta_ld = t.delta_pk ? pk_stride(L->d_out) : L->d_out;
     t.deg_new = g->out_deg;
     t.deg_old = g->out_deg_prev;
     t.coeff_gcn = L->model == RTEC_MODEL_GCN;

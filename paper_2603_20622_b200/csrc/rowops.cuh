@@ -54,60 +54,6 @@ __device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, ui
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// ---------------------------------------------------------------- packed source-delta rows
-// The source deltas of a layer after a ReLU are half exact zeros (δ_u = c_new h_new - c_old h_old
-// vanishes wherever both rows were clipped), so rows of d = 128·S floats (S >= 2) may be stored
-// packed: d/32 mask words (bit j of word b = column 32 b + j nonzero), then per 128-column
-// segment s a value region at d/32 + 128 s holding that segment's nonzeros in column order.
-// A reader touches the mask and the nonzeros only (~53 % of a dense row); lossless, same sums.
-__host__ __device__ __forceinline__ int pk_stride(int d) { return d + d / 32; }
-__host__ __device__ __forceinline__ bool pk_width_ok(int d) { return d >= 256 && d % 128 == 0; }
-
-// lane l of a warp holding columns 4l..4l+3 of one 128-column segment: the segment's 4 mask
-// words (word j: lanes 8j..8j+7), the lane's nibble and its position among the nonzeros
-struct PkLane {
-  uint32_t nib;  // bit t: column 4l + t nonzero
-  int pos;       // nonzeros of the segment before column 4l
-};
-__device__ __forceinline__ PkLane pk_lane_from_words(uint4 w) {
-  const int l = lane_id(), b = l >> 3, sh = (l & 7) * 4;
-  const uint32_t wb = b == 0 ? w.x : b == 1 ? w.y : b == 2 ? w.z : w.w;
-  int pos = __popc(wb & ((1u << sh) - 1u));
-  if (b > 0) pos += __popc(w.x);
-  if (b > 1) pos += __popc(w.y);
-  if (b > 2) pos += __popc(w.z);
-  return PkLane{(wb >> sh) & 0xFu, pos};
-}
-// 4 values at the lane's nonzero slots of a segment's value region (zeros elsewhere)
-__device__ __forceinline__ void pk_load4(const float* __restrict__ vals, PkLane pl, float (&r)[4]) {
-  int p = pl.pos;
-#pragma unroll
-  for (int t = 0; t < 4; ++t) r[t] = 0.f;
-#pragma unroll
-  for (int t = 0; t < 4; ++t)
-    if ((pl.nib >> t) & 1u) r[t] = __ldg(vals + p++);
-}
-// store the lane's 4 values of segment `seg` of a packed row (warp-collective)
-__device__ __forceinline__ void pk_store4(float* row, int d, int seg, const float (&x)[4]) {
-  const int l = lane_id();
-  uint32_t nib = 0;
-#pragma unroll
-  for (int t = 0; t < 4; ++t) nib |= (x[t] != 0.f ? 1u : 0u) << t;
-  const uint32_t grp = 0xFFu << (l & ~7);
-  const uint32_t word = __reduce_or_sync(grp, nib << ((l & 7) * 4));
-  uint4 w;
-  w.x = __shfl_sync(0xffffffffu, word, 0);
-  w.y = __shfl_sync(0xffffffffu, word, 8);
-  w.z = __shfl_sync(0xffffffffu, word, 16);
-  w.w = __shfl_sync(0xffffffffu, word, 24);
-  if ((l & 7) == 0) reinterpret_cast<uint32_t*>(row)[seg * 4 + (l >> 3)] = word;
-  PkLane pl = pk_lane_from_words(w);
-  float* vals = row + d / 32 + seg * 128;
-#pragma unroll
-  for (int t = 0; t < 4; ++t)
-    if ((pl.nib >> t) & 1u) vals[pl.pos++] = x[t];
-}
-
 template <int VEC, int K>
 struct RowAcc {
   float v[K][VEC];
@@ -250,26 +196,6 @@ struct RowAcc {
           row[c] = v[k][0];
         }
       }
-    }
-  }
-  // packed δ rows (pk_stride layout), VEC == 4 and d == 128 K: chunk k is segment k
-  __device__ __forceinline__ void store_packed(float* row, int d) const {
-    static_assert(VEC == 4, "packed rows hold 16-byte column groups");
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const float x[4] = {v[k][0], v[k][1], v[k][2], v[k][3]};
-      pk_store4(row, d, k, x);
-    }
-  }
-  __device__ __forceinline__ static void load_packed(const float* row, int d, float (&r)[K][VEC]) {
-    static_assert(VEC == 4, "packed rows hold 16-byte column groups");
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const uint4 w = __ldg(reinterpret_cast<const uint4*>(row) + k);
-      float x[4];
-      pk_load4(row + d / 32 + k * 128, pk_lane_from_words(w), x);
-#pragma unroll
-      for (int t = 0; t < 4; ++t) r[k][t] = x[t];
     }
   }
   // Columns [col0, col0 + w) of row i into the tcgen05 A-operand image:

@@ -22,7 +22,6 @@ device), so the whole step can be captured in a CUDA graph (`capture()`).
 from __future__ import annotations
 
 import ctypes as C
-import os
 import time
 from dataclasses import dataclass, field
 
@@ -118,7 +117,6 @@ class RTECEngine:
     """B200 incremental engine over a DynamicGraph and an operator Bundle."""
 
     FUSED_DELTA = True
-    PACK_DELTA = True         # packed source-delta rows where the width allows (see __init__)
     GAT_IMG_BUDGET = 8 << 30  # bytes of the GAT projection's tcgen05 A image (all n rows)
 
     def __init__(self, bundle: Bundle, graph: DynamicGraph, features, *, max_batch: int | None = None,
@@ -169,16 +167,9 @@ class RTECEngine:
         # one vertex-indexed δ buffer shared by all layers: layer l's rows are dead once its
         # aggregation has run, before the update epilogue writes layer l+1's (stream order)
         self.delta = [None] * bundle.num_layers
-        # packed δ rows (rtec_state_t.delta_packed) for layers >= 1 whose aggregate width is
-        # 128 S (S >= 2): the rows after a ReLU are half zeros; lossless, same sums
-        self.delta_pk = [False] * bundle.num_layers
-        if self.fused and self.PACK_DELTA and os.environ.get("RTEC_DELTA_PACK", "1") != "0" and \
-                os.environ.get("RTEC_AGG_SLICE", "0") in ("", "0"):
-            self.delta_pk = [l > 0 and d >= 256 and d % 128 == 0 for l, d in enumerate(bundle.agg_dims)]
         if self.fused:
-            strides = [d + d // 32 if pk else d for d, pk in zip(bundle.agg_dims, self.delta_pk)]
-            dbuf = z(n * max(strides))
-            self.delta = [dbuf[: n * w].view(n, w) for w in strides]
+            dbuf = z(n * max(bundle.agg_dims))
+            self.delta = [dbuf[: n * d].view(n, d) for d in bundle.agg_dims]
         for l, w in enumerate(bundle.layers):
             d_in, d_out = w.in_dim, w.out_dim
             dev32 = lambda a: torch.as_tensor(np.ascontiguousarray(a, np.float32), device=self.dev)  # noqa: E731
@@ -280,8 +271,6 @@ class RTECEngine:
             st.delta = p(self.delta[l])
             st.delta_next = p(self.delta[l + 1]) if l + 1 < self.L else None
             st.delta_ready = 1 if l > 0 else 0
-            st.delta_packed = 1 if self.delta_pk[l] else 0
-            st.delta_next_packed = 1 if l + 1 < self.L and self.delta_pk[l + 1] else 0
         return st
 
     # ---------------------------------------------------------------- SPEC bootstrap / run_full

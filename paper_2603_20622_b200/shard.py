@@ -151,7 +151,6 @@ class ShardedRTECEngine(RTECEngine):
     # sum aggregators: the update epilogue writes δ of the owned changed rows and the exchange
     # writes δ of the received ghost rows (no DeltaLog); GAT / GIN-max keep an exchanged DeltaLog
     FUSED_DELTA = True
-    PACK_DELTA = False  # received ghost rows write dense source deltas (rtec_shard_unpack_changed)
 
     def __init__(self, bundle, num_vertices: int, edges, features, comm: Comm, *, max_batch: int | None = None,
                  update: str = "tc", reserve: int | None = None, device=None, exchange_chunk: int = 1 << 20,

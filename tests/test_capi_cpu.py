@@ -62,7 +62,7 @@ def test_struct_layouts_match_header(lib):
     assert ctypes.sizeof(_lib.Batch) == 8 * 20  # + apply_ctr
     assert ctypes.sizeof(_lib.Frontier) == 8 * 11
     assert ctypes.sizeof(_lib.Layer) == 6 * 4 + 9 * 8 + 8  # + Wp, bp, scalar, d_k
-    assert ctypes.sizeof(_lib.State) == 15 * 8 + 16 + 8  # + delta_packed / delta_next_packed
+    assert ctypes.sizeof(_lib.State) == 15 * 8 + 16
 
 
 def test_sass_is_sm100a(lib):

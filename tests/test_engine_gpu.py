@@ -495,44 +495,3 @@ def test_edge_case_batches(P, model):
         op, bs, bd = batches[2]
         eng2.step(op, bs, bd, np.arange(op.size, dtype=np.int64))
         assert not np.any(eng2.aggregates(0)[v])
-
-
-@pytest.mark.parametrize("model,dims", [("gcn", [64, 256, 32]), ("graphsage", [48, 256, 256]),
-                                        ("gin", [32, 256, 256, 16])])
-def test_packed_source_deltas_bit_identical(P, model, dims):
-    # 256-wide aggregates after a ReLU: the source deltas are stored packed (mask words + the
-    # nonzeros, rtec_state_t.delta_packed) -- lossless, summed in the same order, so every
-    # embedding / aggregate equals the dense-row engine bit for bit (light pass, hub chunks,
-    # deleted edges of changed sources); and both stay within 1e-4 of the oracle
-    import paper_2603_20622_b200.engine as EM
-    from oracle import models as OM
-    from oracle.engine import OracleEngine
-    from oracle.graph import OracleGraph
-    from paper_2603_20622_b200.workload import UpdateStream, chung_lu_edges, features
-
-    n, m, B = 4000, 80000, 400
-    s, d = chung_lu_edges(n, m, seed=41)
-    stream = UpdateStream(s, d, holdout=0.1, seed=41)
-    bs, bd, bt = stream.base()
-    X = features(n, dims[0], seed=42)
-    engs = []
-    for pack in (True, False):
-        old = EM.RTECEngine.PACK_DELTA
-        EM.RTECEngine.PACK_DELTA = pack
-        try:
-            engs.append(P.RTECEngine(P.make_bundle(model, dims), P.DynamicGraph.from_edges(n, (bs, bd, bt)), X))
-        finally:
-            EM.RTECEngine.PACK_DELTA = old
-    assert any(engs[0].delta_pk) and not any(engs[1].delta_pk)
-    oe = OracleEngine(OM.make_bundle(model, dims), OracleGraph.from_edges(n, bs, bd, bt), X.astype(np.float64))
-    L = len(dims) - 1
-    for _ in range(3):
-        op, s1, d1, t1 = stream.next_batch(B)
-        r0, r1 = engs[0].step(op, s1, d1, t1), engs[1].step(op, s1, d1, t1)
-        oe.step(op, s1, d1, t1)
-        assert np.array_equal(r0.status, r1.status) and np.array_equal(r0.deltas, r1.deltas)
-        for l in range(L):
-            assert np.array_equal(engs[0].embeddings(l + 1), engs[1].embeddings(l + 1)), l
-            assert np.array_equal(engs[0].aggregates(l), engs[1].aggregates(l)), l
-    for l in range(1, L + 1):
-        assert rowwise_rel(engs[0].embeddings(l), oe.H[l]) <= TOL, l
