@@ -405,8 +405,8 @@ __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_light(Laye
 // destination (run order, then structural edges) matches k_agg_light.
 constexpr int kBatchWin = kChunk;  // flattened edges per window: any light run fits one window
 
-template <int VEC, int K>
-__global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_batch(LayerArgs a, AggRows rows) {
+template <int VEC, int K, int OCC = 0>
+__global__ void __launch_bounds__(kLBlk, OCC > 0 ? OCC : AggOcc<VEC, K>::value) k_agg_batch(LayerArgs a, AggRows rows) {
   using R = RowAcc<VEC, K>;
   constexpr int UNR = kUnroll;  // measured: 8 rows in flight spill next to the prefetched S row
   __shared__ int32_t s_u[kLBlk / 32][kBatchWin];
@@ -678,6 +678,16 @@ static float agg_dense_thr() {
   return t;
 }
 
+// RTEC_AGG_BATCH_OCC env: resident CTAs per SM of the warp-batched pass (0: AggOcc, 6: A/B)
+static int agg_batch_occ() {
+  static int o = -1;
+  if (o < 0) {
+    const char* e = getenv("RTEC_AGG_BATCH_OCC");
+    o = e ? atoi(e) : 0;
+  }
+  return o;
+}
+
 // RTEC_HEAVY_ORDER env: visit hub chunks in relative-position order (default 1; 0: destination-major)
 static bool heavy_order() {
   static int o = -1;
@@ -764,8 +774,11 @@ static int launch_aggregation(LayerArgs& a, AggRows rows, int64_t max_rows, int6
         ab.pick = 1;
         al.pick = 2;
         ab.pick_thr = al.pick_thr = agg_dense_thr();
-        ok = ok && RTEC_ROW_DISPATCH(a.cw, (k_agg_batch<VEC, K><<<grid, kLBlk, 0, s>>>(ab, rows),
-                                            k_agg_light<VEC, K, false><<<grid, kLBlk, 0, s>>>(al, rows)));
+        if (agg_batch_occ() == 6)
+          ok = ok && RTEC_ROW_DISPATCH(a.cw, (k_agg_batch<VEC, K, 6><<<grid, kLBlk, 0, s>>>(ab, rows)));
+        else
+          ok = ok && RTEC_ROW_DISPATCH(a.cw, (k_agg_batch<VEC, K><<<grid, kLBlk, 0, s>>>(ab, rows)));
+        ok = ok && RTEC_ROW_DISPATCH(a.cw, (k_agg_light<VEC, K, false><<<grid, kLBlk, 0, s>>>(al, rows)));
       } else
         ok = ok && (sliced ? RTEC_SLICE_DISPATCH(a.cw, (k_agg_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows)))
                            : RTEC_ROW_DISPATCH(a.cw, (k_agg_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows))));
