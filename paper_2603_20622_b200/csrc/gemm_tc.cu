@@ -128,6 +128,16 @@ static bool gemm_n_wide() {
   return w != 0;
 }
 
+// RTEC_GEMM_SA env: A-ring stages (A/B; 0: the defaults below)
+static int gemm_a_stages() {
+  static int a = -1;
+  if (a < 0) {
+    const char* e = getenv("RTEC_GEMM_SA");
+    a = e ? atoi(e) : 0;
+  }
+  return a;
+}
+
 static TcShape tc_shape(int npad, bool fused) {
   TcShape sh;
   // N > 128 runs in two N-halves (32 KB B stages, deep rings) unless the whole N fits one
@@ -140,8 +150,14 @@ static TcShape tc_shape(int npad, bool fused) {
   sh.oldb = fused ? kOldBytes : 0;
   const int budget = 227 * 1024 - 1024 - 512 - kEpiBytes - static_cast<int>(sh.oldb);
   sh.SA = (fused || wide) ? 2 : 3;  // measured: 2..4 A stages perform alike; the B ring gets the rest
+  const int sa_env = gemm_a_stages();
+  if (sa_env >= 2 && sa_env <= kMaxA) sh.SA = sa_env;
   sh.SB = (budget - sh.SA * 2 * kABlockBytes) / static_cast<int>(sh.bstage);
   if (sh.SB > kMaxB) sh.SB = kMaxB;
+  if (sh.SB < 2) {  // keep a double-buffered B ring
+    sh.SB = 2;
+    sh.SA = (budget - sh.SB * static_cast<int>(sh.bstage)) / (2 * kABlockBytes);
+  }
   return sh;
 }
 
