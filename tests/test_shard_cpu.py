@@ -162,3 +162,86 @@ def test_sharded_frontier_matches_oracle(model):
         o = oe.step(*stream.next_batch(B))
         for l in range(2):
             assert np.array_equal(out[f"v{i}_{l}"], o["frontier"][l]["vdst"]), (model, i, l)
+
+
+def _ghost_main(rank, world, port, td, n, m, B, nb):
+    """The ghost-row protocol of shard.py / shard.cu restated at set level over gloo (world 3):
+    load-time announce, admission by inserts (receiver and owner decide from the same batch),
+    and the targeted exchange -- every rank holding an edge out of a changed vertex receives
+    its row, and peers[u] has bit q exactly when rank q holds a ghost of u."""
+    _init(rank, world, port)
+    import torch
+
+    from oracle.graph import OP_INSERT, OracleGraph
+    from paper_2603_20622_b200.shard import Comm, owner_of
+    from paper_2603_20622_b200.workload import UpdateStream, chung_lu_edges
+
+    c = Comm()
+    s, d = chung_lu_edges(n, m, seed=33)
+    stream = UpdateStream(s, d, holdout=0.1, seed=33)
+    bs, bd, bt = stream.base()
+    g = OracleGraph.from_edges(n, bs, bd, bt)
+    mine = owner_of(bd, world) == rank
+    ghosts = set(np.unique(bs[mine][owner_of(bs[mine], world) != rank]).tolist())
+    # announce: each ghost tells its owner (all_to_all of ids) -> peers bits of owned vertices
+    out = [[u for u in sorted(ghosts) if owner_of(u, world) == q] for q in range(world)]
+    sc = torch.tensor([len(x) for x in out], dtype=torch.int64)
+    rc = c.all_to_all_counts(sc)
+    ids = torch.tensor(sum(out, []) or [0], dtype=torch.int64)[: int(sc.sum())]
+    got = c.all_to_all_rows(ids, sc.tolist(), rc.tolist()).tolist()
+    src_rank = np.repeat(np.arange(world), rc.numpy())
+    peers = {}
+    for u, q in zip(got, src_rank.tolist()):
+        peers[u] = peers.get(u, 0) | (1 << q)
+    res = {}
+    for i in range(nb):
+        op, s1, d1, t1 = stream.next_batch(B)
+        # admission: receiver admits sources of inserts into owned destinations; the owner
+        # sets the peer bit for the same (source, rank) pairs
+        for o, u, v in zip(op.tolist(), s1.tolist(), d1.tolist()):
+            if o != OP_INSERT or owner_of(u, world) == owner_of(v, world):
+                continue
+            if owner_of(v, world) == rank:
+                ghosts.add(u)
+            if owner_of(u, world) == rank:
+                peers[u] = peers.get(u, 0) | (1 << owner_of(v, world))
+        g.apply_batch(op, s1, d1, t1)
+        # a changed set (any vertex ids): every owned changed row goes to the ranks in peers
+        chg = np.unique(np.concatenate([s1, d1]))
+        sends = {q: sorted(u for u in chg.tolist() if owner_of(u, world) == rank and (peers.get(u, 0) >> q) & 1)
+                 for q in range(world)}
+        sc = torch.tensor([len(sends[q]) for q in range(world)], dtype=torch.int64)
+        rc = c.all_to_all_counts(sc)
+        ids = torch.tensor(sum((sends[q] for q in range(world)), []) or [0], dtype=torch.int64)[: int(sc.sum())]
+        recv = set(c.all_to_all_rows(ids, sc.tolist(), rc.tolist()).tolist())
+        nn = np.uint64(n)
+        es, ed = (g.out_keys // nn).astype(np.int64), (g.out_keys % nn).astype(np.int64)
+        here = owner_of(ed, world) == rank
+        need = set(es[here][np.isin(es[here], chg) & (owner_of(es[here], world) != rank)].tolist())
+        res[f"missing{i}"] = np.array(sorted(need - recv), np.int64)      # must be empty
+        res[f"notghost{i}"] = np.array(sorted(recv - ghosts), np.int64)   # must be empty
+        res[f"ghost_sources{i}"] = np.array(sorted(set(es[here][owner_of(es[here], world) != rank].tolist())
+                                                   - ghosts), np.int64)   # must be empty
+    # peers coherence: gather every rank's ghosts, compare with the owners' peer bits
+    gl = c.all_gather_var(torch.tensor(sorted(ghosts) or [0], dtype=torch.int64)[: len(ghosts)], len(ghosts))
+    cnt = c.all_gather_ints([len(ghosts)], torch.device("cpu"))[:, 0]
+    holder = np.repeat(np.arange(world), cnt)
+    want = {}
+    for u, q in zip(gl.tolist(), holder.tolist()):
+        if owner_of(u, world) == rank:
+            want[u] = want.get(u, 0) | (1 << q)
+    res["peers_ok"] = np.array([want == {u: b for u, b in peers.items() if b}], bool)
+    np.savez(os.path.join(td, f"g{rank}.npz"), **res)
+    import torch.distributed as dist
+
+    dist.destroy_process_group()
+
+
+def test_ghost_protocol_world3():
+    out = _spawn(_ghost_main, 3, 2000, 16000, 300, 3)
+    for r in range(3):
+        z = out[f"g{r}.npz"]
+        assert bool(z["peers_ok"][0]), r
+        for i in range(3):
+            assert z[f"missing{i}"].size == 0 and z[f"notghost{i}"].size == 0, (r, i)
+            assert z[f"ghost_sources{i}"].size == 0, (r, i)
