@@ -115,25 +115,39 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_1pass(F f, Count cnt, O out
   }
   int64_t tot;
   int64_t off = block_exclusive_scan<int64_t>(s, sw, &tot);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    // warp-wide look-back: lane k reads the word of tile j - k, 32 predecessors per step
     volatile unsigned long long* vst = st;
+    const int lane = threadIdx.x;
     int64_t excl = 0;
     if (tile == 0) {
-      atomicExch(st, kLbPrefix | static_cast<unsigned long long>(tot));
+      if (lane == 0) atomicExch(st, kLbPrefix | static_cast<unsigned long long>(tot));
     } else {
-      atomicExch(st + tile, kLbAgg | static_cast<unsigned long long>(tot));
+      if (lane == 0) atomicExch(st + tile, kLbAgg | static_cast<unsigned long long>(tot));
       for (int64_t j = tile - 1;;) {
-        const unsigned long long w = vst[j];
-        if (w == 0) continue;  // predecessor still scanning its tile
-        excl += static_cast<int64_t>(w & kLbMask);
-        if (w & kLbPrefix) break;
-        --j;
+        const int64_t idx = j - lane;
+        const unsigned long long w = idx >= 0 ? vst[idx] : (kLbPrefix | 0ull);
+        const unsigned pre = __ballot_sync(0xffffffffu, (w & kLbPrefix) != 0);
+        const unsigned ready = __ballot_sync(0xffffffffu, w != 0);
+        // lanes up to the nearest inclusive prefix (or all 32) must have published
+        const unsigned need = pre ? ((pre & (0u - pre)) << 1) - 1u : 0xffffffffu;
+        if ((ready & need) != need) continue;  // a predecessor is still scanning its tile
+        int64_t v = (need >> lane) & 1u ? static_cast<int64_t>(w & kLbMask) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (pre) break;
+        j -= 32;
       }
-      __threadfence();
-      atomicExch(st + tile, kLbPrefix | static_cast<unsigned long long>(excl + tot));
+      if (lane == 0) {
+        __threadfence();
+        atomicExch(st + tile, kLbPrefix | static_cast<unsigned long long>(excl + tot));
+      }
     }
-    s_prefix = excl;
-    if (total && tile == (ntiles > 0 ? ntiles - 1 : 0)) *total = excl + tot;
+    if (lane == 0) {
+      s_prefix = excl;
+      if (total && tile == (ntiles > 0 ? ntiles - 1 : 0)) *total = excl + tot;
+    }
   }
   __syncthreads();
   off += s_prefix;
