@@ -372,10 +372,11 @@ def run_ours(args, world, rank, local):
         gc.freeze()
     e2e_ms, h2d, d2h = [], 0, 0
     e2e_upd = 0
-    for j in range(E2W):  # warm the public path once (first-call allocations), untimed
-        op, s, d, t = batches[W + K + PROF + j]
-        eng.step(*[torch.from_numpy(np.ascontiguousarray(a, dt)).pin_memory()
-                   for a, dt in ((op, np.uint8), (s, np.int32), (d, np.int32), (t, np.int64))])
+    r = None
+    for j in range(E2W):  # warm the public path (first-call allocations), untimed; each result stays
+        op, s, d, t = batches[W + K + PROF + j]  # alive into the next call, as in the timed loop
+        r = eng.step(*[torch.from_numpy(np.ascontiguousarray(a, dt)).pin_memory()
+                       for a, dt in ((op, np.uint8), (s, np.int32), (d, np.int32), (t, np.int64))])
     torch.cuda.synchronize()
     for j in range(E2E):
         op, s, d, t = batches[W + K + PROF + E2W + j]
