@@ -911,7 +911,7 @@ size_t batch_ws_bytes(int64_t n, int64_t B, int64_t scr_cap) {
   add(sort_ws_bytes(B2));
   add(sizeof(int64_t) * (scan_blocks_for(B2) + 2) * 12);
   add(sizeof(uint32_t) * ((n + 31) / 32));  // touched-vertex bitmap (DegreeDelta rows)
-  add(sizeof(int64_t) * (scan_blocks_for((n + 31) / 32) + 2));
+  add(sizeof(int64_t) * (((n + 31) / 32 + 511) / 512 + 2));
   return b + (1 << 16);
 }
 
@@ -1047,7 +1047,7 @@ int rtec_batch_apply_phase(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src,
   MergePlan po, pi;
   size_t plan_fixed = sizeof(int64_t) * (B + 2) * 7 + sizeof(int32_t) * (B + 2) * 4 + (B + 2) + 4096 + 256;
   size_t sort_reserve = sort_ws_bytes(B2) + sizeof(int64_t) * (scan_blocks_for(B2) + 2) * 16 + (1 << 16) +
-                        sizeof(uint32_t) * ((n + 31) / 32) + sizeof(int64_t) * (scan_blocks_for((n + 31) / 32) + 2) + 512;
+                        sizeof(uint32_t) * ((n + 31) / 32) + sizeof(int64_t) * (((n + 31) / 32 + 511) / 512 + 2) + 512;
   size_t used = w.off + 2 * plan_fixed + sort_reserve;
   int64_t scr_cap = used < w.bytes ? static_cast<int64_t>((w.bytes - used) / 2 / (sizeof(int32_t) + sizeof(int64_t) + 1)) : 0;
   RTEC_TRY(plan_alloc(po, B, scr_cap, true, w));
@@ -1123,7 +1123,7 @@ int rtec_batch_apply_phase(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src,
   TouchedWord tw{tbm, g->in_deg, g->out_deg, g->in_deg_prev, g->out_deg_prev};
   RTEC_TRY(exclusive_scan(tw, Count{nullptr, words}, words,
                           TouchedRows{tw, b->d_vertex, b->d_old_in, b->d_new_in, b->d_old_out, b->d_new_out},
-                          b->n_delta, w, s));
+                          b->n_delta, w, s, /*wide=*/true));
   w.off = mark;
   return RTEC_OK;
 }

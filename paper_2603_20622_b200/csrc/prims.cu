@@ -164,49 +164,73 @@ __global__ void __launch_bounds__(1024) k_sort_small(const uint64_t* __restrict_
   }
 }
 
-// One CTA of 1024 threads, n <= 1024: bitonic network with one (key, val) per thread in
-// registers; pairs closer than a warp exchange by shuffles, farther ones through shared
-// memory (15 of the 55 compare stages of a 1024-sort need a block barrier).
+// One CTA of 1024 threads, n <= 1024, one (key, val) per thread: LSD radix sort over `bits`
+// with 8-bit digits in shared memory.  A pass ranks each element stably among equal digits
+// (warp match + per-warp digit counts, warps in index order), then scatters; ~4 barriers per
+// pass instead of the ~55 compare stages of a bitonic network.
 __global__ void __launch_bounds__(1024) k_sort_reg(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-                                                   uint64_t* kout, uint32_t* vout, Count cnt) {
+                                                   uint64_t* kout, uint32_t* vout, Count cnt, int bits) {
+  __shared__ uint32_t whist[32][257];  // per-warp digit counts, then per-warp exclusive offsets
+  __shared__ uint32_t boff[256];
   __shared__ uint64_t sk[1024];
   __shared__ uint32_t sv[1024];
   const int64_t n = cnt.get();
-  const int t = threadIdx.x;
-  int N = 32;
-  while (N < n) N <<= 1;
-  uint64_t key = t < n ? kin[t] : ~0ull;
-  uint32_t val = t < n ? vin[t] : 0xffffffffu;
-  for (int size = 2; size <= N; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      uint64_t pk;
-      uint32_t pv;
-      if (stride >= 32) {
-        __syncthreads();
-        if (t < N) {
-          sk[t] = key;
-          sv[t] = val;
-        }
-        __syncthreads();
-        pk = t < N ? sk[t ^ stride] : key;
-        pv = t < N ? sv[t ^ stride] : val;
-      } else {
-        pk = __shfl_xor_sync(0xffffffffu, key, stride);
-        pv = __shfl_xor_sync(0xffffffffu, val, stride);
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const bool live = t < n;
+  uint64_t key = live ? kin[t] : ~0ull;
+  uint32_t val = live ? vin[t] : 0xffffffffu;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int shift = 0; shift < bits; shift += 8) {
+    for (int i = t; i < 32 * 257; i += 1024) (&whist[0][0])[i] = 0;
+    __syncthreads();
+    const int dg = live ? static_cast<int>((key >> shift) & 0xff) : 256;  // padding sorts last
+    const unsigned peers = __match_any_sync(0xffffffffu, dg);
+    const uint32_t rk = __popc(peers & lt);
+    if ((__ffs(peers) - 1) == lane) whist[w][dg] = __popc(peers);
+    __syncthreads();
+    if (t < 257) {  // per digit: exclusive offsets over warps, total
+      uint32_t run = 0;
+      for (int q = 0; q < 32; ++q) {
+        const uint32_t c = whist[q][t];
+        whist[q][t] = run;
+        run += c;
       }
-      if (t < N) {
-        const bool up = (t & size) == 0;
-        const bool lower = (t & stride) == 0;
-        const bool gt = key > pk || (key == pk && val > pv);  // self after partner
-        const bool take = lower ? (up ? gt : !gt) : (up ? !gt : gt);
-        if (take && !(key == pk && val == pv)) {
-          key = pk;
-          val = pv;
-        }
+      if (t < 256) boff[t] = run;
+    }
+    __syncthreads();
+    if (t < 32) {  // exclusive scan of the 256 digit totals (8 per lane)
+      uint32_t loc[8], sum = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        loc[j] = boff[t * 8 + j];
+        sum += loc[j];
+      }
+      uint32_t inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      uint32_t ex = inc - sum;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        boff[t * 8 + j] = ex;
+        ex += loc[j];
       }
     }
+    __syncthreads();
+    if (live) {
+      const uint32_t pos = boff[dg] + whist[w][dg] + rk;
+      sk[pos] = key;
+      sv[pos] = val;
+    }
+    __syncthreads();
+    if (live) {
+      key = sk[t];
+      val = sv[t];
+    }
   }
-  if (t < n) {
+  if (live) {
     kout[t] = key;
     vout[t] = val;
   }
@@ -311,7 +335,7 @@ int sort_pairs(const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* keys_
                Count cnt, int64_t max_n, int bits, Ws& ws, cudaStream_t s) {
   if (max_n <= 0) return RTEC_OK;
   if (max_n <= 1024) {
-    k_sort_reg<<<1, 1024, 0, s>>>(keys_in, vals_in, keys_out, vals_out, cnt);
+    k_sort_reg<<<1, 1024, 0, s>>>(keys_in, vals_in, keys_out, vals_out, cnt, bits);
     RTEC_LAUNCH_CHECK("k_sort_reg");
     return RTEC_OK;
   }

@@ -161,8 +161,20 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_1pass(F f, Count cnt, O out
 
 // Exclusive scan: out(i, prefix, value) is called for every i < count; *total
 // (device, may be null) receives the sum.  ws needs scan_blocks_for(max)+2 int64.
+// wide: the functor is expensive (dependent global loads per item) -- never the one-CTA path,
+// one item per thread over as many CTAs as it takes
 template <typename F, typename O>
-int exclusive_scan_bs(F f, Count cnt, int64_t max_n, O out, int64_t* total, int64_t* bs, cudaStream_t s) {
+int exclusive_scan_bs(F f, Count cnt, int64_t max_n, O out, int64_t* total, int64_t* bs, cudaStream_t s,
+                      bool wide = false) {
+  if (wide) {
+    const int64_t nb = (max_n + kScanBlock - 1) / kScanBlock;
+    unsigned long long* st = reinterpret_cast<unsigned long long*>(bs);
+    unsigned int* ctr = reinterpret_cast<unsigned int*>(bs + nb);
+    RTEC_CUDA(cudaMemsetAsync(bs, 0, sizeof(int64_t) * (nb + 1), s));
+    k_scan_1pass<F, O, 1><<<static_cast<unsigned>(nb > 0 ? nb : 1), kScanBlock, 0, s>>>(f, cnt, out, total, st, ctr);
+    RTEC_LAUNCH_CHECK("exclusive_scan");
+    return RTEC_OK;
+  }
   if (max_n <= kScanTile) {
     k_scan_one<F, O><<<1, kScanBlock, 0, s>>>(f, cnt, out, total);
     RTEC_LAUNCH_CHECK("exclusive_scan");
@@ -181,10 +193,11 @@ int exclusive_scan_bs(F f, Count cnt, int64_t max_n, O out, int64_t* total, int6
 }
 
 template <typename F, typename O>
-int exclusive_scan(F f, Count cnt, int64_t max_n, O out, int64_t* total, Ws& ws, cudaStream_t s) {
-  int64_t* bs = ws.alloc<int64_t>(scan_blocks_for(max_n) + 2);
+int exclusive_scan(F f, Count cnt, int64_t max_n, O out, int64_t* total, Ws& ws, cudaStream_t s,
+                   bool wide = false) {
+  int64_t* bs = ws.alloc<int64_t>((wide ? (max_n + kScanBlock - 1) / kScanBlock : scan_blocks_for(max_n)) + 2);
   RTEC_WS_CHECK(ws);
-  return exclusive_scan_bs(f, cnt, max_n, out, total, bs, s);
+  return exclusive_scan_bs(f, cnt, max_n, out, total, bs, s, wide);
 }
 
 // common out-functors
