@@ -332,12 +332,12 @@ class RTECEngine:
 
     # ---------------------------------------------------------------- incremental step
     def _graph_key(self, B: int):
-        """Everything a captured step bakes in: the batch size, the workspace and the raw
-        bytes of the graph / batch descriptors (every run-array pointer, slot count and
-        degree array), so a compaction or a batch-buffer reallocation can never replay a
-        graph against moved or freed buffers."""
+        """Everything a captured step bakes in: the batch size and the graph's buffer layout --
+        DynamicGraph.layout_version moves whenever a run array, degree array, the batch buffers
+        or the workspace is rebound (compaction, a larger batch, workspace growth), so a graph
+        is never replayed against moved or freed buffers (the engine's own tensors are fixed)."""
         gr = self.g
-        return (B, gr.ws.data_ptr(), gr.ws.numel(), bytes(gr.c()), bytes(gr.batch.c()))
+        return (B, id(gr), gr.layout_version, gr.ws.data_ptr())
 
     def enqueue_step(self, B: int) -> None:
         """Enqueue the whole incremental pipeline for the staged batch (no sync).

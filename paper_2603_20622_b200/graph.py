@@ -126,6 +126,16 @@ class DeviceBatch:
 class DynamicGraph:
     """Directed graph over [0, n) in B200 HBM (graph.py:59-235 semantics)."""
 
+    # device buffers a captured CUDA graph bakes in: rebinding any of them (compaction, a larger
+    # batch or workspace) bumps `layout_version`, the engine's graph-cache key
+    _LAYOUT_ATTRS = frozenset({"ws", "batch", "out", "inn", "out_deg", "in_deg", "out_deg_prev", "in_deg_prev",
+                               "num_edges_t"})
+
+    def __setattr__(self, name, value):
+        if name in DynamicGraph._LAYOUT_ATTRS:
+            object.__setattr__(self, "layout_version", self.__dict__.get("layout_version", 0) + 1)
+        object.__setattr__(self, name, value)
+
     def __init__(self, num_vertices: int, *, segment_slots: int = 64,
                  density_bounds: tuple[float, float] = (0.25, 0.875), device=None, slack: float | None = None,
                  min_slack: int = 4, reserve: int | None = None):
