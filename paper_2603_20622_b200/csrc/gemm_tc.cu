@@ -105,6 +105,8 @@ constexpr int kSplitThreads = 160;
 constexpr int kEpiBytes = 8 * 32 * 32 * 4;              // 8 epilogue warps x 32 rows x 32 cols
 
 struct TcShape {
+  int probe;        // timing probes (-DRTEC_GEMM_PROBES builds only; wrong results): 1 no B refills,
+                    // 2 no A refills, 4 no split, 8 no epilogue, 16 no MMAs
   int SA, SB;       // ring depths
   int nh;           // N halves (1 or 2)
   int h0;           // width of half 0 (multiple of 16); half 1 = npad - h0
@@ -140,6 +142,13 @@ static int gemm_a_stages() {
 
 static TcShape tc_shape(int npad, bool fused) {
   TcShape sh;
+  sh.probe = 0;
+#ifdef RTEC_GEMM_PROBES  // bottleneck probes for tools/gemm_probe.sh (build with -DRTEC_GEMM_PROBES)
+  {
+    const char* e = getenv("RTEC_GEMM_PROBE");
+    sh.probe = e ? atoi(e) : 0;
+  }
+#endif
   // N > 128 runs in two N-halves (32 KB B stages, deep rings) unless the whole N fits one
   // MMA with a double-buffered B ring: half the MMA issues and ~25 % fewer shared-memory
   // operand reads (A is read once per K-step instead of once per N-half)
@@ -221,6 +230,7 @@ __global__ void __launch_bounds__(512, 1) k_gemm_tc(TcArgs g, TcShape sh) {
         if (j >= sh.SA) mbar_wait(a_empty + sa, static_cast<uint32_t>(((j / sh.SA) - 1) & 1));
         const int64_t tile = blockIdx.x + (j / g.nkb) * gridDim.x;
         const int kb = static_cast<int>(j % g.nkb);
+        if ((sh.probe & 2) && j >= g.nkb) { mbar_arrive(a_full + sa); continue; }
         mbar_expect_tx(a_full + sa, kABlockBytes);
         bulk_g2s(aring + sa * 2 * kABlockBytes, g.A + (tile * g.nkb + kb) * (kABlockBytes / 4), kABlockBytes,
                  a_full + sa);
@@ -239,6 +249,7 @@ __global__ void __launch_bounds__(512, 1) k_gemm_tc(TcArgs g, TcShape sh) {
         const uint32_t hb = static_cast<uint32_t>(nw) * kTK * 4;
         uint8_t* st = bring + sb * sh.bstage;
         const int64_t off = (static_cast<int64_t>(kb) * g.npad + n0) * kTK;
+        if ((sh.probe & 1) && jb >= static_cast<int64_t>(g.nkb) * sh.nh) { mbar_arrive(b_full + sb); continue; }
         mbar_expect_tx(b_full + sb, 2 * hb);
         bulk_g2s(st, g.Bhi + off, hb, b_full + sb);
         bulk_g2s(st + sh.bstage / 2, g.Blo + off, hb, b_full + sb);
@@ -272,7 +283,7 @@ __global__ void __launch_bounds__(512, 1) k_gemm_tc(TcArgs g, TcShape sh) {
           const uint32_t acc_addr = taddr + static_cast<uint32_t>(b * g.npad + n0);
           if (elect_one()) {
 #pragma unroll
-            for (int k = 0; k < kTK / 8; ++k) {
+            for (int k = 0; k < ((sh.probe & 16) ? 0 : kTK / 8); ++k) {
               const uint64_t off = static_cast<uint64_t>(k * 32) >> 4;  // +32 B along K per k-step
               const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
               mma_tf32(acc_addr, dahi + off, dbhi + off, idesc, acc);
@@ -296,7 +307,7 @@ __global__ void __launch_bounds__(512, 1) k_gemm_tc(TcArgs g, TcShape sh) {
       mbar_wait(a_full + sa, static_cast<uint32_t>((j / sh.SA) & 1));
       float4* raw = reinterpret_cast<float4*>(aring + sa * 2 * kABlockBytes);
       float4* hi = reinterpret_cast<float4*>(aring + sa * 2 * kABlockBytes + kABlockBytes);
-      for (int idx = st_id; idx < kABlockBytes / 16; idx += kSplitThreads) {
+      for (int idx = st_id; idx < ((sh.probe & 4) && j >= g.nkb ? 0 : kABlockBytes / 16); idx += kSplitThreads) {
         float4 x = raw[idx];
         float4 hv = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
         hi[idx] = hv;
@@ -379,7 +390,7 @@ __global__ void __launch_bounds__(512, 1) k_gemm_tc(TcArgs g, TcShape sh) {
       }
       mbar_wait(tfull + b, static_cast<uint32_t>((t >> 1) & 1));
       tc_fence_after();
-      for (int cc = cbeg; cc < cend; ++cc) {
+      for (int cc = cbeg; cc < ((sh.probe & 8) ? cbeg : cend); ++cc) {
         const int c0 = cc * 32;
         if (fused) {
           if (cc + 1 < cend) {
