@@ -5,6 +5,7 @@
 #include <stdio.h>
 
 #include <string>
+#include <utility>
 
 #include "../../include/rtec.h"
 
@@ -56,6 +57,42 @@ struct ProfScope {
   }
 };
 #define RTEC_PROF(name, stream) ::rtec::ProfScope _rtec_prof_scope_##__LINE__(name, stream)
+
+// ---------------------------------------------------------------- launches
+// Programmatic dependent launch (PDL).  Every kernel begins with RTEC_PDL_ENTRY():
+// griddepcontrol.wait blocks until the preceding grid in the stream has completed and
+// its writes are visible (a no-op for a normal launch).  launch() issues every library
+// kernel with programmatic stream serialization, so the next kernel of a dependent
+// chain (and its CUDA-graph node, which keeps the programmatic edge) is launched as the
+// predecessor's CTAs exit instead of after its completion is processed.  An explicit
+// early griddepcontrol.launch_dependents (RTEC_PDL_TRIGGER=1 builds) makes the next
+// grid's CTAs resident during the predecessor's last wave; measured slower on the
+// two-stream passes (profiles/r02t_pdl_ab.md), so the default trigger is CTA exit.
+// RTEC_PDL=0 turns the attribute off (plain stream order; A/B).
+#ifndef RTEC_PDL_TRIGGER
+#define RTEC_PDL_TRIGGER 0
+#endif
+#if RTEC_PDL_TRIGGER
+#define RTEC_PDL_ENTRY() asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
+#else  // dependents launch as this grid's CTAs exit (no early residency)
+#define RTEC_PDL_ENTRY() asm volatile("griddepcontrol.wait;" ::: "memory")
+#endif
+bool pdl_on();
+
+template <typename... KArgs, typename... Args>
+inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  (void)cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);  // errors: RTEC_LAUNCH_CHECK
+}
 
 // ---------------------------------------------------------------- side stream
 // Library-owned side stream + fork / join events for independent passes inside one

@@ -18,6 +18,7 @@ constexpr int kFBlk = 256;
 // Dg bits and dst(I ∪ D) bits
 __global__ void k_seed_layer0(const rtec_batch_t b, int32_t src_degree_dependent, uint32_t* bm_src,
                               uint32_t* bm_dst) {
+  RTEC_PDL_ENTRY();
   if (err_set(b.err)) return;
   int64_t nd = *b.n_delta, na = *b.n_applied;
   int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -35,6 +36,7 @@ __global__ void k_seed_layer0(const rtec_batch_t b, int32_t src_degree_dependent
 
 __global__ void k_union_words(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, uint32_t* out,
                               int64_t words) {
+  RTEC_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < words; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = a[i] | b[i];
 }
@@ -51,6 +53,7 @@ struct WordPop {
 // thread per word writes its bits (many CTAs; the scan's out-functor stays cheap)
 __global__ void __launch_bounds__(kFBlk) k_word_list(WordPop f, const int64_t* __restrict__ woff, int64_t words,
                                                      int32_t* list, int32_t* slot) {
+  RTEC_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < words; i += (int64_t)gridDim.x * blockDim.x) {
     uint32_t w = f.word(i);
     int64_t off = woff[i];
@@ -68,7 +71,7 @@ __global__ void __launch_bounds__(kFBlk) k_word_list(WordPop f, const int64_t* _
 static int bitmap_to_list(WordPop f, int64_t words, int32_t* list, int32_t* slot, int64_t* count, int64_t* woff,
                           Ws& w, cudaStream_t s) {
   RTEC_TRY(exclusive_scan(f, Count{nullptr, words}, words, StorePrefix{woff}, count, w, s));
-  k_word_list<<<grid_for(words, kFBlk), kFBlk, 0, s>>>(f, woff, words, list, slot);
+  launch(k_word_list, grid_for(words, kFBlk), kFBlk, 0, s, f, woff, words, list, slot);
   RTEC_LAUNCH_CHECK("k_word_list");
   return RTEC_OK;
 }
@@ -98,6 +101,7 @@ __device__ __forceinline__ bool pull_mode(const int64_t* n_new, const int64_t* o
 __global__ void __launch_bounds__(kFBlk) k_expand(const int32_t* __restrict__ nlist, const int64_t* n_new,
                                                   const int64_t* __restrict__ off, rtec_adj_t out,
                                                   uint32_t* bm_dst, const int64_t* num_edges) {
+  RTEC_PDL_ENTRY();
   int64_t N = *n_new;
   if (N == 0 || pull_mode(n_new, off, num_edges)) return;
   int64_t E = off[N];
@@ -127,6 +131,7 @@ __global__ void __launch_bounds__(kFBlk) k_expand(const int32_t* __restrict__ nl
 __global__ void __launch_bounds__(kFBlk) k_pull(const uint32_t* __restrict__ bm_src, const uint32_t* __restrict__ prev_src,
                                                 const int64_t* n_new, const int64_t* __restrict__ off,
                                                 const int64_t* num_edges, rtec_adj_t in, int64_t n, uint32_t* bm_dst) {
+  RTEC_PDL_ENTRY();
   if (!pull_mode(n_new, off, num_edges)) return;
   int64_t words = (n + 31) / 32;
   int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -158,6 +163,7 @@ __global__ void k_counters(const int32_t* __restrict__ slist, const int64_t* n_s
                            const int32_t* __restrict__ out_len, const int32_t* __restrict__ in_len,
                            const int32_t* __restrict__ dlist, const rtec_batch_t b, const uint32_t* bm_src,
                            int64_t* counters) {
+  RTEC_PDL_ENTRY();
   int64_t ns = *n_src, nd = *n_dst, na = err_set(b.err) ? 0 : *b.n_applied;
   int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -215,14 +221,14 @@ extern "C" int rtec_frontier_layer(const rtec_graph_t* g, const rtec_batch_t* b,
     RTEC_CUDA(cudaMemsetAsync(f->bm_src, 0, sizeof(uint32_t) * words, s));
     RTEC_CUDA(cudaMemsetAsync(f->bm_dst, 0, sizeof(uint32_t) * words, s));
     // sharded: Dg is the global out-degree change set, not the shard's DegreeDelta
-    k_seed_layer0<<<grid_for(b->cap * 2, kFBlk), kFBlk, 0, s>>>(*b, b->dg_bm ? 0 : src_degree_dependent, f->bm_src,
+    launch(k_seed_layer0, grid_for(b->cap * 2, kFBlk), kFBlk, 0, s, *b, b->dg_bm ? 0 : src_degree_dependent, f->bm_src,
                                                                  f->bm_dst);
     if (b->dg_bm && src_degree_dependent)
-      k_union_words<<<grid_for(words, kFBlk), kFBlk, 0, s>>>(f->bm_src, b->dg_bm, f->bm_src, words);
+      launch(k_union_words, grid_for(words, kFBlk), kFBlk, 0, s, f->bm_src, b->dg_bm, f->bm_src, words);
   } else {
     // S(l) = S(l-1) ∪ V_chg(l-1); V_dst(l) starts as V_dst(l-1) (this shard's part when sharded)
     const uint32_t* chg = prev->bm_chg ? prev->bm_chg : prev->bm_dst;
-    k_union_words<<<grid_for(words, kFBlk), kFBlk, 0, s>>>(prev->bm_src, chg, f->bm_src, words);
+    launch(k_union_words, grid_for(words, kFBlk), kFBlk, 0, s, prev->bm_src, chg, f->bm_src, words);
     RTEC_CUDA(cudaMemcpyAsync(f->bm_dst, prev->bm_dst, sizeof(uint32_t) * words, cudaMemcpyDeviceToDevice, s));
     prev_src = prev->bm_src;
   }
@@ -232,8 +238,8 @@ extern "C" int rtec_frontier_layer(const rtec_graph_t* g, const rtec_batch_t* b,
   RTEC_TRY(exclusive_scan(OutLenOf{nlist, g->out.len}, Count{n_new, n}, n, StoreOffTailF{noff, n_new}, nullptr, w, s));
   {
     RTEC_PROF("k_expand", s);
-    k_expand<<<kSMs * 8, kFBlk, 0, s>>>(nlist, n_new, noff, g->out, f->bm_dst, g->num_edges);
-    k_pull<<<kSMs * 8, kFBlk, 0, s>>>(f->bm_src, prev_src, n_new, noff, g->num_edges, g->in, n, f->bm_dst);
+    launch(k_expand, kSMs * 8, kFBlk, 0, s, nlist, n_new, noff, g->out, f->bm_dst, g->num_edges);
+    launch(k_pull, kSMs * 8, kFBlk, 0, s, f->bm_src, prev_src, n_new, noff, g->num_edges, g->in, n, f->bm_dst);
   }
   RTEC_LAUNCH_CHECK("k_expand");
   // lists + slots
@@ -241,7 +247,7 @@ extern "C" int rtec_frontier_layer(const rtec_graph_t* g, const rtec_batch_t* b,
   RTEC_TRY(bitmap_to_list(sp, words, f->src_list, f->src_slot, f->n_src, woff, w, s));
   WordPop dp{f->bm_dst, nullptr};
   RTEC_TRY(bitmap_to_list(dp, words, f->dst_list, f->dst_slot, f->n_dst, woff, w, s));
-  k_counters<<<kSMs * 2, kFBlk, 0, s>>>(f->src_list, f->n_src, f->n_dst, g->out.len, g->in.len, f->dst_list, *b,
+  launch(k_counters, kSMs * 2, kFBlk, 0, s, f->src_list, f->n_src, f->n_dst, g->out.len, g->in.len, f->dst_list, *b,
                                         f->bm_src, f->counters);
   RTEC_LAUNCH_CHECK("k_counters");
   return RTEC_OK;
@@ -283,6 +289,7 @@ struct SampleBeg {
 __global__ void __launch_bounds__(kFBlk) k_ns_sample(rtec_adj_t in, const int32_t* __restrict__ rows,
                                                      const int64_t* n_rows, int64_t max_rows, int32_t fanout,
                                                      uint64_t seed, int32_t hop, rtec_adj_t smp, uint32_t* bm_next) {
+  RTEC_PDL_ENTRY();
   const int64_t nr = n_rows ? *n_rows : max_rows;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -340,7 +347,7 @@ extern "C" int rtec_ns_sample(const rtec_adj_t* in, const int32_t* rows, const i
   RTEC_CUDA(cudaMemsetAsync(bm_next, 0, sizeof(uint32_t) * ((n + 31) / 32), s));
   RTEC_TRY(exclusive_scan(SampleCount{rows, in->len, fanout}, Count{n_rows, max_rows}, max_rows,
                           SampleBeg{rows, sampled->beg, sampled->len}, sampled->top, w, s));
-  k_ns_sample<<<kSMs * 8, kFBlk, 0, s>>>(*in, rows, n_rows, max_rows, fanout, seed, hop, *sampled, bm_next);
+  launch(k_ns_sample, kSMs * 8, kFBlk, 0, s, *in, rows, n_rows, max_rows, fanout, seed, hop, *sampled, bm_next);
   RTEC_LAUNCH_CHECK("k_ns_sample");
   return RTEC_OK;
 }
@@ -360,6 +367,7 @@ extern "C" int rtec_bitmap_to_list(const uint32_t* bm, int64_t n, int32_t* list,
 namespace rtec {
 __global__ void __launch_bounds__(kFBlk) k_in_expand(rtec_adj_t in, const int32_t* __restrict__ rows,
                                                      const int64_t* n_rows, int64_t max_rows, uint32_t* bm) {
+  RTEC_PDL_ENTRY();
   const int64_t nr = n_rows ? *n_rows : max_rows;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -381,7 +389,7 @@ extern "C" int rtec_in_expand(const rtec_adj_t* in, const int32_t* rows, const i
                               uint32_t* bm, rtec_stream_t stream) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (max_rows <= 0) return RTEC_OK;
-  k_in_expand<<<kSMs * 8, kFBlk, 0, s>>>(*in, rows, n_rows, max_rows, bm);
+  launch(k_in_expand, kSMs * 8, kFBlk, 0, s, *in, rows, n_rows, max_rows, bm);
   RTEC_LAUNCH_CHECK("k_in_expand");
   return RTEC_OK;
 }

@@ -171,6 +171,7 @@ static TcShape tc_shape(int npad, bool fused) {
 }
 
 __global__ void __launch_bounds__(512, 1) k_gemm_tc(TcArgs g, TcShape sh) {
+  RTEC_PDL_ENTRY();
   extern __shared__ uint8_t smem_raw[];
   if (g.err && err_set(g.err)) return;
   const int64_t nrows = g.n_rows ? *g.n_rows : g.max_rows;
@@ -480,6 +481,7 @@ __global__ void __launch_bounds__(512, 1) k_gemm_tc(TcArgs g, TcShape sh) {
 
 // W [d_out, d_in] -> Bhi/Blo [nkb][npad][32] swizzled, zero padded
 __global__ void k_prep_b(const float* __restrict__ W, int d_in, int d_out, int nkb, int npad, float* Bhi, float* Blo) {
+  RTEC_PDL_ENTRY();
   int64_t total = static_cast<int64_t>(nkb) * npad * kTK;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     int kb = static_cast<int>(e / (static_cast<int64_t>(npad) * kTK));
@@ -500,6 +502,7 @@ __global__ void k_prep_b(const float* __restrict__ W, int d_in, int d_out, int n
 // store per lane into its swizzled 16-byte slot
 __global__ void k_pack_rows(const float* __restrict__ X, int64_t ld, int d, const int32_t* __restrict__ rows,
                             const int64_t* n_rows, int64_t n_all, float* __restrict__ img, int nkb, const uint64_t* err) {
+  RTEC_PDL_ENTRY();
   if (err && err_set(err)) return;
   const int64_t nr = n_rows ? *n_rows : n_all;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -527,7 +530,7 @@ int gemm_tc_pack_rows(const float* X, int64_t ld, int d, const int32_t* rows, co
                       float* img, int nkb, const uint64_t* err, cudaStream_t s) {
   if (n_all <= 0) return RTEC_OK;
   RTEC_PROF("k_pack_rows", s);
-  k_pack_rows<<<grid_for(n_all * 32, 256, kSMs * 8), 256, 0, s>>>(X, ld, d, rows, n_rows, n_all, img, nkb, err);
+  launch(k_pack_rows, grid_for(n_all * 32, 256, kSMs * 8), 256, 0, s, X, ld, d, rows, n_rows, n_all, img, nkb, err);
   RTEC_LAUNCH_CHECK("k_pack_rows");
   return RTEC_OK;
 }
@@ -551,7 +554,7 @@ int gemm_tc_launch(const TcArgs& g, cudaStream_t s) {
   int64_t tiles = (g.max_rows + kTM - 1) / kTM;
   int grid = static_cast<int>(tiles < kSMs ? tiles : kSMs);
   RTEC_PROF("k_gemm_tc", s);
-  k_gemm_tc<<<grid, 512, smem, s>>>(g, tc_shape(g.npad, fused));
+  launch(k_gemm_tc, grid, 512, smem, s, g, tc_shape(g.npad, fused));
   RTEC_LAUNCH_CHECK("k_gemm_tc");
   return RTEC_OK;
 }
@@ -574,7 +577,7 @@ int rtec_gemm_prepare_weights(const float* W, int32_t d_in, int32_t d_out, float
   int nkb = (d_in + kTK - 1) / kTK;
   int npad = (d_out + 15) / 16 * 16;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  k_prep_b<<<grid_for(static_cast<int64_t>(nkb) * npad * kTK, 256), 256, 0, s>>>(W, d_in, d_out, nkb, npad, Bhi, Blo);
+  launch(k_prep_b, grid_for(static_cast<int64_t>(nkb) * npad * kTK, 256), 256, 0, s, W, d_in, d_out, nkb, npad, Bhi, Blo);
   RTEC_LAUNCH_CHECK("k_prep_b");
   return RTEC_OK;
 }

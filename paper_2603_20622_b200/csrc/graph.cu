@@ -24,12 +24,14 @@ __host__ __device__ __forceinline__ int32_t cap_for(int32_t len, float slack, in
 
 // ------------------------------------------------------------------ small kernels
 __global__ void k_fill_u64(uint64_t* p, uint64_t v, int64_t n) {
+  RTEC_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
 }
 
 // degrees of a bulk edge list (from_edges graph.py:101-102, :118-119)
 __global__ void k_count_degrees(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t m,
                                 int64_t n, int32_t* out_deg, int32_t* in_deg, uint64_t* err) {
+  RTEC_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
     int32_t s = src[i], d = dst[i];
     if (s < 0 || s >= n || d < 0 || d >= n) {
@@ -63,6 +65,7 @@ struct StoreBeg {
 
 __global__ void k_make_keys_bulk(const int32_t* __restrict__ a, const int32_t* __restrict__ b, int64_t m, int64_t n,
                                  uint64_t* keys, uint32_t* vals) {
+  RTEC_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
     keys[i] = static_cast<uint64_t>(a[i]) * static_cast<uint64_t>(n) + static_cast<uint64_t>(b[i]);
     vals[i] = static_cast<uint32_t>(i);
@@ -73,6 +76,7 @@ __global__ void k_make_keys_bulk(const int32_t* __restrict__ a, const int32_t* _
 __global__ void k_fill_runs(const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ sidx, int64_t m, int64_t n,
                             const int64_t* __restrict__ beg, int32_t* __restrict__ nbr, int64_t* __restrict__ ts_out,
                             const int64_t* __restrict__ ts_in, uint64_t* err) {
+  RTEC_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t k = skeys[i];
     if (i > 0 && skeys[i - 1] == k) report_error(err, RTEC_CONFIG_ERROR, 1);
@@ -98,10 +102,10 @@ static int build_direction(int64_t n, rtec_adj_t* a, const int32_t* own, const i
   uint64_t* sk = ws.alloc<uint64_t>(m);
   uint32_t* sv = ws.alloc<uint32_t>(m);
   RTEC_WS_CHECK(ws);
-  k_make_keys_bulk<<<grid_for(m, kBlk), kBlk, 0, s>>>(own, nb, m, n, keys, vals);
+  launch(k_make_keys_bulk, grid_for(m, kBlk), kBlk, 0, s, own, nb, m, n, keys, vals);
   int bits = bits_for(static_cast<uint64_t>(n) * static_cast<uint64_t>(n));
   RTEC_TRY(sort_pairs(keys, vals, sk, sv, Count{nullptr, m}, m, bits, ws, s));
-  k_fill_runs<<<grid_for(m, kBlk), kBlk, 0, s>>>(sk, sv, m, n, a->beg, a->nbr, a->ts, ts, err);
+  launch(k_fill_runs, grid_for(m, kBlk), kBlk, 0, s, sk, sv, m, n, a->beg, a->nbr, a->ts, ts, err);
   RTEC_LAUNCH_CHECK("k_fill_runs");
   return RTEC_OK;
 }
@@ -112,6 +116,7 @@ __global__ void k_copy_runs(int64_t n, const int64_t* __restrict__ beg, const in
                             const int32_t* __restrict__ nbr, const int64_t* __restrict__ ts,
                             const int64_t* __restrict__ off, int32_t* out_v, int32_t* out_nbr, int64_t* out_ts,
                             int64_t* new_beg, int32_t* new_len) {
+  RTEC_PDL_ENTRY();
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int lane = lane_id();
@@ -142,6 +147,7 @@ struct LenAt {
 // ------------------------------------------------------------------ coalesce
 __global__ void k_coalesce_keys(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t B,
                                 uint64_t* keys, uint32_t* vals) {
+  RTEC_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x) {
     keys[i] = (static_cast<uint64_t>(static_cast<uint32_t>(src[i])) << 32) | static_cast<uint32_t>(dst[i]);
     vals[i] = static_cast<uint32_t>(i);
@@ -152,6 +158,7 @@ __global__ void k_coalesce_keys(const int32_t* __restrict__ src, const int32_t* 
 // record the survivor at the key's first position.
 __global__ void k_coalesce_fold(const uint64_t* __restrict__ sk, const uint32_t* __restrict__ sv, int64_t B,
                                 const uint8_t* __restrict__ op, uint8_t* keep) {
+  RTEC_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x) {
     if (i > 0 && sk[i - 1] == sk[i]) continue;  // not a head
     uint32_t first = sv[i];
@@ -171,6 +178,7 @@ __global__ void k_coalesce_fold(const uint64_t* __restrict__ sk, const uint32_t*
 
 __global__ void k_coalesce_map(const uint64_t* __restrict__ sk, const uint32_t* __restrict__ sv_orig,
                                const uint32_t* __restrict__ sv_surv, int64_t B, uint32_t* surv_at_first) {
+  RTEC_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x) {
     if (i > 0 && sk[i - 1] == sk[i]) continue;
     surv_at_first[sv_orig[i]] = sv_surv[i];
@@ -199,6 +207,7 @@ struct CoalesceOut {
 // ------------------------------------------------------------------ apply: validation + probe
 __global__ void k_apply_keys(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t B, int64_t n,
                              uint64_t* keys, uint32_t* vals, uint64_t* err) {
+  RTEC_PDL_ENTRY();
   uint64_t inval = static_cast<uint64_t>(n) * static_cast<uint64_t>(n);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x) {
     int32_t s = src[i], d = dst[i];
@@ -211,6 +220,7 @@ __global__ void k_apply_keys(const int32_t* __restrict__ src, const int32_t* __r
 
 __global__ void k_apply_dups(const uint64_t* __restrict__ sk, const uint32_t* __restrict__ sv, int64_t B, int64_t n,
                              uint64_t* err) {
+  RTEC_PDL_ENTRY();
   uint64_t inval = static_cast<uint64_t>(n) * static_cast<uint64_t>(n);
   for (int64_t i = 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x) {
     if (sk[i] == sk[i - 1] && sk[i] != inval) report_error(err, RTEC_CONFIG_ERROR, sv[i]);  // graph.py:195-197
@@ -224,6 +234,7 @@ __global__ void k_apply_dups(const uint64_t* __restrict__ sk, const uint32_t* __
 __global__ void k_apply_probe(const uint64_t* __restrict__ sk, const uint32_t* __restrict__ sv, int64_t B, int64_t n,
                               rtec_adj_t out, const uint8_t* __restrict__ op, uint8_t* status, uint8_t* aflag,
                               int32_t part_rank, int32_t part_count, const uint64_t* err) {
+  RTEC_PDL_ENTRY();
   if (err_set(err)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t k = sk[i];
@@ -268,6 +279,7 @@ struct CompactApplied {
 
 __global__ void k_in_keys(const int32_t* __restrict__ as, const int32_t* __restrict__ ad, const int64_t* cnt, int64_t n,
                           uint64_t* keys, uint32_t* vals) {
+  RTEC_PDL_ENTRY();
   int64_t K = *cnt;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x) {
     keys[i] = static_cast<uint64_t>(ad[i]) * n + static_cast<uint64_t>(as[i]);
@@ -278,6 +290,7 @@ __global__ void k_in_keys(const int32_t* __restrict__ as, const int32_t* __restr
 __global__ void k_in_gather(const uint32_t* __restrict__ sv, const int64_t* cnt, const int32_t* __restrict__ as,
                             const int32_t* __restrict__ ad, const uint8_t* __restrict__ ao, int32_t* is, int32_t* id,
                             uint8_t* io) {
+  RTEC_PDL_ENTRY();
   int64_t K = *cnt;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x) {
     uint32_t e = sv[i];
@@ -349,6 +362,7 @@ struct StoreHead {
 
 __global__ void k_group_info(MergeIn in, MergePlan p, rtec_adj_t a, float slack, int32_t min_slack,
                              const uint64_t* err) {
+  RTEC_PDL_ENTRY();
   int64_t G = *p.G;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x) {
     int64_t s = p.gstart[g], e = p.gstart[g + 1];
@@ -393,6 +407,7 @@ struct StoreOffTail {
 
 // reserve arena space for relocated runs (single thread): all-or-nothing
 __global__ void k_reserve(MergePlan p, rtec_adj_t a, uint64_t* err, int64_t* ctr) {
+  RTEC_PDL_ENTRY();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   int64_t G = *p.G;
   int64_t demand = G > 0 ? p.arena_off[G] : 0;
@@ -414,12 +429,14 @@ __global__ void k_reserve(MergePlan p, rtec_adj_t a, uint64_t* err, int64_t* ctr
 }
 
 __global__ void k_commit_reserve(MergePlan p, rtec_adj_t a, const uint64_t* err) {
+  RTEC_PDL_ENTRY();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   if (err_set(err)) return;
   *a.top = p.totals[3] + p.totals[2];
 }
 
 __global__ void k_set_dest(MergePlan p, const uint64_t* err) {
+  RTEC_PDL_ENTRY();
   int64_t G = *p.G;
   int64_t base = p.totals[3];
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x) {
@@ -479,6 +496,7 @@ __device__ __forceinline__ int64_t group_of(const TileGroups& tg, const int64_t*
 // element-parallel merge: old elements (from the first changed position) and update items of every group
 __global__ void __launch_bounds__(kBlk) k_merge_items(MergeIn in, MergePlan p, rtec_adj_t a, const uint64_t* err,
                                                       bool choose) {
+  RTEC_PDL_ENTRY();
   __shared__ int64_t s_off[kMT];
   __shared__ int64_t s_g[2];
   if (err_set(err)) return;
@@ -563,6 +581,7 @@ __device__ __forceinline__ void merge_put(const MergePlan& p, const rtec_adj_t& 
 
 __global__ void __launch_bounds__(kBlk) k_merge_items_warp(MergeIn in, MergePlan p, rtec_adj_t a,
                                                            const uint64_t* err, bool choose) {
+  RTEC_PDL_ENTRY();
   if (err_set(err)) return;
   const int64_t G = *p.G;
   if (G == 0) return;
@@ -651,6 +670,7 @@ __global__ void __launch_bounds__(kBlk) k_merge_items_warp(MergeIn in, MergePlan
 // copy in-place runs back from scratch, a warp per kWC scratch positions walking its groups
 __global__ void __launch_bounds__(kBlk) k_merge_copyback_warp(MergePlan p, rtec_adj_t a, const uint64_t* err,
                                                               bool choose) {
+  RTEC_PDL_ENTRY();
   if (err_set(err)) return;
   const int64_t G = *p.G;
   if (G == 0) return;
@@ -682,6 +702,7 @@ __global__ void __launch_bounds__(kBlk) k_merge_copyback_warp(MergePlan p, rtec_
 // copy in-place runs back from scratch (after all reads of the old runs)
 __global__ void __launch_bounds__(kBlk) k_merge_copyback(MergePlan p, rtec_adj_t a, const uint64_t* err,
                                                          bool choose) {
+  RTEC_PDL_ENTRY();
   __shared__ int64_t s_off[kMT];
   __shared__ int64_t s_g[2];
   if (err_set(err)) return;
@@ -704,6 +725,7 @@ __global__ void __launch_bounds__(kBlk) k_merge_copyback(MergePlan p, rtec_adj_t
 }
 
 __global__ void k_merge_commit(MergePlan p, rtec_adj_t a, const uint64_t* err) {
+  RTEC_PDL_ENTRY();
   if (err_set(err)) return;
   int64_t G = *p.G;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x) {
@@ -746,7 +768,7 @@ static int merge_plan(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, floa
   Count K{in.K, in.maxK};
   RTEC_TRY(exclusive_scan(IsIns{in.op}, K, in.maxK, StorePrefixTail{p.pre_ins, in.K}, nullptr, ws, s));
   RTEC_TRY(exclusive_scan(IsHead{in.own}, K, in.maxK, StoreHead{in.own, p.gstart, p.gv, in.K}, p.G, ws, s));
-  k_group_info<<<grid_for(in.maxK, kBlk), kBlk, 0, s>>>(in, p, a, slack, min_slack, err);
+  launch(k_group_info, grid_for(in.maxK, kBlk), kBlk, 0, s, in, p, a, slack, min_slack, err);
   Count G{p.G, in.maxK};
   RTEC_CUDA(cudaMemsetAsync(p.work_off, 0, sizeof(int64_t), s));
   RTEC_CUDA(cudaMemsetAsync(p.scr_off, 0, sizeof(int64_t), s));
@@ -754,8 +776,8 @@ static int merge_plan(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, floa
   RTEC_TRY(exclusive_scan(WorkOf{p, a.len}, G, in.maxK, StoreOffTail{p.work_off, p.G}, nullptr, ws, s));
   RTEC_TRY(exclusive_scan(ScrOf{p}, G, in.maxK, StoreOffTail{p.scr_off, p.G}, nullptr, ws, s));
   RTEC_TRY(exclusive_scan(ArenaOf{p}, G, in.maxK, StoreOffTail{p.arena_off, p.G}, nullptr, ws, s));
-  k_reserve<<<1, 32, 0, s>>>(p, a, err, ctr);
-  k_set_dest<<<grid_for(in.maxK, kBlk), kBlk, 0, s>>>(p, err);
+  launch(k_reserve, 1, 32, 0, s, p, a, err, ctr);
+  launch(k_set_dest, grid_for(in.maxK, kBlk), kBlk, 0, s, p, err);
   RTEC_LAUNCH_CHECK("merge_plan");
   return RTEC_OK;
 }
@@ -780,14 +802,14 @@ static int merge_exec(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, int6
   const int mode = merge_mode();
   const bool warp = mode == 2 || (mode == 1 && a.slots > 96 * (n > 0 ? n : 1));
   if (warp) {
-    k_merge_items_warp<<<grid_for(work_bound, kWC * (kBlk / 32), kSMs * 8), kBlk, 0, s>>>(in, p, a, err, false);
-    k_merge_copyback_warp<<<grid_for(work_bound, kWC * (kBlk / 32), kSMs * 8), kBlk, 0, s>>>(p, a, err, false);
+    launch(k_merge_items_warp, grid_for(work_bound, kWC * (kBlk / 32), kSMs * 8), kBlk, 0, s, in, p, a, err, false);
+    launch(k_merge_copyback_warp, grid_for(work_bound, kWC * (kBlk / 32), kSMs * 8), kBlk, 0, s, p, a, err, false);
   } else {
-    k_merge_items<<<grid_for(work_bound, kMT, kSMs * 8), kBlk, 0, s>>>(in, p, a, err, false);
-    k_merge_copyback<<<grid_for(work_bound, kMT, kSMs * 8), kBlk, 0, s>>>(p, a, err, false);
+    launch(k_merge_items, grid_for(work_bound, kMT, kSMs * 8), kBlk, 0, s, in, p, a, err, false);
+    launch(k_merge_copyback, grid_for(work_bound, kMT, kSMs * 8), kBlk, 0, s, p, a, err, false);
   }
-  k_merge_commit<<<grid_for(in.maxK, kBlk), kBlk, 0, s>>>(p, a, err);
-  k_commit_reserve<<<1, 32, 0, s>>>(p, a, err);
+  launch(k_merge_commit, grid_for(in.maxK, kBlk), kBlk, 0, s, p, a, err);
+  launch(k_commit_reserve, 1, 32, 0, s, p, a, err);
   RTEC_LAUNCH_CHECK("merge_exec");
   return RTEC_OK;
 }
@@ -795,6 +817,7 @@ static int merge_exec(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, int6
 // per-destination ranges of the in-key ordered applied list (replaces a binary
 // search per destination in the layer kernels)
 __global__ void k_irange_set(const int32_t* __restrict__ id, const int64_t* cnt, int2* irange, const uint64_t* err) {
+  RTEC_PDL_ENTRY();
   if (err_set(err)) return;
   int64_t K = *cnt;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x) {
@@ -807,6 +830,7 @@ __global__ void k_irange_set(const int32_t* __restrict__ id, const int64_t* cnt,
 }
 
 __global__ void k_irange_reset(const int32_t* __restrict__ id, const int64_t* cnt, int2* irange) {
+  RTEC_PDL_ENTRY();
   int64_t K = *cnt;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x)
     irange[id[i]] = make_int2(-1, 0);
@@ -816,6 +840,7 @@ __global__ void k_irange_reset(const int32_t* __restrict__ id, const int64_t* cn
 __global__ void k_apply_degrees(const int32_t* __restrict__ as, const int32_t* __restrict__ ad,
                                 const uint8_t* __restrict__ ao, const int64_t* cnt, int32_t* out_deg,
                                 int32_t* in_deg, int64_t* num_edges, const uint64_t* err) {
+  RTEC_PDL_ENTRY();
   if (err_set(err)) return;
   int64_t K = *cnt;
   int64_t local = 0;
@@ -833,6 +858,7 @@ __global__ void k_apply_degrees(const int32_t* __restrict__ as, const int32_t* _
 // endpoints of the applied updates -> bits of a touched-vertex bitmap
 __global__ void k_touched_bits(const int32_t* __restrict__ as, const int32_t* __restrict__ ad, const int64_t* cnt,
                                uint32_t* bm) {
+  RTEC_PDL_ENTRY();
   const int64_t K = *cnt;
   for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~int64_t(31); i0 < K;
        i0 += (int64_t)gridDim.x * blockDim.x) {
@@ -881,6 +907,7 @@ struct TouchedRows {
 
 __global__ void k_commit_degrees(const int32_t* __restrict__ dv, const int64_t* cnt, const int32_t* in_deg,
                                  const int32_t* out_deg, int32_t* in_prev, int32_t* out_prev) {
+  RTEC_PDL_ENTRY();
   int64_t K = *cnt;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x) {
     int32_t v = dv[i];
@@ -924,7 +951,7 @@ extern "C" {
 int rtec_graph_count(const int32_t* src, const int32_t* dst, int64_t m, int64_t n, int32_t* out_deg,
                      int32_t* in_deg, uint64_t* err, rtec_stream_t stream) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (m > 0) k_count_degrees<<<grid_for(m, kBlk), kBlk, 0, s>>>(src, dst, m, n, out_deg, in_deg, err);
+  if (m > 0) launch(k_count_degrees, grid_for(m, kBlk), kBlk, 0, s, src, dst, m, n, out_deg, in_deg, err);
   RTEC_LAUNCH_CHECK("k_count_degrees");
   return RTEC_OK;
 }
@@ -963,7 +990,7 @@ int rtec_adj_export(int64_t n, const rtec_adj_t* a, int32_t* out_v, int32_t* out
   int64_t* off = w.alloc<int64_t>(n + 1);
   RTEC_WS_CHECK(w);
   RTEC_TRY(exclusive_scan(LenAt{a->len}, Count{nullptr, n}, n, StorePrefix{off}, nullptr, w, s));
-  k_copy_runs<<<grid_for(n * 32, kBlk, kSMs * 16), kBlk, 0, s>>>(n, a->beg, a->len, a->nbr, a->ts, off, out_v,
+  launch(k_copy_runs, grid_for(n * 32, kBlk, kSMs * 16), kBlk, 0, s, n, a->beg, a->len, a->nbr, a->ts, off, out_v,
                                                                  out_nbr, out_ts, nullptr, nullptr);
   RTEC_LAUNCH_CHECK("k_copy_runs");
   return RTEC_OK;
@@ -976,7 +1003,7 @@ int rtec_adj_compact(int64_t n, const rtec_adj_t* src, rtec_adj_t* dst, float sl
   // new beg/cap from current lengths (dst->len receives the lengths)
   RTEC_TRY(exclusive_scan(CapOf{src->len, slack, min_slack}, Count{nullptr, n}, n,
                           StoreBeg{src->len, dst->beg, dst->cap, dst->len}, dst->top, w, s));
-  k_copy_runs<<<grid_for(n * 32, kBlk, kSMs * 16), kBlk, 0, s>>>(n, src->beg, src->len, src->nbr, src->ts, dst->beg,
+  launch(k_copy_runs, grid_for(n * 32, kBlk, kSMs * 16), kBlk, 0, s, n, src->beg, src->len, src->nbr, src->ts, dst->beg,
                                                                  nullptr, dst->nbr, dst->ts, nullptr, nullptr);
   RTEC_LAUNCH_CHECK("compact");
   return RTEC_OK;
@@ -997,12 +1024,12 @@ int rtec_batch_coalesce(const int32_t* src, const int32_t* dst, const uint8_t* o
   uint8_t* keep = w.alloc<uint8_t>(B);
   uint32_t* surv = w.alloc<uint32_t>(B);
   RTEC_WS_CHECK(w);
-  k_coalesce_keys<<<grid_for(B, kBlk), kBlk, 0, s>>>(src, dst, B, keys, vals);
+  launch(k_coalesce_keys, grid_for(B, kBlk), kBlk, 0, s, src, dst, B, keys, vals);
   RTEC_TRY(sort_pairs(keys, vals, sk, sv, Count{nullptr, B}, B, 64, w, s));
   RTEC_CUDA(cudaMemcpyAsync(sv2, sv, sizeof(uint32_t) * B, cudaMemcpyDeviceToDevice, s));
   RTEC_CUDA(cudaMemsetAsync(keep, 0, B, s));
-  k_coalesce_fold<<<grid_for(B, kBlk), kBlk, 0, s>>>(sk, sv2, B, op, keep);
-  k_coalesce_map<<<grid_for(B, kBlk), kBlk, 0, s>>>(sk, sv, sv2, B, surv);
+  launch(k_coalesce_fold, grid_for(B, kBlk), kBlk, 0, s, sk, sv2, B, op, keep);
+  launch(k_coalesce_map, grid_for(B, kBlk), kBlk, 0, s, sk, sv, sv2, B, surv);
   RTEC_TRY(exclusive_scan(KeepAt{keep}, Count{nullptr, B}, B,
                           CoalesceOut{keep, surv, src, dst, op, ts, out_src, out_dst, out_op, out_ts}, n_out, w, s));
   return RTEC_OK;
@@ -1060,13 +1087,13 @@ int rtec_batch_apply_phase(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src,
   MergeIn mi{b->i_dst, b->i_src, b->i_op, nullptr, b->n_applied, B};
   if (plan) {
   // 1. keys + range validation; 2. sort; 3. duplicate validation
-  k_apply_keys<<<grid, kBlk, 0, s>>>(src, dst, B, n, keys, vals, b->err);
+  launch(k_apply_keys, grid, kBlk, 0, s, src, dst, B, n, keys, vals, b->err);
   RTEC_TRY(sort_pairs(keys, vals, sk, sv, Count{nullptr, B}, B, bits, w, s));
   w.off = mark;
-  k_apply_dups<<<grid, kBlk, 0, s>>>(sk, sv, B, n, b->err);
+  launch(k_apply_dups, grid, kBlk, 0, s, sk, sv, B, n, b->err);
   // 4. probe against the pre-batch graph (skipped on validation error: no flags -> nothing applied)
   RTEC_CUDA(cudaMemsetAsync(aflag, 0, B, s));
-  k_apply_probe<<<grid, kBlk, 0, s>>>(sk, sv, B, n, g->out, op, b->status, aflag, g->part_rank, g->part_count,
+  launch(k_apply_probe, grid, kBlk, 0, s, sk, sv, B, n, g->out, op, b->status, aflag, g->part_rank, g->part_count,
                                       b->err);
   // 5. applied updates in out-key order
   RTEC_TRY(exclusive_scan(FlagAt{aflag}, Count{nullptr, B}, B,
@@ -1074,10 +1101,10 @@ int rtec_batch_apply_phase(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src,
                           b->n_applied, w, s));
   w.off = mark;
   // 6. in-key order
-  k_in_keys<<<grid, kBlk, 0, s>>>(b->a_src, b->a_dst, b->n_applied, n, keys, vals);
+  launch(k_in_keys, grid, kBlk, 0, s, b->a_src, b->a_dst, b->n_applied, n, keys, vals);
   RTEC_TRY(sort_pairs(keys, vals, sk, sv, Count{b->n_applied, B}, B, bits, w, s));
   w.off = mark;
-  k_in_gather<<<grid, kBlk, 0, s>>>(sv, b->n_applied, b->a_src, b->a_dst, b->a_op, b->i_src, b->i_dst, b->i_op);
+  launch(k_in_gather, grid, kBlk, 0, s, sv, b->n_applied, b->a_src, b->a_dst, b->a_op, b->i_src, b->i_dst, b->i_op);
   // 7. plan both merges (no mutation; all-or-nothing arena reservation) -- independent of
   // each other: the in-run plan runs on the side stream with its own scratch
   {
@@ -1098,8 +1125,8 @@ int rtec_batch_apply_phase(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src,
   }
   if (!exec) return RTEC_OK;
   // 8. mutate: degrees, runs, per-destination ranges
-  k_irange_set<<<grid, kBlk, 0, s>>>(b->i_dst, b->n_applied, reinterpret_cast<int2*>(b->irange), b->err);
-  k_apply_degrees<<<grid, kBlk, 0, s>>>(b->a_src, b->a_dst, b->a_op, b->n_applied, g->out_deg, g->in_deg,
+  launch(k_irange_set, grid, kBlk, 0, s, b->i_dst, b->n_applied, reinterpret_cast<int2*>(b->irange), b->err);
+  launch(k_apply_degrees, grid, kBlk, 0, s, b->a_src, b->a_dst, b->a_op, b->n_applied, g->out_deg, g->in_deg,
                                         g->num_edges, b->err);
   int64_t work_bound = g->out.slots + B;  // grid-stride loops read the real totals on device
   // the two directions touch disjoint arrays (own plans and scratch): merge them concurrently
@@ -1119,7 +1146,7 @@ int rtec_batch_apply_phase(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src,
   uint32_t* tbm = w.alloc<uint32_t>(words);
   RTEC_WS_CHECK(w);
   RTEC_CUDA(cudaMemsetAsync(tbm, 0, sizeof(uint32_t) * words, s));
-  k_touched_bits<<<grid, kBlk, 0, s>>>(b->a_src, b->a_dst, b->n_applied, tbm);
+  launch(k_touched_bits, grid, kBlk, 0, s, b->a_src, b->a_dst, b->n_applied, tbm);
   TouchedWord tw{tbm, g->in_deg, g->out_deg, g->in_deg_prev, g->out_deg_prev};
   RTEC_TRY(exclusive_scan(tw, Count{nullptr, words}, words,
                           TouchedRows{tw, b->d_vertex, b->d_old_in, b->d_new_in, b->d_old_out, b->d_new_out},
@@ -1130,8 +1157,8 @@ int rtec_batch_apply_phase(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src,
 
 int rtec_batch_commit(rtec_graph_t* g, const rtec_batch_t* b, rtec_stream_t stream) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  k_irange_reset<<<grid_for(b->cap, kBlk), kBlk, 0, s>>>(b->i_dst, b->n_applied, reinterpret_cast<int2*>(b->irange));
-  k_commit_degrees<<<grid_for(b->cap * 2, kBlk), kBlk, 0, s>>>(b->d_vertex, b->n_delta, g->in_deg, g->out_deg,
+  launch(k_irange_reset, grid_for(b->cap, kBlk), kBlk, 0, s, b->i_dst, b->n_applied, reinterpret_cast<int2*>(b->irange));
+  launch(k_commit_degrees, grid_for(b->cap * 2, kBlk), kBlk, 0, s, b->d_vertex, b->n_delta, g->in_deg, g->out_deg,
                                                                g->in_deg_prev, g->out_deg_prev);
   RTEC_LAUNCH_CHECK("k_commit_degrees");
   return RTEC_OK;

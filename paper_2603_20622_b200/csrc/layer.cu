@@ -107,6 +107,7 @@ __device__ __forceinline__ int64_t drow(const LayerArgs& a, int32_t u) {
 // ------------------------------------------------------------------ δ rows (K10)
 template <int VEC, int K>
 __global__ void __launch_bounds__(kLBlk) k_src_delta(LayerArgs a, float* delta) {
+  RTEC_PDL_ENTRY();
   using R = RowAcc<VEC, K>;
   int64_t ns = *a.f.n_src;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -344,6 +345,7 @@ __device__ __forceinline__ void sum_partials(const float* part, int64_t stride, 
 
 template <int VEC, int K, bool FULL>
 __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_light(LayerArgs a, AggRows rows) {
+  RTEC_PDL_ENTRY();
   using R = RowAcc<VEC, K>;
   __shared__ __align__(16) float s_sv[kLBlk / 32][(!FULL && VEC == 4) ? 32 * VEC * K : 4];
   if (!FULL && err_set(a.err)) return;
@@ -407,6 +409,7 @@ constexpr int kBatchWin = kChunk;  // flattened edges per window: any light run 
 
 template <int VEC, int K, int OCC = 0>
 __global__ void __launch_bounds__(kLBlk, OCC > 0 ? OCC : AggOcc<VEC, K>::value) k_agg_batch(LayerArgs a, AggRows rows) {
+  RTEC_PDL_ENTRY();
   using R = RowAcc<VEC, K>;
   constexpr int UNR = kUnroll;  // measured: 8 rows in flight spill next to the prefetched S row
   __shared__ int32_t s_u[kLBlk / 32][kBatchWin];
@@ -548,6 +551,7 @@ __global__ void __launch_bounds__(kLBlk, OCC > 0 ? OCC : AggOcc<VEC, K>::value) 
 
 template <int VEC, int K, bool FULL>
 __global__ void __launch_bounds__(kLBlk, AggOcc<VEC, K>::value) k_agg_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
+  RTEC_PDL_ENTRY();
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
   const int64_t nh = *hp.n_heavy;
@@ -627,6 +631,7 @@ struct StoreOffTailL {
 };
 
 __global__ void k_chunk_map(HeavyPlan hp) {
+  RTEC_PDL_ENTRY();
   int64_t nh = *hp.n_heavy;
   if (blockIdx.x == 0 && threadIdx.x == 0) hp.n_heavy[1] = hp.hoff[nh];  // total chunks (sort count)
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -723,7 +728,7 @@ static int plan_heavy(const LayerArgs& a, AggRows rows, int64_t max_rows, int64_
     hp.oval = w.alloc<uint32_t>(max_chunks);
     RTEC_WS_CHECK(w);
   }
-  k_chunk_map<<<kSMs * 4, kLBlk, 0, s>>>(hp);
+  launch(k_chunk_map, kSMs * 4, kLBlk, 0, s, hp);
   RTEC_LAUNCH_CHECK("k_chunk_map");
   if (hp.okey) {
     uint64_t* kout = w.alloc<uint64_t>(max_chunks);
@@ -763,8 +768,8 @@ static int launch_aggregation(LayerArgs& a, AggRows rows, int64_t max_rows, int6
     }
     {
       RTEC_PROF(FULL ? "k_agg_full_heavy" : "k_agg_inc_heavy", hs);
-      ok = (sliced ? RTEC_SLICE_DISPATCH(a.cw, (k_agg_heavy<VEC, K, FULL><<<grid, kLBlk, 0, hs>>>(a, rows, hp)))
-                   : RTEC_ROW_DISPATCH(a.cw, (k_agg_heavy<VEC, K, FULL><<<grid, kLBlk, 0, hs>>>(a, rows, hp))));
+      ok = (sliced ? RTEC_SLICE_DISPATCH(a.cw, (launch(k_agg_heavy<VEC, K, FULL>, grid, kLBlk, 0, hs, a, rows, hp)))
+                   : RTEC_ROW_DISPATCH(a.cw, (launch(k_agg_heavy<VEC, K, FULL>, grid, kLBlk, 0, hs, a, rows, hp))));
     }
     {
       RTEC_PROF(FULL ? "k_agg_full_light" : "k_agg_inc", s);
@@ -775,13 +780,13 @@ static int launch_aggregation(LayerArgs& a, AggRows rows, int64_t max_rows, int6
         al.pick = 2;
         ab.pick_thr = al.pick_thr = agg_dense_thr();
         if (agg_batch_occ() == 6)
-          ok = ok && RTEC_ROW_DISPATCH(a.cw, (k_agg_batch<VEC, K, 6><<<grid, kLBlk, 0, s>>>(ab, rows)));
+          ok = ok && RTEC_ROW_DISPATCH(a.cw, (launch(k_agg_batch<VEC, K, 6>, grid, kLBlk, 0, s, ab, rows)));
         else
-          ok = ok && RTEC_ROW_DISPATCH(a.cw, (k_agg_batch<VEC, K><<<grid, kLBlk, 0, s>>>(ab, rows)));
-        ok = ok && RTEC_ROW_DISPATCH(a.cw, (k_agg_light<VEC, K, false><<<grid, kLBlk, 0, s>>>(al, rows)));
+          ok = ok && RTEC_ROW_DISPATCH(a.cw, (launch(k_agg_batch<VEC, K>, grid, kLBlk, 0, s, ab, rows)));
+        ok = ok && RTEC_ROW_DISPATCH(a.cw, (launch(k_agg_light<VEC, K, false>, grid, kLBlk, 0, s, al, rows)));
       } else
-        ok = ok && (sliced ? RTEC_SLICE_DISPATCH(a.cw, (k_agg_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows)))
-                           : RTEC_ROW_DISPATCH(a.cw, (k_agg_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows))));
+        ok = ok && (sliced ? RTEC_SLICE_DISPATCH(a.cw, (launch(k_agg_light<VEC, K, FULL>, grid, kLBlk, 0, s, a, rows)))
+                           : RTEC_ROW_DISPATCH(a.cw, (launch(k_agg_light<VEC, K, FULL>, grid, kLBlk, 0, s, a, rows))));
     }
     if (hs != s) {
       RTEC_CUDA(cudaEventRecord(side_join(), hs));
@@ -954,6 +959,7 @@ __device__ __forceinline__ void dd_finalize(const LayerArgs& a, int64_t i, int32
 
 template <int VEC, int K, bool FULL>
 __global__ void __launch_bounds__(kLBlk) k_dd_light(LayerArgs a, AggRows rows) {
+  RTEC_PDL_ENTRY();
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
   const int64_t nr = rows.count();
@@ -976,6 +982,7 @@ __global__ void __launch_bounds__(kLBlk) k_dd_light(LayerArgs a, AggRows rows) {
 
 template <int VEC, int K, bool FULL>
 __global__ void __launch_bounds__(kLBlk) k_dd_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
+  RTEC_PDL_ENTRY();
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
   const int64_t nh = *hp.n_heavy;
@@ -1025,11 +1032,11 @@ static int launch_dd(LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_e
   bool ok;
   {
     RTEC_PROF(FULL ? "k_dd_full_heavy" : "k_dd_inc_heavy", s);
-    ok = RTEC_ROW_DISPATCH(d, (k_dd_heavy<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows, hp)));
+    ok = RTEC_ROW_DISPATCH(d, (launch(k_dd_heavy<VEC, K, FULL>, grid, kLBlk, 0, s, a, rows, hp)));
   }
   {
     RTEC_PROF(FULL ? "k_dd_full_light" : "k_dd_inc", s);
-    ok = ok && RTEC_ROW_DISPATCH(d, (k_dd_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows)));
+    ok = ok && RTEC_ROW_DISPATCH(d, (launch(k_dd_light<VEC, K, FULL>, grid, kLBlk, 0, s, a, rows)));
   }
   if (!ok) {
     set_error("row width %d unsupported", d);
@@ -1218,6 +1225,7 @@ __device__ __forceinline__ bool max_direct(const LayerArgs& a) {
 // destinations with <= kChunk scanned edges: one warp each, re-max in place on retract
 template <int VEC, int K, bool FULL>
 __global__ void __launch_bounds__(kLBlk) k_max_light(LayerArgs a, AggRows rows) {
+  RTEC_PDL_ENTRY();
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
   const int d = a.d_agg;
@@ -1266,6 +1274,7 @@ struct MaxRescan {
 // the last chunk to arrive finalizes, or queues the destination for a rescan
 template <int VEC, int K, bool FULL>
 __global__ void __launch_bounds__(kLBlk) k_max_heavy(LayerArgs a, AggRows rows, HeavyPlan hp, MaxRescan rq) {
+  RTEC_PDL_ENTRY();
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
   const int64_t nh = *hp.n_heavy;
@@ -1332,6 +1341,7 @@ __global__ void __launch_bounds__(kLBlk) k_max_heavy(LayerArgs a, AggRows rows, 
 // heavy destinations, pass 2: chunked re-max of the queued destinations
 template <int VEC, int K>
 __global__ void __launch_bounds__(kLBlk) k_max_rescan(LayerArgs a, AggRows rows, HeavyPlan hp, MaxRescan rq) {
+  RTEC_PDL_ENTRY();
   using R = RowAcc<VEC, K>;
   if (err_set(a.err)) return;
   const int64_t T = *rq.total;
@@ -1385,9 +1395,9 @@ static int launch_max(LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_
   RTEC_CUDA(cudaMemsetAsync(rq.n, 0, sizeof(int64_t) * 2, s));
   RTEC_CUDA(cudaMemsetAsync(rq.flag, 0, sizeof(int32_t) * (max_rows + 1), s));
   RTEC_PROF(FULL ? "k_max_full" : "k_max_inc", s);
-  bool ok = RTEC_ROW_DISPATCH(d, (k_max_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows),
-                                  k_max_heavy<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows, hp, rq)));
-  if (ok && !FULL) ok = RTEC_ROW_DISPATCH(d, (k_max_rescan<VEC, K><<<grid, kLBlk, 0, s>>>(a, rows, hp, rq)));
+  bool ok = RTEC_ROW_DISPATCH(d, (launch(k_max_light<VEC, K, FULL>, grid, kLBlk, 0, s, a, rows),
+                                  launch(k_max_heavy<VEC, K, FULL>, grid, kLBlk, 0, s, a, rows, hp, rq)));
+  if (ok && !FULL) ok = RTEC_ROW_DISPATCH(d, (launch(k_max_rescan<VEC, K>, grid, kLBlk, 0, s, a, rows, hp, rq)));
   if (!ok) {
     set_error("row width %d unsupported", d);
     return RTEC_SHAPE_ERROR;
@@ -1589,6 +1599,7 @@ __device__ __forceinline__ void gat_finalize(const LayerArgs& a, int64_t i, int3
 // p50 3 CTAs 16.4 ms, 4 CTAs 14.7, 5 CTAs 14.55, 6 CTAs 14.1
 template <int VEC, int K, bool FULL>
 __global__ void __launch_bounds__(kLBlk, 6) k_gat_light(LayerArgs a, AggRows rows) {
+  RTEC_PDL_ENTRY();
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
   const int64_t nr = rows.count();
@@ -1623,6 +1634,7 @@ __global__ void __launch_bounds__(kLBlk, 6) k_gat_light(LayerArgs a, AggRows row
 
 template <int VEC, int K, bool FULL>
 __global__ void __launch_bounds__(kLBlk, 6) k_gat_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
+  RTEC_PDL_ENTRY();
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
   const int64_t nh = *hp.n_heavy;
@@ -1693,8 +1705,8 @@ __global__ void __launch_bounds__(kLBlk, 6) k_gat_heavy(LayerArgs a, AggRows row
 template <int VEC, int K, bool FULL>
 static int launch_gat_passes(const LayerArgs& a, AggRows rows, const HeavyPlan& hp, int grid, cudaStream_t s,
                              cudaStream_t hs) {
-  k_gat_heavy<VEC, K, FULL><<<grid, kLBlk, 0, hs>>>(a, rows, hp);
-  k_gat_light<VEC, K, FULL><<<grid, kLBlk, 0, s>>>(a, rows);
+  launch(k_gat_heavy<VEC, K, FULL>, grid, kLBlk, 0, hs, a, rows, hp);
+  launch(k_gat_light<VEC, K, FULL>, grid, kLBlk, 0, s, a, rows);
   return RTEC_OK;
 }
 
@@ -1731,14 +1743,14 @@ static int launch_gat(LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_
     int kk = (d + 31) / 32;
     ok = true;
     if (kk <= 1) {
-      k_gat_light<1, 1, FULL><<<grid, kLBlk, 0, s>>>(a, rows);
-      k_gat_heavy<1, 1, FULL><<<grid, kLBlk, 0, s>>>(a, rows, hp);
+      launch(k_gat_light<1, 1, FULL>, grid, kLBlk, 0, s, a, rows);
+      launch(k_gat_heavy<1, 1, FULL>, grid, kLBlk, 0, s, a, rows, hp);
     } else if (kk <= 4) {
-      k_gat_light<1, 4, FULL><<<grid, kLBlk, 0, s>>>(a, rows);
-      k_gat_heavy<1, 4, FULL><<<grid, kLBlk, 0, s>>>(a, rows, hp);
+      launch(k_gat_light<1, 4, FULL>, grid, kLBlk, 0, s, a, rows);
+      launch(k_gat_heavy<1, 4, FULL>, grid, kLBlk, 0, s, a, rows, hp);
     } else if (kk <= 8) {
-      k_gat_light<1, 8, FULL><<<grid, kLBlk, 0, s>>>(a, rows);
-      k_gat_heavy<1, 8, FULL><<<grid, kLBlk, 0, s>>>(a, rows, hp);
+      launch(k_gat_light<1, 8, FULL>, grid, kLBlk, 0, s, a, rows);
+      launch(k_gat_heavy<1, 8, FULL>, grid, kLBlk, 0, s, a, rows, hp);
     } else {
       ok = false;
     }
@@ -1755,6 +1767,7 @@ static int launch_gat(LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_
 __global__ void k_gat_logits(const float* __restrict__ Z, const int32_t* rows, const int64_t* n_rows, int64_t n_all,
                              int d, int H, const float* __restrict__ att, float* el, float* er, float* er_log,
                              const uint64_t* err) {
+  RTEC_PDL_ENTRY();
   if (err && err_set(err)) return;
   int dh = d / H;
   int64_t nr = rows ? *n_rows : n_all;
@@ -1802,6 +1815,7 @@ struct GemmArgs {
 constexpr int kGM = 64, kGN = 64, kGK = 16;
 
 __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs g) {
+  RTEC_PDL_ENTRY();
   __shared__ float As[kGK][kGM + 4];
   __shared__ float Bs[kGK][kGN + 4];
   if (g.err && err_set(g.err)) return;
@@ -1871,7 +1885,7 @@ int gemm_launch(const GemmArgs& g, cudaStream_t s) {
   if (g.max_rows <= 0) return RTEC_OK;
   dim3 grid(static_cast<unsigned>((g.max_rows + kGM - 1) / kGM), static_cast<unsigned>((g.d_out + kGN - 1) / kGN));
   RTEC_PROF("k_gemm_update", s);
-  k_gemm_simt<<<grid, 256, 0, s>>>(g);
+  launch(k_gemm_simt, grid, 256, 0, s, g);
   RTEC_LAUNCH_CHECK("k_gemm_simt");
   return RTEC_OK;
 }
@@ -1884,6 +1898,7 @@ __global__ void __launch_bounds__(256) k_quadform(const float* __restrict__ H, c
                                                   const int64_t* n_rows, int64_t n_all, int d,
                                                   const float* __restrict__ Wq, const float* __restrict__ mu,
                                                   float* P, float* P_log, const uint64_t* err) {
+  RTEC_PDL_ENTRY();
   if (err && err_set(err)) return;
   const int64_t nr = rows ? *n_rows : n_all;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -1925,6 +1940,7 @@ __global__ void __launch_bounds__(256) k_quadform(const float* __restrict__ H, c
 // ------------------------------------------------------------------ query (K18)
 __global__ void k_query(const float* __restrict__ H, int64_t d, const int32_t* __restrict__ ids, int64_t k, int32_t n,
                         float* out, uint64_t* err) {
+  RTEC_PDL_ENTRY();
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = warp; i < k; i += nw) {
@@ -2071,7 +2087,7 @@ int rtec_layer_incremental(const rtec_graph_t* g, const rtec_batch_t* b, const r
   bool ok;
   {
     RTEC_PROF("k_src_delta", s);
-    ok = RTEC_ROW_DISPATCH(a.d_agg, (k_src_delta<VEC, K><<<grid, kLBlk, 0, s>>>(a, delta)));
+    ok = RTEC_ROW_DISPATCH(a.d_agg, (launch(k_src_delta<VEC, K>, grid, kLBlk, 0, s, a, delta)));
   }
   if (!ok) {
     set_error("row width %d unsupported", a.d_agg);
@@ -2149,7 +2165,7 @@ int rtec_gat_project(const rtec_layer_t* L, const float* H, const int32_t* rows,
     RTEC_TRY(gemm_launch(gz, s));
   }
   RTEC_PROF("k_gat_logits", s);
-  k_gat_logits<<<kSMs * 8, kLBlk, 0, s>>>(Z, rows, n_rows, n_or_max_rows, L->d_out, L->heads, L->att, el, er, er_log,
+  launch(k_gat_logits, kSMs * 8, kLBlk, 0, s, Z, rows, n_rows, n_or_max_rows, L->d_out, L->heads, L->att, el, er, er_log,
                                           rows ? err : nullptr);
   RTEC_LAUNCH_CHECK("k_gat_logits");
   return RTEC_OK;
@@ -2180,7 +2196,7 @@ int rtec_project(const rtec_layer_t* L, const float* H, const int32_t* rows, con
         return RTEC_SHAPE_ERROR;
       }
       RTEC_PROF("k_quadform", s);
-      k_quadform<<<kSMs * 8, 256, 0, s>>>(H, rows, nr, n_or_max_rows, d, L->Wp, L->bp, P, P_log, err);
+      launch(k_quadform, kSMs * 8, 256, 0, s, H, rows, nr, n_or_max_rows, d, L->Wp, L->bp, P, P_log, err);
       RTEC_LAUNCH_CHECK("k_quadform");
       return RTEC_OK;
     }
@@ -2193,7 +2209,7 @@ int rtec_query(const float* H, int64_t d, const int32_t* ids, int64_t k, float* 
                rtec_stream_t stream) {
   if (k <= 0) return RTEC_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  k_query<<<grid_for(k * 32, 256), 256, 0, s>>>(H, d, ids, k, n, out, err);
+  launch(k_query, grid_for(k * 32, 256), 256, 0, s, H, d, ids, k, n, out, err);
   RTEC_LAUNCH_CHECK("k_query");
   return RTEC_OK;
 }

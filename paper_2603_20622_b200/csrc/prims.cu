@@ -6,6 +6,8 @@
 
 #include "prims.cuh"
 
+#include <stdlib.h>
+
 namespace rtec {
 
 // ---------------------------------------------------------------- errors
@@ -98,6 +100,15 @@ int sm_count() {
   return cache[d];
 }
 
+bool pdl_on() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("RTEC_PDL");
+    on = e ? (atoi(e) != 0) : 1;
+  }
+  return on != 0;
+}
+
 // side stream + fork / join events of the current device (the two-stream passes)
 cudaStream_t side_stream() {
   static cudaStream_t st[kMaxDevices] = {};
@@ -124,6 +135,7 @@ constexpr int kSmallSort = 2048;
 
 __global__ void __launch_bounds__(1024) k_sort_small(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                      uint64_t* kout, uint32_t* vout, Count cnt) {
+  RTEC_PDL_ENTRY();
   __shared__ uint64_t sk[kSmallSort];
   __shared__ uint32_t sv[kSmallSort];
   int64_t n = cnt.get();
@@ -170,6 +182,7 @@ __global__ void __launch_bounds__(1024) k_sort_small(const uint64_t* __restrict_
 // pass instead of the ~55 compare stages of a bitonic network.
 __global__ void __launch_bounds__(1024) k_sort_reg(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                    uint64_t* kout, uint32_t* vout, Count cnt, int bits) {
+  RTEC_PDL_ENTRY();
   __shared__ uint32_t whist[32][257];  // per-warp digit counts, then per-warp exclusive offsets
   __shared__ uint32_t boff[256];
   __shared__ uint64_t sk[1024];
@@ -246,6 +259,7 @@ inline int rx_items_for(int64_t max_n) { return max_n <= 131072 ? 1 : (max_n <= 
 template <int ITEMS>
 __global__ void __launch_bounds__(kRxBlock) k_rx_hist(const uint64_t* __restrict__ keys, Count cnt, int shift,
                                                       int64_t ntiles, uint32_t* __restrict__ counts) {
+  RTEC_PDL_ENTRY();
   __shared__ uint32_t hist[kRxBins];
   hist[threadIdx.x] = 0;
   __syncthreads();
@@ -265,6 +279,7 @@ __global__ void __launch_bounds__(kRxBlock) k_rx_scatter(const uint64_t* __restr
                                                          uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                          Count cnt, int shift, int64_t ntiles,
                                                          const int64_t* __restrict__ offsets) {
+  RTEC_PDL_ENTRY();
   constexpr int kWarps = kRxBlock / 32;
   __shared__ uint32_t run[kRxBins];
   __shared__ uint32_t whist[kWarps][kRxBins];
@@ -335,12 +350,12 @@ int sort_pairs(const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* keys_
                Count cnt, int64_t max_n, int bits, Ws& ws, cudaStream_t s) {
   if (max_n <= 0) return RTEC_OK;
   if (max_n <= 1024) {
-    k_sort_reg<<<1, 1024, 0, s>>>(keys_in, vals_in, keys_out, vals_out, cnt, bits);
+    launch(k_sort_reg, 1, 1024, 0, s, keys_in, vals_in, keys_out, vals_out, cnt, bits);
     RTEC_LAUNCH_CHECK("k_sort_reg");
     return RTEC_OK;
   }
   if (max_n <= kSmallSort) {
-    k_sort_small<<<1, 1024, 0, s>>>(keys_in, vals_in, keys_out, vals_out, cnt);
+    launch(k_sort_small, 1, 1024, 0, s, keys_in, vals_in, keys_out, vals_out, cnt);
     RTEC_LAUNCH_CHECK("k_sort_small");
     return RTEC_OK;
   }
@@ -363,14 +378,14 @@ int sort_pairs(const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* keys_
     uint32_t* vo = last ? vals_out : ((p & 1) ? vb : va);
     int shift = 8 * p;
     const unsigned grid = static_cast<unsigned>(ntiles);
-    if (items == 1) k_rx_hist<1><<<grid, kRxBlock, 0, s>>>(ki, cnt, shift, ntiles, counts);
-    else if (items == 4) k_rx_hist<4><<<grid, kRxBlock, 0, s>>>(ki, cnt, shift, ntiles, counts);
-    else k_rx_hist<kRxItems><<<grid, kRxBlock, 0, s>>>(ki, cnt, shift, ntiles, counts);
+    if (items == 1) launch(k_rx_hist<1>, grid, kRxBlock, 0, s, ki, cnt, shift, ntiles, counts);
+    else if (items == 4) launch(k_rx_hist<4>, grid, kRxBlock, 0, s, ki, cnt, shift, ntiles, counts);
+    else launch(k_rx_hist<kRxItems>, grid, kRxBlock, 0, s, ki, cnt, shift, ntiles, counts);
     RTEC_TRY(exclusive_scan_bs(U32At{counts}, Count{nullptr, kRxBins * ntiles}, kRxBins * ntiles,
                                StorePrefix{offs}, nullptr, bs, s));
-    if (items == 1) k_rx_scatter<1><<<grid, kRxBlock, 0, s>>>(ki, vi, ko, vo, cnt, shift, ntiles, offs);
-    else if (items == 4) k_rx_scatter<4><<<grid, kRxBlock, 0, s>>>(ki, vi, ko, vo, cnt, shift, ntiles, offs);
-    else k_rx_scatter<kRxItems><<<grid, kRxBlock, 0, s>>>(ki, vi, ko, vo, cnt, shift, ntiles, offs);
+    if (items == 1) launch(k_rx_scatter<1>, grid, kRxBlock, 0, s, ki, vi, ko, vo, cnt, shift, ntiles, offs);
+    else if (items == 4) launch(k_rx_scatter<4>, grid, kRxBlock, 0, s, ki, vi, ko, vo, cnt, shift, ntiles, offs);
+    else launch(k_rx_scatter<kRxItems>, grid, kRxBlock, 0, s, ki, vi, ko, vo, cnt, shift, ntiles, offs);
     RTEC_LAUNCH_CHECK("k_rx_scatter");
     ki = ko;
     vi = vo;

@@ -62,6 +62,7 @@ inline int64_t scan_blocks_for(int64_t max_n) {
 // whole scan in one CTA when the (host-side) bound fits one tile: one launch instead of three
 template <typename F, typename O>
 __global__ void __launch_bounds__(kScanBlock) k_scan_one(F f, Count cnt, O out, int64_t* total) {
+  RTEC_PDL_ENTRY();
   __shared__ int64_t sw[kScanBlock / 32];
   int64_t n = cnt.get();
   int64_t vals[kScanItems];
@@ -94,6 +95,7 @@ constexpr unsigned long long kLbAgg = 1ull << 62, kLbPrefix = 2ull << 62, kLbMas
 template <typename F, typename O, int ITEMS>
 __global__ void __launch_bounds__(kScanBlock) k_scan_1pass(F f, Count cnt, O out, int64_t* total,
                                                            unsigned long long* st, unsigned int* tile_ctr) {
+  RTEC_PDL_ENTRY();
   __shared__ int64_t sw[kScanBlock / 32];
   __shared__ int64_t s_prefix;
   __shared__ unsigned int s_tile;
@@ -171,12 +173,12 @@ int exclusive_scan_bs(F f, Count cnt, int64_t max_n, O out, int64_t* total, int6
     unsigned long long* st = reinterpret_cast<unsigned long long*>(bs);
     unsigned int* ctr = reinterpret_cast<unsigned int*>(bs + nb);
     RTEC_CUDA(cudaMemsetAsync(bs, 0, sizeof(int64_t) * (nb + 1), s));
-    k_scan_1pass<F, O, 1><<<static_cast<unsigned>(nb > 0 ? nb : 1), kScanBlock, 0, s>>>(f, cnt, out, total, st, ctr);
+    launch(k_scan_1pass<F, O, 1>, static_cast<unsigned>(nb > 0 ? nb : 1), kScanBlock, 0, s, f, cnt, out, total, st, ctr);
     RTEC_LAUNCH_CHECK("exclusive_scan");
     return RTEC_OK;
   }
   if (max_n <= kScanTile) {
-    k_scan_one<F, O><<<1, kScanBlock, 0, s>>>(f, cnt, out, total);
+    launch(k_scan_one<F, O>, 1, kScanBlock, 0, s, f, cnt, out, total);
     RTEC_LAUNCH_CHECK("exclusive_scan");
     return RTEC_OK;
   }
@@ -185,9 +187,9 @@ int exclusive_scan_bs(F f, Count cnt, int64_t max_n, O out, int64_t* total, int6
   unsigned int* ctr = reinterpret_cast<unsigned int*>(bs + nb);
   RTEC_CUDA(cudaMemsetAsync(bs, 0, sizeof(int64_t) * (nb + 1), s));
   if (scan_items_for(max_n) == 1)
-    k_scan_1pass<F, O, 1><<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(f, cnt, out, total, st, ctr);
+    launch(k_scan_1pass<F, O, 1>, static_cast<unsigned>(nb), kScanBlock, 0, s, f, cnt, out, total, st, ctr);
   else
-    k_scan_1pass<F, O, kScanItems><<<static_cast<unsigned>(nb), kScanBlock, 0, s>>>(f, cnt, out, total, st, ctr);
+    launch(k_scan_1pass<F, O, kScanItems>, static_cast<unsigned>(nb), kScanBlock, 0, s, f, cnt, out, total, st, ctr);
   RTEC_LAUNCH_CHECK("exclusive_scan");
   return RTEC_OK;
 }

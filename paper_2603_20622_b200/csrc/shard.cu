@@ -37,6 +37,7 @@ __device__ __forceinline__ int32_t owner_of(int32_t v, int32_t world) { return v
 // ------------------------------------------------------------------ batch validation
 __global__ void k_val_keys(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t B, int64_t n,
                            uint64_t* keys, uint32_t* vals, uint64_t* err) {
+  RTEC_PDL_ENTRY();
   const uint64_t inval = static_cast<uint64_t>(n) * static_cast<uint64_t>(n);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t s = src[i], d = dst[i];
@@ -49,6 +50,7 @@ __global__ void k_val_keys(const int32_t* __restrict__ src, const int32_t* __res
 
 __global__ void k_val_dups(const uint64_t* __restrict__ sk, const uint32_t* __restrict__ sv, int64_t B, int64_t n,
                            uint64_t* err) {
+  RTEC_PDL_ENTRY();
   const uint64_t inval = static_cast<uint64_t>(n) * static_cast<uint64_t>(n);
   for (int64_t i = 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x)
     if (sk[i] == sk[i - 1] && sk[i] != inval) report_error(err, RTEC_CONFIG_ERROR, sv[i]);  // graph.py:195-197
@@ -61,6 +63,7 @@ __global__ void k_val_dups(const uint64_t* __restrict__ sk, const uint32_t* __re
 __global__ void k_admit(rtec_shard_t sh, const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
                         const uint8_t* __restrict__ op, int64_t B, const uint64_t* err, uint32_t* bm_adm,
                         int32_t* send_u, int32_t* send_q, int64_t* n_send, int64_t* peer_count) {
+  RTEC_PDL_ENTRY();
   if (err_set(err)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x) {
     if (op[i] != RTEC_OP_INSERT) continue;
@@ -114,6 +117,7 @@ struct AdmAssign {
   }
 };
 __global__ void k_admit_commit(int64_t* n_loc, const int64_t* n_adm, int64_t cap) {
+  RTEC_PDL_ENTRY();
   const int64_t t = *n_loc + *n_adm;
   *n_loc = t < cap ? t : cap;
 }
@@ -145,6 +149,7 @@ struct Localize {
 // per-peer row counts of a list of owned local ids (each row goes to every rank in peers[v])
 __global__ void k_count_peers(rtec_shard_t sh, const int32_t* __restrict__ list, const int64_t* n_list,
                               int64_t max_list, int64_t* peer_count) {
+  RTEC_PDL_ENTRY();
   const int64_t n = n_list ? *n_list : max_list;
   for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~int64_t(31); i0 < n;
        i0 += (int64_t)gridDim.x * blockDim.x) {
@@ -196,6 +201,7 @@ __global__ void __launch_bounds__(kSBlk) k_pack(rtec_shard_t sh, PackSrc ps, con
                                                 const int32_t* __restrict__ pair_u, const int32_t* __restrict__ pair_q,
                                                 int64_t n_pairs, int64_t* cursor, int32_t* out_ids, int32_t* out_deg,
                                                 float* out_rows) {
+  RTEC_PDL_ENTRY();
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   if (pair_u) {
@@ -218,6 +224,7 @@ __global__ void __launch_bounds__(kSBlk) k_pack(rtec_shard_t sh, PackSrc ps, con
 __global__ void __launch_bounds__(kSBlk) k_unpack_rows(rtec_shard_t sh, PackSrc ps, const int32_t* __restrict__ ids,
                                                        const int32_t* __restrict__ degs,
                                                        const float* __restrict__ rows, int64_t k, int32_t* out_local) {
+  RTEC_PDL_ENTRY();
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = warp; i < k; i += nw) {
@@ -263,6 +270,7 @@ __global__ void __launch_bounds__(kSBlk) k_unpack_changed(rtec_shard_t sh, int32
                                                           const int32_t* __restrict__ own_slot, ChgOut o,
                                                           uint32_t* bm_chg, int32_t* chg_slot, int32_t* chg_list,
                                                           int64_t* n_chg) {
+  RTEC_PDL_ENTRY();
   const int64_t no = own_list ? *n_own : 0;
   const int64_t total = k + no;
   if (blockIdx.x == 0 && threadIdx.x == 0 && own_list) *n_chg = pos_base + total;
@@ -319,6 +327,7 @@ __global__ void __launch_bounds__(kSBlk) k_unpack_changed(rtec_shard_t sh, int32
 __global__ void k_gdeg(rtec_shard_t sh, const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
                        const uint8_t* __restrict__ op, const uint8_t* __restrict__ gst, int64_t B,
                        uint32_t* bm_touch) {
+  RTEC_PDL_ENTRY();
   for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~int64_t(31); i0 < B;
        i0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = i0 + lane_id();
@@ -340,6 +349,7 @@ __global__ void k_gdeg(rtec_shard_t sh, const int32_t* __restrict__ src, const i
 
 __global__ void k_gdeg_dg(rtec_shard_t sh, const int32_t* __restrict__ src, const uint8_t* __restrict__ gst, int64_t B,
                           uint32_t* dg_bm) {
+  RTEC_PDL_ENTRY();
   for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~int64_t(31); i0 < B;
        i0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = i0 + lane_id();
@@ -389,6 +399,7 @@ struct OwnedDeltaRows {
 
 __global__ void k_gdeg_commit(rtec_shard_t sh, const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
                               const uint8_t* __restrict__ gst, int64_t B, uint32_t* dg_bm, uint32_t* bm_touch) {
+  RTEC_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x) {
     if (!gst[i]) continue;
     const int32_t s = src[i], d = dst[i];
@@ -447,9 +458,9 @@ int rtec_batch_validate(const int32_t* src, const int32_t* dst, int64_t B, int64
   uint32_t* sv = w.alloc<uint32_t>(B);
   RTEC_WS_CHECK(w);
   const int grid = grid_for(B, kSBlk);
-  k_val_keys<<<grid, kSBlk, 0, s>>>(src, dst, B, n, keys, vals, err);
+  launch(k_val_keys, grid, kSBlk, 0, s, src, dst, B, n, keys, vals, err);
   RTEC_TRY(sort_pairs(keys, vals, sk, sv, Count{nullptr, B}, B, bits_for(static_cast<uint64_t>(n) * n), w, s));
-  k_val_dups<<<grid, kSBlk, 0, s>>>(sk, sv, B, n, err);
+  launch(k_val_dups, grid, kSBlk, 0, s, sk, sv, B, n, err);
   RTEC_LAUNCH_CHECK("batch_validate");
   return RTEC_OK;
 }
@@ -465,13 +476,13 @@ int rtec_shard_admit(const rtec_shard_t* sh, const int32_t* src, const int32_t* 
   RTEC_CUDA(cudaMemsetAsync(peer_count, 0, sizeof(int64_t) * sh->world, s));
   if (B <= 0) return RTEC_OK;
   RTEC_PROF("shard_admit", s);
-  k_admit<<<grid_for(B, kSBlk), kSBlk, 0, s>>>(*sh, src, dst, op, B, err, bm_adm, send_u, send_q, n_send, peer_count);
+  launch(k_admit, grid_for(B, kSBlk), kSBlk, 0, s, *sh, src, dst, op, B, err, bm_adm, send_u, send_q, n_send, peer_count);
   RTEC_LAUNCH_CHECK("k_admit");
   Ws w(ws, ws_bytes);
   const int64_t words = (sh->n + 31) / 32;
   RTEC_TRY(exclusive_scan(AdmWord{bm_adm}, Count{nullptr, words}, words, AdmAssign{bm_adm, *sh, adm_list, err},
                           n_adm, w, s));
-  k_admit_commit<<<1, 1, 0, s>>>(sh->n_loc, n_adm, sh->cap);
+  launch(k_admit_commit, 1, 1, 0, s, sh->n_loc, n_adm, sh->cap);
   RTEC_LAUNCH_CHECK("k_admit_commit");
   return RTEC_OK;
 }
@@ -497,7 +508,7 @@ int rtec_shard_count_peers(const rtec_shard_t* sh, const int32_t* list, const in
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   RTEC_CUDA(cudaMemsetAsync(peer_count, 0, sizeof(int64_t) * sh->world, s));
   if (max_list <= 0) return RTEC_OK;
-  k_count_peers<<<grid_for(max_list, kSBlk, kSMs * 8), kSBlk, 0, s>>>(*sh, list, n_list, max_list, peer_count);
+  launch(k_count_peers, grid_for(max_list, kSBlk, kSMs * 8), kSBlk, 0, s, *sh, list, n_list, max_list, peer_count);
   RTEC_LAUNCH_CHECK("k_count_peers");
   return RTEC_OK;
 }
@@ -514,7 +525,7 @@ int rtec_shard_pack(const rtec_shard_t* sh, int32_t nmat, const float* const* ma
   const int64_t work = pair_u ? n_pairs : max_list;
   if (work <= 0) return RTEC_OK;
   RTEC_PROF("shard_pack", s);
-  k_pack<<<grid_for(work * 32, kSBlk, kSMs * 8), kSBlk, 0, s>>>(*sh, ps, list, n_list, max_list, pair_u, pair_q,
+  launch(k_pack, grid_for(work * 32, kSBlk, kSMs * 8), kSBlk, 0, s, *sh, ps, list, n_list, max_list, pair_u, pair_q,
                                                                  n_pairs, cursor, out_ids, out_deg, out_rows);
   RTEC_LAUNCH_CHECK("k_pack");
   return RTEC_OK;
@@ -529,7 +540,7 @@ int rtec_shard_unpack_rows(const rtec_shard_t* sh, int32_t nmat, float* const* m
   RTEC_TRY(pack_src(ps, nmat, const_cast<const float* const*>(mats), dims, sh->world, nullptr));
   if (k <= 0) return RTEC_OK;
   RTEC_PROF("shard_unpack", s);
-  k_unpack_rows<<<grid_for(k * 32, kSBlk, kSMs * 8), kSBlk, 0, s>>>(*sh, ps, ids, degs, rows, k, out_local);
+  launch(k_unpack_rows, grid_for(k * 32, kSBlk, kSMs * 8), kSBlk, 0, s, *sh, ps, ids, degs, rows, k, out_local);
   RTEC_LAUNCH_CHECK("k_unpack_rows");
   return RTEC_OK;
 }
@@ -556,10 +567,10 @@ int rtec_shard_unpack_changed(const rtec_shard_t* sh, int32_t d, const int32_t* 
   const int grid = grid_for((work > 0 ? work : 1) * 32, kSBlk, kSMs * 8);
   const ChgOut o{glog, delta, coeff_gcn, deg_off};
   if (d % 4 == 0)
-    k_unpack_changed<true><<<grid, kSBlk, 0, s>>>(*sh, d, ids, rows, k, pos_base, H, own_list, n_own, own_log, own_slot,
+    launch(k_unpack_changed<true>, grid, kSBlk, 0, s, *sh, d, ids, rows, k, pos_base, H, own_list, n_own, own_log, own_slot,
                                                   o, bm_chg, chg_slot, chg_list, n_chg);
   else
-    k_unpack_changed<false><<<grid, kSBlk, 0, s>>>(*sh, d, ids, rows, k, pos_base, H, own_list, n_own, own_log,
+    launch(k_unpack_changed<false>, grid, kSBlk, 0, s, *sh, d, ids, rows, k, pos_base, H, own_list, n_own, own_log,
                                                    own_slot, o, bm_chg, chg_slot, chg_list, n_chg);
   RTEC_LAUNCH_CHECK("k_unpack_changed");
   return RTEC_OK;
@@ -574,8 +585,8 @@ int rtec_shard_degrees(const rtec_shard_t* sh, const int32_t* src, const int32_t
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   RTEC_PROF("shard_degrees", s);
   if (B > 0) {
-    k_gdeg<<<grid_for(B, kSBlk), kSBlk, 0, s>>>(*sh, src, dst, op, gstatus, B, bm_touch);
-    k_gdeg_dg<<<grid_for(B, kSBlk), kSBlk, 0, s>>>(*sh, src, gstatus, B, dg_bm);
+    launch(k_gdeg, grid_for(B, kSBlk), kSBlk, 0, s, *sh, src, dst, op, gstatus, B, bm_touch);
+    launch(k_gdeg_dg, grid_for(B, kSBlk), kSBlk, 0, s, *sh, src, gstatus, B, dg_bm);
     RTEC_LAUNCH_CHECK("k_gdeg");
   }
   Ws w(ws, ws_bytes);
@@ -589,7 +600,7 @@ int rtec_shard_commit(const rtec_shard_t* sh, const int32_t* src, const int32_t*
                       int64_t B, uint32_t* dg_bm, uint32_t* bm_touch, rtec_stream_t stream) {
   RTEC_TRY(shard_ok(sh));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (B > 0) k_gdeg_commit<<<grid_for(B, kSBlk), kSBlk, 0, s>>>(*sh, src, dst, gstatus, B, dg_bm, bm_touch);
+  if (B > 0) launch(k_gdeg_commit, grid_for(B, kSBlk), kSBlk, 0, s, *sh, src, dst, gstatus, B, dg_bm, bm_touch);
   RTEC_LAUNCH_CHECK("k_gdeg_commit");
   return RTEC_OK;
 }
