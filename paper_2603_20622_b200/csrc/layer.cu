@@ -1428,7 +1428,7 @@ struct GatEdgeState {
 
 // contributions of in-run positions [e0, e1) of v: all edges (recompute) or the
 // ValueChange edges (sources in S(l), edge not inserted) -> acc, cacc
-template <int VEC, int K>
+template <int VEC, int K, int UNR = 1>
 __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState& es, int64_t beg, int32_t e0,
                                           int32_t e1, int64_t p, int64_t q, bool all, RowAcc<VEC, K>& acc,
                                           float (&cacc)[K]) {
@@ -1467,7 +1467,51 @@ __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState
         }
     }
     __syncwarp();
-    {
+    if constexpr (UNR == 2) {
+      // two edges' row pairs in flight per warp, accumulated in edge order (same sums)
+      while (m) {
+        const int s0 = __ffs(m) - 1;
+        m &= m - 1;
+        const int s1 = m ? __ffs(m) - 1 : -1;
+        if (m) m &= m - 1;
+        const int s1c = s1 >= 0 ? s1 : s0;
+        const int32_t u0 = __shfl_sync(0xffffffffu, u, s0), u1 = __shfl_sync(0xffffffffu, u, s1c);
+        const int32_t l0 = __shfl_sync(0xffffffffu, sl, s0), l1 = __shfl_sync(0xffffffffu, sl, s1c);
+        float zn0[K][VEC], zo0[K][VEC], zn1[K][VEC], zo1[K][VEC];
+        R::load(a.st.Z + static_cast<int64_t>(u0) * d, d, zn0);
+        if (!all) R::load(a.st.Z_log + static_cast<int64_t>(l0) * d, d, zo0);
+        if (s1 >= 0) {
+          R::load(a.st.Z + static_cast<int64_t>(u1) * d, d, zn1);
+          if (!all) R::load(a.st.Z_log + static_cast<int64_t>(l1) * d, d, zo1);
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const float wn = an[s0][hk[k]];
+          const float wo = all ? 0.f : ao[s0][hk[k]];
+          cacc[k] += all ? wn : wn - wo;
+#pragma unroll
+          for (int jj = 0; jj < VEC; ++jj) {
+            float x = wn * zn0[k][jj];
+            if (!all) x = fmaf(-wo, zo0[k][jj], x);
+            acc.v[k][jj] += x;
+          }
+        }
+        if (s1 >= 0) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const float wn = an[s1][hk[k]];
+            const float wo = all ? 0.f : ao[s1][hk[k]];
+            cacc[k] += all ? wn : wn - wo;
+#pragma unroll
+            for (int jj = 0; jj < VEC; ++jj) {
+              float x = wn * zn1[k][jj];
+              if (!all) x = fmaf(-wo, zo1[k][jj], x);
+              acc.v[k][jj] += x;
+            }
+          }
+        }
+      }
+    } else {
       while (m) {
         const int src = __ffs(m) - 1;
         m &= m - 1;
@@ -1594,11 +1638,11 @@ __device__ __forceinline__ void gat_finalize(const LayerArgs& a, int64_t i, int3
   if (__any_sync(0xffffffffu, !finite) && lane_id() == 0) report_error(a.err, RTEC_NUMERIC_ERROR, v);
 }
 
-// 6 CTAs / SM (42 registers, spills): the GAT passes are latency-bound on their row
-// gathers and the two streams' passes co-reside, so occupancy wins -- measured c3-gat
-// p50 3 CTAs 16.4 ms, 4 CTAs 14.7, 5 CTAs 14.55, 6 CTAs 14.1
-template <int VEC, int K, bool FULL>
-__global__ void __launch_bounds__(kLBlk, 6) k_gat_light(LayerArgs a, AggRows rows) {
+// Occupancy / rows in flight: template OCC (CTAs / SM) and UNR (edges gathered per warp
+// step); with one row pair in flight 6 CTAs / SM won (c3-gat p50 3 CTAs 16.4 ms, 4 CTAs
+// 14.7, 5 CTAs 14.55, 6 CTAs 14.1), two pairs at 4 CTAs win over that (launch_gat_passes)
+template <int VEC, int K, bool FULL, int UNR = 1, int OCC = 6>
+__global__ void __launch_bounds__(kLBlk, OCC) k_gat_light(LayerArgs a, AggRows rows) {
   RTEC_PDL_ENTRY();
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
@@ -1626,14 +1670,14 @@ __global__ void __launch_bounds__(kLBlk, 6) k_gat_light(LayerArgs a, AggRows row
     float cacc[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) cacc[k] = 0.f;
-    if (scan) gat_edges<VEC, K>(a, es, a.g.in.beg[v], 0, len, p, q, recompute, acc, cacc);
+    if (scan) gat_edges<VEC, K, UNR>(a, es, a.g.in.beg[v], 0, len, p, q, recompute, acc, cacc);
     if (!recompute) gat_struct<VEC, K>(a, es, p, q, acc, cacc);
     gat_finalize<VEC, K, FULL>(a, i, v, len, recompute, acc, cacc);
   }
 }
 
-template <int VEC, int K, bool FULL>
-__global__ void __launch_bounds__(kLBlk, 6) k_gat_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
+template <int VEC, int K, bool FULL, int UNR = 1, int OCC = 6>
+__global__ void __launch_bounds__(kLBlk, OCC) k_gat_heavy(LayerArgs a, AggRows rows, HeavyPlan hp) {
   RTEC_PDL_ENTRY();
   using R = RowAcc<VEC, K>;
   if (!FULL && err_set(a.err)) return;
@@ -1670,7 +1714,7 @@ __global__ void __launch_bounds__(kLBlk, 6) k_gat_heavy(LayerArgs a, AggRows row
 #pragma unroll
     for (int k = 0; k < K; ++k) cacc[k] = 0.f;
     int32_t e0 = c * kChunk, e1 = min(len, e0 + kChunk);
-    gat_edges<VEC, K>(a, es, a.g.in.beg[v], e0, e1, p, q, recompute, acc, cacc);
+    gat_edges<VEC, K, UNR>(a, es, a.g.in.beg[v], e0, e1, p, q, recompute, acc, cacc);
     if (!recompute && c == 0) gat_struct<VEC, K>(a, es, p, q, acc, cacc);
     float* part = hp.part + t * pw;
     acc.store(part, d);
@@ -1702,11 +1746,29 @@ __global__ void __launch_bounds__(kLBlk, 6) k_gat_heavy(LayerArgs a, AggRows row
   }
 }
 
+// Gathers of the VEC = 4 passes: two edges' (Z, Z_log) row pairs in flight per warp at
+// 4 CTAs / SM (64 registers) -- measured c3-gat GAT stage 6.2 -> 5.5 ms against one pair at
+// 6 CTAs / SM; three or four pairs at 2-3 CTAs / SM and two pairs at 5-6 (spills) lose
+// (profiles/r02v_gat_unroll_ab.md).  RTEC_GAT_UNR=1: one pair at 6 CTAs / SM (A/B).
+static bool gat_unr1() {
+  static int u = -1;
+  if (u < 0) {
+    const char* e = getenv("RTEC_GAT_UNR");
+    u = e ? (atoi(e) == 1) : 0;
+  }
+  return u != 0;
+}
+
 template <int VEC, int K, bool FULL>
 static int launch_gat_passes(const LayerArgs& a, AggRows rows, const HeavyPlan& hp, int grid, cudaStream_t s,
                              cudaStream_t hs) {
-  launch(k_gat_heavy<VEC, K, FULL>, grid, kLBlk, 0, hs, a, rows, hp);
-  launch(k_gat_light<VEC, K, FULL>, grid, kLBlk, 0, s, a, rows);
+  if (gat_unr1()) {
+    launch(k_gat_heavy<VEC, K, FULL, 1, 6>, grid, kLBlk, 0, hs, a, rows, hp);
+    launch(k_gat_light<VEC, K, FULL, 1, 6>, grid, kLBlk, 0, s, a, rows);
+  } else {
+    launch(k_gat_heavy<VEC, K, FULL, 2, 4>, grid, kLBlk, 0, hs, a, rows, hp);
+    launch(k_gat_light<VEC, K, FULL, 2, 4>, grid, kLBlk, 0, s, a, rows);
+  }
   return RTEC_OK;
 }
 
