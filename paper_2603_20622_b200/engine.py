@@ -22,6 +22,7 @@ device), so the whole step can be captured in a CUDA graph (`capture()`).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -135,7 +136,10 @@ class RTECEngine:
         self.use_graphs = bool(use_graphs)
         self._graphs: dict = {}
         self._seen: dict = {}
-        self.graph_kernels: dict = {}  # batch size -> kernel nodes of the captured step
+        self.graph_kernels: dict = {}  # batch size -> kernel nodes of the captured step (both parts)
+        self._graph_nodes: dict = {}
+        # RTEC_STEP_OVERLAP=0: read the apply results back after the whole step (A/B)
+        self._overlap_rb = os.environ.get("RTEC_STEP_OVERLAP", "1") != "0"
         self._host = None  # pinned result buffers of step()
         self.lib = graph.lib
         self.dev = graph.dev
@@ -340,32 +344,40 @@ class RTECEngine:
         return (B, id(gr), gr.layout_version, gr.ws.data_ptr())
 
     def enqueue_step(self, B: int) -> None:
-        """Enqueue the whole incremental pipeline for the staged batch (no sync).
+        """Enqueue the whole incremental pipeline for the staged batch (no sync): part 1 the
+        apply chain (statuses, DegreeDelta rows final), part 2 frontiers, layers and commit.
 
-        With `use_graphs`, the pipeline (~100-200 launches) is captured into a CUDA
+        With `use_graphs`, each part (~100-200 launches together) is captured into a CUDA
         graph on the second batch of a given size and replayed afterwards; any
         reallocation (workspace growth, compaction, larger batch buffers) changes
-        the key and triggers a fresh capture."""
+        the key and triggers a fresh capture.  step() reads the apply results back
+        between the two parts, under part 2's compute."""
+        self._enqueue_part(B, 1)
+        self._enqueue_part(B, 2)
+
+    def _enqueue_part(self, B: int, part: int) -> None:
         self._ensure_ws(self.g.batch.cap)
+        run = (lambda: self.g.apply_staged(B)) if part == 1 else (lambda: self._enqueue_layers(B))
         if not self.use_graphs:
-            self._enqueue_eager(B)
+            run()
             return
-        key = self._graph_key(B)
+        key = self._graph_key(B) + (part,)
         cg = self._graphs.get(key)
         if cg is None:
             if self._seen.get(key, 0) < 1:  # first batch of this shape runs eagerly (lazy init, warm-up)
                 self._seen[key] = self._seen.get(key, 0) + 1
-                self._enqueue_eager(B)
+                run()
                 return
             prof = _lib.prof_enabled()
             self.lib.rtec_prof_enable(0)
             cg = torch.cuda.CUDAGraph(keep_graph=True)
             with torch.cuda.graph(cg):
-                self._enqueue_eager(B)
+                run()
             cg.instantiate()
             self.lib.rtec_prof_enable(1 if prof else 0)
-            self.graph_kernels[B] = int(self.lib.rtec_graph_kernel_nodes(cg.raw_cuda_graph()))
-            if len(self._graphs) >= 4:
+            self._graph_nodes[key] = int(self.lib.rtec_graph_kernel_nodes(cg.raw_cuda_graph()))
+            self.graph_kernels[B] = sum(v for k, v in self._graph_nodes.items() if k[0] == B)
+            if len(self._graphs) >= 8:
                 self._graphs.pop(next(iter(self._graphs)))
             self._graphs[key] = cg
         cg.replay()
@@ -373,8 +385,12 @@ class RTECEngine:
     def _enqueue_eager(self, B: int, mode: str = "inc") -> None:
         """mode 'inc': Alg. 1 / Alg. 3 (run_incremental); 'uer': the same affected rows
         recomputed over their full in-neighbourhoods (SPEC.md:455 run_uer)."""
+        self.g.apply_staged(B)
+        self._enqueue_layers(B, mode)
+
+    def _enqueue_layers(self, B: int, mode: str = "inc") -> None:
+        """Frontiers, layers and the batch commit for the applied batch (after apply_staged)."""
         gr = self.g
-        gr.apply_staged(B)
         g, b = gr._gc, gr._bc
         st = _lib.stream_handle()
         ws, wsb = _lib.ptr(gr.ws), gr.ws.numel()
@@ -437,10 +453,8 @@ class RTECEngine:
             self._fws = torch.empty(need, dtype=torch.uint8, device=self.dev)
         return self._fws
 
-    def _readback(self, B: int):
-        """Queue the batch's results into pinned host buffers (one sync for all of them)."""
-        b = self.g.batch
-        cap = b.cap
+    def _host_buffers(self):
+        cap = self.g.batch.cap
         hb = self._host
         if hb is None or hb["cap"] < cap:
             pin = lambda t, k: torch.empty(k, dtype=t, pin_memory=True)  # noqa: E731
@@ -448,17 +462,60 @@ class RTECEngine:
                                "status": pin(torch.uint8, cap),
                                "d": torch.empty((2 * cap, 5), dtype=torch.int32, pin_memory=True),
                                "ctr": pin(torch.int64, 8 * self.L)}
-        hb["err"].copy_(b.err, non_blocking=True)
+        return hb
+
+    def _readback_apply(self, hb, B: int) -> None:
+        """Queue the apply results (DegreeDelta count, statuses, DegreeDelta rows) into the
+        pinned buffers on the current stream."""
+        b = self.g.batch
         hb["nd"].copy_(b.n_delta, non_blocking=True)
         if B:
             hb["status"][:B].copy_(b.status[:B], non_blocking=True)
             # DegreeDelta rows (at most 2B) interleaved into [rows, 5] on the device: one copy,
             # and the host result is a slice instead of a stack of five columns
             hb["d"][: 2 * B].copy_(torch.stack([t[: 2 * B] for t in b.d], dim=1), non_blocking=True)
+
+    def _readback_tail(self, hb) -> None:
+        """Queue the error word and the frontier counters (after the layers)."""
+        hb["err"].copy_(self.g.batch.err, non_blocking=True)
         for l, f in enumerate(self.fr):
             hb["ctr"][8 * l: 8 * l + 8].copy_(f.counters, non_blocking=True)
+
+    def _readback(self, B: int):
+        """Queue the batch's results into pinned host buffers (one sync for all of them)."""
+        hb = self._host_buffers()
+        self._readback_apply(hb, B)
+        self._readback_tail(hb)
         torch.cuda.current_stream().synchronize()
         return hb
+
+    def _step_overlapped(self, B: int):
+        """The incremental step with its apply results read back under the layer compute:
+        part 1 (apply chain), then on a side stream the D2H of statuses and DegreeDelta
+        rows, then part 2 (frontiers, layers, commit) on the main stream; the host turns
+        the apply results into arrays while part 2 runs, and waits for the main stream
+        only for the error word and counters."""
+        hb = self._host_buffers()
+        main = torch.cuda.current_stream()
+        self._enqueue_part(B, 1)
+        if getattr(self, "_rb_stream", None) is None:
+            self._rb_stream = torch.cuda.Stream(device=self.dev)
+            self._rb_events = (torch.cuda.Event(), torch.cuda.Event())
+        side, (e_apply, e_rb) = self._rb_stream, self._rb_events
+        e_apply.record(main)
+        side.wait_event(e_apply)
+        with torch.cuda.stream(side):
+            self._readback_apply(hb, B)
+        e_rb.record(side)
+        self._enqueue_part(B, 2)
+        self._readback_tail(hb)
+        main.wait_event(e_rb)  # the side copies finish before the main stream moves on
+        e_rb.synchronize()
+        status = hb["status"][:B].numpy().copy()
+        k = int(hb["nd"][0])
+        deltas = hb["d"][:k].numpy().copy() if k else np.zeros((0, 5), np.int32)
+        main.synchronize()
+        return hb, status, deltas
 
     def _metrics_from(self, ctr, mode: str = "inc") -> Metrics:
         m = Metrics(mode=mode)
@@ -668,7 +725,10 @@ class RTECEngine:
             raise E.StaleState("deferred (ODEC) rows pending: call odec_flush() before another mode")
         B = self.g.stage(op, src, dst, ts)
         for attempt in range(4):
-            if mode == "inc":
+            early = None
+            if mode == "inc" and self._overlap_rb:
+                hb, *early = self._step_overlapped(B)
+            elif mode == "inc":
                 self.enqueue_step(B)
             else:
                 self._ensure_ws(self.g.batch.cap)
@@ -682,7 +742,8 @@ class RTECEngine:
                     stale = self._odec_state()
                     for l in range(self.L):
                         stale[l] |= self.fr[l].bm_dst
-            hb = self._readback(B)
+            if early is None:
+                hb = self._readback(B)
             word = int(hb["err"][0]) & _lib.ERR_OK
             d = _lib.decode_err(word)
             if d is not None and d[0] == _lib.ARENA_FULL:
@@ -695,10 +756,13 @@ class RTECEngine:
             break
         else:
             raise E.NativeError("run_incremental: arena still full after compaction")
-        status = hb["status"][:B].numpy().copy()
-        k = int(hb["nd"][0])
-        # DegreeDelta rows (vertex, old_in, new_in, old_out, new_out) as int32 [k, 5]
-        deltas = hb["d"][:k].numpy().copy() if k else np.zeros((0, 5), np.int32)
+        if early is not None:
+            status, deltas = early
+        else:
+            status = hb["status"][:B].numpy().copy()
+            k = int(hb["nd"][0])
+            # DegreeDelta rows (vertex, old_in, new_in, old_out, new_out) as int32 [k, 5]
+            deltas = hb["d"][:k].numpy().copy() if k else np.zeros((0, 5), np.int32)
         m = self._metrics_from(hb["ctr"], mode)
         changed = self._changed_final(mode, m)
         if mode in ("inc", "uer") and self.refresh_every:
