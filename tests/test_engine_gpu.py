@@ -244,6 +244,54 @@ def test_cuda_graph_replay_matches_eager(P):
         assert np.array_equal(a, b)
 
 
+def _stream_results(P, overlap: bool, graphs: bool = True, nb: int = 5):
+    from paper_2603_20622_b200.workload import UpdateStream, chung_lu_edges, features
+
+    n = 2500
+    s, d = chung_lu_edges(n, 25000, seed=21)
+    X = features(n, 24, seed=5)
+    stream = UpdateStream(s, d, holdout=0.2, seed=21)
+    bs, bd, bt = stream.base()
+    g = P.DynamicGraph.from_edges(n, (bs, bd, bt), reserve=512)  # small arena: a compaction replay mid-stream
+    eng = P.RTECEngine(P.make_bundle("gcn", [24, 32, 16]), g, X, use_graphs=graphs)
+    eng._overlap_rb = overlap
+    res = []
+    for _ in range(nb):
+        r = eng.step(*stream.next_batch(400))
+        res.append((r.status.copy(), r.deltas.copy(), list(r.metrics.e_curr), list(r.metrics.v_dst)))
+    return res, eng.embeddings(2)
+
+
+def test_overlapped_readback_matches_step_end_readback(P):
+    # step() reads statuses / DegreeDelta rows back on a side stream between the two graph
+    # parts; the results equal the read-back-after-the-step order bit for bit
+    a, ha = _stream_results(P, overlap=True)
+    b, hb = _stream_results(P, overlap=False)
+    for (sa, da, ea, va), (sb, db, eb, vb) in zip(a, b):
+        assert np.array_equal(sa, sb) and np.array_equal(da, db) and ea == eb and va == vb
+    assert np.array_equal(ha, hb)
+    c, hc = _stream_results(P, overlap=True, graphs=False)  # eager parts
+    assert np.array_equal(ha, hc)
+
+
+def test_pdl_off_matches_default(P, tmp_path):
+    # programmatic dependent launch only changes scheduling: a process with RTEC_PDL=0
+    # (plain stream order) produces the same embeddings bit for bit
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "h.npy"
+    code = ("import sys; sys.path.insert(0, %r); sys.path.insert(0, %r); import numpy as np; "
+            "import paper_2603_20622_b200 as P; import test_engine_gpu as T; "
+            "_, h = T._stream_results(P, overlap=True); np.save(%r, h)") % (root, os.path.join(root, "tests"), str(out))
+    env = dict(os.environ, RTEC_PDL="0")
+    subprocess.run([sys.executable, "-c", code], env=env, check=True, timeout=600)
+    _, h = _stream_results(P, overlap=True)
+    assert np.array_equal(np.load(out), h)
+
+
 @pytest.mark.parametrize("model,dims", [("gcn", [24, 32, 16]), ("gat", [24, 32, 32]), ("gin_max", [16, 24, 16])])
 def test_uer_and_full_modes_match_oracle(P, model, dims):
     # SPEC run_uer / run_full on the same stream: both equal the
