@@ -109,12 +109,21 @@ template <int VEC, int K>
 __global__ void __launch_bounds__(kLBlk) k_src_delta(LayerArgs a, float* delta) {
   RTEC_PDL_ENTRY();
   using R = RowAcc<VEC, K>;
-  int64_t ns = *a.f.n_src;
+  // After a fused update (unsharded), S(l) \ V_chg(l-1) = Dg \ V_chg(l-1): walk the batch's
+  // DegreeDelta vertices (<= 2B) instead of all of S(l) (c2-gcn layer 2: 124K vs 2.19M)
+  const bool dg_walk = a.st.delta_ready && a.prev_bm_dst && !a.st.delta_slot && a.b.dg_bm == nullptr;
+  int64_t ns = dg_walk ? *a.b.n_delta : *a.f.n_src;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int d = a.d_agg;
   for (int64_t i = warp; i < ns; i += nw) {
-    int32_t u = a.f.src_list[i];
+    int32_t u;
+    if (dg_walk) {
+      u = a.b.d_vertex[i];
+      if (!bm_test(a.f.bm_src, u)) continue;
+    } else {
+      u = a.f.src_list[i];
+    }
     // rows of V_chg(l-1) were written by the previous layer's update epilogue
     if (a.st.delta_ready && a.prev_bm_dst && bm_test(a.prev_bm_dst, u)) continue;
     int32_t dn = a.g.out_deg[u], dp = a.g.out_deg_prev[u];
