@@ -797,10 +797,11 @@ static int merge_mode() {
 static int merge_exec(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, int64_t n, int64_t work_bound,
                       uint64_t* err, cudaStream_t s) {
   RTEC_PROF("adj_merge", s);
-  // warp-per-chunk merges for long runs (measured on c3-gat's ~490-edge runs), element-parallel
-  // ones for short runs (c2 / c1); the regime from the run slots per vertex (host-known)
+  // warp-per-chunk merges for long runs (measured on c3-gat's ~490-edge runs and the skewed
+  // R-MAT runs of c4, ~60 edges on average but hub-dominated), element-parallel ones for short
+  // runs (c2 / c1, < 50 slots per vertex); the regime from the run slots per vertex (host-known)
   const int mode = merge_mode();
-  const bool warp = mode == 2 || (mode == 1 && a.slots > 96 * (n > 0 ? n : 1));
+  const bool warp = mode == 2 || (mode == 1 && a.slots > 64 * (n > 0 ? n : 1));
   if (warp) {
     launch(k_merge_items_warp, grid_for(work_bound, kWC * (kBlk / 32), kSMs * 8), kBlk, 0, s, in, p, a, err, false);
     launch(k_merge_copyback_warp, grid_for(work_bound, kWC * (kBlk / 32), kSMs * 8), kBlk, 0, s, p, a, err, false);
