@@ -1,3 +1,4 @@
+# Record of a reverted experiment (profiles/r02v_gat_unroll_ab.md): the env knob it sets no longer exists at HEAD.
 # A/B: GAT gathers with two row pairs in flight per warp (RTEC_GAT_UNR 24/25/26) vs one (0)
 mkdir -p gpurun_out; out=gpurun_out/ab_gatunr.txt; rm -f $out
 RTEC_GAT_UNR=42 timeout 600 python -m pytest tests -m gpu -x -q -k "gat" > gpurun_out/ab_gatunr_pytest.txt 2>&1; tail -2 gpurun_out/ab_gatunr_pytest.txt >> $out

@@ -1,3 +1,4 @@
+# Record of a reverted experiment (profiles/r02v_gat_unroll_ab.md): the env knob it sets no longer exists at HEAD.
 # GAT recomputes: four rows in flight (RTEC_GAT_UNR4=1) vs two (0); old one-pair kernel for reference
 mkdir -p gpurun_out; out=gpurun_out/ab_gatunr4.txt; rm -f $out
 RTEC_GAT_UNR4=1 timeout 600 python -m pytest tests -m gpu -x -q -k "gat" > gpurun_out/ab_gatunr4_pytest.txt 2>&1; tail -1 gpurun_out/ab_gatunr4_pytest.txt >> $out

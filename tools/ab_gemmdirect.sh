@@ -1,3 +1,4 @@
+# Record of a reverted experiment (profiles/r02r_gemm_direct_epilogue_ab.md): the env knob it sets no longer exists at HEAD.
 # A/B: staged vs direct (register) GEMM epilogue, and wide-N with direct + SA=3
 mkdir -p gpurun_out
 rm -f gpurun_out/ab_direct.txt

@@ -1,3 +1,4 @@
+# Record of a reverted experiment (profiles/r02w_merge_small_ab.md): the env knob it sets no longer exists at HEAD.
 # A/B: small in-place run merges through shared memory (RTEC_MERGE_SMALL=1, default) vs scratch path
 mkdir -p gpurun_out; out=gpurun_out/ab_msmall.txt; rm -f $out
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/ab_msmall_pytest.txt 2>&1; tail -2 gpurun_out/ab_msmall_pytest.txt >> $out
