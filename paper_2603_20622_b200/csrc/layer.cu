@@ -310,7 +310,7 @@ struct HeavyPlan {
   // nullptr: destination-major.  Execution order only: partials are still reduced
   // in chunk order (results identical).
   const uint32_t* order;
-  uint64_t* okey;   // 16-bit sort keys (c << 16) / nch written by k_chunk_map
+  uint64_t* okey;   // 8-bit sort keys (c << 8) / nch written by k_chunk_map (256 position bands: one radix pass)
   uint32_t* oval;   // chunk ids
 };
 
@@ -650,7 +650,7 @@ __global__ void k_chunk_map(HeavyPlan hp) {
     for (int64_t c = c0 + lane_id(); c < c1; c += 32) {
       hp.cmap[c] = static_cast<int32_t>(j);
       if (hp.okey) {
-        hp.okey[c] = static_cast<uint64_t>(((c - c0) << 16) / (c1 - c0));
+        hp.okey[c] = static_cast<uint64_t>(((c - c0) << 8) / (c1 - c0));
         hp.oval[c] = static_cast<uint32_t>(c);
       }
     }
@@ -743,7 +743,7 @@ static int plan_heavy(const LayerArgs& a, AggRows rows, int64_t max_rows, int64_
     uint64_t* kout = w.alloc<uint64_t>(max_chunks);
     uint32_t* order = w.alloc<uint32_t>(max_chunks);
     RTEC_WS_CHECK(w);
-    RTEC_TRY(sort_pairs(hp.okey, hp.oval, kout, order, Count{hp.n_heavy + 1, max_chunks}, max_chunks, 16, w, s));
+    RTEC_TRY(sort_pairs(hp.okey, hp.oval, kout, order, Count{hp.n_heavy + 1, max_chunks}, max_chunks, 8, w, s));
     hp.order = order;
   }
   return RTEC_OK;
