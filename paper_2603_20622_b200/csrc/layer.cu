@@ -299,7 +299,7 @@ struct AggRows {
 
 struct HeavyPlan {
   int32_t* heavy;   // dst indices i of heavy destinations
-  int64_t* n_heavy; // [1]
+  int64_t* n_heavy; // [0] heavy destinations, [1] chunks, [2] packed scan total (then hoff)
   int64_t* hoff;    // [n_heavy + 1] chunk offsets
   int32_t* cmap;    // chunk -> heavy index j
   int32_t* arrive;  // [n_heavy] arrival counters (zeroed per launch)
@@ -622,12 +622,29 @@ struct HeavyStore {
     if (v) heavy[off] = static_cast<int32_t>(i);
   }
 };
-struct HeavyChunks {
+// one scan for the heavy list and its chunk offsets: (1 << 32 | chunks) per heavy destination
+// (heavy count < 2^31, chunks < 2^32: the packed sums never carry between the halves)
+struct HeavyPackF {
+  HeavyFlagF f;
+  __device__ __forceinline__ int64_t operator()(int64_t i) const {
+    if (f.n_src && *f.n_src == 0) return 0;
+    const int32_t len = f.len[f.rows.at(i)];
+    return len > kChunk ? ((int64_t(1) << 32) | ((len + kChunk - 1) / kChunk)) : 0;
+  }
+};
+struct HeavyPackStore {
   AggRows rows;
-  const int32_t* len;
-  const int32_t* heavy;
-  __device__ __forceinline__ int64_t operator()(int64_t j) const {
-    return (len[rows.at(heavy[j])] + kChunk - 1) / kChunk;
+  int32_t* heavy;
+  int64_t* hoff;
+  __device__ __forceinline__ void operator()(int64_t i, int64_t off, int64_t v) const {
+    if (v) {
+      heavy[off >> 32] = static_cast<int32_t>(i);
+      hoff[off >> 32] = off & 0xffffffffll;
+    }
+    if (i == rows.count() - 1) {  // tail: hoff[n_heavy] = total chunks
+      const int64_t t = off + v;
+      hoff[t >> 32] = t & 0xffffffffll;
+    }
   }
 };
 struct StoreOffTailL {
@@ -641,8 +658,12 @@ struct StoreOffTailL {
 
 __global__ void k_chunk_map(HeavyPlan hp) {
   RTEC_PDL_ENTRY();
-  int64_t nh = *hp.n_heavy;
-  if (blockIdx.x == 0 && threadIdx.x == 0) hp.n_heavy[1] = hp.hoff[nh];  // total chunks (sort count)
+  const int64_t packed = hp.n_heavy[2];  // HeavyPackF total: heavy count << 32 | chunks
+  const int64_t nh = packed >> 32;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    hp.n_heavy[0] = nh;
+    hp.n_heavy[1] = packed & 0xffffffffll;  // total chunks (sort count)
+  }
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t j = warp; j < nh; j += nw) {
@@ -717,21 +738,19 @@ template <bool FULL>
 static int plan_heavy(const LayerArgs& a, AggRows rows, int64_t max_rows, int64_t max_edges, int pw, Ws& w,
                       cudaStream_t s, HeavyPlan& hp, bool every_long_run = false) {
   hp.heavy = w.alloc<int32_t>(max_rows + 1);
-  hp.n_heavy = w.alloc<int64_t>(2);
-  hp.hoff = w.alloc<int64_t>(max_rows + 2);
+  hp.n_heavy = w.alloc<int64_t>(max_rows + 2 + 4);  // [0] heavy count, [1] chunks, [2] packed total
+  hp.hoff = hp.n_heavy + 4;
   int64_t max_chunks = heavy_chunk_bound(max_edges);
   hp.cmap = w.alloc<int32_t>(max_chunks);
   hp.arrive = w.alloc<int32_t>(max_rows + 1);
   hp.part = w.alloc<float>(max_chunks * static_cast<int64_t>(pw));
   RTEC_WS_CHECK(w);
-  RTEC_CUDA(cudaMemsetAsync(hp.n_heavy, 0, sizeof(int64_t) * 2, s));
-  RTEC_CUDA(cudaMemsetAsync(hp.hoff, 0, sizeof(int64_t), s));
+  RTEC_CUDA(cudaMemsetAsync(hp.n_heavy, 0, sizeof(int64_t) * 5, s));  // counts, packed total, hoff[0]
   HeavyFlagF hf{rows, a.g.in.len, (FULL || every_long_run) ? nullptr : a.f.n_src};
   Count cnt{rows.n_dev, max_rows};
   if (!rows.n_dev) cnt = Count{nullptr, rows.n_all};
-  RTEC_TRY(exclusive_scan(hf, cnt, max_rows, HeavyStore{hf, hp.heavy}, hp.n_heavy, w, s));
-  RTEC_TRY(exclusive_scan(HeavyChunks{rows, a.g.in.len, hp.heavy}, Count{hp.n_heavy, max_rows}, max_rows,
-                          StoreOffTailL{hp.hoff, hp.n_heavy}, nullptr, w, s));
+  RTEC_TRY(exclusive_scan(HeavyPackF{hf}, cnt, max_rows, HeavyPackStore{rows, hp.heavy, hp.hoff}, hp.n_heavy + 2, w,
+                          s));
   if (heavy_order()) {
     hp.okey = w.alloc<uint64_t>(max_chunks);
     hp.oval = w.alloc<uint32_t>(max_chunks);
