@@ -330,35 +330,6 @@ struct MergePlan {
   int64_t scr_cap;
 };
 
-struct IsIns {
-  const uint8_t* op;
-  __device__ __forceinline__ int64_t operator()(int64_t i) const { return op[i] == RTEC_OP_INSERT ? 1 : 0; }
-};
-struct StorePrefixTail {
-  int64_t* dst;
-  const int64_t* K;
-  __device__ __forceinline__ void operator()(int64_t i, int64_t off, int64_t v) const {
-    dst[i] = off;
-    if (i == *K - 1) dst[i + 1] = off + v;
-  }
-};
-struct IsHead {
-  const int32_t* own;
-  __device__ __forceinline__ int64_t operator()(int64_t i) const { return (i == 0 || own[i] != own[i - 1]) ? 1 : 0; }
-};
-struct StoreHead {
-  const int32_t* own;
-  int64_t* gstart;
-  int32_t* gv;
-  const int64_t* K;
-  __device__ __forceinline__ void operator()(int64_t i, int64_t off, int64_t v) const {
-    if (v) {
-      gstart[off] = i;
-      gv[off] = own[i];
-    }
-    if (i == *K - 1) gstart[off + v] = *K;
-  }
-};
 
 __global__ void k_group_info(MergeIn in, MergePlan p, rtec_adj_t a, float slack, int32_t min_slack,
                              const uint64_t* err) {
@@ -760,19 +731,47 @@ static int plan_alloc(MergePlan& p, int64_t maxK, int64_t scr_cap, bool with_ts,
 }
 
 // plan: groups, new lengths, offsets, arena reservation; no mutation
+// One scan yields both the insert prefix and the group heads: (is_insert << 32 | is_head)
+// per update (counts < 2^31: the packed sums never carry between the halves)
+struct InsHeadPack {
+  const uint8_t* op;
+  const int32_t* own;
+  __device__ __forceinline__ int64_t operator()(int64_t i) const {
+    return (static_cast<int64_t>(op[i] == RTEC_OP_INSERT ? 1 : 0) << 32) | ((i == 0 || own[i] != own[i - 1]) ? 1 : 0);
+  }
+};
+struct InsHeadStore {
+  int64_t* pre_ins;
+  int64_t* gstart;
+  int32_t* gv;
+  const int32_t* own;
+  const int64_t* K;
+  int64_t* G;
+  __device__ __forceinline__ void operator()(int64_t i, int64_t off, int64_t v) const {
+    pre_ins[i] = off >> 32;
+    if (v & 0xffffffffll) {
+      gstart[off & 0xffffffffll] = i;
+      gv[off & 0xffffffffll] = own[i];
+    }
+    if (i == *K - 1) {  // tails: pre_ins[K], gstart[G] = K, the group count
+      const int64_t t = off + v;
+      pre_ins[i + 1] = t >> 32;
+      gstart[t & 0xffffffffll] = *K;
+      *G = t & 0xffffffffll;
+    }
+  }
+};
+
+// The run arrays below are read only for groups g < G, every one of which the scans write
+// (element 0 and the tail included), so only the group count needs a reset (K = 0).
 static int merge_plan(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, float slack, int32_t min_slack,
                       uint64_t* err, Ws& ws, cudaStream_t s, int64_t* ctr) {
   RTEC_CUDA(cudaMemsetAsync(p.G, 0, sizeof(int64_t), s));
-  RTEC_CUDA(cudaMemsetAsync(p.pre_ins, 0, sizeof(int64_t), s));
-  RTEC_CUDA(cudaMemsetAsync(p.gstart, 0, sizeof(int64_t), s));
   Count K{in.K, in.maxK};
-  RTEC_TRY(exclusive_scan(IsIns{in.op}, K, in.maxK, StorePrefixTail{p.pre_ins, in.K}, nullptr, ws, s));
-  RTEC_TRY(exclusive_scan(IsHead{in.own}, K, in.maxK, StoreHead{in.own, p.gstart, p.gv, in.K}, p.G, ws, s));
+  RTEC_TRY(exclusive_scan(InsHeadPack{in.op, in.own}, K, in.maxK,
+                          InsHeadStore{p.pre_ins, p.gstart, p.gv, in.own, in.K, p.G}, nullptr, ws, s));
   launch(k_group_info, grid_for(in.maxK, kBlk), kBlk, 0, s, in, p, a, slack, min_slack, err);
   Count G{p.G, in.maxK};
-  RTEC_CUDA(cudaMemsetAsync(p.work_off, 0, sizeof(int64_t), s));
-  RTEC_CUDA(cudaMemsetAsync(p.scr_off, 0, sizeof(int64_t), s));
-  RTEC_CUDA(cudaMemsetAsync(p.arena_off, 0, sizeof(int64_t), s));
   RTEC_TRY(exclusive_scan(WorkOf{p, a.len}, G, in.maxK, StoreOffTail{p.work_off, p.G}, nullptr, ws, s));
   RTEC_TRY(exclusive_scan(ScrOf{p}, G, in.maxK, StoreOffTail{p.scr_off, p.G}, nullptr, ws, s));
   RTEC_TRY(exclusive_scan(ArenaOf{p}, G, in.maxK, StoreOffTail{p.arena_off, p.G}, nullptr, ws, s));
