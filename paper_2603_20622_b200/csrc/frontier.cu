@@ -209,17 +209,23 @@ extern "C" int rtec_frontier_layer(const rtec_graph_t* g, const rtec_batch_t* b,
   RTEC_PROF("frontier_layer", s);
   Ws w(ws, ws_bytes);
   int32_t* nlist = w.alloc<int32_t>(n + 1);
-  int64_t* noff = w.alloc<int64_t>(n + 2);
-  int64_t* n_new = w.alloc<int64_t>(4);
+  int64_t* n_new = w.alloc<int64_t>(4 + n + 2);  // n_new[4], then noff[n + 2]
+  int64_t* noff = n_new + 4;
   int64_t* woff = w.alloc<int64_t>(words + 1);
   RTEC_WS_CHECK(w);
-  RTEC_CUDA(cudaMemsetAsync(f->counters, 0, sizeof(int64_t) * 8, s));
-  RTEC_CUDA(cudaMemsetAsync(n_new, 0, sizeof(int64_t) * 4, s));
-  RTEC_CUDA(cudaMemsetAsync(noff, 0, sizeof(int64_t), s));
+  // counters, n_new + noff[0] and (layer 0) both bitmaps cleared by one fill kernel
+  Fill4 clr{};
+  clr.s[0] = FillSpan{f->counters, static_cast<int64_t>(sizeof(int64_t)) * 8, 0u};
+  clr.s[1] = FillSpan{n_new, static_cast<int64_t>(sizeof(int64_t)) * 5, 0u};
+  clr.n = 2;
+  if (l == 0) {
+    clr.s[2] = FillSpan{f->bm_src, static_cast<int64_t>(sizeof(uint32_t)) * words, 0u};
+    clr.s[3] = FillSpan{f->bm_dst, static_cast<int64_t>(sizeof(uint32_t)) * words, 0u};
+    clr.n = 4;
+  }
+  RTEC_TRY(fill_spans(clr, s));
   const uint32_t* prev_src = nullptr;
   if (l == 0) {
-    RTEC_CUDA(cudaMemsetAsync(f->bm_src, 0, sizeof(uint32_t) * words, s));
-    RTEC_CUDA(cudaMemsetAsync(f->bm_dst, 0, sizeof(uint32_t) * words, s));
     // sharded: Dg is the global out-degree change set, not the shard's DegreeDelta
     launch(k_seed_layer0, grid_for(b->cap * 2, kFBlk), kFBlk, 0, s, *b, b->dg_bm ? 0 : src_degree_dependent, f->bm_src,
                                                                  f->bm_dst);

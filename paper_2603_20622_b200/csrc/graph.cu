@@ -235,8 +235,12 @@ __global__ void k_apply_probe(const uint64_t* __restrict__ sk, const uint32_t* _
                               rtec_adj_t out, const uint8_t* __restrict__ op, uint8_t* status, uint8_t* aflag,
                               int32_t part_rank, int32_t part_count, const uint64_t* err) {
   RTEC_PDL_ENTRY();
-  if (err_set(err)) return;
+  const bool bad = err_set(err);  // validation failed: no flags -> nothing applied
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x) {
+    if (bad) {
+      aflag[i] = 0;
+      continue;
+    }
     uint64_t k = sk[i];
     int32_t s = static_cast<int32_t>(k / static_cast<uint64_t>(n));
     int32_t d = static_cast<int32_t>(k - static_cast<uint64_t>(s) * n);
@@ -1056,10 +1060,13 @@ int rtec_batch_apply_phase(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src,
     return RTEC_CONFIG_ERROR;
   }
   const bool plan = phase & 1, exec = phase & 2;
-  if (plan) {
-    RTEC_CUDA(cudaMemsetAsync(b->err, 0xff, sizeof(uint64_t), s));
-    RTEC_CUDA(cudaMemsetAsync(b->n_applied, 0, sizeof(int64_t), s));
-    RTEC_CUDA(cudaMemsetAsync(b->n_delta, 0, sizeof(int64_t), s));
+  if (plan) {  // error word to "none", applied / DegreeDelta counts to 0: one fill kernel
+    Fill4 clr{};
+    clr.s[0] = FillSpan{b->err, static_cast<int64_t>(sizeof(uint64_t)), 0xffffffffu};
+    clr.s[1] = FillSpan{b->n_applied, static_cast<int64_t>(sizeof(int64_t)), 0u};
+    clr.s[2] = FillSpan{b->n_delta, static_cast<int64_t>(sizeof(int64_t)), 0u};
+    clr.n = 3;
+    RTEC_TRY(fill_spans(clr, s));
   }
   if (B <= 0) return RTEC_OK;
   RTEC_PROF("batch_apply", s);
@@ -1092,7 +1099,6 @@ int rtec_batch_apply_phase(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src,
   w.off = mark;
   launch(k_apply_dups, grid, kBlk, 0, s, sk, sv, B, n, b->err);
   // 4. probe against the pre-batch graph (skipped on validation error: no flags -> nothing applied)
-  RTEC_CUDA(cudaMemsetAsync(aflag, 0, B, s));
   launch(k_apply_probe, grid, kBlk, 0, s, sk, sv, B, n, g->out, op, b->status, aflag, g->part_rank, g->part_count,
                                       b->err);
   // 5. applied updates in out-key order

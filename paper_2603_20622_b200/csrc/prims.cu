@@ -249,6 +249,35 @@ __global__ void __launch_bounds__(1024) k_sort_reg(const uint64_t* __restrict__ 
   }
 }
 
+// ---------------------------------------------------------------- fills
+__global__ void k_fill4(Fill4 f) {
+  RTEC_PDL_ENTRY();
+  int64_t w[4], tot = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    w[k] = k < f.n ? f.s[k].bytes / 4 : 0;
+    tot += w[k];
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t j = i;
+    int k = 0;
+    while (j >= w[k]) {
+      j -= w[k];
+      ++k;
+    }
+    static_cast<uint32_t*>(f.s[k].p)[j] = f.s[k].word;
+  }
+}
+
+int fill_spans(const Fill4& f, cudaStream_t s) {
+  int64_t tot = 0;
+  for (int k = 0; k < f.n; ++k) tot += f.s[k].bytes / 4;
+  if (tot <= 0) return RTEC_OK;
+  launch(k_fill4, grid_for(tot, 256, kSMs * 4), 256, 0, s, f);
+  RTEC_LAUNCH_CHECK("k_fill4");
+  return RTEC_OK;
+}
+
 // ---------------------------------------------------------------- radix sort
 constexpr int kRxBlock = 256;
 constexpr int kRxItems = 8;

@@ -208,6 +208,20 @@ struct StorePrefix {
   __device__ __forceinline__ void operator()(int64_t i, int64_t off, int64_t) const { dst[i] = off; }
 };
 
+// ---------------------------------------------------------------- fills
+// Up to four 4-byte-aligned spans (whole 32-bit words) set to a word pattern in ONE kernel
+// launch: one graph node instead of one memset node per span on the per-batch chain.
+struct FillSpan {
+  void* p;
+  int64_t bytes;  // multiple of 4
+  uint32_t word;
+};
+struct Fill4 {
+  FillSpan s[4];
+  int n;
+};
+int fill_spans(const Fill4& f, cudaStream_t s);
+
 // ---------------------------------------------------------------- sort
 // Sorts (key, val) pairs ascending by key (stable w.r.t. input order) over
 // bits [0, bits).  Result lands in keys_out/vals_out.  Needs sort_ws_bytes.
