@@ -381,41 +381,27 @@ struct StoreOffTail {
 };
 
 // reserve arena space for relocated runs (single thread): all-or-nothing
-__global__ void k_reserve(MergePlan p, rtec_adj_t a, uint64_t* err, int64_t* ctr) {
+// arena reservation for relocated runs (thread 0: all-or-nothing) and the groups' destinations
+// (every thread; the arena top only moves at the commit) in one launch
+__global__ void k_reserve_dest(MergePlan p, rtec_adj_t a, uint64_t* err, int64_t* ctr) {
   RTEC_PDL_ENTRY();
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  int64_t G = *p.G;
-  int64_t demand = G > 0 ? p.arena_off[G] : 0;
-  int64_t scr = G > 0 ? p.scr_off[G] : 0;
-  int64_t top = *a.top;
-  p.totals[0] = G > 0 ? p.work_off[G] : 0;
-  p.totals[1] = scr;
-  if (ctr) {  // merge volume (elements) for the bench's algorithmic bytes
-    ctr[0] = p.totals[0];
-    ctr[1] = scr;
+  const int64_t G = *p.G;
+  const int64_t top = *a.top;
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    int64_t demand = G > 0 ? p.arena_off[G] : 0;
+    int64_t scr = G > 0 ? p.scr_off[G] : 0;
+    p.totals[0] = G > 0 ? p.work_off[G] : 0;
+    p.totals[1] = scr;
+    if (ctr) {  // merge volume (elements) for the bench's algorithmic bytes
+      ctr[0] = p.totals[0];
+      ctr[1] = scr;
+    }
+    p.totals[2] = demand;
+    p.totals[3] = top;
+    if (!err_set(err) && (top + demand > a.slots || scr > p.scr_cap)) report_error(err, kCodeArenaFull, kArenaFullPos);
   }
-  p.totals[2] = demand;
-  p.totals[3] = top;
-  if (err_set(err)) return;
-  if (top + demand > a.slots || scr > p.scr_cap) {
-    report_error(err, kCodeArenaFull, kArenaFullPos);
-    return;
-  }
-}
-
-__global__ void k_commit_reserve(MergePlan p, rtec_adj_t a, const uint64_t* err) {
-  RTEC_PDL_ENTRY();
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  if (err_set(err)) return;
-  *a.top = p.totals[3] + p.totals[2];
-}
-
-__global__ void k_set_dest(MergePlan p, const uint64_t* err) {
-  RTEC_PDL_ENTRY();
-  int64_t G = *p.G;
-  int64_t base = p.totals[3];
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x) {
-    p.dest[g] = p.inplace[g] ? -1 : base + p.arena_off[g];
+    p.dest[g] = p.inplace[g] ? -1 : top + p.arena_off[g];
   }
 }
 
@@ -702,6 +688,7 @@ __global__ void __launch_bounds__(kBlk) k_merge_copyback(MergePlan p, rtec_adj_t
 __global__ void k_merge_commit(MergePlan p, rtec_adj_t a, const uint64_t* err) {
   RTEC_PDL_ENTRY();
   if (err_set(err)) return;
+  if (threadIdx.x == 0 && blockIdx.x == 0) *a.top = p.totals[3] + p.totals[2];  // commit the reservation
   int64_t G = *p.G;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x) {
     int32_t v = p.gv[g];
@@ -779,8 +766,7 @@ static int merge_plan(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, floa
   RTEC_TRY(exclusive_scan(WorkOf{p, a.len}, G, in.maxK, StoreOffTail{p.work_off, p.G}, nullptr, ws, s));
   RTEC_TRY(exclusive_scan(ScrOf{p}, G, in.maxK, StoreOffTail{p.scr_off, p.G}, nullptr, ws, s));
   RTEC_TRY(exclusive_scan(ArenaOf{p}, G, in.maxK, StoreOffTail{p.arena_off, p.G}, nullptr, ws, s));
-  launch(k_reserve, 1, 32, 0, s, p, a, err, ctr);
-  launch(k_set_dest, grid_for(in.maxK, kBlk), kBlk, 0, s, p, err);
+  launch(k_reserve_dest, grid_for(in.maxK, kBlk), kBlk, 0, s, p, a, err, ctr);
   RTEC_LAUNCH_CHECK("merge_plan");
   return RTEC_OK;
 }
@@ -813,25 +799,10 @@ static int merge_exec(const MergeIn& in, MergePlan& p, const rtec_adj_t& a, int6
     launch(k_merge_copyback, grid_for(work_bound, kMT, kSMs * 8), kBlk, 0, s, p, a, err, false);
   }
   launch(k_merge_commit, grid_for(in.maxK, kBlk), kBlk, 0, s, p, a, err);
-  launch(k_commit_reserve, 1, 32, 0, s, p, a, err);
   RTEC_LAUNCH_CHECK("merge_exec");
   return RTEC_OK;
 }
 
-// per-destination ranges of the in-key ordered applied list (replaces a binary
-// search per destination in the layer kernels)
-__global__ void k_irange_set(const int32_t* __restrict__ id, const int64_t* cnt, int2* irange, const uint64_t* err) {
-  RTEC_PDL_ENTRY();
-  if (err_set(err)) return;
-  int64_t K = *cnt;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x) {
-    int32_t v = id[i];
-    if (i > 0 && id[i - 1] == v) continue;
-    int64_t j = i + 1;
-    while (j < K && id[j] == v) ++j;
-    irange[v] = make_int2(static_cast<int32_t>(i), static_cast<int32_t>(j - i));
-  }
-}
 
 __global__ void k_irange_reset(const int32_t* __restrict__ id, const int64_t* cnt, int2* irange) {
   RTEC_PDL_ENTRY();
@@ -841,15 +812,24 @@ __global__ void k_irange_reset(const int32_t* __restrict__ id, const int64_t* cn
 }
 
 // ------------------------------------------------------------------ degrees + deltas
-__global__ void k_apply_degrees(const int32_t* __restrict__ as, const int32_t* __restrict__ ad,
-                                const uint8_t* __restrict__ ao, const int64_t* cnt, int32_t* out_deg,
-                                int32_t* in_deg, int64_t* num_edges, const uint64_t* err) {
+
+// over the applied updates in one launch: per-destination ranges of the in-key ordered list
+// (replaces a binary search per destination in the layer kernels) and the degree updates
+__global__ void k_irange_degrees(const int32_t* __restrict__ id, int2* irange, const int32_t* __restrict__ as,
+                                 const int32_t* __restrict__ ad, const uint8_t* __restrict__ ao, const int64_t* cnt,
+                                 int32_t* out_deg, int32_t* in_deg, int64_t* num_edges, const uint64_t* err) {
   RTEC_PDL_ENTRY();
   if (err_set(err)) return;
-  int64_t K = *cnt;
+  const int64_t K = *cnt;
   int64_t local = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x) {
-    int32_t d = ao[i] == RTEC_OP_INSERT ? 1 : -1;
+    const int32_t v = id[i];
+    if (i == 0 || id[i - 1] != v) {
+      int64_t j = i + 1;
+      while (j < K && id[j] == v) ++j;
+      irange[v] = make_int2(static_cast<int32_t>(i), static_cast<int32_t>(j - i));
+    }
+    const int32_t d = ao[i] == RTEC_OP_INSERT ? 1 : -1;
     atomicAdd(out_deg + as[i], d);
     atomicAdd(in_deg + ad[i], d);
     local += d;
@@ -1131,9 +1111,8 @@ int rtec_batch_apply_phase(rtec_graph_t* g, rtec_batch_t* b, const int32_t* src,
   }
   if (!exec) return RTEC_OK;
   // 8. mutate: degrees, runs, per-destination ranges
-  launch(k_irange_set, grid, kBlk, 0, s, b->i_dst, b->n_applied, reinterpret_cast<int2*>(b->irange), b->err);
-  launch(k_apply_degrees, grid, kBlk, 0, s, b->a_src, b->a_dst, b->a_op, b->n_applied, g->out_deg, g->in_deg,
-                                        g->num_edges, b->err);
+  launch(k_irange_degrees, grid, kBlk, 0, s, b->i_dst, reinterpret_cast<int2*>(b->irange), b->a_src, b->a_dst, b->a_op,
+         b->n_applied, g->out_deg, g->in_deg, g->num_edges, b->err);
   int64_t work_bound = g->out.slots + B;  // grid-stride loops read the real totals on device
   // the two directions touch disjoint arrays (own plans and scratch): merge them concurrently
   cudaStream_t ms = g_prof_on ? s : side_stream();
