@@ -1,0 +1,13 @@
+# both frontier lists from one packed scan (new) vs two bitmap-to-list passes (old build)
+mkdir -p gpurun_out; out=gpurun_out/ab_wl.txt; rm -f $out
+L=paper_2603_20622_b200/librtec.so
+cp $L /tmp/librtec_new.so
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/ab_wl_pytest.txt 2>&1; tail -2 gpurun_out/ab_wl_pytest.txt >> $out
+for w in c1-gcn c2-sage c2-gcn c1-gcn c2-sage c2-gcn; do
+for v in new old; do
+  if [ $v = old ]; then cp paper_2603_20622_b200/librtec_old.so.ab $L; else cp /tmp/librtec_new.so $L; fi
+  timeout 600 python bench.py --workload $w --steps 20 --warmup 3 --no-cpu-baseline --no-baselines --no-parity --e2e-steps 5 > gpurun_out/ab_wl_${w}_$v.json 2>gpurun_out/ab_wl_${w}_$v.err
+  python -c "import json;r=json.load(open('gpurun_out/ab_wl_${w}_$v.json'));k=r['kernels'];print('$w $v', r['p50_batch_ms'], 'e2e', r['e2e']['p50_batch_ms'], 'agg', k.get('aggregation',k.get('k_gat_layer',{})).get('ms_per_launch'))" >> $out 2>&1
+done; done
+cp /tmp/librtec_new.so $L
+cat $out
