@@ -1496,46 +1496,78 @@ __device__ __forceinline__ void gat_edges(const LayerArgs& a, const GatEdgeState
     }
     __syncwarp();
     if constexpr (UNR == 2) {
-      // two edges' row pairs in flight per warp, accumulated in edge order (same sums)
+      // two edges' (Z, Z_log) row pairs in flight per warp -- or, for a recompute (no
+      // DeltaLog rows), four edges' Z rows in the same registers; accumulated in edge
+      // order (same sums)
+      const int32_t v2 = all ? u : sl;  // the second pair: log slots or two more sources
+      const float* zb = all ? a.st.Z : a.st.Z_log;
       while (m) {
         const int s0 = __ffs(m) - 1;
         m &= m - 1;
         const int s1 = m ? __ffs(m) - 1 : -1;
         if (m) m &= m - 1;
+        int s2 = -1, s3 = -1;
+        if (all) {
+          s2 = m ? __ffs(m) - 1 : -1;
+          if (m) m &= m - 1;
+          s3 = m ? __ffs(m) - 1 : -1;
+          if (m) m &= m - 1;
+        }
         const int s1c = s1 >= 0 ? s1 : s0;
+        const int t0 = all ? (s2 >= 0 ? s2 : s0) : s0;
+        const int t1 = all ? (s3 >= 0 ? s3 : s0) : s1c;
         const int32_t u0 = __shfl_sync(0xffffffffu, u, s0), u1 = __shfl_sync(0xffffffffu, u, s1c);
-        const int32_t l0 = __shfl_sync(0xffffffffu, sl, s0), l1 = __shfl_sync(0xffffffffu, sl, s1c);
+        const int32_t x0 = __shfl_sync(0xffffffffu, v2, t0), x1 = __shfl_sync(0xffffffffu, v2, t1);
+        const bool b0 = all ? s2 >= 0 : true, b1 = all ? s3 >= 0 : s1 >= 0;
         float zn0[K][VEC], zo0[K][VEC], zn1[K][VEC], zo1[K][VEC];
         R::load(a.st.Z + static_cast<int64_t>(u0) * d, d, zn0);
-        if (!all) R::load(a.st.Z_log + static_cast<int64_t>(l0) * d, d, zo0);
-        if (s1 >= 0) {
-          R::load(a.st.Z + static_cast<int64_t>(u1) * d, d, zn1);
-          if (!all) R::load(a.st.Z_log + static_cast<int64_t>(l1) * d, d, zo1);
+        if (b0) R::load(zb + static_cast<int64_t>(x0) * d, d, zo0);
+        if (s1 >= 0) R::load(a.st.Z + static_cast<int64_t>(u1) * d, d, zn1);
+        if (b1) R::load(zb + static_cast<int64_t>(x1) * d, d, zo1);
+        if (all) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const float w0 = an[s0][hk[k]];
+            cacc[k] += w0;
+#pragma unroll
+            for (int jj = 0; jj < VEC; ++jj) acc.v[k][jj] += w0 * zn0[k][jj];
+            if (s1 >= 0) {
+              const float w1 = an[s1][hk[k]];
+              cacc[k] += w1;
+#pragma unroll
+              for (int jj = 0; jj < VEC; ++jj) acc.v[k][jj] += w1 * zn1[k][jj];
+            }
+            if (b0) {
+              const float w2 = an[t0][hk[k]];
+              cacc[k] += w2;
+#pragma unroll
+              for (int jj = 0; jj < VEC; ++jj) acc.v[k][jj] += w2 * zo0[k][jj];
+            }
+            if (b1) {
+              const float w3 = an[t1][hk[k]];
+              cacc[k] += w3;
+#pragma unroll
+              for (int jj = 0; jj < VEC; ++jj) acc.v[k][jj] += w3 * zo1[k][jj];
+            }
+          }
+          continue;
         }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           const float wn = an[s0][hk[k]];
-          const float wo = all ? 0.f : ao[s0][hk[k]];
-          cacc[k] += all ? wn : wn - wo;
+          const float wo = ao[s0][hk[k]];
+          cacc[k] += wn - wo;
 #pragma unroll
-          for (int jj = 0; jj < VEC; ++jj) {
-            float x = wn * zn0[k][jj];
-            if (!all) x = fmaf(-wo, zo0[k][jj], x);
-            acc.v[k][jj] += x;
-          }
+          for (int jj = 0; jj < VEC; ++jj) acc.v[k][jj] += fmaf(-wo, zo0[k][jj], wn * zn0[k][jj]);
         }
         if (s1 >= 0) {
 #pragma unroll
           for (int k = 0; k < K; ++k) {
             const float wn = an[s1][hk[k]];
-            const float wo = all ? 0.f : ao[s1][hk[k]];
-            cacc[k] += all ? wn : wn - wo;
+            const float wo = ao[s1][hk[k]];
+            cacc[k] += wn - wo;
 #pragma unroll
-            for (int jj = 0; jj < VEC; ++jj) {
-              float x = wn * zn1[k][jj];
-              if (!all) x = fmaf(-wo, zo1[k][jj], x);
-              acc.v[k][jj] += x;
-            }
+            for (int jj = 0; jj < VEC; ++jj) acc.v[k][jj] += fmaf(-wo, zo1[k][jj], wn * zn1[k][jj]);
           }
         }
       }
